@@ -1,0 +1,164 @@
+/*
+ * tc.h — C-ABI of libtc, the B200 execution stage for tensor-network weighted
+ * model counting (arXiv 2006.15512).
+ *
+ * The reference path being replaced is pure Python (tensorcount):
+ *   sliced_execute        pkg/src/tensorcount/slicing.py:112-146  (Algorithm 3)
+ *   _execute_tracked      pkg/src/tensorcount/slicing.py:91-109   (Algorithm 2 + accounting)
+ *   mem_cost              pkg/src/tensorcount/slicing.py:52-67
+ *   choose_slice_index    pkg/src/tensorcount/slicing.py:70-79
+ *   _slice_plan/slice_tensor  slicing.py:30-41, tensor.py:118-125
+ *   execute               pkg/src/tensorcount/network.py:151-163
+ *   contract_pair         pkg/src/tensorcount/tensor.py:96-108
+ *   add (slice sum)       pkg/src/tensorcount/tensor.py:111-115
+ * It is bound from Python with ctypes (paper_2006_15512_b200/_lib.py); see
+ * INTEGRATION.md for the binding a tensorcount maintainer would add.
+ *
+ * Conventions
+ *  - All arrays are caller-owned, read-only for the duration of the call;
+ *    libtc copies what it needs.  No C++ exception crosses this boundary;
+ *    every entry point returns a tc_status.  tc_last_error() gives the message
+ *    of the last failure on the calling thread.
+ *  - Index ids are dense 0..num_indices-1.  sort_rank[i] is the rank of the
+ *    reference's Index.sort_key() (tensor.py:35-37) and is the greedy
+ *    tie-break (slicing.py:73-79).
+ *  - Leaf values are FP64, row-major, first listed index slowest
+ *    (tensor.py:1-5, 55-62).  Operand slots: slot < num_leaves is leaf `slot`
+ *    (network order), slot >= num_leaves is internal node slot-num_leaves,
+ *    internal nodes listed in postorder (network.py:114-124) — the numbering
+ *    of serialize_plan (network.py:235-258).
+ *  - Byte sizes of the memory model are 128-bit (reference uses Python ints;
+ *    sizes reach 2^76 on real plans).
+ */
+#ifndef TC_H_
+#define TC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum tc_status {
+  TC_OK = 0,
+  TC_BAD_ARG = 1,            /* -> ValueError                         */
+  TC_PLAN_MISMATCH = 2,      /* -> PlanMismatch   (network.py:143-148) */
+  TC_BUDGET_INFEASIBLE = 3,  /* -> BudgetInfeasible (slicing.py:124-128) */
+  TC_NO_CANDIDATES = 4,      /* -> NoCandidates   (slicing.py:74-75)  */
+  TC_OOM = 5,                /* -> MemoryError                         */
+  TC_CUDA = 6,               /* -> RuntimeError (DeviceError)          */
+  TC_NCCL = 7,               /* -> RuntimeError (DeviceError)          */
+  TC_OVERFLOW = 8,           /* size does not fit 128 bits -> ValueError */
+  TC_INDEX_OVERUSE = 9,      /* -> IndexOveruse   (network.py:42-43)  */
+  TC_NOT_A_BOND = 10         /* -> NotABondIndex  (slicing.py:24-26)  */
+} tc_status;
+
+typedef struct tc_u128 {
+  uint64_t lo;
+  uint64_t hi;
+} tc_u128;
+
+/* The flattened (TensorNetwork, ContractionTree) pair. */
+typedef struct tc_plan_desc {
+  int32_t num_indices;
+  const int32_t* domain;        /* [num_indices] domain sizes (>= 1)          */
+  const int32_t* sort_rank;     /* [num_indices] rank of Index.sort_key()     */
+  int32_t num_leaves;
+  const int64_t* leaf_idx_off;  /* [num_leaves+1]                              */
+  const int32_t* leaf_idx;      /* index ids of each leaf, row-major order     */
+  const int64_t* leaf_val_off;  /* [num_leaves+1]                              */
+  const double* leaf_val;       /* FP64 values, C-contiguous per leaf          */
+  int32_t num_nodes;            /* internal nodes (= num_leaves-1 for a tree)  */
+  const int32_t* left;          /* [num_nodes] operand slots, postorder        */
+  const int32_t* right;         /* [num_nodes]                                 */
+  int32_t root_slot;
+} tc_plan_desc;
+
+typedef struct tc_plan tc_plan; /* validated symbolic plan (host only)   */
+typedef struct tc_exec tc_exec; /* compiled program resident on a device */
+
+typedef struct tc_plan_info {
+  int32_t num_bonds;
+  int32_t num_free;
+  int32_t max_rank;              /* network.py:178-180                      */
+  int32_t root_rank;
+  tc_u128 contraction_ops;       /* network.py:190-201 (MACs)               */
+  tc_u128 mem_cost;              /* unsliced mem_cost, slicing.py:52-67     */
+} tc_plan_info;
+
+typedef struct tc_stats {
+  tc_u128 mem_estimate;          /* mem_cost(n, t, drop=chosen)             */
+  tc_u128 peak_observed;         /* _execute_tracked accounting, slicing.py:96-108 */
+  int64_t num_slices;
+  int64_t device_peak_bytes;     /* real HBM high-water mark (arena + leaves) */
+  double device_ms;              /* CUDA-event time of the slice loop (max over devices) */
+  double compile_ms;             /* host program compile + graph build       */
+  int64_t gpu_launches;          /* kernels launched by the slice loop       */
+  int32_t n_tiny_nodes, n_stream_nodes, n_gemm_nodes, n_generic_nodes;
+  tc_u128 alg_bytes;             /* per slice: sum over nodes 8(|A|+|B|+|C|) */
+  tc_u128 alg_flops;             /* per slice: sum over nodes 2*prod(union)  */
+} tc_stats;
+
+/* ---- symbolic plan (host) ---------------------------------------------- */
+int tc_plan_create(const tc_plan_desc* desc, tc_plan** out);
+void tc_plan_free(tc_plan* plan);
+int tc_plan_info_get(const tc_plan* plan, tc_plan_info* out);
+
+/* mem_cost(n, t, drop) — slicing.py:52-67, exact (128-bit). */
+int tc_mem_cost(const tc_plan* plan, const int32_t* drop, int32_t n_drop, tc_u128* out);
+
+/* choose_slice_index(n, t, already) — slicing.py:70-79.  Incremental: only
+ * the two leaf->root paths of each candidate are re-evaluated. */
+int tc_choose_slice_index(const tc_plan* plan, const int32_t* already, int32_t n_already,
+                          int32_t* out_index);
+
+/* The greedy loop of sliced_execute, slicing.py:119-128: append picks to
+ * `chosen` until mem_cost <= mem_budget.  TC_BUDGET_INFEASIBLE when the
+ * bonds run out; *needs (may be NULL) = mem_cost with every bond dropped. */
+int tc_choose_slices(const tc_plan* plan, int64_t mem_budget, int32_t* chosen, int32_t cap,
+                     int32_t* n_chosen, tc_u128* needs);
+
+/* Reference-order index list of the result (kept_a ++ kept_b recursively,
+ * tensor.py:108), sliced indices removed.  *rank receives its length. */
+int tc_result_indices(const tc_plan* plan, const int32_t* sliced, int32_t n_sliced,
+                      int32_t* out_idx, int32_t cap, int32_t* rank);
+
+/* ---- device execution --------------------------------------------------- */
+/* Compile the plan with the given slice set for one device: layouts, kernel
+ * selection, arena, leaf upload, CUDA graph.  Everything the per-slice loop
+ * needs becomes resident in HBM. */
+int tc_exec_create(const tc_plan* plan, const int32_t* sliced, int32_t n_sliced, int32_t device,
+                   tc_exec** out);
+void tc_exec_free(tc_exec* ex);
+
+/* Run slices [slice_begin, slice_end) (lexicographic ids, first sliced index
+ * slowest, slicing.py:138-139).  Per-slice results stay on the device until
+ * tc_exec_fetch.  Timed with CUDA events on the exec's stream. */
+int tc_exec_run(tc_exec* ex, int64_t slice_begin, int64_t slice_end, tc_stats* stats);
+
+/* Copy the per-slice results of the last run ([n_slices][result_size]) to
+ * host and/or fold them in lexicographic order on the device
+ * (tensor.py:111-115 left fold).  Either pointer may be NULL. */
+int tc_exec_fetch(tc_exec* ex, double* per_slice, double* folded);
+int64_t tc_exec_result_size(const tc_exec* ex);
+
+/* One-shot Algorithm 3 (slicing.py:112-146) from host buffers: pick slices
+ * (explicit ids when n_slice_ids >= 0, greedy from mem_budget when
+ * n_slice_ids < 0 and mem_budget >= 0, none otherwise), compile, run every
+ * slice on `devices` (block partition of lexicographic ids; multi-device
+ * partial results are combined with one NCCL all-reduce), fold, copy out.
+ * out_val holds the result in reference index order (out_idx, *out_rank). */
+int tc_sliced_execute(const tc_plan* plan, int64_t mem_budget, const int32_t* slice_ids,
+                      int32_t n_slice_ids, const int32_t* devices, int32_t n_devices,
+                      double* out_val, int64_t out_cap, int32_t* out_idx, int32_t idx_cap,
+                      int32_t* out_rank, int32_t* chosen, int32_t chosen_cap,
+                      int32_t* n_chosen, tc_stats* stats);
+
+const char* tc_last_error(void);
+int32_t tc_version(void);
+int32_t tc_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TC_H_ */

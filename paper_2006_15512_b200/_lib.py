@@ -1,0 +1,300 @@
+"""ctypes binding of libtc (``include/tc.h``).
+
+The library is built in-tree (``python -m paper_2006_15512_b200.build``) and
+loaded from ``paper_2006_15512_b200/lib/libtc.so``.  There is no fallback: if
+the library is missing or was built for another architecture, importing the
+execution path raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import errors
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libtc.so")
+
+I32P = C.POINTER(C.c_int32)
+I64P = C.POINTER(C.c_int64)
+F64P = C.POINTER(C.c_double)
+
+INT64_MIN = -(2**63)
+INT64_MAX = 2**63 - 1
+
+
+class U128(C.Structure):
+    _fields_ = [("lo", C.c_uint64), ("hi", C.c_uint64)]
+
+    def value(self) -> int:
+        return int(self.lo) | (int(self.hi) << 64)
+
+
+class PlanDesc(C.Structure):
+    _fields_ = [
+        ("num_indices", C.c_int32),
+        ("domain", I32P),
+        ("sort_rank", I32P),
+        ("num_leaves", C.c_int32),
+        ("leaf_idx_off", I64P),
+        ("leaf_idx", I32P),
+        ("leaf_val_off", I64P),
+        ("leaf_val", F64P),
+        ("num_nodes", C.c_int32),
+        ("left", I32P),
+        ("right", I32P),
+        ("root_slot", C.c_int32),
+    ]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [
+        ("num_bonds", C.c_int32),
+        ("num_free", C.c_int32),
+        ("max_rank", C.c_int32),
+        ("root_rank", C.c_int32),
+        ("contraction_ops", U128),
+        ("mem_cost", U128),
+    ]
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("mem_estimate", U128),
+        ("peak_observed", U128),
+        ("num_slices", C.c_int64),
+        ("device_peak_bytes", C.c_int64),
+        ("device_ms", C.c_double),
+        ("compile_ms", C.c_double),
+        ("gpu_launches", C.c_int64),
+        ("n_tiny_nodes", C.c_int32),
+        ("n_stream_nodes", C.c_int32),
+        ("n_gemm_nodes", C.c_int32),
+        ("n_generic_nodes", C.c_int32),
+        ("alg_bytes", U128),
+        ("alg_flops", U128),
+    ]
+
+    def as_dict(self):
+        return dict(
+            mem_estimate=self.mem_estimate.value(),
+            peak_observed=self.peak_observed.value(),
+            num_slices=int(self.num_slices),
+            device_peak_bytes=int(self.device_peak_bytes),
+            device_ms=float(self.device_ms),
+            compile_ms=float(self.compile_ms),
+            gpu_launches=int(self.gpu_launches),
+            n_tiny_nodes=int(self.n_tiny_nodes),
+            n_stream_nodes=int(self.n_stream_nodes),
+            n_gemm_nodes=int(self.n_gemm_nodes),
+            n_generic_nodes=int(self.n_generic_nodes),
+            alg_bytes=self.alg_bytes.value(),
+            alg_flops=self.alg_flops.value(),
+        )
+
+
+# every symbol include/tc.h declares, with its ctypes signature
+SIGNATURES = {
+    "tc_plan_create": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(C.c_void_p)]),
+    "tc_plan_free": (None, [C.c_void_p]),
+    "tc_plan_info_get": (C.c_int, [C.c_void_p, C.POINTER(PlanInfo)]),
+    "tc_mem_cost": (C.c_int, [C.c_void_p, I32P, C.c_int32, C.POINTER(U128)]),
+    "tc_choose_slice_index": (C.c_int, [C.c_void_p, I32P, C.c_int32, I32P]),
+    "tc_choose_slices": (C.c_int, [C.c_void_p, C.c_int64, I32P, C.c_int32, I32P, C.POINTER(U128)]),
+    "tc_result_indices": (C.c_int, [C.c_void_p, I32P, C.c_int32, I32P, C.c_int32, I32P]),
+    "tc_exec_create": (C.c_int, [C.c_void_p, I32P, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "tc_exec_free": (None, [C.c_void_p]),
+    "tc_exec_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(Stats)]),
+    "tc_exec_fetch": (C.c_int, [C.c_void_p, F64P, F64P]),
+    "tc_exec_result_size": (C.c_int64, [C.c_void_p]),
+    "tc_sliced_execute": (
+        C.c_int,
+        [C.c_void_p, C.c_int64, I32P, C.c_int32, I32P, C.c_int32, F64P, C.c_int64, I32P, C.c_int32,
+         I32P, I32P, C.c_int32, I32P, C.POINTER(Stats)],
+    ),
+    "tc_last_error": (C.c_char_p, []),
+    "tc_version": (C.c_int32, []),
+    "tc_device_count": (C.c_int32, []),
+}
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"libtc.so not found at {LIB_PATH}: build it with "
+                "`python -m paper_2006_15512_b200.build` (there is no CPU fallback)"
+            )
+        h = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(h, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = h
+    return _lib
+
+
+_STATUS = {
+    1: ValueError,
+    2: errors.PlanMismatch,
+    3: errors.BudgetInfeasible,
+    4: errors.NoCandidates,
+    5: MemoryError,
+    6: errors.DeviceError,
+    7: errors.DeviceError,
+    8: OverflowError,
+    9: errors.IndexOveruse,
+    10: errors.NotABondIndex,
+}
+
+
+def check(status: int):
+    if status != 0:
+        msg = lib().tc_last_error().decode(errors="replace")
+        raise _STATUS.get(status, RuntimeError)(msg)
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t)
+
+
+def ids_ptr(ids):
+    a = np.ascontiguousarray(np.asarray(ids, dtype=np.int32))
+    return a, _p(a, I32P), len(a)
+
+
+class PlanHandle:
+    """Owns a ``tc_plan`` built from a ``flatten.FlatPlan``."""
+
+    def __init__(self, flat):
+        self.flat = flat
+        L = lib()
+        arrays = dict(
+            domain=np.ascontiguousarray(flat.domain, dtype=np.int32),
+            sort_rank=np.ascontiguousarray(flat.sort_rank, dtype=np.int32),
+            leaf_idx_off=np.ascontiguousarray(flat.leaf_idx_off, dtype=np.int64),
+            leaf_idx=np.ascontiguousarray(flat.leaf_idx, dtype=np.int32),
+            leaf_val_off=np.ascontiguousarray(flat.leaf_val_off, dtype=np.int64),
+            leaf_val=np.ascontiguousarray(flat.leaf_val, dtype=np.float64),
+            left=np.ascontiguousarray(flat.left, dtype=np.int32),
+            right=np.ascontiguousarray(flat.right, dtype=np.int32),
+        )
+        d = PlanDesc(
+            num_indices=len(arrays["domain"]),
+            domain=_p(arrays["domain"], I32P),
+            sort_rank=_p(arrays["sort_rank"], I32P),
+            num_leaves=len(arrays["leaf_idx_off"]) - 1,
+            leaf_idx_off=_p(arrays["leaf_idx_off"], I64P),
+            leaf_idx=_p(arrays["leaf_idx"], I32P),
+            leaf_val_off=_p(arrays["leaf_val_off"], I64P),
+            leaf_val=_p(arrays["leaf_val"], F64P),
+            num_nodes=len(arrays["left"]),
+            left=_p(arrays["left"], I32P),
+            right=_p(arrays["right"], I32P),
+            root_slot=int(flat.root_slot),
+        )
+        h = C.c_void_p()
+        check(L.tc_plan_create(C.byref(d), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.tc_plan_free(self.h)
+            self.h = None
+
+    def info(self) -> PlanInfo:
+        out = PlanInfo()
+        check(lib().tc_plan_info_get(self.h, C.byref(out)))
+        return out
+
+    def mem_cost(self, drop_ids) -> int:
+        a, p, n = ids_ptr(drop_ids)
+        out = U128()
+        check(lib().tc_mem_cost(self.h, p, n, C.byref(out)))
+        return out.value()
+
+    def choose_slice_index(self, already_ids) -> int:
+        a, p, n = ids_ptr(already_ids)
+        out = C.c_int32()
+        check(lib().tc_choose_slice_index(self.h, p, n, C.byref(out)))
+        return int(out.value)
+
+    def result_indices(self, sliced_ids=()):
+        a, p, n = ids_ptr(sliced_ids)
+        cap = max(1, len(self.flat.domain))
+        out = np.zeros(cap, dtype=np.int32)
+        r = C.c_int32()
+        check(lib().tc_result_indices(self.h, p, n, _p(out, I32P), cap, C.byref(r)))
+        return out[: r.value].tolist()
+
+    def sliced_execute(self, mem_budget, slice_ids, devices):
+        L = lib()
+        root = self.result_indices(())
+        cap = 1
+        for i in root:
+            cap *= int(self.flat.domain[i])
+        out_val = np.zeros(max(1, cap), dtype=np.float64)
+        out_idx = np.zeros(max(1, len(root)), dtype=np.int32)
+        rank = C.c_int32()
+        nb = max(1, len(self.flat.domain))
+        chosen = np.zeros(nb, dtype=np.int32)
+        nch = C.c_int32()
+        st = Stats()
+        if slice_ids is None:
+            sa, sp, sn = ids_ptr([])
+            sn = -1
+        else:
+            sa, sp, sn = ids_ptr(slice_ids)
+        if mem_budget is None:
+            budget = INT64_MIN
+        else:
+            budget = max(INT64_MIN + 1, min(INT64_MAX, int(mem_budget)))
+        da, dp, dn = ids_ptr(devices if devices else [0])
+        check(L.tc_sliced_execute(self.h, budget, sp, sn, dp, dn, _p(out_val, F64P), len(out_val),
+                                  _p(out_idx, I32P), len(out_idx), C.byref(rank), _p(chosen, I32P),
+                                  len(chosen), C.byref(nch), C.byref(st)))
+        r = rank.value
+        idx = out_idx[:r].tolist()
+        size = 1
+        for i in idx:
+            size *= int(self.flat.domain[i])
+        return out_val[:size].copy(), idx, chosen[: nch.value].tolist(), st.as_dict()
+
+
+class Exec:
+    """A compiled, HBM-resident program (``tc_exec``) for repeated runs — the
+    bench's device-timed arm."""
+
+    def __init__(self, plan: PlanHandle, slice_ids=(), device: int = 0):
+        self.plan = plan
+        a, p, n = ids_ptr(slice_ids)
+        h = C.c_void_p()
+        check(lib().tc_exec_create(plan.h, p, n, int(device), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.tc_exec_free(self.h)
+            self.h = None
+
+    def run(self, begin: int, end: int) -> dict:
+        st = Stats()
+        check(lib().tc_exec_run(self.h, int(begin), int(end), C.byref(st)))
+        return st.as_dict()
+
+    def result_size(self) -> int:
+        return int(lib().tc_exec_result_size(self.h))
+
+    def fetch(self, per_slice_n: int | None = None):
+        R = self.result_size()
+        folded = np.zeros(R, dtype=np.float64)
+        per = None
+        if per_slice_n:
+            per = np.zeros(per_slice_n * R, dtype=np.float64)
+        check(lib().tc_exec_fetch(self.h, _p(per, F64P) if per is not None else None, _p(folded, F64P)))
+        return folded, per

@@ -1,0 +1,63 @@
+"""Build libtc.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+    python -m paper_2006_15512_b200.build
+
+The shared library lands in ``paper_2006_15512_b200/lib/libtc.so`` (git-ignored,
+shipped to the GPU box with the working tree).  cudart is linked statically so
+the library does not depend on torch's CUDA runtime version.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "lib", "libtc.so")
+
+SOURCES = ["plan.cpp", "compile.cpp", "runtime.cu"]
+HEADERS = ["plan.hpp", "compile.hpp", "program.h", "kernels.cuh"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nvcc():
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if c and (os.path.isabs(c) and os.path.exists(c) or not os.path.isabs(c)):
+            return c
+    return "nvcc"
+
+
+def _stale(out, deps):
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps.append(os.path.join(ROOT, "include", "tc.h"))
+    deps.append(os.path.abspath(__file__))
+    if not force and not _stale(LIB, deps):
+        return LIB
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
+    cmd = [
+        nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-shared",
+        "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-O3",
+        "--expt-relaxed-constexpr",
+        "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+        *[os.path.join(CSRC, f) for f in SOURCES],
+        "-o", LIB + ".tmp", "-lpthread", "-ldl",
+    ]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

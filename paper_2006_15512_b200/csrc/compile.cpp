@@ -1,0 +1,807 @@
+// Host program compiler (see compile.hpp).
+//
+// What it decides, per internal node of the (sliced) contraction tree:
+//   * kernel class — TINY (whole small subtrees evaluated in one CTA's shared
+//     memory, many subtrees per launch), STREAM (big tensor x <=64-entry
+//     operand, HBM-bound), GEMM (FP64 DMMA), GENERIC (mixed radix fallback);
+//   * the memory layout of every intermediate.  The reference always emits
+//     kept_a ++ kept_b (tensor.py:108) and numpy pays a transpose copy per
+//     tensordot (60-70% of CPU time).  Here layouts are chosen
+//     top-down so that a STREAM node's output is an in-place relabel of its
+//     big input (shared bits of the input and free bits of the small operand
+//     share address bits) and a GEMM's operands are K-lowest matrices; the
+//     permutation is folded into the producing kernel's addressing and no
+//     separate transpose pass exists;
+//   * a static arena: offsets from a first-fit simulation in postorder, with
+//     write-after-read edges added to the launch DAG wherever a buffer reuses
+//     memory, so independent branches may run concurrently in the CUDA graph.
+#include "compile.hpp"
+
+#include <algorithm>
+#include <map>
+#include <set>
+
+namespace tc {
+
+namespace {
+
+constexpr int64_t kTinyMax = 4096;           // entries per tiny tensor
+constexpr int32_t kTinySmemCap = 20 * 1024;  // doubles of smem per tiny CTA (160 KB)
+constexpr int64_t kAlign = 256;
+
+[[noreturn]] void fail(int st, const std::string& m) { throw Error{st, m}; }
+
+struct Alloc {
+  std::map<int64_t, int64_t> free_;                   // off -> size
+  std::map<int64_t, std::pair<int64_t, int>> seg;     // off -> (end, last reader step)
+  int64_t top = 0;
+
+  int64_t alloc(int64_t size, std::vector<int>& hazards) {
+    size = (size + kAlign - 1) / kAlign * kAlign;
+    int64_t off = -1;
+    for (auto it = free_.begin(); it != free_.end(); ++it) {
+      if (it->second >= size) {
+        off = it->first;
+        int64_t rest = it->second - size;
+        free_.erase(it);
+        if (rest > 0) free_[off + size] = rest;
+        break;
+      }
+    }
+    if (off < 0) {
+      // extend: reuse a free block touching the top
+      if (!free_.empty()) {
+        auto last = std::prev(free_.end());
+        if (last->first + last->second == top) {
+          off = last->first;
+          free_.erase(last);
+          top = off + size;
+        }
+      }
+      if (off < 0) {
+        off = top;
+        top += size;
+      }
+    }
+    // hazards: previous readers of any byte we are about to overwrite
+    int64_t end = off + size;
+    auto it = seg.upper_bound(off);
+    if (it != seg.begin()) --it;
+    while (it != seg.end() && it->first < end) {
+      int64_t s0 = it->first, s1 = it->second.first;
+      int rd = it->second.second;
+      if (s1 <= off) {
+        ++it;
+        continue;
+      }
+      hazards.push_back(rd);
+      it = seg.erase(it);
+      if (s0 < off) seg[s0] = {off, rd};
+      if (s1 > end) seg[end] = {s1, rd};
+      it = seg.lower_bound(std::min(s1, end));
+    }
+    return off;
+  }
+
+  void release(int64_t off, int64_t size, int reader) {
+    size = (size + kAlign - 1) / kAlign * kAlign;
+    seg[off] = {off + size, reader};
+    auto nx = free_.lower_bound(off);
+    int64_t o = off, s = size;
+    if (nx != free_.end() && nx->first == off + size) {
+      s += nx->second;
+      nx = free_.erase(nx);
+    }
+    if (nx != free_.begin()) {
+      auto pv = std::prev(nx);
+      if (pv->first + pv->second == o) {
+        o = pv->first;
+        s += pv->second;
+        free_.erase(pv);
+      }
+    }
+    free_[o] = s;
+  }
+};
+
+BitRuns make_runs(const std::vector<std::pair<int, int>>& bits) {  // (src bit, dst bit), src ascending
+  BitRuns r{};
+  r.n = 0;
+  for (size_t j = 0; j < bits.size(); ++j) {
+    int s = bits[j].first, d = bits[j].second;
+    if (r.n > 0) {
+      int k = r.n - 1;
+      if (r.src[k] + r.len[k] == s && r.dst[k] + r.len[k] == d) {
+        r.len[k]++;
+        continue;
+      }
+    }
+    if (r.n >= kMaxRuns) throw Error{-1, "runs"};
+    r.src[r.n] = (uint8_t)s;
+    r.dst[r.n] = (uint8_t)d;
+    r.len[r.n] = 1;
+    r.n++;
+  }
+  return r;
+}
+
+}  // namespace
+
+Program compile_program(const Plan& p, const std::vector<int>& chosen_in) {
+  Program g;
+  const int S = p.nslots();
+  std::vector<char> drop(p.NI, 0);
+  for (int i : chosen_in) {
+    if (i < 0 || i >= p.NI) fail(TC_BAD_ARG, "slice index id out of range");
+    if (!p.is_bond[i]) fail(TC_NOT_A_BOND, "slice index is not a bond index of the network");
+    if (drop[i]) fail(TC_BAD_ARG, "slice index listed twice");
+    drop[i] = 1;
+  }
+  g.chosen = chosen_in;
+  g.num_slices = 1;
+  for (int i : chosen_in) {
+    g.chosen_dim.push_back(p.dom[i]);
+    if (__builtin_mul_overflow(g.num_slices, (int64_t)p.dom[i], &g.num_slices))
+      fail(TC_OVERFLOW, "number of slices exceeds 2^63");
+  }
+  g.mem_estimate = mem_cost(p, drop);
+  g.peak_observed = tracked_peak(p, drop);
+
+  // ---- effective sets / sizes ------------------------------------------------
+  std::vector<std::vector<int>> eff(S);
+  std::vector<int64_t> size(S);
+  for (int s = 0; s < S; ++s) {
+    for (int i : p.sets[s])
+      if (!drop[i]) eff[s].push_back(i);
+    u128 z = set_bytes(p, eff[s], drop) / 8;
+    if (z > ((u128)1 << 50)) fail(TC_OOM, "intermediate tensor larger than 2^50 entries");
+    size[s] = (int64_t)z;
+  }
+  auto natural = [&](int s) {
+    std::vector<int> o;
+    const auto& ro = p.ref_order[s];
+    for (auto it = ro.rbegin(); it != ro.rend(); ++it)
+      if (!drop[*it]) o.push_back(*it);
+    return o;
+  };
+  auto inter = [](const std::vector<int>& a, const std::vector<int>& b) {
+    std::vector<int> o;
+    std::set_intersection(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(o));
+    return o;
+  };
+  auto minus = [](const std::vector<int>& a, const std::vector<int>& b) {
+    std::vector<int> o;
+    std::set_difference(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(o));
+    return o;
+  };
+  auto has = [](const std::vector<int>& s, int i) { return std::binary_search(s.begin(), s.end(), i); };
+
+  // ---- classification --------------------------------------------------------
+  g.cls.assign(S, NC_LEAF);
+  auto all2 = [&](int s) {
+    for (int i : eff[s])
+      if (p.dom[i] != 2) return false;
+    return true;
+  };
+  for (int k = 0; k < p.NN; ++k) {
+    int v = p.NL + k, a = p.left[k], b = p.right[k];
+    auto tok = [&](int x) { return p.is_leaf(x) ? size[x] <= kTinyMax : g.cls[x] == NC_TINY; };
+    int8_t c;
+    if (std::max({size[a], size[b], size[v]}) <= kTinyMax && tok(a) && tok(b)) {
+      c = NC_TINY;
+    } else if (all2(a) && all2(b)) {
+      int ks = (int)inter(eff[a], eff[b]).size();
+      int ra = (int)eff[a].size() - ks, rb = (int)eff[b].size() - ks;
+      int f = (eff[b].size() <= eff[a].size()) ? rb : ra;  // free bits of the smaller operand
+      if (ks <= 4 && f <= 4 && ks + f <= 6)
+        c = NC_STREAM;
+      else if (ra >= 6 && rb >= 6 && ks >= 4)
+        c = NC_GEMM;
+      else
+        c = NC_GENERIC;
+    } else {
+      c = NC_GENERIC;
+    }
+    g.cls[v] = c;
+  }
+
+  // ---- layouts (top-down) ----------------------------------------------------
+  g.layout.assign(S, {});
+  std::vector<char> have(S, 0);
+  for (int l = 0; l < p.NL; ++l) {
+    g.layout[l] = natural(l);
+    have[l] = 1;
+  }
+  std::vector<int> pos(p.NI, -1);
+  auto set_pos = [&](const std::vector<int>& L) {
+    for (size_t q = 0; q < L.size(); ++q) pos[L[q]] = (int)q;
+  };
+  auto clr_pos = [&](const std::vector<int>& L) {
+    for (int i : L) pos[i] = -1;
+  };
+  if (!p.is_leaf(p.root)) {
+    g.layout[p.root] = natural(p.root);
+    have[p.root] = 1;
+  }
+  auto want = [&](int child, std::vector<int> L) {
+    if (p.is_leaf(child)) return;
+    g.layout[child] = std::move(L);
+    have[child] = 1;
+  };
+  for (int k = p.NN - 1; k >= 0; --k) {
+    int v = p.NL + k, a = p.left[k], b = p.right[k];
+    const std::vector<int>& L = g.layout[v];
+    switch (g.cls[v]) {
+      case NC_STREAM: {
+        bool b_small = eff[b].size() <= eff[a].size();
+        int big = b_small ? a : b, sm = b_small ? b : a;
+        std::vector<int> Sh = inter(eff[a], eff[b]);
+        std::vector<int> F = minus(eff[sm], Sh);
+        std::vector<int> Lg;
+        size_t si = 0;
+        for (int i : L) {
+          if (has(F, i)) {
+            if (si < Sh.size()) Lg.push_back(Sh[si++]);
+          } else {
+            Lg.push_back(i);
+          }
+        }
+        while (si < Sh.size()) Lg.push_back(Sh[si++]);
+        want(big, Lg);
+        want(sm, natural(sm));
+        break;
+      }
+      case NC_GEMM: {
+        std::vector<int> K = inter(eff[a], eff[b]);
+        std::vector<int> M = minus(eff[a], K), N = minus(eff[b], K);
+        // K order: follow a fixed-layout (leaf) operand when there is one
+        int ref = p.is_leaf(a) ? a : (p.is_leaf(b) ? b : -1);
+        if (ref >= 0) {
+          set_pos(g.layout[ref]);
+          std::sort(K.begin(), K.end(), [&](int x, int y) { return pos[x] < pos[y]; });
+          clr_pos(g.layout[ref]);
+        }
+        set_pos(L);
+        std::sort(M.begin(), M.end(), [&](int x, int y) { return pos[x] < pos[y]; });
+        std::sort(N.begin(), N.end(), [&](int x, int y) { return pos[x] < pos[y]; });
+        clr_pos(L);
+        std::vector<int> La = K, Lb = K;
+        La.insert(La.end(), M.begin(), M.end());
+        Lb.insert(Lb.end(), N.begin(), N.end());
+        want(a, La);
+        want(b, Lb);
+        break;
+      }
+      default:
+        want(a, natural(a));
+        want(b, natural(b));
+    }
+  }
+
+  // ---- leaves: plain or per-slice selected ----------------------------------
+  g.loc.assign(S, Loc{LOC_LEAF, 0});
+  std::vector<int64_t> pv(g.chosen.size(), 1);
+  for (int j = (int)g.chosen.size() - 2; j >= 0; --j) pv[j] = pv[j + 1] * g.chosen_dim[j + 1];
+  std::vector<int> chosen_slot(p.NI, -1);
+  for (size_t j = 0; j < g.chosen.size(); ++j) chosen_slot[g.chosen[j]] = (int)j;
+  for (int l = 0; l < p.NL; ++l) {
+    const auto& ro = p.ref_order[l];
+    bool sl = false;
+    for (int i : ro) sl |= (bool)drop[i];
+    if (!sl) {
+      g.loc[l] = Loc{LOC_LEAF, p.lval_off[l]};
+      continue;
+    }
+    g.loc[l] = Loc{LOC_SLICED, g.sliced_doubles};
+    std::vector<int64_t> stride(ro.size());
+    int64_t st = 1;
+    for (int q = (int)ro.size() - 1; q >= 0; --q) {
+      stride[q] = st;
+      st *= p.dom[ro[q]];
+    }
+    int32_t t0 = (int32_t)g.sel_terms.size();
+    for (size_t q = 0; q < ro.size(); ++q)
+      if (drop[ro[q]]) {
+        int j = chosen_slot[ro[q]];
+        g.sel_terms.push_back(SelTerm{pv[j], g.chosen_dim[j], stride[q]});
+      }
+    int32_t nt = (int32_t)g.sel_terms.size() - t0;
+    // effective entries in effective layout order (LSB-first = reversed ref order)
+    std::vector<int> kq;  // positions in ro of kept indices, row-major order
+    for (size_t q = 0; q < ro.size(); ++q)
+      if (!drop[ro[q]]) kq.push_back((int)q);
+    for (int64_t e = 0; e < size[l]; ++e) {
+      int64_t rem = e, src = p.lval_off[l];
+      for (int q = (int)kq.size() - 1; q >= 0; --q) {
+        int64_t d = p.dom[ro[kq[q]]];
+        src += (rem % d) * stride[kq[q]];
+        rem /= d;
+      }
+      g.sel_ent.push_back(SelEntry{g.sliced_doubles + e, src, t0, nt});
+    }
+    g.sliced_doubles += size[l];
+  }
+
+  // ---- tiny groups -------------------------------------------------------------
+  std::vector<char> forced(S, 0);
+  std::vector<std::vector<int>> groups;  // internal slots, postorder
+  std::vector<int> group_of(S, -1);
+  std::vector<int32_t> group_smem;
+  auto is_tiny = [&](int s) { return !p.is_leaf(s) && g.cls[s] == NC_TINY; };
+  auto is_troot = [&](int s) {
+    return is_tiny(s) && (forced[s] || p.parent[s] < 0 || !is_tiny(p.parent[s]));
+  };
+  for (int iter = 0;; ++iter) {
+    groups.clear();
+    group_smem.clear();
+    std::fill(group_of.begin(), group_of.end(), -1);
+    bool split = false;
+    for (int k = 0; k < p.NN; ++k) {
+      int r = p.NL + k;
+      if (!is_troot(r)) continue;
+      std::vector<int> nodes, st{r};
+      while (!st.empty()) {
+        int v = st.back();
+        st.pop_back();
+        nodes.push_back(v);
+        for (int c : {p.kid_l(v), p.kid_r(v)})
+          if (is_tiny(c) && !is_troot(c)) st.push_back(c);
+      }
+      std::sort(nodes.begin(), nodes.end());
+      // smem first-fit simulation
+      std::map<int32_t, int32_t> fr;  // off -> size (doubles)
+      int32_t top = 0;
+      std::map<int, int32_t> off;
+      auto salloc = [&](int32_t n) {
+        n = (n + 1) & ~1;  // 16-byte aligned
+        for (auto it = fr.begin(); it != fr.end(); ++it)
+          if (it->second >= n) {
+            int32_t o = it->first, rest = it->second - n;
+            fr.erase(it);
+            if (rest) fr[o + n] = rest;
+            return o;
+          }
+        int32_t o = top;
+        top += n;
+        return o;
+      };
+      auto sfree = [&](int32_t o, int32_t n) {
+        n = (n + 1) & ~1;
+        fr[o] = n;
+        // coalesce
+        auto it = fr.find(o);
+        auto nx = std::next(it);
+        if (nx != fr.end() && nx->first == o + it->second) {
+          it->second += nx->second;
+          fr.erase(nx);
+        }
+        if (it != fr.begin()) {
+          auto pv2 = std::prev(it);
+          if (pv2->first + pv2->second == it->first) {
+            pv2->second += it->second;
+            fr.erase(it);
+          }
+        }
+        if (!fr.empty()) {
+          auto last = std::prev(fr.end());
+          if (last->first + last->second == top) {
+            top = last->first;
+            fr.erase(last);
+          }
+        }
+      };
+      int32_t peak = 0;
+      for (int v : nodes) {
+        if (v != r) {
+          off[v] = salloc((int32_t)size[v]);
+          peak = std::max(peak, top);
+        }
+        for (int c : {p.kid_l(v), p.kid_r(v)})
+          if (off.count(c)) sfree(off[c], (int32_t)size[c]);
+      }
+      if (peak > kTinySmemCap) {
+        split = true;
+        for (int c : {p.kid_l(r), p.kid_r(r)})
+          if (is_tiny(c)) forced[c] = 1;
+        if (!is_tiny(p.kid_l(r)) && !is_tiny(p.kid_r(r))) fail(TC_BAD_ARG, "tiny split failed");
+      }
+      for (int v : nodes) group_of[v] = (int)groups.size();
+      groups.push_back(nodes);
+      group_smem.push_back(peak);
+    }
+    if (!split) break;
+    if (iter > 64) fail(TC_BAD_ARG, "tiny grouping did not converge");
+  }
+  // group levels: a group consuming a forced root of another group runs later
+  std::vector<int> glevel(groups.size(), 0);
+  int nlevels = groups.empty() ? 0 : 1;
+  for (size_t gi = 0; gi < groups.size(); ++gi) {  // groups are in postorder of roots
+    for (int v : groups[gi])
+      for (int c : {p.kid_l(v), p.kid_r(v)})
+        if (is_tiny(c) && group_of[c] != (int)gi)
+          glevel[gi] = std::max(glevel[gi], glevel[group_of[c]] + 1);
+    nlevels = std::max(nlevels, glevel[gi] + 1);
+  }
+
+  // ---- steps + arena --------------------------------------------------------
+  Alloc arena;
+  std::vector<int> producer(S, -1);
+  int sel_step = -1;
+  if (!g.sel_ent.empty()) {
+    Step st;
+    st.kind = ST_SELECT;
+    sel_step = (int)g.steps.size();
+    g.steps.push_back(st);
+    for (int l = 0; l < p.NL; ++l)
+      if (g.loc[l].kind == LOC_SLICED) producer[l] = sel_step;
+  }
+  // tiny roots: arena outputs allocated up front
+  std::vector<int64_t> bytes(S);
+  for (int s = 0; s < S; ++s) bytes[s] = size[s] * 8;
+  std::vector<int> haz;
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    int r = groups[gi].back();
+    haz.clear();
+    g.loc[r] = Loc{LOC_ARENA, arena.alloc(bytes[r], haz)};
+  }
+  std::vector<int> tiny_step(nlevels, -1);
+  for (int lv = 0; lv < nlevels; ++lv) {
+    Step st;
+    st.kind = ST_TINY;
+    if (sel_step >= 0) st.deps.push_back(sel_step);
+    if (lv > 0) st.deps.push_back(tiny_step[lv - 1]);
+    tiny_step[lv] = (int)g.steps.size();
+    g.steps.push_back(st);
+  }
+  // tiny descriptors, ordered by level then group
+  std::vector<int> smem_off(S, -1);
+  std::vector<std::vector<int>> level_groups(nlevels);
+  for (size_t gi = 0; gi < groups.size(); ++gi) level_groups[glevel[gi]].push_back((int)gi);
+  std::vector<std::pair<int32_t, int32_t>> level_range(nlevels);
+  for (int lv = 0; lv < nlevels; ++lv) {
+    level_range[lv].first = (int32_t)g.tiny_groups.size();
+    for (int gi : level_groups[lv]) {
+      const auto& nodes = groups[gi];
+      int r = nodes.back();
+      // smem offsets again (same simulation as above, deterministic)
+      std::map<int32_t, int32_t> fr;
+      int32_t top = 0;
+      auto salloc = [&](int32_t n) {
+        n = (n + 1) & ~1;
+        for (auto it = fr.begin(); it != fr.end(); ++it)
+          if (it->second >= n) {
+            int32_t o = it->first, rest = it->second - n;
+            fr.erase(it);
+            if (rest) fr[o + n] = rest;
+            return o;
+          }
+        int32_t o = top;
+        top += n;
+        return o;
+      };
+      auto sfree = [&](int32_t o, int32_t n) {
+        n = (n + 1) & ~1;
+        fr[o] = n;
+        auto it = fr.find(o);
+        auto nx = std::next(it);
+        if (nx != fr.end() && nx->first == o + it->second) {
+          it->second += nx->second;
+          fr.erase(nx);
+        }
+        if (it != fr.begin()) {
+          auto pv2 = std::prev(it);
+          if (pv2->first + pv2->second == it->first) {
+            pv2->second += it->second;
+            fr.erase(it);
+          }
+        }
+        if (!fr.empty()) {
+          auto last = std::prev(fr.end());
+          if (last->first + last->second == top) {
+            top = last->first;
+            fr.erase(last);
+          }
+        }
+      };
+      TinyGroup tg;
+      tg.beg = (int32_t)g.tiny_nodes.size();
+      for (int v : nodes) {
+        int a = p.kid_l(v), b = p.kid_r(v);
+        TinyNode tn{};
+        Loc la{LOC_SMEM, 0}, lb{LOC_SMEM, 0}, lo{LOC_SMEM, 0};
+        auto opnd = [&](int c, Loc& l, int32_t& so) {
+          if (smem_off[c] >= 0 && group_of[c] == gi) {
+            so = smem_off[c];
+            l = Loc{LOC_SMEM, 0};
+          } else {
+            l = g.loc[c];  // leaf / sliced leaf / forced root in arena
+            so = 0;
+          }
+        };
+        opnd(a, la, tn.sa);
+        opnd(b, lb, tn.sb);
+        if (v == r) {
+          lo = g.loc[r];
+        } else {
+          smem_off[v] = salloc((int32_t)size[v]);
+          tn.sout = smem_off[v];
+        }
+        for (int c : {a, b})
+          if (smem_off[c] >= 0 && group_of[c] == gi) sfree(smem_off[c], (int32_t)size[c]);
+        // digits
+        const auto& La = g.layout[a];
+        const auto& Lb = g.layout[b];
+        const auto& Lc = g.layout[v];
+        std::vector<int64_t> sa(p.NI > 0 ? 0 : 0);
+        auto strides = [&](const std::vector<int>& L, std::map<int, int64_t>& m) {
+          int64_t st2 = 1;
+          for (int i : L) {
+            m[i] = st2;
+            st2 *= p.dom[i];
+          }
+        };
+        std::map<int, int64_t> ma, mb;
+        strides(La, ma);
+        strides(Lb, mb);
+        tn.dig = (int32_t)g.tiny_digits.size();
+        bool p2 = true;
+        for (int i : Lc) {
+          TinyDigit d{p.dom[i], ma.count(i) ? (int32_t)ma[i] : 0, mb.count(i) ? (int32_t)mb[i] : 0, 0};
+          p2 &= (p.dom[i] == 2);
+          g.tiny_digits.push_back(d);
+        }
+        std::vector<int> Sh = inter(eff[a], eff[b]);
+        int64_t ssz = 1;
+        for (int i : Sh) {
+          g.tiny_digits.push_back(TinyDigit{p.dom[i], (int32_t)ma[i], (int32_t)mb[i], 0});
+          p2 &= (p.dom[i] == 2);
+          ssz *= p.dom[i];
+        }
+        tn.nc = (int32_t)Lc.size();
+        tn.ns = (int32_t)Sh.size();
+        tn.c_size = (int32_t)size[v];
+        tn.s_size = (int32_t)ssz;
+        tn.pow2 = p2 ? 1 : 0;
+        g.tiny_nodes.push_back(tn);
+        g.tiny_ga.push_back(la);
+        g.tiny_gb.push_back(lb);
+        g.tiny_gout.push_back(lo);
+        g.n_tiny++;
+      }
+      tg.end = (int32_t)g.tiny_nodes.size();
+      g.tiny_groups.push_back(tg);
+      g.tiny_smem_doubles = std::max(g.tiny_smem_doubles, group_smem[gi]);
+      for (int v : nodes)
+        if (v == r) producer[v] = tiny_step[lv];
+    }
+    level_range[lv].second = (int32_t)g.tiny_groups.size();
+  }
+  // forced roots consumed inside a tiny level: release with that level as reader
+  for (size_t gi = 0; gi < groups.size(); ++gi)
+    for (int v : groups[gi])
+      for (int c : {p.kid_l(v), p.kid_r(v)})
+        if (is_tiny(c) && group_of[c] != (int)gi) arena.release(g.loc[c].off, bytes[c], tiny_step[glevel[gi]]);
+  // store level ranges in the TINY steps (reuse `work` / gdig_off fields)
+  for (int lv = 0; lv < nlevels; ++lv) {
+    g.steps[tiny_step[lv]].gdig_off = level_range[lv].first;
+    g.steps[tiny_step[lv]].work = level_range[lv].second - level_range[lv].first;
+  }
+
+  // big nodes in postorder
+  auto stride_map = [&](const std::vector<int>& L) {
+    std::map<int, int64_t> m;
+    int64_t st2 = 1;
+    for (int i : L) {
+      m[i] = st2;
+      st2 *= p.dom[i];
+    }
+    return m;
+  };
+  for (int k = 0; k < p.NN; ++k) {
+    int v = p.NL + k, a = p.left[k], b = p.right[k];
+    {
+      std::vector<int> uni;
+      std::set_union(eff[a].begin(), eff[a].end(), eff[b].begin(), eff[b].end(), std::back_inserter(uni));
+      g.alg_flops += 2 * (set_bytes(p, uni, drop) / 8);
+      g.alg_bytes += (u128)8 * (u128)(size[a] + size[b] + size[v]);
+    }
+    if (g.cls[v] == NC_TINY) continue;
+    Step st;
+    st.slot = v;
+    st.la = g.loc[a];
+    st.lb = g.loc[b];
+    for (int c : {a, b})
+      if (producer[c] >= 0) st.deps.push_back(producer[c]);
+    haz.clear();
+    g.loc[v] = Loc{LOC_ARENA, arena.alloc(bytes[v], haz)};
+    for (int h : haz) st.deps.push_back(h);
+    st.lc = g.loc[v];
+    const auto& La = g.layout[a];
+    const auto& Lb = g.layout[b];
+    const auto& Lc = g.layout[v];
+    bool done = false;
+    if (g.cls[v] == NC_STREAM) {
+      try {
+        bool b_small = eff[b].size() <= eff[a].size();
+        int big = b_small ? a : b, sm = b_small ? b : a;
+        const auto& Lg = g.layout[big];
+        const auto& Lq = g.layout[sm];
+        std::vector<int> Sh = inter(eff[a], eff[b]);
+        std::vector<int> F = minus(eff[sm], Sh);
+        std::map<int, int> pg, pc, pq;
+        for (size_t q = 0; q < Lg.size(); ++q) pg[Lg[q]] = (int)q;
+        for (size_t q = 0; q < Lc.size(); ++q) pc[Lc[q]] = (int)q;
+        for (size_t q = 0; q < Lq.size(); ++q) pq[Lq[q]] = (int)q;
+        // x bits: kept indices of big, in C address order
+        std::vector<std::pair<int, int>> xa, xc;
+        int j = 0;
+        for (size_t q = 0; q < Lc.size(); ++q) {
+          int i = Lc[q];
+          if (has(F, i)) continue;
+          xc.push_back({j, (int)q});
+          j++;
+        }
+        // xa needs src ascending: same j order, dst = position in big
+        j = 0;
+        for (size_t q = 0; q < Lc.size(); ++q) {
+          int i = Lc[q];
+          if (has(F, i)) continue;
+          xa.push_back({j, pg[i]});
+          j++;
+        }
+        StreamParams sp{};
+        sp.xa = make_runs(xa);
+        sp.xc = make_runs(xc);
+        sp.nx = (int64_t)1 << j;
+        int ns = (int)Sh.size(), nf = (int)F.size();
+        // order F by C position, S by big-operand position
+        std::sort(F.begin(), F.end(), [&](int x, int y) { return pc[x] < pc[y]; });
+        std::sort(Sh.begin(), Sh.end(), [&](int x, int y) { return pg[x] < pg[y]; });
+        for (int s = 0; s < (1 << ns); ++s) {
+          int64_t o = 0, oq = 0;
+          for (int t = 0; t < ns; ++t)
+            if (s >> t & 1) {
+              o += (int64_t)1 << pg[Sh[t]];
+              oq += (int64_t)1 << pq[Sh[t]];
+            }
+          sp.offA[s] = o;
+          for (int f = 0; f < (1 << nf); ++f) {
+            int64_t of = 0;
+            for (int t = 0; t < nf; ++t)
+              if (f >> t & 1) of += (int64_t)1 << pq[F[t]];
+            sp.offP[s * (1 << nf) + f] = (int32_t)(oq + of);
+          }
+        }
+        for (int f = 0; f < (1 << nf); ++f) {
+          int64_t o = 0;
+          for (int t = 0; t < nf; ++t)
+            if (f >> t & 1) o += (int64_t)1 << pc[F[t]];
+          sp.offC[f] = o;
+        }
+        st.kind = ST_STREAM;
+        st.sp = sp;
+        st.ns = ns;
+        st.nf = nf;
+        st.la = g.loc[big];
+        st.lb = g.loc[sm];
+        st.work = sp.nx;
+        g.n_stream++;
+        done = true;
+      } catch (const Error& e) {
+        if (e.status != -1) throw;
+      }
+    } else if (g.cls[v] == NC_GEMM) {
+      try {
+        std::vector<int> K = inter(eff[a], eff[b]);
+        std::vector<int> M = minus(eff[a], K), N = minus(eff[b], K);
+        std::map<int, int> pa, pb, pc;
+        for (size_t q = 0; q < La.size(); ++q) pa[La[q]] = (int)q;
+        for (size_t q = 0; q < Lb.size(); ++q) pb[Lb[q]] = (int)q;
+        for (size_t q = 0; q < Lc.size(); ++q) pc[Lc[q]] = (int)q;
+        std::sort(M.begin(), M.end(), [&](int x, int y) { return pc[x] < pc[y]; });
+        std::sort(N.begin(), N.end(), [&](int x, int y) { return pc[x] < pc[y]; });
+        std::sort(K.begin(), K.end(), [&](int x, int y) { return pa[x] < pa[y]; });
+        const int MT = 6, NT = 6, KT = 4;
+        GemmParams gp{};
+        gp.m_hi = (int)M.size() - MT;
+        gp.n_hi = (int)N.size() - NT;
+        gp.k_tiles = (int64_t)1 << ((int)K.size() - KT);
+        std::vector<std::pair<int, int>> r;
+        r.clear();
+        for (int t = MT; t < (int)M.size(); ++t) r.push_back({t - MT, pa[M[t]]});
+        gp.a_m = make_runs(r);
+        r.clear();
+        for (int t = KT; t < (int)K.size(); ++t) r.push_back({t - KT, pa[K[t]]});
+        gp.a_k = make_runs(r);
+        r.clear();
+        for (int t = NT; t < (int)N.size(); ++t) r.push_back({t - NT, pb[N[t]]});
+        gp.b_n = make_runs(r);
+        r.clear();
+        for (int t = KT; t < (int)K.size(); ++t) r.push_back({t - KT, pb[K[t]]});
+        gp.b_k = make_runs(r);
+        r.clear();
+        for (int t = MT; t < (int)M.size(); ++t) r.push_back({t - MT, pc[M[t]]});
+        gp.c_m = make_runs(r);
+        r.clear();
+        for (int t = NT; t < (int)N.size(); ++t) r.push_back({t - NT, pc[N[t]]});
+        gp.c_n = make_runs(r);
+        auto tmap = [&](std::map<int, int>& P, const std::vector<int>& R1, int n1,
+                        const std::vector<int>& R2, int n2) {
+          // R1 tile bits -> kind 0, R2 tile bits -> kind 1
+          std::vector<std::tuple<int, int, int>> bits;  // pos, kind, sub
+          for (int t = 0; t < n1; ++t) bits.emplace_back(P[R1[t]], 0, t);
+          for (int t = 0; t < n2; ++t) bits.emplace_back(P[R2[t]], 1, t);
+          std::sort(bits.begin(), bits.end());
+          TileMap tm{};
+          tm.nbits = (int)bits.size();
+          for (size_t q = 0; q < bits.size(); ++q) {
+            tm.pos[q] = (int8_t)std::get<0>(bits[q]);
+            tm.kind[q] = (int8_t)std::get<1>(bits[q]);
+            tm.sub[q] = (int8_t)std::get<2>(bits[q]);
+          }
+          return tm;
+        };
+        gp.ta = tmap(pa, M, MT, K, KT);
+        gp.tb = tmap(pb, N, NT, K, KT);
+        gp.tc = tmap(pc, M, MT, N, NT);
+        gp.grid_swizzle_log = std::min(gp.m_hi, 3);
+        st.kind = ST_GEMM;
+        st.gp = gp;
+        st.work = (int64_t)1 << (gp.m_hi + gp.n_hi);
+        g.n_gemm++;
+        done = true;
+      } catch (const Error& e) {
+        if (e.status != -1) throw;
+      }
+    }
+    if (!done) {
+      auto ma = stride_map(La), mb = stride_map(Lb);
+      GenericParams np{};
+      st.gdig_off = (int64_t)g.gdigits.size();
+      for (int i : Lc) g.gdigits.push_back(GDigit{p.dom[i], ma.count(i) ? ma[i] : 0, mb.count(i) ? mb[i] : 0});
+      std::vector<int> Sh = inter(eff[a], eff[b]);
+      int64_t ssz = 1;
+      for (int i : Sh) {
+        g.gdigits.push_back(GDigit{p.dom[i], ma[i], mb[i]});
+        ssz *= p.dom[i];
+      }
+      np.c_size = size[v];
+      np.s_size = ssz;
+      np.nc = (int32_t)Lc.size();
+      np.ns = (int32_t)Sh.size();
+      st.kind = ST_GENERIC;
+      st.np = np;
+      st.work = size[v];
+      g.cls[v] = NC_GENERIC;
+      g.n_generic++;
+    }
+    int me = (int)g.steps.size();
+    producer[v] = me;
+    g.steps.push_back(st);
+    for (int c : {a, b})
+      if (g.loc[c].kind == LOC_ARENA) arena.release(g.loc[c].off, bytes[c], me);
+  }
+
+  // root copy into the per-slice result slot, then advance the slice counter
+  g.R = size[p.root];
+  g.root_loc = g.loc[p.root];
+  Step rc;
+  rc.kind = ST_ROOTCOPY;
+  if (producer[p.root] >= 0) rc.deps.push_back(producer[p.root]);
+  rc.work = g.R;
+  int rcs = (int)g.steps.size();
+  g.steps.push_back(rc);
+  Step et;
+  et.kind = ST_ETA;
+  et.deps.push_back(rcs);
+  if (sel_step >= 0) et.deps.push_back(sel_step);
+  g.steps.push_back(et);
+  g.arena_bytes = std::max<int64_t>(arena.top, kAlign);
+  for (auto& s : g.steps) {
+    std::sort(s.deps.begin(), s.deps.end());
+    s.deps.erase(std::unique(s.deps.begin(), s.deps.end()), s.deps.end());
+  }
+  return g;
+}
+
+}  // namespace tc

@@ -1,0 +1,70 @@
+// Host program compiler: turns a symbolic Plan + slice set into a DAG of
+// kernel launches with a static HBM arena (offsets only; pointers are bound
+// per device by the runtime).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "plan.hpp"
+#include "program.h"
+
+namespace tc {
+
+enum NodeClass : int8_t { NC_LEAF = 0, NC_TINY = 1, NC_STREAM = 2, NC_GEMM = 3, NC_GENERIC = 4 };
+
+// Where an operand lives at run time.
+enum LocKind : int8_t { LOC_LEAF = 0, LOC_SLICED = 1, LOC_ARENA = 2, LOC_SMEM = 3 };
+struct Loc {
+  LocKind kind;
+  int64_t off;  // doubles (LEAF: into leaf values, SLICED: into sliced buffer) or bytes (ARENA)
+};
+
+enum StepKind : int8_t { ST_SELECT, ST_TINY, ST_STREAM, ST_GEMM, ST_GENERIC, ST_ROOTCOPY, ST_ETA };
+
+struct Step {
+  StepKind kind;
+  int slot = -1;  // node for STREAM/GEMM/GENERIC
+  std::vector<int> deps;
+  // kernel parameters with pointer fields holding Loc-encoded placeholders
+  StreamParams sp{};
+  GemmParams gp{};
+  GenericParams np{};
+  int32_t ns = 0, nf = 0;          // stream template selector
+  Loc la{}, lb{}, lc{};            // operand/output locations
+  int64_t gdig_off = 0;            // generic digits offset (in GDigit units)
+  int64_t work = 0;                // elements (for launch sizing)
+};
+
+struct Program {
+  int64_t R = 1;                 // result entries
+  int64_t num_slices = 1;
+  std::vector<int> chosen;       // sliced index ids, pick order
+  std::vector<int64_t> chosen_dim;
+  std::vector<int8_t> cls;       // per slot
+  std::vector<std::vector<int>> layout;  // per slot, LSB-first index ids (effective)
+  std::vector<Loc> loc;          // per slot
+  // sliced leaves
+  int64_t sliced_doubles = 0;
+  std::vector<SelEntry> sel_ent;
+  std::vector<SelTerm> sel_terms;
+  // tiny forest
+  std::vector<TinyNode> tiny_nodes;  // ga/gb/gout hold Loc-encoded placeholders
+  std::vector<Loc> tiny_ga, tiny_gb, tiny_gout;
+  std::vector<TinyDigit> tiny_digits;
+  std::vector<TinyGroup> tiny_groups;
+  int32_t tiny_smem_doubles = 0;
+  // generic digits
+  std::vector<GDigit> gdigits;
+  // arena
+  int64_t arena_bytes = 0;
+  Loc root_loc{};
+  std::vector<Step> steps;
+  // stats
+  int n_tiny = 0, n_stream = 0, n_gemm = 0, n_generic = 0;
+  u128 alg_bytes = 0, alg_flops = 0;
+  u128 mem_estimate = 0, peak_observed = 0;
+};
+
+Program compile_program(const Plan& p, const std::vector<int>& chosen);
+
+}  // namespace tc

@@ -1,0 +1,362 @@
+// sm_100a kernels of the execution stage.  Included once, by runtime.cu.
+//
+//   k_select   K5  per-slice leaf selection            (slicing.py:30-41, tensor.py:118-125)
+//   k_tiny     K4  tiny-subtree forest, one CTA per subtree, smem-resident
+//   k_stream   K2  big x <=64-entry operand, HBM streaming, permutation folded in
+//   k_gemm     K3  FP64 DMMA (mma.sync m8n8k4 f64) GEMM, bit-permuted operands
+//   k_generic      mixed-radix pairwise contraction (domains != 2, odd shapes)
+//   k_rootcopy / k_eta / k_fold   per-slice result slot, slice counter, and the
+//                  lexicographic left fold of the slice sum (slicing.py:139-145)
+//
+// Every kernel is deterministic: each output entry is produced by exactly one
+// thread with a fixed summation order (no floating-point atomics), so reruns
+// and different device counts give bitwise-identical results.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "program.h"
+
+namespace tc {
+
+// ---------------------------------------------------------------------------
+__global__ void k_select(const SelectParams p) {
+  const int64_t eta = p.eta[0];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p.n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    SelEntry en = p.ent[e];
+    int64_t src = en.src;
+    for (int t = 0; t < en.nt; ++t) {
+      SelTerm tm = p.terms[en.t0 + t];
+      src += ((eta / tm.pv) % tm.dim) * tm.stride;
+    }
+    p.out[en.dst] = p.lval[src];
+  }
+}
+
+__global__ void k_rootcopy(const RootCopyParams p) {
+  const int64_t slot = p.eta[0] - p.eta[1];
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p.R;
+       r += (int64_t)gridDim.x * blockDim.x)
+    p.results[slot * p.R + r] = p.src[r];
+}
+
+__global__ void k_eta(int64_t* eta) { eta[0] += 1; }
+
+// left fold in lexicographic slice order: ((p0 + p1) + p2) + ...  (tensor.py:111-115)
+__global__ void k_fold(const double* results, int64_t R, int64_t n, double* out) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double acc = results[r];
+    for (int64_t s = 1; s < n; ++s) acc = acc + results[s * R + r];
+    out[r] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: one CTA walks one tiny subtree in postorder; intermediates live in smem.
+constexpr int kTinyThreads = 256;
+constexpr int kTinyMaxDigits = 64;
+
+__global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restrict__ nodes,
+                                                       const TinyDigit* __restrict__ digs,
+                                                       const TinyGroup* __restrict__ groups,
+                                                       int32_t smem_doubles) {
+  extern __shared__ double sm[];
+  double* red = sm + smem_doubles;  // kTinyThreads scratch for cooperative sums
+  __shared__ TinyDigit sd[kTinyMaxDigits];
+  __shared__ TinyNode tn;
+  const TinyGroup G = groups[blockIdx.x];
+  const int tid = threadIdx.x;
+  for (int n = G.beg; n < G.end; ++n) {
+    if (tid == 0) tn = nodes[n];
+    __syncthreads();
+    const int nd = tn.nc + tn.ns;
+    for (int j = tid; j < nd; j += blockDim.x) sd[j] = digs[tn.dig + j];
+    __syncthreads();
+    const double* A = tn.ga ? tn.ga : sm + tn.sa;
+    const double* B = tn.gb ? tn.gb : sm + tn.sb;
+    double* C = tn.gout ? tn.gout : sm + tn.sout;
+    const int nc = tn.nc, ns = tn.ns;
+    const TinyDigit* sdS = sd + nc;
+    if (tn.c_size * 4 >= (int)blockDim.x || tn.s_size < 64) {
+      for (int c = tid; c < tn.c_size; c += blockDim.x) {
+        int oa = 0, ob = 0;
+        if (tn.pow2) {
+          for (int j = 0; j < nc; ++j) {
+            int bit = (c >> j) & 1;
+            oa += bit * sd[j].sa;
+            ob += bit * sd[j].sb;
+          }
+        } else {
+          int r = c;
+          for (int j = 0; j < nc; ++j) {
+            int q = r % sd[j].dim;
+            r /= sd[j].dim;
+            oa += q * sd[j].sa;
+            ob += q * sd[j].sb;
+          }
+        }
+        double acc = 0.0;
+        for (int s = 0; s < tn.s_size; ++s) {
+          int xa = oa, xb = ob;
+          if (tn.pow2) {
+            for (int j = 0; j < ns; ++j) {
+              int bit = (s >> j) & 1;
+              xa += bit * sdS[j].sa;
+              xb += bit * sdS[j].sb;
+            }
+          } else {
+            int r = s;
+            for (int j = 0; j < ns; ++j) {
+              int q = r % sdS[j].dim;
+              r /= sdS[j].dim;
+              xa += q * sdS[j].sa;
+              xb += q * sdS[j].sb;
+            }
+          }
+          acc = fma(A[xa], B[xb], acc);
+        }
+        C[c] = acc;
+      }
+    } else {
+      // few outputs, long sums: the CTA splits each sum, fixed-shape tree reduce
+      for (int c = 0; c < tn.c_size; ++c) {
+        int oa = 0, ob = 0, r = c;
+        for (int j = 0; j < nc; ++j) {
+          int q = r % sd[j].dim;
+          r /= sd[j].dim;
+          oa += q * sd[j].sa;
+          ob += q * sd[j].sb;
+        }
+        double acc = 0.0;
+        for (int s = tid; s < tn.s_size; s += blockDim.x) {
+          int xa = oa, xb = ob, r2 = s;
+          for (int j = 0; j < ns; ++j) {
+            int q = r2 % sdS[j].dim;
+            r2 /= sdS[j].dim;
+            xa += q * sdS[j].sa;
+            xb += q * sdS[j].sb;
+          }
+          acc = fma(A[xa], B[xb], acc);
+        }
+        red[tid] = acc;
+        __syncthreads();
+        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+          if (tid < w) red[tid] = red[tid] + red[tid + w];
+          __syncthreads();
+        }
+        if (tid == 0) C[c] = red[0];
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: streaming contraction with a <=64-entry operand held in smem.
+constexpr int kStreamThreads = 256;
+constexpr int kStreamUnroll = 4;
+
+template <int NS, int NF>
+__global__ void __launch_bounds__(kStreamThreads) k_stream(const StreamParams p) {
+  constexpr int SV = 1 << NS, FV = 1 << NF;
+  __shared__ double P[SV * FV];
+  if (threadIdx.x < SV * FV) P[threadIdx.x] = p.P[p.offP[threadIdx.x]];
+  __syncthreads();
+  const int64_t chunk = (int64_t)kStreamThreads * kStreamUnroll;
+  for (int64_t base = blockIdx.x * chunk; base < p.nx; base += (int64_t)gridDim.x * chunk) {
+    double a[kStreamUnroll][SV];
+    int64_t bc[kStreamUnroll];
+    bool ok[kStreamUnroll];
+#pragma unroll
+    for (int u = 0; u < kStreamUnroll; ++u) {
+      const int64_t x = base + u * kStreamThreads + threadIdx.x;
+      ok[u] = x < p.nx;
+      const int64_t ba = ok[u] ? deposit(x, p.xa) : 0;
+      bc[u] = ok[u] ? deposit(x, p.xc) : 0;
+#pragma unroll
+      for (int s = 0; s < SV; ++s) a[u][s] = ok[u] ? __ldcs(p.A + ba + p.offA[s]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kStreamUnroll; ++u) {
+      if (!ok[u]) continue;
+#pragma unroll
+      for (int f = 0; f < FV; ++f) {
+        double acc = 0.0;
+#pragma unroll
+        for (int s = 0; s < SV; ++s) acc = fma(a[u][s], P[s * FV + f], acc);
+        p.C[bc[u] + p.offC[f]] = acc;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: FP64 tensor-core GEMM.  CTA tile 64x64x16, 4 warps (2x2), warp tile
+// 32x32 = 4x4 DMMA m8n8k4 fragments; 4-stage cp.async pipeline; operands are
+// gathered with per-thread precomputed tile offsets (any bit layout), stored
+// k-major in smem with +4 padding (conflict-free fragment loads); the C tile
+// is staged through smem and written in C's own address order.
+constexpr int GBM = 64, GBN = 64, GBK = 16, GTHREADS = 128, GSTAGES = 4;
+constexpr int GLDA = GBM + 4, GLDB = GBN + 4, GLDC = GBN + 4;
+constexpr int kGemmSmemBytes = GSTAGES * GBK * (GLDA + GLDB) * 8;
+static_assert(GBM * GLDC * 8 <= kGemmSmemBytes, "epilogue tile must fit");
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void tile_elem(const TileMap& t, int e, int64_t& off, int& r, int& k) {
+  off = 0;
+  r = 0;
+  k = 0;
+  for (int j = 0; j < t.nbits; ++j)
+    if ((e >> j) & 1) {
+      off += (int64_t)1 << t.pos[j];
+      if (t.kind[j]) k |= 1 << t.sub[j];
+      else r |= 1 << t.sub[j];
+    }
+}
+
+__global__ void __launch_bounds__(GTHREADS) k_gemm(const GemmParams p) {
+  extern __shared__ __align__(16) double gsm[];
+  double* As = gsm;
+  double* Bs = gsm + GSTAGES * GBK * GLDA;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+
+  // tile coordinates with a grouped walk over m for L2 reuse of B
+  const int64_t t = blockIdx.x;
+  const int g = p.grid_swizzle_log;
+  const int64_t gsz = (int64_t)1 << g;
+  const int64_t ntn = (int64_t)1 << p.n_hi;
+  const int64_t grp = t / (gsz * ntn), in = t % (gsz * ntn);
+  const int64_t tm = grp * gsz + (in & (gsz - 1));
+  const int64_t tn = in >> g;
+
+  constexpr int EL = GBM * GBK / GTHREADS;  // 8 elements of A (and B) per thread per stage
+  int64_t aoff[EL], boff[EL];
+  int asx[EL], bsx[EL];
+#pragma unroll
+  for (int i = 0; i < EL; ++i) {
+    int r, k;
+    tile_elem(p.ta, tid + i * GTHREADS, aoff[i], r, k);
+    asx[i] = k * GLDA + r;
+    tile_elem(p.tb, tid + i * GTHREADS, boff[i], r, k);
+    bsx[i] = k * GLDB + r;
+  }
+  const double* Ab = p.A + deposit(tm, p.a_m);
+  const double* Bb = p.B + deposit(tn, p.b_n);
+
+  auto load_stage = [&](int stage, int64_t kt) {
+    const double* Ag = Ab + deposit(kt, p.a_k);
+    const double* Bg = Bb + deposit(kt, p.b_k);
+    double* as = As + stage * GBK * GLDA;
+    double* bs = Bs + stage * GBK * GLDB;
+#pragma unroll
+    for (int i = 0; i < EL; ++i) cp_async8(as + asx[i], Ag + aoff[i]);
+#pragma unroll
+    for (int i = 0; i < EL; ++i) cp_async8(bs + bsx[i], Bg + boff[i]);
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < GSTAGES - 1; ++s) {
+    if (s < p.k_tiles) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int64_t kt = 0; kt < p.k_tiles; ++kt) {
+    cp_async_wait<GSTAGES - 2>();
+    __syncthreads();
+    {
+      int64_t nk = kt + GSTAGES - 1;
+      if (nk < p.k_tiles) load_stage((int)(nk % GSTAGES), nk);
+      cp_async_commit();
+    }
+    const double* as = As + (kt % GSTAGES) * GBK * GLDA;
+    const double* bs = Bs + (kt % GSTAGES) * GBK * GLDB;
+#pragma unroll
+    for (int kk = 0; kk < GBK / 4; ++kk) {
+      double af[4], bf[4];
+      const int kr = kk * 4 + (lane & 3);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = as[kr * GLDA + wm * 32 + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = bs[kr * GLDB + wn * 32 + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  double* Cs = gsm;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int row = wm * 32 + i * 8 + (lane >> 2);
+      const int col = wn * 32 + j * 8 + (lane & 3) * 2;
+      Cs[row * GLDC + col] = acc[i][j][0];
+      Cs[row * GLDC + col + 1] = acc[i][j][1];
+    }
+  __syncthreads();
+  double* Cg = p.C + deposit(tm, p.c_m) + deposit(tn, p.c_n);
+  for (int e = tid; e < GBM * GBN; e += GTHREADS) {
+    int64_t off;
+    int r, k;
+    tile_elem(p.tc, e, off, r, k);
+    Cg[off] = Cs[r * GLDC + k];
+  }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_generic(const GenericParams p) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < p.c_size;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    int64_t oa = 0, ob = 0, r = c;
+    for (int j = 0; j < p.nc; ++j) {
+      const GDigit d = p.dig[j];
+      int64_t q = r % d.dim;
+      r /= d.dim;
+      oa += q * d.sa;
+      ob += q * d.sb;
+    }
+    double acc = 0.0;
+    for (int64_t s = 0; s < p.s_size; ++s) {
+      int64_t xa = oa, xb = ob, r2 = s;
+      for (int j = 0; j < p.ns; ++j) {
+        const GDigit d = p.dig[p.nc + j];
+        int64_t q = r2 % d.dim;
+        r2 /= d.dim;
+        xa += q * d.sa;
+        xb += q * d.sb;
+      }
+      acc = fma(p.A[xa], p.B[xb], acc);
+    }
+    p.C[c] = acc;
+  }
+}
+
+}  // namespace tc

@@ -1,0 +1,662 @@
+// libtc runtime: the C-ABI of include/tc.h.
+//
+//  * tc_plan_*              symbolic plan (plan.cpp)
+//  * tc_exec_create         compile (compile.cpp) -> bind device pointers ->
+//                           one CUDA graph per device whose kernel nodes mirror
+//                           the contraction DAG (independent branches run
+//                           concurrently; arena reuse adds WAR edges)
+//  * tc_exec_run            replay the graph once per slice; per-slice result
+//                           slots stay in HBM
+//  * tc_sliced_execute      Algorithm 3 end to end, multi-device with one
+//                           NCCL all-reduce over the zero-padded per-slice
+//                           vector (exact: one non-zero contributor per slot),
+//                           then the lexicographic fold on device.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "compile.hpp"
+#include "kernels.cuh"
+#include "plan.hpp"
+#include "tc.h"
+
+using namespace tc;
+
+struct tc_plan {
+  Plan p;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int st, const std::string& m) {
+  g_err = m;
+  return st;
+}
+
+#define CU(x)                                                                             \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess) {                                                              \
+      int st_ = (e_ == cudaErrorMemoryAllocation) ? TC_OOM : TC_CUDA;                     \
+      throw Error{st_, std::string(#x) + ": " + cudaGetErrorString(e_)};                  \
+    }                                                                                     \
+  } while (0)
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return TC_OK;
+  } catch (const Error& e) {
+    return set_err(e.status, e.msg);
+  } catch (const std::bad_alloc&) {
+    return set_err(TC_OOM, "host out of memory");
+  } catch (const std::exception& e) {
+    return set_err(TC_BAD_ARG, e.what());
+  }
+}
+
+std::string u128_str(u128 v) {
+  if (v == 0) return "0";
+  std::string s;
+  while (v) {
+    s.push_back(char('0' + (int)(v % 10)));
+    v /= 10;
+  }
+  return std::string(s.rbegin(), s.rend());
+}
+
+template <class T>
+T* dalloc(size_t n, int64_t& total) {
+  T* p = nullptr;
+  size_t b = std::max<size_t>(n * sizeof(T), 16);
+  CU(cudaMalloc(&p, b));
+  total += (int64_t)b;
+  return p;
+}
+
+using StreamFn = void (*)(StreamParams);
+StreamFn stream_fn(int ns, int nf) {
+#define SF(a, b) \
+  if (ns == a && nf == b) return k_stream<a, b>;
+  SF(0, 0) SF(0, 1) SF(0, 2) SF(0, 3) SF(0, 4)
+  SF(1, 0) SF(1, 1) SF(1, 2) SF(1, 3) SF(1, 4)
+  SF(2, 0) SF(2, 1) SF(2, 2) SF(2, 3) SF(2, 4)
+  SF(3, 0) SF(3, 1) SF(3, 2) SF(3, 3)
+  SF(4, 0) SF(4, 1) SF(4, 2)
+#undef SF
+  throw Error{TC_BAD_ARG, "no stream kernel for this shape"};
+}
+
+int sm_count(int dev) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+unsigned grid_for(int64_t work, int per_block, int dev, int max_per_sm = 8) {
+  int64_t g = (work + per_block - 1) / per_block;
+  int64_t cap = (int64_t)sm_count(dev) * max_per_sm;
+  return (unsigned)std::max<int64_t>(1, std::min(g, cap));
+}
+
+}  // namespace
+
+struct tc_exec {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  Program prog;
+  int64_t dev_bytes = 0;
+  char* arena = nullptr;
+  double* leafbuf = nullptr;
+  double* slicedbuf = nullptr;
+  TinyNode* tnodes = nullptr;
+  TinyDigit* tdigs = nullptr;
+  TinyGroup* tgroups = nullptr;
+  GDigit* gdig = nullptr;
+  SelEntry* sel = nullptr;
+  SelTerm* selt = nullptr;
+  int64_t* eta = nullptr;
+  double* results = nullptr;
+  int64_t results_cap = 0;  // slices
+  double* folded = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int64_t kernels_per_slice = 0;
+  int64_t last_n = 0;
+  double compile_ms = 0;
+  // parameter storage (kernel node params point here while adding)
+  std::vector<SelectParams> selp;
+  std::vector<RootCopyParams> rcp;
+
+  ~tc_exec() {
+    if (device >= 0) cudaSetDevice(device);
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (graph) cudaGraphDestroy(graph);
+    for (void* q : {(void*)arena, (void*)leafbuf, (void*)slicedbuf, (void*)tnodes, (void*)tdigs,
+                    (void*)tgroups, (void*)gdig, (void*)sel, (void*)selt, (void*)eta, (void*)results,
+                    (void*)folded})
+      if (q) cudaFree(q);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  const double* ptr(const Loc& l) const {
+    switch (l.kind) {
+      case LOC_LEAF: return leafbuf + l.off;
+      case LOC_SLICED: return slicedbuf + l.off;
+      case LOC_ARENA: return (const double*)(arena + l.off);
+      default: return nullptr;
+    }
+  }
+
+  void build(const Plan& p, const std::vector<int>& chosen) {
+    auto t0 = std::chrono::steady_clock::now();
+    prog = compile_program(p, chosen);
+    CU(cudaSetDevice(device));
+    CU(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    Program& g = prog;
+    arena = dalloc<char>((size_t)g.arena_bytes, dev_bytes);
+    leafbuf = dalloc<double>(p.lval.size(), dev_bytes);
+    CU(cudaMemcpyAsync(leafbuf, p.lval.data(), p.lval.size() * 8, cudaMemcpyHostToDevice, stream));
+    if (g.sliced_doubles) slicedbuf = dalloc<double>((size_t)g.sliced_doubles, dev_bytes);
+    if (!g.sel_ent.empty()) {
+      sel = dalloc<SelEntry>(g.sel_ent.size(), dev_bytes);
+      selt = dalloc<SelTerm>(std::max<size_t>(1, g.sel_terms.size()), dev_bytes);
+      CU(cudaMemcpyAsync(sel, g.sel_ent.data(), g.sel_ent.size() * sizeof(SelEntry), cudaMemcpyHostToDevice, stream));
+      if (!g.sel_terms.empty())
+        CU(cudaMemcpyAsync(selt, g.sel_terms.data(), g.sel_terms.size() * sizeof(SelTerm), cudaMemcpyHostToDevice,
+                           stream));
+    }
+    if (!g.tiny_nodes.empty()) {
+      std::vector<TinyNode> tn = g.tiny_nodes;
+      for (size_t i = 0; i < tn.size(); ++i) {
+        tn[i].ga = ptr(g.tiny_ga[i]);
+        tn[i].gb = ptr(g.tiny_gb[i]);
+        tn[i].gout = (double*)ptr(g.tiny_gout[i]);
+      }
+      tnodes = dalloc<TinyNode>(tn.size(), dev_bytes);
+      tdigs = dalloc<TinyDigit>(std::max<size_t>(1, g.tiny_digits.size()), dev_bytes);
+      tgroups = dalloc<TinyGroup>(g.tiny_groups.size(), dev_bytes);
+      CU(cudaMemcpyAsync(tnodes, tn.data(), tn.size() * sizeof(TinyNode), cudaMemcpyHostToDevice, stream));
+      if (!g.tiny_digits.empty())
+        CU(cudaMemcpyAsync(tdigs, g.tiny_digits.data(), g.tiny_digits.size() * sizeof(TinyDigit),
+                           cudaMemcpyHostToDevice, stream));
+      CU(cudaMemcpyAsync(tgroups, g.tiny_groups.data(), g.tiny_groups.size() * sizeof(TinyGroup),
+                         cudaMemcpyHostToDevice, stream));
+    }
+    if (!g.gdigits.empty()) {
+      gdig = dalloc<GDigit>(g.gdigits.size(), dev_bytes);
+      CU(cudaMemcpyAsync(gdig, g.gdigits.data(), g.gdigits.size() * sizeof(GDigit), cudaMemcpyHostToDevice, stream));
+    }
+    eta = dalloc<int64_t>(2, dev_bytes);
+    folded = dalloc<double>((size_t)g.R, dev_bytes);
+    CU(cudaStreamSynchronize(stream));
+
+    const int tiny_smem = (int)(g.tiny_smem_doubles + kTinyThreads) * 8;
+    CU(cudaFuncSetAttribute(k_tiny, cudaFuncAttributeMaxDynamicSharedMemorySize, tiny_smem));
+    CU(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes));
+
+    // ---- graph: one kernel node per step, edges = data + WAR deps ----
+    CU(cudaGraphCreate(&graph, 0));
+    std::vector<cudaGraphNode_t> nodes(g.steps.size());
+    selp.reserve(1);
+    rcp.reserve(1);
+    kernels_per_slice = 0;
+    for (size_t si = 0; si < g.steps.size(); ++si) {
+      Step& st = g.steps[si];
+      std::vector<cudaGraphNode_t> deps;
+      for (int d : st.deps) deps.push_back(nodes[d]);
+      cudaKernelNodeParams kp{};
+      kp.blockDim = dim3(256);
+      kp.sharedMemBytes = 0;
+      void* args[4];
+      kp.kernelParams = args;
+      StreamParams sp;
+      GemmParams gp;
+      GenericParams np;
+      SelectParams slp;
+      RootCopyParams rp;
+      const TinyNode* a_nodes = tnodes;
+      const TinyDigit* a_digs = tdigs;
+      const TinyGroup* a_groups = nullptr;
+      int32_t smd = g.tiny_smem_doubles;
+      int64_t* eta_arg = eta;
+      switch (st.kind) {
+        case ST_SELECT:
+          slp = SelectParams{leafbuf, slicedbuf, sel, selt, (int64_t)g.sel_ent.size(), eta};
+          kp.func = (void*)k_select;
+          kp.gridDim = dim3(grid_for(slp.n, 256, device));
+          args[0] = &slp;
+          break;
+        case ST_TINY:
+          a_groups = tgroups + st.gdig_off;
+          kp.func = (void*)k_tiny;
+          kp.gridDim = dim3((unsigned)st.work);
+          kp.blockDim = dim3(kTinyThreads);
+          kp.sharedMemBytes = tiny_smem;
+          args[0] = &a_nodes;
+          args[1] = &a_digs;
+          args[2] = &a_groups;
+          args[3] = &smd;
+          break;
+        case ST_STREAM:
+          sp = st.sp;
+          sp.A = ptr(st.la);
+          sp.P = ptr(st.lb);
+          sp.C = (double*)ptr(st.lc);
+          kp.func = (void*)stream_fn(st.ns, st.nf);
+          kp.blockDim = dim3(kStreamThreads);
+          kp.gridDim = dim3(grid_for(sp.nx, kStreamThreads * kStreamUnroll, device));
+          args[0] = &sp;
+          break;
+        case ST_GEMM:
+          gp = st.gp;
+          gp.A = ptr(st.la);
+          gp.B = ptr(st.lb);
+          gp.C = (double*)ptr(st.lc);
+          kp.func = (void*)k_gemm;
+          kp.blockDim = dim3(GTHREADS);
+          kp.gridDim = dim3((unsigned)st.work);
+          kp.sharedMemBytes = kGemmSmemBytes;
+          args[0] = &gp;
+          break;
+        case ST_GENERIC:
+          np = st.np;
+          np.A = ptr(st.la);
+          np.B = ptr(st.lb);
+          np.C = (double*)ptr(st.lc);
+          np.dig = gdig + st.gdig_off;
+          kp.func = (void*)k_generic;
+          kp.gridDim = dim3(grid_for(np.c_size, 256, device));
+          args[0] = &np;
+          break;
+        case ST_ROOTCOPY:
+          rp = RootCopyParams{ptr(g.root_loc), nullptr, g.R, eta};
+          rcp.push_back(rp);
+          kp.func = (void*)k_rootcopy;
+          kp.gridDim = dim3(grid_for(g.R, 256, device));
+          args[0] = &rcp.back();  // results pointer patched per run (node params update)
+          break;
+        case ST_ETA:
+          kp.func = (void*)k_eta;
+          kp.gridDim = dim3(1);
+          kp.blockDim = dim3(1);
+          args[0] = &eta_arg;
+          break;
+      }
+      CU(cudaGraphAddKernelNode(&nodes[si], graph, deps.data(), deps.size(), &kp));
+      ++kernels_per_slice;
+      if (st.kind == ST_ROOTCOPY) rootcopy_node = nodes[si];
+    }
+    CU(cudaGraphInstantiate(&gexec, graph, 0));
+    compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+
+  cudaGraphNode_t rootcopy_node = nullptr;
+
+  void ensure_results(int64_t n) {
+    if (n <= results_cap) return;
+    if (results) CU(cudaFree(results));
+    results = nullptr;
+    int64_t dummy = 0;
+    results = dalloc<double>((size_t)(n * prog.R), dummy);
+    results_cap = n;
+    // patch the root-copy node with the new results pointer
+    RootCopyParams rp = rcp.back();
+    rp.results = results;
+    rcp.back() = rp;
+    cudaKernelNodeParams kp{};
+    void* args[1] = {&rcp.back()};
+    kp.func = (void*)k_rootcopy;
+    kp.gridDim = dim3(grid_for(prog.R, 256, device));
+    kp.blockDim = dim3(256);
+    kp.kernelParams = args;
+    CU(cudaGraphExecKernelNodeSetParams(gexec, rootcopy_node, &kp));
+  }
+
+  double run(int64_t b, int64_t e) {
+    CU(cudaSetDevice(device));
+    int64_t n = e - b;
+    if (n <= 0) {
+      last_n = 0;
+      return 0.0;
+    }
+    ensure_results(n);
+    int64_t h[2] = {b, b};
+    CU(cudaMemcpyAsync(eta, h, sizeof(h), cudaMemcpyHostToDevice, stream));
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    CU(cudaEventRecord(e0, stream));
+    for (int64_t s = 0; s < n; ++s) CU(cudaGraphLaunch(gexec, stream));
+    CU(cudaEventRecord(e1, stream));
+    CU(cudaEventSynchronize(e1));
+    CU(cudaGetLastError());
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    last_n = n;
+    return ms;
+  }
+
+  void fold(double* out_host) {
+    CU(cudaSetDevice(device));
+    k_fold<<<grid_for(prog.R, 256, device), 256, 0, stream>>>(results, prog.R, last_n, folded);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(out_host, folded, prog.R * 8, cudaMemcpyDeviceToHost, stream));
+    CU(cudaStreamSynchronize(stream));
+  }
+};
+
+// ---------------------------------------------------------------------------
+// NCCL (single process, one communicator per device), loaded on first use.
+namespace {
+typedef struct ncclComm* ncclComm_t;
+typedef int ncclResult_t;
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      n.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (n.h) break;
+    }
+    if (!n.h) return;
+    n.CommInitAll = (decltype(n.CommInitAll))dlsym(n.h, "ncclCommInitAll");
+    n.AllReduce = (decltype(n.AllReduce))dlsym(n.h, "ncclAllReduce");
+    n.GroupStart = (decltype(n.GroupStart))dlsym(n.h, "ncclGroupStart");
+    n.GroupEnd = (decltype(n.GroupEnd))dlsym(n.h, "ncclGroupEnd");
+    n.CommDestroy = (decltype(n.CommDestroy))dlsym(n.h, "ncclCommDestroy");
+    n.GetErrorString = (decltype(n.GetErrorString))dlsym(n.h, "ncclGetErrorString");
+  });
+  if (!n.h || !n.CommInitAll || !n.AllReduce) throw Error{TC_NCCL, "libnccl.so.2 not loadable"};
+  return n;
+}
+#define NC(x)                                                                          \
+  do {                                                                                 \
+    ncclResult_t r_ = (x);                                                             \
+    if (r_ != 0) throw Error{TC_NCCL, std::string(#x) + ": " + nccl().GetErrorString(r_)}; \
+  } while (0)
+constexpr int kNcclFloat64 = 8, kNcclSum = 0;
+}  // namespace
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* tc_last_error(void) { return g_err.c_str(); }
+int32_t tc_version(void) { return 1; }
+int32_t tc_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int tc_plan_create(const tc_plan_desc* desc, tc_plan** out) {
+  return guard([&] {
+    if (!desc || !out) throw Error{TC_BAD_ARG, "null argument"};
+    auto h = std::make_unique<tc_plan>();
+    h->p = build_plan(*desc);
+    *out = h.release();
+  });
+}
+
+void tc_plan_free(tc_plan* plan) { delete plan; }
+
+int tc_plan_info_get(const tc_plan* plan, tc_plan_info* out) {
+  return guard([&] {
+    const Plan& p = plan->p;
+    out->num_bonds = (int32_t)p.bonds_sorted.size();
+    int nf = 0;
+    for (int i = 0; i < p.NI; ++i) nf += (p.occ0[i] >= 0 && p.occ1[i] < 0);
+    out->num_free = nf;
+    out->max_rank = max_rank(p);
+    out->root_rank = (int32_t)p.sets[p.root].size();
+    out->contraction_ops = to_abi(contraction_ops(p));
+    std::vector<char> none(p.NI, 0);
+    out->mem_cost = to_abi(mem_cost(p, none));
+  });
+}
+
+int tc_mem_cost(const tc_plan* plan, const int32_t* drop, int32_t n_drop, tc_u128* out) {
+  return guard([&] { *out = to_abi(mem_cost(plan->p, mask_of(plan->p, drop, n_drop))); });
+}
+
+int tc_choose_slice_index(const tc_plan* plan, const int32_t* already, int32_t n_already, int32_t* out_index) {
+  return guard([&] { *out_index = choose_slice_index(plan->p, mask_of(plan->p, already, n_already)); });
+}
+
+int tc_choose_slices(const tc_plan* plan, int64_t mem_budget, int32_t* chosen, int32_t cap, int32_t* n_chosen,
+                     tc_u128* needs) {
+  return guard([&] {
+    const Plan& p = plan->p;
+    std::vector<char> mask(p.NI, 0);
+    int n = 0;
+    auto over = [&](u128 c) { return mem_budget < 0 || c > (u128)mem_budget; };
+    while (over(mem_cost(p, mask))) {
+      int pick;
+      try {
+        pick = choose_slice_index(p, mask);
+      } catch (const Error& e) {
+        if (e.status != TC_NO_CANDIDATES) throw;
+        std::vector<char> all(p.NI, 0);
+        for (int i : p.bonds_sorted) all[i] = 1;
+        u128 need = mem_cost(p, all);
+        if (needs) *needs = to_abi(need);
+        *n_chosen = n;
+        throw Error{TC_BUDGET_INFEASIBLE, "cannot fit in " + std::to_string(mem_budget) +
+                                              " bytes even fully sliced (needs " + u128_str(need) + ")"};
+      }
+      if (n >= cap) throw Error{TC_BAD_ARG, "chosen buffer too small"};
+      chosen[n++] = pick;
+      mask[pick] = 1;
+    }
+    *n_chosen = n;
+  });
+}
+
+int tc_result_indices(const tc_plan* plan, const int32_t* sliced, int32_t n_sliced, int32_t* out_idx, int32_t cap,
+                      int32_t* rank) {
+  return guard([&] {
+    const Plan& p = plan->p;
+    auto m = mask_of(p, sliced, n_sliced);
+    int r = 0;
+    for (int i : p.ref_order[p.root])
+      if (!m[i]) {
+        if (r >= cap) throw Error{TC_BAD_ARG, "index buffer too small"};
+        out_idx[r++] = i;
+      }
+    *rank = r;
+  });
+}
+
+int tc_exec_create(const tc_plan* plan, const int32_t* sliced, int32_t n_sliced, int32_t device, tc_exec** out) {
+  return guard([&] {
+    auto ex = std::make_unique<tc_exec>();
+    ex->device = device;
+    std::vector<int> ch(sliced, sliced + std::max(0, n_sliced));
+    ex->build(plan->p, ch);
+    *out = ex.release();
+  });
+}
+
+void tc_exec_free(tc_exec* ex) { delete ex; }
+
+int64_t tc_exec_result_size(const tc_exec* ex) { return ex->prog.R; }
+
+static void fill_stats(const tc_exec& ex, double ms, tc_stats* s) {
+  if (!s) return;
+  const Program& g = ex.prog;
+  s->mem_estimate = to_abi(g.mem_estimate);
+  s->peak_observed = to_abi(g.peak_observed);
+  s->num_slices = g.num_slices;
+  s->device_peak_bytes = ex.dev_bytes;
+  s->device_ms = ms;
+  s->compile_ms = ex.compile_ms;
+  s->gpu_launches = ex.kernels_per_slice * ex.last_n;
+  s->n_tiny_nodes = g.n_tiny;
+  s->n_stream_nodes = g.n_stream;
+  s->n_gemm_nodes = g.n_gemm;
+  s->n_generic_nodes = g.n_generic;
+  s->alg_bytes = to_abi(g.alg_bytes);
+  s->alg_flops = to_abi(g.alg_flops);
+}
+
+int tc_exec_run(tc_exec* ex, int64_t slice_begin, int64_t slice_end, tc_stats* stats) {
+  return guard([&] {
+    if (slice_begin < 0 || slice_end > ex->prog.num_slices || slice_begin > slice_end)
+      throw Error{TC_BAD_ARG, "slice range out of bounds"};
+    double ms = ex->run(slice_begin, slice_end);
+    fill_stats(*ex, ms, stats);
+  });
+}
+
+int tc_exec_fetch(tc_exec* ex, double* per_slice, double* folded) {
+  return guard([&] {
+    CU(cudaSetDevice(ex->device));
+    if (per_slice && ex->last_n > 0)
+      CU(cudaMemcpy(per_slice, ex->results, ex->last_n * ex->prog.R * 8, cudaMemcpyDeviceToHost));
+    if (folded) {
+      if (ex->last_n <= 0) throw Error{TC_BAD_ARG, "no slices were run"};
+      ex->fold(folded);
+    }
+  });
+}
+
+int tc_sliced_execute(const tc_plan* plan, int64_t mem_budget, const int32_t* slice_ids, int32_t n_slice_ids,
+                      const int32_t* devices, int32_t n_devices, double* out_val, int64_t out_cap,
+                      int32_t* out_idx, int32_t idx_cap, int32_t* out_rank, int32_t* chosen, int32_t chosen_cap,
+                      int32_t* n_chosen, tc_stats* stats) {
+  return guard([&] {
+    const Plan& p = plan->p;
+    std::vector<int> ch;
+    if (n_slice_ids >= 0) {
+      ch.assign(slice_ids, slice_ids + n_slice_ids);
+    } else if (mem_budget != INT64_MIN) {  // INT64_MIN encodes mem_budget=None
+      std::vector<int32_t> buf(p.bonds_sorted.size() + 1);
+      int32_t nc = 0;
+      tc_u128 need{};
+      int st = tc_choose_slices(plan, mem_budget, buf.data(), (int32_t)buf.size(), &nc, &need);
+      if (st != TC_OK) throw Error{st, g_err};
+      ch.assign(buf.begin(), buf.begin() + nc);
+    }
+    if ((int)ch.size() > chosen_cap) throw Error{TC_BAD_ARG, "chosen buffer too small"};
+    for (size_t j = 0; j < ch.size(); ++j) chosen[j] = ch[j];
+    *n_chosen = (int32_t)ch.size();
+    {
+      auto m = mask_of(p, ch.data(), (int)ch.size());
+      int r = 0;
+      for (int i : p.ref_order[p.root])
+        if (!m[i]) {
+          if (r >= idx_cap) throw Error{TC_BAD_ARG, "index buffer too small"};
+          out_idx[r++] = i;
+        }
+      *out_rank = r;
+    }
+    std::vector<int> devs;
+    if (n_devices <= 0) devs.push_back(0);
+    else devs.assign(devices, devices + n_devices);
+    const int G = (int)devs.size();
+    std::vector<std::unique_ptr<tc_exec>> ex(G);
+    std::vector<Error> errs(G, Error{TC_OK, ""});
+    std::vector<double> ms(G, 0.0);
+    // compile once per device (threads), then block-partition the slice ids
+    int64_t NS = 1, R = 1;
+    for (int i : ch) {
+      if (i < 0 || i >= p.NI) throw Error{TC_BAD_ARG, "slice index id out of range"};
+      if (__builtin_mul_overflow(NS, (int64_t)p.dom[i], &NS)) throw Error{TC_OVERFLOW, "too many slices"};
+    }
+    {
+      auto m = mask_of(p, ch.data(), (int)ch.size());
+      for (int i : p.sets[p.root])
+        if (!m[i]) R *= p.dom[i];
+    }
+    if (R > out_cap) throw Error{TC_BAD_ARG, "output buffer too small"};
+    const int64_t per = (NS + G - 1) / G;
+    auto work = [&](int gi) {
+      try {
+        ex[gi] = std::make_unique<tc_exec>();
+        ex[gi]->device = devs[gi];
+        ex[gi]->build(p, ch);
+        int64_t b = std::min<int64_t>(NS, gi * per), e = std::min<int64_t>(NS, b + per);
+        ms[gi] = ex[gi]->run(b, e);
+      } catch (const Error& e) {
+        errs[gi] = e;
+      }
+    };
+    if (G == 1) {
+      work(0);
+    } else {
+      std::vector<std::thread> th;
+      for (int gi = 0; gi < G; ++gi) th.emplace_back(work, gi);
+      for (auto& t : th) t.join();
+    }
+    for (auto& e : errs)
+      if (e.status != TC_OK) throw e;
+    if (G == 1) {
+      ex[0]->fold(out_val);
+    } else {
+      // zero-padded [NS][R] vector on every device, one all-reduce (exact: a
+      // single non-zero contributor per position), fold on device 0
+      auto& nc = nccl();
+      std::vector<ncclComm_t> comms(G);
+      NC(nc.CommInitAll(comms.data(), G, devs.data()));
+      std::vector<double*> full(G, nullptr);
+      for (int gi = 0; gi < G; ++gi) {
+        CU(cudaSetDevice(devs[gi]));
+        int64_t dummy = 0;
+        full[gi] = dalloc<double>((size_t)(NS * R), dummy);
+        CU(cudaMemsetAsync(full[gi], 0, NS * R * 8, ex[gi]->stream));
+        int64_t b = std::min<int64_t>(NS, gi * per);
+        if (ex[gi]->last_n > 0)
+          CU(cudaMemcpyAsync(full[gi] + b * R, ex[gi]->results, ex[gi]->last_n * R * 8, cudaMemcpyDeviceToDevice,
+                             ex[gi]->stream));
+      }
+      NC(nc.GroupStart());
+      for (int gi = 0; gi < G; ++gi) NC(nc.AllReduce(full[gi], full[gi], NS * R, kNcclFloat64, kNcclSum, comms[gi], ex[gi]->stream));
+      NC(nc.GroupEnd());
+      for (int gi = 0; gi < G; ++gi) {
+        CU(cudaSetDevice(devs[gi]));
+        CU(cudaStreamSynchronize(ex[gi]->stream));
+      }
+      tc_exec& e0 = *ex[0];
+      CU(cudaSetDevice(e0.device));
+      k_fold<<<grid_for(R, 256, e0.device), 256, 0, e0.stream>>>(full[0], R, NS, e0.folded);
+      CU(cudaGetLastError());
+      CU(cudaMemcpyAsync(out_val, e0.folded, R * 8, cudaMemcpyDeviceToHost, e0.stream));
+      CU(cudaStreamSynchronize(e0.stream));
+      for (int gi = 0; gi < G; ++gi) {
+        cudaSetDevice(devs[gi]);
+        cudaFree(full[gi]);
+        if (nc.CommDestroy) nc.CommDestroy(comms[gi]);
+      }
+    }
+    if (stats) {
+      fill_stats(*ex[0], *std::max_element(ms.begin(), ms.end()), stats);
+      int64_t launches = 0;
+      for (auto& e : ex) launches += e->kernels_per_slice * e->last_n;
+      stats->gpu_launches = launches;
+      stats->num_slices = NS;
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+"""Swap the B200 execution stage into an imported ``tensorcount`` package.
+
+The reference has no plugin API for this path: ``driver.py:27``
+binds ``sliced_execute`` at import and calls it at ``driver.py:235``;
+``slicing.py`` and ``network.py`` are imported by the tests directly.  So the
+swap is by module attribute:
+
+    import tensorcount
+    from paper_2006_15512_b200 import reference_patch
+    reference_patch.install(tensorcount)      # count_formula now runs on the GPU
+
+Errors raised by the backend are re-raised as the reference's own exception
+classes (same names), and the return value is the reference's
+``SlicedExecution`` dataclass, so callers cannot tell the difference.
+"""
+
+from __future__ import annotations
+
+import functools
+import importlib
+
+from . import errors as own_errors
+from . import network as own_network
+from . import slicing as own_slicing
+
+_SAVED = {}
+
+
+def _translate(ref_errors):
+    mapping = {}
+    for name in ("IndexMismatch", "BindingOutOfDomain", "IndexOveruse", "PlanMismatch",
+                 "NotABondIndex", "NoCandidates", "BudgetInfeasible"):
+        mapping[getattr(own_errors, name)] = getattr(ref_errors, name)
+    return mapping
+
+
+def install(tensorcount=None, devices=None):
+    """Patch ``tensorcount.{driver,slicing,network}`` to use libtc."""
+    if tensorcount is None:
+        tensorcount = importlib.import_module("tensorcount")
+    driver = importlib.import_module(tensorcount.__name__ + ".driver")
+    slicing = importlib.import_module(tensorcount.__name__ + ".slicing")
+    network = importlib.import_module(tensorcount.__name__ + ".network")
+    ref_errors = importlib.import_module(tensorcount.__name__ + ".errors")
+    emap = _translate(ref_errors)
+    RefSE = slicing.SlicedExecution
+
+    def wrap(fn, convert=None):
+        @functools.wraps(fn)
+        def inner(*a, **kw):
+            try:
+                out = fn(*a, **kw)
+            except tuple(emap) as e:
+                raise emap[type(e)](str(e)) from None
+            return convert(out) if convert else out
+        return inner
+
+    def to_ref(se):
+        return RefSE(se.result, list(se.sliced_indices), se.mem_estimate, se.peak_observed, se.num_slices)
+
+    def sliced_execute(n, t, mem_budget=None, **kw):
+        if devices is not None and "devices" not in kw:
+            kw["devices"] = devices
+        return own_slicing.sliced_execute(n, t, mem_budget, **kw)
+
+    def execute(n, t):
+        return own_network.execute(n, t, devices=devices)
+
+    patched = {
+        (driver, "sliced_execute"): wrap(sliced_execute, to_ref),
+        (slicing, "sliced_execute"): wrap(sliced_execute, to_ref),
+        (slicing, "mem_cost"): wrap(own_slicing.mem_cost),
+        (slicing, "choose_slice_index"): wrap(own_slicing.choose_slice_index),
+        (network, "execute"): wrap(execute),
+        (tensorcount, "sliced_execute"): wrap(sliced_execute, to_ref),
+        (tensorcount, "execute"): wrap(execute),
+    }
+    for (mod, name), fn in patched.items():
+        _SAVED.setdefault((mod, name), getattr(mod, name))
+        setattr(mod, name, fn)
+
+
+def uninstall():
+    for (mod, name), fn in _SAVED.items():
+        setattr(mod, name, fn)
+    _SAVED.clear()

@@ -1,0 +1,108 @@
+"""Memory-bounded execution by index slicing — the drop-in for the reference's
+``slicing.py`` (Algorithm 3, ``pkg/src/tensorcount/slicing.py:112-146``).
+
+Same names, signatures, return type and error behaviour:
+
+* ``mem_cost(n, t, drop=frozenset())``          — slicing.py:52-67 (exact, libtc)
+* ``choose_slice_index(n, t, already=frozenset())`` — slicing.py:70-79 (libtc,
+  incremental; identical picks incl. the sort_key tie-break)
+* ``sliced_execute(n, t, mem_budget=None)``     — slicing.py:112-146, executed
+  on the B200 by libtc.  Extra keyword-only arguments: ``slice_indices``
+  (explicit slice set, skips the greedy), ``devices`` (list of CUDA ordinals).
+* ``SlicedExecution``                           — slicing.py:82-88 (+ ``stats``)
+
+Inputs may be this package's mirror types or the reference's own objects
+(duck-typed); the result tensor is built with the caller's Tensor class.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import BudgetInfeasible, NoCandidates, PlanMismatch
+from .flatten import flatten
+
+BYTES_PER_ENTRY = 8
+
+
+@dataclass
+class SlicedExecution:
+    result: object
+    sliced_indices: list = field(default_factory=list)
+    mem_estimate: int = 0
+    peak_observed: int = 0
+    num_slices: int = 1
+    stats: dict = field(default=None, repr=False, compare=False)
+
+
+def _plan(n, t):
+    flat = flatten(n, t)
+    if flat.root_slot < 0 or (flat.left < 0).any() or (flat.right < 0).any():
+        raise PlanMismatch("contraction tree leaves do not match the network")
+    return flat, _lib.PlanHandle(flat)
+
+
+def _ids(flat, indices):
+    pos = {ix: k for k, ix in enumerate(flat.indices)}
+    out = []
+    for ix in indices:
+        k = pos.get(ix)
+        if k is None:
+            continue  # an index absent from the network drops nothing
+        out.append(k)
+    return out
+
+
+def mem_cost(n, t, drop=frozenset()) -> int:
+    """Peak live bytes of strict postorder execution with ``drop`` sliced."""
+    flat, h = _plan(n, t)
+    return h.mem_cost(_ids(flat, drop))
+
+
+def choose_slice_index(n, t, already=frozenset()):
+    """Greedy pick: the bond minimising mem_cost, ties by smallest sort_key."""
+    flat, h = _plan(n, t)
+    k = h.choose_slice_index(_ids(flat, already))
+    return flat.indices[k]
+
+
+def _run(n, t, mem_budget=None, devices=None, slice_indices=None):
+    flat, h = _plan(n, t)
+    sl = None if slice_indices is None else [flat.indices.index(ix) if ix in flat.indices else -1
+                                             for ix in slice_indices]
+    if sl is not None and any(k < 0 for k in sl):
+        from .errors import NotABondIndex
+        raise NotABondIndex("slice index is not an index of the network")
+    vals, idx, chosen, stats = h.sliced_execute(mem_budget, sl, devices)
+    tensor_cls = type(n.tensors[0])
+    inds = tuple(flat.indices[i] for i in idx)
+    shape = tuple(int(flat.domain[i]) for i in idx)
+    result = tensor_cls(inds, np.asarray(vals, dtype=np.float64).reshape(shape))
+    return SlicedExecution(
+        result=result,
+        sliced_indices=[flat.indices[i] for i in chosen],
+        mem_estimate=stats["mem_estimate"],
+        peak_observed=stats["peak_observed"],
+        num_slices=stats["num_slices"],
+        stats=stats,
+    )
+
+
+def sliced_execute(n, t, mem_budget: int | None = None, *, slice_indices=None, devices=None) -> SlicedExecution:
+    """Execute the plan within the byte budget on the GPU, slicing bond
+    indices as needed and summing per-slice results in lexicographic order."""
+    return _run(n, t, mem_budget=mem_budget, devices=devices, slice_indices=slice_indices)
+
+
+__all__ = [
+    "BYTES_PER_ENTRY",
+    "BudgetInfeasible",
+    "NoCandidates",
+    "SlicedExecution",
+    "choose_slice_index",
+    "mem_cost",
+    "sliced_execute",
+]
