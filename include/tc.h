@@ -136,10 +136,31 @@ void tc_exec_free(tc_exec* ex);
  * tc_exec_fetch.  Timed with CUDA events on the exec's stream. */
 int tc_exec_run(tc_exec* ex, int64_t slice_begin, int64_t slice_end, tc_stats* stats);
 
+/* `repeats` back-to-back passes over [slice_begin, slice_end), timed as one
+ * CUDA-event interval on the exec's stream (stats->device_ms = total). */
+int tc_exec_run_repeat(tc_exec* ex, int64_t slice_begin, int64_t slice_end, int64_t repeats,
+                       tc_stats* stats);
+
+/* Copy the last run's per-slice results ([n][R] FP64) into a caller-owned
+ * DEVICE buffer on the exec's device (e.g. a torch tensor's data_ptr()). */
+int tc_exec_copy_results(tc_exec* ex, double* dst_device);
+
+/* Lexicographic left fold of a [n][R] FP64 device array into out[R]
+ * (device pointers on `device`): ((p0 + p1) + p2) + ... */
+int tc_fold_device(const double* per_slice_device, int64_t R, int64_t n, double* out_device,
+                   int32_t device);
+
 /* Copy the per-slice results of the last run ([n_slices][result_size]) to
  * host and/or fold them in lexicographic order on the device
  * (tensor.py:111-115 left fold).  Either pointer may be NULL. */
 int tc_exec_fetch(tc_exec* ex, double* per_slice, double* folded);
+
+/* Diagnostics: replay one slice eagerly, one kernel at a time, and report
+ * per-launch CUDA-event time, kind (0 select, 1 tiny, 2 stream, 3 gemm,
+ * 4 generic, 5 root copy, 6 slice counter), node slot and algorithmic
+ * bytes / flops.  Arrays hold `cap` entries; *n = number of launches. */
+int tc_exec_profile(tc_exec* ex, int64_t slice, float* step_ms, int32_t* step_kind, int32_t* step_slot,
+                    double* step_bytes, double* step_flops, int32_t cap, int32_t* n);
 int64_t tc_exec_result_size(const tc_exec* ex);
 
 /* One-shot Algorithm 3 (slicing.py:112-146) from host buffers: pick slices

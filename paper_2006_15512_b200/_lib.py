@@ -107,7 +107,12 @@ SIGNATURES = {
     "tc_exec_create": (C.c_int, [C.c_void_p, I32P, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
     "tc_exec_free": (None, [C.c_void_p]),
     "tc_exec_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(Stats)]),
+    "tc_exec_run_repeat": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.POINTER(Stats)]),
+    "tc_exec_copy_results": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "tc_fold_device": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32]),
     "tc_exec_fetch": (C.c_int, [C.c_void_p, F64P, F64P]),
+    "tc_exec_profile": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_float), I32P, I32P, F64P, F64P,
+                                  C.c_int32, I32P]),
     "tc_exec_result_size": (C.c_int64, [C.c_void_p]),
     "tc_sliced_execute": (
         C.c_int,
@@ -282,10 +287,31 @@ class Exec:
             _lib.tc_exec_free(self.h)
             self.h = None
 
-    def run(self, begin: int, end: int) -> dict:
+    def run(self, begin: int, end: int, repeats: int = 1) -> dict:
         st = Stats()
-        check(lib().tc_exec_run(self.h, int(begin), int(end), C.byref(st)))
+        check(lib().tc_exec_run_repeat(self.h, int(begin), int(end), int(repeats), C.byref(st)))
         return st.as_dict()
+
+    def copy_results(self, dst_device_ptr: int):
+        """Per-slice results of the last run -> caller's device buffer."""
+        check(lib().tc_exec_copy_results(self.h, C.c_void_p(int(dst_device_ptr))))
+
+    KINDS = ["select", "tiny", "stream", "gemm", "generic", "rootcopy", "eta", "gemm_reduce"]
+
+    def profile(self, slice_id: int = 0):
+        """Per-launch (kind, slot, ms, alg_bytes, alg_flops) of one eager slice."""
+        cap = 1 << 20
+        ms = np.zeros(cap, dtype=np.float32)
+        kind = np.zeros(cap, dtype=np.int32)
+        slot = np.zeros(cap, dtype=np.int32)
+        by = np.zeros(cap, dtype=np.float64)
+        fl = np.zeros(cap, dtype=np.float64)
+        n = C.c_int32()
+        check(lib().tc_exec_profile(self.h, int(slice_id), ms.ctypes.data_as(C.POINTER(C.c_float)), _p(kind, I32P),
+                                    _p(slot, I32P), _p(by, F64P), _p(fl, F64P), cap, C.byref(n)))
+        k = n.value
+        return [dict(kind=self.KINDS[kind[i]], slot=int(slot[i]), ms=float(ms[i]), bytes=float(by[i]),
+                     flops=float(fl[i])) for i in range(k)]
 
     def result_size(self) -> int:
         return int(lib().tc_exec_result_size(self.h))
@@ -298,3 +324,9 @@ class Exec:
             per = np.zeros(per_slice_n * R, dtype=np.float64)
         check(lib().tc_exec_fetch(self.h, _p(per, F64P) if per is not None else None, _p(folded, F64P)))
         return folded, per
+
+
+def fold_device(per_slice_ptr: int, R: int, n: int, out_ptr: int, device: int):
+    """Lexicographic left fold of a [n][R] FP64 device array into out[R]."""
+    check(lib().tc_fold_device(C.c_void_p(int(per_slice_ptr)), int(R), int(n), C.c_void_p(int(out_ptr)),
+                               int(device)))

@@ -28,6 +28,7 @@ namespace {
 constexpr int64_t kTinyMax = 4096;           // entries per tiny tensor
 constexpr int32_t kTinySmemCap = 20 * 1024;  // doubles of smem per tiny CTA (160 KB)
 constexpr int64_t kAlign = 256;
+constexpr int64_t kSMs = 148;                // B200 SM count (split-K sizing)
 
 [[noreturn]] void fail(int st, const std::string& m) { throw Error{st, m}; }
 
@@ -193,12 +194,12 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in) {
       int ks = (int)inter(eff[a], eff[b]).size();
       int ra = (int)eff[a].size() - ks, rb = (int)eff[b].size() - ks;
       int f = (eff[b].size() <= eff[a].size()) ? rb : ra;  // free bits of the smaller operand
+      (void)ra;
+      (void)rb;
       if (ks <= 4 && f <= 4 && ks + f <= 6)
         c = NC_STREAM;
-      else if (ra >= 6 && rb >= 6 && ks >= 4)
-        c = NC_GEMM;
       else
-        c = NC_GENERIC;
+        c = NC_GEMM;  // any m, n, k: tile bits beyond the shape are virtual
     } else {
       c = NC_GENERIC;
     }
@@ -605,9 +606,24 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in) {
       g.alg_flops += 2 * (set_bytes(p, uni, drop) / 8);
       g.alg_bytes += (u128)8 * (u128)(size[a] + size[b] + size[v]);
     }
-    if (g.cls[v] == NC_TINY) continue;
+    const double nb_ = 8.0 * (double)(size[a] + size[b] + size[v]);
+    double nf_;
+    {
+      std::vector<int> uni;
+      std::set_union(eff[a].begin(), eff[a].end(), eff[b].begin(), eff[b].end(), std::back_inserter(uni));
+      nf_ = 2.0 * (double)(set_bytes(p, uni, drop) / 8);
+    }
+    if (g.cls[v] == NC_TINY) {
+      int gi = group_of[v];
+      int ts = tiny_step[glevel[gi]];
+      g.steps[ts].alg_bytes += nb_;
+      g.steps[ts].alg_flops += nf_;
+      continue;
+    }
     Step st;
     st.slot = v;
+    st.alg_bytes = nb_;
+    st.alg_flops = nf_;
     st.la = g.loc[a];
     st.lb = g.loc[b];
     for (int c : {a, b})
@@ -701,11 +717,12 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in) {
         std::sort(M.begin(), M.end(), [&](int x, int y) { return pc[x] < pc[y]; });
         std::sort(N.begin(), N.end(), [&](int x, int y) { return pc[x] < pc[y]; });
         std::sort(K.begin(), K.end(), [&](int x, int y) { return pa[x] < pa[y]; });
-        const int MT = 6, NT = 6, KT = 4;
+        const int m = (int)M.size(), n = (int)N.size(), kk = (int)K.size();
+        const int MT = std::max(3, std::min(6, m)), NT = std::max(3, std::min(6, n)), KT = 4;
         GemmParams gp{};
-        gp.m_hi = (int)M.size() - MT;
-        gp.n_hi = (int)N.size() - NT;
-        gp.k_tiles = (int64_t)1 << ((int)K.size() - KT);
+        gp.m_hi = std::max(0, m - MT);
+        gp.n_hi = std::max(0, n - NT);
+        gp.k_tiles = (int64_t)1 << std::max(0, kk - KT);
         std::vector<std::pair<int, int>> r;
         r.clear();
         for (int t = MT; t < (int)M.size(); ++t) r.push_back({t - MT, pa[M[t]]});
@@ -727,11 +744,19 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in) {
         gp.c_n = make_runs(r);
         auto tmap = [&](std::map<int, int>& P, const std::vector<int>& R1, int n1,
                         const std::vector<int>& R2, int n2) {
-          // R1 tile bits -> kind 0, R2 tile bits -> kind 1
-          std::vector<std::tuple<int, int, int>> bits;  // pos, kind, sub
-          for (int t = 0; t < n1; ++t) bits.emplace_back(P[R1[t]], 0, t);
-          for (int t = 0; t < n2; ++t) bits.emplace_back(P[R2[t]], 1, t);
+          // R1 tile bits -> kind 0, R2 tile bits -> kind 1; bits past the
+          // shape are virtual (pos -1), placed after the real ones
+          std::vector<std::tuple<int, int, int>> bits, virt;  // pos, kind, sub
+          for (int t = 0; t < n1; ++t) {
+            if (t < (int)R1.size()) bits.emplace_back(P[R1[t]], 0, t);
+            else virt.emplace_back(-1, 0, t);
+          }
+          for (int t = 0; t < n2; ++t) {
+            if (t < (int)R2.size()) bits.emplace_back(P[R2[t]], 1, t);
+            else virt.emplace_back(-1, 1, t);
+          }
           std::sort(bits.begin(), bits.end());
+          bits.insert(bits.end(), virt.begin(), virt.end());
           TileMap tm{};
           tm.nbits = (int)bits.size();
           for (size_t q = 0; q < bits.size(); ++q) {
@@ -745,9 +770,19 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in) {
         gp.tb = tmap(pb, N, NT, K, KT);
         gp.tc = tmap(pc, M, MT, N, NT);
         gp.grid_swizzle_log = std::min(gp.m_hi, 3);
+        // split-K when the output tiles cannot fill the machine
+        const int64_t tiles = (int64_t)1 << (gp.m_hi + gp.n_hi);
+        int64_t splits = 1;
+        if (tiles < 2 * kSMs && gp.k_tiles >= 8)
+          splits = std::min<int64_t>(gp.k_tiles / 4, (2 * kSMs + tiles - 1) / tiles);
+        splits = std::max<int64_t>(1, splits);
+        gp.k_per_split = (gp.k_tiles + splits - 1) / splits;
+        gp.splits = (int32_t)((gp.k_tiles + gp.k_per_split - 1) / gp.k_per_split);
         st.kind = ST_GEMM;
         st.gp = gp;
-        st.work = (int64_t)1 << (gp.m_hi + gp.n_hi);
+        st.bm = MT;
+        st.bn = NT;
+        st.work = tiles;
         g.n_gemm++;
         done = true;
       } catch (const Error& e) {
@@ -776,8 +811,32 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in) {
       g.n_generic++;
     }
     int me = (int)g.steps.size();
-    producer[v] = me;
-    g.steps.push_back(st);
+    if (st.kind == ST_GEMM && st.gp.splits > 1) {
+      // split-K workspace: [splits][tiles][BM*BN] partial tiles, reduced in split order
+      const int64_t ws_bytes = (int64_t)st.gp.splits * st.work * ((int64_t)1 << (st.bm + st.bn)) * 8;
+      haz.clear();
+      st.lws = Loc{LOC_ARENA, arena.alloc(ws_bytes, haz)};
+      for (int h : haz) st.deps.push_back(h);
+      g.steps.push_back(st);
+      Step rd;
+      rd.kind = ST_GEMM_REDUCE;
+      rd.slot = v;
+      rd.gp = st.gp;
+      rd.bm = st.bm;
+      rd.bn = st.bn;
+      rd.la = st.la;
+      rd.lb = st.lb;
+      rd.lc = st.lc;
+      rd.lws = st.lws;
+      rd.work = st.work;
+      rd.deps.push_back(me);
+      producer[v] = me + 1;
+      g.steps.push_back(rd);
+      arena.release(st.lws.off, ws_bytes, me + 1);
+    } else {
+      producer[v] = me;
+      g.steps.push_back(st);
+    }
     for (int c : {a, b})
       if (g.loc[c].kind == LOC_ARENA) arena.release(g.loc[c].off, bytes[c], me);
   }

@@ -19,7 +19,7 @@ struct Loc {
   int64_t off;  // doubles (LEAF: into leaf values, SLICED: into sliced buffer) or bytes (ARENA)
 };
 
-enum StepKind : int8_t { ST_SELECT, ST_TINY, ST_STREAM, ST_GEMM, ST_GENERIC, ST_ROOTCOPY, ST_ETA };
+enum StepKind : int8_t { ST_SELECT, ST_TINY, ST_STREAM, ST_GEMM, ST_GENERIC, ST_ROOTCOPY, ST_ETA, ST_GEMM_REDUCE };
 
 struct Step {
   StepKind kind;
@@ -30,9 +30,11 @@ struct Step {
   GemmParams gp{};
   GenericParams np{};
   int32_t ns = 0, nf = 0;          // stream template selector
-  Loc la{}, lb{}, lc{};            // operand/output locations
+  int32_t bm = 6, bn = 6;          // GEMM tile bits (template selector)
+  Loc la{}, lb{}, lc{}, lws{};     // operand/output/workspace locations
   int64_t gdig_off = 0;            // generic digits offset (in GDigit units)
   int64_t work = 0;                // elements (for launch sizing)
+  double alg_bytes = 0, alg_flops = 0;  // algorithmic traffic / flops of the node(s)
 };
 
 struct Program {

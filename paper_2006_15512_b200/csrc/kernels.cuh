@@ -43,6 +43,7 @@ __global__ void k_rootcopy(const RootCopyParams p) {
 }
 
 __global__ void k_eta(int64_t* eta) { eta[0] += 1; }
+__global__ void k_eta_reset(int64_t* eta) { eta[0] = eta[1]; }
 
 // left fold in lexicographic slice order: ((p0 + p1) + p2) + ...  (tensor.py:111-115)
 __global__ void k_fold(const double* results, int64_t R, int64_t n, double* out) {
@@ -195,15 +196,14 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream(const StreamParams p)
 }
 
 // ---------------------------------------------------------------------------
-// K3: FP64 tensor-core GEMM.  CTA tile 64x64x16, 4 warps (2x2), warp tile
-// 32x32 = 4x4 DMMA m8n8k4 fragments; 4-stage cp.async pipeline; operands are
-// gathered with per-thread precomputed tile offsets (any bit layout), stored
-// k-major in smem with +4 padding (conflict-free fragment loads); the C tile
-// is staged through smem and written in C's own address order.
-constexpr int GBM = 64, GBN = 64, GBK = 16, GTHREADS = 128, GSTAGES = 4;
-constexpr int GLDA = GBM + 4, GLDB = GBN + 4, GLDC = GBN + 4;
-constexpr int kGemmSmemBytes = GSTAGES * GBK * (GLDA + GLDB) * 8;
-static_assert(GBM * GLDC * 8 <= kGemmSmemBytes, "epilogue tile must fit");
+// K3: FP64 tensor-core GEMM family.  CTA tile BMxBNx16 (BM, BN in 8..64),
+// WGM x WGN warps, each warp a (BM/WGM)x(BN/WGN) block of DMMA m8n8k4
+// fragments; 4-stage cp.async pipeline.  Operands are gathered with
+// per-thread precomputed tile offsets (any bit layout: the index permutation
+// of tensordot is folded into the loads), stored k-major in smem with +4
+// padding (conflict-free fragment loads).  The C tile is staged through smem
+// and written in C's own address order (coalesced for any output layout).
+constexpr int GBK = 16, GSTAGES = 4;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -221,24 +221,44 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void tile_elem(const TileMap& t, int e, int64_t& off, int& r, int& k) {
+// element e of a tile -> (address offset, row coord, k coord); false if virtual
+__device__ __forceinline__ bool tile_elem(const TileMap& t, int e, int64_t& off, int& r, int& k) {
   off = 0;
   r = 0;
   k = 0;
+  bool real = true;
   for (int j = 0; j < t.nbits; ++j)
     if ((e >> j) & 1) {
-      off += (int64_t)1 << t.pos[j];
+      if (t.pos[j] < 0) real = false;
+      else off += (int64_t)1 << t.pos[j];
       if (t.kind[j]) k |= 1 << t.sub[j];
       else r |= 1 << t.sub[j];
     }
+  return real;
 }
 
-__global__ void __launch_bounds__(GTHREADS) k_gemm(const GemmParams p) {
+template <int BM, int BN, int WGM, int WGN>
+struct GemmCfg {
+  static constexpr int NT = 32 * WGM * WGN;
+  static constexpr int LDA = BM + 4, LDB = BN + 4, LDC = BN + 4;
+  static constexpr int WTM = BM / WGM, WTN = BN / WGN;
+  static constexpr int FM = WTM / 8, FN = WTN / 8;
+  static constexpr int ELA = (BM * GBK + NT - 1) / NT, ELB = (BN * GBK + NT - 1) / NT;
+  static constexpr int SMEM = GSTAGES * GBK * (LDA + LDB) * 8 > BM * LDC * 8 ? GSTAGES * GBK * (LDA + LDB) * 8
+                                                                               : BM * LDC * 8;
+  static_assert(FM >= 1 && FN >= 1, "warp tile below 8x8");
+};
+
+template <int BM, int BN, int WGM, int WGN>
+__global__ void __launch_bounds__(32 * WGM * WGN) k_gemm(const GemmParams p) {
+  using Cfg = GemmCfg<BM, BN, WGM, WGN>;
+  constexpr int NT = Cfg::NT, LDA = Cfg::LDA, LDB = Cfg::LDB, LDC = Cfg::LDC;
+  constexpr int FM = Cfg::FM, FN = Cfg::FN, ELA = Cfg::ELA, ELB = Cfg::ELB;
   extern __shared__ __align__(16) double gsm[];
   double* As = gsm;
-  double* Bs = gsm + GSTAGES * GBK * GLDA;
+  double* Bs = gsm + GSTAGES * GBK * LDA;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;
+  const int wm = warp / WGN, wn = warp % WGN;
 
   // tile coordinates with a grouped walk over m for L2 reuse of B
   const int64_t t = blockIdx.x;
@@ -248,17 +268,31 @@ __global__ void __launch_bounds__(GTHREADS) k_gemm(const GemmParams p) {
   const int64_t grp = t / (gsz * ntn), in = t % (gsz * ntn);
   const int64_t tm = grp * gsz + (in & (gsz - 1));
   const int64_t tn = in >> g;
+  const int split = blockIdx.y;
+  const int64_t kt0 = split * p.k_per_split;
+  const int64_t kt1 = min(p.k_tiles, kt0 + p.k_per_split);
+  const int64_t nkt = kt1 > kt0 ? kt1 - kt0 : 0;
 
-  constexpr int EL = GBM * GBK / GTHREADS;  // 8 elements of A (and B) per thread per stage
-  int64_t aoff[EL], boff[EL];
-  int asx[EL], bsx[EL];
+  int64_t aoff[ELA], boff[ELB];
+  int asx[ELA], bsx[ELB];
+  unsigned areal = 0, breal = 0;
 #pragma unroll
-  for (int i = 0; i < EL; ++i) {
-    int r, k;
-    tile_elem(p.ta, tid + i * GTHREADS, aoff[i], r, k);
-    asx[i] = k * GLDA + r;
-    tile_elem(p.tb, tid + i * GTHREADS, boff[i], r, k);
-    bsx[i] = k * GLDB + r;
+  for (int i = 0; i < ELA; ++i) {
+    int r, k, e = tid + i * NT;
+    bool ok = e < BM * GBK && tile_elem(p.ta, e, aoff[i], r, k);
+    asx[i] = k * LDA + r;
+    if (ok) areal |= 1u << i;
+    if (e < BM * GBK && !ok)
+      for (int s = 0; s < GSTAGES; ++s) As[s * GBK * LDA + asx[i]] = 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < ELB; ++i) {
+    int r, k, e = tid + i * NT;
+    bool ok = e < BN * GBK && tile_elem(p.tb, e, boff[i], r, k);
+    bsx[i] = k * LDB + r;
+    if (ok) breal |= 1u << i;
+    if (e < BN * GBK && !ok)
+      for (int s = 0; s < GSTAGES; ++s) Bs[s * GBK * LDB + bsx[i]] = 0.0;
   }
   const double* Ab = p.A + deposit(tm, p.a_m);
   const double* Bb = p.B + deposit(tn, p.b_n);
@@ -266,68 +300,102 @@ __global__ void __launch_bounds__(GTHREADS) k_gemm(const GemmParams p) {
   auto load_stage = [&](int stage, int64_t kt) {
     const double* Ag = Ab + deposit(kt, p.a_k);
     const double* Bg = Bb + deposit(kt, p.b_k);
-    double* as = As + stage * GBK * GLDA;
-    double* bs = Bs + stage * GBK * GLDB;
+    double* as = As + stage * GBK * LDA;
+    double* bs = Bs + stage * GBK * LDB;
 #pragma unroll
-    for (int i = 0; i < EL; ++i) cp_async8(as + asx[i], Ag + aoff[i]);
+    for (int i = 0; i < ELA; ++i)
+      if (areal >> i & 1) cp_async8(as + asx[i], Ag + aoff[i]);
 #pragma unroll
-    for (int i = 0; i < EL; ++i) cp_async8(bs + bsx[i], Bg + boff[i]);
+    for (int i = 0; i < ELB; ++i)
+      if (breal >> i & 1) cp_async8(bs + bsx[i], Bg + boff[i]);
   };
 
-  double acc[4][4][2];
+  double acc[FM][FN][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
   for (int s = 0; s < GSTAGES - 1; ++s) {
-    if (s < p.k_tiles) load_stage(s, s);
+    if (s < nkt) load_stage(s, kt0 + s);
     cp_async_commit();
   }
-  for (int64_t kt = 0; kt < p.k_tiles; ++kt) {
+  for (int64_t it = 0; it < nkt; ++it) {
     cp_async_wait<GSTAGES - 2>();
     __syncthreads();
     {
-      int64_t nk = kt + GSTAGES - 1;
-      if (nk < p.k_tiles) load_stage((int)(nk % GSTAGES), nk);
+      int64_t nk = it + GSTAGES - 1;
+      if (nk < nkt) load_stage((int)(nk % GSTAGES), kt0 + nk);
       cp_async_commit();
     }
-    const double* as = As + (kt % GSTAGES) * GBK * GLDA;
-    const double* bs = Bs + (kt % GSTAGES) * GBK * GLDB;
+    const double* as = As + (it % GSTAGES) * GBK * LDA;
+    const double* bs = Bs + (it % GSTAGES) * GBK * LDB;
 #pragma unroll
     for (int kk = 0; kk < GBK / 4; ++kk) {
-      double af[4], bf[4];
+      double af[FM], bf[FN];
       const int kr = kk * 4 + (lane & 3);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = as[kr * GLDA + wm * 32 + i * 8 + (lane >> 2)];
+      for (int i = 0; i < FM; ++i) af[i] = as[kr * LDA + wm * Cfg::WTM + i * 8 + (lane >> 2)];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = bs[kr * GLDB + wn * 32 + j * 8 + (lane >> 2)];
+      for (int j = 0; j < FN; ++j) bf[j] = bs[kr * LDB + wn * Cfg::WTN + j * 8 + (lane >> 2)];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
   }
   cp_async_wait<0>();
   __syncthreads();
   double* Cs = gsm;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int row = wm * 32 + i * 8 + (lane >> 2);
-      const int col = wn * 32 + j * 8 + (lane & 3) * 2;
-      Cs[row * GLDC + col] = acc[i][j][0];
-      Cs[row * GLDC + col + 1] = acc[i][j][1];
+    for (int j = 0; j < FN; ++j) {
+      const int row = wm * Cfg::WTM + i * 8 + (lane >> 2);
+      const int col = wn * Cfg::WTN + j * 8 + (lane & 3) * 2;
+      Cs[row * LDC + col] = acc[i][j][0];
+      Cs[row * LDC + col + 1] = acc[i][j][1];
     }
   __syncthreads();
+  if (p.splits > 1) {
+    // partial tile, C-tile element order, contiguous per (split, tile)
+    double* W = p.ws + ((int64_t)split * gridDim.x + t) * (BM * BN);
+    for (int e = tid; e < BM * BN; e += NT) {
+      int64_t off;
+      int r, k;
+      tile_elem(p.tc, e, off, r, k);
+      W[e] = Cs[r * LDC + k];
+    }
+    return;
+  }
   double* Cg = p.C + deposit(tm, p.c_m) + deposit(tn, p.c_n);
-  for (int e = tid; e < GBM * GBN; e += GTHREADS) {
+  for (int e = tid; e < BM * BN; e += NT) {
     int64_t off;
     int r, k;
-    tile_elem(p.tc, e, off, r, k);
-    Cg[off] = Cs[r * GLDC + k];
+    if (tile_elem(p.tc, e, off, r, k)) Cg[off] = Cs[r * LDC + k];
+  }
+}
+
+// fixed-order split-K reduction: C = ((W0 + W1) + W2) + ...
+__global__ void k_splitk_reduce(const GemmParams p, int64_t tiles, int tile_elems) {
+  const int64_t total = tiles * tile_elems;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = id / tile_elems;
+    const int e = (int)(id % tile_elems);
+    int64_t off;
+    int r, k;
+    if (!tile_elem(p.tc, e, off, r, k)) continue;
+    double acc = p.ws[t * tile_elems + e];
+    for (int s = 1; s < p.splits; ++s) acc = acc + p.ws[((int64_t)s * tiles + t) * tile_elems + e];
+    const int g = p.grid_swizzle_log;
+    const int64_t gsz = (int64_t)1 << g;
+    const int64_t ntn = (int64_t)1 << p.n_hi;
+    const int64_t grp = t / (gsz * ntn), in = t % (gsz * ntn);
+    const int64_t tm = grp * gsz + (in & (gsz - 1));
+    const int64_t tn = in >> g;
+    p.C[deposit(tm, p.c_m) + deposit(tn, p.c_n) + off] = acc;
   }
 }
 

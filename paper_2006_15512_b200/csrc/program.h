@@ -55,16 +55,23 @@ struct StreamParams {
 constexpr int kGemmBits = 16;
 struct TileMap {
   int32_t nbits;
-  int8_t pos[kGemmBits];   // address bit of tile-element bit j (ascending)
+  int8_t pos[kGemmBits];   // address bit of tile-element bit j (real bits ascending; -1 = virtual)
   int8_t kind[kGemmBits];  // 0: row-type bit (m or n), 1: k bit (for C: 0=m, 1=n)
   int8_t sub[kGemmBits];   // bit index inside the tile coordinate
 };
+// Shapes smaller than the tile use "virtual" tile bits (pos = -1): those
+// elements are zero in smem and never stored, so one kernel family covers
+// every m, n, k >= 0.  Split-K (splits > 1) writes per-split partial tiles to
+// `ws` (in C-tile element order); k_splitk_reduce sums them in split order.
 struct GemmParams {
   const double* A;
   const double* B;
   double* C;
+  double* ws;
   int32_t m_hi, n_hi;  // grid bits
   int64_t k_tiles;
+  int64_t k_per_split;
+  int32_t splits;
   BitRuns a_m, a_k, b_n, b_k, c_m, c_n;  // hi-part deposits
   TileMap ta, tb, tc;
   int32_t grid_swizzle_log;  // group of 2^g m-tiles walked together (L2 reuse)

@@ -97,6 +97,40 @@ StreamFn stream_fn(int ns, int nf) {
   throw Error{TC_BAD_ARG, "no stream kernel for this shape"};
 }
 
+struct GemmVariant {
+  void* fn;
+  int threads;
+  int smem;
+};
+template <int BM, int BN, int WGM, int WGN>
+GemmVariant gv() {
+  using Cfg = GemmCfg<BM, BN, WGM, WGN>;
+  return GemmVariant{(void*)k_gemm<BM, BN, WGM, WGN>, Cfg::NT, Cfg::SMEM};
+}
+// tile bits (bm, bn) in [3, 6] -> kernel instantiation (warp grid chosen so
+// every warp owns >= 8x8)
+GemmVariant gemm_variant(int bm, int bn) {
+  switch (bm * 8 + bn) {
+    case 6 * 8 + 6: return gv<64, 64, 2, 2>();
+    case 6 * 8 + 5: return gv<64, 32, 2, 2>();
+    case 5 * 8 + 6: return gv<32, 64, 2, 2>();
+    case 5 * 8 + 5: return gv<32, 32, 2, 2>();
+    case 6 * 8 + 4: return gv<64, 16, 4, 1>();
+    case 4 * 8 + 6: return gv<16, 64, 1, 4>();
+    case 6 * 8 + 3: return gv<64, 8, 4, 1>();
+    case 3 * 8 + 6: return gv<8, 64, 1, 4>();
+    case 5 * 8 + 4: return gv<32, 16, 2, 2>();
+    case 4 * 8 + 5: return gv<16, 32, 2, 2>();
+    case 5 * 8 + 3: return gv<32, 8, 4, 1>();
+    case 3 * 8 + 5: return gv<8, 32, 1, 4>();
+    case 4 * 8 + 4: return gv<16, 16, 2, 2>();
+    case 4 * 8 + 3: return gv<16, 8, 2, 1>();
+    case 3 * 8 + 4: return gv<8, 16, 1, 2>();
+    case 3 * 8 + 3: return gv<8, 8, 1, 1>();
+  }
+  throw Error{TC_BAD_ARG, "no GEMM variant for this tile"};
+}
+
 int sm_count(int dev) {
   int n = 0;
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -111,7 +145,37 @@ unsigned grid_for(int64_t work, int per_block, int dev, int max_per_sm = 8) {
 
 }  // namespace
 
+struct Launch {
+  void* func = nullptr;
+  dim3 grid, block;
+  unsigned smem = 0;
+  int kind = 0, slot = -1;
+  double bytes = 0, flops = 0;
+  std::vector<char> blob;
+  std::vector<size_t> off;
+  std::vector<void*> ptrs;
+  template <class T>
+  void arg(const T& v) {
+    size_t o = (blob.size() + 15) / 16 * 16;
+    blob.resize(o + sizeof(T));
+    std::memcpy(blob.data() + o, &v, sizeof(T));
+    off.push_back(o);
+  }
+  cudaKernelNodeParams params() {
+    ptrs.resize(off.size());
+    for (size_t i = 0; i < off.size(); ++i) ptrs[i] = blob.data() + off[i];
+    cudaKernelNodeParams kp{};
+    kp.func = func;
+    kp.gridDim = grid;
+    kp.blockDim = block;
+    kp.sharedMemBytes = smem;
+    kp.kernelParams = ptrs.data();
+    return kp;
+  }
+};
+
 struct tc_exec {
+  std::vector<Launch> launches;
   int device = 0;
   cudaStream_t stream = nullptr;
   Program prog;
@@ -134,9 +198,6 @@ struct tc_exec {
   int64_t kernels_per_slice = 0;
   int64_t last_n = 0;
   double compile_ms = 0;
-  // parameter storage (kernel node params point here while adding)
-  std::vector<SelectParams> selp;
-  std::vector<RootCopyParams> rcp;
 
   ~tc_exec() {
     if (device >= 0) cudaSetDevice(device);
@@ -203,105 +264,127 @@ struct tc_exec {
 
     const int tiny_smem = (int)(g.tiny_smem_doubles + kTinyThreads) * 8;
     CU(cudaFuncSetAttribute(k_tiny, cudaFuncAttributeMaxDynamicSharedMemorySize, tiny_smem));
-    CU(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes));
+    for (int bm = 3; bm <= 6; ++bm)
+      for (int bn = 3; bn <= 6; ++bn) {
+        GemmVariant v = gemm_variant(bm, bn);
+        CU(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
+      }
 
-    // ---- graph: one kernel node per step, edges = data + WAR deps ----
-    CU(cudaGraphCreate(&graph, 0));
-    std::vector<cudaGraphNode_t> nodes(g.steps.size());
-    selp.reserve(1);
-    rcp.reserve(1);
-    kernels_per_slice = 0;
+    // ---- launch records (one per step), then the graph from them ----
+    launches.clear();
+    launches.reserve(g.steps.size());
     for (size_t si = 0; si < g.steps.size(); ++si) {
       Step& st = g.steps[si];
-      std::vector<cudaGraphNode_t> deps;
-      for (int d : st.deps) deps.push_back(nodes[d]);
-      cudaKernelNodeParams kp{};
-      kp.blockDim = dim3(256);
-      kp.sharedMemBytes = 0;
-      void* args[4];
-      kp.kernelParams = args;
-      StreamParams sp;
-      GemmParams gp;
-      GenericParams np;
-      SelectParams slp;
-      RootCopyParams rp;
-      const TinyNode* a_nodes = tnodes;
-      const TinyDigit* a_digs = tdigs;
-      const TinyGroup* a_groups = nullptr;
-      int32_t smd = g.tiny_smem_doubles;
-      int64_t* eta_arg = eta;
+      Launch L;
+      L.kind = st.kind;
+      L.slot = st.slot;
+      L.bytes = st.alg_bytes;
+      L.flops = st.alg_flops;
+      L.block = dim3(256);
       switch (st.kind) {
-        case ST_SELECT:
-          slp = SelectParams{leafbuf, slicedbuf, sel, selt, (int64_t)g.sel_ent.size(), eta};
-          kp.func = (void*)k_select;
-          kp.gridDim = dim3(grid_for(slp.n, 256, device));
-          args[0] = &slp;
+        case ST_SELECT: {
+          SelectParams slp{leafbuf, slicedbuf, sel, selt, (int64_t)g.sel_ent.size(), eta};
+          L.func = (void*)k_select;
+          L.grid = dim3(grid_for(slp.n, 256, device));
+          L.arg(slp);
           break;
-        case ST_TINY:
-          a_groups = tgroups + st.gdig_off;
-          kp.func = (void*)k_tiny;
-          kp.gridDim = dim3((unsigned)st.work);
-          kp.blockDim = dim3(kTinyThreads);
-          kp.sharedMemBytes = tiny_smem;
-          args[0] = &a_nodes;
-          args[1] = &a_digs;
-          args[2] = &a_groups;
-          args[3] = &smd;
+        }
+        case ST_TINY: {
+          L.func = (void*)k_tiny;
+          L.grid = dim3((unsigned)st.work);
+          L.block = dim3(kTinyThreads);
+          L.smem = tiny_smem;
+          L.arg((const TinyNode*)tnodes);
+          L.arg((const TinyDigit*)tdigs);
+          L.arg((const TinyGroup*)(tgroups + st.gdig_off));
+          L.arg((int32_t)g.tiny_smem_doubles);
           break;
-        case ST_STREAM:
-          sp = st.sp;
+        }
+        case ST_STREAM: {
+          StreamParams sp = st.sp;
           sp.A = ptr(st.la);
           sp.P = ptr(st.lb);
           sp.C = (double*)ptr(st.lc);
-          kp.func = (void*)stream_fn(st.ns, st.nf);
-          kp.blockDim = dim3(kStreamThreads);
-          kp.gridDim = dim3(grid_for(sp.nx, kStreamThreads * kStreamUnroll, device));
-          args[0] = &sp;
+          L.func = (void*)stream_fn(st.ns, st.nf);
+          L.block = dim3(kStreamThreads);
+          L.grid = dim3(grid_for(sp.nx, kStreamThreads * kStreamUnroll, device));
+          L.arg(sp);
           break;
-        case ST_GEMM:
-          gp = st.gp;
+        }
+        case ST_GEMM: {
+          GemmParams gp = st.gp;
           gp.A = ptr(st.la);
           gp.B = ptr(st.lb);
           gp.C = (double*)ptr(st.lc);
-          kp.func = (void*)k_gemm;
-          kp.blockDim = dim3(GTHREADS);
-          kp.gridDim = dim3((unsigned)st.work);
-          kp.sharedMemBytes = kGemmSmemBytes;
-          args[0] = &gp;
+          gp.ws = (double*)ptr(st.lws);
+          GemmVariant v = gemm_variant(st.bm, st.bn);
+          L.func = v.fn;
+          L.block = dim3(v.threads);
+          L.grid = dim3((unsigned)st.work, (unsigned)gp.splits);
+          L.smem = v.smem;
+          L.arg(gp);
           break;
-        case ST_GENERIC:
-          np = st.np;
+        }
+        case ST_GEMM_REDUCE: {
+          GemmParams gp = st.gp;
+          gp.A = ptr(st.la);
+          gp.B = ptr(st.lb);
+          gp.C = (double*)ptr(st.lc);
+          gp.ws = (double*)ptr(st.lws);
+          const int te = 1 << (st.bm + st.bn);
+          L.func = (void*)k_splitk_reduce;
+          L.grid = dim3(grid_for(st.work * te, 256, device));
+          L.arg(gp);
+          L.arg((int64_t)st.work);
+          L.arg(te);
+          break;
+        }
+        case ST_GENERIC: {
+          GenericParams np = st.np;
           np.A = ptr(st.la);
           np.B = ptr(st.lb);
           np.C = (double*)ptr(st.lc);
           np.dig = gdig + st.gdig_off;
-          kp.func = (void*)k_generic;
-          kp.gridDim = dim3(grid_for(np.c_size, 256, device));
-          args[0] = &np;
+          L.func = (void*)k_generic;
+          L.grid = dim3(grid_for(np.c_size, 256, device));
+          L.arg(np);
           break;
-        case ST_ROOTCOPY:
-          rp = RootCopyParams{ptr(g.root_loc), nullptr, g.R, eta};
-          rcp.push_back(rp);
-          kp.func = (void*)k_rootcopy;
-          kp.gridDim = dim3(grid_for(g.R, 256, device));
-          args[0] = &rcp.back();  // results pointer patched per run (node params update)
+        }
+        case ST_ROOTCOPY: {
+          RootCopyParams rp{ptr(g.root_loc), nullptr, g.R, eta};
+          L.func = (void*)k_rootcopy;
+          L.grid = dim3(grid_for(g.R, 256, device));
+          L.arg(rp);
+          rootcopy_launch = (int)si;
           break;
-        case ST_ETA:
-          kp.func = (void*)k_eta;
-          kp.gridDim = dim3(1);
-          kp.blockDim = dim3(1);
-          args[0] = &eta_arg;
+        }
+        case ST_ETA: {
+          L.func = (void*)k_eta;
+          L.grid = dim3(1);
+          L.block = dim3(1);
+          L.arg(eta);
           break;
+        }
       }
+      launches.push_back(std::move(L));
+    }
+    CU(cudaGraphCreate(&graph, 0));
+    std::vector<cudaGraphNode_t> nodes(g.steps.size());
+    kernels_per_slice = 0;
+    for (size_t si = 0; si < g.steps.size(); ++si) {
+      std::vector<cudaGraphNode_t> deps;
+      for (int d : g.steps[si].deps) deps.push_back(nodes[d]);
+      cudaKernelNodeParams kp = launches[si].params();
       CU(cudaGraphAddKernelNode(&nodes[si], graph, deps.data(), deps.size(), &kp));
       ++kernels_per_slice;
-      if (st.kind == ST_ROOTCOPY) rootcopy_node = nodes[si];
     }
+    rootcopy_node = nodes[rootcopy_launch];
     CU(cudaGraphInstantiate(&gexec, graph, 0));
     compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
 
   cudaGraphNode_t rootcopy_node = nullptr;
+  int rootcopy_launch = -1;
 
   void ensure_results(int64_t n) {
     if (n <= results_cap) return;
@@ -311,19 +394,40 @@ struct tc_exec {
     results = dalloc<double>((size_t)(n * prog.R), dummy);
     results_cap = n;
     // patch the root-copy node with the new results pointer
-    RootCopyParams rp = rcp.back();
+    Launch& L = launches[rootcopy_launch];
+    RootCopyParams rp;
+    std::memcpy(&rp, L.blob.data(), sizeof(rp));
     rp.results = results;
-    rcp.back() = rp;
-    cudaKernelNodeParams kp{};
-    void* args[1] = {&rcp.back()};
-    kp.func = (void*)k_rootcopy;
-    kp.gridDim = dim3(grid_for(prog.R, 256, device));
-    kp.blockDim = dim3(256);
-    kp.kernelParams = args;
+    std::memcpy(L.blob.data(), &rp, sizeof(rp));
+    cudaKernelNodeParams kp = L.params();
     CU(cudaGraphExecKernelNodeSetParams(gexec, rootcopy_node, &kp));
   }
 
-  double run(int64_t b, int64_t e) {
+  // Eager replay of one slice, one kernel at a time, timed per launch with
+  // CUDA events (diagnostics: per-node-class time shares).
+  void profile(int64_t slice, std::vector<float>& ms) {
+    CU(cudaSetDevice(device));
+    ensure_results(1);
+    int64_t h[2] = {slice, slice};
+    CU(cudaMemcpyAsync(eta, h, sizeof(h), cudaMemcpyHostToDevice, stream));
+    std::vector<cudaEvent_t> ev(launches.size() + 1);
+    for (auto& e : ev) CU(cudaEventCreate(&e));
+    CU(cudaEventRecord(ev[0], stream));
+    for (size_t i = 0; i < launches.size(); ++i) {
+      Launch& L = launches[i];
+      auto kp = L.params();
+      CU(cudaLaunchKernel(L.func, L.grid, L.block, kp.kernelParams, L.smem, stream));
+      CU(cudaEventRecord(ev[i + 1], stream));
+    }
+    CU(cudaEventSynchronize(ev.back()));
+    CU(cudaGetLastError());
+    ms.resize(launches.size());
+    for (size_t i = 0; i < launches.size(); ++i) CU(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
+    for (auto& e : ev) cudaEventDestroy(e);
+    last_n = 1;
+  }
+
+  double run(int64_t b, int64_t e, int64_t repeats = 1) {
     CU(cudaSetDevice(device));
     int64_t n = e - b;
     if (n <= 0) {
@@ -332,12 +436,16 @@ struct tc_exec {
     }
     ensure_results(n);
     int64_t h[2] = {b, b};
-    CU(cudaMemcpyAsync(eta, h, sizeof(h), cudaMemcpyHostToDevice, stream));
     cudaEvent_t e0, e1;
     CU(cudaEventCreate(&e0));
     CU(cudaEventCreate(&e1));
+    CU(cudaMemcpyAsync(eta, h, sizeof(h), cudaMemcpyHostToDevice, stream));
+    CU(cudaStreamSynchronize(stream));
     CU(cudaEventRecord(e0, stream));
-    for (int64_t s = 0; s < n; ++s) CU(cudaGraphLaunch(gexec, stream));
+    for (int64_t r = 0; r < repeats; ++r) {
+      if (r > 0) k_eta_reset<<<1, 1, 0, stream>>>(eta);
+      for (int64_t s = 0; s < n; ++s) CU(cudaGraphLaunch(gexec, stream));
+    }
     CU(cudaEventRecord(e1, stream));
     CU(cudaEventSynchronize(e1));
     CU(cudaGetLastError());
@@ -521,11 +629,54 @@ static void fill_stats(const tc_exec& ex, double ms, tc_stats* s) {
 }
 
 int tc_exec_run(tc_exec* ex, int64_t slice_begin, int64_t slice_end, tc_stats* stats) {
+  return tc_exec_run_repeat(ex, slice_begin, slice_end, 1, stats);
+}
+
+int tc_exec_run_repeat(tc_exec* ex, int64_t slice_begin, int64_t slice_end, int64_t repeats, tc_stats* stats) {
   return guard([&] {
-    if (slice_begin < 0 || slice_end > ex->prog.num_slices || slice_begin > slice_end)
+    if (slice_begin < 0 || slice_end > ex->prog.num_slices || slice_begin > slice_end || repeats < 1)
       throw Error{TC_BAD_ARG, "slice range out of bounds"};
-    double ms = ex->run(slice_begin, slice_end);
+    double ms = ex->run(slice_begin, slice_end, repeats);
     fill_stats(*ex, ms, stats);
+    if (stats) stats->gpu_launches = (ex->kernels_per_slice * ex->last_n + 1) * repeats - 1;
+  });
+}
+
+int tc_exec_copy_results(tc_exec* ex, double* dst_device) {
+  return guard([&] {
+    CU(cudaSetDevice(ex->device));
+    if (ex->last_n > 0)
+      CU(cudaMemcpyAsync(dst_device, ex->results, ex->last_n * ex->prog.R * 8, cudaMemcpyDeviceToDevice,
+                         ex->stream));
+    CU(cudaStreamSynchronize(ex->stream));
+  });
+}
+
+int tc_fold_device(const double* per_slice_device, int64_t R, int64_t n, double* out_device, int32_t device) {
+  return guard([&] {
+    if (R < 1 || n < 1) throw Error{TC_BAD_ARG, "empty fold"};
+    CU(cudaSetDevice(device));
+    k_fold<<<grid_for(R, 256, device), 256>>>(per_slice_device, R, n, out_device);
+    CU(cudaGetLastError());
+    CU(cudaDeviceSynchronize());
+  });
+}
+
+int tc_exec_profile(tc_exec* ex, int64_t slice, float* step_ms, int32_t* step_kind, int32_t* step_slot,
+                    double* step_bytes, double* step_flops, int32_t cap, int32_t* n) {
+  return guard([&] {
+    if (slice < 0 || slice >= ex->prog.num_slices) throw Error{TC_BAD_ARG, "slice out of range"};
+    std::vector<float> ms;
+    ex->profile(slice, ms);
+    int k = (int)std::min<size_t>(ms.size(), (size_t)std::max(0, cap));
+    for (int i = 0; i < k; ++i) {
+      if (step_ms) step_ms[i] = ms[i];
+      if (step_kind) step_kind[i] = ex->launches[i].kind;
+      if (step_slot) step_slot[i] = ex->launches[i].slot;
+      if (step_bytes) step_bytes[i] = ex->launches[i].bytes;
+      if (step_flops) step_flops[i] = ex->launches[i].flops;
+    }
+    *n = (int32_t)ms.size();
   });
 }
 

@@ -47,5 +47,27 @@ def main(names):
         json.dump(data, open(OUT, "w"), indent=1, sort_keys=True)
 
 
+
+
+def greedy(name, picks):
+    """Reference greedy prefix (slicing.py:70-79) on a frozen plan."""
+    from tensorcount.slicing import choose_slice_index
+    data = json.load(open(OUT)) if os.path.exists(OUT) else {}
+    flat, meta = planfile.load(os.path.join(ROOT, "data", "plans", f"{name}.tcplan.npz"), index_cls=Index)
+    n, t = planfile.to_objects(flat, Tensor, TensorNetwork, ContractionTree)
+    pos = {ix: k for k, ix in enumerate(flat.indices)}
+    chosen = []
+    t0 = time.time()
+    for _ in range(picks):
+        chosen.append(choose_slice_index(n, t, already=frozenset(chosen)))
+    data[f"{name}_greedy{picks}"] = dict(ids=[pos[i] for i in chosen], id_reprs=[repr(i.id) for i in chosen],
+                                         ref_seconds=time.time() - t0)
+    print(data[f"{name}_greedy{picks}"], flush=True)
+    json.dump(data, open(OUT, "w"), indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
-    main(sys.argv[1:])
+    if sys.argv[1:2] == ["greedy"]:
+        greedy(sys.argv[2], int(sys.argv[3]))
+    else:
+        main(sys.argv[1:])

@@ -1,0 +1,186 @@
+"""CPU tests of the host side: the C-ABI library loads and exports every symbol
+include/tc.h declares; libtc's exact memory model / greedy chooser / plan
+validation agree with the golden fixtures and the oracle; the plan
+interchange format and generators are stable.  No kernel is launched."""
+
+import ctypes
+import json
+import os
+import random
+import re
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, PLANS, ROOT, case_flat, load_cases
+from oracle import oracle
+from paper_2006_15512_b200 import _lib, planfile
+from paper_2006_15512_b200.errors import BudgetInfeasible, IndexOveruse, NoCandidates, PlanMismatch
+from paper_2006_15512_b200.flatten import flatten
+
+CASES = load_cases()
+
+
+def test_library_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "tc.h")).read()
+    declared = set(re.findall(r"\b(tc_[a-z0-9_]+)\s*\(", hdr))
+    assert declared, "no declarations parsed"
+    so = ctypes.CDLL(_lib.LIB_PATH)
+    for name in sorted(declared):
+        assert hasattr(so, name), f"libtc.so does not export {name}"
+    # and the Python binding covers all of them
+    assert declared == set(_lib.SIGNATURES)
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c["family"] == "random_network"],
+                         ids=[c["name"] for c in CASES if c["family"] == "random_network"])
+def test_mem_cost_and_choose_match_reference(case):
+    flat = case_flat(case)
+    h = _lib.PlanHandle(flat)
+    for k, v in case["expected"]["mem_cost"].items():
+        assert h.mem_cost([int(k)] if k else []) == int(v)
+    if "choose" in case["expected"]:
+        assert h.choose_slice_index([]) == case["expected"]["choose"]
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if "budgeted" in c["expected"]],
+                         ids=[c["name"] for c in CASES if "budgeted" in c["expected"]])
+def test_greedy_slice_set_matches_reference(case):
+    flat = case_flat(case)
+    h = _lib.PlanHandle(flat)
+    exp = case["expected"]["budgeted"]
+    chosen = np.zeros(max(1, len(flat.domain)), np.int32)
+    n = ctypes.c_int32()
+    need = _lib.U128()
+    st = _lib.lib().tc_choose_slices(h.h, exp["budget"], chosen.ctypes.data_as(_lib.I32P), len(chosen),
+                                     ctypes.byref(n), ctypes.byref(need))
+    if "error" in exp:
+        assert st == 3
+        msg = _lib.lib().tc_last_error().decode()
+        assert msg == exp["message"]  # reference wording, slicing.py:124-128
+        return
+    assert st == 0
+    assert chosen[: n.value].tolist() == exp["chosen"]
+    assert h.mem_cost(exp["chosen"]) == int(exp["mem_estimate"])
+
+
+def test_infeasible_message_and_status():
+    c = next(c for c in CASES if c["family"] == "random_network")
+    flat = case_flat(c)
+    h = _lib.PlanHandle(flat)
+    inf = c["expected"]["infeasible"]
+    chosen = np.zeros(len(flat.domain) + 1, np.int32)
+    n = ctypes.c_int32()
+    st = _lib.lib().tc_choose_slices(h.h, 1, chosen.ctypes.data_as(_lib.I32P), len(chosen), ctypes.byref(n), None)
+    assert st == 3 and _lib.lib().tc_last_error().decode() == inf["message"]
+    with pytest.raises(BudgetInfeasible):
+        _lib.check(st)
+
+
+def test_choose_no_candidates():
+    from paper_2006_15512_b200 import Index, Tensor, TensorNetwork, left_deep_tree
+    i = Index("i", 2)
+    n = TensorNetwork((Tensor((i,), np.ones(2)),))
+    h = _lib.PlanHandle(flatten(n, left_deep_tree(n.tensors)))
+    with pytest.raises(NoCandidates):
+        h.choose_slice_index([])
+
+
+def test_plan_validation_errors():
+    from paper_2006_15512_b200 import ContractionTree, Index, Tensor, TensorNetwork, join, leaf
+    from paper_2006_15512_b200 import slicing
+    i, j = Index("i", 2), Index("j", 2)
+    a, b = Tensor((i, j), np.ones((2, 2))), Tensor((j,), np.ones(2))
+    n = TensorNetwork((a, b))
+    stranger = Tensor((i,), np.ones(2))
+    with pytest.raises(PlanMismatch):
+        slicing.mem_cost(n, join(leaf(a), leaf(stranger)))
+    # an index used three times is rejected by the library as well
+    flat = flatten(n, join(leaf(a), leaf(b)))
+    flat.leaf_idx = np.array([0, 0, 1], np.int32)  # i twice in one leaf
+    with pytest.raises(ValueError):
+        _lib.PlanHandle(flat)
+    c = Tensor((j,), np.ones(2))
+    n3 = TensorNetwork((a, b))
+    flat3 = flatten(n3, join(join(leaf(a), leaf(b)), leaf(b)))
+    assert flat3.root_slot >= 0
+    # j in three leaves -> IndexOveruse (network.py:42-43)
+    flat3 = flatten(TensorNetwork((a, b, Tensor((i,), np.ones(2)))),
+                    join(leaf(a), leaf(b)))
+    flat3.leaf_idx = np.array([0, 1, 1, 1], np.int32)
+    with pytest.raises(IndexOveruse):
+        _lib.PlanHandle(flat3)
+    del c
+
+
+def test_result_indices_reference_order():
+    for c in CASES:
+        flat = case_flat(c)
+        h = _lib.PlanHandle(flat)
+        assert h.result_indices([]) == c["expected"]["unsliced"]["indices"], c["name"]
+
+
+def test_random_mem_cost_vs_oracle():
+    rng = random.Random(3)
+    for c in [c for c in CASES if c["family"] in ("random_network", "cnf")]:
+        flat = case_flat(c)
+        h = _lib.PlanHandle(flat)
+        occ = np.bincount(flat.leaf_idx, minlength=len(flat.domain))
+        bonds = np.nonzero(occ == 2)[0].tolist()
+        for _ in range(4):
+            drop = rng.sample(bonds, rng.randint(0, len(bonds))) if bonds else []
+            assert h.mem_cost(drop) == oracle.mem_cost(flat, drop)
+
+
+@pytest.mark.parametrize("name", ["c1a", "c2", "c1b", "c3", "c4", "c5"])
+def test_frozen_plans_memory_model(name):
+    path = os.path.join(PLANS, f"{name}.tcplan.npz")
+    flat, meta = planfile.load(path)
+    h = _lib.PlanHandle(flat)
+    info = h.info()
+    assert info.mem_cost.value() == int(meta["mem_cost_unsliced"])  # reference mem_cost at planning time
+    assert info.max_rank == meta["max_rank"]
+    assert info.contraction_ops.value() == meta["contraction_ops"]
+
+
+def test_greedy_prefix_matches_reference_on_c1a():
+    counts = json.load(open(os.path.join(GOLDEN, "counts.json")))
+    key = next((k for k in counts if k.startswith("c1a_greedy")), None)
+    if key is None:
+        pytest.skip("reference greedy prefix not recorded")
+    flat, _ = planfile.load(os.path.join(PLANS, "c1a.tcplan.npz"))
+    h = _lib.PlanHandle(flat)
+    chosen = []
+    for _ in counts[key]["ids"]:
+        chosen.append(h.choose_slice_index(chosen))
+    assert chosen == counts[key]["ids"]
+    assert [repr(flat.indices[i].id) for i in chosen] == counts[key]["id_reprs"]
+
+
+def test_planfile_roundtrip(tmp_path):
+    c = next(c for c in CASES if c["name"] == "cnf_example4")
+    flat = case_flat(c)
+    p = tmp_path / "x.tcplan.npz"
+    planfile.save(str(p), flat, {"k": 1})
+    back, meta = planfile.load(str(p))
+    assert meta == {"k": 1}
+    for f in ("domain", "sort_rank", "leaf_idx_off", "leaf_idx", "leaf_val_off", "leaf_val", "left", "right"):
+        assert np.array_equal(getattr(back, f), getattr(flat, f))
+    assert [ix.id for ix in back.indices] == [ix.id for ix in flat.indices]
+    n, t = planfile.to_objects(back)
+    again = flatten(n, t)
+    assert np.array_equal(again.left, flat.left) and again.root_slot == flat.root_slot
+
+
+def test_generators_deterministic():
+    from paper_2006_15512_b200.generators import banded_3cnf, grid_ising, uniform_3cnf
+    assert uniform_3cnf(30, 3.0, 1) == uniform_3cnf(30, 3.0, 1)
+    assert banded_3cnf(200, 3.5, 29, 1).count("\n") == 1 + 700 + 200
+    g = grid_ising(4, 1)
+    assert g.startswith("p cnf 40 96")
