@@ -209,11 +209,17 @@ def traffic_for(config, kernel):
 
 
 # ---------------------------------------------------------------- reference
-def reference_objects(flat):
+def _reference_path():
     for p in (os.path.join(ROOT, "oracle", "_ref"), os.path.join(ROOT, "baseline", "_ref")):
         if os.path.isdir(os.path.join(p, "tensorcount")):
-            sys.path.insert(0, p)
-            break
+            if p not in sys.path:
+                sys.path.insert(0, p)
+            return p
+    raise ImportError("reference not installed (oracle/_ref or baseline/_ref)")
+
+
+def reference_objects(flat):
+    _reference_path()
     from tensorcount.network import ContractionTree, TensorNetwork
     from tensorcount.tensor import Index, Tensor
 
@@ -228,6 +234,7 @@ def time_reference(flat, chosen, steps, warm=True):
     full run per step.  Sliced: slice 0 through the reference's own slice code
     path (_slice_plan + _execute_tracked, slicing.py:139-145), extrapolated x
     num_slices."""
+    _reference_path()
     from tensorcount import slicing as ref_slicing
     from tensorcount.tensor import Assignment
 

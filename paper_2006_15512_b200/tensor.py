@@ -105,6 +105,7 @@ def contract_pair(a, b, device: int = 0):
     from .network import TensorNetwork, join, leaf
     from .slicing import _run
 
-    n = TensorNetwork((a, b))
+    # fresh wrappers: the operands may be the same object (contract_pair(a, a))
+    n = TensorNetwork((type(a)(a.indices, a.values), type(b)(b.indices, b.values)))
     t = join(leaf(n.tensors[0]), leaf(n.tensors[1]))
     return _run(n, t, mem_budget=None, devices=[device]).result
