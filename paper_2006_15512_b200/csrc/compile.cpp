@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <map>
+#include <cstdlib>
 #include <set>
 
 namespace tc {
@@ -277,6 +278,68 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in) {
         want(a, natural(a));
         want(b, natural(b));
     }
+  }
+
+  // ---- chain segments: runs of STREAM nodes fused into one launch -----------
+  // v_{i+1}'s big operand is v_i.  Inner bits = every index of the input the
+  // segment touches plus the ones it creates; all must fit kChainU at every
+  // step (touching a new input index widens every earlier step too).
+  struct Seg {
+    std::vector<int> nodes, big, small;
+    std::vector<int> u0;     // inner indices loaded with the input tile
+    std::vector<int> inner;  // inner indices of the current output (sorted)
+    std::vector<int> w;      // inner width before step 0 and after each step
+  };
+  std::vector<Seg> segs;
+  std::vector<int> seg_of(S, -1);
+  // smem chain fusion is opt-in (TC_CHAIN=1): measured slower than graph-
+  // concurrent k_stream launches on C2/C1b
+  const bool fuse_chains = std::getenv("TC_CHAIN") != nullptr;
+  // fusion pays where launches dominate (small tensors); big tensors stream at
+  // HBM speed through k_stream with L2 reuse between consecutive steps
+  int chain_max_bits = 20;
+  if (const char* e = std::getenv("TC_CHAIN_MAX_BITS")) chain_max_bits = std::atoi(e);
+  for (int k = 0; k < p.NN && fuse_chains; ++k) {
+    const int v = p.NL + k, a = p.left[k], b = p.right[k];
+    if (g.cls[v] != NC_STREAM) continue;
+    if ((int)std::max(eff[a].size(), eff[b].size()) > chain_max_bits || (int)eff[v].size() > chain_max_bits) continue;
+    const bool b_small = eff[b].size() <= eff[a].size();
+    const int big = b_small ? a : b, sm = b_small ? b : a;
+    std::vector<int> Sh = inter(eff[a], eff[b]);
+    std::vector<int> F = minus(eff[sm], Sh);
+    if (!p.is_leaf(big) && seg_of[big] >= 0) {
+      Seg& sg = segs[seg_of[big]];
+      if (sg.nodes.back() == big && (int)sg.nodes.size() < kChainMax) {
+        std::vector<int> s_orig = minus(Sh, sg.inner);
+        std::vector<int> un;
+        std::set_union(sg.inner.begin(), sg.inner.end(), Sh.begin(), Sh.end(), std::back_inserter(un));
+        std::vector<int> nin = minus(un, Sh);
+        std::vector<int> nin2;
+        std::set_union(nin.begin(), nin.end(), F.begin(), F.end(), std::back_inserter(nin2));
+        int mx = (int)nin2.size();
+        for (int x : sg.w) mx = std::max(mx, x + (int)s_orig.size());
+        if (mx <= kChainU) {
+          for (int& x : sg.w) x += (int)s_orig.size();
+          sg.w.push_back((int)nin2.size());
+          for (int x : s_orig) sg.u0.push_back(x);
+          sg.inner = nin2;
+          sg.nodes.push_back(v);
+          sg.big.push_back(big);
+          sg.small.push_back(sm);
+          seg_of[v] = seg_of[big];
+          continue;
+        }
+      }
+    }
+    Seg sg;
+    sg.nodes = {v};
+    sg.big = {big};
+    sg.small = {sm};
+    sg.u0 = Sh;
+    sg.inner = F;
+    sg.w = {(int)Sh.size(), (int)F.size()};
+    seg_of[v] = (int)segs.size();
+    segs.push_back(sg);
   }
 
   // ---- leaves: plain or per-slice selected ----------------------------------
@@ -598,32 +661,23 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in) {
     }
     return m;
   };
+  std::vector<double> node_bytes(S, 0.0), node_flops(S, 0.0);
   for (int k = 0; k < p.NN; ++k) {
     int v = p.NL + k, a = p.left[k], b = p.right[k];
-    {
-      std::vector<int> uni;
-      std::set_union(eff[a].begin(), eff[a].end(), eff[b].begin(), eff[b].end(), std::back_inserter(uni));
-      g.alg_flops += 2 * (set_bytes(p, uni, drop) / 8);
-      g.alg_bytes += (u128)8 * (u128)(size[a] + size[b] + size[v]);
-    }
-    const double nb_ = 8.0 * (double)(size[a] + size[b] + size[v]);
-    double nf_;
-    {
-      std::vector<int> uni;
-      std::set_union(eff[a].begin(), eff[a].end(), eff[b].begin(), eff[b].end(), std::back_inserter(uni));
-      nf_ = 2.0 * (double)(set_bytes(p, uni, drop) / 8);
-    }
-    if (g.cls[v] == NC_TINY) {
-      int gi = group_of[v];
-      int ts = tiny_step[glevel[gi]];
-      g.steps[ts].alg_bytes += nb_;
-      g.steps[ts].alg_flops += nf_;
-      continue;
-    }
+    std::vector<int> uni;
+    std::set_union(eff[a].begin(), eff[a].end(), eff[b].begin(), eff[b].end(), std::back_inserter(uni));
+    const u128 fl = 2 * (set_bytes(p, uni, drop) / 8);
+    g.alg_flops += fl;
+    g.alg_bytes += (u128)8 * (u128)(size[a] + size[b] + size[v]);
+    node_bytes[v] = 8.0 * (double)(size[a] + size[b] + size[v]);
+    node_flops[v] = (double)fl;
+  }
+  auto emit_node = [&](int v) {
+    const int k = v - p.NL, a = p.left[k], b = p.right[k];
     Step st;
     st.slot = v;
-    st.alg_bytes = nb_;
-    st.alg_flops = nf_;
+    st.alg_bytes = node_bytes[v];
+    st.alg_flops = node_flops[v];
     st.la = g.loc[a];
     st.lb = g.loc[b];
     for (int c : {a, b})
@@ -718,7 +772,10 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in) {
         std::sort(N.begin(), N.end(), [&](int x, int y) { return pc[x] < pc[y]; });
         std::sort(K.begin(), K.end(), [&](int x, int y) { return pa[x] < pa[y]; });
         const int m = (int)M.size(), n = (int)N.size(), kk = (int)K.size();
-        const int MT = std::max(3, std::min(6, m)), NT = std::max(3, std::min(6, n)), KT = 4;
+        // 128x64 CTA tiles (8 warps) for large GEMMs, 64x64 and below otherwise
+        static const int big_tiles = std::getenv("TC_GEMM_BIG") ? std::atoi(std::getenv("TC_GEMM_BIG")) : 1;
+        const bool big = big_tiles && m >= 7 && n >= 6 && kk >= 8;
+        const int MT = big ? 7 : std::max(3, std::min(6, m)), NT = std::max(3, std::min(6, n)), KT = 4;
         GemmParams gp{};
         gp.m_hi = std::max(0, m - MT);
         gp.n_hi = std::max(0, n - NT);
@@ -839,6 +896,163 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in) {
     }
     for (int c : {a, b})
       if (g.loc[c].kind == LOC_ARENA) arena.release(g.loc[c].off, bytes[c], me);
+  };
+
+  // one fused launch for a multi-step chain segment; false if the address
+  // maps do not fit the kernel's run/tile limits (then: one launch per node)
+  auto emit_chain = [&](const Seg& sg) -> bool {
+    const int v1 = sg.nodes.front(), vk = sg.nodes.back();
+    const int A = sg.big.front();
+    const auto& La = g.layout[A];
+    const auto& Lc = g.layout[vk];
+    std::map<int, int> pa, pc;
+    for (size_t q = 0; q < La.size(); ++q) pa[La[q]] = (int)q;
+    for (size_t q = 0; q < Lc.size(); ++q) pc[Lc[q]] = (int)q;
+    // inner bookkeeping
+    std::vector<int> cur = sg.u0;  // inner bit j <-> index
+    std::vector<ChainStep> cs;
+    for (size_t i = 0; i < sg.nodes.size(); ++i) {
+      const int u = sg.nodes[i], sm = sg.small[i], bg = sg.big[i];
+      std::vector<int> Sh = inter(eff[bg], eff[sm]);
+      std::vector<int> F = minus(eff[sm], Sh);
+      const auto& Lq = g.layout[sm];
+      std::map<int, int> pq;
+      for (size_t q = 0; q < Lq.size(); ++q) pq[Lq[q]] = (int)q;
+      std::vector<int> nw;
+      for (int x : cur)
+        if (!has(Sh, x)) nw.push_back(x);
+      const int nkeep = (int)nw.size();
+      for (int x : F) nw.push_back(x);
+      if ((int)nw.size() > kChainU || (int)cur.size() > kChainU) return false;
+      ChainStep c{};
+      c.ns = (int)Sh.size();
+      c.nf = (int)F.size();
+      c.nnew = (int)nw.size();
+      auto cpos = [&](int x) { return (int)(std::find(cur.begin(), cur.end(), x) - cur.begin()); };
+      for (int s = 0; s < (1 << c.ns); ++s) {
+        int sb = 0, oq = 0;
+        for (int t = 0; t < c.ns; ++t)
+          if (s >> t & 1) {
+            sb |= 1 << cpos(Sh[t]);
+            oq += 1 << pq[Sh[t]];
+          }
+        c.stab[s] = (uint8_t)sb;
+        for (int f = 0; f < (1 << c.nf); ++f) {
+          int of = 0;
+          for (int t = 0; t < c.nf; ++t)
+            if (f >> t & 1) of += 1 << pq[F[t]];
+          c.offP[s * (1 << c.nf) + f] = oq + of;
+        }
+      }
+      for (int un = 0; un < (1 << c.nnew); ++un) {
+        int ub = 0, f = 0;
+        for (int j = 0; j < c.nnew; ++j)
+          if (un >> j & 1) {
+            if (j < nkeep) ub |= 1 << cpos(nw[j]);
+            else f |= 1 << (j - nkeep);
+          }
+        c.utab[un] = (uint16_t)(ub | (f << 8));
+      }
+      cs.push_back(c);
+      cur = nw;
+      (void)u;
+    }
+    const std::vector<int>& Uk = cur;
+    std::vector<int> O = minus(eff[A], [&] {
+      std::vector<int> s = sg.u0;
+      std::sort(s.begin(), s.end());
+      return s;
+    }());
+    std::sort(O.begin(), O.end(), [&](int x, int y) { return pa[x] < pa[y]; });
+    int umax = (int)sg.u0.size();
+    for (auto& c : cs) umax = std::max(umax, c.nnew);
+    int lbuf = 0;
+    while ((2 << lbuf) <= kChainBuf) ++lbuf;  // log2(kChainBuf)
+    const int xt = std::min((int)O.size(), lbuf - umax);
+    if (xt < 0) return false;
+    ChainParams cp{};
+    cp.nsteps = (int)cs.size();
+    cp.xt = xt;
+    cp.n_tiles = (int64_t)1 << ((int)O.size() - xt);
+    std::vector<std::pair<int, int>> ra, rc;
+    for (int j = xt; j < (int)O.size(); ++j) {
+      ra.push_back({j - xt, pa[O[j]]});
+      rc.push_back({j - xt, pc[O[j]]});
+    }
+    try {
+      cp.a_hi = make_runs(ra);
+      cp.c_hi = make_runs(rc);
+    } catch (const Error& e) {
+      if (e.status != -1) throw;
+      return false;
+    }
+    auto tmap = [&](std::map<int, int>& P, const std::vector<int>& inner) {
+      std::vector<std::tuple<int, int, int>> bits;
+      for (int j = 0; j < xt; ++j) bits.emplace_back(P[O[j]], 0, j);
+      for (size_t t = 0; t < inner.size(); ++t) bits.emplace_back(P[inner[t]], 1, (int)t);
+      std::sort(bits.begin(), bits.end());
+      TileMap tm{};
+      tm.nbits = (int)bits.size();
+      for (size_t q = 0; q < bits.size(); ++q) {
+        tm.pos[q] = (int8_t)std::get<0>(bits[q]);
+        tm.kind[q] = (int8_t)std::get<1>(bits[q]);
+        tm.sub[q] = (int8_t)std::get<2>(bits[q]);
+      }
+      return tm;
+    };
+    cp.ta = tmap(pa, sg.u0);
+    cp.tc = tmap(pc, Uk);
+    Step st;
+    st.kind = ST_CHAIN;
+    st.slot = vk;
+    st.cp = cp;
+    st.la = g.loc[A];
+    st.chain_off = (int64_t)g.chain_steps.size();
+    for (size_t i = 0; i < cs.size(); ++i) {
+      g.chain_steps.push_back(cs[i]);
+      g.chain_piece.push_back(g.loc[sg.small[i]]);
+    }
+    st.work = cp.n_tiles;
+    for (int u : sg.nodes) {
+      st.alg_bytes += node_bytes[u];
+      st.alg_flops += node_flops[u];
+    }
+    if (producer[A] >= 0) st.deps.push_back(producer[A]);
+    for (int sm : sg.small)
+      if (producer[sm] >= 0) st.deps.push_back(producer[sm]);
+    haz.clear();
+    g.loc[vk] = Loc{LOC_ARENA, arena.alloc(bytes[vk], haz)};
+    for (int h : haz) st.deps.push_back(h);
+    st.lc = g.loc[vk];
+    const int me = (int)g.steps.size();
+    g.steps.push_back(st);
+    producer[vk] = me;
+    if (g.loc[A].kind == LOC_ARENA) arena.release(g.loc[A].off, bytes[A], me);
+    for (int sm : sg.small)
+      if (g.loc[sm].kind == LOC_ARENA) arena.release(g.loc[sm].off, bytes[sm], me);
+    g.n_stream += (int)sg.nodes.size();
+    g.n_chain++;
+    (void)v1;
+    return true;
+  };
+
+  for (int k = 0; k < p.NN; ++k) {
+    const int v = p.NL + k;
+    if (g.cls[v] == NC_TINY) {
+      int gi = group_of[v];
+      int ts = tiny_step[glevel[gi]];
+      g.steps[ts].alg_bytes += node_bytes[v];
+      g.steps[ts].alg_flops += node_flops[v];
+      continue;
+    }
+    if (g.cls[v] == NC_STREAM && seg_of[v] >= 0 && segs[seg_of[v]].nodes.size() > 1) {
+      const Seg& sg = segs[seg_of[v]];
+      if (v != sg.nodes.back()) continue;  // fused: no buffer, no launch
+      if (emit_chain(sg)) continue;
+      for (int u : sg.nodes) emit_node(u);
+      continue;
+    }
+    emit_node(v);
   }
 
   // root copy into the per-slice result slot, then advance the slice counter

@@ -19,7 +19,9 @@ struct Loc {
   int64_t off;  // doubles (LEAF: into leaf values, SLICED: into sliced buffer) or bytes (ARENA)
 };
 
-enum StepKind : int8_t { ST_SELECT, ST_TINY, ST_STREAM, ST_GEMM, ST_GENERIC, ST_ROOTCOPY, ST_ETA, ST_GEMM_REDUCE };
+enum StepKind : int8_t {
+  ST_SELECT, ST_TINY, ST_STREAM, ST_GEMM, ST_GENERIC, ST_ROOTCOPY, ST_ETA, ST_GEMM_REDUCE, ST_CHAIN
+};
 
 struct Step {
   StepKind kind;
@@ -29,6 +31,8 @@ struct Step {
   StreamParams sp{};
   GemmParams gp{};
   GenericParams np{};
+  ChainParams cp{};
+  int64_t chain_off = 0;           // first ChainStep of this chain in Program::chain_steps
   int32_t ns = 0, nf = 0;          // stream template selector
   int32_t bm = 6, bn = 6;          // GEMM tile bits (template selector)
   Loc la{}, lb{}, lc{}, lws{};     // operand/output/workspace locations
@@ -57,6 +61,10 @@ struct Program {
   int32_t tiny_smem_doubles = 0;
   // generic digits
   std::vector<GDigit> gdigits;
+  // fused chains: per-step descriptors (P bound per device from chain_piece)
+  std::vector<ChainStep> chain_steps;
+  std::vector<Loc> chain_piece;
+  int n_chain = 0;
   // arena
   int64_t arena_bytes = 0;
   Loc root_loc{};

@@ -196,15 +196,6 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream(const StreamParams p)
 }
 
 // ---------------------------------------------------------------------------
-// K3: FP64 tensor-core GEMM family.  CTA tile BMxBNx16 (BM, BN in 8..64),
-// WGM x WGN warps, each warp a (BM/WGM)x(BN/WGN) block of DMMA m8n8k4
-// fragments; 4-stage cp.async pipeline.  Operands are gathered with
-// per-thread precomputed tile offsets (any bit layout: the index permutation
-// of tensordot is folded into the loads), stored k-major in smem with +4
-// padding (conflict-free fragment loads).  The C tile is staged through smem
-// and written in C's own address order (coalesced for any output layout).
-constexpr int GBK = 16, GSTAGES = 4;
-
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
@@ -214,6 +205,112 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
+
+// ---------------------------------------------------------------------------
+// K2c: fused chain.  Per tile: gather (x_lo, inner) from A in A's address
+// order with cp.async (the next tile's gather overlaps this tile's compute),
+// apply the chain's small operands in smem (tables precomputed on the host),
+// scatter (x_lo, inner') to C in C's address order.  Intermediates of the
+// chain never touch HBM.
+constexpr int kChainThreads = 256;
+constexpr int kChainEl = kChainBuf / kChainThreads;  // max tile elements per thread
+
+__device__ __forceinline__ void tile_part(const TileMap& t, int e, int xt, int64_t& off, int& sidx) {
+  // additive decomposition of tile element e: offset + smem index (u << xt | x)
+  off = 0;
+  int x = 0, u = 0;
+  for (int j = 0; j < t.nbits; ++j)
+    if ((e >> j) & 1) {
+      off += (int64_t)1 << t.pos[j];
+      if (t.kind[j]) u |= 1 << t.sub[j];
+      else x |= 1 << t.sub[j];
+    }
+  sidx = (u << xt) | x;
+}
+
+__global__ void __launch_bounds__(kChainThreads) k_chain(const ChainParams p) {
+  extern __shared__ __align__(16) double csm[];
+  double* lbuf[2] = {csm, csm + kChainBuf};
+  double* wbuf = csm + 2 * kChainBuf;
+  double* pcs = csm + 3 * kChainBuf;                    // kChainMax * 64
+  ChainStep* st = (ChainStep*)(pcs + kChainMax * 64);   // nsteps
+  const int tid = threadIdx.x;
+  {
+    const int words = p.nsteps * (int)sizeof(ChainStep) / 4;
+    const int* src = (const int*)p.steps;
+    int* dst = (int*)st;
+    for (int w = tid; w < words; w += blockDim.x) dst[w] = src[w];
+  }
+  // tile element e = tid + i*256 decomposes additively: thread part (bits
+  // 0..7, registers) + block part (bits 8.., a 16-entry smem table)
+  const int na = 1 << p.ta.nbits, nc = 1 << p.tc.nbits;
+  __shared__ int64_t hi_aoff[kChainEl], hi_coff[kChainEl];
+  __shared__ int hi_asx[kChainEl], hi_csx[kChainEl];
+  if (tid < kChainEl) {
+    tile_part(p.ta, tid * kChainThreads, p.xt, hi_aoff[tid], hi_asx[tid]);
+    tile_part(p.tc, tid * kChainThreads, p.xt, hi_coff[tid], hi_csx[tid]);
+  }
+  int64_t aoff_t, coff_t;
+  int asx_t, csx_t;
+  tile_part(p.ta, tid, p.xt, aoff_t, asx_t);
+  tile_part(p.tc, tid, p.xt, coff_t, csx_t);
+  __syncthreads();
+  for (int i = 0; i < p.nsteps; ++i) {
+    const int nv = 1 << (st[i].ns + st[i].nf);
+    for (int q = tid; q < nv; q += blockDim.x) pcs[i * 64 + q] = st[i].P[st[i].offP[q]];
+  }
+  const int xmask = (1 << p.xt) - 1;
+  auto issue = [&](int64_t tile, double* dst) {
+    const double* Ag = p.A + deposit(tile, p.a_hi);
+    for (int i = 0; i < kChainEl; ++i)
+      if (tid + i * kChainThreads < na) cp_async8(dst + asx_t + hi_asx[i], Ag + aoff_t + hi_aoff[i]);
+  };
+  int64_t tile = blockIdx.x;
+  if (tile < p.n_tiles) issue(tile, lbuf[0]);
+  cp_async_commit();
+  for (int it = 0; tile < p.n_tiles; tile += gridDim.x, ++it) {
+    const int64_t next = tile + gridDim.x;
+    if (next < p.n_tiles) issue(next, lbuf[(it + 1) & 1]);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    double* cur = lbuf[it & 1];
+    double* nxt = wbuf;
+    for (int i = 0; i < p.nsteps; ++i) {
+      const ChainStep& S = st[i];
+      const int n = (1 << S.nnew) << p.xt;
+      const int sv = 1 << S.ns, fv = 1 << S.nf;
+      const double* P = pcs + i * 64;
+      for (int e = tid; e < n; e += kChainThreads) {
+        const int x = e & xmask;
+        const unsigned t = S.utab[e >> p.xt];
+        const int ub = t & 0xff, f = t >> 8;
+        double acc = 0.0;
+        for (int s = 0; s < sv; ++s) acc = fma(cur[((ub | S.stab[s]) << p.xt) | x], P[s * fv + f], acc);
+        nxt[e] = acc;
+      }
+      __syncthreads();
+      double* tmp = cur;
+      cur = nxt;
+      nxt = tmp;
+    }
+    double* Cg = p.C + deposit(tile, p.c_hi);
+    for (int i = 0; i < kChainEl; ++i)
+      if (tid + i * kChainThreads < nc) Cg[coff_t + hi_coff[i]] = cur[csx_t + hi_csx[i]];
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
+// K3: FP64 tensor-core GEMM family.  CTA tile BMxBNx16 (BM, BN in 8..64),
+// WGM x WGN warps, each warp a (BM/WGM)x(BN/WGN) block of DMMA m8n8k4
+// fragments; 4-stage cp.async pipeline.  Operands are gathered with
+// per-thread precomputed tile offsets (any bit layout: the index permutation
+// of tensordot is folded into the loads), stored k-major in smem with +4
+// padding (conflict-free fragment loads).  The C tile is staged through smem
+// and written in C's own address order (coalesced for any output layout).
+constexpr int GBK = 16, GSTAGES = 4;
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -250,7 +347,8 @@ struct GemmCfg {
 };
 
 template <int BM, int BN, int WGM, int WGN>
-__global__ void __launch_bounds__(32 * WGM * WGN) k_gemm(const GemmParams p) {
+__global__ void __launch_bounds__(32 * WGM * WGN, (WGM * WGN >= 8) ? 2 : ((WGM * WGN >= 4) ? 3 : 4))
+    k_gemm(const GemmParams p) {
   using Cfg = GemmCfg<BM, BN, WGM, WGN>;
   constexpr int NT = Cfg::NT, LDA = Cfg::LDA, LDB = Cfg::LDB, LDC = Cfg::LDC;
   constexpr int FM = Cfg::FM, FN = Cfg::FN, ELA = Cfg::ELA, ELB = Cfg::ELB;
@@ -273,27 +371,39 @@ __global__ void __launch_bounds__(32 * WGM * WGN) k_gemm(const GemmParams p) {
   const int64_t kt1 = min(p.k_tiles, kt0 + p.k_per_split);
   const int64_t nkt = kt1 > kt0 ? kt1 - kt0 : 0;
 
-  int64_t aoff[ELA], boff[ELB];
-  int asx[ELA], bsx[ELB];
-  unsigned areal = 0, breal = 0;
-#pragma unroll
-  for (int i = 0; i < ELA; ++i) {
-    int r, k, e = tid + i * NT;
-    bool ok = e < BM * GBK && tile_elem(p.ta, e, aoff[i], r, k);
-    asx[i] = k * LDA + r;
-    if (ok) areal |= 1u << i;
-    if (e < BM * GBK && !ok)
-      for (int s = 0; s < GSTAGES; ++s) As[s * GBK * LDA + asx[i]] = 0.0;
+  // tile element e = tid + i*NT decomposes additively: thread part in
+  // registers + block part in a small smem table (keeps registers low)
+  __shared__ int64_t ha_off[ELA], hb_off[ELB];
+  __shared__ int ha_sx[ELA], hb_sx[ELB];
+  __shared__ bool ha_ok[ELA], hb_ok[ELB];
+  if (tid < ELA) {
+    int r, k;
+    ha_ok[tid] = tile_elem(p.ta, tid * NT, ha_off[tid], r, k) && tid * NT < BM * GBK;
+    ha_sx[tid] = k * LDA + r;
   }
-#pragma unroll
-  for (int i = 0; i < ELB; ++i) {
-    int r, k, e = tid + i * NT;
-    bool ok = e < BN * GBK && tile_elem(p.tb, e, boff[i], r, k);
-    bsx[i] = k * LDB + r;
-    if (ok) breal |= 1u << i;
-    if (e < BN * GBK && !ok)
-      for (int s = 0; s < GSTAGES; ++s) Bs[s * GBK * LDB + bsx[i]] = 0.0;
+  if (tid < ELB) {
+    int r, k;
+    hb_ok[tid] = tile_elem(p.tb, tid * NT, hb_off[tid], r, k) && tid * NT < BN * GBK;
+    hb_sx[tid] = k * LDB + r;
   }
+  int64_t aoff_t, boff_t;
+  int asx_t, bsx_t;
+  bool aok_t, bok_t;
+  {
+    int r, k;
+    aok_t = tile_elem(p.ta, tid, aoff_t, r, k);
+    asx_t = k * LDA + r;
+    bok_t = tile_elem(p.tb, tid, boff_t, r, k);
+    bsx_t = k * LDB + r;
+  }
+  __syncthreads();
+  // virtual elements are zero in every stage and never loaded
+  for (int i = 0; i < ELA; ++i)
+    if (tid + i * NT < BM * GBK && !(aok_t && ha_ok[i]))
+      for (int s = 0; s < GSTAGES; ++s) As[s * GBK * LDA + asx_t + ha_sx[i]] = 0.0;
+  for (int i = 0; i < ELB; ++i)
+    if (tid + i * NT < BN * GBK && !(bok_t && hb_ok[i]))
+      for (int s = 0; s < GSTAGES; ++s) Bs[s * GBK * LDB + bsx_t + hb_sx[i]] = 0.0;
   const double* Ab = p.A + deposit(tm, p.a_m);
   const double* Bb = p.B + deposit(tn, p.b_n);
 
@@ -302,12 +412,16 @@ __global__ void __launch_bounds__(32 * WGM * WGN) k_gemm(const GemmParams p) {
     const double* Bg = Bb + deposit(kt, p.b_k);
     double* as = As + stage * GBK * LDA;
     double* bs = Bs + stage * GBK * LDB;
+    if (aok_t) {
 #pragma unroll
-    for (int i = 0; i < ELA; ++i)
-      if (areal >> i & 1) cp_async8(as + asx[i], Ag + aoff[i]);
+      for (int i = 0; i < ELA; ++i)
+        if (ha_ok[i]) cp_async8(as + asx_t + ha_sx[i], Ag + aoff_t + ha_off[i]);
+    }
+    if (bok_t) {
 #pragma unroll
-    for (int i = 0; i < ELB; ++i)
-      if (breal >> i & 1) cp_async8(bs + bsx[i], Bg + boff[i]);
+      for (int i = 0; i < ELB; ++i)
+        if (hb_ok[i]) cp_async8(bs + bsx_t + hb_sx[i], Bg + boff_t + hb_off[i]);
+    }
   };
 
   double acc[FM][FN][2];
@@ -369,11 +483,27 @@ __global__ void __launch_bounds__(32 * WGM * WGN) k_gemm(const GemmParams p) {
     }
     return;
   }
-  double* Cg = p.C + deposit(tm, p.c_m) + deposit(tn, p.c_n);
-  for (int e = tid; e < BM * BN; e += NT) {
-    int64_t off;
+  // C element e = tid + i*NT: offset/slot split into a thread part and a
+  // block part (table), so the scatter costs one add per element
+  constexpr int ELC = BM * BN / NT;
+  __shared__ int64_t hc_off[ELC];
+  __shared__ int hc_sx[ELC];
+  __shared__ bool hc_ok[ELC];
+  if (tid < ELC) {
     int r, k;
-    if (tile_elem(p.tc, e, off, r, k)) Cg[off] = Cs[r * LDC + k];
+    hc_ok[tid] = tile_elem(p.tc, tid * NT, hc_off[tid], r, k);
+    hc_sx[tid] = r * LDC + k;
+  }
+  int64_t c_off_t;
+  int rt, kt_;
+  const bool c_ok_t = tile_elem(p.tc, tid, c_off_t, rt, kt_);
+  const int c_sx_t = rt * LDC + kt_;
+  __syncthreads();
+  double* Cg = p.C + deposit(tm, p.c_m) + deposit(tn, p.c_n);
+  if (c_ok_t) {
+#pragma unroll 8
+    for (int i = 0; i < ELC; ++i)
+      if (hc_ok[i]) Cg[c_off_t + hc_off[i]] = Cs[c_sx_t + hc_sx[i]];
   }
 }
 

@@ -77,6 +77,32 @@ struct GemmParams {
   int32_t grid_swizzle_log;  // group of 2^g m-tiles walked together (L2 reuse)
 };
 
+// ---- K2c: fused chain of big x small contractions (dim 2) -----------------
+// A chain v1..vk (v_{i+1}'s big operand is v_i) runs as ONE pass: a CTA loads
+// a tile = (x_lo outer bits) x (all "inner" bits the chain touches) of the
+// input, applies the k small operands in shared memory, stores the tile of
+// v_k.  Intermediates v_1..v_{k-1} never touch HBM.
+constexpr int kChainU = 6;       // max inner bits alive at any step (x_lo >= 6 bits)
+constexpr int kChainMax = 16;    // max steps per fused segment
+constexpr int kChainBuf = 4096;  // doubles per smem tile buffer (x_lo * 2^inner)
+struct ChainStep {
+  const double* P;         // small operand
+  int32_t offP[64];        // s * 2^nf + f -> offset in P
+  uint16_t utab[1 << kChainU];  // new inner u -> (cur inner base | f << 8)
+  uint8_t stab[16];        // s -> cur inner bits of the shared indices
+  int32_t ns, nf, nnew, pad;
+};
+struct ChainParams {
+  const double* A;
+  double* C;
+  const ChainStep* steps;
+  int32_t nsteps;
+  int32_t xt;  // x_lo bits
+  int64_t n_tiles;
+  BitRuns a_hi, c_hi;  // x_hi -> offsets
+  TileMap ta, tc;      // (x_lo kind 0, inner kind 1) in A / C address order
+};
+
 // ---- K4: tiny-subtree forest (any domain) ----------------------------------
 struct TinyNode {
   const double* ga;  // global operand (leaf / forced root) or nullptr -> smem

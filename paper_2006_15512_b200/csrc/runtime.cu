@@ -111,6 +111,7 @@ GemmVariant gv() {
 // every warp owns >= 8x8)
 GemmVariant gemm_variant(int bm, int bn) {
   switch (bm * 8 + bn) {
+    case 7 * 8 + 6: return gv<128, 64, 4, 2>();
     case 6 * 8 + 6: return gv<64, 64, 2, 2>();
     case 6 * 8 + 5: return gv<64, 32, 2, 2>();
     case 5 * 8 + 6: return gv<32, 64, 2, 2>();
@@ -129,6 +130,10 @@ GemmVariant gemm_variant(int bm, int bn) {
     case 3 * 8 + 3: return gv<8, 8, 1, 1>();
   }
   throw Error{TC_BAD_ARG, "no GEMM variant for this tile"};
+}
+
+int chain_smem(int nsteps) {
+  return (3 * kChainBuf + kChainMax * 64) * 8 + nsteps * (int)sizeof(ChainStep);
 }
 
 int sm_count(int dev) {
@@ -187,6 +192,7 @@ struct tc_exec {
   TinyDigit* tdigs = nullptr;
   TinyGroup* tgroups = nullptr;
   GDigit* gdig = nullptr;
+  ChainStep* chains = nullptr;
   SelEntry* sel = nullptr;
   SelTerm* selt = nullptr;
   int64_t* eta = nullptr;
@@ -204,7 +210,7 @@ struct tc_exec {
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
     for (void* q : {(void*)arena, (void*)leafbuf, (void*)slicedbuf, (void*)tnodes, (void*)tdigs,
-                    (void*)tgroups, (void*)gdig, (void*)sel, (void*)selt, (void*)eta, (void*)results,
+                    (void*)tgroups, (void*)gdig, (void*)chains, (void*)sel, (void*)selt, (void*)eta, (void*)results,
                     (void*)folded})
       if (q) cudaFree(q);
     if (stream) cudaStreamDestroy(stream);
@@ -254,6 +260,13 @@ struct tc_exec {
       CU(cudaMemcpyAsync(tgroups, g.tiny_groups.data(), g.tiny_groups.size() * sizeof(TinyGroup),
                          cudaMemcpyHostToDevice, stream));
     }
+    if (!g.chain_steps.empty()) {
+      std::vector<ChainStep> cs = g.chain_steps;
+      for (size_t i = 0; i < cs.size(); ++i) cs[i].P = ptr(g.chain_piece[i]);
+      chains = dalloc<ChainStep>(cs.size(), dev_bytes);
+      CU(cudaMemcpyAsync(chains, cs.data(), cs.size() * sizeof(ChainStep), cudaMemcpyHostToDevice, stream));
+      CU(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, chain_smem(kChainMax)));
+    }
     if (!g.gdigits.empty()) {
       gdig = dalloc<GDigit>(g.gdigits.size(), dev_bytes);
       CU(cudaMemcpyAsync(gdig, g.gdigits.data(), g.gdigits.size() * sizeof(GDigit), cudaMemcpyHostToDevice, stream));
@@ -264,8 +277,9 @@ struct tc_exec {
 
     const int tiny_smem = (int)(g.tiny_smem_doubles + kTinyThreads) * 8;
     CU(cudaFuncSetAttribute(k_tiny, cudaFuncAttributeMaxDynamicSharedMemorySize, tiny_smem));
-    for (int bm = 3; bm <= 6; ++bm)
+    for (int bm = 3; bm <= 7; ++bm)
       for (int bn = 3; bn <= 6; ++bn) {
+        if (bm == 7 && bn != 6) continue;
         GemmVariant v = gemm_variant(bm, bn);
         CU(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
       }
@@ -323,6 +337,18 @@ struct tc_exec {
           L.grid = dim3((unsigned)st.work, (unsigned)gp.splits);
           L.smem = v.smem;
           L.arg(gp);
+          break;
+        }
+        case ST_CHAIN: {
+          ChainParams cp = st.cp;
+          cp.A = ptr(st.la);
+          cp.C = (double*)ptr(st.lc);
+          cp.steps = chains + st.chain_off;
+          L.func = (void*)k_chain;
+          L.block = dim3(kChainThreads);
+          L.grid = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cp.n_tiles, (int64_t)sm_count(device) * 4)));
+          L.smem = chain_smem(cp.nsteps);
+          L.arg(cp);
           break;
         }
         case ST_GEMM_REDUCE: {
