@@ -97,6 +97,8 @@ typedef struct tc_stats {
   int32_t n_tiny_nodes, n_stream_nodes, n_gemm_nodes, n_generic_nodes;
   tc_u128 alg_bytes;             /* per slice: sum over nodes 8(|A|+|B|+|C|) */
   tc_u128 alg_flops;             /* per slice: sum over nodes 2*prod(union)  */
+  int32_t n_alias_nodes;         /* exact relabels (identity pieces): no launch */
+  int32_t n_chain_launches;      /* fused chain launches                      */
 } tc_stats;
 
 /* ---- symbolic plan (host) ---------------------------------------------- */
@@ -161,6 +163,10 @@ int tc_exec_fetch(tc_exec* ex, double* per_slice, double* folded);
  * bytes / flops.  Arrays hold `cap` entries; *n = number of launches. */
 int tc_exec_profile(tc_exec* ex, int64_t slice, float* step_ms, int32_t* step_kind, int32_t* step_slot,
                     double* step_bytes, double* step_flops, int32_t cap, int32_t* n);
+
+/* Diagnostics: the launch DAG in CSR form (dep_off[n+1], deps[...]; launch
+ * i depends on deps[dep_off[i] .. dep_off[i+1])).  *n = launches, *m = edges. */
+int tc_exec_deps(const tc_exec* ex, int32_t* dep_off, int32_t* deps, int32_t cap, int32_t* n, int32_t* m);
 int64_t tc_exec_result_size(const tc_exec* ex);
 
 /* One-shot Algorithm 3 (slicing.py:112-146) from host buffers: pick slices

@@ -75,6 +75,8 @@ class Stats(C.Structure):
         ("n_generic_nodes", C.c_int32),
         ("alg_bytes", U128),
         ("alg_flops", U128),
+        ("n_alias_nodes", C.c_int32),
+        ("n_chain_launches", C.c_int32),
     ]
 
     def as_dict(self):
@@ -92,6 +94,8 @@ class Stats(C.Structure):
             n_generic_nodes=int(self.n_generic_nodes),
             alg_bytes=self.alg_bytes.value(),
             alg_flops=self.alg_flops.value(),
+            n_alias_nodes=int(self.n_alias_nodes),
+            n_chain_launches=int(self.n_chain_launches),
         )
 
 
@@ -114,6 +118,7 @@ SIGNATURES = {
     "tc_exec_profile": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_float), I32P, I32P, F64P, F64P,
                                   C.c_int32, I32P]),
     "tc_exec_result_size": (C.c_int64, [C.c_void_p]),
+    "tc_exec_deps": (C.c_int, [C.c_void_p, I32P, I32P, C.c_int32, I32P, I32P]),
     "tc_sliced_execute": (
         C.c_int,
         [C.c_void_p, C.c_int64, I32P, C.c_int32, I32P, C.c_int32, F64P, C.c_int64, I32P, C.c_int32,
@@ -312,6 +317,15 @@ class Exec:
         k = n.value
         return [dict(kind=self.KINDS[kind[i]], slot=int(slot[i]), ms=float(ms[i]), bytes=float(by[i]),
                      flops=float(fl[i])) for i in range(k)]
+
+    def deps(self):
+        """Launch DAG: list of dependency lists (diagnostics)."""
+        cap = 1 << 22
+        off = np.zeros(cap + 1, dtype=np.int32)
+        dd = np.zeros(cap, dtype=np.int32)
+        n, m = C.c_int32(), C.c_int32()
+        check(lib().tc_exec_deps(self.h, _p(off, I32P), _p(dd, I32P), cap, C.byref(n), C.byref(m)))
+        return [dd[off[i]:off[i + 1]].tolist() for i in range(n.value)]
 
     def result_size(self) -> int:
         return int(lib().tc_exec_result_size(self.h))

@@ -38,8 +38,15 @@ struct Alloc {
   std::map<int64_t, std::pair<int64_t, int>> seg;     // off -> (end, last reader step)
   int64_t top = 0;
 
+  bool no_reuse = false;  // every buffer gets fresh memory: no WAR edges at all
+
   int64_t alloc(int64_t size, std::vector<int>& hazards) {
     size = (size + kAlign - 1) / kAlign * kAlign;
+    if (no_reuse) {
+      int64_t o = top;
+      top += size;
+      return o;
+    }
     int64_t off = -1;
     for (auto it = free_.begin(); it != free_.end(); ++it) {
       if (it->second >= size) {
@@ -86,6 +93,7 @@ struct Alloc {
   }
 
   void release(int64_t off, int64_t size, int reader) {
+    if (no_reuse) return;
     size = (size + kAlign - 1) / kAlign * kAlign;
     seg[off] = {off + size, reader};
     auto nx = free_.lower_bound(off);
@@ -129,7 +137,7 @@ BitRuns make_runs(const std::vector<std::pair<int, int>>& bits) {  // (src bit, 
 
 }  // namespace
 
-Program compile_program(const Plan& p, const std::vector<int>& chosen_in) {
+Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_t no_reuse_limit) {
   Program g;
   const int S = p.nslots();
   std::vector<char> drop(p.NI, 0);
@@ -277,6 +285,37 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in) {
       default:
         want(a, natural(a));
         want(b, natural(b));
+    }
+  }
+
+  // ---- exact relabels ---------------------------------------------------------
+  // big x (2x2 identity) piece: C[.., f, ..] = sum_s A[.., s, ..] I[s, f] is A
+  // with index s renamed f (x*1 + y*0 == x for finite y, bit for bit).  The
+  // layout pass put f at s's address bit, so C IS A's buffer: no launch, no
+  // traffic.  (In C2 these are 2004 of 2783 big x piece nodes: the
+  // non-carrier pieces of factored copy tensors, factoring.py:194-206.)
+  std::vector<int> alias_src(S, -1);
+  if (!std::getenv("TC_NO_ALIAS")) {
+    for (int k = 0; k < p.NN; ++k) {
+      const int v = p.NL + k, a = p.left[k], b = p.right[k];
+      if (g.cls[v] != NC_STREAM) continue;
+      const bool b_small = eff[b].size() <= eff[a].size();
+      const int big = b_small ? a : b, sm = b_small ? b : a;
+      if (p.is_leaf(big) || !p.is_leaf(sm) || p.sets[sm].size() != 2 || eff[sm].size() != 2) continue;
+      std::vector<int> Sh = inter(eff[a], eff[b]);
+      std::vector<int> F = minus(eff[sm], Sh);
+      if (Sh.size() != 1 || F.size() != 1) continue;
+      const double* q = p.lval.data() + p.lval_off[sm];
+      if (!(q[0] == 1.0 && q[3] == 1.0 && q[1] == 0.0 && q[2] == 0.0)) continue;
+      const auto& Lv = g.layout[v];
+      const auto& Lg = g.layout[big];
+      bool same = Lv.size() == Lg.size();
+      for (size_t i = 0; same && i < Lv.size(); ++i)
+        same = Lv[i] == Lg[i] || (Lg[i] == Sh[0] && Lv[i] == F[0]);
+      if (!same) continue;
+      g.cls[v] = NC_ALIAS;
+      alias_src[v] = big;
+      g.n_alias++;
     }
   }
 
@@ -489,6 +528,21 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in) {
 
   // ---- steps + arena --------------------------------------------------------
   Alloc arena;
+  {
+    // Arena policy.  Reusing freed memory adds write-after-read edges that
+    // serialise the launch DAG; when every intermediate fits in the HBM the
+    // caller grants (no_reuse_limit), give each buffer its own memory so
+    // independent branches of the tree run concurrently.
+    int64_t total = 0;
+    for (int k = 0; k < p.NN; ++k) {
+      int v = p.NL + k;
+      if (g.cls[v] != NC_TINY || p.parent[v] < 0 || g.cls[p.parent[v]] != NC_TINY)
+        total += (size[v] * 8 + kAlign - 1) / kAlign * kAlign;
+    }
+    total += total / 8 + ((int64_t)1 << 20);  // split-K workspaces, alignment
+    const char* env = std::getenv("TC_ARENA_REUSE");
+    arena.no_reuse = env ? std::atoi(env) == 0 : total <= no_reuse_limit;
+  }
   std::vector<int> producer(S, -1);
   int sel_step = -1;
   if (!g.sel_ent.empty()) {
@@ -968,8 +1022,9 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in) {
     for (auto& c : cs) umax = std::max(umax, c.nnew);
     int lbuf = 0;
     while ((2 << lbuf) <= kChainBuf) ++lbuf;  // log2(kChainBuf)
-    const int xt = std::min((int)O.size(), lbuf - umax);
-    if (xt < 0) return false;
+    // x_lo bits: as wide as the smem tile allows, but leave >= ~2 tiles per SM
+    const int xt = std::max(0, std::min({(int)O.size(), lbuf - umax, std::max(2, (int)O.size() - 9)}));
+    if (lbuf - umax < 0) return false;
     ChainParams cp{};
     cp.nsteps = (int)cs.size();
     cp.xt = xt;
@@ -1043,6 +1098,13 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in) {
       int ts = tiny_step[glevel[gi]];
       g.steps[ts].alg_bytes += node_bytes[v];
       g.steps[ts].alg_flops += node_flops[v];
+      continue;
+    }
+    if (g.cls[v] == NC_ALIAS) {  // same buffer, same bits: ownership moves to v
+      const int src = alias_src[v];
+      g.loc[v] = g.loc[src];
+      bytes[v] = bytes[src];
+      producer[v] = producer[src];
       continue;
     }
     if (g.cls[v] == NC_STREAM && seg_of[v] >= 0 && segs[seg_of[v]].nodes.size() > 1) {

@@ -10,7 +10,7 @@
 
 namespace tc {
 
-enum NodeClass : int8_t { NC_LEAF = 0, NC_TINY = 1, NC_STREAM = 2, NC_GEMM = 3, NC_GENERIC = 4 };
+enum NodeClass : int8_t { NC_LEAF = 0, NC_TINY = 1, NC_STREAM = 2, NC_GEMM = 3, NC_GENERIC = 4, NC_ALIAS = 5 };
 
 // Where an operand lives at run time.
 enum LocKind : int8_t { LOC_LEAF = 0, LOC_SLICED = 1, LOC_ARENA = 2, LOC_SMEM = 3 };
@@ -70,11 +70,13 @@ struct Program {
   Loc root_loc{};
   std::vector<Step> steps;
   // stats
-  int n_tiny = 0, n_stream = 0, n_gemm = 0, n_generic = 0;
+  int n_tiny = 0, n_stream = 0, n_gemm = 0, n_generic = 0, n_alias = 0;
   u128 alg_bytes = 0, alg_flops = 0;
   u128 mem_estimate = 0, peak_observed = 0;
 };
 
-Program compile_program(const Plan& p, const std::vector<int>& chosen);
+// no_reuse_limit: if all intermediates together need at most this many bytes,
+// every buffer gets its own memory (no write-after-read edges in the DAG).
+Program compile_program(const Plan& p, const std::vector<int>& chosen, int64_t no_reuse_limit = 0);
 
 }  // namespace tc

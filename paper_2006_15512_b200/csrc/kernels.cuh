@@ -228,6 +228,34 @@ __device__ __forceinline__ void tile_part(const TileMap& t, int e, int xt, int64
   sidx = (u << xt) | x;
 }
 
+// one chain step with the small operand and the shared-bit offsets in registers
+template <int NS, int NF>
+__device__ __forceinline__ void chain_step(const ChainStep& S, const double* P, const double* cur, double* nxt,
+                                           int n, int xt, int xmask, int tid) {
+  constexpr int SV = 1 << NS, FV = 1 << NF;
+  double pr[SV * FV];
+  int sb[SV];
+#pragma unroll
+  for (int q = 0; q < SV * FV; ++q) pr[q] = P[q];
+#pragma unroll
+  for (int s = 0; s < SV; ++s) sb[s] = S.stab[s];
+  for (int e = tid; e < n; e += kChainThreads) {
+    const int x = e & xmask;
+    const unsigned t = S.utab[e >> xt];
+    const int ub = t & 0xff, f = t >> 8;
+    double acc = 0.0;
+#pragma unroll
+    for (int s = 0; s < SV; ++s) {
+      double pv = pr[s * FV];
+#pragma unroll
+      for (int ff = 1; ff < FV; ++ff)
+        if (f == ff) pv = pr[s * FV + ff];
+      acc = fma(cur[((ub | sb[s]) << xt) | x], pv, acc);
+    }
+    nxt[e] = acc;
+  }
+}
+
 __global__ void __launch_bounds__(kChainThreads) k_chain(const ChainParams p) {
   extern __shared__ __align__(16) double csm[];
   double* lbuf[2] = {csm, csm + kChainBuf};
@@ -281,13 +309,22 @@ __global__ void __launch_bounds__(kChainThreads) k_chain(const ChainParams p) {
       const int n = (1 << S.nnew) << p.xt;
       const int sv = 1 << S.ns, fv = 1 << S.nf;
       const double* P = pcs + i * 64;
-      for (int e = tid; e < n; e += kChainThreads) {
-        const int x = e & xmask;
-        const unsigned t = S.utab[e >> p.xt];
-        const int ub = t & 0xff, f = t >> 8;
-        double acc = 0.0;
-        for (int s = 0; s < sv; ++s) acc = fma(cur[((ub | S.stab[s]) << p.xt) | x], P[s * fv + f], acc);
-        nxt[e] = acc;
+      const int key = S.ns * 8 + S.nf;
+      if (key == 1 * 8 + 1) chain_step<1, 1>(S, P, cur, nxt, n, p.xt, xmask, tid);
+      else if (key == 2 * 8 + 1) chain_step<2, 1>(S, P, cur, nxt, n, p.xt, xmask, tid);
+      else if (key == 1 * 8 + 2) chain_step<1, 2>(S, P, cur, nxt, n, p.xt, xmask, tid);
+      else if (key == 2 * 8 + 2) chain_step<2, 2>(S, P, cur, nxt, n, p.xt, xmask, tid);
+      else if (key == 1 * 8 + 0) chain_step<1, 0>(S, P, cur, nxt, n, p.xt, xmask, tid);
+      else if (key == 2 * 8 + 0) chain_step<2, 0>(S, P, cur, nxt, n, p.xt, xmask, tid);
+      else {
+        for (int e = tid; e < n; e += kChainThreads) {
+          const int x = e & xmask;
+          const unsigned t = S.utab[e >> p.xt];
+          const int ub = t & 0xff, f = t >> 8;
+          double acc = 0.0;
+          for (int s = 0; s < sv; ++s) acc = fma(cur[((ub | S.stab[s]) << p.xt) | x], P[s * fv + f], acc);
+          nxt[e] = acc;
+        }
       }
       __syncthreads();
       double* tmp = cur;

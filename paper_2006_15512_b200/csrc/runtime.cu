@@ -227,8 +227,14 @@ struct tc_exec {
 
   void build(const Plan& p, const std::vector<int>& chosen) {
     auto t0 = std::chrono::steady_clock::now();
-    prog = compile_program(p, chosen);
     CU(cudaSetDevice(device));
+    size_t free_b = 0, total_b = 0;
+    CU(cudaMemGetInfo(&free_b, &total_b));
+    // Reuse-free arenas only on request (TC_ARENA_REUSE=0): the factored trees
+    // are spines (C2: 2434 of 2918 launches on the critical path even without
+    // write-after-read edges) and mapping a 45 GB arena costs ~200 ms per call.
+    prog = compile_program(p, chosen, 0);
+    (void)free_b;
     CU(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     Program& g = prog;
     arena = dalloc<char>((size_t)g.arena_bytes, dev_bytes);
@@ -652,6 +658,8 @@ static void fill_stats(const tc_exec& ex, double ms, tc_stats* s) {
   s->n_generic_nodes = g.n_generic;
   s->alg_bytes = to_abi(g.alg_bytes);
   s->alg_flops = to_abi(g.alg_flops);
+  s->n_alias_nodes = g.n_alias;
+  s->n_chain_launches = g.n_chain;
 }
 
 int tc_exec_run(tc_exec* ex, int64_t slice_begin, int64_t slice_end, tc_stats* stats) {
@@ -703,6 +711,23 @@ int tc_exec_profile(tc_exec* ex, int64_t slice, float* step_ms, int32_t* step_ki
       if (step_flops) step_flops[i] = ex->launches[i].flops;
     }
     *n = (int32_t)ms.size();
+  });
+}
+
+int tc_exec_deps(const tc_exec* ex, int32_t* dep_off, int32_t* deps, int32_t cap, int32_t* n, int32_t* m) {
+  return guard([&] {
+    const auto& st = ex->prog.steps;
+    int32_t e = 0;
+    for (size_t i = 0; i < st.size(); ++i) {
+      if (dep_off && (int32_t)i <= cap) dep_off[i] = e;
+      for (int d : st[i].deps) {
+        if (deps && e < cap) deps[e] = d;
+        ++e;
+      }
+    }
+    if (dep_off && (int32_t)st.size() <= cap) dep_off[st.size()] = e;
+    *n = (int32_t)st.size();
+    *m = e;
   });
 }
 

@@ -53,6 +53,29 @@ def main():
     for k, (n, ms, by, fl) in sorted(agg.items(), key=lambda x: -x[1][1]):
         print(f"  {k:9s} n={n:6d} ms={ms:9.3f} ({100 * ms / tot:5.1f}%)  GB/s={by / ms / 1e6 if ms else 0:8.1f}"
               f"  GF/s={fl / ms / 1e6 if ms else 0:9.1f}")
+    # critical path of the launch DAG with eager per-launch times
+    deps = ex.deps()
+    fin = [0.0] * len(prof)
+    pred = [-1] * len(prof)
+    for i, p in enumerate(prof):
+        best, arg = 0.0, -1
+        for d in deps[i]:
+            if fin[d] > best:
+                best, arg = fin[d], d
+        fin[i] = best + p["ms"]
+        pred[i] = arg
+    end = max(range(len(prof)), key=lambda i: fin[i])
+    path = []
+    while end >= 0:
+        path.append(end)
+        end = pred[end]
+    cp = collections.Counter()
+    cpn = collections.Counter()
+    for i in path:
+        cp[prof[i]["kind"]] += prof[i]["ms"]
+        cpn[prof[i]["kind"]] += 1
+    print(f"critical path (eager times): {max(fin):.3f} ms over {len(path)} launches:",
+          {k: (cpn[k], round(v, 3)) for k, v in cp.items()})
     print("top launches:")
     for p in sorted(prof, key=lambda p: -p["ms"])[: a.top]:
         print(f"  {p['kind']:8s} slot={p['slot']:7d} shape(ra,rb,rc,k)={shape.get(p['slot'])} ms={p['ms']:.4f}"
