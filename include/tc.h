@@ -120,6 +120,15 @@ int tc_choose_slice_index(const tc_plan* plan, const int32_t* already, int32_t n
 int tc_choose_slices(const tc_plan* plan, int64_t mem_budget, int32_t* chosen, int32_t cap,
                      int32_t* n_chosen, tc_u128* needs);
 
+/* Work-aware slice chooser (an extension; the reference has only the
+ * memory-greedy above).  Appends bond picks to `chosen` (which may already
+ * hold n_already picks) until every intermediate has <= max_entries entries:
+ * each pick shrinks the current largest intermediates and keeps the most
+ * roofline work inside sliced nodes.  Use with tc_exec_create /
+ * tc_sliced_execute(slice_ids=...). */
+int tc_choose_slices_work(const tc_plan* plan, int32_t* chosen, int32_t n_already, int32_t cap,
+                          int64_t max_entries, int32_t* n_chosen);
+
 /* Reference-order index list of the result (kept_a ++ kept_b recursively,
  * tensor.py:108), sliced indices removed.  *rank receives its length. */
 int tc_result_indices(const tc_plan* plan, const int32_t* sliced, int32_t n_sliced,

@@ -108,6 +108,7 @@ SIGNATURES = {
     "tc_choose_slice_index": (C.c_int, [C.c_void_p, I32P, C.c_int32, I32P]),
     "tc_choose_slices": (C.c_int, [C.c_void_p, C.c_int64, I32P, C.c_int32, I32P, C.POINTER(U128)]),
     "tc_result_indices": (C.c_int, [C.c_void_p, I32P, C.c_int32, I32P, C.c_int32, I32P]),
+    "tc_choose_slices_work": (C.c_int, [C.c_void_p, I32P, C.c_int32, C.c_int32, C.c_int64, I32P]),
     "tc_exec_create": (C.c_int, [C.c_void_p, I32P, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
     "tc_exec_free": (None, [C.c_void_p]),
     "tc_exec_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(Stats)]),
@@ -233,6 +234,16 @@ class PlanHandle:
         out = C.c_int32()
         check(lib().tc_choose_slice_index(self.h, p, n, C.byref(out)))
         return int(out.value)
+
+    def choose_slices_work(self, max_entries: int, already=()):
+        """Work-aware slice set (extension): picks until every intermediate
+        has <= max_entries entries."""
+        cap = max(1, len(self.flat.domain))
+        buf = np.zeros(cap, dtype=np.int32)
+        buf[: len(already)] = list(already)
+        n = C.c_int32()
+        check(lib().tc_choose_slices_work(self.h, _p(buf, I32P), len(already), cap, int(max_entries), C.byref(n)))
+        return buf[: n.value].tolist()
 
     def result_indices(self, sliced_ids=()):
         a, p, n = ids_ptr(sliced_ids)

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstring>
 #include <thread>
 
@@ -268,6 +269,56 @@ int choose_slice_index(const Plan& p, const std::vector<char>& already) {
     }
   }
   return cand[bk];
+}
+
+std::vector<int> choose_slices_work(const Plan& p, const std::vector<int>& already, u128 max_entries,
+                                    int max_picks, double bw, double fp) {
+  std::vector<char> drop(p.NI, 0);
+  for (int i : already) drop.at(i) = 1;
+  std::vector<int> picks;
+  const int S = p.nslots();
+  std::vector<double> lsz(S), work(S);
+  for (int it = 0; it < max_picks; ++it) {
+    // current sizes (log2 for dim-2 plans is exact enough for ranking; use doubles)
+    double mx = 0;
+    for (int s = 0; s < S; ++s) {
+      double z = 1;
+      for (int i : p.sets[s])
+        if (!drop[i]) z *= p.dom[i];
+      lsz[s] = z;
+      if (s >= p.NL) mx = std::max(mx, z);
+    }
+    if ((u128)mx <= max_entries) break;
+    for (int k = 0; k < p.NN; ++k) {
+      const int v = p.NL + k, a = p.left[k], b = p.right[k];
+      // |A u B| = |A||B|/|shared|, |shared|^2 = |A||B|/|C| for a pairwise contraction
+      const double sh = std::sqrt(std::max(1.0, lsz[a] * lsz[b] / std::max(1.0, lsz[v])));
+      const double un = lsz[a] * lsz[b] / sh;
+      work[v] = std::max(8.0 * (lsz[a] + lsz[b] + lsz[v]) / bw, 2.0 * un / fp);
+    }
+    int best = -1;
+    double best_hits = -1, best_w = -1;
+    for (int c : p.bonds_sorted) {
+      if (drop[c]) continue;
+      double hits = 0, w = 0;
+      for (int leafv : {p.occ0[c], p.occ1[c]}) {
+        for (int v = p.parent[leafv]; v >= 0 && std::binary_search(p.sets[v].begin(), p.sets[v].end(), c);
+             v = p.parent[v]) {
+          if (lsz[v] >= mx) hits += 1;
+          w += work[v];
+        }
+      }
+      if (hits > best_hits || (hits == best_hits && w > best_w)) {
+        best = c;
+        best_hits = hits;
+        best_w = w;
+      }
+    }
+    if (best < 0) throw Error{TC_NO_CANDIDATES, "no bond index left to slice"};
+    picks.push_back(best);
+    drop[best] = 1;
+  }
+  return picks;
 }
 
 u128 tracked_peak(const Plan& p, const std::vector<char>& drop) {

@@ -55,6 +55,14 @@ u128 mem_cost(const Plan& p, const std::vector<char>& drop);
 // slicing.py:70-79 (incremental, parallel over candidates)
 int choose_slice_index(const Plan& p, const std::vector<char>& already);
 
+// Work-aware slice chooser (not in the reference): pick bonds until the largest
+// intermediate has at most max_entries entries; each pick must shrink the
+// current largest intermediates and, among those, keeps the most roofline work
+// inside the sliced nodes (adding index c doubles the total work of every node
+// NOT containing c).  Returns the picks in order.
+std::vector<int> choose_slices_work(const Plan& p, const std::vector<int>& already, u128 max_entries,
+                                    int max_picks, double hbm_bytes_per_s, double flops_per_s);
+
 // slicing.py:91-109 accounting only (no arithmetic): the tracked peak
 u128 tracked_peak(const Plan& p, const std::vector<char>& drop);
 

@@ -613,6 +613,21 @@ int tc_choose_slices(const tc_plan* plan, int64_t mem_budget, int32_t* chosen, i
   });
 }
 
+int tc_choose_slices_work(const tc_plan* plan, int32_t* chosen, int32_t n_already, int32_t cap, int64_t max_entries,
+                          int32_t* n_chosen) {
+  return guard([&] {
+    std::vector<int> already(chosen, chosen + std::max(0, n_already));
+    auto picks = choose_slices_work(plan->p, already, (u128)std::max<int64_t>(1, max_entries),
+                                    std::max(0, cap - n_already), 6.5517e12, 35.5e12);
+    int n = n_already;
+    for (int c : picks) {
+      if (n >= cap) throw Error{TC_BAD_ARG, "chosen buffer too small"};
+      chosen[n++] = c;
+    }
+    *n_chosen = n;
+  });
+}
+
 int tc_result_indices(const tc_plan* plan, const int32_t* sliced, int32_t n_sliced, int32_t* out_idx, int32_t cap,
                       int32_t* rank) {
   return guard([&] {
