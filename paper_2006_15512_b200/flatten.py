@@ -4,12 +4,17 @@ that cross the C-ABI (``include/tc.h``, ``tc_plan_desc``).
 Works on the reference's objects (``tensorcount.network.TensorNetwork`` /
 ``ContractionTree`` / ``tensor.Tensor`` / ``Index``) and on this package's
 mirror types alike: only ``n.tensors``, ``tensor.indices``, ``tensor.values``,
-``index.id``, ``index.domain_size``, ``index.sort_key()``, ``node.is_leaf``,
-``node.tensor``, ``node.left`` and ``node.right`` are read.
+``index.id``, ``index.domain_size``, ``index.sort_key()``, ``node.tensor``,
+``node.left`` and ``node.right`` are read.
 
 Slot numbering follows ``serialize_plan`` (reference ``network.py:235-258``):
 leaves are numbered by network order, internal nodes continue the numbering in
 postorder (left subtree, right subtree, node; ``network.py:114-124``).
+
+This runs on every call of the public API, so it is written for speed: index
+identity is keyed on ``Index.id`` (the reference's equality, ``tensor.py:29-33``),
+values are gathered with one ``np.concatenate``, and ``sort_key`` ranks (only
+needed by the greedy slice chooser) can be skipped.
 """
 
 from __future__ import annotations
@@ -41,67 +46,58 @@ class FlatPlan:
         return len(self.left)
 
 
-def _postorder_internal(t):
-    """Internal nodes in reference postorder, iteratively (deep spines)."""
-    out = []
-    stack = [t]
-    while stack:
-        node = stack.pop()
-        out.append(node)
-        if not node.is_leaf:
-            stack.append(node.left)
-            stack.append(node.right)
-    out.reverse()
-    return out
+def sort_ranks(indices) -> np.ndarray:
+    order = sorted(range(len(indices)), key=lambda d: indices[d].sort_key())
+    r = np.empty(len(indices), dtype=np.int32)
+    r[order] = np.arange(len(indices), dtype=np.int32)
+    return r
 
 
-def flatten(n, t, index_table=None) -> FlatPlan:
-    tensors = list(n.tensors)
+def flatten(n, t, with_sort_rank: bool = True) -> FlatPlan:
+    tensors = n.tensors
+    nl = len(tensors)
+    pos = {}
+    indices = []
+    idx_list = []
+    ranks = np.empty(nl, dtype=np.int64)
+    vals = []
     leaf_slot = {}
     for k, ten in enumerate(tensors):
         leaf_slot[id(ten)] = k
-
-    # dense index ids in order of first appearance over the network
-    if index_table is None:
-        index_table = {}
-    indices = []
-    idx_list = []
-    idx_off = [0]
-    val_chunks = []
-    val_off = [0]
-    for ten in tensors:
-        for ix in ten.indices:
-            d = index_table.get(ix)
+        inds = ten.indices
+        ranks[k] = len(inds)
+        for ix in inds:
+            d = pos.get(ix.id)
             if d is None:
-                d = len(index_table)
-                index_table[ix] = d
+                d = pos[ix.id] = len(indices)
                 indices.append(ix)
             idx_list.append(d)
-        idx_off.append(len(idx_list))
-        v = np.ascontiguousarray(np.asarray(ten.values, dtype=np.float64)).reshape(-1)
-        val_chunks.append(v)
-        val_off.append(val_off[-1] + v.size)
-    if len(indices) != len(index_table):
-        # caller-supplied table: rebuild the position list
-        indices = [None] * len(index_table)
-        for ix, d in index_table.items():
-            indices[d] = ix
-    domain = np.array([ix.domain_size for ix in indices], dtype=np.int32)
-    order = sorted(range(len(indices)), key=lambda d: indices[d].sort_key())
-    sort_rank = np.empty(len(indices), dtype=np.int32)
-    sort_rank[order] = np.arange(len(indices), dtype=np.int32)
+        vals.append(ten.values)
+    flat_vals = [np.ravel(v) for v in vals]
+    sizes = np.fromiter((v.size for v in flat_vals), dtype=np.int64, count=nl)
+    idx_off = np.zeros(nl + 1, dtype=np.int64)
+    np.cumsum(ranks, out=idx_off[1:])
+    val_off = np.zeros(nl + 1, dtype=np.int64)
+    np.cumsum(sizes, out=val_off[1:])
+    leaf_val = np.concatenate(flat_vals).astype(np.float64, copy=False) if flat_vals else np.zeros(0)
+    domain = np.fromiter((ix.domain_size for ix in indices), dtype=np.int32, count=len(indices))
+    sort_rank = sort_ranks(indices) if with_sort_rank else np.arange(len(indices), dtype=np.int32)
 
-    nodes = _postorder_internal(t)
-    slot_of = {}
+    # internal nodes in reference postorder, iteratively (deep spines)
     left, right = [], []
-    nl = len(tensors)
+    slot_of = {}
     nxt = nl
-    for node in nodes:
-        if node.is_leaf:
-            s = leaf_slot.get(id(node.tensor))
-            if s is None:
-                s = -1  # not a network tensor: reported as PlanMismatch by the caller
-            slot_of[id(node)] = s
+    stack = [t]
+    seq = []
+    while stack:
+        node = stack.pop()
+        seq.append(node)
+        if node.tensor is None:
+            stack.append(node.left)
+            stack.append(node.right)
+    for node in reversed(seq):
+        if node.tensor is not None:
+            slot_of[id(node)] = leaf_slot.get(id(node.tensor), -1)
         else:
             left.append(slot_of[id(node.left)])
             right.append(slot_of[id(node.right)])
@@ -111,10 +107,10 @@ def flatten(n, t, index_table=None) -> FlatPlan:
         indices=indices,
         domain=domain,
         sort_rank=sort_rank,
-        leaf_idx_off=np.array(idx_off, dtype=np.int64),
+        leaf_idx_off=idx_off,
         leaf_idx=np.array(idx_list, dtype=np.int32),
-        leaf_val_off=np.array(val_off, dtype=np.int64),
-        leaf_val=np.concatenate(val_chunks) if val_chunks else np.zeros(0),
+        leaf_val_off=val_off,
+        leaf_val=leaf_val,
         left=np.array(left, dtype=np.int32),
         right=np.array(right, dtype=np.int32),
         root_slot=slot_of[id(t)],

@@ -38,8 +38,8 @@ class SlicedExecution:
     stats: dict = field(default=None, repr=False, compare=False)
 
 
-def _plan(n, t):
-    flat = flatten(n, t)
+def _plan(n, t, with_sort_rank=True):
+    flat = flatten(n, t, with_sort_rank=with_sort_rank)
     if flat.root_slot < 0 or (flat.left < 0).any() or (flat.right < 0).any():
         raise PlanMismatch("contraction tree leaves do not match the network")
     return flat, _lib.PlanHandle(flat)
@@ -70,7 +70,8 @@ def choose_slice_index(n, t, already=frozenset()):
 
 
 def _run(n, t, mem_budget=None, devices=None, slice_indices=None):
-    flat, h = _plan(n, t)
+    # sort_key ranks only matter to the greedy chooser (slicing.py:73-79)
+    flat, h = _plan(n, t, with_sort_rank=mem_budget is not None and slice_indices is None)
     sl = None if slice_indices is None else [flat.indices.index(ix) if ix in flat.indices else -1
                                              for ix in slice_indices]
     if sl is not None and any(k < 0 for k in sl):
