@@ -828,7 +828,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         const int m = (int)M.size(), n = (int)N.size(), kk = (int)K.size();
         // 128x64 CTA tiles (8 warps) for large GEMMs, 64x64 and below otherwise
         static const int big_tiles = std::getenv("TC_GEMM_BIG") ? std::atoi(std::getenv("TC_GEMM_BIG")) : 1;
-        static const int big_k = std::getenv("TC_GEMM_BIG_K") ? std::atoi(std::getenv("TC_GEMM_BIG_K")) : 8;
+        static const int big_k = std::getenv("TC_GEMM_BIG_K") ? std::atoi(std::getenv("TC_GEMM_BIG_K")) : 4;
         const bool big = big_tiles && m >= 7 && n >= 6 && kk >= big_k;
         const int MT = big ? 7 : std::max(3, std::min(6, m)), NT = std::max(3, std::min(6, n)), KT = 4;
         GemmParams gp{};

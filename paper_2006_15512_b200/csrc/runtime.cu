@@ -111,9 +111,8 @@ GemmVariant gv() {
 // tile bits (bm, bn) in [3, 6] -> kernel instantiation (warp grid chosen so
 // every warp owns >= 8x8)
 GemmVariant gemm_variant(int bm, int bn) {
-  static const int wide = std::getenv("TC_GEMM_W4") ? std::atoi(std::getenv("TC_GEMM_W4")) : 0;
   switch (bm * 8 + bn) {
-    case 7 * 8 + 6: return wide ? gv<128, 64, 2, 2>() : gv<128, 64, 4, 2>();
+    case 7 * 8 + 6: return gv<128, 64, 4, 2>();
     case 6 * 8 + 6: return gv<64, 64, 2, 2>();
     case 6 * 8 + 5: return gv<64, 32, 2, 2>();
     case 5 * 8 + 6: return gv<32, 64, 2, 2>();

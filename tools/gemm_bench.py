@@ -24,7 +24,9 @@ def one(m, n, k, reps=5):
     K = [Index(("k", i), 2) for i in range(k)]
     rng = np.random.default_rng(0)
     a = Tensor(tuple(M + K), rng.uniform(-1, 1, [2] * (m + k)))
-    b = Tensor(tuple(K + N), rng.uniform(-1, 1, [2] * (k + n)))
+    # both operands K-lowest (row-major M x K and N x K), the layouts the
+    # compiler's layout pass requests for GEMM operands
+    b = Tensor(tuple(N + K), rng.uniform(-1, 1, [2] * (n + k)))
     nw = TensorNetwork((a, b))
     fl = flatten(nw, join(leaf(a), leaf(b)))
     h = _lib.PlanHandle(fl)
@@ -36,7 +38,7 @@ def one(m, n, k, reps=5):
     # correctness spot check on the full result
     folded, _ = ex.fetch()
     A = torch.tensor(a.values.reshape(2 ** m, 2 ** k), device="cuda")
-    B = torch.tensor(b.values.reshape(2 ** k, 2 ** n), device="cuda")
+    B = torch.tensor(b.values.reshape(2 ** n, 2 ** k), device="cuda").t().contiguous()
     C = (A @ B).cpu().numpy().reshape(-1)
     err = float(np.max(np.abs(folded - C)) / max(1e-300, np.max(np.abs(C))))
     for _ in range(2):
