@@ -378,20 +378,21 @@ struct GemmCfg {
   static constexpr int WTM = BM / WGM, WTN = BN / WGN;
   static constexpr int FM = WTM / 8, FN = WTN / 8;
   static constexpr int ELA = (BM * GBK + NT - 1) / NT, ELB = (BN * GBK + NT - 1) / NT;
-  static constexpr int SMEM = GSTAGES * GBK * (LDA + LDB) * 8 > BM * LDC * 8 ? GSTAGES * GBK * (LDA + LDB) * 8
-                                                                               : BM * LDC * 8;
+  // 3 stages for the 4-warp tiles so 4 CTAs fit an SM (occupancy over depth)
+  static constexpr int ST = (WGM * WGN == 4) ? 3 : GSTAGES;
+  static constexpr int SMEM = ST * GBK * (LDA + LDB) * 8 > BM * LDC * 8 ? ST * GBK * (LDA + LDB) * 8 : BM * LDC * 8;
   static_assert(FM >= 1 && FN >= 1, "warp tile below 8x8");
 };
 
 template <int BM, int BN, int WGM, int WGN>
-__global__ void __launch_bounds__(32 * WGM * WGN, (WGM * WGN >= 8) ? 2 : ((WGM * WGN >= 4) ? 3 : 4))
+__global__ void __launch_bounds__(32 * WGM * WGN, (WGM * WGN >= 8) ? 2 : 4)
     k_gemm(const GemmParams p) {
   using Cfg = GemmCfg<BM, BN, WGM, WGN>;
   constexpr int NT = Cfg::NT, LDA = Cfg::LDA, LDB = Cfg::LDB, LDC = Cfg::LDC;
   constexpr int FM = Cfg::FM, FN = Cfg::FN, ELA = Cfg::ELA, ELB = Cfg::ELB;
   extern __shared__ __align__(16) double gsm[];
   double* As = gsm;
-  double* Bs = gsm + GSTAGES * GBK * LDA;
+  double* Bs = gsm + Cfg::ST * GBK * LDA;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / WGN, wn = warp % WGN;
 
@@ -437,10 +438,10 @@ __global__ void __launch_bounds__(32 * WGM * WGN, (WGM * WGN >= 8) ? 2 : ((WGM *
   // virtual elements are zero in every stage and never loaded
   for (int i = 0; i < ELA; ++i)
     if (tid + i * NT < BM * GBK && !(aok_t && ha_ok[i]))
-      for (int s = 0; s < GSTAGES; ++s) As[s * GBK * LDA + asx_t + ha_sx[i]] = 0.0;
+      for (int s = 0; s < Cfg::ST; ++s) As[s * GBK * LDA + asx_t + ha_sx[i]] = 0.0;
   for (int i = 0; i < ELB; ++i)
     if (tid + i * NT < BN * GBK && !(bok_t && hb_ok[i]))
-      for (int s = 0; s < GSTAGES; ++s) Bs[s * GBK * LDB + bsx_t + hb_sx[i]] = 0.0;
+      for (int s = 0; s < Cfg::ST; ++s) Bs[s * GBK * LDB + bsx_t + hb_sx[i]] = 0.0;
   const double* Ab = p.A + deposit(tm, p.a_m);
   const double* Bb = p.B + deposit(tn, p.b_n);
 
@@ -468,20 +469,20 @@ __global__ void __launch_bounds__(32 * WGM * WGN, (WGM * WGN >= 8) ? 2 : ((WGM *
     for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
-  for (int s = 0; s < GSTAGES - 1; ++s) {
+  for (int s = 0; s < Cfg::ST - 1; ++s) {
     if (s < nkt) load_stage(s, kt0 + s);
     cp_async_commit();
   }
   for (int64_t it = 0; it < nkt; ++it) {
-    cp_async_wait<GSTAGES - 2>();
+    cp_async_wait<Cfg::ST - 2>();
     __syncthreads();
     {
-      int64_t nk = it + GSTAGES - 1;
-      if (nk < nkt) load_stage((int)(nk % GSTAGES), kt0 + nk);
+      int64_t nk = it + Cfg::ST - 1;
+      if (nk < nkt) load_stage((int)(nk % Cfg::ST), kt0 + nk);
       cp_async_commit();
     }
-    const double* as = As + (it % GSTAGES) * GBK * LDA;
-    const double* bs = Bs + (it % GSTAGES) * GBK * LDB;
+    const double* as = As + (it % Cfg::ST) * GBK * LDA;
+    const double* bs = Bs + (it % Cfg::ST) * GBK * LDB;
 #pragma unroll
     for (int kk = 0; kk < GBK / 4; ++kk) {
       double af[FM], bf[FN];
