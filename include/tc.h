@@ -99,6 +99,9 @@ typedef struct tc_stats {
   tc_u128 alg_flops;             /* per slice: sum over nodes 2*prod(union)  */
   int32_t n_alias_nodes;         /* exact relabels (identity pieces): no launch */
   int32_t n_chain_launches;      /* fused chain launches                      */
+  double program_ms;             /* compile_ms split: host program compile    */
+  double setup_ms;               /*   device allocations + uploads            */
+  double graph_ms;               /*   CUDA graph build + instantiate          */
 } tc_stats;
 
 /* ---- symbolic plan (host) ---------------------------------------------- */
@@ -128,6 +131,11 @@ int tc_choose_slices(const tc_plan* plan, int64_t mem_budget, int32_t* chosen, i
  * tc_sliced_execute(slice_ids=...). */
 int tc_choose_slices_work(const tc_plan* plan, int32_t* chosen, int32_t n_already, int32_t cap,
                           int64_t max_entries, int32_t* n_chosen);
+
+/* Host-only: compile the program for a slice set without touching a device;
+ * fills the node-class counts, per-slice algorithmic bytes/flops, the memory
+ * model fields and program_ms (kernel classification is testable on CPU). */
+int tc_compile_stats(const tc_plan* plan, const int32_t* sliced, int32_t n_sliced, tc_stats* stats);
 
 /* Reference-order index list of the result (kept_a ++ kept_b recursively,
  * tensor.py:108), sliced indices removed.  *rank receives its length. */

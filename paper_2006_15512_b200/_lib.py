@@ -77,6 +77,9 @@ class Stats(C.Structure):
         ("alg_flops", U128),
         ("n_alias_nodes", C.c_int32),
         ("n_chain_launches", C.c_int32),
+        ("program_ms", C.c_double),
+        ("setup_ms", C.c_double),
+        ("graph_ms", C.c_double),
     ]
 
     def as_dict(self):
@@ -96,6 +99,9 @@ class Stats(C.Structure):
             alg_flops=self.alg_flops.value(),
             n_alias_nodes=int(self.n_alias_nodes),
             n_chain_launches=int(self.n_chain_launches),
+            program_ms=float(self.program_ms),
+            setup_ms=float(self.setup_ms),
+            graph_ms=float(self.graph_ms),
         )
 
 
@@ -109,6 +115,7 @@ SIGNATURES = {
     "tc_choose_slices": (C.c_int, [C.c_void_p, C.c_int64, I32P, C.c_int32, I32P, C.POINTER(U128)]),
     "tc_result_indices": (C.c_int, [C.c_void_p, I32P, C.c_int32, I32P, C.c_int32, I32P]),
     "tc_choose_slices_work": (C.c_int, [C.c_void_p, I32P, C.c_int32, C.c_int32, C.c_int64, I32P]),
+    "tc_compile_stats": (C.c_int, [C.c_void_p, I32P, C.c_int32, C.c_void_p]),
     "tc_exec_create": (C.c_int, [C.c_void_p, I32P, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
     "tc_exec_free": (None, [C.c_void_p]),
     "tc_exec_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(Stats)]),
@@ -234,6 +241,13 @@ class PlanHandle:
         out = C.c_int32()
         check(lib().tc_choose_slice_index(self.h, p, n, C.byref(out)))
         return int(out.value)
+
+    def compile_stats(self, sliced_ids=()) -> dict:
+        """Host-only program compile (no device): class counts, memory model."""
+        a, p, n = ids_ptr(sliced_ids)
+        st = Stats()
+        check(lib().tc_compile_stats(self.h, p, n, C.byref(st)))
+        return st.as_dict()
 
     def choose_slices_work(self, max_entries: int, already=()):
         """Work-aware slice set (extension): picks until every intermediate

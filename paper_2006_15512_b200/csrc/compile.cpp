@@ -18,6 +18,8 @@
 #include "compile.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <map>
 #include <cstdlib>
 #include <set>
@@ -114,6 +116,23 @@ struct Alloc {
   }
 };
 
+// linear-probe map for the small key sets of one node (layouts of rank <= ~64)
+template <class V>
+struct SmallMap {
+  std::vector<std::pair<int, V>> kv;
+  V& operator[](int k) {
+    for (auto& e : kv)
+      if (e.first == k) return e.second;
+    kv.push_back({k, V{}});
+    return kv.back().second;
+  }
+  size_t count(int k) const {
+    for (auto& e : kv)
+      if (e.first == k) return 1;
+    return 0;
+  }
+};
+
 BitRuns make_runs(const std::vector<std::pair<int, int>>& bits) {  // (src bit, dst bit), src ascending
   BitRuns r{};
   r.n = 0;
@@ -139,6 +158,18 @@ BitRuns make_runs(const std::vector<std::pair<int, int>>& bits) {  // (src bit, 
 
 Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_t no_reuse_limit) {
   Program g;
+  // section timings to stderr when TC_COMPILE_TIMING is set (diagnostics)
+  static const bool timing = std::getenv("TC_COMPILE_TIMING") != nullptr;
+  auto tlast = std::chrono::steady_clock::now();
+  std::string prev = "start";
+  auto tmark = [&](const char* name) {
+    if (!timing) return;
+    auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[compile] %-22s %8.2f ms\n", prev.c_str(),
+                 std::chrono::duration<double, std::milli>(now - tlast).count());
+    tlast = now;
+    prev = name;
+  };
   const int S = p.nslots();
   std::vector<char> drop(p.NI, 0);
   for (int i : chosen_in) {
@@ -157,6 +188,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   g.mem_estimate = mem_cost(p, drop);
   g.peak_observed = tracked_peak(p, drop);
 
+  tmark("effective sets / siz");
   // ---- effective sets / sizes ------------------------------------------------
   std::vector<std::vector<int>> eff(S);
   std::vector<int64_t> size(S);
@@ -186,6 +218,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   };
   auto has = [](const std::vector<int>& s, int i) { return std::binary_search(s.begin(), s.end(), i); };
 
+  tmark("classification");
   // ---- classification --------------------------------------------------------
   g.cls.assign(S, NC_LEAF);
   auto all2 = [&](int s) {
@@ -215,6 +248,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     g.cls[v] = c;
   }
 
+  tmark("layouts (top-down)");
   // ---- layouts (top-down) ----------------------------------------------------
   g.layout.assign(S, {});
   std::vector<char> have(S, 0);
@@ -288,6 +322,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     }
   }
 
+  tmark("exact relabels");
   // ---- exact relabels ---------------------------------------------------------
   // big x (2x2 identity) piece: C[.., f, ..] = sum_s A[.., s, ..] I[s, f] is A
   // with index s renamed f (x*1 + y*0 == x for finite y, bit for bit).  The
@@ -319,6 +354,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     }
   }
 
+  tmark("chain segments");
   // ---- chain segments: runs of STREAM nodes fused into one launch -----------
   // v_{i+1}'s big operand is v_i.  Inner bits = every index of the input the
   // segment touches plus the ones it creates; all must fit kChainU at every
@@ -381,6 +417,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     segs.push_back(sg);
   }
 
+  tmark("leaves");
   // ---- leaves: plain or per-slice selected ----------------------------------
   g.loc.assign(S, Loc{LOC_LEAF, 0});
   std::vector<int64_t> pv(g.chosen.size(), 1);
@@ -425,6 +462,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     g.sliced_doubles += size[l];
   }
 
+  tmark("tiny groups");
   // ---- tiny groups -------------------------------------------------------------
   std::vector<char> forced(S, 0);
   std::vector<std::vector<int>> groups;  // internal slots, postorder
@@ -454,7 +492,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       // smem first-fit simulation
       std::map<int32_t, int32_t> fr;  // off -> size (doubles)
       int32_t top = 0;
-      std::map<int, int32_t> off;
+      SmallMap<int32_t> off;
       auto salloc = [&](int32_t n) {
         n = (n + 1) & ~1;  // 16-byte aligned
         for (auto it = fr.begin(); it != fr.end(); ++it)
@@ -526,6 +564,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     nlevels = std::max(nlevels, glevel[gi] + 1);
   }
 
+  tmark("steps + arena");
   // ---- steps + arena --------------------------------------------------------
   Alloc arena;
   {
@@ -651,14 +690,14 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         const auto& Lb = g.layout[b];
         const auto& Lc = g.layout[v];
         std::vector<int64_t> sa(p.NI > 0 ? 0 : 0);
-        auto strides = [&](const std::vector<int>& L, std::map<int, int64_t>& m) {
+        auto strides = [&](const std::vector<int>& L, SmallMap<int64_t>& m) {
           int64_t st2 = 1;
           for (int i : L) {
             m[i] = st2;
             st2 *= p.dom[i];
           }
         };
-        std::map<int, int64_t> ma, mb;
+        SmallMap<int64_t> ma, mb;
         strides(La, ma);
         strides(Lb, mb);
         tn.dig = (int32_t)g.tiny_digits.size();
@@ -705,9 +744,10 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     g.steps[tiny_step[lv]].work = level_range[lv].second - level_range[lv].first;
   }
 
+  tmark("big nodes in postord");
   // big nodes in postorder
   auto stride_map = [&](const std::vector<int>& L) {
-    std::map<int, int64_t> m;
+    SmallMap<int64_t> m;
     int64_t st2 = 1;
     for (int i : L) {
       m[i] = st2;
@@ -752,7 +792,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         const auto& Lq = g.layout[sm];
         std::vector<int> Sh = inter(eff[a], eff[b]);
         std::vector<int> F = minus(eff[sm], Sh);
-        std::map<int, int> pg, pc, pq;
+        SmallMap<int> pg, pc, pq;
         for (size_t q = 0; q < Lg.size(); ++q) pg[Lg[q]] = (int)q;
         for (size_t q = 0; q < Lc.size(); ++q) pc[Lc[q]] = (int)q;
         for (size_t q = 0; q < Lq.size(); ++q) pq[Lq[q]] = (int)q;
@@ -818,7 +858,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       try {
         std::vector<int> K = inter(eff[a], eff[b]);
         std::vector<int> M = minus(eff[a], K), N = minus(eff[b], K);
-        std::map<int, int> pa, pb, pc;
+        SmallMap<int> pa, pb, pc;
         for (size_t q = 0; q < La.size(); ++q) pa[La[q]] = (int)q;
         for (size_t q = 0; q < Lb.size(); ++q) pb[Lb[q]] = (int)q;
         for (size_t q = 0; q < Lc.size(); ++q) pc[Lc[q]] = (int)q;
@@ -854,7 +894,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         r.clear();
         for (int t = NT; t < (int)N.size(); ++t) r.push_back({t - NT, pc[N[t]]});
         gp.c_n = make_runs(r);
-        auto tmap = [&](std::map<int, int>& P, const std::vector<int>& R1, int n1,
+        auto tmap = [&](SmallMap<int>& P, const std::vector<int>& R1, int n1,
                         const std::vector<int>& R2, int n2) {
           // R1 tile bits -> kind 0, R2 tile bits -> kind 1; bits past the
           // shape are virtual (pos -1), placed after the real ones
@@ -960,7 +1000,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     const int A = sg.big.front();
     const auto& La = g.layout[A];
     const auto& Lc = g.layout[vk];
-    std::map<int, int> pa, pc;
+    SmallMap<int> pa, pc;
     for (size_t q = 0; q < La.size(); ++q) pa[La[q]] = (int)q;
     for (size_t q = 0; q < Lc.size(); ++q) pc[Lc[q]] = (int)q;
     // inner bookkeeping
@@ -971,7 +1011,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       std::vector<int> Sh = inter(eff[bg], eff[sm]);
       std::vector<int> F = minus(eff[sm], Sh);
       const auto& Lq = g.layout[sm];
-      std::map<int, int> pq;
+      SmallMap<int> pq;
       for (size_t q = 0; q < Lq.size(); ++q) pq[Lq[q]] = (int)q;
       std::vector<int> nw;
       for (int x : cur)
@@ -1042,7 +1082,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       if (e.status != -1) throw;
       return false;
     }
-    auto tmap = [&](std::map<int, int>& P, const std::vector<int>& inner) {
+    auto tmap = [&](SmallMap<int>& P, const std::vector<int>& inner) {
       std::vector<std::tuple<int, int, int>> bits;
       for (int j = 0; j < xt; ++j) bits.emplace_back(P[O[j]], 0, j);
       for (size_t t = 0; t < inner.size(); ++t) bits.emplace_back(P[inner[t]], 1, (int)t);
@@ -1118,6 +1158,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     emit_node(v);
   }
 
+  tmark("root copy into the p");
   // root copy into the per-slice result slot, then advance the slice counter
   g.R = size[p.root];
   g.root_loc = g.loc[p.root];
@@ -1132,6 +1173,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   et.deps.push_back(rcs);
   if (sel_step >= 0) et.deps.push_back(sel_step);
   g.steps.push_back(et);
+  tmark("end");
   g.arena_bytes = std::max<int64_t>(arena.top, kAlign);
   for (auto& s : g.steps) {
     std::sort(s.deps.begin(), s.deps.end());

@@ -17,6 +17,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -76,13 +77,73 @@ std::string u128_str(u128 v) {
   return std::string(s.rbegin(), s.rend());
 }
 
+// Process-wide caching device allocator: programs are built per call of the
+// public API, so freed buffers go back to a per-device free list instead of
+// cudaFree (a 1.6 GB cudaMalloc/cudaFree pair costs ~10-100 ms).  On OOM the
+// cache of that device is released and the allocation retried once.
+struct DevCache {
+  std::mutex mu;
+  std::vector<std::multimap<size_t, void*>> free_;
+  static size_t round(size_t b) { return (std::max<size_t>(b, 256) + 511) & ~(size_t)511; }
+  void* get(int dev, size_t bytes) {
+    bytes = round(bytes);
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      if ((int)free_.size() > dev) {
+        auto& f = free_[dev];
+        auto it = f.lower_bound(bytes);
+        if (it != f.end() && it->first <= 2 * bytes + ((size_t)1 << 20)) {
+          void* p = it->second;
+          f.erase(it);
+          sizes_[p] = bytes;  // reported size: the request
+          return p;
+        }
+      }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      release(dev);
+      e = cudaMalloc(&p, bytes);
+    }
+    if (e != cudaSuccess) {
+      int st = (e == cudaErrorMemoryAllocation) ? TC_OOM : TC_CUDA;
+      throw Error{st, std::string("cudaMalloc: ") + cudaGetErrorString(e)};
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    real_[p] = bytes;
+    sizes_[p] = bytes;
+    return p;
+  }
+  void put(int dev, void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(mu);
+    if ((int)free_.size() <= dev) free_.resize(dev + 1);
+    free_[dev].emplace(real_[p], p);
+  }
+  void release(int dev) {
+    std::lock_guard<std::mutex> lk(mu);
+    if ((int)free_.size() <= dev) return;
+    for (auto& kv : free_[dev]) {
+      cudaFree(kv.second);
+      real_.erase(kv.second);
+      sizes_.erase(kv.second);
+    }
+    free_[dev].clear();
+  }
+  std::map<void*, size_t> real_, sizes_;
+};
+DevCache& dcache() {
+  static DevCache c;
+  return c;
+}
+
 template <class T>
-T* dalloc(size_t n, int64_t& total) {
-  T* p = nullptr;
+T* dalloc(size_t n, int64_t& total, int dev) {
   size_t b = std::max<size_t>(n * sizeof(T), 16);
-  CU(cudaMalloc(&p, b));
   total += (int64_t)b;
-  return p;
+  return (T*)dcache().get(dev, b);
 }
 
 using StreamFn = void (*)(StreamParams);
@@ -210,10 +271,11 @@ struct tc_exec {
     if (device >= 0) cudaSetDevice(device);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
+    if (stream) cudaStreamSynchronize(stream);
     for (void* q : {(void*)arena, (void*)leafbuf, (void*)slicedbuf, (void*)tnodes, (void*)tdigs,
                     (void*)tgroups, (void*)gdig, (void*)chains, (void*)sel, (void*)selt, (void*)eta, (void*)results,
                     (void*)folded})
-      if (q) cudaFree(q);
+      dcache().put(device, q);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -229,22 +291,21 @@ struct tc_exec {
   void build(const Plan& p, const std::vector<int>& chosen) {
     auto t0 = std::chrono::steady_clock::now();
     CU(cudaSetDevice(device));
-    size_t free_b = 0, total_b = 0;
-    CU(cudaMemGetInfo(&free_b, &total_b));
     // Reuse-free arenas only on request (TC_ARENA_REUSE=0): the factored trees
     // are spines (C2: 2434 of 2918 launches on the critical path even without
     // write-after-read edges) and mapping a 45 GB arena costs ~200 ms per call.
     prog = compile_program(p, chosen, 0);
-    (void)free_b;
+    auto t_prog = std::chrono::steady_clock::now();
+    program_ms = std::chrono::duration<double, std::milli>(t_prog - t0).count();
     CU(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     Program& g = prog;
-    arena = dalloc<char>((size_t)g.arena_bytes, dev_bytes);
-    leafbuf = dalloc<double>(p.lval.size(), dev_bytes);
+    arena = dalloc<char>((size_t)g.arena_bytes, dev_bytes, device);
+    leafbuf = dalloc<double>(p.lval.size(), dev_bytes, device);
     CU(cudaMemcpyAsync(leafbuf, p.lval.data(), p.lval.size() * 8, cudaMemcpyHostToDevice, stream));
-    if (g.sliced_doubles) slicedbuf = dalloc<double>((size_t)g.sliced_doubles, dev_bytes);
+    if (g.sliced_doubles) slicedbuf = dalloc<double>((size_t)g.sliced_doubles, dev_bytes, device);
     if (!g.sel_ent.empty()) {
-      sel = dalloc<SelEntry>(g.sel_ent.size(), dev_bytes);
-      selt = dalloc<SelTerm>(std::max<size_t>(1, g.sel_terms.size()), dev_bytes);
+      sel = dalloc<SelEntry>(g.sel_ent.size(), dev_bytes, device);
+      selt = dalloc<SelTerm>(std::max<size_t>(1, g.sel_terms.size()), dev_bytes, device);
       CU(cudaMemcpyAsync(sel, g.sel_ent.data(), g.sel_ent.size() * sizeof(SelEntry), cudaMemcpyHostToDevice, stream));
       if (!g.sel_terms.empty())
         CU(cudaMemcpyAsync(selt, g.sel_terms.data(), g.sel_terms.size() * sizeof(SelTerm), cudaMemcpyHostToDevice,
@@ -257,9 +318,9 @@ struct tc_exec {
         tn[i].gb = ptr(g.tiny_gb[i]);
         tn[i].gout = (double*)ptr(g.tiny_gout[i]);
       }
-      tnodes = dalloc<TinyNode>(tn.size(), dev_bytes);
-      tdigs = dalloc<TinyDigit>(std::max<size_t>(1, g.tiny_digits.size()), dev_bytes);
-      tgroups = dalloc<TinyGroup>(g.tiny_groups.size(), dev_bytes);
+      tnodes = dalloc<TinyNode>(tn.size(), dev_bytes, device);
+      tdigs = dalloc<TinyDigit>(std::max<size_t>(1, g.tiny_digits.size()), dev_bytes, device);
+      tgroups = dalloc<TinyGroup>(g.tiny_groups.size(), dev_bytes, device);
       CU(cudaMemcpyAsync(tnodes, tn.data(), tn.size() * sizeof(TinyNode), cudaMemcpyHostToDevice, stream));
       if (!g.tiny_digits.empty())
         CU(cudaMemcpyAsync(tdigs, g.tiny_digits.data(), g.tiny_digits.size() * sizeof(TinyDigit),
@@ -270,16 +331,16 @@ struct tc_exec {
     if (!g.chain_steps.empty()) {
       std::vector<ChainStep> cs = g.chain_steps;
       for (size_t i = 0; i < cs.size(); ++i) cs[i].P = ptr(g.chain_piece[i]);
-      chains = dalloc<ChainStep>(cs.size(), dev_bytes);
+      chains = dalloc<ChainStep>(cs.size(), dev_bytes, device);
       CU(cudaMemcpyAsync(chains, cs.data(), cs.size() * sizeof(ChainStep), cudaMemcpyHostToDevice, stream));
       CU(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, chain_smem(kChainMax)));
     }
     if (!g.gdigits.empty()) {
-      gdig = dalloc<GDigit>(g.gdigits.size(), dev_bytes);
+      gdig = dalloc<GDigit>(g.gdigits.size(), dev_bytes, device);
       CU(cudaMemcpyAsync(gdig, g.gdigits.data(), g.gdigits.size() * sizeof(GDigit), cudaMemcpyHostToDevice, stream));
     }
-    eta = dalloc<int64_t>(2, dev_bytes);
-    folded = dalloc<double>((size_t)g.R, dev_bytes);
+    eta = dalloc<int64_t>(2, dev_bytes, device);
+    folded = dalloc<double>((size_t)g.R, dev_bytes, device);
     CU(cudaStreamSynchronize(stream));
 
     const int tiny_smem = (int)(g.tiny_smem_doubles + kTinyThreads) * 8;
@@ -401,6 +462,20 @@ struct tc_exec {
       }
       launches.push_back(std::move(L));
     }
+    auto t_end = std::chrono::steady_clock::now();
+    setup_ms = std::chrono::duration<double, std::milli>(t_end - t_prog).count();
+    compile_ms = std::chrono::duration<double, std::milli>(t_end - t0).count();
+    kernels_per_slice = (int64_t)launches.size();
+  }
+
+  // The CUDA graph (one kernel node per step, edges = data + WAR deps) is
+  // built on the first run that replays the program more than twice; one-shot
+  // calls launch the steps eagerly on the stream (graph build + instantiate of
+  // ~900 nodes costs ~13 ms, more than the launches it saves).
+  void ensure_graph() {
+    if (gexec) return;
+    Program& g = prog;
+    auto t_graph0 = std::chrono::steady_clock::now();
     CU(cudaGraphCreate(&graph, 0));
     std::vector<cudaGraphNode_t> nodes(g.steps.size());
     kernels_per_slice = 0;
@@ -413,18 +488,19 @@ struct tc_exec {
     }
     rootcopy_node = nodes[rootcopy_launch];
     CU(cudaGraphInstantiate(&gexec, graph, 0));
-    compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    graph_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_graph0).count();
   }
+  double program_ms = 0, setup_ms = 0, graph_ms = 0;
 
   cudaGraphNode_t rootcopy_node = nullptr;
   int rootcopy_launch = -1;
 
   void ensure_results(int64_t n) {
     if (n <= results_cap) return;
-    if (results) CU(cudaFree(results));
+    if (results) dcache().put(device, results);
     results = nullptr;
     int64_t dummy = 0;
-    results = dalloc<double>((size_t)(n * prog.R), dummy);
+    results = dalloc<double>((size_t)(n * prog.R), dummy, device);
     results_cap = n;
     // patch the root-copy node with the new results pointer
     Launch& L = launches[rootcopy_launch];
@@ -432,8 +508,18 @@ struct tc_exec {
     std::memcpy(&rp, L.blob.data(), sizeof(rp));
     rp.results = results;
     std::memcpy(L.blob.data(), &rp, sizeof(rp));
-    cudaKernelNodeParams kp = L.params();
-    CU(cudaGraphExecKernelNodeSetParams(gexec, rootcopy_node, &kp));
+    if (gexec) {
+      cudaKernelNodeParams kp = L.params();
+      CU(cudaGraphExecKernelNodeSetParams(gexec, rootcopy_node, &kp));
+    }
+  }
+
+  // one slice in step order on the stream (no graph)
+  void launch_eager() {
+    for (auto& L : launches) {
+      auto kp = L.params();
+      CU(cudaLaunchKernel(L.func, L.grid, L.block, kp.kernelParams, L.smem, stream));
+    }
   }
 
   // Eager replay of one slice, one kernel at a time, timed per launch with
@@ -468,6 +554,8 @@ struct tc_exec {
       return 0.0;
     }
     ensure_results(n);
+    const bool eager = !gexec && n * repeats <= 2;
+    if (!eager) ensure_graph();
     int64_t h[2] = {b, b};
     cudaEvent_t e0, e1;
     CU(cudaEventCreate(&e0));
@@ -477,7 +565,10 @@ struct tc_exec {
     CU(cudaEventRecord(e0, stream));
     for (int64_t r = 0; r < repeats; ++r) {
       if (r > 0) k_eta_reset<<<1, 1, 0, stream>>>(eta);
-      for (int64_t s = 0; s < n; ++s) CU(cudaGraphLaunch(gexec, stream));
+      for (int64_t s = 0; s < n; ++s) {
+        if (eager) launch_eager();
+        else CU(cudaGraphLaunch(gexec, stream));
+      }
     }
     CU(cudaEventRecord(e1, stream));
     CU(cudaEventSynchronize(e1));
@@ -629,6 +720,30 @@ int tc_choose_slices_work(const tc_plan* plan, int32_t* chosen, int32_t n_alread
   });
 }
 
+int tc_compile_stats(const tc_plan* plan, const int32_t* sliced, int32_t n_sliced, tc_stats* s) {
+  return guard([&] {
+    std::vector<int> ch(sliced, sliced + std::max(0, n_sliced));
+    auto t0 = std::chrono::steady_clock::now();
+    Program g = compile_program(plan->p, ch, 0);
+    double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    *s = tc_stats{};
+    s->mem_estimate = to_abi(g.mem_estimate);
+    s->peak_observed = to_abi(g.peak_observed);
+    s->num_slices = g.num_slices;
+    s->device_peak_bytes = g.arena_bytes;
+    s->gpu_launches = (int64_t)g.steps.size();
+    s->n_tiny_nodes = g.n_tiny;
+    s->n_stream_nodes = g.n_stream;
+    s->n_gemm_nodes = g.n_gemm;
+    s->n_generic_nodes = g.n_generic;
+    s->alg_bytes = to_abi(g.alg_bytes);
+    s->alg_flops = to_abi(g.alg_flops);
+    s->n_alias_nodes = g.n_alias;
+    s->n_chain_launches = g.n_chain;
+    s->program_ms = ms;
+  });
+}
+
 int tc_result_indices(const tc_plan* plan, const int32_t* sliced, int32_t n_sliced, int32_t* out_idx, int32_t cap,
                       int32_t* rank) {
   return guard([&] {
@@ -676,6 +791,9 @@ static void fill_stats(const tc_exec& ex, double ms, tc_stats* s) {
   s->alg_flops = to_abi(g.alg_flops);
   s->n_alias_nodes = g.n_alias;
   s->n_chain_launches = g.n_chain;
+  s->program_ms = ex.program_ms;
+  s->setup_ms = ex.setup_ms;
+  s->graph_ms = ex.graph_ms;
 }
 
 int tc_exec_run(tc_exec* ex, int64_t slice_begin, int64_t slice_end, tc_stats* stats) {
@@ -841,7 +959,7 @@ int tc_sliced_execute(const tc_plan* plan, int64_t mem_budget, const int32_t* sl
       for (int gi = 0; gi < G; ++gi) {
         CU(cudaSetDevice(devs[gi]));
         int64_t dummy = 0;
-        full[gi] = dalloc<double>((size_t)(NS * R), dummy);
+        full[gi] = dalloc<double>((size_t)(NS * R), dummy, devs[gi]);
         CU(cudaMemsetAsync(full[gi], 0, NS * R * 8, ex[gi]->stream));
         int64_t b = std::min<int64_t>(NS, gi * per);
         if (ex[gi]->last_n > 0)
@@ -863,7 +981,7 @@ int tc_sliced_execute(const tc_plan* plan, int64_t mem_budget, const int32_t* sl
       CU(cudaStreamSynchronize(e0.stream));
       for (int gi = 0; gi < G; ++gi) {
         cudaSetDevice(devs[gi]);
-        cudaFree(full[gi]);
+        dcache().put(devs[gi], full[gi]);
         if (nc.CommDestroy) nc.CommDestroy(comms[gi]);
       }
     }
