@@ -17,6 +17,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib", "libtc.so")
+FLAT_SRC = os.path.join(CSRC, "flatten_ext.c")
 
 SOURCES = ["plan.cpp", "compile.cpp", "runtime.cu"]
 HEADERS = ["plan.hpp", "compile.hpp", "program.h", "kernels.cuh"]
@@ -37,7 +38,31 @@ def _stale(out, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def flat_ext_path() -> str:
+    import sysconfig
+
+    return os.path.join(PKG, "lib", "_tcflat" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_flat_ext(force: bool = False, verbose: bool = False) -> str:
+    """The native host-side flattener (CPython C API, gcc): _tcflat.*.so."""
+    import sysconfig
+
+    out = flat_ext_path()
+    if not force and not _stale(out, [FLAT_SRC, os.path.abspath(__file__)]):
+        return out
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC", "-std=c11", "-Wall",
+           "-I", sysconfig.get_paths()["include"], FLAT_SRC, "-o", out + ".tmp"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    os.replace(out + ".tmp", out)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_flat_ext(force=force, verbose=verbose)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "tc.h"))
     deps.append(os.path.abspath(__file__))

@@ -133,6 +133,48 @@ struct SmallMap {
   }
 };
 
+// first-fit shared-memory allocator of one tiny group (doubles, 16-byte
+// granules): lowest-offset free block that fits, coalescing frees, top trim
+struct SmemFit {
+  std::vector<std::pair<int32_t, int32_t>> fr;  // sorted (off, size)
+  int32_t top = 0;
+  void reset() {
+    fr.clear();
+    top = 0;
+  }
+  int32_t alloc(int32_t n) {
+    n = (n + 1) & ~1;
+    for (size_t q = 0; q < fr.size(); ++q)
+      if (fr[q].second >= n) {
+        const int32_t o = fr[q].first, rest = fr[q].second - n;
+        if (rest) fr[q] = {o + n, rest};
+        else fr.erase(fr.begin() + q);
+        return o;
+      }
+    const int32_t o = top;
+    top += n;
+    return o;
+  }
+  void free(int32_t o, int32_t n) {
+    n = (n + 1) & ~1;
+    auto it = std::lower_bound(fr.begin(), fr.end(), std::make_pair(o, (int32_t)0));
+    it = fr.insert(it, {o, n});
+    size_t q = (size_t)(it - fr.begin());
+    if (q + 1 < fr.size() && fr[q + 1].first == o + fr[q].second) {
+      fr[q].second += fr[q + 1].second;
+      fr.erase(fr.begin() + q + 1);
+    }
+    if (q > 0 && fr[q - 1].first + fr[q - 1].second == fr[q].first) {
+      fr[q - 1].second += fr[q].second;
+      fr.erase(fr.begin() + q);
+    }
+    if (!fr.empty() && fr.back().first + fr.back().second == top) {
+      top = fr.back().first;
+      fr.pop_back();
+    }
+  }
+};
+
 BitRuns make_runs(const std::vector<std::pair<int, int>>& bits) {  // (src bit, dst bit), src ascending
   BitRuns r{};
   r.n = 0;
@@ -190,11 +232,34 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
 
   tmark("effective sets / siz");
   // ---- effective sets / sizes ------------------------------------------------
-  std::vector<std::vector<int>> eff(S);
+  // eff[s]: the slot's index set without the sliced indices (a view of
+  // p.sets when the slot holds none of them)
+  std::vector<std::vector<int>> eff_own;
+  std::vector<const std::vector<int>*> effp(S);
+  {
+    std::vector<int> own_of(S, -1);
+    for (int s = 0; s < S; ++s) {
+      bool any = false;
+      for (int i : p.sets[s]) any |= (bool)drop[i];
+      if (any) own_of[s] = (int)eff_own.size(), eff_own.emplace_back();
+    }
+    for (int s = 0; s < S; ++s) {
+      if (own_of[s] < 0) {
+        effp[s] = &p.sets[s];
+        continue;
+      }
+      auto& e = eff_own[own_of[s]];
+      for (int i : p.sets[s])
+        if (!drop[i]) e.push_back(i);
+      effp[s] = &e;
+    }
+  }
+  struct EffView {
+    const std::vector<const std::vector<int>*>* v;
+    const std::vector<int>& operator[](int s) const { return *(*v)[s]; }
+  } eff{&effp};
   std::vector<int64_t> size(S);
   for (int s = 0; s < S; ++s) {
-    for (int i : p.sets[s])
-      if (!drop[i]) eff[s].push_back(i);
     u128 z = set_bytes(p, eff[s], drop) / 8;
     if (z > ((u128)1 << 50)) fail(TC_OOM, "intermediate tensor larger than 2^50 entries");
     size[s] = (int64_t)z;
@@ -202,6 +267,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   auto natural = [&](int s) {
     std::vector<int> o;
     const auto& ro = p.ref_order[s];
+    o.reserve(ro.size());
     for (auto it = ro.rbegin(); it != ro.rend(); ++it)
       if (!drop[*it]) o.push_back(*it);
     return o;
@@ -292,7 +358,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         }
         while (si < Sh.size()) Lg.push_back(Sh[si++]);
         want(big, Lg);
-        want(sm, natural(sm));
+        if (!p.is_leaf(sm)) want(sm, natural(sm));
         break;
       }
       case NC_GEMM: {
@@ -317,8 +383,8 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         break;
       }
       default:
-        want(a, natural(a));
-        want(b, natural(b));
+        if (!p.is_leaf(a)) want(a, natural(a));
+        if (!p.is_leaf(b)) want(b, natural(b));
     }
   }
 
@@ -472,86 +538,67 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   auto is_troot = [&](int s) {
     return is_tiny(s) && (forced[s] || p.parent[s] < 0 || !is_tiny(p.parent[s]));
   };
-  for (int iter = 0;; ++iter) {
-    groups.clear();
-    group_smem.clear();
-    std::fill(group_of.begin(), group_of.end(), -1);
-    bool split = false;
-    for (int k = 0; k < p.NN; ++k) {
-      int r = p.NL + k;
-      if (!is_troot(r)) continue;
-      std::vector<int> nodes, st{r};
-      while (!st.empty()) {
-        int v = st.back();
-        st.pop_back();
-        nodes.push_back(v);
-        for (int c : {p.kid_l(v), p.kid_r(v)})
-          if (is_tiny(c) && !is_troot(c)) st.push_back(c);
-      }
-      std::sort(nodes.begin(), nodes.end());
-      // smem first-fit simulation
-      std::map<int32_t, int32_t> fr;  // off -> size (doubles)
-      int32_t top = 0;
-      SmallMap<int32_t> off;
-      auto salloc = [&](int32_t n) {
-        n = (n + 1) & ~1;  // 16-byte aligned
-        for (auto it = fr.begin(); it != fr.end(); ++it)
-          if (it->second >= n) {
-            int32_t o = it->first, rest = it->second - n;
-            fr.erase(it);
-            if (rest) fr[o + n] = rest;
-            return o;
+  // Each group root r collects its tiny subtree (stopping at other roots) and
+  // simulates first-fit smem in postorder; a group over the smem cap forces
+  // r's tiny children to be roots and is re-collected (a group's node set
+  // changes only through its own overflow, so a worklist reaches the same
+  // fixpoint as re-grouping the whole forest).  Offsets are kept for the
+  // descriptor pass below.
+  std::vector<int32_t> soff(S, -1);  // smem offset of a non-root tiny node
+  {
+    std::vector<std::pair<int, int32_t>> done;  // (root, peak)
+    std::vector<std::vector<int>> gnodes;
+    std::vector<int> work, nodes, st;
+    SmemFit fit;
+    for (int k = 0; k < p.NN; ++k)
+      if (is_troot(p.NL + k)) work.push_back(p.NL + k);
+    while (!work.empty()) {
+      const int r = work.back();
+      work.pop_back();
+      for (;;) {
+        nodes.clear();
+        st.assign(1, r);
+        while (!st.empty()) {
+          int v = st.back();
+          st.pop_back();
+          nodes.push_back(v);
+          for (int c : {p.kid_l(v), p.kid_r(v)})
+            if (is_tiny(c) && !is_troot(c)) st.push_back(c);
+        }
+        std::sort(nodes.begin(), nodes.end());
+        fit.reset();
+        int32_t peak = 0;
+        for (int v : nodes) {
+          if (v != r) {
+            soff[v] = fit.alloc((int32_t)size[v]);
+            peak = std::max(peak, fit.top);
           }
-        int32_t o = top;
-        top += n;
-        return o;
-      };
-      auto sfree = [&](int32_t o, int32_t n) {
-        n = (n + 1) & ~1;
-        fr[o] = n;
-        // coalesce
-        auto it = fr.find(o);
-        auto nx = std::next(it);
-        if (nx != fr.end() && nx->first == o + it->second) {
-          it->second += nx->second;
-          fr.erase(nx);
+          for (int c : {p.kid_l(v), p.kid_r(v)})
+            if (c != r && is_tiny(c) && !is_troot(c)) fit.free(soff[c], (int32_t)size[c]);
         }
-        if (it != fr.begin()) {
-          auto pv2 = std::prev(it);
-          if (pv2->first + pv2->second == it->first) {
-            pv2->second += it->second;
-            fr.erase(it);
-          }
+        if (peak > kTinySmemCap) {
+          if (!is_tiny(p.kid_l(r)) && !is_tiny(p.kid_r(r))) fail(TC_BAD_ARG, "tiny split failed");
+          for (int c : {p.kid_l(r), p.kid_r(r)})
+            if (is_tiny(c) && !forced[c]) {
+              forced[c] = 1;
+              work.push_back(c);
+            }
+          continue;
         }
-        if (!fr.empty()) {
-          auto last = std::prev(fr.end());
-          if (last->first + last->second == top) {
-            top = last->first;
-            fr.erase(last);
-          }
-        }
-      };
-      int32_t peak = 0;
-      for (int v : nodes) {
-        if (v != r) {
-          off[v] = salloc((int32_t)size[v]);
-          peak = std::max(peak, top);
-        }
-        for (int c : {p.kid_l(v), p.kid_r(v)})
-          if (off.count(c)) sfree(off[c], (int32_t)size[c]);
+        done.push_back({r, peak});
+        gnodes.push_back(nodes);
+        break;
       }
-      if (peak > kTinySmemCap) {
-        split = true;
-        for (int c : {p.kid_l(r), p.kid_r(r)})
-          if (is_tiny(c)) forced[c] = 1;
-        if (!is_tiny(p.kid_l(r)) && !is_tiny(p.kid_r(r))) fail(TC_BAD_ARG, "tiny split failed");
-      }
-      for (int v : nodes) group_of[v] = (int)groups.size();
-      groups.push_back(nodes);
-      group_smem.push_back(peak);
     }
-    if (!split) break;
-    if (iter > 64) fail(TC_BAD_ARG, "tiny grouping did not converge");
+    // groups in postorder of their roots
+    std::vector<int> ord(done.size());
+    for (size_t q = 0; q < ord.size(); ++q) ord[q] = (int)q;
+    std::sort(ord.begin(), ord.end(), [&](int x, int y) { return done[x].first < done[y].first; });
+    for (int q : ord) {
+      for (int v : gnodes[q]) group_of[v] = (int)groups.size();
+      groups.push_back(std::move(gnodes[q]));
+      group_smem.push_back(done[q].second);
+    }
   }
   // group levels: a group consuming a forced root of another group runs later
   std::vector<int> glevel(groups.size(), 0);
@@ -582,6 +629,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     const char* env = std::getenv("TC_ARENA_REUSE");
     arena.no_reuse = env ? std::atoi(env) == 0 : total <= no_reuse_limit;
   }
+  tmark("arena policy");
   std::vector<int> producer(S, -1);
   int sel_step = -1;
   if (!g.sel_ent.empty()) {
@@ -610,8 +658,9 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     tiny_step[lv] = (int)g.steps.size();
     g.steps.push_back(st);
   }
+  tmark("tiny descriptors");
   // tiny descriptors, ordered by level then group
-  std::vector<int> smem_off(S, -1);
+  std::vector<int64_t> str_a(p.NI, 0), str_b(p.NI, 0);  // index -> stride (0: absent)
   std::vector<std::vector<int>> level_groups(nlevels);
   for (size_t gi = 0; gi < groups.size(); ++gi) level_groups[glevel[gi]].push_back((int)gi);
   std::vector<std::pair<int32_t, int32_t>> level_range(nlevels);
@@ -620,56 +669,15 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     for (int gi : level_groups[lv]) {
       const auto& nodes = groups[gi];
       int r = nodes.back();
-      // smem offsets again (same simulation as above, deterministic)
-      std::map<int32_t, int32_t> fr;
-      int32_t top = 0;
-      auto salloc = [&](int32_t n) {
-        n = (n + 1) & ~1;
-        for (auto it = fr.begin(); it != fr.end(); ++it)
-          if (it->second >= n) {
-            int32_t o = it->first, rest = it->second - n;
-            fr.erase(it);
-            if (rest) fr[o + n] = rest;
-            return o;
-          }
-        int32_t o = top;
-        top += n;
-        return o;
-      };
-      auto sfree = [&](int32_t o, int32_t n) {
-        n = (n + 1) & ~1;
-        fr[o] = n;
-        auto it = fr.find(o);
-        auto nx = std::next(it);
-        if (nx != fr.end() && nx->first == o + it->second) {
-          it->second += nx->second;
-          fr.erase(nx);
-        }
-        if (it != fr.begin()) {
-          auto pv2 = std::prev(it);
-          if (pv2->first + pv2->second == it->first) {
-            pv2->second += it->second;
-            fr.erase(it);
-          }
-        }
-        if (!fr.empty()) {
-          auto last = std::prev(fr.end());
-          if (last->first + last->second == top) {
-            top = last->first;
-            fr.erase(last);
-          }
-        }
-      };
       TinyGroup tg;
       tg.beg = (int32_t)g.tiny_nodes.size();
       for (int v : nodes) {
-        int a = p.kid_l(v), b = p.kid_r(v);
+        const int a = p.kid_l(v), b = p.kid_r(v);
         TinyNode tn{};
         Loc la{LOC_SMEM, 0}, lb{LOC_SMEM, 0}, lo{LOC_SMEM, 0};
         auto opnd = [&](int c, Loc& l, int32_t& so) {
-          if (smem_off[c] >= 0 && group_of[c] == gi) {
-            so = smem_off[c];
-            l = Loc{LOC_SMEM, 0};
+          if (c != r && group_of[c] == gi && soff[c] >= 0) {
+            so = soff[c];
           } else {
             l = g.loc[c];  // leaf / sliced leaf / forced root in arena
             so = 0;
@@ -677,45 +685,49 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         };
         opnd(a, la, tn.sa);
         opnd(b, lb, tn.sb);
-        if (v == r) {
-          lo = g.loc[r];
-        } else {
-          smem_off[v] = salloc((int32_t)size[v]);
-          tn.sout = smem_off[v];
-        }
-        for (int c : {a, b})
-          if (smem_off[c] >= 0 && group_of[c] == gi) sfree(smem_off[c], (int32_t)size[c]);
-        // digits
+        if (v == r) lo = g.loc[r];
+        else tn.sout = soff[v];
+        // digits: output indices in C's layout order, then the shared ones
         const auto& La = g.layout[a];
         const auto& Lb = g.layout[b];
         const auto& Lc = g.layout[v];
-        std::vector<int64_t> sa(p.NI > 0 ? 0 : 0);
-        auto strides = [&](const std::vector<int>& L, SmallMap<int64_t>& m) {
-          int64_t st2 = 1;
-          for (int i : L) {
-            m[i] = st2;
-            st2 *= p.dom[i];
-          }
-        };
-        SmallMap<int64_t> ma, mb;
-        strides(La, ma);
-        strides(Lb, mb);
+        int64_t st2 = 1;
+        for (int i : La) {
+          str_a[i] = st2;
+          st2 *= p.dom[i];
+        }
+        st2 = 1;
+        for (int i : Lb) {
+          str_b[i] = st2;
+          st2 *= p.dom[i];
+        }
         tn.dig = (int32_t)g.tiny_digits.size();
         bool p2 = true;
         for (int i : Lc) {
-          TinyDigit d{p.dom[i], ma.count(i) ? (int32_t)ma[i] : 0, mb.count(i) ? (int32_t)mb[i] : 0, 0};
+          g.tiny_digits.push_back(TinyDigit{p.dom[i], (int32_t)str_a[i], (int32_t)str_b[i], 0});
           p2 &= (p.dom[i] == 2);
-          g.tiny_digits.push_back(d);
         }
-        std::vector<int> Sh = inter(eff[a], eff[b]);
         int64_t ssz = 1;
-        for (int i : Sh) {
-          g.tiny_digits.push_back(TinyDigit{p.dom[i], (int32_t)ma[i], (int32_t)mb[i], 0});
-          p2 &= (p.dom[i] == 2);
-          ssz *= p.dom[i];
+        int ns = 0;
+        const auto& Ea = eff[a];
+        const auto& Eb = eff[b];
+        for (size_t x = 0, y = 0; x < Ea.size() && y < Eb.size();) {
+          if (Ea[x] < Eb[y]) ++x;
+          else if (Eb[y] < Ea[x]) ++y;
+          else {
+            const int i = Ea[x];
+            g.tiny_digits.push_back(TinyDigit{p.dom[i], (int32_t)str_a[i], (int32_t)str_b[i], 0});
+            p2 &= (p.dom[i] == 2);
+            ssz *= p.dom[i];
+            ++ns;
+            ++x;
+            ++y;
+          }
         }
+        for (int i : La) str_a[i] = 0;
+        for (int i : Lb) str_b[i] = 0;
         tn.nc = (int32_t)Lc.size();
-        tn.ns = (int32_t)Sh.size();
+        tn.ns = ns;
         tn.c_size = (int32_t)size[v];
         tn.s_size = (int32_t)ssz;
         tn.pow2 = p2 ? 1 : 0;
@@ -758,14 +770,28 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   std::vector<double> node_bytes(S, 0.0), node_flops(S, 0.0);
   for (int k = 0; k < p.NN; ++k) {
     int v = p.NL + k, a = p.left[k], b = p.right[k];
-    std::vector<int> uni;
-    std::set_union(eff[a].begin(), eff[a].end(), eff[b].begin(), eff[b].end(), std::back_inserter(uni));
-    const u128 fl = 2 * (set_bytes(p, uni, drop) / 8);
+    // 2 * prod of the union's domains (eff sets are sorted, drop-free)
+    u128 un = 1;
+    {
+      const auto& Ea = eff[a];
+      const auto& Eb = eff[b];
+      size_t x = 0, y = 0;
+      while (x < Ea.size() || y < Eb.size()) {
+        int i;
+        if (y == Eb.size() || (x < Ea.size() && Ea[x] < Eb[y])) i = Ea[x++];
+        else if (x == Ea.size() || Eb[y] < Ea[x]) i = Eb[y++];
+        else i = Ea[x++], ++y;
+        un *= (u128)p.dom[i];
+        if (un > ((u128)1 << 100)) fail(TC_OVERFLOW, "contraction size overflows 2^100");
+      }
+    }
+    const u128 fl = 2 * un;
     g.alg_flops += fl;
     g.alg_bytes += (u128)8 * (u128)(size[a] + size[b] + size[v]);
     node_bytes[v] = 8.0 * (double)(size[a] + size[b] + size[v]);
     node_flops[v] = (double)fl;
   }
+  tmark("emit nodes");
   auto emit_node = [&](int v) {
     const int k = v - p.NL, a = p.left[k], b = p.right[k];
     Step st;

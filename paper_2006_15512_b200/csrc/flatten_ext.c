@@ -1,0 +1,357 @@
+// _tcflat: native flattening of a (TensorNetwork, ContractionTree) pair into
+// the arrays of tc_plan_desc (include/tc.h).  Same output as the pure-Python
+// paper_2006_15512_b200/flatten.py (which documents the format), but walks
+// the Python objects through the C API: it runs on every public-API call and
+// the Python loop cost ~27 ms on C2's 16k leaves / 16k internal nodes.
+//
+//   flatten(tensors, tree) -> (indices: list[Index], domain: bytes(int32),
+//       leaf_idx_off: bytes(int64), leaf_idx: bytes(int32),
+//       leaf_val_off: bytes(int64), leaf_val: bytes(float64),
+//       left: bytes(int32), right: bytes(int32), root_slot: int)
+//
+// Reads only n.tensors[k].indices / .values, index.id / .domain_size and
+// node.tensor / .left / .right (reference network.py:83-124, tensor.py:18-62).
+// Index identity is Index.id (tensor.py:29-33); leaf identity is the tensor
+// object (network.py:143-148); slots follow serialize_plan (network.py:235-258):
+// leaves in network order, then internal nodes in left-first postorder.
+#define PY_SSIZE_T_CLEAN
+#include <Python.h>
+#include <stdint.h>
+#include <string.h>
+
+typedef struct {
+  char* p;
+  size_t n, cap;
+} Buf;
+
+static int buf_put(Buf* b, const void* src, size_t len) {
+  if (b->n + len > b->cap) {
+    size_t c = b->cap ? b->cap * 2 : 4096;
+    while (c < b->n + len) c *= 2;
+    char* q = (char*)PyMem_Realloc(b->p, c);
+    if (!q) {
+      PyErr_NoMemory();
+      return -1;
+    }
+    b->p = q;
+    b->cap = c;
+  }
+  memcpy(b->p + b->n, src, len);
+  b->n += len;
+  return 0;
+}
+
+static PyObject* buf_bytes(Buf* b) { return PyBytes_FromStringAndSize(b->p ? b->p : "", (Py_ssize_t)b->n); }
+
+// pointer -> int open-addressing map (leaf tensor object -> slot, tree node -> slot)
+typedef struct {
+  uintptr_t* key;
+  int64_t* val;
+  size_t mask;
+} PtrMap;
+
+static int pm_init(PtrMap* m, size_t n) {
+  size_t c = 16;
+  while (c < 2 * n + 2) c <<= 1;
+  m->key = (uintptr_t*)PyMem_Calloc(c, sizeof(uintptr_t));
+  m->val = (int64_t*)PyMem_Malloc(c * sizeof(int64_t));
+  m->mask = c - 1;
+  if (!m->key || !m->val) {
+    PyErr_NoMemory();
+    return -1;
+  }
+  return 0;
+}
+static void pm_free(PtrMap* m) {
+  PyMem_Free(m->key);
+  PyMem_Free(m->val);
+}
+static inline size_t pm_hash(uintptr_t k) { return (size_t)((k >> 4) * 0x9E3779B97F4A7C15ull); }
+static void pm_set(PtrMap* m, uintptr_t k, int64_t v) {
+  size_t h = pm_hash(k) & m->mask;
+  while (m->key[h] && m->key[h] != k) h = (h + 1) & m->mask;
+  m->key[h] = k;
+  m->val[h] = v;
+}
+static int64_t pm_get(const PtrMap* m, uintptr_t k, int64_t dflt) {
+  size_t h = pm_hash(k) & m->mask;
+  while (m->key[h]) {
+    if (m->key[h] == k) return m->val[h];
+    h = (h + 1) & m->mask;
+  }
+  return dflt;
+}
+
+static PyObject *s_indices, *s_values, *s_id, *s_domain_size, *s_tensor, *s_left, *s_right;
+
+// append the row-major float64 contents of `values` to vals; returns entries or -1
+static Py_ssize_t put_values(Buf* vals, PyObject* values) {
+  Py_buffer v;
+  if (PyObject_GetBuffer(values, &v, PyBUF_STRIDES | PyBUF_FORMAT) == 0) {
+    const char* f = v.format ? v.format : "B";
+    if (f[0] == '<' || f[0] == '=' || f[0] == '@') f++;
+    if (v.itemsize == 8 && f[0] == 'd' && f[1] == 0) {
+      Py_ssize_t n = v.len / 8;
+      int rc;
+      if (PyBuffer_IsContiguous(&v, 'C')) {
+        rc = buf_put(vals, v.buf, (size_t)v.len);
+      } else {
+        size_t at = vals->n;
+        double zero = 0.0;
+        rc = 0;
+        for (Py_ssize_t i = 0; i < n && rc == 0; ++i) rc = buf_put(vals, &zero, 8);
+        if (rc == 0) rc = PyBuffer_ToContiguous(vals->p + at, &v, v.len, 'C');
+      }
+      PyBuffer_Release(&v);
+      return rc == 0 ? n : -1;
+    }
+    PyBuffer_Release(&v);
+  } else {
+    PyErr_Clear();
+  }
+  // anything else (other dtype, non-buffer): let numpy convert
+  PyObject* np = PyImport_ImportModule("numpy");
+  if (!np) return -1;
+  PyObject* arr = PyObject_CallMethod(np, "ascontiguousarray", "Os", values, "float64");
+  Py_DECREF(np);
+  if (!arr) return -1;
+  Py_ssize_t n = put_values(vals, arr);
+  Py_DECREF(arr);
+  return n;
+}
+
+static PyObject* flatten(PyObject* self, PyObject* args) {
+  PyObject *tensors_in, *tree;
+  if (!PyArg_ParseTuple(args, "OO", &tensors_in, &tree)) return NULL;
+  PyObject* tensors = PySequence_Fast(tensors_in, "n.tensors must be a sequence");
+  if (!tensors) return NULL;
+  const Py_ssize_t nl = PySequence_Fast_GET_SIZE(tensors);
+  PyObject** tv = PySequence_Fast_ITEMS(tensors);
+
+  PyObject* result = NULL;
+  PyObject* indices = PyList_New(0);
+  PyObject* pos = PyDict_New();  // Index.id -> dense id
+  Buf dom = {0}, ioff = {0}, iarr = {0}, voff = {0}, vals = {0}, lft = {0}, rgt = {0};
+  PtrMap leaf = {0}, ixp = {0};
+  size_t pm_size = 0, pm_cap = 4096;
+  if (!indices || !pos) goto done;
+  if (pm_init(&leaf, (size_t)nl) < 0 || pm_init(&ixp, pm_cap) < 0) goto done;
+
+  int64_t off = 0, voffv = 0;
+  if (buf_put(&ioff, &off, 8) < 0 || buf_put(&voff, &voffv, 8) < 0) goto done;
+  for (Py_ssize_t k = 0; k < nl; ++k) {
+    PyObject* ten = tv[k];
+    pm_set(&leaf, (uintptr_t)ten, k);
+    PyObject* inds = PyObject_GetAttr(ten, s_indices);
+    if (!inds) goto done;
+    PyObject* fi = PySequence_Fast(inds, "tensor.indices must be a sequence");
+    Py_DECREF(inds);
+    if (!fi) goto done;
+    const Py_ssize_t r = PySequence_Fast_GET_SIZE(fi);
+    PyObject** iv = PySequence_Fast_ITEMS(fi);
+    for (Py_ssize_t q = 0; q < r; ++q) {
+      PyObject* ix = iv[q];
+      // the same Index object seen before: no attribute read, no id hashing
+      int64_t known = pm_get(&ixp, (uintptr_t)ix, -1);
+      if (known >= 0) {
+        int32_t di = (int32_t)known;
+        if (buf_put(&iarr, &di, 4) < 0) {
+          Py_DECREF(fi);
+          goto done;
+        }
+        continue;
+      }
+      PyObject* key = PyObject_GetAttr(ix, s_id);
+      if (!key) {
+        Py_DECREF(fi);
+        goto done;
+      }
+      PyObject* d = PyDict_GetItemWithError(pos, key);
+      int32_t di;
+      if (d) {
+        di = (int32_t)PyLong_AsLong(d);
+      } else {
+        if (PyErr_Occurred()) {
+          Py_DECREF(key);
+          Py_DECREF(fi);
+          goto done;
+        }
+        di = (int32_t)PyList_GET_SIZE(indices);
+        PyObject* dv = PyLong_FromLong(di);
+        PyObject* ds = PyObject_GetAttr(ix, s_domain_size);
+        long dsz = ds ? PyLong_AsLong(ds) : -1;
+        Py_XDECREF(ds);
+        int32_t dsz32 = (int32_t)dsz;
+        if (!dv || dsz < 0 || PyDict_SetItem(pos, key, dv) < 0 || PyList_Append(indices, ix) < 0 ||
+            buf_put(&dom, &dsz32, 4) < 0) {
+          if (!PyErr_Occurred()) PyErr_SetString(PyExc_ValueError, "bad index domain_size");
+          Py_XDECREF(dv);
+          Py_DECREF(key);
+          Py_DECREF(fi);
+          goto done;
+        }
+        Py_DECREF(dv);
+      }
+      Py_DECREF(key);
+      // cache only first occurrences: `indices` owns them, so the pointer
+      // cannot be recycled during this call
+      if (di == (int32_t)PyList_GET_SIZE(indices) - 1 && PyList_GET_ITEM(indices, di) == ix) {
+      if (pm_size >= pm_cap) {  // grow the pointer cache (rehash)
+        PtrMap bigger;
+        if (pm_init(&bigger, 2 * pm_cap) < 0) {
+          Py_DECREF(fi);
+          goto done;
+        }
+        for (size_t h = 0; h <= ixp.mask; ++h)
+          if (ixp.key[h]) pm_set(&bigger, ixp.key[h], ixp.val[h]);
+        pm_free(&ixp);
+        ixp = bigger;
+        pm_cap *= 2;
+      }
+      pm_set(&ixp, (uintptr_t)ix, di);
+      pm_size++;
+      }
+      if (buf_put(&iarr, &di, 4) < 0) {
+        Py_DECREF(fi);
+        goto done;
+      }
+    }
+    Py_DECREF(fi);
+    off += r;
+    if (buf_put(&ioff, &off, 8) < 0) goto done;
+    PyObject* values = PyObject_GetAttr(ten, s_values);
+    if (!values) goto done;
+    Py_ssize_t nv = put_values(&vals, values);
+    Py_DECREF(values);
+    if (nv < 0) goto done;
+    voffv += nv;
+    if (buf_put(&voff, &voffv, 8) < 0) goto done;
+  }
+
+  // right-first preorder, reversed = left-first postorder (network.py:114-124).
+  // Pass 1 reads each node's attributes once and records its parent; pass 2
+  // (reverse order: children before parents) numbers the internal nodes.
+  {
+    typedef struct {
+      PyObject* node;  // owned
+      int64_t parent;  // seq index of the parent, -1 for the root
+      int64_t kid[2];  // slots of left/right (internal nodes)
+      int64_t leaf;    // leaf slot (-1: not in the network), or -2: internal
+      int side;        // 0: left child, 1: right child
+    } Ent;
+    typedef struct {
+      PyObject* node;
+      int64_t parent;
+      int side;
+    } Pend;
+    size_t cap = 1024, sp = 0, ns = 0, scap = 1024;
+    Pend* stk = (Pend*)PyMem_Malloc(cap * sizeof(Pend));
+    Ent* ent = (Ent*)PyMem_Malloc(scap * sizeof(Ent));
+    if (!stk || !ent) {
+      PyMem_Free(stk);
+      PyMem_Free(ent);
+      PyErr_NoMemory();
+      goto done;
+    }
+    Py_INCREF(tree);
+    stk[sp++] = (Pend){tree, -1, 0};  // owned references on the stack and in ent
+    while (sp) {
+      Pend pd = stk[--sp];
+      if (ns == scap) {
+        scap *= 2;
+        Ent* q = (Ent*)PyMem_Realloc(ent, scap * sizeof(Ent));
+        if (!q) {
+          Py_DECREF(pd.node);
+          PyErr_NoMemory();
+          goto tree_fail;
+        }
+        ent = q;
+      }
+      Ent* e = &ent[ns++];
+      e->node = pd.node;
+      e->parent = pd.parent;
+      e->side = pd.side;
+      e->kid[0] = e->kid[1] = -1;
+      PyObject* t = PyObject_GetAttr(pd.node, s_tensor);
+      if (!t) goto tree_fail;
+      if (t != Py_None) {
+        e->leaf = pm_get(&leaf, (uintptr_t)t, -1);
+        Py_DECREF(t);
+        continue;
+      }
+      Py_DECREF(t);
+      e->leaf = -2;
+      if (sp + 2 > cap) {
+        cap *= 2;
+        Pend* q = (Pend*)PyMem_Realloc(stk, cap * sizeof(Pend));
+        if (!q) {
+          PyErr_NoMemory();
+          goto tree_fail;
+        }
+        stk = q;
+      }
+      PyObject* l = PyObject_GetAttr(pd.node, s_left);
+      if (!l) goto tree_fail;
+      stk[sp++] = (Pend){l, (int64_t)(ns - 1), 0};
+      PyObject* r = PyObject_GetAttr(pd.node, s_right);
+      if (!r) goto tree_fail;
+      stk[sp++] = (Pend){r, (int64_t)(ns - 1), 1};
+    }
+    {
+      int64_t nxt = nl, root_slot = -1;
+      for (size_t q = ns; q-- > 0;) {
+        Ent* e = &ent[q];
+        int64_t s;
+        if (e->leaf != -2) {
+          s = e->leaf;
+        } else {
+          int32_t ls = (int32_t)e->kid[0], rs = (int32_t)e->kid[1];
+          if (buf_put(&lft, &ls, 4) < 0 || buf_put(&rgt, &rs, 4) < 0) goto tree_fail;
+          s = nxt++;
+        }
+        if (e->parent >= 0) ent[e->parent].kid[e->side] = s;
+        else root_slot = s;
+      }
+      result = Py_BuildValue("(ONNNNNNNL)", indices, buf_bytes(&dom), buf_bytes(&ioff), buf_bytes(&iarr),
+                             buf_bytes(&voff), buf_bytes(&vals), buf_bytes(&lft), buf_bytes(&rgt),
+                             (long long)root_slot);
+    }
+  tree_fail:
+    for (size_t q = 0; q < ns; ++q) Py_DECREF(ent[q].node);
+    for (size_t q = 0; q < sp; ++q) Py_DECREF(stk[q].node);
+    PyMem_Free(stk);
+    PyMem_Free(ent);
+  }
+
+done:
+  pm_free(&leaf);
+  pm_free(&ixp);
+  PyMem_Free(dom.p);
+  PyMem_Free(ioff.p);
+  PyMem_Free(iarr.p);
+  PyMem_Free(voff.p);
+  PyMem_Free(vals.p);
+  PyMem_Free(lft.p);
+  PyMem_Free(rgt.p);
+  Py_XDECREF(indices);
+  Py_XDECREF(pos);
+  Py_DECREF(tensors);
+  return result;
+}
+
+static PyMethodDef methods[] = {
+    {"flatten", flatten, METH_VARARGS, "flatten(tensors, tree) -> plan arrays (see paper_2006_15512_b200/flatten.py)"},
+    {NULL, NULL, 0, NULL}};
+
+static struct PyModuleDef mod = {PyModuleDef_HEAD_INIT, "_tcflat", NULL, -1, methods};
+
+PyMODINIT_FUNC PyInit__tcflat(void) {
+  s_indices = PyUnicode_InternFromString("indices");
+  s_values = PyUnicode_InternFromString("values");
+  s_id = PyUnicode_InternFromString("id");
+  s_domain_size = PyUnicode_InternFromString("domain_size");
+  s_tensor = PyUnicode_InternFromString("tensor");
+  s_left = PyUnicode_InternFromString("left");
+  s_right = PyUnicode_InternFromString("right");
+  return PyModule_Create(&mod);
+}

@@ -11,7 +11,9 @@ Slot numbering follows ``serialize_plan`` (reference ``network.py:235-258``):
 leaves are numbered by network order, internal nodes continue the numbering in
 postorder (left subtree, right subtree, node; ``network.py:114-124``).
 
-This runs on every call of the public API, so it is written for speed: index
+This runs on every call of the public API, so the work is done by a small
+CPython C extension (``csrc/flatten_ext.c`` -> ``lib/_tcflat*.so``); the
+pure-Python ``flatten_py`` below is its specification.  In both, index
 identity is keyed on ``Index.id`` (the reference's equality, ``tensor.py:29-33``),
 values are gathered with one ``np.concatenate``, and ``sort_key`` ranks (only
 needed by the greedy slice chooser) can be skipped.
@@ -53,7 +55,50 @@ def sort_ranks(indices) -> np.ndarray:
     return r
 
 
+def _native():
+    """The C flattener (csrc/flatten_ext.c, built in-tree by build.py), or None."""
+    global _NATIVE
+    if _NATIVE is False:
+        import importlib.util
+        import os
+
+        from .build import flat_ext_path
+
+        path = flat_ext_path()
+        _NATIVE = None
+        if os.path.exists(path):
+            spec = importlib.util.spec_from_file_location("_tcflat", path)
+            mod = importlib.util.module_from_spec(spec)
+            spec.loader.exec_module(mod)
+            _NATIVE = mod
+    return _NATIVE
+
+
+_NATIVE = False
+
+
 def flatten(n, t, with_sort_rank: bool = True) -> FlatPlan:
+    nat = _native()
+    if nat is not None:
+        indices, dom, ioff, iarr, voff, vals, lft, rgt, root = nat.flatten(n.tensors, t)
+        return FlatPlan(
+            indices=indices,
+            domain=np.frombuffer(dom, dtype=np.int32),
+            sort_rank=sort_ranks(indices) if with_sort_rank else np.arange(len(indices), dtype=np.int32),
+            leaf_idx_off=np.frombuffer(ioff, dtype=np.int64),
+            leaf_idx=np.frombuffer(iarr, dtype=np.int32),
+            leaf_val_off=np.frombuffer(voff, dtype=np.int64),
+            leaf_val=np.frombuffer(vals, dtype=np.float64),
+            left=np.frombuffer(lft, dtype=np.int32),
+            right=np.frombuffer(rgt, dtype=np.int32),
+            root_slot=int(root),
+        )
+    return flatten_py(n, t, with_sort_rank)
+
+
+def flatten_py(n, t, with_sort_rank: bool = True) -> FlatPlan:
+    """Pure-Python flattener (same output as the native one; fallback when
+    the host extension is not built, and its cross-check in the tests)."""
     tensors = n.tensors
     nl = len(tensors)
     pos = {}

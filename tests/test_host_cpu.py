@@ -184,3 +184,39 @@ def test_generators_deterministic():
     assert banded_3cnf(200, 3.5, 29, 1).count("\n") == 1 + 700 + 200
     g = grid_ising(4, 1)
     assert g.startswith("p cnf 40 96")
+
+
+def _flat_equal(x, y):
+    for f in ("domain", "sort_rank", "leaf_idx_off", "leaf_idx", "leaf_val_off", "leaf_val", "left", "right"):
+        assert np.array_equal(getattr(x, f), getattr(y, f)), f
+    assert x.root_slot == y.root_slot
+    assert [ix.id for ix in x.indices] == [ix.id for ix in y.indices]
+
+
+def test_native_flatten_matches_python_spec():
+    from paper_2006_15512_b200.flatten import _native, flatten_py
+    assert _native() is not None, "host extension _tcflat not built"
+    for c in CASES[:40]:
+        n, t = planfile.to_objects(case_flat(c))
+        _flat_equal(flatten(n, t), flatten_py(n, t))
+    n, t = planfile.to_objects(planfile.load(os.path.join(PLANS, "c1a.tcplan.npz"))[0])
+    _flat_equal(flatten(n, t), flatten_py(n, t))
+
+
+def test_native_flatten_views_dtypes_and_mismatch():
+    from paper_2006_15512_b200 import Index, Tensor, TensorNetwork
+    from paper_2006_15512_b200.flatten import flatten_py
+    from paper_2006_15512_b200.network import join, leaf
+    i, j, k = Index("i", 2), Index("j", 3), Index(("k", 1), 2)
+    base = np.arange(12.0).reshape(2, 3, 2)
+    a = Tensor((i, j), base[:, :, 1])          # non-contiguous view
+    b = Tensor((Index("j", 3), k), np.ones((3, 2), dtype=np.float32).T.T)  # equal-by-id, distinct object
+    s = Tensor((), np.array(2.5))
+    n = TensorNetwork((a, b, s))
+    t = join(join(leaf(a), leaf(b)), leaf(s))
+    x, y = flatten(n, t), flatten_py(n, t)
+    _flat_equal(x, y)
+    assert list(x.leaf_val[:6]) == [1.0, 3.0, 5.0, 7.0, 9.0, 11.0]
+    other = Tensor((i,), np.ones(2))
+    bad = flatten(n, join(join(leaf(a), leaf(other)), leaf(s)))
+    assert (bad.left < 0).any() or (bad.right < 0).any()
