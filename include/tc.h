@@ -98,10 +98,12 @@ typedef struct tc_stats {
   tc_u128 alg_bytes;             /* per slice: sum over nodes 8(|A|+|B|+|C|) */
   tc_u128 alg_flops;             /* per slice: sum over nodes 2*prod(union)  */
   int32_t n_alias_nodes;         /* exact relabels (identity pieces): no launch */
-  int32_t n_chain_launches;      /* fused chain launches                      */
+  int32_t n_tied_leaves;         /* leaves stored over tie blocks (diagonal copy pieces) */
   double program_ms;             /* compile_ms split: host program compile    */
   double setup_ms;               /*   device allocations + uploads            */
   double graph_ms;               /*   CUDA graph build + instantiate          */
+  tc_u128 phys_bytes;            /* per slice: executed bytes over physical (tied) variables */
+  tc_u128 phys_flops;            /* per slice: executed flops over physical variables        */
 } tc_stats;
 
 /* ---- symbolic plan (host) ---------------------------------------------- */

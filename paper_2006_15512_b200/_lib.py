@@ -76,10 +76,12 @@ class Stats(C.Structure):
         ("alg_bytes", U128),
         ("alg_flops", U128),
         ("n_alias_nodes", C.c_int32),
-        ("n_chain_launches", C.c_int32),
+        ("n_tied_leaves", C.c_int32),
         ("program_ms", C.c_double),
         ("setup_ms", C.c_double),
         ("graph_ms", C.c_double),
+        ("phys_bytes", U128),
+        ("phys_flops", U128),
     ]
 
     def as_dict(self):
@@ -98,10 +100,12 @@ class Stats(C.Structure):
             alg_bytes=self.alg_bytes.value(),
             alg_flops=self.alg_flops.value(),
             n_alias_nodes=int(self.n_alias_nodes),
-            n_chain_launches=int(self.n_chain_launches),
+            n_tied_leaves=int(self.n_tied_leaves),
             program_ms=float(self.program_ms),
             setup_ms=float(self.setup_ms),
             graph_ms=float(self.graph_ms),
+            phys_bytes=self.phys_bytes.value(),
+            phys_flops=self.phys_flops.value(),
         )
 
 

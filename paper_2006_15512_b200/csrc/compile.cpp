@@ -1,17 +1,36 @@
 // Host program compiler (see compile.hpp).
 //
 // What it decides, per internal node of the (sliced) contraction tree:
+//   * the PHYSICAL shape of every tensor.  FactorTree's copy-tensor pieces
+//     (factoring.py:194-206) are generalised diagonals: an identity piece
+//     I[a,b] or a rank-3 piece delta[a,b,c] is exactly zero unless all its
+//     indices agree.  A leaf whose entries are zero off such a diagonal is
+//     stored over its "tie blocks" (one physical variable per block of
+//     indices that must agree), and ties propagate through contractions by
+//     union-find (a component of tied indices is one variable of the
+//     product).  Every tensor is then a dense array over its physical
+//     variables; the structurally-zero entries of the reference's dense
+//     tensors are never stored, read, or multiplied.  The result is
+//     identical: each dropped term is an exact 0 (x*0 = 0 and acc + 0 = acc
+//     for finite values; only the sign of an exact zero can differ), so a
+//     dense sum and the compressed sum agree bit for bit on the nonzero
+//     terms in the same order.  A contraction's variables fall into M (A and
+//     C), N (B and C), K (A and B, summed) and batch (A, B and C; only tied
+//     networks have these).  TC_NO_TIES=1 keeps every index its own
+//     variable (dense semantics).
 //   * kernel class — TINY (whole small subtrees evaluated in one CTA's shared
 //     memory, many subtrees per launch), STREAM (big tensor x <=64-entry
-//     operand, HBM-bound), GEMM (FP64 DMMA), GENERIC (mixed radix fallback);
+//     operand, HBM-bound), GEMM (FP64 DMMA, optional batch variables),
+//     GENERIC (mixed radix fallback), ALIAS (C is A's buffer with variables
+//     renamed: contractions with an all-ones tie piece, e.g. every identity
+//     and delta piece of a copy tensor);
 //   * the memory layout of every intermediate.  The reference always emits
 //     kept_a ++ kept_b (tensor.py:108) and numpy pays a transpose copy per
 //     tensordot (60-70% of CPU time).  Here layouts are chosen
 //     top-down so that a STREAM node's output is an in-place relabel of its
-//     big input (shared bits of the input and free bits of the small operand
-//     share address bits) and a GEMM's operands are K-lowest matrices; the
-//     permutation is folded into the producing kernel's addressing and no
-//     separate transpose pass exists;
+//     big input and a GEMM's operands are K-lowest matrices; the permutation
+//     is folded into the producing kernel's addressing and no separate
+//     transpose pass exists;
 //   * a static arena: offsets from a first-fit simulation in postorder, with
 //     write-after-read edges added to the launch DAG wherever a buffer reuses
 //     memory, so independent branches may run concurrently in the CUDA graph.
@@ -19,10 +38,13 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cstdio>
-#include <map>
 #include <cstdlib>
+#include <map>
 #include <set>
+#include <string>
+#include <tuple>
 
 namespace tc {
 
@@ -32,6 +54,7 @@ constexpr int64_t kTinyMax = 4096;           // entries per tiny tensor
 constexpr int32_t kTinySmemCap = 20 * 1024;  // doubles of smem per tiny CTA (160 KB)
 constexpr int64_t kAlign = 256;
 constexpr int64_t kSMs = 148;                // B200 SM count (split-K sizing)
+constexpr int kMaxTie = 4;                   // physical variables of one operand in one component
 
 [[noreturn]] void fail(int st, const std::string& m) { throw Error{st, m}; }
 
@@ -126,11 +149,6 @@ struct SmallMap {
     kv.push_back({k, V{}});
     return kv.back().second;
   }
-  size_t count(int k) const {
-    for (auto& e : kv)
-      if (e.first == k) return 1;
-    return 0;
-  }
 };
 
 // first-fit shared-memory allocator of one tiny group (doubles, 16-byte
@@ -196,6 +214,77 @@ BitRuns make_runs(const std::vector<std::pair<int, int>>& bits) {  // (src bit, 
   return r;
 }
 
+// One component of tied indices at a contraction: its variable in C (-1:
+// summed) and its variables in the operands A (left) and B (right).
+struct Comp {
+  int32_t c;
+  int8_t na, nb;
+  int32_t a[kMaxTie], b[kMaxTie];
+  int32_t key() const { return std::min(na ? a[0] : INT_MAX, nb ? b[0] : INT_MAX); }
+};
+
+// Coarsest partition of the kept positions of a dim-2 leaf (<= 4 of them)
+// such that every nonzero entry agrees within each block (restricted growth
+// strings in lexicographic order; first minimum wins).  lab[q] = block.
+bool leaf_ties(const Plan& p, int l, const std::vector<char>& drop, std::vector<int>& lab) {
+  const auto& ro = p.ref_order[l];
+  std::vector<int> kq;
+  for (size_t q = 0; q < ro.size(); ++q)
+    if (!drop[ro[q]]) {
+      if (p.dom[ro[q]] != 2) return false;
+      kq.push_back((int)q);
+    }
+  const int r = (int)kq.size();
+  if (r < 2 || r > 4 || p.leaf_size(l) > 4096) return false;
+  const double* v = p.lval.data() + p.lval_off[l];
+  const int64_t n = p.leaf_size(l);
+  std::vector<int64_t> stride(ro.size());
+  int64_t st = 1;
+  for (int q = (int)ro.size() - 1; q >= 0; --q) {
+    stride[q] = st;
+    st *= p.dom[ro[q]];
+  }
+  // kept digits of every nonzero entry
+  std::vector<int> nzd;  // r digits per nonzero entry
+  for (int64_t e = 0; e < n; ++e) {
+    if (v[e] == 0.0) continue;
+    for (int q : kq) nzd.push_back((int)((e / stride[q]) % p.dom[ro[q]]));
+  }
+  std::vector<int> cur(r, 0), best;
+  int best_blocks = r + 1;
+  for (;;) {
+    int blocks = 0;
+    for (int x : cur) blocks = std::max(blocks, x + 1);
+    if (blocks < best_blocks) {
+      bool ok = true;
+      for (size_t base = 0; ok && base < nzd.size(); base += r)
+        for (int x = 0; ok && x < r; ++x)
+          for (int y = x + 1; ok && y < r; ++y)
+            if (cur[x] == cur[y] && nzd[base + x] != nzd[base + y]) ok = false;
+      if (ok) {
+        best = cur;
+        best_blocks = blocks;
+      }
+    }
+    // next restricted growth string
+    int q = r - 1;
+    for (; q >= 1; --q) {
+      int m = 0;
+      for (int t = 0; t < q; ++t) m = std::max(m, cur[t]);
+      if (cur[q] <= m) {
+        cur[q]++;
+        for (int t = q + 1; t < r; ++t) cur[t] = 0;
+        break;
+      }
+    }
+    if (q < 1) break;
+  }
+  if (best_blocks >= r) return false;
+  lab.assign(ro.size(), -1);
+  for (int x = 0; x < r; ++x) lab[kq[x]] = best[x];
+  return true;
+}
+
 }  // namespace
 
 Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_t no_reuse_limit) {
@@ -230,59 +319,232 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   g.mem_estimate = mem_cost(p, drop);
   g.peak_observed = tracked_peak(p, drop);
 
-  tmark("effective sets / siz");
-  // ---- effective sets / sizes ------------------------------------------------
-  // eff[s]: the slot's index set without the sliced indices (a view of
-  // p.sets when the slot holds none of them)
-  std::vector<std::vector<int>> eff_own;
-  std::vector<const std::vector<int>*> effp(S);
-  {
-    std::vector<int> own_of(S, -1);
-    for (int s = 0; s < S; ++s) {
-      bool any = false;
-      for (int i : p.sets[s]) any |= (bool)drop[i];
-      if (any) own_of[s] = (int)eff_own.size(), eff_own.emplace_back();
+  tmark("dense sizes");
+  // ---- dense (reference) sizes: the result size and the dense roofline ------
+  std::vector<u128> dsize(S);
+  for (int s = 0; s < S; ++s) dsize[s] = set_bytes(p, p.sets[s], drop) / 8;
+  for (int k = 0; k < p.NN; ++k) {
+    const int v = p.NL + k, a = p.left[k], b = p.right[k];
+    // |A u B| = |A| |B| / |A n B|
+    u128 sh = 1;
+    const auto& Ea = p.sets[a];
+    const auto& Eb = p.sets[b];
+    for (size_t x = 0, y = 0; x < Ea.size() && y < Eb.size();) {
+      if (Ea[x] < Eb[y]) ++x;
+      else if (Eb[y] < Ea[x]) ++y;
+      else {
+        if (!drop[Ea[x]]) sh *= (u128)p.dom[Ea[x]];
+        ++x, ++y;
+      }
     }
-    for (int s = 0; s < S; ++s) {
-      if (own_of[s] < 0) {
-        effp[s] = &p.sets[s];
+    g.alg_flops += 2 * (dsize[a] / sh) * dsize[b];
+    g.alg_bytes += (u128)8 * (dsize[a] + dsize[b] + dsize[v]);
+  }
+
+  tmark("physical variables");
+  // ---- physical variables: tie blocks of leaves, union-find at nodes --------
+  // mem[s]: (logical index, variable) pairs sorted by logical index; a
+  // variable is named by the smallest logical index of its block.
+  bool ties = std::getenv("TC_NO_TIES") == nullptr;
+  std::vector<std::vector<std::pair<int, int>>> mem(S);
+  std::vector<std::vector<int>> vars(S);  // sorted variable ids per slot
+  std::vector<Comp> cpool;
+  std::vector<int32_t> coff(p.NN + 1, 0);
+  std::vector<int> lab;
+  std::vector<int> uf(p.NI, -1), own_a(p.NI, -1), own_b(p.NI, -1), cidx(p.NI, -1);
+  std::vector<char> leaf_tied(p.NL, 0);
+  auto find = [&](int x) {
+    while (uf[x] != x) {
+      uf[x] = uf[uf[x]];
+      x = uf[x];
+    }
+    return x;
+  };
+  // Tie push-down: when a contraction reads two variables of an internal
+  // operand as one (a diagonal read: a copy-tensor piece ties two indices the
+  // operand keeps separately), the operand's off-diagonal entries are
+  // computed and never used.  The tie is pushed down to the node where the
+  // two indices first meet (they come from different children there) and
+  // realised as a merge at that node, so every tensor on the way is computed
+  // directly on the diagonal: half the work and bytes per tie, and no gather.
+  std::vector<std::vector<std::pair<int, int>>> req(p.NN);
+  auto has_logical = [&](int s, int l) {
+    const auto& m = mem[s];
+    auto f = std::lower_bound(m.begin(), m.end(), std::make_pair(l, INT_MIN));
+    return f != m.end() && f->first == l;
+  };
+  int pushdown_rounds = 0;
+  for (int attempt = 0;; ++attempt) {
+    bool overflow = false;
+    cpool.clear();
+    for (int l = 0; l < p.NL; ++l) {
+      const auto& ro = p.ref_order[l];
+      auto& m = mem[l];
+      m.clear();
+      leaf_tied[l] = ties && leaf_ties(p, l, drop, lab);
+      if (leaf_tied[l]) {
+        int bmin[8];
+        for (int q = 0; q < 8; ++q) bmin[q] = INT_MAX;
+        for (size_t q = 0; q < ro.size(); ++q)
+          if (lab[q] >= 0) bmin[lab[q]] = std::min(bmin[lab[q]], ro[q]);
+        for (size_t q = 0; q < ro.size(); ++q)
+          if (lab[q] >= 0) m.push_back({ro[q], bmin[lab[q]]});
+      } else {
+        for (int i : ro)
+          if (!drop[i]) m.push_back({i, i});
+      }
+      std::sort(m.begin(), m.end());
+      auto& vv = vars[l];
+      vv.clear();
+      for (auto& e : m) vv.push_back(e.second);
+      std::sort(vv.begin(), vv.end());
+      vv.erase(std::unique(vv.begin(), vv.end()), vv.end());
+    }
+    std::vector<Comp> cs;
+    for (int k = 0; k < p.NN && !overflow; ++k) {
+      const int v = p.NL + k, a = p.left[k], b = p.right[k];
+      coff[k] = (int32_t)cpool.size();
+      for (auto& e : mem[a]) own_a[e.first] = e.second;
+      for (auto& e : mem[b]) own_b[e.first] = e.second;
+      for (int x : vars[a]) uf[x] = x;
+      for (int x : vars[b]) uf[x] = x;
+      for (auto& e : mem[b])
+        if (own_a[e.first] >= 0) {
+          int r1 = find(own_a[e.first]), r2 = find(e.second);
+          if (r1 != r2) uf[std::max(r1, r2)] = std::min(r1, r2);
+        }
+      for (auto& q : req[k]) {  // pushed-down ties realised here
+        const int x = own_a[q.first] >= 0 ? own_a[q.first] : own_b[q.first];
+        const int y = own_a[q.second] >= 0 ? own_a[q.second] : own_b[q.second];
+        if (x < 0 || y < 0) continue;
+        int r1 = find(x), r2 = find(y);
+        if (r1 != r2) uf[std::max(r1, r2)] = std::min(r1, r2);
+      }
+      cs.clear();
+      auto comp_of = [&](int var) -> Comp& {
+        int r = find(var);
+        if (cidx[r] < 0) {
+          cidx[r] = (int)cs.size();
+          Comp c{};
+          c.c = -1;
+          cs.push_back(c);
+        }
+        return cs[cidx[r]];
+      };
+      for (int x : vars[a]) {
+        Comp& c = comp_of(x);
+        if (c.na == kMaxTie) overflow = true;
+        else c.a[c.na++] = x;
+      }
+      for (int x : vars[b]) {
+        Comp& c = comp_of(x);
+        if (c.nb == kMaxTie) overflow = true;
+        else c.b[c.nb++] = x;
+      }
+      // kept logical indices -> component's C variable (smallest kept index)
+      auto& mv = mem[v];
+      mv.clear();
+      for (auto& e : mem[a])
+        if (own_b[e.first] < 0) mv.push_back({e.first, e.second});
+      for (auto& e : mem[b])
+        if (own_a[e.first] < 0) mv.push_back({e.first, e.second});
+      std::sort(mv.begin(), mv.end());
+      for (auto& e : mv) {
+        Comp& c = comp_of(e.second);
+        if (c.c < 0) c.c = e.first;  // mv is sorted: first kept = smallest
+      }
+      for (auto& e : mv) e.second = comp_of(e.second).c;
+      auto& vv = vars[v];
+      vv.clear();
+      for (auto& e : mv) vv.push_back(e.second);
+      std::sort(vv.begin(), vv.end());
+      vv.erase(std::unique(vv.begin(), vv.end()), vv.end());
+      // reset scratch (before reordering cs: cidx indexes into it)
+      for (int x : vars[a]) cidx[find(x)] = -1;
+      for (int x : vars[b]) cidx[find(x)] = -1;
+      for (int x : vars[a]) uf[x] = -1;
+      for (int x : vars[b]) uf[x] = -1;
+      for (auto& e : mem[a]) own_a[e.first] = -1;
+      for (auto& e : mem[b]) own_b[e.first] = -1;
+      std::sort(cs.begin(), cs.end(), [](const Comp& x, const Comp& y) { return x.key() < y.key(); });
+      cpool.insert(cpool.end(), cs.begin(), cs.end());
+    }
+    coff[p.NN] = (int32_t)cpool.size();
+    if (!overflow) {
+      bool pushed = false;
+      if (ties && pushdown_rounds < 8) {
+        for (int k = 0; k < p.NN; ++k) {
+          const int ch[2] = {p.left[k], p.right[k]};
+          for (int32_t q = coff[k]; q < coff[k + 1]; ++q) {
+            const Comp& c = cpool[q];
+            for (int side = 0; side < 2; ++side) {
+              const int n = side ? c.nb : c.na;
+              const int32_t* vv = side ? c.b : c.a;
+              if (n < 2 || p.is_leaf(ch[side])) continue;
+              for (int t = 1; t < n; ++t) {
+                int u = ch[side];
+                const int l1 = vv[0], l2 = vv[t];
+                for (;;) {
+                  const int ku = u - p.NL, ca = p.left[ku], cb = p.right[ku];
+                  const int c1 = has_logical(ca, l1) ? ca : cb, c2 = has_logical(ca, l2) ? ca : cb;
+                  if (c1 == c2 && !p.is_leaf(c1)) {
+                    u = c1;
+                    continue;
+                  }
+                  req[ku].push_back({l1, l2});
+                  pushed = true;
+                  break;
+                }
+              }
+            }
+          }
+        }
+      }
+      if (pushed) {
+        ++pushdown_rounds;
         continue;
       }
-      auto& e = eff_own[own_of[s]];
-      for (int i : p.sets[s])
-        if (!drop[i]) e.push_back(i);
-      effp[s] = &e;
+      for (int l = 0; l < p.NL; ++l) g.n_tied_leaves += leaf_tied[l];
+      break;
     }
+    if (!ties || attempt > 8) fail(TC_BAD_ARG, "tie component too large");
+    ties = false;  // pathological tie structure: fall back to dense variables
+    for (auto& r : req) r.clear();
   }
   struct EffView {
-    const std::vector<const std::vector<int>*>* v;
-    const std::vector<int>& operator[](int s) const { return *(*v)[s]; }
-  } eff{&effp};
+    const std::vector<std::vector<int>>* v;
+    const std::vector<int>& operator[](int s) const { return (*v)[s]; }
+  } eff{&vars};
+  auto comps = [&](int v) {
+    return std::make_pair((const Comp*)cpool.data() + coff[v - p.NL], (const Comp*)cpool.data() + coff[v - p.NL + 1]);
+  };
   std::vector<int64_t> size(S);
   for (int s = 0; s < S; ++s) {
-    u128 z = set_bytes(p, eff[s], drop) / 8;
+    u128 z = 1;
+    for (int i : vars[s]) z *= (u128)p.dom[i];
     if (z > ((u128)1 << 50)) fail(TC_OOM, "intermediate tensor larger than 2^50 entries");
     size[s] = (int64_t)z;
   }
+  auto var_of = [&](int s, int logical) {
+    const auto& m = mem[s];
+    return std::lower_bound(m.begin(), m.end(), std::make_pair(logical, INT_MIN))->second;
+  };
+  // natural layout: the reference's row-major order (first index slowest),
+  // LSB-first, one entry per variable (first occurrence)
+  std::vector<int> seen_mark(p.NI, -1);
   auto natural = [&](int s) {
     std::vector<int> o;
     const auto& ro = p.ref_order[s];
-    o.reserve(ro.size());
-    for (auto it = ro.rbegin(); it != ro.rend(); ++it)
-      if (!drop[*it]) o.push_back(*it);
+    o.reserve(vars[s].size());
+    for (auto it = ro.rbegin(); it != ro.rend(); ++it) {
+      if (drop[*it]) continue;
+      const int var = var_of(s, *it);
+      if (seen_mark[var] == s) continue;
+      seen_mark[var] = s;
+      o.push_back(var);
+    }
     return o;
   };
-  auto inter = [](const std::vector<int>& a, const std::vector<int>& b) {
-    std::vector<int> o;
-    std::set_intersection(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(o));
-    return o;
-  };
-  auto minus = [](const std::vector<int>& a, const std::vector<int>& b) {
-    std::vector<int> o;
-    std::set_difference(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(o));
-    return o;
-  };
-  auto has = [](const std::vector<int>& s, int i) { return std::binary_search(s.begin(), s.end(), i); };
 
   tmark("classification");
   // ---- classification --------------------------------------------------------
@@ -299,15 +561,24 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     if (std::max({size[a], size[b], size[v]}) <= kTinyMax && tok(a) && tok(b)) {
       c = NC_TINY;
     } else if (all2(a) && all2(b)) {
-      int ks = (int)inter(eff[a], eff[b]).size();
-      int ra = (int)eff[a].size() - ks, rb = (int)eff[b].size() - ks;
-      int f = (eff[b].size() <= eff[a].size()) ? rb : ra;  // free bits of the smaller operand
-      (void)ra;
-      (void)rb;
-      if (ks <= 4 && f <= 4 && ks + f <= 6)
+      const bool b_small = eff[b].size() <= eff[a].size();
+      int ks = 0, f = 0, big_bits = 0;
+      bool diag = false;
+      for (auto [cp, ce] = comps(v); cp != ce; ++cp) {
+        const int nbig = b_small ? cp->na : cp->nb;
+        if (cp->c < 0) ks++;
+        else if (nbig == 0) f++;
+        big_bits = std::max(big_bits, nbig);
+        diag |= cp->na > 1 || cp->nb > 1;
+      }
+      const int sm = b_small ? b : a;
+      (void)sm;
+      if (ks <= 4 && f <= 5 && ks + f <= 7 && big_bits <= 2)
         c = NC_STREAM;
-      else
+      else if (!diag)
         c = NC_GEMM;  // any m, n, k: tile bits beyond the shape are virtual
+      else
+        c = NC_GENERIC;
     } else {
       c = NC_GENERIC;
     }
@@ -317,11 +588,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   tmark("layouts (top-down)");
   // ---- layouts (top-down) ----------------------------------------------------
   g.layout.assign(S, {});
-  std::vector<char> have(S, 0);
-  for (int l = 0; l < p.NL; ++l) {
-    g.layout[l] = natural(l);
-    have[l] = 1;
-  }
+  for (int l = 0; l < p.NL; ++l) g.layout[l] = natural(l);
   std::vector<int> pos(p.NI, -1);
   auto set_pos = [&](const std::vector<int>& L) {
     for (size_t q = 0; q < L.size(); ++q) pos[L[q]] = (int)q;
@@ -329,55 +596,92 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   auto clr_pos = [&](const std::vector<int>& L) {
     for (int i : L) pos[i] = -1;
   };
-  if (!p.is_leaf(p.root)) {
-    g.layout[p.root] = natural(p.root);
-    have[p.root] = 1;
-  }
+  if (!p.is_leaf(p.root)) g.layout[p.root] = natural(p.root);
   auto want = [&](int child, std::vector<int> L) {
     if (p.is_leaf(child)) return;
     g.layout[child] = std::move(L);
-    have[child] = 1;
   };
+  std::vector<const Comp*> ccomp(p.NI, nullptr);  // C variable -> its component (per node)
+  std::vector<const Comp*> K, M, N, Bt;
   for (int k = p.NN - 1; k >= 0; --k) {
     int v = p.NL + k, a = p.left[k], b = p.right[k];
     const std::vector<int>& L = g.layout[v];
+    auto [c0, c1] = comps(v);
     switch (g.cls[v]) {
       case NC_STREAM: {
-        bool b_small = eff[b].size() <= eff[a].size();
-        int big = b_small ? a : b, sm = b_small ? b : a;
-        std::vector<int> Sh = inter(eff[a], eff[b]);
-        std::vector<int> F = minus(eff[sm], Sh);
+        const bool b_small = eff[b].size() <= eff[a].size();
+        const int big = b_small ? a : b, sm = b_small ? b : a;
+        auto bigv = [&](const Comp* c) { return b_small ? c->a : c->b; };
+        auto nbig = [&](const Comp* c) { return b_small ? c->na : c->nb; };
+        K.clear();
+        for (const Comp* c = c0; c != c1; ++c) {
+          if (c->c >= 0) ccomp[c->c] = c;
+          else K.push_back(c);
+        }
+        std::sort(K.begin(), K.end(), [&](const Comp* x, const Comp* y) { return bigv(x)[0] < bigv(y)[0]; });
+        // kept big variables at their C positions, a summed one at each
+        // new (small-only) variable's position: C is an in-place relabel of
+        // the big operand when no diagonal read is involved.  Both bits of a
+        // diagonal read go to the top, so the read touches exactly the
+        // diagonal half of the big operand in contiguous runs.
         std::vector<int> Lg;
         size_t si = 0;
+        std::vector<const Comp*> K1;
+        for (const Comp* c : K)
+          if (nbig(c) == 1) K1.push_back(c);
         for (int i : L) {
-          if (has(F, i)) {
-            if (si < Sh.size()) Lg.push_back(Sh[si++]);
-          } else {
-            Lg.push_back(i);
-          }
+          const Comp* c = ccomp[i];
+          if (nbig(c) == 1) Lg.push_back(bigv(c)[0]);
+          else if (nbig(c) == 0 && si < K1.size()) Lg.push_back(bigv(K1[si++])[0]);
         }
-        while (si < Sh.size()) Lg.push_back(Sh[si++]);
+        while (si < K1.size()) Lg.push_back(bigv(K1[si++])[0]);
+        for (int i : L) {
+          const Comp* c = ccomp[i];
+          if (nbig(c) > 1)
+            for (int t = 0; t < nbig(c); ++t) Lg.push_back(bigv(c)[t]);
+        }
+        for (const Comp* c : K)
+          if (nbig(c) > 1)
+            for (int t = 0; t < nbig(c); ++t) Lg.push_back(bigv(c)[t]);
+        for (const Comp* c = c0; c != c1; ++c)
+          if (c->c >= 0) ccomp[c->c] = nullptr;
         want(big, Lg);
         if (!p.is_leaf(sm)) want(sm, natural(sm));
         break;
       }
       case NC_GEMM: {
-        std::vector<int> K = inter(eff[a], eff[b]);
-        std::vector<int> M = minus(eff[a], K), N = minus(eff[b], K);
+        K.clear();
+        M.clear();
+        N.clear();
+        Bt.clear();
+        for (const Comp* c = c0; c != c1; ++c) {
+          if (c->c < 0) K.push_back(c);
+          else if (c->na && c->nb) Bt.push_back(c);
+          else if (c->na) M.push_back(c);
+          else N.push_back(c);
+        }
+        std::sort(K.begin(), K.end(), [&](const Comp* x, const Comp* y) { return x->a[0] < y->a[0]; });
         // K order: follow a fixed-layout (leaf) operand when there is one
         int ref = p.is_leaf(a) ? a : (p.is_leaf(b) ? b : -1);
         if (ref >= 0) {
           set_pos(g.layout[ref]);
-          std::sort(K.begin(), K.end(), [&](int x, int y) { return pos[x] < pos[y]; });
+          const bool ra = ref == a;
+          std::sort(K.begin(), K.end(), [&](const Comp* x, const Comp* y) {
+            return pos[ra ? x->a[0] : x->b[0]] < pos[ra ? y->a[0] : y->b[0]];
+          });
           clr_pos(g.layout[ref]);
         }
         set_pos(L);
-        std::sort(M.begin(), M.end(), [&](int x, int y) { return pos[x] < pos[y]; });
-        std::sort(N.begin(), N.end(), [&](int x, int y) { return pos[x] < pos[y]; });
+        auto by_c = [&](const Comp* x, const Comp* y) { return pos[x->c] < pos[y->c]; };
+        std::sort(M.begin(), M.end(), by_c);
+        std::sort(N.begin(), N.end(), by_c);
+        std::sort(Bt.begin(), Bt.end(), by_c);
         clr_pos(L);
-        std::vector<int> La = K, Lb = K;
-        La.insert(La.end(), M.begin(), M.end());
-        Lb.insert(Lb.end(), N.begin(), N.end());
+        std::vector<int> La, Lb;
+        for (const Comp* c : K) La.push_back(c->a[0]), Lb.push_back(c->b[0]);
+        for (const Comp* c : M) La.push_back(c->a[0]);
+        for (const Comp* c : N) Lb.push_back(c->b[0]);
+        for (const Comp* c : Bt) La.push_back(c->a[0]), Lb.push_back(c->b[0]);
         want(a, La);
         want(b, Lb);
         break;
@@ -388,13 +692,53 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     }
   }
 
+  // physical values of a leaf: raw values when untied, else the compressed
+  // block diagonal in the leaf's layout order (cvals)
+  auto leaf_strides = [&](int l) {
+    const auto& ro = p.ref_order[l];
+    std::vector<int64_t> stride(ro.size());
+    int64_t st = 1;
+    for (int q = (int)ro.size() - 1; q >= 0; --q) {
+      stride[q] = st;
+      st *= p.dom[ro[q]];
+    }
+    return stride;
+  };
+  // raw offset (kept indices only) of physical entry e of leaf l
+  auto leaf_entry_src = [&](int l, int64_t e, const std::vector<int64_t>& stride) {
+    const auto& Ll = g.layout[l];
+    const auto& ro = p.ref_order[l];
+    int64_t src = 0, rem = e;
+    for (size_t t = 0; t < Ll.size(); ++t) {
+      const int d = (int)(rem % p.dom[Ll[t]]);
+      rem /= p.dom[Ll[t]];
+      for (size_t q = 0; q < ro.size(); ++q)
+        if (!drop[ro[q]] && var_of(l, ro[q]) == Ll[t]) src += d * stride[q];
+    }
+    return src;
+  };
+  std::vector<int64_t> cval_off(p.NL, -1);
+  for (int l = 0; l < p.NL; ++l) {
+    if (!leaf_tied[l]) continue;
+    bool sl = false;
+    for (int i : p.ref_order[l]) sl |= (bool)drop[i];
+    if (sl) continue;  // sliced leaves are gathered per slice (k_select)
+    auto stride = leaf_strides(l);
+    cval_off[l] = (int64_t)g.cvals.size();
+    for (int64_t e = 0; e < size[l]; ++e) g.cvals.push_back(p.lval[p.lval_off[l] + leaf_entry_src(l, e, stride)]);
+  }
+  auto leaf_phys = [&](int l, int64_t e) {
+    return cval_off[l] >= 0 ? g.cvals[cval_off[l] + e] : p.lval[p.lval_off[l] + e];
+  };
+
   tmark("exact relabels");
   // ---- exact relabels ---------------------------------------------------------
-  // big x (2x2 identity) piece: C[.., f, ..] = sum_s A[.., s, ..] I[s, f] is A
-  // with index s renamed f (x*1 + y*0 == x for finite y, bit for bit).  The
-  // layout pass put f at s's address bit, so C IS A's buffer: no launch, no
-  // traffic.  (In C2 these are 2004 of 2783 big x piece nodes: the
-  // non-carrier pieces of factored copy tensors, factoring.py:194-206.)
+  // C IS the big operand's buffer (no launch, no traffic) when the small
+  // operand is an all-ones tie piece (every big variable maps to one C
+  // variable at the same address bit, nothing is summed, x*1 == x), or, with
+  // dense variables, a 2x2 identity piece (x*1 + y*0 == x for finite y).
+  // These are the non-carrier pieces of factored copy tensors
+  // (factoring.py:194-206).
   std::vector<int> alias_src(S, -1);
   if (!std::getenv("TC_NO_ALIAS")) {
     for (int k = 0; k < p.NN; ++k) {
@@ -402,109 +746,65 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       if (g.cls[v] != NC_STREAM) continue;
       const bool b_small = eff[b].size() <= eff[a].size();
       const int big = b_small ? a : b, sm = b_small ? b : a;
-      if (p.is_leaf(big) || !p.is_leaf(sm) || p.sets[sm].size() != 2 || eff[sm].size() != 2) continue;
-      std::vector<int> Sh = inter(eff[a], eff[b]);
-      std::vector<int> F = minus(eff[sm], Sh);
-      if (Sh.size() != 1 || F.size() != 1) continue;
-      const double* q = p.lval.data() + p.lval_off[sm];
-      if (!(q[0] == 1.0 && q[3] == 1.0 && q[1] == 0.0 && q[2] == 0.0)) continue;
+      if (p.is_leaf(big) || !p.is_leaf(sm)) continue;
       const auto& Lv = g.layout[v];
       const auto& Lg = g.layout[big];
-      bool same = Lv.size() == Lg.size();
-      for (size_t i = 0; same && i < Lv.size(); ++i)
-        same = Lv[i] == Lg[i] || (Lg[i] == Sh[0] && Lv[i] == F[0]);
-      if (!same) continue;
+      if (Lv.size() != Lg.size()) continue;
+      auto [c0, c1] = comps(v);
+      bool ok = false;
+      if (leaf_tied[sm]) {
+        ok = true;
+        for (int64_t e = 0; ok && e < size[sm]; ++e) ok = leaf_phys(sm, e) == 1.0;
+        for (const Comp* c = c0; ok && c != c1; ++c) {
+          const int nbig = b_small ? c->na : c->nb;
+          if (c->c < 0 || nbig != 1) ok = false;
+        }
+        if (ok) {
+          for (const Comp* c = c0; c != c1; ++c) ccomp[c->c] = c;
+          for (size_t i = 0; ok && i < Lv.size(); ++i) {
+            const Comp* c = ccomp[Lv[i]];
+            ok = c && (b_small ? c->a[0] : c->b[0]) == Lg[i];
+          }
+          for (const Comp* c = c0; c != c1; ++c) ccomp[c->c] = nullptr;
+        }
+      } else if (p.sets[sm].size() == 2 && eff[sm].size() == 2) {
+        // dense identity piece: one summed index s, one new index f
+        int s = -1, f = -1, nk = 0, nf = 0;
+        for (const Comp* c = c0; c != c1; ++c) {
+          const int nbig = b_small ? c->na : c->nb;
+          if (c->c < 0) s = b_small ? c->a[0] : c->b[0], nk++;
+          else if (nbig == 0) f = c->c, nf++;
+        }
+        const double* q = p.lval.data() + p.lval_off[sm];
+        ok = nk == 1 && nf == 1 && q[0] == 1.0 && q[3] == 1.0 && q[1] == 0.0 && q[2] == 0.0;
+        for (size_t i = 0; ok && i < Lv.size(); ++i) ok = Lv[i] == Lg[i] || (Lg[i] == s && Lv[i] == f);
+      }
+      if (!ok) continue;
       g.cls[v] = NC_ALIAS;
       alias_src[v] = big;
       g.n_alias++;
     }
   }
 
-  tmark("chain segments");
-  // ---- chain segments: runs of STREAM nodes fused into one launch -----------
-  // v_{i+1}'s big operand is v_i.  Inner bits = every index of the input the
-  // segment touches plus the ones it creates; all must fit kChainU at every
-  // step (touching a new input index widens every earlier step too).
-  struct Seg {
-    std::vector<int> nodes, big, small;
-    std::vector<int> u0;     // inner indices loaded with the input tile
-    std::vector<int> inner;  // inner indices of the current output (sorted)
-    std::vector<int> w;      // inner width before step 0 and after each step
-  };
-  std::vector<Seg> segs;
-  std::vector<int> seg_of(S, -1);
-  // smem chain fusion is opt-in (TC_CHAIN=1): measured slower than graph-
-  // concurrent k_stream launches on C2/C1b
-  const bool fuse_chains = std::getenv("TC_CHAIN") != nullptr;
-  // fusion pays where launches dominate (small tensors); big tensors stream at
-  // HBM speed through k_stream with L2 reuse between consecutive steps
-  int chain_max_bits = 20;
-  if (const char* e = std::getenv("TC_CHAIN_MAX_BITS")) chain_max_bits = std::atoi(e);
-  for (int k = 0; k < p.NN && fuse_chains; ++k) {
-    const int v = p.NL + k, a = p.left[k], b = p.right[k];
-    if (g.cls[v] != NC_STREAM) continue;
-    if ((int)std::max(eff[a].size(), eff[b].size()) > chain_max_bits || (int)eff[v].size() > chain_max_bits) continue;
-    const bool b_small = eff[b].size() <= eff[a].size();
-    const int big = b_small ? a : b, sm = b_small ? b : a;
-    std::vector<int> Sh = inter(eff[a], eff[b]);
-    std::vector<int> F = minus(eff[sm], Sh);
-    if (!p.is_leaf(big) && seg_of[big] >= 0) {
-      Seg& sg = segs[seg_of[big]];
-      if (sg.nodes.back() == big && (int)sg.nodes.size() < kChainMax) {
-        std::vector<int> s_orig = minus(Sh, sg.inner);
-        std::vector<int> un;
-        std::set_union(sg.inner.begin(), sg.inner.end(), Sh.begin(), Sh.end(), std::back_inserter(un));
-        std::vector<int> nin = minus(un, Sh);
-        std::vector<int> nin2;
-        std::set_union(nin.begin(), nin.end(), F.begin(), F.end(), std::back_inserter(nin2));
-        int mx = (int)nin2.size();
-        for (int x : sg.w) mx = std::max(mx, x + (int)s_orig.size());
-        if (mx <= kChainU) {
-          for (int& x : sg.w) x += (int)s_orig.size();
-          sg.w.push_back((int)nin2.size());
-          for (int x : s_orig) sg.u0.push_back(x);
-          sg.inner = nin2;
-          sg.nodes.push_back(v);
-          sg.big.push_back(big);
-          sg.small.push_back(sm);
-          seg_of[v] = seg_of[big];
-          continue;
-        }
-      }
-    }
-    Seg sg;
-    sg.nodes = {v};
-    sg.big = {big};
-    sg.small = {sm};
-    sg.u0 = Sh;
-    sg.inner = F;
-    sg.w = {(int)Sh.size(), (int)F.size()};
-    seg_of[v] = (int)segs.size();
-    segs.push_back(sg);
-  }
-
   tmark("leaves");
-  // ---- leaves: plain or per-slice selected ----------------------------------
+  // ---- leaves: plain, compressed, or per-slice selected ----------------------
   g.loc.assign(S, Loc{LOC_LEAF, 0});
   std::vector<int64_t> pv(g.chosen.size(), 1);
   for (int j = (int)g.chosen.size() - 2; j >= 0; --j) pv[j] = pv[j + 1] * g.chosen_dim[j + 1];
   std::vector<int> chosen_slot(p.NI, -1);
   for (size_t j = 0; j < g.chosen.size(); ++j) chosen_slot[g.chosen[j]] = (int)j;
+  const int64_t nraw = (int64_t)p.lval.size();
   for (int l = 0; l < p.NL; ++l) {
     const auto& ro = p.ref_order[l];
     bool sl = false;
     for (int i : ro) sl |= (bool)drop[i];
     if (!sl) {
-      g.loc[l] = Loc{LOC_LEAF, p.lval_off[l]};
+      // compressed leaves follow the raw values in the device leaf buffer
+      g.loc[l] = cval_off[l] >= 0 ? Loc{LOC_LEAF, nraw + cval_off[l]} : Loc{LOC_LEAF, p.lval_off[l]};
       continue;
     }
     g.loc[l] = Loc{LOC_SLICED, g.sliced_doubles};
-    std::vector<int64_t> stride(ro.size());
-    int64_t st = 1;
-    for (int q = (int)ro.size() - 1; q >= 0; --q) {
-      stride[q] = st;
-      st *= p.dom[ro[q]];
-    }
+    auto stride = leaf_strides(l);
     int32_t t0 = (int32_t)g.sel_terms.size();
     for (size_t q = 0; q < ro.size(); ++q)
       if (drop[ro[q]]) {
@@ -512,19 +812,9 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         g.sel_terms.push_back(SelTerm{pv[j], g.chosen_dim[j], stride[q]});
       }
     int32_t nt = (int32_t)g.sel_terms.size() - t0;
-    // effective entries in effective layout order (LSB-first = reversed ref order)
-    std::vector<int> kq;  // positions in ro of kept indices, row-major order
-    for (size_t q = 0; q < ro.size(); ++q)
-      if (!drop[ro[q]]) kq.push_back((int)q);
-    for (int64_t e = 0; e < size[l]; ++e) {
-      int64_t rem = e, src = p.lval_off[l];
-      for (int q = (int)kq.size() - 1; q >= 0; --q) {
-        int64_t d = p.dom[ro[kq[q]]];
-        src += (rem % d) * stride[kq[q]];
-        rem /= d;
-      }
-      g.sel_ent.push_back(SelEntry{g.sliced_doubles + e, src, t0, nt});
-    }
+    // physical entries in layout order (LSB-first = reversed ref order)
+    for (int64_t e = 0; e < size[l]; ++e)
+      g.sel_ent.push_back(SelEntry{g.sliced_doubles + e, p.lval_off[l] + leaf_entry_src(l, e, stride), t0, nt});
     g.sliced_doubles += size[l];
   }
 
@@ -629,7 +919,6 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     const char* env = std::getenv("TC_ARENA_REUSE");
     arena.no_reuse = env ? std::atoi(env) == 0 : total <= no_reuse_limit;
   }
-  tmark("arena policy");
   std::vector<int> producer(S, -1);
   int sel_step = -1;
   if (!g.sel_ent.empty()) {
@@ -659,8 +948,26 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     g.steps.push_back(st);
   }
   tmark("tiny descriptors");
-  // tiny descriptors, ordered by level then group
-  std::vector<int64_t> str_a(p.NI, 0), str_b(p.NI, 0);  // index -> stride (0: absent)
+  // tiny descriptors, ordered by level then group.  Digit strides are sums
+  // over a component's variables (a diagonal read has two address bits).
+  std::vector<int64_t> str_a(p.NI, 0), str_b(p.NI, 0);  // variable -> stride (0: absent)
+  auto comp_strides = [&](const Comp* c, int64_t& sa, int64_t& sb) {
+    sa = sb = 0;
+    for (int t = 0; t < c->na; ++t) sa += str_a[c->a[t]];
+    for (int t = 0; t < c->nb; ++t) sb += str_b[c->b[t]];
+  };
+  auto load_strides = [&](const std::vector<int>& La, const std::vector<int>& Lb) {
+    int64_t st2 = 1;
+    for (int i : La) {
+      str_a[i] = st2;
+      st2 *= p.dom[i];
+    }
+    st2 = 1;
+    for (int i : Lb) {
+      str_b[i] = st2;
+      st2 *= p.dom[i];
+    }
+  };
   std::vector<std::vector<int>> level_groups(nlevels);
   for (size_t gi = 0; gi < groups.size(); ++gi) level_groups[glevel[gi]].push_back((int)gi);
   std::vector<std::pair<int32_t, int32_t>> level_range(nlevels);
@@ -687,42 +994,36 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         opnd(b, lb, tn.sb);
         if (v == r) lo = g.loc[r];
         else tn.sout = soff[v];
-        // digits: output indices in C's layout order, then the shared ones
+        // digits: output variables in C's layout order, then the summed ones
         const auto& La = g.layout[a];
         const auto& Lb = g.layout[b];
         const auto& Lc = g.layout[v];
-        int64_t st2 = 1;
-        for (int i : La) {
-          str_a[i] = st2;
-          st2 *= p.dom[i];
-        }
-        st2 = 1;
-        for (int i : Lb) {
-          str_b[i] = st2;
-          st2 *= p.dom[i];
-        }
+        load_strides(La, Lb);
+        auto [c0, c1] = comps(v);
+        for (const Comp* c = c0; c != c1; ++c)
+          if (c->c >= 0) ccomp[c->c] = c;
         tn.dig = (int32_t)g.tiny_digits.size();
         bool p2 = true;
         for (int i : Lc) {
-          g.tiny_digits.push_back(TinyDigit{p.dom[i], (int32_t)str_a[i], (int32_t)str_b[i], 0});
+          int64_t sa, sb;
+          comp_strides(ccomp[i], sa, sb);
+          g.tiny_digits.push_back(TinyDigit{p.dom[i], (int32_t)sa, (int32_t)sb, 0});
           p2 &= (p.dom[i] == 2);
         }
         int64_t ssz = 1;
         int ns = 0;
-        const auto& Ea = eff[a];
-        const auto& Eb = eff[b];
-        for (size_t x = 0, y = 0; x < Ea.size() && y < Eb.size();) {
-          if (Ea[x] < Eb[y]) ++x;
-          else if (Eb[y] < Ea[x]) ++y;
-          else {
-            const int i = Ea[x];
-            g.tiny_digits.push_back(TinyDigit{p.dom[i], (int32_t)str_a[i], (int32_t)str_b[i], 0});
-            p2 &= (p.dom[i] == 2);
-            ssz *= p.dom[i];
-            ++ns;
-            ++x;
-            ++y;
+        for (const Comp* c = c0; c != c1; ++c) {  // sorted by smallest variable
+          if (c->c >= 0) {
+            ccomp[c->c] = nullptr;
+            continue;
           }
+          int64_t sa, sb;
+          comp_strides(c, sa, sb);
+          const int d = p.dom[c->a[0]];
+          g.tiny_digits.push_back(TinyDigit{d, (int32_t)sa, (int32_t)sb, 0});
+          p2 &= (d == 2);
+          ssz *= d;
+          ++ns;
         }
         for (int i : La) str_a[i] = 0;
         for (int i : Lb) str_b[i] = 0;
@@ -756,41 +1057,22 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     g.steps[tiny_step[lv]].work = level_range[lv].second - level_range[lv].first;
   }
 
-  tmark("big nodes in postord");
-  // big nodes in postorder
-  auto stride_map = [&](const std::vector<int>& L) {
-    SmallMap<int64_t> m;
-    int64_t st2 = 1;
-    for (int i : L) {
-      m[i] = st2;
-      st2 *= p.dom[i];
-    }
-    return m;
-  };
+  tmark("node work");
+  // physical (executed) work per node: operands and output once, 2*prod of
+  // the component domains flops
   std::vector<double> node_bytes(S, 0.0), node_flops(S, 0.0);
   for (int k = 0; k < p.NN; ++k) {
     int v = p.NL + k, a = p.left[k], b = p.right[k];
-    // 2 * prod of the union's domains (eff sets are sorted, drop-free)
-    u128 un = 1;
-    {
-      const auto& Ea = eff[a];
-      const auto& Eb = eff[b];
-      size_t x = 0, y = 0;
-      while (x < Ea.size() || y < Eb.size()) {
-        int i;
-        if (y == Eb.size() || (x < Ea.size() && Ea[x] < Eb[y])) i = Ea[x++];
-        else if (x == Ea.size() || Eb[y] < Ea[x]) i = Eb[y++];
-        else i = Ea[x++], ++y;
-        un *= (u128)p.dom[i];
-        if (un > ((u128)1 << 100)) fail(TC_OVERFLOW, "contraction size overflows 2^100");
-      }
-    }
-    const u128 fl = 2 * un;
-    g.alg_flops += fl;
-    g.alg_bytes += (u128)8 * (u128)(size[a] + size[b] + size[v]);
+    double fl = 2;
+    for (auto [c, ce] = comps(v); c != ce; ++c) fl *= p.dom[c->na ? c->a[0] : c->b[0]];
     node_bytes[v] = 8.0 * (double)(size[a] + size[b] + size[v]);
-    node_flops[v] = (double)fl;
+    node_flops[v] = fl;
+    if (g.cls[v] != NC_ALIAS) {
+      g.phys_bytes += (u128)(8 * (size[a] + size[b] + size[v]));
+      g.phys_flops += (u128)fl;
+    }
   }
+
   tmark("emit nodes");
   auto emit_node = [&](int v) {
     const int k = v - p.NL, a = p.left[k], b = p.right[k];
@@ -809,65 +1091,89 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     const auto& La = g.layout[a];
     const auto& Lb = g.layout[b];
     const auto& Lc = g.layout[v];
+    auto [c0, c1] = comps(v);
     bool done = false;
     if (g.cls[v] == NC_STREAM) {
       try {
-        bool b_small = eff[b].size() <= eff[a].size();
-        int big = b_small ? a : b, sm = b_small ? b : a;
+        const bool b_small = eff[b].size() <= eff[a].size();
+        const int big = b_small ? a : b, sm = b_small ? b : a;
         const auto& Lg = g.layout[big];
         const auto& Lq = g.layout[sm];
-        std::vector<int> Sh = inter(eff[a], eff[b]);
-        std::vector<int> F = minus(eff[sm], Sh);
+        auto bigv = [&](const Comp* c) { return b_small ? c->a : c->b; };
+        auto nbig = [&](const Comp* c) { return b_small ? c->na : c->nb; };
+        auto smv = [&](const Comp* c) { return b_small ? c->b : c->a; };
+        auto nsm = [&](const Comp* c) { return b_small ? c->nb : c->na; };
         SmallMap<int> pg, pc, pq;
         for (size_t q = 0; q < Lg.size(); ++q) pg[Lg[q]] = (int)q;
         for (size_t q = 0; q < Lc.size(); ++q) pc[Lc[q]] = (int)q;
         for (size_t q = 0; q < Lq.size(); ++q) pq[Lq[q]] = (int)q;
-        // x bits: kept indices of big, in C address order
-        std::vector<std::pair<int, int>> xa, xc;
-        int j = 0;
-        for (size_t q = 0; q < Lc.size(); ++q) {
-          int i = Lc[q];
-          if (has(F, i)) continue;
-          xc.push_back({j, (int)q});
-          j++;
+        K.clear();
+        N.clear();
+        for (const Comp* c = c0; c != c1; ++c) {
+          if (c->c >= 0) ccomp[c->c] = c;
+          if (c->c < 0) K.push_back(c);
+          else if (nbig(c) == 0) N.push_back(c);
         }
-        // xa needs src ascending: same j order, dst = position in big
-        j = 0;
-        for (size_t q = 0; q < Lc.size(); ++q) {
-          int i = Lc[q];
-          if (has(F, i)) continue;
-          xa.push_back({j, pg[i]});
-          j++;
-        }
+        auto small_off = [&](const Comp* c) {
+          int64_t o = 0;
+          for (int t = 0; t < nsm(c); ++t) o += (int64_t)1 << pq[smv(c)[t]];
+          return o;
+        };
+        // x bits: C variables with a big-side variable, in C address order
+        std::vector<std::pair<int, int>> xa, xa2, xc;
         StreamParams sp{};
+        int j = 0;
+        bool bad = false;
+        for (size_t q = 0; q < Lc.size(); ++q) {
+          const Comp* c = ccomp[Lc[q]];
+          if (nbig(c) == 0) continue;
+          xc.push_back({j, (int)q});
+          xa.push_back({j, pg[bigv(c)[0]]});
+          if (nbig(c) == 2) xa2.push_back({j, pg[bigv(c)[1]]});
+          if (nsm(c) > 0) {  // batch variable: also indexes the small operand
+            if (sp.nbt == kStreamMaxBatch) bad = true;
+            else {
+              sp.bt_xbit[sp.nbt] = j;
+              sp.bt_poff[sp.nbt] = small_off(c);
+              sp.nbt++;
+              if (j < kStreamChunkBits) sp.nlb++;
+            }
+          }
+          j++;
+        }
+        for (const Comp* c = c0; c != c1; ++c)
+          if (c->c >= 0) ccomp[c->c] = nullptr;
+        if (bad) throw Error{-1, "batch"};
         sp.xa = make_runs(xa);
+        sp.xa2 = make_runs(xa2);
         sp.xc = make_runs(xc);
         sp.nx = (int64_t)1 << j;
-        int ns = (int)Sh.size(), nf = (int)F.size();
-        // order F by C position, S by big-operand position
-        std::sort(F.begin(), F.end(), [&](int x, int y) { return pc[x] < pc[y]; });
-        std::sort(Sh.begin(), Sh.end(), [&](int x, int y) { return pg[x] < pg[y]; });
+        const int ns = (int)K.size(), nf = (int)N.size();
+        // N by C position, K by big-operand position
+        std::sort(N.begin(), N.end(), [&](const Comp* x, const Comp* y) { return pc[x->c] < pc[y->c]; });
+        std::sort(K.begin(), K.end(), [&](const Comp* x, const Comp* y) { return pg[bigv(x)[0]] < pg[bigv(y)[0]]; });
         for (int s = 0; s < (1 << ns); ++s) {
           int64_t o = 0, oq = 0;
           for (int t = 0; t < ns; ++t)
             if (s >> t & 1) {
-              o += (int64_t)1 << pg[Sh[t]];
-              oq += (int64_t)1 << pq[Sh[t]];
+              for (int u = 0; u < nbig(K[t]); ++u) o += (int64_t)1 << pg[bigv(K[t])[u]];
+              oq += small_off(K[t]);
             }
           sp.offA[s] = o;
           for (int f = 0; f < (1 << nf); ++f) {
             int64_t of = 0;
             for (int t = 0; t < nf; ++t)
-              if (f >> t & 1) of += (int64_t)1 << pq[F[t]];
+              if (f >> t & 1) of += small_off(N[t]);
             sp.offP[s * (1 << nf) + f] = (int32_t)(oq + of);
           }
         }
         for (int f = 0; f < (1 << nf); ++f) {
           int64_t o = 0;
           for (int t = 0; t < nf; ++t)
-            if (f >> t & 1) o += (int64_t)1 << pc[F[t]];
+            if (f >> t & 1) o += (int64_t)1 << pc[N[t]->c];
           sp.offC[f] = o;
         }
+        if (((1 << sp.nlb) << (ns + nf)) > kStreamSmemMax) throw Error{-1, "small operand"};
         st.kind = ST_STREAM;
         st.sp = sp;
         st.ns = ns;
@@ -880,18 +1186,33 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       } catch (const Error& e) {
         if (e.status != -1) throw;
       }
-    } else if (g.cls[v] == NC_GEMM) {
+    }
+    bool diag = false;
+    for (const Comp* c = c0; c != c1; ++c) diag |= c->na > 1 || c->nb > 1;
+    // GEMM: its own class, or a stream node whose shape the stream kernel
+    // cannot stage (any layout works: the tile tables gather)
+    if (!done && !diag && (g.cls[v] == NC_GEMM || g.cls[v] == NC_STREAM)) {
       try {
-        std::vector<int> K = inter(eff[a], eff[b]);
-        std::vector<int> M = minus(eff[a], K), N = minus(eff[b], K);
+        K.clear();
+        M.clear();
+        N.clear();
+        Bt.clear();
+        for (const Comp* c = c0; c != c1; ++c) {
+          if (c->c < 0) K.push_back(c);
+          else if (c->na && c->nb) Bt.push_back(c);
+          else if (c->na) M.push_back(c);
+          else N.push_back(c);
+        }
         SmallMap<int> pa, pb, pc;
         for (size_t q = 0; q < La.size(); ++q) pa[La[q]] = (int)q;
         for (size_t q = 0; q < Lb.size(); ++q) pb[Lb[q]] = (int)q;
         for (size_t q = 0; q < Lc.size(); ++q) pc[Lc[q]] = (int)q;
-        std::sort(M.begin(), M.end(), [&](int x, int y) { return pc[x] < pc[y]; });
-        std::sort(N.begin(), N.end(), [&](int x, int y) { return pc[x] < pc[y]; });
-        std::sort(K.begin(), K.end(), [&](int x, int y) { return pa[x] < pa[y]; });
-        const int m = (int)M.size(), n = (int)N.size(), kk = (int)K.size();
+        auto by_c = [&](const Comp* x, const Comp* y) { return pc[x->c] < pc[y->c]; };
+        std::sort(M.begin(), M.end(), by_c);
+        std::sort(N.begin(), N.end(), by_c);
+        std::sort(Bt.begin(), Bt.end(), by_c);
+        std::sort(K.begin(), K.end(), [&](const Comp* x, const Comp* y) { return pa[x->a[0]] < pa[y->a[0]]; });
+        const int m = (int)M.size(), n = (int)N.size(), kk = (int)K.size(), nbt = (int)Bt.size();
         // 128x64 CTA tiles (8 warps) for large GEMMs, 64x64 and below otherwise
         static const int big_tiles = std::getenv("TC_GEMM_BIG") ? std::atoi(std::getenv("TC_GEMM_BIG")) : 1;
         static const int big_k = std::getenv("TC_GEMM_BIG_K") ? std::atoi(std::getenv("TC_GEMM_BIG_K")) : 4;
@@ -901,36 +1222,36 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         gp.m_hi = std::max(0, m - MT);
         gp.n_hi = std::max(0, n - NT);
         gp.k_tiles = (int64_t)1 << std::max(0, kk - KT);
+        gp.bt_bits = nbt;
         std::vector<std::pair<int, int>> r;
-        r.clear();
-        for (int t = MT; t < (int)M.size(); ++t) r.push_back({t - MT, pa[M[t]]});
-        gp.a_m = make_runs(r);
-        r.clear();
-        for (int t = KT; t < (int)K.size(); ++t) r.push_back({t - KT, pa[K[t]]});
-        gp.a_k = make_runs(r);
-        r.clear();
-        for (int t = NT; t < (int)N.size(); ++t) r.push_back({t - NT, pb[N[t]]});
-        gp.b_n = make_runs(r);
-        r.clear();
-        for (int t = KT; t < (int)K.size(); ++t) r.push_back({t - KT, pb[K[t]]});
-        gp.b_k = make_runs(r);
-        r.clear();
-        for (int t = MT; t < (int)M.size(); ++t) r.push_back({t - MT, pc[M[t]]});
-        gp.c_m = make_runs(r);
-        r.clear();
-        for (int t = NT; t < (int)N.size(); ++t) r.push_back({t - NT, pc[N[t]]});
-        gp.c_n = make_runs(r);
-        auto tmap = [&](SmallMap<int>& P, const std::vector<int>& R1, int n1,
-                        const std::vector<int>& R2, int n2) {
+        auto runs = [&](const std::vector<const Comp*>& V, int from, auto var, SmallMap<int>& P) {
+          r.clear();
+          for (int t = from; t < (int)V.size(); ++t) r.push_back({t - from, P[var(V[t])]});
+          return make_runs(r);
+        };
+        auto va = [](const Comp* c) { return c->a[0]; };
+        auto vb = [](const Comp* c) { return c->b[0]; };
+        auto vc = [](const Comp* c) { return c->c; };
+        gp.a_m = runs(M, MT, va, pa);
+        gp.a_k = runs(K, KT, va, pa);
+        gp.b_n = runs(N, NT, vb, pb);
+        gp.b_k = runs(K, KT, vb, pb);
+        gp.c_m = runs(M, MT, vc, pc);
+        gp.c_n = runs(N, NT, vc, pc);
+        gp.a_bt = runs(Bt, 0, va, pa);
+        gp.b_bt = runs(Bt, 0, vb, pb);
+        gp.c_bt = runs(Bt, 0, vc, pc);
+        auto tmap = [&](SmallMap<int>& P, const std::vector<const Comp*>& R1, auto v1, int n1,
+                        const std::vector<const Comp*>& R2, auto v2, int n2) {
           // R1 tile bits -> kind 0, R2 tile bits -> kind 1; bits past the
           // shape are virtual (pos -1), placed after the real ones
           std::vector<std::tuple<int, int, int>> bits, virt;  // pos, kind, sub
           for (int t = 0; t < n1; ++t) {
-            if (t < (int)R1.size()) bits.emplace_back(P[R1[t]], 0, t);
+            if (t < (int)R1.size()) bits.emplace_back(P[v1(R1[t])], 0, t);
             else virt.emplace_back(-1, 0, t);
           }
           for (int t = 0; t < n2; ++t) {
-            if (t < (int)R2.size()) bits.emplace_back(P[R2[t]], 1, t);
+            if (t < (int)R2.size()) bits.emplace_back(P[v2(R2[t])], 1, t);
             else virt.emplace_back(-1, 1, t);
           }
           std::sort(bits.begin(), bits.end());
@@ -944,12 +1265,12 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
           }
           return tm;
         };
-        gp.ta = tmap(pa, M, MT, K, KT);
-        gp.tb = tmap(pb, N, NT, K, KT);
-        gp.tc = tmap(pc, M, MT, N, NT);
+        gp.ta = tmap(pa, M, va, MT, K, va, KT);
+        gp.tb = tmap(pb, N, vb, NT, K, vb, KT);
+        gp.tc = tmap(pc, M, vc, MT, N, vc, NT);
         gp.grid_swizzle_log = std::min(gp.m_hi, 3);
         // split-K when the output tiles cannot fill the machine
-        const int64_t tiles = (int64_t)1 << (gp.m_hi + gp.n_hi);
+        const int64_t tiles = (int64_t)1 << (gp.m_hi + gp.n_hi + nbt);
         int64_t splits = 1;
         if (tiles < 2 * kSMs && gp.k_tiles >= 8)
           splits = std::min<int64_t>(gp.k_tiles / 4, (2 * kSMs + tiles - 1) / tiles);
@@ -968,20 +1289,36 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       }
     }
     if (!done) {
-      auto ma = stride_map(La), mb = stride_map(Lb);
+      load_strides(La, Lb);
+      for (const Comp* c = c0; c != c1; ++c)
+        if (c->c >= 0) ccomp[c->c] = c;
       GenericParams np{};
       st.gdig_off = (int64_t)g.gdigits.size();
-      for (int i : Lc) g.gdigits.push_back(GDigit{p.dom[i], ma.count(i) ? ma[i] : 0, mb.count(i) ? mb[i] : 0});
-      std::vector<int> Sh = inter(eff[a], eff[b]);
-      int64_t ssz = 1;
-      for (int i : Sh) {
-        g.gdigits.push_back(GDigit{p.dom[i], ma[i], mb[i]});
-        ssz *= p.dom[i];
+      for (int i : Lc) {
+        int64_t sa, sb;
+        comp_strides(ccomp[i], sa, sb);
+        g.gdigits.push_back(GDigit{p.dom[i], sa, sb});
       }
+      int64_t ssz = 1;
+      int ns = 0;
+      for (const Comp* c = c0; c != c1; ++c) {
+        if (c->c >= 0) {
+          ccomp[c->c] = nullptr;
+          continue;
+        }
+        int64_t sa, sb;
+        comp_strides(c, sa, sb);
+        const int d = p.dom[c->a[0]];
+        g.gdigits.push_back(GDigit{d, sa, sb});
+        ssz *= d;
+        ++ns;
+      }
+      for (int i : La) str_a[i] = 0;
+      for (int i : Lb) str_b[i] = 0;
       np.c_size = size[v];
       np.s_size = ssz;
       np.nc = (int32_t)Lc.size();
-      np.ns = (int32_t)Sh.size();
+      np.ns = ns;
       st.kind = ST_GENERIC;
       st.np = np;
       st.work = size[v];
@@ -1019,145 +1356,6 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       if (g.loc[c].kind == LOC_ARENA) arena.release(g.loc[c].off, bytes[c], me);
   };
 
-  // one fused launch for a multi-step chain segment; false if the address
-  // maps do not fit the kernel's run/tile limits (then: one launch per node)
-  auto emit_chain = [&](const Seg& sg) -> bool {
-    const int v1 = sg.nodes.front(), vk = sg.nodes.back();
-    const int A = sg.big.front();
-    const auto& La = g.layout[A];
-    const auto& Lc = g.layout[vk];
-    SmallMap<int> pa, pc;
-    for (size_t q = 0; q < La.size(); ++q) pa[La[q]] = (int)q;
-    for (size_t q = 0; q < Lc.size(); ++q) pc[Lc[q]] = (int)q;
-    // inner bookkeeping
-    std::vector<int> cur = sg.u0;  // inner bit j <-> index
-    std::vector<ChainStep> cs;
-    for (size_t i = 0; i < sg.nodes.size(); ++i) {
-      const int u = sg.nodes[i], sm = sg.small[i], bg = sg.big[i];
-      std::vector<int> Sh = inter(eff[bg], eff[sm]);
-      std::vector<int> F = minus(eff[sm], Sh);
-      const auto& Lq = g.layout[sm];
-      SmallMap<int> pq;
-      for (size_t q = 0; q < Lq.size(); ++q) pq[Lq[q]] = (int)q;
-      std::vector<int> nw;
-      for (int x : cur)
-        if (!has(Sh, x)) nw.push_back(x);
-      const int nkeep = (int)nw.size();
-      for (int x : F) nw.push_back(x);
-      if ((int)nw.size() > kChainU || (int)cur.size() > kChainU) return false;
-      ChainStep c{};
-      c.ns = (int)Sh.size();
-      c.nf = (int)F.size();
-      c.nnew = (int)nw.size();
-      auto cpos = [&](int x) { return (int)(std::find(cur.begin(), cur.end(), x) - cur.begin()); };
-      for (int s = 0; s < (1 << c.ns); ++s) {
-        int sb = 0, oq = 0;
-        for (int t = 0; t < c.ns; ++t)
-          if (s >> t & 1) {
-            sb |= 1 << cpos(Sh[t]);
-            oq += 1 << pq[Sh[t]];
-          }
-        c.stab[s] = (uint8_t)sb;
-        for (int f = 0; f < (1 << c.nf); ++f) {
-          int of = 0;
-          for (int t = 0; t < c.nf; ++t)
-            if (f >> t & 1) of += 1 << pq[F[t]];
-          c.offP[s * (1 << c.nf) + f] = oq + of;
-        }
-      }
-      for (int un = 0; un < (1 << c.nnew); ++un) {
-        int ub = 0, f = 0;
-        for (int j = 0; j < c.nnew; ++j)
-          if (un >> j & 1) {
-            if (j < nkeep) ub |= 1 << cpos(nw[j]);
-            else f |= 1 << (j - nkeep);
-          }
-        c.utab[un] = (uint16_t)(ub | (f << 8));
-      }
-      cs.push_back(c);
-      cur = nw;
-      (void)u;
-    }
-    const std::vector<int>& Uk = cur;
-    std::vector<int> O = minus(eff[A], [&] {
-      std::vector<int> s = sg.u0;
-      std::sort(s.begin(), s.end());
-      return s;
-    }());
-    std::sort(O.begin(), O.end(), [&](int x, int y) { return pa[x] < pa[y]; });
-    int umax = (int)sg.u0.size();
-    for (auto& c : cs) umax = std::max(umax, c.nnew);
-    int lbuf = 0;
-    while ((2 << lbuf) <= kChainBuf) ++lbuf;  // log2(kChainBuf)
-    // x_lo bits: as wide as the smem tile allows, but leave >= ~2 tiles per SM
-    const int xt = std::max(0, std::min({(int)O.size(), lbuf - umax, std::max(2, (int)O.size() - 9)}));
-    if (lbuf - umax < 0) return false;
-    ChainParams cp{};
-    cp.nsteps = (int)cs.size();
-    cp.xt = xt;
-    cp.n_tiles = (int64_t)1 << ((int)O.size() - xt);
-    std::vector<std::pair<int, int>> ra, rc;
-    for (int j = xt; j < (int)O.size(); ++j) {
-      ra.push_back({j - xt, pa[O[j]]});
-      rc.push_back({j - xt, pc[O[j]]});
-    }
-    try {
-      cp.a_hi = make_runs(ra);
-      cp.c_hi = make_runs(rc);
-    } catch (const Error& e) {
-      if (e.status != -1) throw;
-      return false;
-    }
-    auto tmap = [&](SmallMap<int>& P, const std::vector<int>& inner) {
-      std::vector<std::tuple<int, int, int>> bits;
-      for (int j = 0; j < xt; ++j) bits.emplace_back(P[O[j]], 0, j);
-      for (size_t t = 0; t < inner.size(); ++t) bits.emplace_back(P[inner[t]], 1, (int)t);
-      std::sort(bits.begin(), bits.end());
-      TileMap tm{};
-      tm.nbits = (int)bits.size();
-      for (size_t q = 0; q < bits.size(); ++q) {
-        tm.pos[q] = (int8_t)std::get<0>(bits[q]);
-        tm.kind[q] = (int8_t)std::get<1>(bits[q]);
-        tm.sub[q] = (int8_t)std::get<2>(bits[q]);
-      }
-      return tm;
-    };
-    cp.ta = tmap(pa, sg.u0);
-    cp.tc = tmap(pc, Uk);
-    Step st;
-    st.kind = ST_CHAIN;
-    st.slot = vk;
-    st.cp = cp;
-    st.la = g.loc[A];
-    st.chain_off = (int64_t)g.chain_steps.size();
-    for (size_t i = 0; i < cs.size(); ++i) {
-      g.chain_steps.push_back(cs[i]);
-      g.chain_piece.push_back(g.loc[sg.small[i]]);
-    }
-    st.work = cp.n_tiles;
-    for (int u : sg.nodes) {
-      st.alg_bytes += node_bytes[u];
-      st.alg_flops += node_flops[u];
-    }
-    if (producer[A] >= 0) st.deps.push_back(producer[A]);
-    for (int sm : sg.small)
-      if (producer[sm] >= 0) st.deps.push_back(producer[sm]);
-    haz.clear();
-    g.loc[vk] = Loc{LOC_ARENA, arena.alloc(bytes[vk], haz)};
-    for (int h : haz) st.deps.push_back(h);
-    st.lc = g.loc[vk];
-    const int me = (int)g.steps.size();
-    g.steps.push_back(st);
-    producer[vk] = me;
-    if (g.loc[A].kind == LOC_ARENA) arena.release(g.loc[A].off, bytes[A], me);
-    for (int sm : sg.small)
-      if (g.loc[sm].kind == LOC_ARENA) arena.release(g.loc[sm].off, bytes[sm], me);
-    g.n_stream += (int)sg.nodes.size();
-    g.n_chain++;
-    (void)v1;
-    return true;
-  };
-
   for (int k = 0; k < p.NN; ++k) {
     const int v = p.NL + k;
     if (g.cls[v] == NC_TINY) {
@@ -1174,20 +1372,47 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       producer[v] = producer[src];
       continue;
     }
-    if (g.cls[v] == NC_STREAM && seg_of[v] >= 0 && segs[seg_of[v]].nodes.size() > 1) {
-      const Seg& sg = segs[seg_of[v]];
-      if (v != sg.nodes.back()) continue;  // fused: no buffer, no launch
-      if (emit_chain(sg)) continue;
-      for (int u : sg.nodes) emit_node(u);
-      continue;
-    }
     emit_node(v);
   }
 
-  tmark("root copy into the p");
-  // root copy into the per-slice result slot, then advance the slice counter
-  g.R = size[p.root];
+  tmark("root copy");
+  // root copy into the per-slice result slot, then advance the slice counter.
+  // The result is dense over the root's kept indices in the reference's
+  // row-major order; a root with tied indices is expanded through root_map.
+  g.R = (int64_t)dsize[p.root];
   g.root_loc = g.loc[p.root];
+  if (g.R != size[p.root]) {
+    const auto& ro = p.ref_order[p.root];
+    const auto& Lr = g.layout[p.root];
+    std::vector<int> kept;
+    for (int i : ro)
+      if (!drop[i]) kept.push_back(i);
+    std::vector<int64_t> vstride(p.NI, 0);
+    int64_t st2 = 1;
+    for (int i : Lr) {
+      vstride[i] = st2;
+      st2 *= p.dom[i];
+    }
+    std::vector<int> var_digit(p.NI, -1);
+    g.root_map.resize((size_t)g.R);
+    for (int64_t r = 0; r < g.R; ++r) {
+      int64_t rem = r, off = 0;
+      bool ok = true;
+      for (int q = (int)kept.size() - 1; q >= 0; --q) {
+        const int d = (int)(rem % p.dom[kept[q]]);
+        rem /= p.dom[kept[q]];
+        const int var = var_of(p.root, kept[q]);
+        if (var_digit[var] < 0) {
+          var_digit[var] = d;
+          off += d * vstride[var];
+        } else if (var_digit[var] != d) {
+          ok = false;
+        }
+      }
+      for (int i : kept) var_digit[var_of(p.root, i)] = -1;
+      g.root_map[r] = ok ? off : -1;
+    }
+  }
   Step rc;
   rc.kind = ST_ROOTCOPY;
   if (producer[p.root] >= 0) rc.deps.push_back(producer[p.root]);

@@ -20,7 +20,7 @@ struct Loc {
 };
 
 enum StepKind : int8_t {
-  ST_SELECT, ST_TINY, ST_STREAM, ST_GEMM, ST_GENERIC, ST_ROOTCOPY, ST_ETA, ST_GEMM_REDUCE, ST_CHAIN
+  ST_SELECT, ST_TINY, ST_STREAM, ST_GEMM, ST_GENERIC, ST_ROOTCOPY, ST_ETA, ST_GEMM_REDUCE
 };
 
 struct Step {
@@ -31,8 +31,6 @@ struct Step {
   StreamParams sp{};
   GemmParams gp{};
   GenericParams np{};
-  ChainParams cp{};
-  int64_t chain_off = 0;           // first ChainStep of this chain in Program::chain_steps
   int32_t ns = 0, nf = 0;          // stream template selector
   int32_t bm = 6, bn = 6;          // GEMM tile bits (template selector)
   Loc la{}, lb{}, lc{}, lws{};     // operand/output/workspace locations
@@ -61,17 +59,19 @@ struct Program {
   int32_t tiny_smem_doubles = 0;
   // generic digits
   std::vector<GDigit> gdigits;
-  // fused chains: per-step descriptors (P bound per device from chain_piece)
-  std::vector<ChainStep> chain_steps;
-  std::vector<Loc> chain_piece;
-  int n_chain = 0;
+  // compressed (tied) leaf values, placed after the raw leaf values on device
+  std::vector<double> cvals;
+  // dense result entry -> physical root offset (-1: structural zero); empty = identity
+  std::vector<int64_t> root_map;
+  int n_tied_leaves = 0;
   // arena
   int64_t arena_bytes = 0;
   Loc root_loc{};
   std::vector<Step> steps;
   // stats
   int n_tiny = 0, n_stream = 0, n_gemm = 0, n_generic = 0, n_alias = 0;
-  u128 alg_bytes = 0, alg_flops = 0;
+  u128 alg_bytes = 0, alg_flops = 0;    // dense (reference) per-node work, summed
+  u128 phys_bytes = 0, phys_flops = 0;  // executed work over physical variables
   u128 mem_estimate = 0, peak_observed = 0;
 };
 

@@ -3,7 +3,9 @@
 //   k_select   K5  per-slice leaf selection            (slicing.py:30-41, tensor.py:118-125)
 //   k_tiny     K4  tiny-subtree forest, one CTA per subtree, smem-resident
 //   k_stream   K2  big x <=64-entry operand, HBM streaming, permutation folded in
-//   k_gemm     K3  FP64 DMMA (mma.sync m8n8k4 f64) GEMM, bit-permuted operands
+//                  (batch / diagonal-read variables of tied networks)
+//   k_gemm     K3  FP64 DMMA (mma.sync m8n8k4 f64) GEMM, bit-permuted operands,
+//                  optional batch variables
 //   k_generic      mixed-radix pairwise contraction (domains != 2, odd shapes)
 //   k_rootcopy / k_eta / k_fold   per-slice result slot, slice counter, and the
 //                  lexicographic left fold of the slice sum (slicing.py:139-145)
@@ -38,8 +40,11 @@ __global__ void k_select(const SelectParams p) {
 __global__ void k_rootcopy(const RootCopyParams p) {
   const int64_t slot = p.eta[0] - p.eta[1];
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p.R;
-       r += (int64_t)gridDim.x * blockDim.x)
-    p.results[slot * p.R + r] = p.src[r];
+       r += (int64_t)gridDim.x * blockDim.x) {
+    // tied root indices: dense entries off the diagonal are structural zeros
+    const int64_t m = p.map ? p.map[r] : r;
+    p.results[slot * p.R + r] = m >= 0 ? p.src[m] : 0.0;
+  }
 }
 
 __global__ void k_eta(int64_t* eta) { eta[0] += 1; }
@@ -158,37 +163,62 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
 
 // ---------------------------------------------------------------------------
 // K2: streaming contraction with a <=64-entry operand held in smem.
+// C[x, f] = sum_s A[x, s] P[b(x), s, f]; b(x) are the batch bits of x (tied
+// variables shared by A, P and C), usually none.  A diagonal read adds a
+// second A address bit per x bit (xa2).
 constexpr int kStreamThreads = 256;
 constexpr int kStreamUnroll = 4;
 
 template <int NS, int NF>
 __global__ void __launch_bounds__(kStreamThreads) k_stream(const StreamParams p) {
-  constexpr int SV = 1 << NS, FV = 1 << NF;
-  __shared__ double P[SV * FV];
-  if (threadIdx.x < SV * FV) P[threadIdx.x] = p.P[p.offP[threadIdx.x]];
-  __syncthreads();
+  constexpr int SV = 1 << NS, FV = 1 << NF, SVFV = SV * FV;
+  static_assert((kStreamThreads * kStreamUnroll) == (1 << kStreamChunkBits), "chunk");
+  extern __shared__ double P[];  // (SVFV << nlb) staged entries of the small operand
+  const int nbt = p.nbt, nlb = p.nlb;
+  int64_t staged = -1;
   const int64_t chunk = (int64_t)kStreamThreads * kStreamUnroll;
   for (int64_t base = blockIdx.x * chunk; base < p.nx; base += (int64_t)gridDim.x * chunk) {
+    // P offset of the batch bits fixed in this chunk; restage when it changes
+    int64_t hoff = 0;
+    for (int t = nlb; t < nbt; ++t)
+      if ((base >> p.bt_xbit[t]) & 1) hoff += p.bt_poff[t];
+    if (hoff != staged) {
+      __syncthreads();
+      for (int q = threadIdx.x; q < (SVFV << nlb); q += blockDim.x) {
+        const int lbi = q / SVFV;
+        int64_t off = hoff + p.offP[q % SVFV];
+        for (int t = 0; t < nlb; ++t)
+          if ((lbi >> t) & 1) off += p.bt_poff[t];
+        P[q] = p.P[off];
+      }
+      __syncthreads();
+      staged = hoff;
+    }
     double a[kStreamUnroll][SV];
     int64_t bc[kStreamUnroll];
+    int pb[kStreamUnroll];
     bool ok[kStreamUnroll];
 #pragma unroll
     for (int u = 0; u < kStreamUnroll; ++u) {
       const int64_t x = base + u * kStreamThreads + threadIdx.x;
       ok[u] = x < p.nx;
-      const int64_t ba = ok[u] ? deposit(x, p.xa) : 0;
+      const int64_t ba = ok[u] ? deposit(x, p.xa) + deposit(x, p.xa2) : 0;
       bc[u] = ok[u] ? deposit(x, p.xc) : 0;
+      int lbi = 0;
+      for (int t = 0; t < nlb; ++t) lbi |= (int)((x >> p.bt_xbit[t]) & 1) << t;
+      pb[u] = lbi * SVFV;
 #pragma unroll
       for (int s = 0; s < SV; ++s) a[u][s] = ok[u] ? __ldcs(p.A + ba + p.offA[s]) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < kStreamUnroll; ++u) {
       if (!ok[u]) continue;
+      const double* Pu = P + pb[u];
 #pragma unroll
       for (int f = 0; f < FV; ++f) {
         double acc = 0.0;
 #pragma unroll
-        for (int s = 0; s < SV; ++s) acc = fma(a[u][s], P[s * FV + f], acc);
+        for (int s = 0; s < SV; ++s) acc = fma(a[u][s], Pu[s * FV + f], acc);
         p.C[bc[u] + p.offC[f]] = acc;
       }
     }
@@ -204,139 +234,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-// ---------------------------------------------------------------------------
-// K2c: fused chain.  Per tile: gather (x_lo, inner) from A in A's address
-// order with cp.async (the next tile's gather overlaps this tile's compute),
-// apply the chain's small operands in smem (tables precomputed on the host),
-// scatter (x_lo, inner') to C in C's address order.  Intermediates of the
-// chain never touch HBM.
-constexpr int kChainThreads = 256;
-constexpr int kChainEl = kChainBuf / kChainThreads;  // max tile elements per thread
-
-__device__ __forceinline__ void tile_part(const TileMap& t, int e, int xt, int64_t& off, int& sidx) {
-  // additive decomposition of tile element e: offset + smem index (u << xt | x)
-  off = 0;
-  int x = 0, u = 0;
-  for (int j = 0; j < t.nbits; ++j)
-    if ((e >> j) & 1) {
-      off += (int64_t)1 << t.pos[j];
-      if (t.kind[j]) u |= 1 << t.sub[j];
-      else x |= 1 << t.sub[j];
-    }
-  sidx = (u << xt) | x;
-}
-
-// one chain step with the small operand and the shared-bit offsets in registers
-template <int NS, int NF>
-__device__ __forceinline__ void chain_step(const ChainStep& S, const double* P, const double* cur, double* nxt,
-                                           int n, int xt, int xmask, int tid) {
-  constexpr int SV = 1 << NS, FV = 1 << NF;
-  double pr[SV * FV];
-  int sb[SV];
-#pragma unroll
-  for (int q = 0; q < SV * FV; ++q) pr[q] = P[q];
-#pragma unroll
-  for (int s = 0; s < SV; ++s) sb[s] = S.stab[s];
-  for (int e = tid; e < n; e += kChainThreads) {
-    const int x = e & xmask;
-    const unsigned t = S.utab[e >> xt];
-    const int ub = t & 0xff, f = t >> 8;
-    double acc = 0.0;
-#pragma unroll
-    for (int s = 0; s < SV; ++s) {
-      double pv = pr[s * FV];
-#pragma unroll
-      for (int ff = 1; ff < FV; ++ff)
-        if (f == ff) pv = pr[s * FV + ff];
-      acc = fma(cur[((ub | sb[s]) << xt) | x], pv, acc);
-    }
-    nxt[e] = acc;
-  }
-}
-
-__global__ void __launch_bounds__(kChainThreads) k_chain(const ChainParams p) {
-  extern __shared__ __align__(16) double csm[];
-  double* lbuf[2] = {csm, csm + kChainBuf};
-  double* wbuf = csm + 2 * kChainBuf;
-  double* pcs = csm + 3 * kChainBuf;                    // kChainMax * 64
-  ChainStep* st = (ChainStep*)(pcs + kChainMax * 64);   // nsteps
-  const int tid = threadIdx.x;
-  {
-    const int words = p.nsteps * (int)sizeof(ChainStep) / 4;
-    const int* src = (const int*)p.steps;
-    int* dst = (int*)st;
-    for (int w = tid; w < words; w += blockDim.x) dst[w] = src[w];
-  }
-  // tile element e = tid + i*256 decomposes additively: thread part (bits
-  // 0..7, registers) + block part (bits 8.., a 16-entry smem table)
-  const int na = 1 << p.ta.nbits, nc = 1 << p.tc.nbits;
-  __shared__ int64_t hi_aoff[kChainEl], hi_coff[kChainEl];
-  __shared__ int hi_asx[kChainEl], hi_csx[kChainEl];
-  if (tid < kChainEl) {
-    tile_part(p.ta, tid * kChainThreads, p.xt, hi_aoff[tid], hi_asx[tid]);
-    tile_part(p.tc, tid * kChainThreads, p.xt, hi_coff[tid], hi_csx[tid]);
-  }
-  int64_t aoff_t, coff_t;
-  int asx_t, csx_t;
-  tile_part(p.ta, tid, p.xt, aoff_t, asx_t);
-  tile_part(p.tc, tid, p.xt, coff_t, csx_t);
-  __syncthreads();
-  for (int i = 0; i < p.nsteps; ++i) {
-    const int nv = 1 << (st[i].ns + st[i].nf);
-    for (int q = tid; q < nv; q += blockDim.x) pcs[i * 64 + q] = st[i].P[st[i].offP[q]];
-  }
-  const int xmask = (1 << p.xt) - 1;
-  auto issue = [&](int64_t tile, double* dst) {
-    const double* Ag = p.A + deposit(tile, p.a_hi);
-    for (int i = 0; i < kChainEl; ++i)
-      if (tid + i * kChainThreads < na) cp_async8(dst + asx_t + hi_asx[i], Ag + aoff_t + hi_aoff[i]);
-  };
-  int64_t tile = blockIdx.x;
-  if (tile < p.n_tiles) issue(tile, lbuf[0]);
-  cp_async_commit();
-  for (int it = 0; tile < p.n_tiles; tile += gridDim.x, ++it) {
-    const int64_t next = tile + gridDim.x;
-    if (next < p.n_tiles) issue(next, lbuf[(it + 1) & 1]);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    double* cur = lbuf[it & 1];
-    double* nxt = wbuf;
-    for (int i = 0; i < p.nsteps; ++i) {
-      const ChainStep& S = st[i];
-      const int n = (1 << S.nnew) << p.xt;
-      const int sv = 1 << S.ns, fv = 1 << S.nf;
-      const double* P = pcs + i * 64;
-      const int key = S.ns * 8 + S.nf;
-      if (key == 1 * 8 + 1) chain_step<1, 1>(S, P, cur, nxt, n, p.xt, xmask, tid);
-      else if (key == 2 * 8 + 1) chain_step<2, 1>(S, P, cur, nxt, n, p.xt, xmask, tid);
-      else if (key == 1 * 8 + 2) chain_step<1, 2>(S, P, cur, nxt, n, p.xt, xmask, tid);
-      else if (key == 2 * 8 + 2) chain_step<2, 2>(S, P, cur, nxt, n, p.xt, xmask, tid);
-      else if (key == 1 * 8 + 0) chain_step<1, 0>(S, P, cur, nxt, n, p.xt, xmask, tid);
-      else if (key == 2 * 8 + 0) chain_step<2, 0>(S, P, cur, nxt, n, p.xt, xmask, tid);
-      else {
-        for (int e = tid; e < n; e += kChainThreads) {
-          const int x = e & xmask;
-          const unsigned t = S.utab[e >> p.xt];
-          const int ub = t & 0xff, f = t >> 8;
-          double acc = 0.0;
-          for (int s = 0; s < sv; ++s) acc = fma(cur[((ub | S.stab[s]) << p.xt) | x], P[s * fv + f], acc);
-          nxt[e] = acc;
-        }
-      }
-      __syncthreads();
-      double* tmp = cur;
-      cur = nxt;
-      nxt = tmp;
-    }
-    double* Cg = p.C + deposit(tile, p.c_hi);
-    for (int i = 0; i < kChainEl; ++i)
-      if (tid + i * kChainThreads < nc) Cg[coff_t + hi_coff[i]] = cur[csx_t + hi_csx[i]];
-    __syncthreads();
-  }
-  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------
@@ -396,8 +293,11 @@ __global__ void __launch_bounds__(32 * WGM * WGN, (WGM * WGN >= 8) ? 2 : 4)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / WGN, wn = warp % WGN;
 
-  // tile coordinates with a grouped walk over m for L2 reuse of B
-  const int64_t t = blockIdx.x;
+  // tile coordinates with a grouped walk over m for L2 reuse of B; batch
+  // variables (tied networks) index the grid above the tiles
+  const int tbits = p.m_hi + p.n_hi;
+  const int64_t bt = (int64_t)blockIdx.x >> tbits;
+  const int64_t t = (int64_t)blockIdx.x & (((int64_t)1 << tbits) - 1);
   const int g = p.grid_swizzle_log;
   const int64_t gsz = (int64_t)1 << g;
   const int64_t ntn = (int64_t)1 << p.n_hi;
@@ -442,8 +342,8 @@ __global__ void __launch_bounds__(32 * WGM * WGN, (WGM * WGN >= 8) ? 2 : 4)
   for (int i = 0; i < ELB; ++i)
     if (tid + i * NT < BN * GBK && !(bok_t && hb_ok[i]))
       for (int s = 0; s < Cfg::ST; ++s) Bs[s * GBK * LDB + bsx_t + hb_sx[i]] = 0.0;
-  const double* Ab = p.A + deposit(tm, p.a_m);
-  const double* Bb = p.B + deposit(tn, p.b_n);
+  const double* Ab = p.A + deposit(tm, p.a_m) + deposit(bt, p.a_bt);
+  const double* Bb = p.B + deposit(tn, p.b_n) + deposit(bt, p.b_bt);
 
   auto load_stage = [&](int stage, int64_t kt) {
     const double* Ag = Ab + deposit(kt, p.a_k);
@@ -512,7 +412,7 @@ __global__ void __launch_bounds__(32 * WGM * WGN, (WGM * WGN >= 8) ? 2 : 4)
   __syncthreads();
   if (p.splits > 1) {
     // partial tile, C-tile element order, contiguous per (split, tile)
-    double* W = p.ws + ((int64_t)split * gridDim.x + t) * (BM * BN);
+    double* W = p.ws + ((int64_t)split * gridDim.x + blockIdx.x) * (BM * BN);
     for (int e = tid; e < BM * BN; e += NT) {
       int64_t off;
       int r, k;
@@ -537,7 +437,7 @@ __global__ void __launch_bounds__(32 * WGM * WGN, (WGM * WGN >= 8) ? 2 : 4)
   const bool c_ok_t = tile_elem(p.tc, tid, c_off_t, rt, kt_);
   const int c_sx_t = rt * LDC + kt_;
   __syncthreads();
-  double* Cg = p.C + deposit(tm, p.c_m) + deposit(tn, p.c_n);
+  double* Cg = p.C + deposit(tm, p.c_m) + deposit(tn, p.c_n) + deposit(bt, p.c_bt);
   if (c_ok_t) {
 #pragma unroll 8
     for (int i = 0; i < ELC; ++i)
@@ -550,20 +450,23 @@ __global__ void k_splitk_reduce(const GemmParams p, int64_t tiles, int tile_elem
   const int64_t total = tiles * tile_elems;
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
        id += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = id / tile_elems;
+    const int64_t ta = id / tile_elems;
     const int e = (int)(id % tile_elems);
     int64_t off;
     int r, k;
     if (!tile_elem(p.tc, e, off, r, k)) continue;
-    double acc = p.ws[t * tile_elems + e];
-    for (int s = 1; s < p.splits; ++s) acc = acc + p.ws[((int64_t)s * tiles + t) * tile_elems + e];
+    double acc = p.ws[ta * tile_elems + e];
+    for (int s = 1; s < p.splits; ++s) acc = acc + p.ws[((int64_t)s * tiles + ta) * tile_elems + e];
+    const int tbits = p.m_hi + p.n_hi;
+    const int64_t bt = ta >> tbits;
+    const int64_t t = ta & (((int64_t)1 << tbits) - 1);
     const int g = p.grid_swizzle_log;
     const int64_t gsz = (int64_t)1 << g;
     const int64_t ntn = (int64_t)1 << p.n_hi;
     const int64_t grp = t / (gsz * ntn), in = t % (gsz * ntn);
     const int64_t tm = grp * gsz + (in & (gsz - 1));
     const int64_t tn = in >> g;
-    p.C[deposit(tm, p.c_m) + deposit(tn, p.c_n) + off] = acc;
+    p.C[deposit(tm, p.c_m) + deposit(tn, p.c_n) + deposit(bt, p.c_bt) + off] = acc;
   }
 }
 

@@ -36,15 +36,27 @@ TC_HD int64_t deposit(uint64_t x, const BitRuns& r) {
 // ---- K2: big x small streaming contraction (dim 2) ------------------------
 // C[x, f] = sum_s A[x, s] * P[s, f]; x enumerates the kept indices of the big
 // operand A, s the shared ones (<= 2^4), f the small operand's free ones (<= 2^4).
+// With tied (physical) variables an x bit may also read a second address
+// bit of A (a diagonal read, xa2) and index the small operand (a batch
+// variable: P offset bt_poff[t] when x bit bt_xbit[t] is set).  A CTA
+// iteration covers 2^kStreamChunkBits consecutive x, so batch bits at or
+// above that are fixed per chunk (P's slice for them is staged in smem per
+// chunk) and the nlb lower ones select among the staged copies per element.
+constexpr int kStreamMaxBatch = 24;
+constexpr int kStreamChunkBits = 10;
+constexpr int kStreamSmemMax = 4096;  // doubles of staged P per CTA
 struct StreamParams {
   const double* A;
   const double* P;
   double* C;
   int64_t nx;
-  BitRuns xa, xc;
-  int64_t offA[16];  // s -> offset in A
-  int64_t offC[16];  // f -> offset in C
-  int32_t offP[64];  // s * 2^NF + f -> offset in P
+  BitRuns xa, xa2, xc;
+  int64_t offA[16];   // s -> offset in A
+  int64_t offC[32];   // f -> offset in C
+  int32_t offP[128];  // s * 2^NF + f -> offset in P
+  int32_t nbt, nlb;   // batch bits (ascending x bit), of which nlb below the chunk
+  int32_t bt_xbit[kStreamMaxBatch];
+  int64_t bt_poff[kStreamMaxBatch];
 };
 
 // ---- K3: FP64 DMMA GEMM with bit-permuted operands (dim 2) -----------------
@@ -73,34 +85,10 @@ struct GemmParams {
   int64_t k_per_split;
   int32_t splits;
   BitRuns a_m, a_k, b_n, b_k, c_m, c_n;  // hi-part deposits
+  int32_t bt_bits;                       // batch variables (grid-major above the tiles)
+  BitRuns a_bt, b_bt, c_bt;
   TileMap ta, tb, tc;
   int32_t grid_swizzle_log;  // group of 2^g m-tiles walked together (L2 reuse)
-};
-
-// ---- K2c: fused chain of big x small contractions (dim 2) -----------------
-// A chain v1..vk (v_{i+1}'s big operand is v_i) runs as ONE pass: a CTA loads
-// a tile = (x_lo outer bits) x (all "inner" bits the chain touches) of the
-// input, applies the k small operands in shared memory, stores the tile of
-// v_k.  Intermediates v_1..v_{k-1} never touch HBM.
-constexpr int kChainU = 6;       // max inner bits alive at any step (x_lo >= 6 bits)
-constexpr int kChainMax = 16;    // max steps per fused segment
-constexpr int kChainBuf = 4096;  // doubles per smem tile buffer (x_lo * 2^inner)
-struct ChainStep {
-  const double* P;         // small operand
-  int32_t offP[64];        // s * 2^nf + f -> offset in P
-  uint16_t utab[1 << kChainU];  // new inner u -> (cur inner base | f << 8)
-  uint8_t stab[16];        // s -> cur inner bits of the shared indices
-  int32_t ns, nf, nnew, pad;
-};
-struct ChainParams {
-  const double* A;
-  double* C;
-  const ChainStep* steps;
-  int32_t nsteps;
-  int32_t xt;  // x_lo bits
-  int64_t n_tiles;
-  BitRuns a_hi, c_hi;  // x_hi -> offsets
-  TileMap ta, tc;      // (x_lo kind 0, inner kind 1) in A / C address order
 };
 
 // ---- K4: tiny-subtree forest (any domain) ----------------------------------
@@ -157,6 +145,7 @@ struct SelectParams {
 struct RootCopyParams {
   const double* src;
   double* results;
+  const int64_t* map;  // dense entry -> physical offset or -1 (nullptr: identity)
   int64_t R;
   const int64_t* eta;  // [0] = current slice, [1] = first slice of the run
 };

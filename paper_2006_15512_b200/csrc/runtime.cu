@@ -150,11 +150,11 @@ using StreamFn = void (*)(StreamParams);
 StreamFn stream_fn(int ns, int nf) {
 #define SF(a, b) \
   if (ns == a && nf == b) return k_stream<a, b>;
-  SF(0, 0) SF(0, 1) SF(0, 2) SF(0, 3) SF(0, 4)
-  SF(1, 0) SF(1, 1) SF(1, 2) SF(1, 3) SF(1, 4)
-  SF(2, 0) SF(2, 1) SF(2, 2) SF(2, 3) SF(2, 4)
-  SF(3, 0) SF(3, 1) SF(3, 2) SF(3, 3)
-  SF(4, 0) SF(4, 1) SF(4, 2)
+  SF(0, 0) SF(0, 1) SF(0, 2) SF(0, 3) SF(0, 4) SF(0, 5)
+  SF(1, 0) SF(1, 1) SF(1, 2) SF(1, 3) SF(1, 4) SF(1, 5)
+  SF(2, 0) SF(2, 1) SF(2, 2) SF(2, 3) SF(2, 4) SF(2, 5)
+  SF(3, 0) SF(3, 1) SF(3, 2) SF(3, 3) SF(3, 4)
+  SF(4, 0) SF(4, 1) SF(4, 2) SF(4, 3)
 #undef SF
   throw Error{TC_BAD_ARG, "no stream kernel for this shape"};
 }
@@ -192,10 +192,6 @@ GemmVariant gemm_variant(int bm, int bn) {
     case 3 * 8 + 3: return gv<8, 8, 1, 1>();
   }
   throw Error{TC_BAD_ARG, "no GEMM variant for this tile"};
-}
-
-int chain_smem(int nsteps) {
-  return (3 * kChainBuf + kChainMax * 64) * 8 + nsteps * (int)sizeof(ChainStep);
 }
 
 int sm_count(int dev) {
@@ -254,7 +250,7 @@ struct tc_exec {
   TinyDigit* tdigs = nullptr;
   TinyGroup* tgroups = nullptr;
   GDigit* gdig = nullptr;
-  ChainStep* chains = nullptr;
+  int64_t* rootmap = nullptr;
   SelEntry* sel = nullptr;
   SelTerm* selt = nullptr;
   int64_t* eta = nullptr;
@@ -273,7 +269,7 @@ struct tc_exec {
     if (graph) cudaGraphDestroy(graph);
     if (stream) cudaStreamSynchronize(stream);
     for (void* q : {(void*)arena, (void*)leafbuf, (void*)slicedbuf, (void*)tnodes, (void*)tdigs,
-                    (void*)tgroups, (void*)gdig, (void*)chains, (void*)sel, (void*)selt, (void*)eta, (void*)results,
+                    (void*)tgroups, (void*)gdig, (void*)rootmap, (void*)sel, (void*)selt, (void*)eta, (void*)results,
                     (void*)folded})
       dcache().put(device, q);
     if (stream) cudaStreamDestroy(stream);
@@ -300,8 +296,16 @@ struct tc_exec {
     CU(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     Program& g = prog;
     arena = dalloc<char>((size_t)g.arena_bytes, dev_bytes, device);
-    leafbuf = dalloc<double>(p.lval.size(), dev_bytes, device);
+    // raw leaf values, then the compressed (tied) leaves (compile.cpp)
+    leafbuf = dalloc<double>(p.lval.size() + g.cvals.size(), dev_bytes, device);
     CU(cudaMemcpyAsync(leafbuf, p.lval.data(), p.lval.size() * 8, cudaMemcpyHostToDevice, stream));
+    if (!g.cvals.empty())
+      CU(cudaMemcpyAsync(leafbuf + p.lval.size(), g.cvals.data(), g.cvals.size() * 8, cudaMemcpyHostToDevice,
+                         stream));
+    if (!g.root_map.empty()) {
+      rootmap = dalloc<int64_t>(g.root_map.size(), dev_bytes, device);
+      CU(cudaMemcpyAsync(rootmap, g.root_map.data(), g.root_map.size() * 8, cudaMemcpyHostToDevice, stream));
+    }
     if (g.sliced_doubles) slicedbuf = dalloc<double>((size_t)g.sliced_doubles, dev_bytes, device);
     if (!g.sel_ent.empty()) {
       sel = dalloc<SelEntry>(g.sel_ent.size(), dev_bytes, device);
@@ -327,13 +331,6 @@ struct tc_exec {
                            cudaMemcpyHostToDevice, stream));
       CU(cudaMemcpyAsync(tgroups, g.tiny_groups.data(), g.tiny_groups.size() * sizeof(TinyGroup),
                          cudaMemcpyHostToDevice, stream));
-    }
-    if (!g.chain_steps.empty()) {
-      std::vector<ChainStep> cs = g.chain_steps;
-      for (size_t i = 0; i < cs.size(); ++i) cs[i].P = ptr(g.chain_piece[i]);
-      chains = dalloc<ChainStep>(cs.size(), dev_bytes, device);
-      CU(cudaMemcpyAsync(chains, cs.data(), cs.size() * sizeof(ChainStep), cudaMemcpyHostToDevice, stream));
-      CU(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, chain_smem(kChainMax)));
     }
     if (!g.gdigits.empty()) {
       gdig = dalloc<GDigit>(g.gdigits.size(), dev_bytes, device);
@@ -389,6 +386,7 @@ struct tc_exec {
           sp.C = (double*)ptr(st.lc);
           L.func = (void*)stream_fn(st.ns, st.nf);
           L.block = dim3(kStreamThreads);
+          L.smem = (unsigned)((((1 << st.ns) << st.nf) << sp.nlb) * sizeof(double));
           L.grid = dim3(grid_for(sp.nx, kStreamThreads * kStreamUnroll, device));
           L.arg(sp);
           break;
@@ -405,18 +403,6 @@ struct tc_exec {
           L.grid = dim3((unsigned)st.work, (unsigned)gp.splits);
           L.smem = v.smem;
           L.arg(gp);
-          break;
-        }
-        case ST_CHAIN: {
-          ChainParams cp = st.cp;
-          cp.A = ptr(st.la);
-          cp.C = (double*)ptr(st.lc);
-          cp.steps = chains + st.chain_off;
-          L.func = (void*)k_chain;
-          L.block = dim3(kChainThreads);
-          L.grid = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cp.n_tiles, (int64_t)sm_count(device) * 4)));
-          L.smem = chain_smem(cp.nsteps);
-          L.arg(cp);
           break;
         }
         case ST_GEMM_REDUCE: {
@@ -445,7 +431,7 @@ struct tc_exec {
           break;
         }
         case ST_ROOTCOPY: {
-          RootCopyParams rp{ptr(g.root_loc), nullptr, g.R, eta};
+          RootCopyParams rp{ptr(g.root_loc), nullptr, rootmap, g.R, eta};
           L.func = (void*)k_rootcopy;
           L.grid = dim3(grid_for(g.R, 256, device));
           L.arg(rp);
@@ -739,7 +725,9 @@ int tc_compile_stats(const tc_plan* plan, const int32_t* sliced, int32_t n_slice
     s->alg_bytes = to_abi(g.alg_bytes);
     s->alg_flops = to_abi(g.alg_flops);
     s->n_alias_nodes = g.n_alias;
-    s->n_chain_launches = g.n_chain;
+    s->n_tied_leaves = g.n_tied_leaves;
+    s->phys_bytes = to_abi(g.phys_bytes);
+    s->phys_flops = to_abi(g.phys_flops);
     s->program_ms = ms;
   });
 }
@@ -790,7 +778,9 @@ static void fill_stats(const tc_exec& ex, double ms, tc_stats* s) {
   s->alg_bytes = to_abi(g.alg_bytes);
   s->alg_flops = to_abi(g.alg_flops);
   s->n_alias_nodes = g.n_alias;
-  s->n_chain_launches = g.n_chain;
+  s->n_tied_leaves = g.n_tied_leaves;
+  s->phys_bytes = to_abi(g.phys_bytes);
+  s->phys_flops = to_abi(g.phys_flops);
   s->program_ms = ex.program_ms;
   s->setup_ms = ex.setup_ms;
   s->graph_ms = ex.graph_ms;
