@@ -41,6 +41,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <future>
 #include <map>
 #include <set>
 #include <string>
@@ -226,62 +227,79 @@ struct Comp {
 // Coarsest partition of the kept positions of a dim-2 leaf (<= 4 of them)
 // such that every nonzero entry agrees within each block (restricted growth
 // strings in lexicographic order; first minimum wins).  lab[q] = block.
+// Works on the set of kept-digit patterns of the nonzero entries (a 16-bit
+// mask) against each partition's mask of diagonal patterns.
+struct TiePartitions {
+  // per r: (labels, blocks, allowed-pattern mask) in RGS order
+  std::vector<std::tuple<std::vector<int>, int, uint32_t>> by_r[5];
+  TiePartitions() {
+    for (int r = 2; r <= 4; ++r) {
+      std::vector<int> cur(r, 0);
+      for (;;) {
+        int blocks = 0;
+        for (int x : cur) blocks = std::max(blocks, x + 1);
+        uint32_t allowed = 0;
+        for (int pat = 0; pat < (1 << r); ++pat) {
+          bool ok = true;
+          for (int x = 0; x < r && ok; ++x)
+            for (int y = x + 1; y < r && ok; ++y)
+              if (cur[x] == cur[y] && ((pat >> x) & 1) != ((pat >> y) & 1)) ok = false;
+          if (ok) allowed |= 1u << pat;
+        }
+        by_r[r].emplace_back(cur, blocks, allowed);
+        int q = r - 1;
+        for (; q >= 1; --q) {
+          int m = 0;
+          for (int t = 0; t < q; ++t) m = std::max(m, cur[t]);
+          if (cur[q] <= m) {
+            cur[q]++;
+            for (int t = q + 1; t < r; ++t) cur[t] = 0;
+            break;
+          }
+        }
+        if (q < 1) break;
+      }
+    }
+  }
+};
+
 bool leaf_ties(const Plan& p, int l, const std::vector<char>& drop, std::vector<int>& lab) {
+  static const TiePartitions parts;
   const auto& ro = p.ref_order[l];
-  std::vector<int> kq;
+  int kq[4];
+  int r = 0;
   for (size_t q = 0; q < ro.size(); ++q)
     if (!drop[ro[q]]) {
-      if (p.dom[ro[q]] != 2) return false;
-      kq.push_back((int)q);
+      if (p.dom[ro[q]] != 2 || r == 4) return false;
+      kq[r++] = (int)q;
     }
-  const int r = (int)kq.size();
-  if (r < 2 || r > 4 || p.leaf_size(l) > 4096) return false;
+  if (r < 2 || p.leaf_size(l) > 4096) return false;
   const double* v = p.lval.data() + p.lval_off[l];
   const int64_t n = p.leaf_size(l);
-  std::vector<int64_t> stride(ro.size());
+  int64_t stride[16];
+  if (ro.size() > 16) return false;
   int64_t st = 1;
   for (int q = (int)ro.size() - 1; q >= 0; --q) {
     stride[q] = st;
     st *= p.dom[ro[q]];
   }
-  // kept digits of every nonzero entry
-  std::vector<int> nzd;  // r digits per nonzero entry
+  uint32_t nz = 0;  // kept-digit patterns of the nonzero entries
   for (int64_t e = 0; e < n; ++e) {
     if (v[e] == 0.0) continue;
-    for (int q : kq) nzd.push_back((int)((e / stride[q]) % p.dom[ro[q]]));
+    int pat = 0;
+    for (int x = 0; x < r; ++x) pat |= (int)((e / stride[kq[x]]) & 1) << x;
+    nz |= 1u << pat;
   }
-  std::vector<int> cur(r, 0), best;
-  int best_blocks = r + 1;
-  for (;;) {
-    int blocks = 0;
-    for (int x : cur) blocks = std::max(blocks, x + 1);
-    if (blocks < best_blocks) {
-      bool ok = true;
-      for (size_t base = 0; ok && base < nzd.size(); base += r)
-        for (int x = 0; ok && x < r; ++x)
-          for (int y = x + 1; ok && y < r; ++y)
-            if (cur[x] == cur[y] && nzd[base + x] != nzd[base + y]) ok = false;
-      if (ok) {
-        best = cur;
-        best_blocks = blocks;
-      }
+  const std::vector<int>* best = nullptr;
+  int best_blocks = r;
+  for (const auto& [labs, blocks, allowed] : parts.by_r[r])
+    if (blocks < best_blocks && (nz & ~allowed) == 0) {
+      best = &labs;
+      best_blocks = blocks;
     }
-    // next restricted growth string
-    int q = r - 1;
-    for (; q >= 1; --q) {
-      int m = 0;
-      for (int t = 0; t < q; ++t) m = std::max(m, cur[t]);
-      if (cur[q] <= m) {
-        cur[q]++;
-        for (int t = q + 1; t < r; ++t) cur[t] = 0;
-        break;
-      }
-    }
-    if (q < 1) break;
-  }
-  if (best_blocks >= r) return false;
+  if (!best) return false;
   lab.assign(ro.size(), -1);
-  for (int x = 0; x < r; ++x) lab[kq[x]] = best[x];
+  for (int x = 0; x < r; ++x) lab[kq[x]] = (*best)[x];
   return true;
 }
 
@@ -316,30 +334,33 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     if (__builtin_mul_overflow(g.num_slices, (int64_t)p.dom[i], &g.num_slices))
       fail(TC_OVERFLOW, "number of slices exceeds 2^63");
   }
-  g.mem_estimate = mem_cost(p, drop);
-  g.peak_observed = tracked_peak(p, drop);
-
-  tmark("dense sizes");
-  // ---- dense (reference) sizes: the result size and the dense roofline ------
+  // The reference accounting (mem_cost / tracked peak, slicing.py:52-67,
+  // 91-109) and the dense per-node work only feed the statistics: computed
+  // on a second thread while the program is built.
   std::vector<u128> dsize(S);
-  for (int s = 0; s < S; ++s) dsize[s] = set_bytes(p, p.sets[s], drop) / 8;
-  for (int k = 0; k < p.NN; ++k) {
-    const int v = p.NL + k, a = p.left[k], b = p.right[k];
-    // |A u B| = |A| |B| / |A n B|
-    u128 sh = 1;
-    const auto& Ea = p.sets[a];
-    const auto& Eb = p.sets[b];
-    for (size_t x = 0, y = 0; x < Ea.size() && y < Eb.size();) {
-      if (Ea[x] < Eb[y]) ++x;
-      else if (Eb[y] < Ea[x]) ++y;
-      else {
-        if (!drop[Ea[x]]) sh *= (u128)p.dom[Ea[x]];
-        ++x, ++y;
+  u128 dense_bytes = 0, dense_flops = 0, mem_est = 0, peak_obs = 0;
+  auto accounting = std::async(std::launch::async, [&] {
+    mem_est = mem_cost(p, drop);
+    peak_obs = tracked_peak(p, drop);
+    for (int s = 0; s < S; ++s) dsize[s] = set_bytes(p, p.sets[s], drop) / 8;
+    for (int k = 0; k < p.NN; ++k) {
+      const int v = p.NL + k, a = p.left[k], b = p.right[k];
+      // |A u B| = |A| |B| / |A n B|
+      u128 sh = 1;
+      const auto& Ea = p.sets[a];
+      const auto& Eb = p.sets[b];
+      for (size_t x = 0, y = 0; x < Ea.size() && y < Eb.size();) {
+        if (Ea[x] < Eb[y]) ++x;
+        else if (Eb[y] < Ea[x]) ++y;
+        else {
+          if (!drop[Ea[x]]) sh *= (u128)p.dom[Ea[x]];
+          ++x, ++y;
+        }
       }
+      dense_flops += 2 * (dsize[a] / sh) * dsize[b];
+      dense_bytes += (u128)8 * (dsize[a] + dsize[b] + dsize[v]);
     }
-    g.alg_flops += 2 * (dsize[a] / sh) * dsize[b];
-    g.alg_bytes += (u128)8 * (dsize[a] + dsize[b] + dsize[v]);
-  }
+  });
 
   tmark("physical variables");
   // ---- physical variables: tie blocks of leaves, union-find at nodes --------
@@ -374,13 +395,13 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     return f != m.end() && f->first == l;
   };
   int pushdown_rounds = 0;
-  for (int attempt = 0;; ++attempt) {
-    bool overflow = false;
-    cpool.clear();
+  auto build_leaves = [&]() {
     for (int l = 0; l < p.NL; ++l) {
       const auto& ro = p.ref_order[l];
       auto& m = mem[l];
       m.clear();
+      m.reserve(ro.size());
+      vars[l].reserve(ro.size());
       leaf_tied[l] = ties && leaf_ties(p, l, drop, lab);
       if (leaf_tied[l]) {
         int bmin[8];
@@ -400,10 +421,57 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       std::sort(vv.begin(), vv.end());
       vv.erase(std::unique(vv.begin(), vv.end()), vv.end());
     }
+  };
+  build_leaves();
+  // Requests known before the pass: a tied leaf piece whose block holds two
+  // indices of its sibling subtree (the common copy-tensor case) is pushed
+  // down symbolically; the rounds below catch ties that arise deeper.
+  auto push_down = [&](int u, int l1, int l2) {
+    auto in_set = [&](int sl, int l) { return std::binary_search(p.sets[sl].begin(), p.sets[sl].end(), l); };
+    for (;;) {
+      const int ku = u - p.NL, ca = p.left[ku], cb = p.right[ku];
+      const int c1 = in_set(ca, l1) ? ca : cb, c2 = in_set(ca, l2) ? ca : cb;
+      if (c1 == c2 && !p.is_leaf(c1)) {
+        u = c1;
+        continue;
+      }
+      req[ku].push_back({l1, l2});
+      return;
+    }
+  };
+  if (ties) {
+    for (int l = 0; l < p.NL; ++l) {
+      if (!leaf_tied[l] || p.parent[l] < 0) continue;
+      const int v = p.parent[l], k = v - p.NL;
+      const int x = p.left[k] == l ? p.right[k] : p.left[k];
+      if (p.is_leaf(x)) continue;
+      const auto& m = mem[l];
+      for (size_t i = 0; i < m.size(); ++i)
+        for (size_t j = i + 1; j < m.size(); ++j)
+          if (m[i].second == m[j].second && std::binary_search(p.sets[x].begin(), p.sets[x].end(), m[i].first) &&
+              std::binary_search(p.sets[x].begin(), p.sets[x].end(), m[j].first))
+            push_down(x, m[i].first, m[j].first);
+    }
+  }
+  tmark("phys: node passes");
+  // push-down rounds recompute only the nodes on paths from new requests up
+  std::vector<char> dirty(S, 1);
+  std::vector<Comp> cpool_prev;
+  std::vector<int32_t> coff_prev;
+  for (int attempt = 0;; ++attempt) {
+    bool overflow = false;
+    cpool_prev.swap(cpool);
+    coff_prev = coff;
+    cpool.clear();
     std::vector<Comp> cs;
     for (int k = 0; k < p.NN && !overflow; ++k) {
       const int v = p.NL + k, a = p.left[k], b = p.right[k];
       coff[k] = (int32_t)cpool.size();
+      dirty[v] = dirty[v] || dirty[a] || dirty[b];
+      if (!dirty[v]) {  // unchanged since the last round
+        cpool.insert(cpool.end(), cpool_prev.begin() + coff_prev[k], cpool_prev.begin() + coff_prev[k + 1]);
+        continue;
+      }
       for (auto& e : mem[a]) own_a[e.first] = e.second;
       for (auto& e : mem[b]) own_b[e.first] = e.second;
       for (int x : vars[a]) uf[x] = x;
@@ -444,11 +512,19 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       // kept logical indices -> component's C variable (smallest kept index)
       auto& mv = mem[v];
       mv.clear();
-      for (auto& e : mem[a])
-        if (own_b[e.first] < 0) mv.push_back({e.first, e.second});
-      for (auto& e : mem[b])
-        if (own_a[e.first] < 0) mv.push_back({e.first, e.second});
-      std::sort(mv.begin(), mv.end());
+      mv.reserve(mem[a].size() + mem[b].size());
+      {
+        const auto& Ma = mem[a];
+        const auto& Mb = mem[b];
+        size_t x = 0, y = 0;
+        for (;;) {  // merge the kept entries of both (each sorted by logical index)
+          while (x < Ma.size() && own_b[Ma[x].first] >= 0) ++x;
+          while (y < Mb.size() && own_a[Mb[y].first] >= 0) ++y;
+          if (x == Ma.size() && y == Mb.size()) break;
+          if (y == Mb.size() || (x < Ma.size() && Ma[x].first < Mb[y].first)) mv.push_back(Ma[x++]);
+          else mv.push_back(Mb[y++]);
+        }
+      }
       for (auto& e : mv) {
         Comp& c = comp_of(e.second);
         if (c.c < 0) c.c = e.first;  // mv is sorted: first kept = smallest
@@ -456,9 +532,10 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       for (auto& e : mv) e.second = comp_of(e.second).c;
       auto& vv = vars[v];
       vv.clear();
-      for (auto& e : mv) vv.push_back(e.second);
+      vv.reserve(cs.size());
+      for (const Comp& c : cs)
+        if (c.c >= 0) vv.push_back(c.c);
       std::sort(vv.begin(), vv.end());
-      vv.erase(std::unique(vv.begin(), vv.end()), vv.end());
       // reset scratch (before reordering cs: cidx indexes into it)
       for (int x : vars[a]) cidx[find(x)] = -1;
       for (int x : vars[b]) cidx[find(x)] = -1;
@@ -470,8 +547,10 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       cpool.insert(cpool.end(), cs.begin(), cs.end());
     }
     coff[p.NN] = (int32_t)cpool.size();
+    tmark("phys: requests");
     if (!overflow) {
       bool pushed = false;
+      std::fill(dirty.begin(), dirty.end(), 0);
       if (ties && pushdown_rounds < 8) {
         for (int k = 0; k < p.NN; ++k) {
           const int ch[2] = {p.left[k], p.right[k]};
@@ -492,6 +571,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
                     continue;
                   }
                   req[ku].push_back({l1, l2});
+                  dirty[u] = 1;
                   pushed = true;
                   break;
                 }
@@ -500,7 +580,9 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
           }
         }
       }
+      tmark("phys: node passes");
       if (pushed) {
+        if (timing) std::fprintf(stderr, "[compile] tie push-down round %d\n", pushdown_rounds);
         ++pushdown_rounds;
         continue;
       }
@@ -510,6 +592,8 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     if (!ties || attempt > 8) fail(TC_BAD_ARG, "tie component too large");
     ties = false;  // pathological tie structure: fall back to dense variables
     for (auto& r : req) r.clear();
+    build_leaves();
+    std::fill(dirty.begin(), dirty.end(), 1);
   }
   struct EffView {
     const std::vector<std::vector<int>>* v;
@@ -1376,6 +1460,11 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   }
 
   tmark("root copy");
+  accounting.get();  // rethrows TC_OVERFLOW from the accounting thread
+  g.mem_estimate = mem_est;
+  g.peak_observed = peak_obs;
+  g.alg_bytes = dense_bytes;
+  g.alg_flops = dense_flops;
   // root copy into the per-slice result slot, then advance the slice counter.
   // The result is dense over the root's kept indices in the reference's
   // row-major order; a root with tied indices is expanded through root_map.
