@@ -162,6 +162,12 @@ int tc_exec_run(tc_exec* ex, int64_t slice_begin, int64_t slice_end, tc_stats* s
 int tc_exec_run_repeat(tc_exec* ex, int64_t slice_begin, int64_t slice_end, int64_t repeats,
                        tc_stats* stats);
 
+/* Benchmark form: `repeats` passes, each preceded by an untimed write of
+ * flush_bytes to a scratch buffer (evicts the 126 MB L2) and timed on its own
+ * CUDA-event pair; stats->device_ms = sum of the per-pass times. */
+int tc_exec_run_flushed(tc_exec* ex, int64_t slice_begin, int64_t slice_end, int64_t repeats,
+                        int64_t flush_bytes, tc_stats* stats);
+
 /* Copy the last run's per-slice results ([n][R] FP64) into a caller-owned
  * DEVICE buffer on the exec's device (e.g. a torch tensor's data_ptr()). */
 int tc_exec_copy_results(tc_exec* ex, double* dst_device);

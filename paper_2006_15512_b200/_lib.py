@@ -124,6 +124,7 @@ SIGNATURES = {
     "tc_exec_free": (None, [C.c_void_p]),
     "tc_exec_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(Stats)]),
     "tc_exec_run_repeat": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.POINTER(Stats)]),
+    "tc_exec_run_flushed": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.POINTER(Stats)]),
     "tc_exec_copy_results": (C.c_int, [C.c_void_p, C.c_void_p]),
     "tc_fold_device": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32]),
     "tc_exec_fetch": (C.c_int, [C.c_void_p, F64P, F64P]),
@@ -321,9 +322,15 @@ class Exec:
             _lib.tc_exec_free(self.h)
             self.h = None
 
-    def run(self, begin: int, end: int, repeats: int = 1) -> dict:
+    def run(self, begin: int, end: int, repeats: int = 1, flush_bytes: int = 0) -> dict:
+        """repeats passes over slices [begin, end); with flush_bytes > 0 each
+        pass is timed alone after an untimed L2-evicting write (benchmark)."""
         st = Stats()
-        check(lib().tc_exec_run_repeat(self.h, int(begin), int(end), int(repeats), C.byref(st)))
+        if flush_bytes > 0:
+            check(lib().tc_exec_run_flushed(self.h, int(begin), int(end), int(repeats), int(flush_bytes),
+                                            C.byref(st)))
+        else:
+            check(lib().tc_exec_run_repeat(self.h, int(begin), int(end), int(repeats), C.byref(st)))
         return st.as_dict()
 
     def copy_results(self, dst_device_ptr: int):

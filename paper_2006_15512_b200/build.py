@@ -52,8 +52,10 @@ def build_flat_ext(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale(out, [FLAT_SRC, os.path.abspath(__file__)]):
         return out
     os.makedirs(os.path.dirname(out), exist_ok=True)
+    import numpy
+
     cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC", "-std=c11", "-Wall",
-           "-I", sysconfig.get_paths()["include"], FLAT_SRC, "-o", out + ".tmp"]
+           "-I", sysconfig.get_paths()["include"], "-I", numpy.get_include(), FLAT_SRC, "-o", out + ".tmp"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

@@ -52,7 +52,8 @@ namespace tc {
 namespace {
 
 constexpr int64_t kTinyMax = 4096;           // entries per tiny tensor
-constexpr int32_t kTinySmemCap = 20 * 1024;  // doubles of smem per tiny CTA (160 KB)
+constexpr int32_t kTinySmemCap = 16 * 1024;  // doubles of intermediates per tiny CTA (128 KB; the
+                                             // rest of the 227 KB holds the staged batch)
 constexpr int64_t kAlign = 256;
 constexpr int64_t kSMs = 148;                // B200 SM count (split-K sizing)
 constexpr int kMaxTie = 4;                   // physical variables of one operand in one component
@@ -1053,6 +1054,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     }
   };
   std::vector<std::vector<int>> level_groups(nlevels);
+  std::vector<int> tiny_slot;  // slot of each tiny descriptor
   for (size_t gi = 0; gi < groups.size(); ++gi) level_groups[glevel[gi]].push_back((int)gi);
   std::vector<std::pair<int32_t, int32_t>> level_range(nlevels);
   for (int lv = 0; lv < nlevels; ++lv) {
@@ -1117,12 +1119,38 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         tn.s_size = (int32_t)ssz;
         tn.pow2 = p2 ? 1 : 0;
         g.tiny_nodes.push_back(tn);
+        tiny_slot.push_back(v);
         g.tiny_ga.push_back(la);
         g.tiny_gb.push_back(lb);
         g.tiny_gout.push_back(lo);
         g.n_tiny++;
       }
       tg.end = (int32_t)g.tiny_nodes.size();
+      // batches of kTinyBatch nodes: staging offsets of small global operands
+      // (leaves, sliced leaves, small forced roots) and the digit block size
+      for (int b0 = tg.beg; b0 < tg.end; b0 += kTinyBatch) {
+        const int b1 = std::min(tg.end, b0 + kTinyBatch);
+        int32_t cur = 0;
+        for (int q = b0; q < b1; ++q) {
+          TinyNode& t = g.tiny_nodes[q];
+          const int k2 = (int)(q - tg.beg);
+          (void)k2;
+          auto stage = [&](const Loc& l, int64_t n, int32_t& st, int32_t& cnt) {
+            st = -1;
+            cnt = 0;
+            if (l.kind == LOC_SMEM || n > kTinyStageMax) return;
+            st = cur;
+            cnt = (int32_t)n;
+            cur += (int32_t)((n + 1) & ~1);
+          };
+          const int v = tiny_slot[q];
+          stage(g.tiny_ga[q], size[p.kid_l(v)], t.sta, t.na);
+          stage(g.tiny_gb[q], size[p.kid_r(v)], t.stb, t.nb);
+        }
+        g.tiny_stage_doubles = std::max(g.tiny_stage_doubles, cur);
+        const TinyNode& l = g.tiny_nodes[b1 - 1];
+        g.tiny_dig_max = std::max(g.tiny_dig_max, l.dig + l.nc + l.ns - g.tiny_nodes[b0].dig);
+      }
       g.tiny_groups.push_back(tg);
       g.tiny_smem_doubles = std::max(g.tiny_smem_doubles, group_smem[gi]);
       for (int v : nodes)
@@ -1257,7 +1285,19 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
             if (f >> t & 1) o += (int64_t)1 << pc[N[t]->c];
           sp.offC[f] = o;
         }
-        if (((1 << sp.nlb) << (ns + nf)) > kStreamSmemMax) throw Error{-1, "small operand"};
+        sp.stage_all = ((1 << sp.nbt) << (ns + nf)) <= kStreamStageMax;
+        if (j > kStreamXBits) throw Error{-1, "x bits"};
+        for (int jb = 0; jb < kStreamXBits; ++jb) {
+          sp.bitA[jb] = deposit((uint64_t)1 << jb, sp.xa) + deposit((uint64_t)1 << jb, sp.xa2);
+          sp.bitC[jb] = deposit((uint64_t)1 << jb, sp.xc);
+          sp.bitP[jb] = 0;
+          sp.bitPo[jb] = 0;
+          for (int t = 0; t < sp.nbt; ++t)
+            if (sp.bt_xbit[t] == jb) {
+              sp.bitP[jb] = 1 << t;
+              sp.bitPo[jb] = sp.bt_poff[t];
+            }
+        }
         st.kind = ST_STREAM;
         st.sp = sp;
         st.ns = ns;

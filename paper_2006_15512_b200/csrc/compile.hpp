@@ -57,6 +57,8 @@ struct Program {
   std::vector<TinyDigit> tiny_digits;
   std::vector<TinyGroup> tiny_groups;
   int32_t tiny_smem_doubles = 0;
+  int32_t tiny_stage_doubles = 0;  // per-batch staged global operands (max over batches)
+  int32_t tiny_dig_max = 0;        // per-batch digit block (max over batches)
   // generic digits
   std::vector<GDigit> gdigits;
   // compressed (tied) leaf values, placed after the raw leaf values on device

@@ -16,6 +16,8 @@
 // leaves in network order, then internal nodes in left-first postorder.
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
+#define NPY_NO_DEPRECATED_API NPY_1_7_API_VERSION
+#include <numpy/arrayobject.h>
 #include <stdint.h>
 #include <string.h>
 
@@ -86,6 +88,14 @@ static PyObject *s_indices, *s_values, *s_id, *s_domain_size, *s_tensor, *s_left
 
 // append the row-major float64 contents of `values` to vals; returns entries or -1
 static Py_ssize_t put_values(Buf* vals, PyObject* values) {
+  // fast path: an aligned, C-contiguous float64 ndarray (what Tensor holds)
+  if (PyArray_Check(values)) {
+    PyArrayObject* arr = (PyArrayObject*)values;
+    if (PyArray_TYPE(arr) == NPY_DOUBLE && PyArray_IS_C_CONTIGUOUS(arr) && PyArray_ISNOTSWAPPED(arr)) {
+      const Py_ssize_t n = PyArray_SIZE(arr);
+      return buf_put(vals, PyArray_DATA(arr), (size_t)n * 8) == 0 ? n : -1;
+    }
+  }
   Py_buffer v;
   if (PyObject_GetBuffer(values, &v, PyBUF_STRIDES | PyBUF_FORMAT) == 0) {
     const char* f = v.format ? v.format : "B";
@@ -346,6 +356,7 @@ static PyMethodDef methods[] = {
 static struct PyModuleDef mod = {PyModuleDef_HEAD_INIT, "_tcflat", NULL, -1, methods};
 
 PyMODINIT_FUNC PyInit__tcflat(void) {
+  import_array();
   s_indices = PyUnicode_InternFromString("indices");
   s_values = PyUnicode_InternFromString("values");
   s_id = PyUnicode_InternFromString("id");

@@ -50,6 +50,12 @@ __global__ void k_rootcopy(const RootCopyParams p) {
 __global__ void k_eta(int64_t* eta) { eta[0] += 1; }
 __global__ void k_eta_reset(int64_t* eta) { eta[0] = eta[1]; }
 
+// L2 eviction between timed passes (benchmark only): stream a scratch buffer
+__global__ void k_flush(double4* buf, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    buf[i] = make_double4(v, v, v, v);
+}
+
 // left fold in lexicographic slice order: ((p0 + p1) + p2) + ...  (tensor.py:111-115)
 __global__ void k_fold(const double* results, int64_t R, int64_t n, double* out) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
@@ -63,101 +69,123 @@ __global__ void k_fold(const double* results, int64_t R, int64_t n, double* out)
 // ---------------------------------------------------------------------------
 // K4: one CTA walks one tiny subtree in postorder; intermediates live in smem.
 constexpr int kTinyThreads = 256;
-constexpr int kTinyMaxDigits = 64;
 
+// smem: [intermediates: smem_doubles][reduce: kTinyThreads][staged operands:
+// stage_doubles][kTinyBatch TinyNode][dig_max TinyDigit]
 __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restrict__ nodes,
                                                        const TinyDigit* __restrict__ digs,
                                                        const TinyGroup* __restrict__ groups,
-                                                       int32_t smem_doubles) {
+                                                       int32_t smem_doubles, int32_t stage_doubles) {
   extern __shared__ double sm[];
   double* red = sm + smem_doubles;  // kTinyThreads scratch for cooperative sums
-  __shared__ TinyDigit sd[kTinyMaxDigits];
-  __shared__ TinyNode tn;
+  double* stg = red + kTinyThreads;
+  TinyNode* bn = (TinyNode*)(stg + stage_doubles);
+  TinyDigit* bd = (TinyDigit*)(bn + kTinyBatch);
   const TinyGroup G = groups[blockIdx.x];
-  const int tid = threadIdx.x;
-  for (int n = G.beg; n < G.end; ++n) {
-    if (tid == 0) tn = nodes[n];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int b0 = G.beg; b0 < G.end; b0 += kTinyBatch) {
+    const int cnt = min(kTinyBatch, G.end - b0);
+    __syncthreads();  // the previous batch is done with the staging buffers
+    {
+      const int words = cnt * (int)(sizeof(TinyNode) / 4);
+      const int* src = (const int*)(nodes + b0);
+      for (int w = tid; w < words; w += blockDim.x) ((int*)bn)[w] = src[w];
+    }
+    const int dig0 = nodes[b0].dig;
+    const int dig1 = nodes[b0 + cnt - 1].dig + nodes[b0 + cnt - 1].nc + nodes[b0 + cnt - 1].ns;
+    for (int j = tid; j < dig1 - dig0; j += blockDim.x) bd[j] = digs[dig0 + j];
     __syncthreads();
-    const int nd = tn.nc + tn.ns;
-    for (int j = tid; j < nd; j += blockDim.x) sd[j] = digs[tn.dig + j];
+    // small global operands: one warp per operand, lanes over entries
+    for (int o = warp; o < 2 * cnt; o += kTinyThreads / 32) {
+      const TinyNode& t = bn[o >> 1];
+      const int st = (o & 1) ? t.stb : t.sta;
+      if (st < 0) continue;
+      const double* g = (o & 1) ? t.gb : t.ga;
+      const int n = (o & 1) ? t.nb : t.na;
+      for (int e = lane; e < n; e += 32) stg[st + e] = g[e];
+    }
     __syncthreads();
-    const double* A = tn.ga ? tn.ga : sm + tn.sa;
-    const double* B = tn.gb ? tn.gb : sm + tn.sb;
-    double* C = tn.gout ? tn.gout : sm + tn.sout;
-    const int nc = tn.nc, ns = tn.ns;
-    const TinyDigit* sdS = sd + nc;
-    if (tn.c_size * 4 >= (int)blockDim.x || tn.s_size < 64) {
-      for (int c = tid; c < tn.c_size; c += blockDim.x) {
-        int oa = 0, ob = 0;
-        if (tn.pow2) {
-          for (int j = 0; j < nc; ++j) {
-            int bit = (c >> j) & 1;
-            oa += bit * sd[j].sa;
-            ob += bit * sd[j].sb;
+    for (int i = 0; i < cnt; ++i) {
+      const TinyNode& tn = bn[i];
+      const TinyDigit* sd = bd + (tn.dig - dig0);
+      const double* A = tn.sta >= 0 ? stg + tn.sta : (tn.ga ? tn.ga : sm + tn.sa);
+      const double* B = tn.stb >= 0 ? stg + tn.stb : (tn.gb ? tn.gb : sm + tn.sb);
+      double* C = tn.gout ? tn.gout : sm + tn.sout;
+      const int nc = tn.nc, ns = tn.ns;
+      const TinyDigit* sdS = sd + nc;
+      if (tn.c_size * 4 >= (int)blockDim.x || tn.s_size < 64) {
+        for (int c = tid; c < tn.c_size; c += blockDim.x) {
+          int oa = 0, ob = 0;
+          if (tn.pow2) {
+            for (int j = 0; j < nc; ++j) {
+              int bit = (c >> j) & 1;
+              oa += bit * sd[j].sa;
+              ob += bit * sd[j].sb;
+            }
+          } else {
+            int r = c;
+            for (int j = 0; j < nc; ++j) {
+              int q = r % sd[j].dim;
+              r /= sd[j].dim;
+              oa += q * sd[j].sa;
+              ob += q * sd[j].sb;
+            }
           }
-        } else {
-          int r = c;
+          double acc = 0.0;
+          for (int s = 0; s < tn.s_size; ++s) {
+            int xa = oa, xb = ob;
+            if (tn.pow2) {
+              for (int j = 0; j < ns; ++j) {
+                int bit = (s >> j) & 1;
+                xa += bit * sdS[j].sa;
+                xb += bit * sdS[j].sb;
+              }
+            } else {
+              int r = s;
+              for (int j = 0; j < ns; ++j) {
+                int q = r % sdS[j].dim;
+                r /= sdS[j].dim;
+                xa += q * sdS[j].sa;
+                xb += q * sdS[j].sb;
+              }
+            }
+            acc = fma(A[xa], B[xb], acc);
+          }
+          C[c] = acc;
+        }
+      } else {
+        // few outputs, long sums: the CTA splits each sum, fixed-shape tree reduce
+        for (int c = 0; c < tn.c_size; ++c) {
+          int oa = 0, ob = 0, r = c;
           for (int j = 0; j < nc; ++j) {
             int q = r % sd[j].dim;
             r /= sd[j].dim;
             oa += q * sd[j].sa;
             ob += q * sd[j].sb;
           }
-        }
-        double acc = 0.0;
-        for (int s = 0; s < tn.s_size; ++s) {
-          int xa = oa, xb = ob;
-          if (tn.pow2) {
+          double acc = 0.0;
+          for (int s = tid; s < tn.s_size; s += blockDim.x) {
+            int xa = oa, xb = ob, r2 = s;
             for (int j = 0; j < ns; ++j) {
-              int bit = (s >> j) & 1;
-              xa += bit * sdS[j].sa;
-              xb += bit * sdS[j].sb;
-            }
-          } else {
-            int r = s;
-            for (int j = 0; j < ns; ++j) {
-              int q = r % sdS[j].dim;
-              r /= sdS[j].dim;
+              int q = r2 % sdS[j].dim;
+              r2 /= sdS[j].dim;
               xa += q * sdS[j].sa;
               xb += q * sdS[j].sb;
             }
+            acc = fma(A[xa], B[xb], acc);
           }
-          acc = fma(A[xa], B[xb], acc);
-        }
-        C[c] = acc;
-      }
-    } else {
-      // few outputs, long sums: the CTA splits each sum, fixed-shape tree reduce
-      for (int c = 0; c < tn.c_size; ++c) {
-        int oa = 0, ob = 0, r = c;
-        for (int j = 0; j < nc; ++j) {
-          int q = r % sd[j].dim;
-          r /= sd[j].dim;
-          oa += q * sd[j].sa;
-          ob += q * sd[j].sb;
-        }
-        double acc = 0.0;
-        for (int s = tid; s < tn.s_size; s += blockDim.x) {
-          int xa = oa, xb = ob, r2 = s;
-          for (int j = 0; j < ns; ++j) {
-            int q = r2 % sdS[j].dim;
-            r2 /= sdS[j].dim;
-            xa += q * sdS[j].sa;
-            xb += q * sdS[j].sb;
+          red[tid] = acc;
+          __syncthreads();
+          for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+            if (tid < w) red[tid] = red[tid] + red[tid + w];
+            __syncthreads();
           }
-          acc = fma(A[xa], B[xb], acc);
-        }
-        red[tid] = acc;
-        __syncthreads();
-        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-          if (tid < w) red[tid] = red[tid] + red[tid + w];
+          if (tid == 0) C[c] = red[0];
           __syncthreads();
         }
-        if (tid == 0) C[c] = red[0];
-        __syncthreads();
       }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
@@ -172,54 +200,96 @@ constexpr int kStreamUnroll = 4;
 template <int NS, int NF>
 __global__ void __launch_bounds__(kStreamThreads) k_stream(const StreamParams p) {
   constexpr int SV = 1 << NS, FV = 1 << NF, SVFV = SV * FV;
-  static_assert((kStreamThreads * kStreamUnroll) == (1 << kStreamChunkBits), "chunk");
-  extern __shared__ double P[];  // (SVFV << nlb) staged entries of the small operand
-  const int nbt = p.nbt, nlb = p.nlb;
-  int64_t staged = -1;
-  const int64_t chunk = (int64_t)kStreamThreads * kStreamUnroll;
-  for (int64_t base = blockIdx.x * chunk; base < p.nx; base += (int64_t)gridDim.x * chunk) {
-    // P offset of the batch bits fixed in this chunk; restage when it changes
-    int64_t hoff = 0;
-    for (int t = nlb; t < nbt; ++t)
-      if ((base >> p.bt_xbit[t]) & 1) hoff += p.bt_poff[t];
-    if (hoff != staged) {
-      __syncthreads();
-      for (int q = threadIdx.x; q < (SVFV << nlb); q += blockDim.x) {
-        const int lbi = q / SVFV;
-        int64_t off = hoff + p.offP[q % SVFV];
-        for (int t = 0; t < nlb; ++t)
-          if ((lbi >> t) & 1) off += p.bt_poff[t];
-        P[q] = p.P[off];
+  constexpr int CB = kStreamChunkBits;
+  static_assert((kStreamThreads * kStreamUnroll) == (1 << CB), "chunk");
+  static_assert(kStreamThreads == 256 && kStreamUnroll == 4, "x = base + u*256 + tid");
+  __shared__ double Ps[kStreamStageMax];  // staged small operand (stage_all)
+  const int tid = threadIdx.x;
+  const bool staged = p.stage_all;
+  // x = chunk * 2^CB + u * 256 + tid.  Every address is a sum of per-bit
+  // table entries: the thread's low parts once, the CTA's chunk bits once,
+  // then each step of the Gray-code chunk walk flips one bit (one add).
+  int64_t ta = 0, tcc = 0, tpo = 0;
+  int tp = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if ((tid >> j) & 1) {
+      ta += p.bitA[j];
+      tcc += p.bitC[j];
+      tp += p.bitP[j];
+      tpo += p.bitPo[j];
+    }
+  int64_t lo_a[kStreamUnroll], lo_c[kStreamUnroll], lo_p[kStreamUnroll];
+#pragma unroll
+  for (int u = 0; u < kStreamUnroll; ++u) {
+    lo_a[u] = ta + ((u & 1) ? p.bitA[8] : 0) + ((u & 2) ? p.bitA[9] : 0);
+    lo_c[u] = tcc + ((u & 1) ? p.bitC[8] : 0) + ((u & 2) ? p.bitC[9] : 0);
+    lo_p[u] = staged ? (int64_t)(tp + ((u & 1) ? p.bitP[8] : 0) + ((u & 2) ? p.bitP[9] : 0)) * SVFV
+                     : tpo + ((u & 1) ? p.bitPo[8] : 0) + ((u & 2) ? p.bitPo[9] : 0);
+  }
+  if (staged) {
+    for (int q = tid; q < (SVFV << p.nbt); q += blockDim.x) {
+      const int bi = q / SVFV;
+      int64_t off = p.offP[q % SVFV];
+      for (int t = 0; t < p.nbt; ++t)
+        if ((bi >> t) & 1) off += p.bt_poff[t];
+      Ps[q] = p.P[off];
+    }
+    __syncthreads();
+  }
+  // this CTA's fixed chunk bits
+  int64_t ha = 0, hc = 0, hp = 0;
+  {
+    uint64_t m = (uint64_t)blockIdx.x << (p.kchunk + CB);
+    while (m) {
+      const int j = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      ha += p.bitA[j];
+      hc += p.bitC[j];
+      hp += staged ? (int64_t)p.bitP[j] * SVFV : p.bitPo[j];
+    }
+  }
+  const double* Pbase = staged ? Ps : p.P;
+  auto pv = [&](const double* Pu, int q) { return staged ? Pu[q] : __ldg(Pu + p.offP[q]); };
+  const int64_t nsteps = (int64_t)1 << p.kchunk;
+  for (int64_t i = 0; i < nsteps; ++i) {
+    if (i > 0) {  // Gray code: chunk bit ctz(i) flips
+      const int j = __ffsll((long long)i) - 1 + CB;
+      const int64_t sg = (((i ^ (i >> 1)) >> (j - CB)) & 1) ? 1 : -1;
+      ha += sg * p.bitA[j];
+      hc += sg * p.bitC[j];
+      hp += sg * (staged ? (int64_t)p.bitP[j] * SVFV : p.bitPo[j]);
+    }
+    const double* Ab = p.A + ha;
+    double* Cb = p.C + hc;
+    const double* Pc = Pbase + hp;
+    if (p.nx >= (1 << CB)) {
+      double a[kStreamUnroll][SV];
+#pragma unroll
+      for (int u = 0; u < kStreamUnroll; ++u)
+#pragma unroll
+        for (int s = 0; s < SV; ++s) a[u][s] = __ldcs(Ab + lo_a[u] + p.offA[s]);
+#pragma unroll
+      for (int u = 0; u < kStreamUnroll; ++u) {
+        const double* Pu = Pc + lo_p[u];
+        double* Cu = Cb + lo_c[u];
+#pragma unroll
+        for (int f = 0; f < FV; ++f) {
+          double acc = 0.0;
+#pragma unroll
+          for (int s = 0; s < SV; ++s) acc = fma(a[u][s], pv(Pu, s * FV + f), acc);
+          Cu[p.offC[f]] = acc;
+        }
       }
-      __syncthreads();
-      staged = hoff;
-    }
-    double a[kStreamUnroll][SV];
-    int64_t bc[kStreamUnroll];
-    int pb[kStreamUnroll];
-    bool ok[kStreamUnroll];
-#pragma unroll
-    for (int u = 0; u < kStreamUnroll; ++u) {
-      const int64_t x = base + u * kStreamThreads + threadIdx.x;
-      ok[u] = x < p.nx;
-      const int64_t ba = ok[u] ? deposit(x, p.xa) + deposit(x, p.xa2) : 0;
-      bc[u] = ok[u] ? deposit(x, p.xc) : 0;
-      int lbi = 0;
-      for (int t = 0; t < nlb; ++t) lbi |= (int)((x >> p.bt_xbit[t]) & 1) << t;
-      pb[u] = lbi * SVFV;
-#pragma unroll
-      for (int s = 0; s < SV; ++s) a[u][s] = ok[u] ? __ldcs(p.A + ba + p.offA[s]) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < kStreamUnroll; ++u) {
-      if (!ok[u]) continue;
-      const double* Pu = P + pb[u];
-#pragma unroll
-      for (int f = 0; f < FV; ++f) {
-        double acc = 0.0;
-#pragma unroll
-        for (int s = 0; s < SV; ++s) acc = fma(a[u][s], Pu[s * FV + f], acc);
-        p.C[bc[u] + p.offC[f]] = acc;
+    } else {  // a single partial chunk (nx < 2^CB)
+      for (int u = 0; u < kStreamUnroll; ++u) {
+        if (u * kStreamThreads + tid >= p.nx) continue;
+        const double* Pu = Pc + lo_p[u];
+        for (int f = 0; f < FV; ++f) {
+          double acc = 0.0;
+          for (int s = 0; s < SV; ++s) acc = fma(Ab[lo_a[u] + p.offA[s]], pv(Pu, s * FV + f), acc);
+          Cb[lo_c[u] + p.offC[f]] = acc;
+        }
       }
     }
   }

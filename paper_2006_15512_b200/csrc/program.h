@@ -33,6 +33,16 @@ TC_HD int64_t deposit(uint64_t x, const BitRuns& r) {
   return (int64_t)o;
 }
 
+// the same, as a rolled loop (setup code: fewer instructions and registers)
+TC_HD int64_t deposit_rolled(uint64_t x, const BitRuns& r) {
+  uint64_t o = 0;
+#if defined(__CUDACC__)
+#pragma unroll 1
+#endif
+  for (int j = 0; j < r.n; ++j) o |= ((x >> r.src[j]) & ((1ull << r.len[j]) - 1ull)) << r.dst[j];
+  return (int64_t)o;
+}
+
 // ---- K2: big x small streaming contraction (dim 2) ------------------------
 // C[x, f] = sum_s A[x, s] * P[s, f]; x enumerates the kept indices of the big
 // operand A, s the shared ones (<= 2^4), f the small operand's free ones (<= 2^4).
@@ -44,7 +54,8 @@ TC_HD int64_t deposit(uint64_t x, const BitRuns& r) {
 // chunk) and the nlb lower ones select among the staged copies per element.
 constexpr int kStreamMaxBatch = 24;
 constexpr int kStreamChunkBits = 10;
-constexpr int kStreamSmemMax = 4096;  // doubles of staged P per CTA
+constexpr int kStreamStageMax = 256;  // doubles of staged P per CTA
+constexpr int kStreamXBits = 44;
 struct StreamParams {
   const double* A;
   const double* P;
@@ -57,6 +68,16 @@ struct StreamParams {
   int32_t nbt, nlb;   // batch bits (ascending x bit), of which nlb below the chunk
   int32_t bt_xbit[kStreamMaxBatch];
   int64_t bt_poff[kStreamMaxBatch];
+  // the low kStreamChunkBits x bits: address contribution of each bit (A incl.
+  // diagonal reads, C) and its weight in the staged-P batch index
+  // per x bit: address contribution (A incl. diagonal reads, C), batch-index
+  // weight (staged mode) and P offset (direct mode).  Deposits are additive
+  // over disjoint bits, so any address is a sum of table entries.
+  int64_t bitA[kStreamXBits], bitC[kStreamXBits], bitPo[kStreamXBits];
+  int32_t bitP[kStreamXBits];
+  int32_t kchunk;  // each CTA walks 2^kchunk chunks (Gray-code order)
+  int32_t stage_all;  // 1: the small operand ((SV*FV) << nbt <= kStreamStageMax entries) is staged
+                      //    in smem once per CTA; 0: it is read through the L1 (direct)
 };
 
 // ---- K3: FP64 DMMA GEMM with bit-permuted operands (dim 2) -----------------
@@ -101,8 +122,15 @@ struct TinyNode {
   int32_t nc, ns;
   int32_t dig;   // first digit (nc C-digits then ns S-digits)
   int32_t pow2;  // all digits have dim 2
+  int32_t sta, stb;  // staging offsets of small global operands within the batch (-1: read global)
+  int32_t na, nb;    // entry counts of the staged operands
   int32_t pad;
 };
+// k_tiny processes a group in batches of kTinyBatch nodes: descriptors,
+// digits and small global operands (leaves) of a batch are copied to smem
+// with one round of independent loads before the batch's nodes run.
+constexpr int kTinyBatch = 32;
+constexpr int kTinyStageMax = 64;  // entries: larger global operands are read in place
 struct TinyDigit {
   int32_t dim, sa, sb, pad;
 };

@@ -340,7 +340,8 @@ struct tc_exec {
     folded = dalloc<double>((size_t)g.R, dev_bytes, device);
     CU(cudaStreamSynchronize(stream));
 
-    const int tiny_smem = (int)(g.tiny_smem_doubles + kTinyThreads) * 8;
+    const int tiny_smem = (int)(g.tiny_smem_doubles + kTinyThreads + g.tiny_stage_doubles) * 8 +
+                          kTinyBatch * (int)sizeof(TinyNode) + g.tiny_dig_max * (int)sizeof(TinyDigit);
     CU(cudaFuncSetAttribute(k_tiny, cudaFuncAttributeMaxDynamicSharedMemorySize, tiny_smem));
     for (int bm = 3; bm <= 7; ++bm)
       for (int bn = 3; bn <= 6; ++bn) {
@@ -377,6 +378,7 @@ struct tc_exec {
           L.arg((const TinyDigit*)tdigs);
           L.arg((const TinyGroup*)(tgroups + st.gdig_off));
           L.arg((int32_t)g.tiny_smem_doubles);
+          L.arg((int32_t)g.tiny_stage_doubles);
           break;
         }
         case ST_STREAM: {
@@ -386,8 +388,15 @@ struct tc_exec {
           sp.C = (double*)ptr(st.lc);
           L.func = (void*)stream_fn(st.ns, st.nf);
           L.block = dim3(kStreamThreads);
-          L.smem = (unsigned)((((1 << st.ns) << st.nf) << sp.nlb) * sizeof(double));
-          L.grid = dim3(grid_for(sp.nx, kStreamThreads * kStreamUnroll, device));
+          // 2^g CTAs, each walking 2^kchunk chunks of 2^kStreamChunkBits x
+          {
+            const int xb = 63 - __builtin_clzll((unsigned long long)sp.nx);  // nx is a power of two
+            const int chunks_log = std::max(0, xb - kStreamChunkBits);
+            int g = 0;
+            while (g < chunks_log && (2 << g) <= sm_count(device) * 4) ++g;
+            sp.kchunk = chunks_log - g;
+            L.grid = dim3(1u << g);
+          }
           L.arg(sp);
           break;
         }
@@ -565,6 +574,44 @@ struct tc_exec {
     cudaEventDestroy(e1);
     last_n = n;
     return ms;
+  }
+
+  // passes timed one by one, each after an untimed L2 flush
+  double run_flushed(int64_t b, int64_t e, int64_t repeats, int64_t flush_bytes) {
+    CU(cudaSetDevice(device));
+    const int64_t n = e - b;
+    if (n <= 0) {
+      last_n = 0;
+      return 0.0;
+    }
+    ensure_results(n);
+    ensure_graph();
+    const int64_t n4 = std::max<int64_t>(1, flush_bytes / 32);
+    int64_t scratch = 0;  // not part of the program footprint
+    double4* fbuf = dalloc<double4>((size_t)n4, scratch, device);
+    std::vector<cudaEvent_t> ev(2 * repeats);
+    for (auto& x : ev) CU(cudaEventCreate(&x));
+    int64_t h[2] = {b, b};
+    CU(cudaMemcpyAsync(eta, h, sizeof(h), cudaMemcpyHostToDevice, stream));
+    for (int64_t r = 0; r < repeats; ++r) {
+      if (r > 0) k_eta_reset<<<1, 1, 0, stream>>>(eta);
+      k_flush<<<grid_for(n4, 256, device), 256, 0, stream>>>(fbuf, n4, (double)r);
+      CU(cudaEventRecord(ev[2 * r], stream));
+      for (int64_t s = 0; s < n; ++s) CU(cudaGraphLaunch(gexec, stream));
+      CU(cudaEventRecord(ev[2 * r + 1], stream));
+    }
+    CU(cudaStreamSynchronize(stream));
+    CU(cudaGetLastError());
+    double total = 0;
+    for (int64_t r = 0; r < repeats; ++r) {
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, ev[2 * r], ev[2 * r + 1]));
+      total += ms;
+    }
+    for (auto& x : ev) cudaEventDestroy(x);
+    dcache().put(device, fbuf);
+    last_n = n;
+    return total;
   }
 
   void fold(double* out_host) {
@@ -797,6 +844,17 @@ int tc_exec_run_repeat(tc_exec* ex, int64_t slice_begin, int64_t slice_end, int6
     double ms = ex->run(slice_begin, slice_end, repeats);
     fill_stats(*ex, ms, stats);
     if (stats) stats->gpu_launches = (ex->kernels_per_slice * ex->last_n + 1) * repeats - 1;
+  });
+}
+
+int tc_exec_run_flushed(tc_exec* ex, int64_t slice_begin, int64_t slice_end, int64_t repeats, int64_t flush_bytes,
+                        tc_stats* stats) {
+  return guard([&] {
+    if (slice_begin < 0 || slice_end > ex->prog.num_slices || slice_begin > slice_end || repeats < 1)
+      throw Error{TC_BAD_ARG, "slice range out of bounds"};
+    double ms = ex->run_flushed(slice_begin, slice_end, repeats, flush_bytes);
+    fill_stats(*ex, ms, stats);
+    if (stats) stats->gpu_launches = ex->kernels_per_slice * ex->last_n * repeats;
   });
 }
 

@@ -1,0 +1,167 @@
+"""GPU tests of tie-aware execution (compile.cpp "physical variables").
+
+FactorTree's copy-tensor pieces are generalised diagonals; libtc stores such
+leaves over their tie blocks and propagates ties through the tree (union-find,
+push-down to where two tied indices meet).  These tests build random networks
+rich in identity / delta / weighted-diagonal pieces -- with free indices tied at
+the root, diagonal reads of internal operands, batch variables, explicit slices
+through tied leaves -- and check the result against a dense numpy einsum of the
+whole network and against libtc's own dense path (TC_NO_TIES=1, read per call).
+"""
+
+import os
+import random
+import string
+
+import numpy as np
+import pytest
+
+from paper_2006_15512_b200 import Index, Tensor, TensorNetwork, join, leaf, planfile, sliced_execute
+from paper_2006_15512_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _delta(inds, w=None):
+    r = len(inds)
+    v = np.zeros([2] * r)
+    v[(0,) * r] = 1.0 if w is None else w[0]
+    v[(1,) * r] = 1.0 if w is None else w[1]
+    return Tensor(tuple(inds), v)
+
+
+def _random_tied_network(rng, n_tensors):
+    """Tensors of rank 1-3 over dim-2 indices, each index in <= 2 tensors;
+    about half are identity / delta / weighted-diagonal pieces."""
+    stubs = []
+    specs = []
+    for t in range(n_tensors):
+        r = rng.choice([1, 2, 2, 3, 3, 3])
+        specs.append(r)
+        stubs += [t] * r
+    rng.shuffle(stubs)
+    inds = [[] for _ in range(n_tensors)]
+    k = 0
+    while stubs:
+        a = stubs.pop()
+        partner = next((j for j, b in enumerate(stubs) if b != a), None)
+        ix = Index(("x", k), 2)
+        k += 1
+        inds[a].append(ix)
+        if partner is not None and rng.random() < 0.9:
+            inds[stubs.pop(partner)].append(ix)
+    ts = []
+    for t in range(n_tensors):
+        ii = inds[t]
+        kind = rng.random()
+        if len(ii) >= 2 and kind < 0.35:
+            ts.append(_delta(ii))
+        elif len(ii) >= 2 and kind < 0.5:
+            ts.append(_delta(ii, (rng.uniform(0.2, 1), rng.uniform(0.2, 1))))
+        else:
+            shape = [2] * len(ii)
+            ts.append(Tensor(tuple(ii), np.array([rng.uniform(-1, 1) for _ in range(2 ** len(ii))]).reshape(shape)))
+    return TensorNetwork(tuple(ts))
+
+
+def _random_tree(rng, tensors):
+    nodes = [leaf(t) for t in tensors]
+    while len(nodes) > 1:
+        i, j = sorted(rng.sample(range(len(nodes)), 2))
+        b = nodes.pop(j)
+        a = nodes.pop(i)
+        nodes.append(join(a, b) if rng.random() < 0.5 else join(b, a))
+    return nodes[0]
+
+
+def _einsum(n, order):
+    letters = {}
+    pool = iter(string.ascii_letters)
+    ops, subs = [], []
+    for t in n.tensors:
+        s = ""
+        for ix in t.indices:
+            if ix.id not in letters:
+                letters[ix.id] = next(pool)
+            s += letters[ix.id]
+        subs.append(s)
+        ops.append(np.asarray(t.values))
+    out = "".join(letters[ix.id] for ix in order)
+    return np.einsum(",".join(subs) + "->" + out, *ops, optimize=True)
+
+
+def _run(n, t, **kw):
+    r = sliced_execute(n, t, **kw)
+    return r, np.asarray(r.result.values)
+
+
+def _dense(n, t, **kw):
+    os.environ["TC_NO_TIES"] = "1"
+    try:
+        return _run(n, t, **kw)
+    finally:
+        del os.environ["TC_NO_TIES"]
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_tied_networks_match_dense(seed):
+    rng = random.Random(1000 + seed)
+    n = _random_tied_network(rng, rng.randint(6, 16))
+    t = _random_tree(rng, list(n.tensors))
+    out, got = _run(n, t)
+    want = _einsum(n, out.result.indices)
+    assert got.shape == want.shape
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
+    d, dv = _dense(n, t)
+    assert list(d.result.indices) == list(out.result.indices)
+    assert np.allclose(got, dv, rtol=1e-12, atol=1e-13)
+    assert out.mem_estimate == d.mem_estimate and out.peak_observed == d.peak_observed
+    # an explicit slice through bonds (possibly inside tied blocks)
+    bonds = sorted({ix.id for ix in n.bond_indices}, key=repr)
+    if bonds:
+        pick = [Index(b, 2) for b in rng.sample(bonds, min(2, len(bonds)))]
+        s, sv = _run(n, t, slice_indices=pick)
+        assert s.num_slices == 2 ** len(pick)
+        assert np.allclose(sv, got, rtol=1e-12, atol=1e-12)
+
+
+def test_root_with_tied_free_indices():
+    """The root keeps two indices tied by a delta piece: the dense result has
+    structural zeros off the diagonal (root_map expansion)."""
+    rng = np.random.default_rng(3)
+    i, j, k, l = (Index(c, 2) for c in "ijkl")
+    a = Tensor((i, j), rng.uniform(-1, 1, (2, 2)))
+    d = _delta((j, k, l))  # k and l stay free, tied
+    n = TensorNetwork((a, d))
+    out, got = _run(n, join(leaf(a), leaf(d)))
+    assert [ix.id for ix in out.result.indices] == ["i", "k", "l"]
+    want = np.einsum("ij,jkl->ikl", a.values, d.values)
+    assert np.array_equal(got, want)
+    assert got[:, 0, 1].tolist() == [0.0, 0.0] and got[:, 1, 0].tolist() == [0.0, 0.0]
+
+
+def test_diagonal_read_and_pushdown():
+    """delta(s1, s2, f) contracts two separate indices of an internal operand:
+    the tie is pushed down to where s1 and s2 meet."""
+    rng = np.random.default_rng(5)
+    idx = [Index(("q", c), 2) for c in range(14)]
+    a = Tensor(tuple(idx[0:7]), rng.uniform(-1, 1, [2] * 7))
+    b = Tensor(tuple(idx[7:14]), rng.uniform(-1, 1, [2] * 7))
+    f = Index("f", 2)
+    d = _delta((idx[3], idx[10], f))
+    n = TensorNetwork((a, b, d))
+    t = join(join(leaf(a), leaf(b)), leaf(d))
+    out, got = _run(n, t)
+    want = _einsum(n, out.result.indices)
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["c1a", "c2"])
+def test_benchmark_plan_dense_path_agrees(name):
+    flat, _ = planfile.load(os.path.join(os.path.dirname(__file__), "..", "data", "plans", f"{name}.tcplan.npz"))
+    n, t = planfile.to_objects(flat)
+    tied, tv = _run(n, t)
+    dense, dv = _dense(n, t)
+    assert abs(float(tv) - float(dv)) <= 1e-12 * abs(float(dv))
+    st = _lib.PlanHandle(flat).compile_stats([])
+    assert st["n_tied_leaves"] > 0 and st["phys_bytes"] < st["alg_bytes"]

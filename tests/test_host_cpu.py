@@ -220,3 +220,23 @@ def test_native_flatten_views_dtypes_and_mismatch():
     other = Tensor((i,), np.ones(2))
     bad = flatten(n, join(join(leaf(a), leaf(other)), leaf(s)))
     assert (bad.left < 0).any() or (bad.right < 0).any()
+
+
+def test_tie_compression_stats_on_benchmark_plan():
+    """Copy-tensor pieces are stored over tie blocks: the executed work of the
+    C2 plan is a small fraction of the dense per-node work; the dense path
+    (TC_NO_TIES=1) keeps dense variables and the same reference accounting."""
+    flat, _ = planfile.load(os.path.join(PLANS, "c2.tcplan.npz"))
+    h = _lib.PlanHandle(flat)
+    tied = h.compile_stats([])
+    os.environ["TC_NO_TIES"] = "1"
+    try:
+        dense = h.compile_stats([])
+    finally:
+        del os.environ["TC_NO_TIES"]
+    assert tied["n_tied_leaves"] > 10000 and dense["n_tied_leaves"] == 0
+    assert tied["alg_bytes"] == dense["alg_bytes"] and tied["alg_flops"] == dense["alg_flops"]
+    assert tied["mem_estimate"] == dense["mem_estimate"] and tied["peak_observed"] == dense["peak_observed"]
+    assert tied["phys_bytes"] * 10 < dense["phys_bytes"]
+    assert tied["phys_flops"] * 100 < dense["phys_flops"]
+    assert tied["device_peak_bytes"] * 10 < dense["device_peak_bytes"]
