@@ -45,6 +45,7 @@
 #include <map>
 #include <set>
 #include <string>
+#include <thread>
 #include <tuple>
 
 namespace tc {
@@ -216,6 +217,21 @@ BitRuns make_runs(const std::vector<std::pair<int, int>>& bits) {  // (src bit, 
   return r;
 }
 
+// Split [0, n) into up to 8 contiguous ranges (at least `grain` items each)
+// run on worker threads; f(lo, hi) must not throw.
+template <class F>
+void parallel_for(int n, int grain, F f) {
+  const int T = std::max(1, std::min(8, n / std::max(1, grain)));
+  if (T == 1) {
+    f(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int w = 1; w < T; ++w) th.emplace_back(f, (int)((int64_t)n * w / T), (int)((int64_t)n * (w + 1) / T));
+  f(0, (int)((int64_t)n / T));
+  for (auto& x : th) x.join();
+}
+
 // One component of tied indices at a contraction: its variable in C (-1:
 // summed) and its variables in the operands A (left) and B (right).
 struct Comp {
@@ -368,11 +384,33 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   // mem[s]: (logical index, variable) pairs sorted by logical index; a
   // variable is named by the smallest logical index of its block.
   bool ties = std::getenv("TC_NO_TIES") == nullptr;
-  std::vector<std::vector<std::pair<int, int>>> mem(S);
-  std::vector<std::vector<int>> vars(S);  // sorted variable ids per slot
+  // Per-slot tables live in two pools (no per-node allocations): leaves at
+  // fixed offsets, internal nodes appended in postorder (a recomputed node
+  // appends again; capacity is reserved before each pass so spans stay valid).
+  using MPair = std::pair<int, int>;
+  struct MemSpan {
+    const MPair *b, *e;
+    const MPair* begin() const { return b; }
+    const MPair* end() const { return e; }
+    size_t size() const { return (size_t)(e - b); }
+    const MPair& operator[](size_t i) const { return b[i]; }
+  };
+  struct IntSpan {
+    const int *b, *e;
+    const int* begin() const { return b; }
+    const int* end() const { return e; }
+    size_t size() const { return (size_t)(e - b); }
+    int operator[](size_t i) const { return b[i]; }
+  };
+  std::vector<MPair> mpool;
+  std::vector<int> vpool;
+  std::vector<int64_t> mbeg(S), mend(S), vbeg(S), vend(S);
+  auto mem = [&](int s) { return MemSpan{mpool.data() + mbeg[s], mpool.data() + mend[s]}; };
+  auto varsv = [&](int s) { return IntSpan{vpool.data() + vbeg[s], vpool.data() + vend[s]}; };
+  int64_t logical_total = 0;
+  for (int s = 0; s < S; ++s) logical_total += (int64_t)p.sets[s].size();
   std::vector<Comp> cpool;
   std::vector<int32_t> coff(p.NN + 1, 0);
-  std::vector<int> lab;
   std::vector<int> uf(p.NI, -1), own_a(p.NI, -1), own_b(p.NI, -1), cidx(p.NI, -1);
   std::vector<char> leaf_tied(p.NL, 0);
   auto find = [&](int x) {
@@ -391,37 +429,49 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   // directly on the diagonal: half the work and bytes per tie, and no gather.
   std::vector<std::vector<std::pair<int, int>>> req(p.NN);
   auto has_logical = [&](int s, int l) {
-    const auto& m = mem[s];
+    const auto m = mem(s);
     auto f = std::lower_bound(m.begin(), m.end(), std::make_pair(l, INT_MIN));
     return f != m.end() && f->first == l;
   };
   int pushdown_rounds = 0;
   auto build_leaves = [&]() {
+    // leaf l owns [off[l], off[l] + kept) in both pools
+    std::vector<int64_t> off(p.NL + 1, 0);
     for (int l = 0; l < p.NL; ++l) {
-      const auto& ro = p.ref_order[l];
-      auto& m = mem[l];
-      m.clear();
-      m.reserve(ro.size());
-      vars[l].reserve(ro.size());
-      leaf_tied[l] = ties && leaf_ties(p, l, drop, lab);
-      if (leaf_tied[l]) {
-        int bmin[8];
-        for (int q = 0; q < 8; ++q) bmin[q] = INT_MAX;
-        for (size_t q = 0; q < ro.size(); ++q)
-          if (lab[q] >= 0) bmin[lab[q]] = std::min(bmin[lab[q]], ro[q]);
-        for (size_t q = 0; q < ro.size(); ++q)
-          if (lab[q] >= 0) m.push_back({ro[q], bmin[lab[q]]});
-      } else {
-        for (int i : ro)
-          if (!drop[i]) m.push_back({i, i});
-      }
-      std::sort(m.begin(), m.end());
-      auto& vv = vars[l];
-      vv.clear();
-      for (auto& e : m) vv.push_back(e.second);
-      std::sort(vv.begin(), vv.end());
-      vv.erase(std::unique(vv.begin(), vv.end()), vv.end());
+      int64_t k = 0;
+      for (int i : p.ref_order[l]) k += !drop[i];
+      off[l + 1] = off[l] + k;
     }
+    mpool.assign(off[p.NL], MPair{0, 0});
+    vpool.assign(off[p.NL], 0);
+    parallel_for(p.NL, 4096, [&](int l0, int l1) {
+      std::vector<int> lab;
+      for (int l = l0; l < l1; ++l) {
+        const auto& ro = p.ref_order[l];
+        MPair* m = mpool.data() + off[l];
+        int n = 0;
+        leaf_tied[l] = ties && leaf_ties(p, l, drop, lab);
+        if (leaf_tied[l]) {
+          int bmin[8];
+          for (int q = 0; q < 8; ++q) bmin[q] = INT_MAX;
+          for (size_t q = 0; q < ro.size(); ++q)
+            if (lab[q] >= 0) bmin[lab[q]] = std::min(bmin[lab[q]], ro[q]);
+          for (size_t q = 0; q < ro.size(); ++q)
+            if (lab[q] >= 0) m[n++] = {ro[q], bmin[lab[q]]};
+        } else {
+          for (int i : ro)
+            if (!drop[i]) m[n++] = {i, i};
+        }
+        std::sort(m, m + n);
+        mbeg[l] = off[l];
+        mend[l] = off[l] + n;
+        int* vv = vpool.data() + off[l];
+        for (int q = 0; q < n; ++q) vv[q] = m[q].second;
+        std::sort(vv, vv + n);
+        vbeg[l] = off[l];
+        vend[l] = off[l] + (std::unique(vv, vv + n) - vv);
+      }
+    });
   };
   build_leaves();
   // Requests known before the pass: a tied leaf piece whose block holds two
@@ -446,7 +496,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       const int v = p.parent[l], k = v - p.NL;
       const int x = p.left[k] == l ? p.right[k] : p.left[k];
       if (p.is_leaf(x)) continue;
-      const auto& m = mem[l];
+      const auto m = mem(l);
       for (size_t i = 0; i < m.size(); ++i)
         for (size_t j = i + 1; j < m.size(); ++j)
           if (m[i].second == m[j].second && std::binary_search(p.sets[x].begin(), p.sets[x].end(), m[i].first) &&
@@ -465,6 +515,9 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     coff_prev = coff;
     cpool.clear();
     std::vector<Comp> cs;
+    // room for every node's tables: spans into the pools stay valid below
+    mpool.reserve(mpool.size() + (size_t)logical_total + 16);
+    vpool.reserve(vpool.size() + (size_t)logical_total + 16);
     for (int k = 0; k < p.NN && !overflow; ++k) {
       const int v = p.NL + k, a = p.left[k], b = p.right[k];
       coff[k] = (int32_t)cpool.size();
@@ -473,11 +526,13 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         cpool.insert(cpool.end(), cpool_prev.begin() + coff_prev[k], cpool_prev.begin() + coff_prev[k + 1]);
         continue;
       }
-      for (auto& e : mem[a]) own_a[e.first] = e.second;
-      for (auto& e : mem[b]) own_b[e.first] = e.second;
-      for (int x : vars[a]) uf[x] = x;
-      for (int x : vars[b]) uf[x] = x;
-      for (auto& e : mem[b])
+      const MemSpan Ma = mem(a), Mb = mem(b);
+      const IntSpan Va = varsv(a), Vb = varsv(b);
+      for (auto& e : Ma) own_a[e.first] = e.second;
+      for (auto& e : Mb) own_b[e.first] = e.second;
+      for (int x : Va) uf[x] = x;
+      for (int x : Vb) uf[x] = x;
+      for (auto& e : Mb)
         if (own_a[e.first] >= 0) {
           int r1 = find(own_a[e.first]), r2 = find(e.second);
           if (r1 != r2) uf[std::max(r1, r2)] = std::min(r1, r2);
@@ -500,50 +555,48 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         }
         return cs[cidx[r]];
       };
-      for (int x : vars[a]) {
+      for (int x : Va) {
         Comp& c = comp_of(x);
         if (c.na == kMaxTie) overflow = true;
         else c.a[c.na++] = x;
       }
-      for (int x : vars[b]) {
+      for (int x : Vb) {
         Comp& c = comp_of(x);
         if (c.nb == kMaxTie) overflow = true;
         else c.b[c.nb++] = x;
       }
       // kept logical indices -> component's C variable (smallest kept index)
-      auto& mv = mem[v];
-      mv.clear();
-      mv.reserve(mem[a].size() + mem[b].size());
+      const int64_t m0 = (int64_t)mpool.size();
       {
-        const auto& Ma = mem[a];
-        const auto& Mb = mem[b];
         size_t x = 0, y = 0;
         for (;;) {  // merge the kept entries of both (each sorted by logical index)
           while (x < Ma.size() && own_b[Ma[x].first] >= 0) ++x;
           while (y < Mb.size() && own_a[Mb[y].first] >= 0) ++y;
           if (x == Ma.size() && y == Mb.size()) break;
-          if (y == Mb.size() || (x < Ma.size() && Ma[x].first < Mb[y].first)) mv.push_back(Ma[x++]);
-          else mv.push_back(Mb[y++]);
+          if (y == Mb.size() || (x < Ma.size() && Ma[x].first < Mb[y].first)) mpool.push_back(Ma[x++]);
+          else mpool.push_back(Mb[y++]);
         }
       }
-      for (auto& e : mv) {
-        Comp& c = comp_of(e.second);
-        if (c.c < 0) c.c = e.first;  // mv is sorted: first kept = smallest
+      for (int64_t q = m0; q < (int64_t)mpool.size(); ++q) {
+        Comp& c = comp_of(mpool[q].second);
+        if (c.c < 0) c.c = mpool[q].first;  // sorted: first kept = smallest
       }
-      for (auto& e : mv) e.second = comp_of(e.second).c;
-      auto& vv = vars[v];
-      vv.clear();
-      vv.reserve(cs.size());
+      for (int64_t q = m0; q < (int64_t)mpool.size(); ++q) mpool[q].second = comp_of(mpool[q].second).c;
+      mbeg[v] = m0;
+      mend[v] = (int64_t)mpool.size();
+      const int64_t v0 = (int64_t)vpool.size();
       for (const Comp& c : cs)
-        if (c.c >= 0) vv.push_back(c.c);
-      std::sort(vv.begin(), vv.end());
+        if (c.c >= 0) vpool.push_back(c.c);
+      std::sort(vpool.begin() + v0, vpool.end());
+      vbeg[v] = v0;
+      vend[v] = (int64_t)vpool.size();
       // reset scratch (before reordering cs: cidx indexes into it)
-      for (int x : vars[a]) cidx[find(x)] = -1;
-      for (int x : vars[b]) cidx[find(x)] = -1;
-      for (int x : vars[a]) uf[x] = -1;
-      for (int x : vars[b]) uf[x] = -1;
-      for (auto& e : mem[a]) own_a[e.first] = -1;
-      for (auto& e : mem[b]) own_b[e.first] = -1;
+      for (int x : Va) cidx[find(x)] = -1;
+      for (int x : Vb) cidx[find(x)] = -1;
+      for (int x : Va) uf[x] = -1;
+      for (int x : Vb) uf[x] = -1;
+      for (auto& e : Ma) own_a[e.first] = -1;
+      for (auto& e : Mb) own_b[e.first] = -1;
       std::sort(cs.begin(), cs.end(), [](const Comp& x, const Comp& y) { return x.key() < y.key(); });
       cpool.insert(cpool.end(), cs.begin(), cs.end());
     }
@@ -597,21 +650,22 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     std::fill(dirty.begin(), dirty.end(), 1);
   }
   struct EffView {
-    const std::vector<std::vector<int>>* v;
-    const std::vector<int>& operator[](int s) const { return (*v)[s]; }
-  } eff{&vars};
+    const std::vector<int>* pool;
+    const std::vector<int64_t>*b, *e;
+    IntSpan operator[](int s) const { return IntSpan{pool->data() + (*b)[s], pool->data() + (*e)[s]}; }
+  } eff{&vpool, &vbeg, &vend};
   auto comps = [&](int v) {
     return std::make_pair((const Comp*)cpool.data() + coff[v - p.NL], (const Comp*)cpool.data() + coff[v - p.NL + 1]);
   };
   std::vector<int64_t> size(S);
   for (int s = 0; s < S; ++s) {
     u128 z = 1;
-    for (int i : vars[s]) z *= (u128)p.dom[i];
+    for (int i : varsv(s)) z *= (u128)p.dom[i];
     if (z > ((u128)1 << 50)) fail(TC_OOM, "intermediate tensor larger than 2^50 entries");
     size[s] = (int64_t)z;
   }
   auto var_of = [&](int s, int logical) {
-    const auto& m = mem[s];
+    const auto m = mem(s);
     return std::lower_bound(m.begin(), m.end(), std::make_pair(logical, INT_MIN))->second;
   };
   // natural layout: the reference's row-major order (first index slowest),
@@ -620,7 +674,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   auto natural = [&](int s) {
     std::vector<int> o;
     const auto& ro = p.ref_order[s];
-    o.reserve(vars[s].size());
+    o.reserve(varsv(s).size());
     for (auto it = ro.rbegin(); it != ro.rend(); ++it) {
       if (drop[*it]) continue;
       const int var = var_of(s, *it);
@@ -673,7 +727,19 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   tmark("layouts (top-down)");
   // ---- layouts (top-down) ----------------------------------------------------
   g.layout.assign(S, {});
-  for (int l = 0; l < p.NL; ++l) g.layout[l] = natural(l);
+  parallel_for(p.NL, 4096, [&](int l0, int l1) {
+    for (int l = l0; l < l1; ++l) {  // natural() without the shared first-occurrence marks
+      std::vector<int> o;
+      const auto& ro = p.ref_order[l];
+      o.reserve(varsv(l).size());
+      for (auto it = ro.rbegin(); it != ro.rend(); ++it) {
+        if (drop[*it]) continue;
+        const int var = var_of(l, *it);
+        if (std::find(o.begin(), o.end(), var) == o.end()) o.push_back(var);
+      }
+      g.layout[l] = std::move(o);
+    }
+  });
   std::vector<int> pos(p.NI, -1);
   auto set_pos = [&](const std::vector<int>& L) {
     for (size_t q = 0; q < L.size(); ++q) pos[L[q]] = (int)q;
@@ -1053,17 +1119,41 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       st2 *= p.dom[i];
     }
   };
-  std::vector<std::vector<int>> level_groups(nlevels);
-  std::vector<int> tiny_slot;  // slot of each tiny descriptor
-  for (size_t gi = 0; gi < groups.size(); ++gi) level_groups[glevel[gi]].push_back((int)gi);
+  // Groups are independent: descriptors are built on worker threads over
+  // contiguous ranges of the level-major group order and concatenated.
+  std::vector<int> gorder;
   std::vector<std::pair<int32_t, int32_t>> level_range(nlevels);
-  for (int lv = 0; lv < nlevels; ++lv) {
-    level_range[lv].first = (int32_t)g.tiny_groups.size();
-    for (int gi : level_groups[lv]) {
+  {
+    std::vector<std::vector<int>> level_groups(nlevels);
+    for (size_t gi = 0; gi < groups.size(); ++gi) level_groups[glevel[gi]].push_back((int)gi);
+    for (int lv = 0; lv < nlevels; ++lv) {
+      level_range[lv].first = (int32_t)gorder.size();
+      for (int gi : level_groups[lv]) gorder.push_back(gi);
+      level_range[lv].second = (int32_t)gorder.size();
+    }
+  }
+  struct TinyOut {
+    std::vector<TinyNode> nodes;
+    std::vector<TinyDigit> digs;
+    std::vector<Loc> ga, gb, go;
+    std::vector<TinyGroup> grp;
+    int32_t stage = 0, digmax = 0;
+  };
+  auto build_groups = [&](int q0, int q1, TinyOut& out) {
+    std::vector<int64_t> sa_(p.NI, 0), sb_(p.NI, 0);
+    std::vector<const Comp*> cc(p.NI, nullptr);
+    auto strides2 = [&](const Comp* c, int64_t& sa, int64_t& sb) {
+      sa = sb = 0;
+      for (int t = 0; t < c->na; ++t) sa += sa_[c->a[t]];
+      for (int t = 0; t < c->nb; ++t) sb += sb_[c->b[t]];
+    };
+    std::vector<int> slot;
+    for (int q = q0; q < q1; ++q) {
+      const int gi = gorder[q];
       const auto& nodes = groups[gi];
-      int r = nodes.back();
+      const int r = nodes.back();
       TinyGroup tg;
-      tg.beg = (int32_t)g.tiny_nodes.size();
+      tg.beg = (int32_t)out.nodes.size();
       for (int v : nodes) {
         const int a = p.kid_l(v), b = p.kid_r(v);
         TinyNode tn{};
@@ -1084,79 +1174,112 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         const auto& La = g.layout[a];
         const auto& Lb = g.layout[b];
         const auto& Lc = g.layout[v];
-        load_strides(La, Lb);
+        int64_t st2 = 1;
+        for (int i : La) sa_[i] = st2, st2 *= p.dom[i];
+        st2 = 1;
+        for (int i : Lb) sb_[i] = st2, st2 *= p.dom[i];
         auto [c0, c1] = comps(v);
         for (const Comp* c = c0; c != c1; ++c)
-          if (c->c >= 0) ccomp[c->c] = c;
-        tn.dig = (int32_t)g.tiny_digits.size();
+          if (c->c >= 0) cc[c->c] = c;
+        tn.dig = (int32_t)out.digs.size();
         bool p2 = true;
         for (int i : Lc) {
           int64_t sa, sb;
-          comp_strides(ccomp[i], sa, sb);
-          g.tiny_digits.push_back(TinyDigit{p.dom[i], (int32_t)sa, (int32_t)sb, 0});
+          strides2(cc[i], sa, sb);
+          out.digs.push_back(TinyDigit{p.dom[i], (int32_t)sa, (int32_t)sb, 0});
           p2 &= (p.dom[i] == 2);
         }
         int64_t ssz = 1;
         int ns = 0;
         for (const Comp* c = c0; c != c1; ++c) {  // sorted by smallest variable
           if (c->c >= 0) {
-            ccomp[c->c] = nullptr;
+            cc[c->c] = nullptr;
             continue;
           }
           int64_t sa, sb;
-          comp_strides(c, sa, sb);
+          strides2(c, sa, sb);
           const int d = p.dom[c->a[0]];
-          g.tiny_digits.push_back(TinyDigit{d, (int32_t)sa, (int32_t)sb, 0});
+          out.digs.push_back(TinyDigit{d, (int32_t)sa, (int32_t)sb, 0});
           p2 &= (d == 2);
           ssz *= d;
           ++ns;
         }
-        for (int i : La) str_a[i] = 0;
-        for (int i : Lb) str_b[i] = 0;
+        for (int i : La) sa_[i] = 0;
+        for (int i : Lb) sb_[i] = 0;
         tn.nc = (int32_t)Lc.size();
         tn.ns = ns;
         tn.c_size = (int32_t)size[v];
         tn.s_size = (int32_t)ssz;
         tn.pow2 = p2 ? 1 : 0;
-        g.tiny_nodes.push_back(tn);
-        tiny_slot.push_back(v);
-        g.tiny_ga.push_back(la);
-        g.tiny_gb.push_back(lb);
-        g.tiny_gout.push_back(lo);
-        g.n_tiny++;
+        out.nodes.push_back(tn);
+        slot.push_back(v);
+        out.ga.push_back(la);
+        out.gb.push_back(lb);
+        out.go.push_back(lo);
       }
-      tg.end = (int32_t)g.tiny_nodes.size();
+      tg.end = (int32_t)out.nodes.size();
       // batches of kTinyBatch nodes: staging offsets of small global operands
       // (leaves, sliced leaves, small forced roots) and the digit block size
       for (int b0 = tg.beg; b0 < tg.end; b0 += kTinyBatch) {
         const int b1 = std::min(tg.end, b0 + kTinyBatch);
         int32_t cur = 0;
-        for (int q = b0; q < b1; ++q) {
-          TinyNode& t = g.tiny_nodes[q];
-          const int k2 = (int)(q - tg.beg);
-          (void)k2;
-          auto stage = [&](const Loc& l, int64_t n, int32_t& st, int32_t& cnt) {
-            st = -1;
-            cnt = 0;
-            if (l.kind == LOC_SMEM || n > kTinyStageMax) return;
-            st = cur;
-            cnt = (int32_t)n;
-            cur += (int32_t)((n + 1) & ~1);
-          };
-          const int v = tiny_slot[q];
-          stage(g.tiny_ga[q], size[p.kid_l(v)], t.sta, t.na);
-          stage(g.tiny_gb[q], size[p.kid_r(v)], t.stb, t.nb);
+        auto stage = [&](const Loc& l, int64_t n, int32_t& st, int32_t& cnt) {
+          st = -1;
+          cnt = 0;
+          if (l.kind == LOC_SMEM || n > kTinyStageMax) return;
+          st = cur;
+          cnt = (int32_t)n;
+          cur += (int32_t)((n + 1) & ~1);
+        };
+        for (int q2 = b0; q2 < b1; ++q2) {
+          TinyNode& t = out.nodes[q2];
+          const int v = slot[q2];
+          stage(out.ga[q2], size[p.kid_l(v)], t.sta, t.na);
+          stage(out.gb[q2], size[p.kid_r(v)], t.stb, t.nb);
         }
-        g.tiny_stage_doubles = std::max(g.tiny_stage_doubles, cur);
-        const TinyNode& l = g.tiny_nodes[b1 - 1];
-        g.tiny_dig_max = std::max(g.tiny_dig_max, l.dig + l.nc + l.ns - g.tiny_nodes[b0].dig);
+        out.stage = std::max(out.stage, cur);
+        const TinyNode& l = out.nodes[b1 - 1];
+        out.digmax = std::max(out.digmax, l.dig + l.nc + l.ns - out.nodes[b0].dig);
       }
-      g.tiny_groups.push_back(tg);
-      g.tiny_smem_doubles = std::max(g.tiny_smem_doubles, group_smem[gi]);
-      for (int v : nodes)
-        if (v == r) producer[v] = tiny_step[lv];
+      out.grp.push_back(tg);
     }
-    level_range[lv].second = (int32_t)g.tiny_groups.size();
+  };
+  {
+    // split the group order into ranges of about equal node counts
+    int64_t total = 0;
+    for (int gi : gorder) total += (int64_t)groups[gi].size();
+    const int T = (int)std::max<int64_t>(1, std::min<int64_t>(8, total / 2048));
+    std::vector<int> cut{0};
+    int64_t acc = 0;
+    for (size_t q = 0; q < gorder.size(); ++q) {
+      acc += (int64_t)groups[gorder[q]].size();
+      if ((int)cut.size() < T && acc * T >= total * (int64_t)cut.size()) cut.push_back((int)q + 1);
+    }
+    while ((int)cut.size() <= T) cut.push_back((int)gorder.size());
+    std::vector<TinyOut> outs(T);
+    std::vector<std::thread> th;
+    for (int w = 1; w < T; ++w) th.emplace_back(build_groups, cut[w], cut[w + 1], std::ref(outs[w]));
+    build_groups(cut[0], cut[1], outs[0]);
+    for (auto& x : th) x.join();
+    for (auto& o : outs) {
+      const int32_t nb = (int32_t)g.tiny_nodes.size(), db = (int32_t)g.tiny_digits.size();
+      for (auto& tn : o.nodes) {
+        tn.dig += db;
+        g.tiny_nodes.push_back(tn);
+      }
+      g.tiny_digits.insert(g.tiny_digits.end(), o.digs.begin(), o.digs.end());
+      g.tiny_ga.insert(g.tiny_ga.end(), o.ga.begin(), o.ga.end());
+      g.tiny_gb.insert(g.tiny_gb.end(), o.gb.begin(), o.gb.end());
+      g.tiny_gout.insert(g.tiny_gout.end(), o.go.begin(), o.go.end());
+      for (auto tg : o.grp) g.tiny_groups.push_back(TinyGroup{tg.beg + nb, tg.end + nb});
+      g.tiny_stage_doubles = std::max(g.tiny_stage_doubles, o.stage);
+      g.tiny_dig_max = std::max(g.tiny_dig_max, o.digmax);
+    }
+    g.n_tiny = (int)g.tiny_nodes.size();
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+      g.tiny_smem_doubles = std::max(g.tiny_smem_doubles, group_smem[gi]);
+      producer[groups[gi].back()] = tiny_step[glevel[gi]];
+    }
   }
   // forced roots consumed inside a tiny level: release with that level as reader
   for (size_t gi = 0; gi < groups.size(); ++gi)
