@@ -42,10 +42,10 @@ UNIT = "slices/s"
 # workload -> (description, greedy slice-prefix rule)
 GiB = 2 ** 30
 # Sliced configs use Algorithm 3 itself: the reference's greedy (exact port) at a
-# mem_budget.  The literal "2^8 / 2^12 slices" of BASELINE.json are restated in
-# on these FactorTree spine plans every greedy pick nearly doubles
-# total work (C4: 8 picks = 1406 s of roofline vs 6.8 s unsliced), and C3/C5 do not
-# reach one B200's HBM before 2^44 / >2^12 slices.
+# mem_budget (the reference's dense memory model decides the slice set).  The
+# literal "2^8 / 2^12 slices" of BASELINE.json are restated in DESIGN.md §5: on
+# these FactorTree spine plans every greedy pick nearly doubles total work, while
+# tie-aware execution fits C4 unsliced and C3 at two slices in one B200's HBM.
 CONFIGS = {
     "c1a": dict(desc="uniform random 3-CNF n=30 ratio 3.0 (restated C1), unsliced"),
     "c1b": dict(desc="uniform random 3-CNF n=40 ratio 3.0 (restated C1), max-rank 30, unsliced"),
@@ -54,8 +54,10 @@ CONFIGS = {
                    desc="C1b sliced by Algorithm 3 at mem_budget 3.5 GiB (greedy: 3 picks, 8 slices)"),
     "c4": dict(budget=100 * GiB,
                desc="banded random 3-CNF n=400 ratio 4.0 window 36 (C4) at mem_budget 100 GiB (2 picks, 4 slices)"),
-    "c3": dict(budget=100 * GiB, infeasible="reference greedy needs 44 picks (2^44 slices) to fit 100 GiB",
-               desc="grid Ising 30x30 (C3), 393 GiB unsliced"),
+    "c4_full": dict(plan="c4", desc="banded random 3-CNF n=400 ratio 4.0 window 36 (C4), unsliced "
+                                    "(192 GiB dense mem_cost; 18 GB of tied tensors on the device)"),
+    "c3": dict(budget=270 * GiB,
+               desc="grid Ising 30x30 (C3), 393 GiB unsliced, at mem_budget 270 GiB (1 pick, 2 slices)"),
     "c5": dict(budget=100 * GiB, infeasible="reference greedy plateaus at 3 TiB per slice after 12 picks",
                desc="banded random 3-CNF n=400 ratio 4.0 window 44 (C5), 12 TiB unsliced"),
 }
@@ -479,7 +481,11 @@ def run_ours(args):
         parity = dict(reference_count=golden["count"], rel_err=abs(count - golden["count"]) / abs(golden["count"]))
 
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    dense_gib = st["mem_estimate"] / GiB
+    if world == 1 and not args.no_cpu_baseline and dense_gib > 24:
+        cpu = dict(value=None, unit=UNIT, cores=host_cores(), kind="reference",
+                   sample=f"not run: the reference's dense working set per slice is {dense_gib:.0f} GiB")
+    elif world == 1 and not args.no_cpu_baseline:
         try:
             per_step, _, sample, ref_count, times = time_reference(flat, chosen, 1)
             cpu = dict(value=nsl / per_step, unit=UNIT, cores=host_cores(), kind="reference", sample=sample,

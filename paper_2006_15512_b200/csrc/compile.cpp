@@ -384,6 +384,47 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   // mem[s]: (logical index, variable) pairs sorted by logical index; a
   // variable is named by the smallest logical index of its block.
   bool ties = std::getenv("TC_NO_TIES") == nullptr;
+  // Tie-aware slicing: a sliced bond fixes every index tied to it (the dense
+  // leaves are zero unless the whole tie class agrees), so those indices are
+  // sliced too ("implied", same value, same place value in the slice id).
+  // pdrop is the physical slice set; the reference accounting keeps `drop`.
+  // Classes holding a free index or two sliced indices are left alone.
+  std::vector<char> pdrop = drop;
+  std::vector<int> implied_src(p.NI, -1);
+  if (ties && !chosen_in.empty()) {
+    std::vector<int> cu(p.NI);
+    for (int i = 0; i < p.NI; ++i) cu[i] = i;
+    auto cfind = [&](int x) {
+      while (cu[x] != x) x = cu[x] = cu[cu[x]];
+      return x;
+    };
+    const std::vector<char> none(p.NI, 0);
+    std::vector<int> lab2;
+    for (int l = 0; l < p.NL; ++l) {
+      if (!leaf_ties(p, l, none, lab2)) continue;
+      const auto& ro = p.ref_order[l];
+      for (size_t q = 0; q < ro.size(); ++q)
+        for (size_t q2 = q + 1; q2 < ro.size(); ++q2)
+          if (lab2[q] >= 0 && lab2[q] == lab2[q2]) {
+            const int x = cfind(ro[q]), y = cfind(ro[q2]);
+            if (x != y) cu[std::max(x, y)] = std::min(x, y);
+          }
+    }
+    std::vector<int> nsl(p.NI, 0), src(p.NI, -1);
+    std::vector<char> has_free(p.NI, 0);
+    for (int i = 0; i < p.NI; ++i) {
+      const int r = cfind(i);
+      if (drop[i]) nsl[r]++, src[r] = i;
+      if (!p.is_bond[i]) has_free[r] = 1;
+    }
+    for (int i = 0; i < p.NI; ++i) {
+      const int r = cfind(i);
+      if (!drop[i] && nsl[r] == 1 && !has_free[r] && p.dom[i] == p.dom[src[r]]) {
+        pdrop[i] = 1;
+        implied_src[i] = src[r];
+      }
+    }
+  }
   // Per-slot tables live in two pools (no per-node allocations): leaves at
   // fixed offsets, internal nodes appended in postorder (a recomputed node
   // appends again; capacity is reserved before each pass so spans stay valid).
@@ -439,7 +480,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     std::vector<int64_t> off(p.NL + 1, 0);
     for (int l = 0; l < p.NL; ++l) {
       int64_t k = 0;
-      for (int i : p.ref_order[l]) k += !drop[i];
+      for (int i : p.ref_order[l]) k += !pdrop[i];
       off[l + 1] = off[l] + k;
     }
     mpool.assign(off[p.NL], MPair{0, 0});
@@ -450,7 +491,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         const auto& ro = p.ref_order[l];
         MPair* m = mpool.data() + off[l];
         int n = 0;
-        leaf_tied[l] = ties && leaf_ties(p, l, drop, lab);
+        leaf_tied[l] = ties && leaf_ties(p, l, pdrop, lab);
         if (leaf_tied[l]) {
           int bmin[8];
           for (int q = 0; q < 8; ++q) bmin[q] = INT_MAX;
@@ -460,7 +501,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
             if (lab[q] >= 0) m[n++] = {ro[q], bmin[lab[q]]};
         } else {
           for (int i : ro)
-            if (!drop[i]) m[n++] = {i, i};
+            if (!pdrop[i]) m[n++] = {i, i};
         }
         std::sort(m, m + n);
         mbeg[l] = off[l];
@@ -676,7 +717,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     const auto& ro = p.ref_order[s];
     o.reserve(varsv(s).size());
     for (auto it = ro.rbegin(); it != ro.rend(); ++it) {
-      if (drop[*it]) continue;
+      if (pdrop[*it]) continue;
       const int var = var_of(s, *it);
       if (seen_mark[var] == s) continue;
       seen_mark[var] = s;
@@ -733,7 +774,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       const auto& ro = p.ref_order[l];
       o.reserve(varsv(l).size());
       for (auto it = ro.rbegin(); it != ro.rend(); ++it) {
-        if (drop[*it]) continue;
+        if (pdrop[*it]) continue;
         const int var = var_of(l, *it);
         if (std::find(o.begin(), o.end(), var) == o.end()) o.push_back(var);
       }
@@ -864,7 +905,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       const int d = (int)(rem % p.dom[Ll[t]]);
       rem /= p.dom[Ll[t]];
       for (size_t q = 0; q < ro.size(); ++q)
-        if (!drop[ro[q]] && var_of(l, ro[q]) == Ll[t]) src += d * stride[q];
+        if (!pdrop[ro[q]] && var_of(l, ro[q]) == Ll[t]) src += d * stride[q];
     }
     return src;
   };
@@ -872,7 +913,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   for (int l = 0; l < p.NL; ++l) {
     if (!leaf_tied[l]) continue;
     bool sl = false;
-    for (int i : p.ref_order[l]) sl |= (bool)drop[i];
+    for (int i : p.ref_order[l]) sl |= (bool)pdrop[i];
     if (sl) continue;  // sliced leaves are gathered per slice (k_select)
     auto stride = leaf_strides(l);
     cval_off[l] = (int64_t)g.cvals.size();
@@ -948,7 +989,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   for (int l = 0; l < p.NL; ++l) {
     const auto& ro = p.ref_order[l];
     bool sl = false;
-    for (int i : ro) sl |= (bool)drop[i];
+    for (int i : ro) sl |= (bool)pdrop[i];
     if (!sl) {
       // compressed leaves follow the raw values in the device leaf buffer
       g.loc[l] = cval_off[l] >= 0 ? Loc{LOC_LEAF, nraw + cval_off[l]} : Loc{LOC_LEAF, p.lval_off[l]};
@@ -958,8 +999,8 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     auto stride = leaf_strides(l);
     int32_t t0 = (int32_t)g.sel_terms.size();
     for (size_t q = 0; q < ro.size(); ++q)
-      if (drop[ro[q]]) {
-        int j = chosen_slot[ro[q]];
+      if (pdrop[ro[q]]) {
+        int j = chosen_slot[drop[ro[q]] ? ro[q] : implied_src[ro[q]]];
         g.sel_terms.push_back(SelTerm{pv[j], g.chosen_dim[j], stride[q]});
       }
     int32_t nt = (int32_t)g.sel_terms.size() - t0;
@@ -1638,7 +1679,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     const auto& Lr = g.layout[p.root];
     std::vector<int> kept;
     for (int i : ro)
-      if (!drop[i]) kept.push_back(i);
+      if (!pdrop[i]) kept.push_back(i);
     std::vector<int64_t> vstride(p.NI, 0);
     int64_t st2 = 1;
     for (int i : Lr) {

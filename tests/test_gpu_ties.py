@@ -165,3 +165,13 @@ def test_benchmark_plan_dense_path_agrees(name):
     assert abs(float(tv) - float(dv)) <= 1e-12 * abs(float(dv))
     st = _lib.PlanHandle(flat).compile_stats([])
     assert st["n_tied_leaves"] > 0 and st["phys_bytes"] < st["alg_bytes"]
+
+
+def test_c4_unsliced_fits_and_counts_zero():
+    """C4 (192 GiB dense mem_cost) runs unsliced on one B200 through the tied
+    tensors; the formula is UNSAT (z3), so the exact count is 0.0."""
+    flat, _ = planfile.load(os.path.join(os.path.dirname(__file__), "..", "data", "plans", "c4.tcplan.npz"))
+    n, t = planfile.to_objects(flat)
+    out, v = _run(n, t)
+    assert float(v) == 0.0
+    assert out.mem_estimate > 150 * 2 ** 30 and out.stats["device_peak_bytes"] < 40 * 2 ** 30

@@ -240,3 +240,25 @@ def test_tie_compression_stats_on_benchmark_plan():
     assert tied["phys_bytes"] * 10 < dense["phys_bytes"]
     assert tied["phys_flops"] * 100 < dense["phys_flops"]
     assert tied["device_peak_bytes"] * 10 < dense["device_peak_bytes"]
+
+
+def test_benchmark_formula_satisfiability():
+    """C4/C5 (banded 3-CNF, ratio 4.0) are UNSAT: their weighted count 0.0 is
+    exact; C2 and C3 are satisfiable."""
+    z3 = pytest.importorskip("z3")
+    from paper_2006_15512_b200.generators import config_dimacs
+
+    def sat(text):
+        s = z3.Solver()
+        xs = {}
+        for line in text.splitlines():
+            if not line or line[0] in "cpw":
+                continue
+            lits = [int(x) for x in line.split()[:-1]]
+            if lits:
+                s.add(z3.Or([xs.setdefault(abs(l), z3.Bool(f"x{abs(l)}")) if l > 0
+                             else z3.Not(xs.setdefault(abs(l), z3.Bool(f"x{abs(l)}"))) for l in lits]))
+        return s.check() == z3.sat
+
+    assert not sat(config_dimacs("c4")) and not sat(config_dimacs("c5"))
+    assert sat(config_dimacs("c2")) and sat(config_dimacs("c3"))
