@@ -144,6 +144,8 @@ static PyObject* flatten(PyObject* self, PyObject* args) {
   Buf dom = {0}, ioff = {0}, iarr = {0}, voff = {0}, vals = {0}, lft = {0}, rgt = {0};
   PtrMap leaf = {0}, ixp = {0};
   size_t pm_size = 0, pm_cap = 4096;
+  int32_t* occ = NULL;  // occurrences of each distinct Index object
+  size_t occ_cap = 0;
   if (!indices || !pos) goto done;
   if (pm_init(&leaf, (size_t)nl) < 0 || pm_init(&ixp, pm_cap) < 0) goto done;
 
@@ -161,65 +163,49 @@ static PyObject* flatten(PyObject* self, PyObject* args) {
     PyObject** iv = PySequence_Fast_ITEMS(fi);
     for (Py_ssize_t q = 0; q < r; ++q) {
       PyObject* ix = iv[q];
-      // the same Index object seen before: no attribute read, no id hashing
+      // identity by object first (a bond's two tensors usually share the Index
+      // object); equal-by-id distinct objects are merged after the loop
       int64_t known = pm_get(&ixp, (uintptr_t)ix, -1);
-      if (known >= 0) {
-        int32_t di = (int32_t)known;
-        if (buf_put(&iarr, &di, 4) < 0) {
-          Py_DECREF(fi);
-          goto done;
-        }
-        continue;
-      }
-      PyObject* key = PyObject_GetAttr(ix, s_id);
-      if (!key) {
-        Py_DECREF(fi);
-        goto done;
-      }
-      PyObject* d = PyDict_GetItemWithError(pos, key);
       int32_t di;
-      if (d) {
-        di = (int32_t)PyLong_AsLong(d);
+      if (known >= 0) {
+        di = (int32_t)known;
+        occ[di]++;
       } else {
-        if (PyErr_Occurred()) {
-          Py_DECREF(key);
-          Py_DECREF(fi);
-          goto done;
-        }
         di = (int32_t)PyList_GET_SIZE(indices);
-        PyObject* dv = PyLong_FromLong(di);
         PyObject* ds = PyObject_GetAttr(ix, s_domain_size);
         long dsz = ds ? PyLong_AsLong(ds) : -1;
         Py_XDECREF(ds);
         int32_t dsz32 = (int32_t)dsz;
-        if (!dv || dsz < 0 || PyDict_SetItem(pos, key, dv) < 0 || PyList_Append(indices, ix) < 0 ||
-            buf_put(&dom, &dsz32, 4) < 0) {
+        if (dsz < 0 || PyList_Append(indices, ix) < 0 || buf_put(&dom, &dsz32, 4) < 0) {
           if (!PyErr_Occurred()) PyErr_SetString(PyExc_ValueError, "bad index domain_size");
-          Py_XDECREF(dv);
-          Py_DECREF(key);
           Py_DECREF(fi);
           goto done;
         }
-        Py_DECREF(dv);
-      }
-      Py_DECREF(key);
-      // cache only first occurrences: `indices` owns them, so the pointer
-      // cannot be recycled during this call
-      if (di == (int32_t)PyList_GET_SIZE(indices) - 1 && PyList_GET_ITEM(indices, di) == ix) {
-      if (pm_size >= pm_cap) {  // grow the pointer cache (rehash)
-        PtrMap bigger;
-        if (pm_init(&bigger, 2 * pm_cap) < 0) {
-          Py_DECREF(fi);
-          goto done;
+        if (pm_size >= pm_cap) {  // grow the pointer map (rehash); `indices` owns the keys
+          PtrMap bigger;
+          if (pm_init(&bigger, 2 * pm_cap) < 0) {
+            Py_DECREF(fi);
+            goto done;
+          }
+          for (size_t h = 0; h <= ixp.mask; ++h)
+            if (ixp.key[h]) pm_set(&bigger, ixp.key[h], ixp.val[h]);
+          pm_free(&ixp);
+          ixp = bigger;
+          pm_cap *= 2;
         }
-        for (size_t h = 0; h <= ixp.mask; ++h)
-          if (ixp.key[h]) pm_set(&bigger, ixp.key[h], ixp.val[h]);
-        pm_free(&ixp);
-        ixp = bigger;
-        pm_cap *= 2;
-      }
-      pm_set(&ixp, (uintptr_t)ix, di);
-      pm_size++;
+        pm_set(&ixp, (uintptr_t)ix, di);
+        pm_size++;
+        if ((size_t)di >= occ_cap) {
+          occ_cap = occ_cap ? 2 * occ_cap : 4096;
+          int32_t* q2 = (int32_t*)PyMem_Realloc(occ, occ_cap * sizeof(int32_t));
+          if (!q2) {
+            PyErr_NoMemory();
+            Py_DECREF(fi);
+            goto done;
+          }
+          occ = q2;
+        }
+        occ[di] = 1;
       }
       if (buf_put(&iarr, &di, 4) < 0) {
         Py_DECREF(fi);
@@ -236,6 +222,83 @@ static PyObject* flatten(PyObject* self, PyObject* args) {
     if (nv < 0) goto done;
     voffv += nv;
     if (buf_put(&voff, &voffv, 8) < 0) goto done;
+  }
+
+  // Index identity is Index.id (tensor.py:29-33).  Objects seen twice are
+  // bonds already; the singly-seen ones (free indices, or a bond whose two
+  // tensors hold distinct but equal Index objects) are matched by id, and
+  // later duplicates are folded into the first, keeping first-appearance order.
+  {
+    const Py_ssize_t nu = PyList_GET_SIZE(indices);
+    int32_t* remap = (int32_t*)PyMem_Malloc((size_t)(nu ? nu : 1) * sizeof(int32_t));
+    if (!remap) {
+      PyErr_NoMemory();
+      goto done;
+    }
+    int merged = 0;
+    for (Py_ssize_t u = 0; u < nu; ++u) {
+      remap[u] = (int32_t)u;
+      if (occ[u] != 1) continue;
+      PyObject* key = PyObject_GetAttr(PyList_GET_ITEM(indices, u), s_id);
+      if (!key) {
+        PyMem_Free(remap);
+        goto done;
+      }
+      PyObject* d = PyDict_GetItemWithError(pos, key);
+      if (d) {
+        remap[u] = (int32_t)PyLong_AsLong(d);
+        merged = 1;
+      } else if (!PyErr_Occurred()) {
+        PyObject* dv = PyLong_FromSsize_t(u);
+        if (!dv || PyDict_SetItem(pos, key, dv) < 0) {
+          Py_XDECREF(dv);
+          Py_DECREF(key);
+          PyMem_Free(remap);
+          goto done;
+        }
+        Py_DECREF(dv);
+      }
+      Py_DECREF(key);
+      if (PyErr_Occurred()) {
+        PyMem_Free(remap);
+        goto done;
+      }
+    }
+    if (merged) {  // compact: dense ids in first-appearance order of each id
+      int32_t* dense = (int32_t*)PyMem_Malloc((size_t)nu * sizeof(int32_t));
+      PyObject* kept = PyList_New(0);
+      Buf dom2 = {0};
+      int32_t nxt = 0;
+      int ok = dense && kept;
+      for (Py_ssize_t u = 0; u < nu && ok; ++u) {
+        if (remap[u] == (int32_t)u) {
+          dense[u] = nxt++;
+          ok = PyList_Append(kept, PyList_GET_ITEM(indices, u)) == 0 &&
+               buf_put(&dom2, ((int32_t*)dom.p) + u, 4) == 0;
+        } else {
+          dense[u] = dense[remap[u]];
+        }
+      }
+      if (ok) {
+        int32_t* ia = (int32_t*)iarr.p;
+        for (size_t q = 0; q < iarr.n / 4; ++q) ia[q] = dense[ia[q]];
+        Py_DECREF(indices);
+        indices = kept;
+        kept = NULL;
+        PyMem_Free(dom.p);
+        dom = dom2;
+        dom2.p = NULL;
+      }
+      Py_XDECREF(kept);
+      PyMem_Free(dom2.p);
+      PyMem_Free(dense);
+      if (!ok) {
+        if (!PyErr_Occurred()) PyErr_NoMemory();
+        PyMem_Free(remap);
+        goto done;
+      }
+    }
+    PyMem_Free(remap);
   }
 
   // right-first preorder, reversed = left-first postorder (network.py:114-124).
@@ -336,6 +399,7 @@ static PyObject* flatten(PyObject* self, PyObject* args) {
 done:
   pm_free(&leaf);
   pm_free(&ixp);
+  PyMem_Free(occ);
   PyMem_Free(dom.p);
   PyMem_Free(ioff.p);
   PyMem_Free(iarr.p);

@@ -17,16 +17,7 @@ namespace tc {
 
 static void fail(int st, const std::string& m) { throw Error{st, m}; }
 
-static std::vector<int> sym_diff(const std::vector<int>& a, const std::vector<int>& b) {
-  std::vector<int> out;
-  out.reserve(a.size() + b.size());
-  std::set_symmetric_difference(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(out));
-  return out;
-}
-
-static bool contains(const std::vector<int>& s, int i) {
-  return std::binary_search(s.begin(), s.end(), i);
-}
+static bool contains(ISpan s, int i) { return std::binary_search(s.begin(), s.end(), i); }
 
 Plan build_plan(const tc_plan_desc& d) {
   Plan p;
@@ -52,14 +43,19 @@ Plan build_plan(const tc_plan_desc& d) {
   p.root = d.root_slot;
 
   const int S = p.nslots();
-  p.sets.resize(S);
-  p.ref_order.resize(S);
   p.occ0.assign(p.NI, -1);
   p.occ1.assign(p.NI, -1);
+  // leaves: sets and orders are the leaf index lists (sorted / as given)
+  p.sets.pool.reserve((size_t)p.lidx_off[p.NL] * 4 + 16);
+  p.ref_order.pool.reserve((size_t)p.lidx_off[p.NL] * 4 + 16);
+  p.sets.off.reserve(S + 1);
+  p.ref_order.off.reserve(S + 1);
   for (int l = 0; l < p.NL; ++l) {
-    std::vector<int> ids(p.lidx.begin() + p.lidx_off[l], p.lidx.begin() + p.lidx_off[l + 1]);
+    const int* ids = p.lidx.data() + p.lidx_off[l];
+    const int nid = (int)(p.lidx_off[l + 1] - p.lidx_off[l]);
     u128 size = 1;
-    for (int i : ids) {
+    for (int q = 0; q < nid; ++q) {
+      const int i = ids[q];
       if (i < 0 || i >= p.NI) fail(TC_BAD_ARG, "plan: leaf index id out of range");
       if (p.occ0[i] < 0) p.occ0[i] = l;
       else if (p.occ1[i] < 0) {
@@ -71,9 +67,12 @@ Plan build_plan(const tc_plan_desc& d) {
       size *= (u128)p.dom[i];
     }
     if (size != (u128)p.leaf_size(l)) fail(TC_BAD_ARG, "plan: leaf value count does not match its domains");
-    p.ref_order[l] = ids;
-    std::sort(ids.begin(), ids.end());
-    p.sets[l] = std::move(ids);
+    p.ref_order.pool.insert(p.ref_order.pool.end(), ids, ids + nid);
+    p.ref_order.close_slot();
+    const size_t s0 = p.sets.pool.size();
+    p.sets.pool.insert(p.sets.pool.end(), ids, ids + nid);
+    std::sort(p.sets.pool.begin() + s0, p.sets.pool.end());
+    p.sets.close_slot();
   }
   p.is_bond.assign(p.NI, 0);
   for (int i = 0; i < p.NI; ++i)
@@ -94,13 +93,21 @@ Plan build_plan(const tc_plan_desc& d) {
       p.parent[c] = me;
     }
     const int a = p.left[k], b = p.right[k];
-    p.sets[me] = sym_diff(p.sets[a], p.sets[b]);
-    auto& ro = p.ref_order[me];
-    ro.reserve(p.sets[me].size());
-    for (int i : p.ref_order[a])
-      if (!contains(p.sets[b], i)) ro.push_back(i);
-    for (int i : p.ref_order[b])
-      if (!contains(p.sets[a], i)) ro.push_back(i);
+    // the pools never reallocate while a span of them is read below
+    const ISpan A = p.sets[a], B = p.sets[b];
+    if (p.sets.pool.size() + A.size() + B.size() > p.sets.pool.capacity() ||
+        p.ref_order.pool.size() + A.size() + B.size() > p.ref_order.pool.capacity()) {
+      p.sets.pool.reserve(2 * p.sets.pool.capacity() + A.size() + B.size());
+      p.ref_order.pool.reserve(2 * p.ref_order.pool.capacity() + A.size() + B.size());
+    }
+    const ISpan A2 = p.sets[a], B2 = p.sets[b], RA = p.ref_order[a], RB = p.ref_order[b];
+    std::set_symmetric_difference(A2.begin(), A2.end(), B2.begin(), B2.end(), std::back_inserter(p.sets.pool));
+    p.sets.close_slot();
+    for (int i : RA)
+      if (!contains(B2, i)) p.ref_order.pool.push_back(i);
+    for (int i : RB)
+      if (!contains(A2, i)) p.ref_order.pool.push_back(i);
+    p.ref_order.close_slot();
   }
   int expect_root = p.NN > 0 ? p.NL + p.NN - 1 : 0;
   if (p.root != expect_root) fail(TC_PLAN_MISMATCH, "contraction tree root is not the last node");
@@ -138,7 +145,7 @@ static inline u128 add_chk(u128 a, u128 b) {
   return r;
 }
 
-u128 set_bytes(const Plan& p, const std::vector<int>& set, const std::vector<char>& drop) {
+u128 set_bytes(const Plan& p, ISpan set, const std::vector<char>& drop) {
   u128 out = 8;
   for (int i : set)
     if (!drop[i]) out = mul_chk(out, (u128)p.dom[i]);
@@ -343,8 +350,8 @@ u128 contraction_ops(const Plan& p) {
   std::vector<char> none(p.NI, 0);
   for (int k = 0; k < p.NN; ++k) {
     std::vector<int> uni;
-    const auto& a = p.sets[p.left[k]];
-    const auto& b = p.sets[p.right[k]];
+    const ISpan a = p.sets[p.left[k]];
+    const ISpan b = p.sets[p.right[k]];
     std::set_union(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(uni));
     total = add_chk(total, set_bytes(p, uni, none) / 8);
   }
@@ -353,7 +360,7 @@ u128 contraction_ops(const Plan& p) {
 
 int max_rank(const Plan& p) {
   size_t r = 0;
-  for (auto& s : p.sets) r = std::max(r, s.size());
+  for (int s = 0; s < p.nslots(); ++s) r = std::max(r, p.sets[s].size());
   return (int)r;
 }
 

@@ -2,6 +2,7 @@
 // the greedy slice chooser.  Host-only C++ (no CUDA).
 #pragma once
 #include <cstdint>
+#include <iterator>
 #include <string>
 #include <vector>
 
@@ -18,6 +19,28 @@ struct Error {
   std::string msg;
 };
 
+// Read-only view of a run of ints (a slot's index set / order in a pool).
+struct ISpan {
+  const int *b = nullptr, *e = nullptr;
+  const int* begin() const { return b; }
+  const int* end() const { return e; }
+  std::reverse_iterator<const int*> rbegin() const { return std::reverse_iterator<const int*>(e); }
+  std::reverse_iterator<const int*> rend() const { return std::reverse_iterator<const int*>(b); }
+  size_t size() const { return (size_t)(e - b); }
+  bool empty() const { return b == e; }
+  int operator[](size_t i) const { return b[i]; }
+};
+
+// Per-slot int lists stored back to back (slots are filled in order 0..S-1):
+// one allocation instead of one vector per slot.
+struct SlotPool {
+  std::vector<int> pool;
+  std::vector<int64_t> off{0};
+  ISpan operator[](int s) const { return ISpan{pool.data() + off[s], pool.data() + off[s + 1]}; }
+  size_t size() const { return off.size() - 1; }
+  void close_slot() { off.push_back((int64_t)pool.size()); }
+};
+
 // Reference-compatible symbolic view of (TensorNetwork, ContractionTree).
 struct Plan {
   int NI = 0, NL = 0, NN = 0, root = 0;
@@ -29,8 +52,8 @@ struct Plan {
 
   // derived
   std::vector<int> parent;                 // per slot, -1 for root
-  std::vector<std::vector<int>> sets;      // per slot: sorted index ids (node_index_sets)
-  std::vector<std::vector<int>> ref_order; // per slot: reference index order (tensor.py:108)
+  SlotPool sets;       // per slot: sorted index ids (node_index_sets)
+  SlotPool ref_order;  // per slot: reference index order (tensor.py:108)
   std::vector<int> occ0, occ1;             // leaves holding index i (-1 if none)
   std::vector<char> is_bond;
   std::vector<int> bonds_sorted;           // bond ids sorted by sort_rank
@@ -47,7 +70,10 @@ struct Plan {
 Plan build_plan(const tc_plan_desc& d);
 
 // 8 * prod(dom[i]) over set minus drop; throws TC_OVERFLOW.
-u128 set_bytes(const Plan& p, const std::vector<int>& set, const std::vector<char>& drop);
+u128 set_bytes(const Plan& p, ISpan set, const std::vector<char>& drop);
+inline u128 set_bytes(const Plan& p, const std::vector<int>& set, const std::vector<char>& drop) {
+  return set_bytes(p, ISpan{set.data(), set.data() + set.size()}, drop);
+}
 
 // slicing.py:52-67
 u128 mem_cost(const Plan& p, const std::vector<char>& drop);

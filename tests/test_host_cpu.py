@@ -262,3 +262,22 @@ def test_benchmark_formula_satisfiability():
 
     assert not sat(config_dimacs("c4")) and not sat(config_dimacs("c5"))
     assert sat(config_dimacs("c2")) and sat(config_dimacs("c3"))
+
+
+def test_native_flatten_merges_equal_ids_in_first_appearance_order():
+    from paper_2006_15512_b200 import Index, Tensor, TensorNetwork
+    from paper_2006_15512_b200.flatten import flatten_py
+    from paper_2006_15512_b200.network import join, leaf
+    i1, i2 = Index(("a", 1), 2), Index(("a", 1), 2)
+    j = Index("j", 3)
+    k1, k2 = Index("k", 2), Index("k", 2)
+    f = Index("free", 2)
+    a = Tensor((i1, j), np.arange(6.0))
+    b = Tensor((j, i2, k1), np.arange(12.0))
+    c = Tensor((k2, f), np.arange(4.0))
+    n = TensorNetwork((a, b, c))
+    t = join(join(leaf(a), leaf(b)), leaf(c))
+    x = flatten(n, t)
+    _flat_equal(x, flatten_py(n, t))
+    assert [q.id for q in x.indices] == [("a", 1), "j", "k", "free"]
+    assert x.leaf_idx.tolist() == [0, 1, 1, 0, 2, 2, 3]
