@@ -22,8 +22,17 @@
 
 namespace tc {
 
+// Programmatic dependent launch (PDL): a kernel lets its dependent launch as
+// soon as it starts (launch_dependents) and waits for its own predecessor's
+// completion and memory (wait) only after the parameter-only prologue.  Both
+// are no-ops for launches without the PDL attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // ---------------------------------------------------------------------------
 __global__ void k_select(const SelectParams p) {
+  pdl_launch();
+  pdl_wait();
   const int64_t eta = p.eta[0];
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p.n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -38,16 +47,23 @@ __global__ void k_select(const SelectParams p) {
 }
 
 __global__ void k_rootcopy(const RootCopyParams p) {
+  pdl_launch();
+  pdl_wait();
   const int64_t slot = p.eta[0] - p.eta[1];
+  double* results = *p.results;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p.R;
        r += (int64_t)gridDim.x * blockDim.x) {
     // tied root indices: dense entries off the diagonal are structural zeros
     const int64_t m = p.map ? p.map[r] : r;
-    p.results[slot * p.R + r] = m >= 0 ? p.src[m] : 0.0;
+    results[slot * p.R + r] = m >= 0 ? p.src[m] : 0.0;
   }
 }
 
-__global__ void k_eta(int64_t* eta) { eta[0] += 1; }
+__global__ void k_eta(int64_t* eta) {
+  pdl_launch();
+  pdl_wait();
+  eta[0] += 1;
+}
 __global__ void k_eta_reset(int64_t* eta) { eta[0] = eta[1]; }
 
 // L2 eviction between timed passes (benchmark only): stream a scratch buffer
@@ -81,6 +97,8 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
   double* stg = red + kTinyThreads;
   TinyNode* bn = (TinyNode*)(stg + stage_doubles);
   TinyDigit* bd = (TinyDigit*)(bn + kTinyBatch);
+  pdl_launch();
+  pdl_wait();
   const TinyGroup G = groups[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int b0 = G.beg; b0 < G.end; b0 += kTinyBatch) {
@@ -227,6 +245,8 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream(const StreamParams p)
     lo_p[u] = staged ? (int64_t)(tp + ((u & 1) ? p.bitP[8] : 0) + ((u & 2) ? p.bitP[9] : 0)) * SVFV
                      : tpo + ((u & 1) ? p.bitPo[8] : 0) + ((u & 2) ? p.bitPo[9] : 0);
   }
+  pdl_launch();
+  pdl_wait();  // the operands below are produced by earlier launches
   if (staged) {
     for (int q = tid; q < (SVFV << p.nbt); q += blockDim.x) {
       const int bi = q / SVFV;
@@ -412,6 +432,8 @@ __global__ void __launch_bounds__(32 * WGM * WGN, (WGM * WGN >= 8) ? 2 : 4)
   for (int i = 0; i < ELB; ++i)
     if (tid + i * NT < BN * GBK && !(bok_t && hb_ok[i]))
       for (int s = 0; s < Cfg::ST; ++s) Bs[s * GBK * LDB + bsx_t + hb_sx[i]] = 0.0;
+  pdl_launch();
+  pdl_wait();  // operands are produced by earlier launches
   const double* Ab = p.A + deposit(tm, p.a_m) + deposit(bt, p.a_bt);
   const double* Bb = p.B + deposit(tn, p.b_n) + deposit(bt, p.b_bt);
 
@@ -517,6 +539,8 @@ __global__ void __launch_bounds__(32 * WGM * WGN, (WGM * WGN >= 8) ? 2 : 4)
 
 // fixed-order split-K reduction: C = ((W0 + W1) + W2) + ...
 __global__ void k_splitk_reduce(const GemmParams p, int64_t tiles, int tile_elems) {
+  pdl_launch();
+  pdl_wait();
   const int64_t total = tiles * tile_elems;
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
        id += (int64_t)gridDim.x * blockDim.x) {
@@ -542,6 +566,8 @@ __global__ void k_splitk_reduce(const GemmParams p, int64_t tiles, int tile_elem
 
 // ---------------------------------------------------------------------------
 __global__ void k_generic(const GenericParams p) {
+  pdl_launch();
+  pdl_wait();
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < p.c_size;
        c += (int64_t)gridDim.x * blockDim.x) {
     int64_t oa = 0, ob = 0, r = c;

@@ -172,7 +172,7 @@ struct SelectParams {
 
 struct RootCopyParams {
   const double* src;
-  double* results;
+  double* const* results;  // device slot holding the [n][R] results buffer (re-pointed by the runtime)
   const int64_t* map;  // dense entry -> physical offset or -1 (nullptr: identity)
   int64_t R;
   const int64_t* eta;  // [0] = current slice, [1] = first slice of the run

@@ -251,6 +251,7 @@ struct tc_exec {
   TinyGroup* tgroups = nullptr;
   GDigit* gdig = nullptr;
   int64_t* rootmap = nullptr;
+  double** results_slot = nullptr;  // device copy of `results` read by k_rootcopy
   SelEntry* sel = nullptr;
   SelTerm* selt = nullptr;
   int64_t* eta = nullptr;
@@ -269,7 +270,7 @@ struct tc_exec {
     if (graph) cudaGraphDestroy(graph);
     if (stream) cudaStreamSynchronize(stream);
     for (void* q : {(void*)arena, (void*)leafbuf, (void*)slicedbuf, (void*)tnodes, (void*)tdigs,
-                    (void*)tgroups, (void*)gdig, (void*)rootmap, (void*)sel, (void*)selt, (void*)eta, (void*)results,
+                    (void*)tgroups, (void*)gdig, (void*)rootmap, (void*)results_slot, (void*)sel, (void*)selt, (void*)eta, (void*)results,
                     (void*)folded})
       dcache().put(device, q);
     if (stream) cudaStreamDestroy(stream);
@@ -337,6 +338,7 @@ struct tc_exec {
       CU(cudaMemcpyAsync(gdig, g.gdigits.data(), g.gdigits.size() * sizeof(GDigit), cudaMemcpyHostToDevice, stream));
     }
     eta = dalloc<int64_t>(2, dev_bytes, device);
+    results_slot = dalloc<double*>(1, dev_bytes, device);
     folded = dalloc<double>((size_t)g.R, dev_bytes, device);
     CU(cudaStreamSynchronize(stream));
 
@@ -440,7 +442,7 @@ struct tc_exec {
           break;
         }
         case ST_ROOTCOPY: {
-          RootCopyParams rp{ptr(g.root_loc), nullptr, rootmap, g.R, eta};
+          RootCopyParams rp{ptr(g.root_loc), results_slot, rootmap, g.R, eta};
           L.func = (void*)k_rootcopy;
           L.grid = dim3(grid_for(g.R, 256, device));
           L.arg(rp);
@@ -463,14 +465,26 @@ struct tc_exec {
     kernels_per_slice = (int64_t)launches.size();
   }
 
-  // The CUDA graph (one kernel node per step, edges = data + WAR deps) is
-  // built on the first run that replays the program more than twice; one-shot
-  // calls launch the steps eagerly on the stream (graph build + instantiate of
-  // ~900 nodes costs ~13 ms, more than the launches it saves).
+  // The CUDA graph is built on the first run that replays the program more
+  // than twice; one-shot calls launch the steps eagerly on the stream (with
+  // PDL: each kernel's launch and prologue overlap its predecessor's tail).
+  // The graph is the explicit DAG (data + WAR edges).  TC_PDL_GRAPH=1 captures
+  // the eager PDL chain instead -- measured: no gain on C2, 38% slower on C4
+  // (early-launched dependents hold SM slots; the chain drops concurrency).
   void ensure_graph() {
     if (gexec) return;
     Program& g = prog;
     auto t_graph0 = std::chrono::steady_clock::now();
+    kernels_per_slice = (int64_t)launches.size();
+    static const bool pdl_graph = std::getenv("TC_PDL_GRAPH") && std::atoi(std::getenv("TC_PDL_GRAPH")) == 1;
+    if (use_pdl() && pdl_graph) {
+      CU(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      launch_eager();
+      CU(cudaStreamEndCapture(stream, &graph));
+      CU(cudaGraphInstantiate(&gexec, graph, 0));
+      graph_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_graph0).count();
+      return;
+    }
     CU(cudaGraphCreate(&graph, 0));
     std::vector<cudaGraphNode_t> nodes(g.steps.size());
     kernels_per_slice = 0;
@@ -481,14 +495,19 @@ struct tc_exec {
       CU(cudaGraphAddKernelNode(&nodes[si], graph, deps.data(), deps.size(), &kp));
       ++kernels_per_slice;
     }
-    rootcopy_node = nodes[rootcopy_launch];
     CU(cudaGraphInstantiate(&gexec, graph, 0));
     graph_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_graph0).count();
   }
   double program_ms = 0, setup_ms = 0, graph_ms = 0;
 
-  cudaGraphNode_t rootcopy_node = nullptr;
   int rootcopy_launch = -1;
+  static bool use_pdl() {
+    static const bool on = [] {
+      const char* e = std::getenv("TC_PDL");
+      return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+  }
 
   void ensure_results(int64_t n) {
     if (n <= results_cap) return;
@@ -497,23 +516,31 @@ struct tc_exec {
     int64_t dummy = 0;
     results = dalloc<double>((size_t)(n * prog.R), dummy, device);
     results_cap = n;
-    // patch the root-copy node with the new results pointer
-    Launch& L = launches[rootcopy_launch];
-    RootCopyParams rp;
-    std::memcpy(&rp, L.blob.data(), sizeof(rp));
-    rp.results = results;
-    std::memcpy(L.blob.data(), &rp, sizeof(rp));
-    if (gexec) {
-      cudaKernelNodeParams kp = L.params();
-      CU(cudaGraphExecKernelNodeSetParams(gexec, rootcopy_node, &kp));
-    }
+    // k_rootcopy reads the buffer through results_slot: graphs stay valid
+    CU(cudaMemcpyAsync(results_slot, &results, sizeof(double*), cudaMemcpyHostToDevice, stream));
+    CU(cudaStreamSynchronize(stream));
   }
 
   // one slice in step order on the stream (no graph)
   void launch_eager() {
-    for (auto& L : launches) {
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    for (size_t i = 0; i < launches.size(); ++i) {
+      Launch& L = launches[i];
       auto kp = L.params();
-      CU(cudaLaunchKernel(L.func, L.grid, L.block, kp.kernelParams, L.smem, stream));
+      if (use_pdl() && i > 0) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = L.grid;
+        cfg.blockDim = L.block;
+        cfg.dynamicSmemBytes = L.smem;
+        cfg.stream = stream;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CU(cudaLaunchKernelExC(&cfg, L.func, kp.kernelParams));
+      } else {
+        CU(cudaLaunchKernel(L.func, L.grid, L.block, kp.kernelParams, L.smem, stream));
+      }
     }
   }
 
