@@ -878,6 +878,8 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         want(b, Lb);
         break;
       }
+      case NC_TINY:
+        break;  // tiny subtrees use natural layouts, built with their descriptors
       default:
         if (!p.is_leaf(a)) want(a, natural(a));
         if (!p.is_leaf(b)) want(b, natural(b));
@@ -1183,6 +1185,21 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   auto build_groups = [&](int q0, int q1, TinyOut& out) {
     std::vector<int64_t> sa_(p.NI, 0), sb_(p.NI, 0);
     std::vector<const Comp*> cc(p.NI, nullptr);
+    // layout of a slot: materialised (leaves, group roots under big parents)
+    // or the natural order, computed here for nodes inside tiny subtrees
+    std::vector<int> nat[3];
+    auto lay = [&](int sl, int which) -> const std::vector<int>& {
+      if (!g.layout[sl].empty() || varsv(sl).size() == 0) return g.layout[sl];
+      auto& o = nat[which];
+      o.clear();
+      const auto ro = p.ref_order[sl];
+      for (auto it = ro.rbegin(); it != ro.rend(); ++it) {
+        if (pdrop[*it]) continue;
+        const int var = var_of(sl, *it);
+        if (std::find(o.begin(), o.end(), var) == o.end()) o.push_back(var);
+      }
+      return o;
+    };
     auto strides2 = [&](const Comp* c, int64_t& sa, int64_t& sb) {
       sa = sb = 0;
       for (int t = 0; t < c->na; ++t) sa += sa_[c->a[t]];
@@ -1212,9 +1229,9 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         if (v == r) lo = g.loc[r];
         else tn.sout = soff[v];
         // digits: output variables in C's layout order, then the summed ones
-        const auto& La = g.layout[a];
-        const auto& Lb = g.layout[b];
-        const auto& Lc = g.layout[v];
+        const auto& La = lay(a, 0);
+        const auto& Lb = lay(b, 1);
+        const auto& Lc = lay(v, 2);
         int64_t st2 = 1;
         for (int i : La) sa_[i] = st2, st2 *= p.dom[i];
         st2 = 1;
