@@ -16,11 +16,15 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cooperative_groups.h>
+
 #include <cstdint>
 
 #include "program.h"
 
 namespace tc {
+
+namespace cg = cooperative_groups;
 
 // Programmatic dependent launch (PDL): a kernel lets its dependent launch as
 // soon as it starts (launch_dependents) and waits for its own predecessor's
@@ -215,14 +219,21 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
 constexpr int kStreamThreads = 256;
 constexpr int kStreamUnroll = 4;
 
+// One stream step executed by CTA `b` of 2^logG CTAs (a standalone launch or
+// one step of k_stream_seq).  The 2^cl chunks split into 2^g CTA blocks of
+// 2^kchunk chunks each; CTAs beyond the chunk count idle.
 template <int NS, int NF>
-__global__ void __launch_bounds__(kStreamThreads) k_stream(const StreamParams p) {
+__device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, int b, int logG) {
   constexpr int SV = 1 << NS, FV = 1 << NF, SVFV = SV * FV;
   constexpr int CB = kStreamChunkBits;
   static_assert((kStreamThreads * kStreamUnroll) == (1 << CB), "chunk");
   static_assert(kStreamThreads == 256 && kStreamUnroll == 4, "x = base + u*256 + tid");
-  __shared__ double Ps[kStreamStageMax];  // staged small operand (stage_all)
   const int tid = threadIdx.x;
+  const int xb = 63 - __clzll((long long)p.nx);  // nx is a power of two
+  const int cl = max(0, xb - CB);
+  const int g = min(logG, cl);
+  if (b >= (1 << g)) return;
+  const int kchunk = cl - g;
   const bool staged = p.stage_all;
   // x = chunk * 2^CB + u * 256 + tid.  Every address is a sum of per-bit
   // table entries: the thread's low parts once, the CTA's chunk bits once,
@@ -245,8 +256,6 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream(const StreamParams p)
     lo_p[u] = staged ? (int64_t)(tp + ((u & 1) ? p.bitP[8] : 0) + ((u & 2) ? p.bitP[9] : 0)) * SVFV
                      : tpo + ((u & 1) ? p.bitPo[8] : 0) + ((u & 2) ? p.bitPo[9] : 0);
   }
-  pdl_launch();
-  pdl_wait();  // the operands below are produced by earlier launches
   if (staged) {
     for (int q = tid; q < (SVFV << p.nbt); q += blockDim.x) {
       const int bi = q / SVFV;
@@ -260,7 +269,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream(const StreamParams p)
   // this CTA's fixed chunk bits
   int64_t ha = 0, hc = 0, hp = 0;
   {
-    uint64_t m = (uint64_t)blockIdx.x << (p.kchunk + CB);
+    uint64_t m = (uint64_t)b << (kchunk + CB);
     while (m) {
       const int j = __ffsll((long long)m) - 1;
       m &= m - 1;
@@ -271,7 +280,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream(const StreamParams p)
   }
   const double* Pbase = staged ? Ps : p.P;
   auto pv = [&](const double* Pu, int q) { return staged ? Pu[q] : __ldg(Pu + p.offP[q]); };
-  const int64_t nsteps = (int64_t)1 << p.kchunk;
+  const int64_t nsteps = (int64_t)1 << kchunk;
   for (int64_t i = 0; i < nsteps; ++i) {
     if (i > 0) {  // Gray code: chunk bit ctz(i) flips
       const int j = __ffsll((long long)i) - 1 + CB;
@@ -312,6 +321,45 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream(const StreamParams p)
         }
       }
     }
+  }
+}
+
+template <int NS, int NF>
+__global__ void __launch_bounds__(kStreamThreads) k_stream(const StreamParams p) {
+  __shared__ double Ps[kStreamStageMax];  // staged small operand (stage_all)
+  pdl_launch();
+  pdl_wait();  // operands are produced by earlier launches
+  stream_run<NS, NF>(p, Ps, blockIdx.x, 31 - __clz(gridDim.x));
+}
+
+// A run of consecutive stream steps in ONE cooperative launch: all CTAs take
+// each step in turn, a grid barrier between steps (the launch gap and ramp of
+// a separate kernel cost more than the barrier for the small steps of tied
+// programs).  Step shapes are limited so the kernel's registers stay at two
+// CTAs per SM.
+constexpr int kSeqMaxNS = 2, kSeqMaxNF = 3;
+__global__ void __launch_bounds__(kStreamThreads, 2)
+    k_stream_seq(const StreamParams* __restrict__ steps, const int* __restrict__ keys, int n, int logG) {
+  __shared__ StreamParams sp;
+  __shared__ double Ps[kStreamStageMax];
+  cg::grid_group grid = cg::this_grid();
+  for (int i = 0; i < n; ++i) {
+    {
+      const uint32_t* src = (const uint32_t*)(steps + i);
+      uint32_t* dst = (uint32_t*)&sp;
+      for (int w = threadIdx.x; w < (int)(sizeof(StreamParams) / 4); w += blockDim.x) dst[w] = src[w];
+    }
+    __syncthreads();
+    switch (keys[i]) {
+#define SQ(a, b) \
+  case a * 8 + b: stream_run<a, b>(sp, Ps, blockIdx.x, logG); break;
+      SQ(0, 0) SQ(0, 1) SQ(0, 2) SQ(0, 3)
+      SQ(1, 0) SQ(1, 1) SQ(1, 2) SQ(1, 3)
+      SQ(2, 0) SQ(2, 1) SQ(2, 2) SQ(2, 3)
+#undef SQ
+      default: break;
+    }
+    grid.sync();
   }
 }
 

@@ -75,7 +75,6 @@ struct StreamParams {
   // over disjoint bits, so any address is a sum of table entries.
   int64_t bitA[kStreamXBits], bitC[kStreamXBits], bitPo[kStreamXBits];
   int32_t bitP[kStreamXBits];
-  int32_t kchunk;  // each CTA walks 2^kchunk chunks (Gray-code order)
   int32_t stage_all;  // 1: the small operand ((SV*FV) << nbt <= kStreamStageMax entries) is staged
                       //    in smem once per CTA; 0: it is read through the L1 (direct)
 };

@@ -213,6 +213,7 @@ struct Launch {
   dim3 grid, block;
   unsigned smem = 0;
   int kind = 0, slot = -1;
+  bool coop = false;  // cooperative launch (k_stream_seq: grid barriers)
   double bytes = 0, flops = 0;
   std::vector<char> blob;
   std::vector<size_t> off;
@@ -252,6 +253,9 @@ struct tc_exec {
   GDigit* gdig = nullptr;
   int64_t* rootmap = nullptr;
   double** results_slot = nullptr;  // device copy of `results` read by k_rootcopy
+  StreamParams* seq_params = nullptr;  // k_stream_seq step descriptors
+  int* seq_keys = nullptr;
+  std::vector<std::vector<int>> ldeps;  // per launch: launches it depends on
   SelEntry* sel = nullptr;
   SelTerm* selt = nullptr;
   int64_t* eta = nullptr;
@@ -270,7 +274,7 @@ struct tc_exec {
     if (graph) cudaGraphDestroy(graph);
     if (stream) cudaStreamSynchronize(stream);
     for (void* q : {(void*)arena, (void*)leafbuf, (void*)slicedbuf, (void*)tnodes, (void*)tdigs,
-                    (void*)tgroups, (void*)gdig, (void*)rootmap, (void*)results_slot, (void*)sel, (void*)selt, (void*)eta, (void*)results,
+                    (void*)tgroups, (void*)gdig, (void*)rootmap, (void*)results_slot, (void*)seq_params, (void*)seq_keys, (void*)sel, (void*)selt, (void*)eta, (void*)results,
                     (void*)folded})
       dcache().put(device, q);
     if (stream) cudaStreamDestroy(stream);
@@ -396,7 +400,6 @@ struct tc_exec {
             const int chunks_log = std::max(0, xb - kStreamChunkBits);
             int g = 0;
             while (g < chunks_log && (2 << g) <= sm_count(device) * 4) ++g;
-            sp.kchunk = chunks_log - g;
             L.grid = dim3(1u << g);
           }
           L.arg(sp);
@@ -459,10 +462,123 @@ struct tc_exec {
       }
       launches.push_back(std::move(L));
     }
+    group_stream_runs();
     auto t_end = std::chrono::steady_clock::now();
     setup_ms = std::chrono::duration<double, std::milli>(t_end - t_prog).count();
     compile_ms = std::chrono::duration<double, std::milli>(t_end - t0).count();
     kernels_per_slice = (int64_t)launches.size();
+  }
+
+  // TC_SEQ=1: runs of >= 2 consecutive stream steps with small shapes become
+  // one cooperative k_stream_seq launch.  Measured slower (C2 1.56 vs 1.28 ms,
+  // C4 87 vs 70 ms): a step's cost is its DRAM/L2 ramp, not the launch, and the
+  // barrier kernel runs at half the occupancy.  Default: one launch per step.
+  // ldeps[i] = launches launch i depends on (data + WAR edges of its steps).
+  void group_stream_runs() {
+    Program& g = prog;
+    const size_t S = g.steps.size();
+    static const bool on = std::getenv("TC_SEQ") && std::atoi(std::getenv("TC_SEQ")) == 1;
+    auto eligible = [&](size_t i) {
+      const Step& st = g.steps[i];
+      return on && st.kind == ST_STREAM && st.ns <= kSeqMaxNS && st.nf <= kSeqMaxNF;
+    };
+    std::vector<std::pair<size_t, size_t>> runs;  // [first, end)
+    for (size_t i = 0; i < S;) {
+      size_t j = i;
+      while (j < S && eligible(j)) ++j;
+      if (j - i >= 2) runs.push_back({i, j});
+      i = (j == i) ? i + 1 : j;
+    }
+    std::vector<int> lid(S, -1);
+    if (runs.empty()) {
+      ldeps.assign(S, {});
+      for (size_t i = 0; i < S; ++i) ldeps[i] = g.steps[i].deps;
+      return;
+    }
+    int nb = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_stream_seq, kStreamThreads, 0));
+    const int64_t co = (int64_t)std::max(1, nb) * sm_count(device);
+    int logG = 0;
+    while ((int64_t)2 << logG <= co) ++logG;
+    size_t total = 0;
+    for (auto& r : runs) total += r.second - r.first;
+    std::vector<StreamParams> sp(total);
+    std::vector<int> keys(total);
+    int64_t dummy = 0;
+    seq_params = dalloc<StreamParams>(total, dev_bytes, device);
+    seq_keys = dalloc<int>(total, dummy, device);
+    std::vector<Launch> out;
+    std::vector<std::vector<int>> odeps;
+    size_t next_run = 0, pos = 0;
+    for (size_t i = 0; i < S;) {
+      if (next_run < runs.size() && runs[next_run].first == i) {
+        const auto r = runs[next_run++];
+        Launch L;
+        L.kind = ST_STREAM;
+        L.slot = g.steps[r.second - 1].slot;
+        L.coop = true;
+        L.func = (void*)k_stream_seq;
+        L.grid = dim3(1u << logG);
+        L.block = dim3(kStreamThreads);
+        const size_t p0 = pos;
+        std::vector<int> dd;
+        for (size_t k = r.first; k < r.second; ++k) {
+          std::memcpy(&sp[pos], launches[k].blob.data() + launches[k].off[0], sizeof(StreamParams));
+          keys[pos] = g.steps[k].ns * 8 + g.steps[k].nf;
+          ++pos;
+          L.bytes += launches[k].bytes;
+          L.flops += launches[k].flops;
+          for (int d : g.steps[k].deps)
+            if ((size_t)d < r.first) dd.push_back(lid[d]);
+          lid[k] = (int)out.size();
+        }
+        L.arg((const StreamParams*)(seq_params + p0));
+        L.arg((const int*)(seq_keys + p0));
+        L.arg((int)(r.second - r.first));
+        L.arg(logG);
+        std::sort(dd.begin(), dd.end());
+        dd.erase(std::unique(dd.begin(), dd.end()), dd.end());
+        out.push_back(std::move(L));
+        odeps.push_back(dd);
+        i = r.second;
+      } else {
+        std::vector<int> dd;
+        for (int d : g.steps[i].deps) dd.push_back(lid[d]);
+        std::sort(dd.begin(), dd.end());
+        dd.erase(std::unique(dd.begin(), dd.end()), dd.end());
+        lid[i] = (int)out.size();
+        if ((int)i == rootcopy_launch) rootcopy_launch = (int)out.size();
+        out.push_back(std::move(launches[i]));
+        odeps.push_back(dd);
+        ++i;
+      }
+    }
+    CU(cudaMemcpyAsync(seq_params, sp.data(), total * sizeof(StreamParams), cudaMemcpyHostToDevice, stream));
+    CU(cudaMemcpyAsync(seq_keys, keys.data(), total * sizeof(int), cudaMemcpyHostToDevice, stream));
+    CU(cudaStreamSynchronize(stream));
+    launches = std::move(out);
+    ldeps = std::move(odeps);
+  }
+
+  void launch_one(Launch& L, bool pdl) {
+    auto kp = L.params();
+    if (L.coop) {
+      CU(cudaLaunchCooperativeKernel(L.func, L.grid, L.block, kp.kernelParams, L.smem, stream));
+    } else if (pdl) {
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = L.grid;
+      cfg.blockDim = L.block;
+      cfg.dynamicSmemBytes = L.smem;
+      cfg.stream = stream;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CU(cudaLaunchKernelExC(&cfg, L.func, kp.kernelParams));
+    } else {
+      CU(cudaLaunchKernel(L.func, L.grid, L.block, kp.kernelParams, L.smem, stream));
+    }
   }
 
   // The CUDA graph is built on the first run that replays the program more
@@ -473,7 +589,6 @@ struct tc_exec {
   // (early-launched dependents hold SM slots; the chain drops concurrency).
   void ensure_graph() {
     if (gexec) return;
-    Program& g = prog;
     auto t_graph0 = std::chrono::steady_clock::now();
     kernels_per_slice = (int64_t)launches.size();
     static const bool pdl_graph = std::getenv("TC_PDL_GRAPH") && std::atoi(std::getenv("TC_PDL_GRAPH")) == 1;
@@ -486,13 +601,18 @@ struct tc_exec {
       return;
     }
     CU(cudaGraphCreate(&graph, 0));
-    std::vector<cudaGraphNode_t> nodes(g.steps.size());
+    std::vector<cudaGraphNode_t> nodes(launches.size());
     kernels_per_slice = 0;
-    for (size_t si = 0; si < g.steps.size(); ++si) {
+    for (size_t si = 0; si < launches.size(); ++si) {
       std::vector<cudaGraphNode_t> deps;
-      for (int d : g.steps[si].deps) deps.push_back(nodes[d]);
+      for (int d : ldeps[si]) deps.push_back(nodes[d]);
       cudaKernelNodeParams kp = launches[si].params();
       CU(cudaGraphAddKernelNode(&nodes[si], graph, deps.data(), deps.size(), &kp));
+      if (launches[si].coop) {
+        cudaLaunchAttributeValue v{};
+        v.cooperative = 1;
+        CU(cudaGraphKernelNodeSetAttribute(nodes[si], cudaLaunchAttributeCooperative, &v));
+      }
       ++kernels_per_slice;
     }
     CU(cudaGraphInstantiate(&gexec, graph, 0));
@@ -523,25 +643,7 @@ struct tc_exec {
 
   // one slice in step order on the stream (no graph)
   void launch_eager() {
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    for (size_t i = 0; i < launches.size(); ++i) {
-      Launch& L = launches[i];
-      auto kp = L.params();
-      if (use_pdl() && i > 0) {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = L.grid;
-        cfg.blockDim = L.block;
-        cfg.dynamicSmemBytes = L.smem;
-        cfg.stream = stream;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        CU(cudaLaunchKernelExC(&cfg, L.func, kp.kernelParams));
-      } else {
-        CU(cudaLaunchKernel(L.func, L.grid, L.block, kp.kernelParams, L.smem, stream));
-      }
-    }
+    for (size_t i = 0; i < launches.size(); ++i) launch_one(launches[i], use_pdl() && i > 0);
   }
 
   // Eager replay of one slice, one kernel at a time, timed per launch with
@@ -555,9 +657,7 @@ struct tc_exec {
     for (auto& e : ev) CU(cudaEventCreate(&e));
     CU(cudaEventRecord(ev[0], stream));
     for (size_t i = 0; i < launches.size(); ++i) {
-      Launch& L = launches[i];
-      auto kp = L.params();
-      CU(cudaLaunchKernel(L.func, L.grid, L.block, kp.kernelParams, L.smem, stream));
+      launch_one(launches[i], false);
       CU(cudaEventRecord(ev[i + 1], stream));
     }
     CU(cudaEventSynchronize(ev.back()));
@@ -925,11 +1025,11 @@ int tc_exec_profile(tc_exec* ex, int64_t slice, float* step_ms, int32_t* step_ki
 
 int tc_exec_deps(const tc_exec* ex, int32_t* dep_off, int32_t* deps, int32_t cap, int32_t* n, int32_t* m) {
   return guard([&] {
-    const auto& st = ex->prog.steps;
+    const auto& st = ex->ldeps;  // per launch (stream runs are one launch)
     int32_t e = 0;
     for (size_t i = 0; i < st.size(); ++i) {
       if (dep_off && (int32_t)i <= cap) dep_off[i] = e;
-      for (int d : st[i].deps) {
+      for (int d : st[i]) {
         if (deps && e < cap) deps[e] = d;
         ++e;
       }
