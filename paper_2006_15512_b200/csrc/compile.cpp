@@ -43,6 +43,7 @@
 #include <cstdlib>
 #include <future>
 #include <map>
+#include <memory>
 #include <set>
 #include <string>
 #include <thread>
@@ -443,24 +444,31 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     size_t size() const { return (size_t)(e - b); }
     int operator[](size_t i) const { return b[i]; }
   };
-  std::vector<MPair> mpool;
-  std::vector<int> vpool;
-  std::vector<int64_t> mbeg(S), mend(S), vbeg(S), vend(S);
-  auto mem = [&](int s) { return MemSpan{mpool.data() + mbeg[s], mpool.data() + mend[s]}; };
-  auto varsv = [&](int s) { return IntSpan{vpool.data() + vbeg[s], vpool.data() + vend[s]}; };
-  int64_t logical_total = 0;
-  for (int s = 0; s < S; ++s) logical_total += (int64_t)p.sets[s].size();
-  std::vector<Comp> cpool;
-  std::vector<int32_t> coff(p.NN + 1, 0);
-  std::vector<int> uf(p.NI, -1), own_a(p.NI, -1), own_b(p.NI, -1), cidx(p.NI, -1);
-  std::vector<char> leaf_tied(p.NL, 0);
-  auto find = [&](int x) {
-    while (uf[x] != x) {
-      uf[x] = uf[uf[x]];
-      x = uf[x];
-    }
-    return x;
+  // Slot tables are spans into arenas whose vectors are reserved up front and
+  // never reallocated: the leaf arena, one arena per worker of the parallel
+  // first pass, one per push-down round.
+  struct Arena {
+    std::vector<MPair> m;
+    std::vector<int> v;
+    std::vector<Comp> c;
   };
+  std::vector<std::unique_ptr<Arena>> arenas;
+  auto new_arena = [&](size_t nm, size_t nv, size_t nc) {
+    arenas.emplace_back(new Arena);
+    Arena& a = *arenas.back();
+    a.m.reserve(nm + 1);
+    a.v.reserve(nv + 1);
+    a.c.reserve(nc + 1);
+    return &a;
+  };
+  std::vector<const MPair*> mB(S, nullptr), mE(S, nullptr);
+  std::vector<const int*> vB(S, nullptr), vE(S, nullptr);
+  std::vector<const Comp*> cB(p.NN, nullptr), cE(p.NN, nullptr);
+  auto mem = [&](int s) { return MemSpan{mB[s], mE[s]}; };
+  auto varsv = [&](int s) { return IntSpan{vB[s], vE[s]}; };
+  std::vector<MPair> mpool;  // leaves
+  std::vector<int> vpool;
+  std::vector<char> leaf_tied(p.NL, 0);
   // Tie push-down: when a contraction reads two variables of an internal
   // operand as one (a diagonal read: a copy-tensor piece ties two indices the
   // operand keeps separately), the operand's off-diagonal entries are
@@ -504,13 +512,13 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
             if (!pdrop[i]) m[n++] = {i, i};
         }
         std::sort(m, m + n);
-        mbeg[l] = off[l];
-        mend[l] = off[l] + n;
+        mB[l] = m;
+        mE[l] = m + n;
         int* vv = vpool.data() + off[l];
         for (int q = 0; q < n; ++q) vv[q] = m[q].second;
         std::sort(vv, vv + n);
-        vbeg[l] = off[l];
-        vend[l] = off[l] + (std::unique(vv, vv + n) - vv);
+        vB[l] = vv;
+        vE[l] = vv + (std::unique(vv, vv + n) - vv);
       }
     });
   };
@@ -546,102 +554,196 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     }
   }
   tmark("phys: node passes");
-  // push-down rounds recompute only the nodes on paths from new requests up
-  std::vector<char> dirty(S, 1);
-  std::vector<Comp> cpool_prev;
-  std::vector<int32_t> coff_prev;
-  for (int attempt = 0;; ++attempt) {
-    bool overflow = false;
-    cpool_prev.swap(cpool);
-    coff_prev = coff;
-    cpool.clear();
+  // One node of the bottom-up pass: union-find over the operands' variables
+  // (shared logical indices, realised push-down requests) -> components, the
+  // node's (logical, variable) table and sorted variables, into arena `ar`.
+  struct Scratch {
+    std::vector<int> uf, own_a, own_b, cidx;
     std::vector<Comp> cs;
-    // room for every node's tables: spans into the pools stay valid below
-    mpool.reserve(mpool.size() + (size_t)logical_total + 16);
-    vpool.reserve(vpool.size() + (size_t)logical_total + 16);
-    for (int k = 0; k < p.NN && !overflow; ++k) {
-      const int v = p.NL + k, a = p.left[k], b = p.right[k];
-      coff[k] = (int32_t)cpool.size();
-      dirty[v] = dirty[v] || dirty[a] || dirty[b];
-      if (!dirty[v]) {  // unchanged since the last round
-        cpool.insert(cpool.end(), cpool_prev.begin() + coff_prev[k], cpool_prev.begin() + coff_prev[k + 1]);
-        continue;
+  };
+  auto make_scratch = [&]() {
+    Scratch sc;
+    sc.uf.assign(p.NI, -1);
+    sc.own_a.assign(p.NI, -1);
+    sc.own_b.assign(p.NI, -1);
+    sc.cidx.assign(p.NI, -1);
+    return sc;
+  };
+  auto process_node = [&](int k, Scratch& sc, Arena& ar, bool& overflow) {
+    const int v = p.NL + k, a = p.left[k], b = p.right[k];
+    auto& uf = sc.uf;
+    auto& own_a = sc.own_a;
+    auto& own_b = sc.own_b;
+    auto& cidx = sc.cidx;
+    auto& cs = sc.cs;
+    auto find = [&](int x) {
+      while (uf[x] != x) {
+        uf[x] = uf[uf[x]];
+        x = uf[x];
       }
-      const MemSpan Ma = mem(a), Mb = mem(b);
-      const IntSpan Va = varsv(a), Vb = varsv(b);
-      for (auto& e : Ma) own_a[e.first] = e.second;
-      for (auto& e : Mb) own_b[e.first] = e.second;
-      for (int x : Va) uf[x] = x;
-      for (int x : Vb) uf[x] = x;
-      for (auto& e : Mb)
-        if (own_a[e.first] >= 0) {
-          int r1 = find(own_a[e.first]), r2 = find(e.second);
-          if (r1 != r2) uf[std::max(r1, r2)] = std::min(r1, r2);
-        }
-      for (auto& q : req[k]) {  // pushed-down ties realised here
-        const int x = own_a[q.first] >= 0 ? own_a[q.first] : own_b[q.first];
-        const int y = own_a[q.second] >= 0 ? own_a[q.second] : own_b[q.second];
-        if (x < 0 || y < 0) continue;
-        int r1 = find(x), r2 = find(y);
+      return x;
+    };
+    const MemSpan Ma = mem(a), Mb = mem(b);
+    const IntSpan Va = varsv(a), Vb = varsv(b);
+    for (auto& e : Ma) own_a[e.first] = e.second;
+    for (auto& e : Mb) own_b[e.first] = e.second;
+    for (int x : Va) uf[x] = x;
+    for (int x : Vb) uf[x] = x;
+    for (auto& e : Mb)
+      if (own_a[e.first] >= 0) {
+        int r1 = find(own_a[e.first]), r2 = find(e.second);
         if (r1 != r2) uf[std::max(r1, r2)] = std::min(r1, r2);
       }
-      cs.clear();
-      auto comp_of = [&](int var) -> Comp& {
-        int r = find(var);
-        if (cidx[r] < 0) {
-          cidx[r] = (int)cs.size();
-          Comp c{};
-          c.c = -1;
-          cs.push_back(c);
-        }
-        return cs[cidx[r]];
-      };
-      for (int x : Va) {
-        Comp& c = comp_of(x);
-        if (c.na == kMaxTie) overflow = true;
-        else c.a[c.na++] = x;
-      }
-      for (int x : Vb) {
-        Comp& c = comp_of(x);
-        if (c.nb == kMaxTie) overflow = true;
-        else c.b[c.nb++] = x;
-      }
-      // kept logical indices -> component's C variable (smallest kept index)
-      const int64_t m0 = (int64_t)mpool.size();
-      {
-        size_t x = 0, y = 0;
-        for (;;) {  // merge the kept entries of both (each sorted by logical index)
-          while (x < Ma.size() && own_b[Ma[x].first] >= 0) ++x;
-          while (y < Mb.size() && own_a[Mb[y].first] >= 0) ++y;
-          if (x == Ma.size() && y == Mb.size()) break;
-          if (y == Mb.size() || (x < Ma.size() && Ma[x].first < Mb[y].first)) mpool.push_back(Ma[x++]);
-          else mpool.push_back(Mb[y++]);
-        }
-      }
-      for (int64_t q = m0; q < (int64_t)mpool.size(); ++q) {
-        Comp& c = comp_of(mpool[q].second);
-        if (c.c < 0) c.c = mpool[q].first;  // sorted: first kept = smallest
-      }
-      for (int64_t q = m0; q < (int64_t)mpool.size(); ++q) mpool[q].second = comp_of(mpool[q].second).c;
-      mbeg[v] = m0;
-      mend[v] = (int64_t)mpool.size();
-      const int64_t v0 = (int64_t)vpool.size();
-      for (const Comp& c : cs)
-        if (c.c >= 0) vpool.push_back(c.c);
-      std::sort(vpool.begin() + v0, vpool.end());
-      vbeg[v] = v0;
-      vend[v] = (int64_t)vpool.size();
-      // reset scratch (before reordering cs: cidx indexes into it)
-      for (int x : Va) cidx[find(x)] = -1;
-      for (int x : Vb) cidx[find(x)] = -1;
-      for (int x : Va) uf[x] = -1;
-      for (int x : Vb) uf[x] = -1;
-      for (auto& e : Ma) own_a[e.first] = -1;
-      for (auto& e : Mb) own_b[e.first] = -1;
-      std::sort(cs.begin(), cs.end(), [](const Comp& x, const Comp& y) { return x.key() < y.key(); });
-      cpool.insert(cpool.end(), cs.begin(), cs.end());
+    for (auto& q : req[k]) {  // pushed-down ties realised here
+      const int x = own_a[q.first] >= 0 ? own_a[q.first] : own_b[q.first];
+      const int y = own_a[q.second] >= 0 ? own_a[q.second] : own_b[q.second];
+      if (x < 0 || y < 0) continue;
+      int r1 = find(x), r2 = find(y);
+      if (r1 != r2) uf[std::max(r1, r2)] = std::min(r1, r2);
     }
-    coff[p.NN] = (int32_t)cpool.size();
+    cs.clear();
+    auto comp_of = [&](int var) -> Comp& {
+      int r = find(var);
+      if (cidx[r] < 0) {
+        cidx[r] = (int)cs.size();
+        Comp c{};
+        c.c = -1;
+        cs.push_back(c);
+      }
+      return cs[cidx[r]];
+    };
+    for (int x : Va) {
+      Comp& c = comp_of(x);
+      if (c.na == kMaxTie) overflow = true;
+      else c.a[c.na++] = x;
+    }
+    for (int x : Vb) {
+      Comp& c = comp_of(x);
+      if (c.nb == kMaxTie) overflow = true;
+      else c.b[c.nb++] = x;
+    }
+    // kept logical indices -> component's C variable (smallest kept index)
+    const size_t m0 = ar.m.size();
+    {
+      size_t x = 0, y = 0;
+      for (;;) {  // merge the kept entries of both (each sorted by logical index)
+        while (x < Ma.size() && own_b[Ma[x].first] >= 0) ++x;
+        while (y < Mb.size() && own_a[Mb[y].first] >= 0) ++y;
+        if (x == Ma.size() && y == Mb.size()) break;
+        if (y == Mb.size() || (x < Ma.size() && Ma[x].first < Mb[y].first)) ar.m.push_back(Ma[x++]);
+        else ar.m.push_back(Mb[y++]);
+      }
+    }
+    for (size_t q = m0; q < ar.m.size(); ++q) {
+      Comp& c = comp_of(ar.m[q].second);
+      if (c.c < 0) c.c = ar.m[q].first;  // sorted: first kept = smallest
+    }
+    for (size_t q = m0; q < ar.m.size(); ++q) ar.m[q].second = comp_of(ar.m[q].second).c;
+    mB[v] = ar.m.data() + m0;
+    mE[v] = ar.m.data() + ar.m.size();
+    const size_t v0 = ar.v.size();
+    for (const Comp& c : cs)
+      if (c.c >= 0) ar.v.push_back(c.c);
+    std::sort(ar.v.begin() + v0, ar.v.end());
+    vB[v] = ar.v.data() + v0;
+    vE[v] = ar.v.data() + ar.v.size();
+    // reset scratch (before reordering cs: cidx indexes into it)
+    for (int x : Va) cidx[find(x)] = -1;
+    for (int x : Vb) cidx[find(x)] = -1;
+    for (int x : Va) uf[x] = -1;
+    for (int x : Vb) uf[x] = -1;
+    for (auto& e : Ma) own_a[e.first] = -1;
+    for (auto& e : Mb) own_b[e.first] = -1;
+    std::sort(cs.begin(), cs.end(), [](const Comp& x, const Comp& y) { return x.key() < y.key(); });
+    const size_t c0 = ar.c.size();
+    ar.c.insert(ar.c.end(), cs.begin(), cs.end());
+    cB[k] = ar.c.data() + c0;
+    cE[k] = ar.c.data() + ar.c.size();
+  };
+  // arena sizes for a set of nodes (upper bounds: kept entries <= |set|)
+  auto bounds = [&](int k, size_t& nm, size_t& nc) {
+    const int v = p.NL + k;
+    nm += p.sets[v].size();
+    nc += p.sets[p.left[k]].size() + p.sets[p.right[k]].size();
+  };
+  // subtree sizes (internal nodes): a subtree's internal slots are the
+  // contiguous postorder range (v - cnt[v], v]
+  std::vector<int> cnt(S, 0);
+  for (int k = 0; k < p.NN; ++k) {
+    const int v = p.NL + k;
+    cnt[v] = 1 + cnt[p.left[k]] + cnt[p.right[k]];
+  }
+  Scratch main_sc = make_scratch();
+  // push-down rounds recompute only the nodes on paths from new requests up
+  std::vector<char> dirty(S, 0);
+  for (int attempt = 0;; ++attempt) {
+    bool overflow = false;
+    if (attempt == 0 || std::all_of(dirty.begin(), dirty.end(), [](char x) { return x != 0; })) {
+      // full pass: maximal subtrees of <= L nodes on worker threads, the
+      // rest (the spine above them) in postorder on this thread
+      const int L = std::max(256, p.NN / 64);
+      std::vector<int> task_roots;
+      for (int k = 0; k < p.NN; ++k) {
+        const int v = p.NL + k;
+        if (cnt[v] <= L && (p.parent[v] < 0 || cnt[p.parent[v]] > L)) task_roots.push_back(v);
+      }
+      std::vector<char> in_task(p.NN, 0);
+      int64_t task_nodes = 0;
+      for (int r : task_roots) {
+        for (int k = r - p.NL - cnt[r] + 1; k <= r - p.NL; ++k) in_task[k] = 1;
+        task_nodes += cnt[r];
+      }
+      const int T = (int)std::max<int64_t>(1, std::min<int64_t>(8, task_nodes / 1024));
+      std::vector<int> cut{0};
+      {
+        int64_t acc = 0;
+        for (size_t q = 0; q < task_roots.size(); ++q) {
+          acc += cnt[task_roots[q]];
+          if ((int)cut.size() < T && acc * T >= task_nodes * (int64_t)cut.size()) cut.push_back((int)q + 1);
+        }
+        while ((int)cut.size() <= T) cut.push_back((int)task_roots.size());
+      }
+      std::vector<Arena*> war(T);
+      for (int w = 0; w < T; ++w) {
+        size_t nm = 0, nc = 0;
+        for (int q = cut[w]; q < cut[w + 1]; ++q)
+          for (int k = task_roots[q] - p.NL - cnt[task_roots[q]] + 1; k <= task_roots[q] - p.NL; ++k) bounds(k, nm, nc);
+        war[w] = new_arena(nm, nm, nc);
+      }
+      std::vector<char> wover(T, 0);
+      auto work = [&](int w) {
+        Scratch sc = w == 0 ? std::move(main_sc) : make_scratch();
+        bool ov = false;
+        for (int q = cut[w]; q < cut[w + 1]; ++q)
+          for (int k = task_roots[q] - p.NL - cnt[task_roots[q]] + 1; k <= task_roots[q] - p.NL; ++k)
+            process_node(k, sc, *war[w], ov);
+        wover[w] = ov;
+        if (w == 0) main_sc = std::move(sc);
+      };
+      std::vector<std::thread> th;
+      for (int w = 1; w < T; ++w) th.emplace_back(work, w);
+      work(0);
+      for (auto& x : th) x.join();
+      for (int w = 0; w < T; ++w) overflow |= (bool)wover[w];
+      size_t nm = 0, nc = 0;
+      for (int k = 0; k < p.NN; ++k)
+        if (!in_task[k]) bounds(k, nm, nc);
+      Arena* top = new_arena(nm, nm, nc);
+      for (int k = 0; k < p.NN && !overflow; ++k)
+        if (!in_task[k]) process_node(k, main_sc, *top, overflow);
+    } else {
+      // a push-down round: the requested nodes and everything above them
+      for (int k = 0; k < p.NN; ++k) {
+        const int v = p.NL + k;
+        dirty[v] = dirty[v] || dirty[p.left[k]] || dirty[p.right[k]];
+      }
+      size_t nm = 0, nc = 0;
+      for (int k = 0; k < p.NN; ++k)
+        if (dirty[p.NL + k]) bounds(k, nm, nc);
+      Arena* ar = new_arena(nm, nm, nc);
+      for (int k = 0; k < p.NN && !overflow; ++k)
+        if (dirty[p.NL + k]) process_node(k, main_sc, *ar, overflow);
+    }
     tmark("phys: requests");
     if (!overflow) {
       bool pushed = false;
@@ -649,8 +751,8 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       if (ties && pushdown_rounds < 8) {
         for (int k = 0; k < p.NN; ++k) {
           const int ch[2] = {p.left[k], p.right[k]};
-          for (int32_t q = coff[k]; q < coff[k + 1]; ++q) {
-            const Comp& c = cpool[q];
+          for (const Comp* cp = cB[k]; cp != cE[k]; ++cp) {
+            const Comp& c = *cp;
             for (int side = 0; side < 2; ++side) {
               const int n = side ? c.nb : c.na;
               const int32_t* vv = side ? c.b : c.a;
@@ -688,16 +790,13 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     ties = false;  // pathological tie structure: fall back to dense variables
     for (auto& r : req) r.clear();
     build_leaves();
-    std::fill(dirty.begin(), dirty.end(), 1);
+    std::fill(dirty.begin(), dirty.end(), 1);  // all dirty: the next attempt is a full pass
   }
   struct EffView {
-    const std::vector<int>* pool;
-    const std::vector<int64_t>*b, *e;
-    IntSpan operator[](int s) const { return IntSpan{pool->data() + (*b)[s], pool->data() + (*e)[s]}; }
-  } eff{&vpool, &vbeg, &vend};
-  auto comps = [&](int v) {
-    return std::make_pair((const Comp*)cpool.data() + coff[v - p.NL], (const Comp*)cpool.data() + coff[v - p.NL + 1]);
-  };
+    const std::vector<const int*>*b, *e;
+    IntSpan operator[](int s) const { return IntSpan{(*b)[s], (*e)[s]}; }
+  } eff{&vB, &vE};
+  auto comps = [&](int v) { return std::make_pair(cB[v - p.NL], cE[v - p.NL]); };
   std::vector<int64_t> size(S);
   for (int s = 0; s < S; ++s) {
     u128 z = 1;
@@ -1306,7 +1405,8 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     // split the group order into ranges of about equal node counts
     int64_t total = 0;
     for (int gi : gorder) total += (int64_t)groups[gi].size();
-    const int T = (int)std::max<int64_t>(1, std::min<int64_t>(8, total / 2048));
+    static const int tmax = std::getenv("TC_TINY_THREADS") ? std::atoi(std::getenv("TC_TINY_THREADS")) : 2;
+    const int T = (int)std::max<int64_t>(1, std::min<int64_t>(tmax, total / 2048));
     std::vector<int> cut{0};
     int64_t acc = 0;
     for (size_t q = 0; q < gorder.size(); ++q) {
