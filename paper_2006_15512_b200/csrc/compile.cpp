@@ -1368,6 +1368,10 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         tn.c_size = (int32_t)size[v];
         tn.s_size = (int32_t)ssz;
         tn.pow2 = p2 ? 1 : 0;
+        // lanes per output: fill the CTA's 256 threads, at most a warp, at
+        // most the number of summed terms
+        tn.lw = 0;
+        while (tn.lw < 5 && (tn.c_size << (tn.lw + 1)) <= 256 && (1 << (tn.lw + 1)) <= ssz) ++tn.lw;
         out.nodes.push_back(tn);
         slot.push_back(v);
         out.ga.push_back(la);

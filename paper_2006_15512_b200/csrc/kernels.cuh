@@ -89,6 +89,7 @@ __global__ void k_fold(const double* results, int64_t R, int64_t n, double* out)
 // ---------------------------------------------------------------------------
 // K4: one CTA walks one tiny subtree in postorder; intermediates live in smem.
 constexpr int kTinyThreads = 256;
+constexpr int kTinyMaxSum = 16;  // summed dim-2 digits with precomputed deltas
 
 // smem: [intermediates: smem_doubles][reduce: kTinyThreads][staged operands:
 // stage_doubles][kTinyBatch TinyNode][dig_max TinyDigit]
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
   double* stg = red + kTinyThreads;
   TinyNode* bn = (TinyNode*)(stg + stage_doubles);
   TinyDigit* bd = (TinyDigit*)(bn + kTinyBatch);
+  __shared__ int dA[kTinyBatch][kTinyMaxSum], dB[kTinyBatch][kTinyMaxSum];
   pdl_launch();
   pdl_wait();
   const TinyGroup G = groups[blockIdx.x];
@@ -126,6 +128,21 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
       const int n = (o & 1) ? t.nb : t.na;
       for (int e = lane; e < n; e += 32) stg[st + e] = g[e];
     }
+    // dim-2 nodes: 2^lw lanes split each output's sum; lane r takes the
+    // terms whose low lw summed bits equal r.  Stepping the high bits q ->
+    // q+1 flips q's low ones to 0 and bit t = ctz(~q) to 1, so the operand
+    // offsets move by stride_{lw+t} - sum_{i<t} stride_{lw+i}.
+    if (tid < cnt && bn[tid].pow2) {
+      const TinyNode& t = bn[tid];
+      const TinyDigit* S = bd + (t.dig - dig0) + t.nc;
+      int pa = 0, pb = 0;
+      for (int j = t.lw; j < t.ns && j - t.lw < kTinyMaxSum; ++j) {
+        dA[tid][j - t.lw] = S[j].sa - pa;
+        dB[tid][j - t.lw] = S[j].sb - pb;
+        pa += S[j].sa;
+        pb += S[j].sb;
+      }
+    }
     __syncthreads();
     for (int i = 0; i < cnt; ++i) {
       const TinyNode& tn = bn[i];
@@ -135,7 +152,33 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
       double* C = tn.gout ? tn.gout : sm + tn.sout;
       const int nc = tn.nc, ns = tn.ns;
       const TinyDigit* sdS = sd + nc;
-      if (tn.c_size * 4 >= (int)blockDim.x || tn.s_size < 64) {
+      if (tn.pow2 && ns - tn.lw <= kTinyMaxSum) {
+        const int lw = tn.lw, W = 1 << lw;
+        const int r = lane & (W - 1);
+        const unsigned mask = (W == 32 ? 0xffffffffu : ((1u << W) - 1u) << (lane & ~(W - 1)));
+        int ra = 0, rb = 0;
+        for (int j = 0; j < lw; ++j)
+          if ((r >> j) & 1) ra += sdS[j].sa, rb += sdS[j].sb;
+        const int nq = tn.s_size >> lw;
+        for (int c = tid >> lw; c < tn.c_size; c += (int)blockDim.x >> lw) {
+          int xa = ra, xb = rb;
+          for (int j = 0; j < nc; ++j)
+            if ((c >> j) & 1) xa += sd[j].sa, xb += sd[j].sb;
+          double acc0 = 0.0, acc1 = 0.0;
+          for (int q = 0; q < nq; ++q) {
+            if (q) {
+              const int t = __ffs(~(q - 1)) - 1;
+              xa += dA[i][t];
+              xb += dB[i][t];
+            }
+            if (q & 1) acc1 = fma(A[xa], B[xb], acc1);
+            else acc0 = fma(A[xa], B[xb], acc0);
+          }
+          double acc = acc0 + acc1;
+          for (int o = W >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(mask, acc, o);
+          if (r == 0) C[c] = acc;
+        }
+      } else if (tn.c_size * 4 >= (int)blockDim.x || tn.s_size < 64) {
         for (int c = tid; c < tn.c_size; c += blockDim.x) {
           int oa = 0, ob = 0;
           if (tn.pow2) {

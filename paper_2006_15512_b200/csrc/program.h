@@ -123,7 +123,7 @@ struct TinyNode {
   int32_t pow2;  // all digits have dim 2
   int32_t sta, stb;  // staging offsets of small global operands within the batch (-1: read global)
   int32_t na, nb;    // entry counts of the staged operands
-  int32_t pad;
+  int32_t lw;        // dim-2 nodes: 2^lw lanes share one output's sum (<= 32)
 };
 // k_tiny processes a group in batches of kTinyBatch nodes: descriptors,
 // digits and small global operands (leaves) of a batch are copied to smem
