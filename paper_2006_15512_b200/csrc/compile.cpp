@@ -41,6 +41,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <deque>
 #include <future>
 #include <map>
 #include <memory>
@@ -1286,12 +1287,24 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     std::vector<const Comp*> cc(p.NI, nullptr);
     // layout of a slot: materialised (leaves, group roots under big parents)
     // or the natural order, computed here for nodes inside tiny subtrees
-    std::vector<int> nat[3];
-    auto lay = [&](int sl, int which) -> const std::vector<int>& {
+    // computed layouts are cached for the group (a node's layout as output is
+    // reused when its parent reads it as an operand)
+    std::deque<std::vector<int>> natc;  // stable references across growth
+    std::vector<int> nat_of(S, -1);
+    std::vector<int> nat_used;
+    auto lay = [&](int sl, int) -> const std::vector<int>& {
       if (!g.layout[sl].empty() || varsv(sl).size() == 0) return g.layout[sl];
-      auto& o = nat[which];
+      if (nat_of[sl] >= 0) return natc[nat_of[sl]];
+      nat_of[sl] = (int)nat_used.size();
+      nat_used.push_back(sl);
+      if (natc.size() < nat_used.size()) natc.emplace_back();
+      auto& o = natc[nat_of[sl]];
       o.clear();
       const auto ro = p.ref_order[sl];
+      if (varsv(sl).size() == ro.size()) {  // untied, nothing sliced: variables are the indices
+        for (auto it = ro.rbegin(); it != ro.rend(); ++it) o.push_back(*it);
+        return o;
+      }
       for (auto it = ro.rbegin(); it != ro.rend(); ++it) {
         if (pdrop[*it]) continue;
         const int var = var_of(sl, *it);
@@ -1379,6 +1392,8 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         out.go.push_back(lo);
       }
       tg.end = (int32_t)out.nodes.size();
+      for (int x : nat_used) nat_of[x] = -1;
+      nat_used.clear();
       // batches of kTinyBatch nodes: staging offsets of small global operands
       // (leaves, sliced leaves, small forced roots) and the digit block size
       for (int b0 = tg.beg; b0 < tg.end; b0 += kTinyBatch) {
