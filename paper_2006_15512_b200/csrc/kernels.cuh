@@ -370,9 +370,9 @@ __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, in
 template <int NS, int NF>
 __global__ void __launch_bounds__(kStreamThreads) k_stream(const StreamParams p) {
   __shared__ double Ps[kStreamStageMax];  // staged small operand (stage_all)
-  pdl_launch();
   pdl_wait();  // operands are produced by earlier launches
   stream_run<NS, NF>(p, Ps, blockIdx.x, 31 - __clz(gridDim.x));
+  pdl_launch();  // dependents start as this CTA retires (overlap the tail only)
 }
 
 // A run of consecutive stream steps in ONE cooperative launch: all CTAs take
@@ -523,7 +523,6 @@ __global__ void __launch_bounds__(32 * WGM * WGN, (WGM * WGN >= 8) ? 2 : 4)
   for (int i = 0; i < ELB; ++i)
     if (tid + i * NT < BN * GBK && !(bok_t && hb_ok[i]))
       for (int s = 0; s < Cfg::ST; ++s) Bs[s * GBK * LDB + bsx_t + hb_sx[i]] = 0.0;
-  pdl_launch();
   pdl_wait();  // operands are produced by earlier launches
   const double* Ab = p.A + deposit(tm, p.a_m) + deposit(bt, p.a_bt);
   const double* Bb = p.B + deposit(tn, p.b_n) + deposit(bt, p.b_bt);
@@ -581,6 +580,7 @@ __global__ void __launch_bounds__(32 * WGM * WGN, (WGM * WGN >= 8) ? 2 : 4)
     }
   }
   cp_async_wait<0>();
+  pdl_launch();  // main loop done: dependents may start their prologue
   __syncthreads();
   double* Cs = gsm;
 #pragma unroll
