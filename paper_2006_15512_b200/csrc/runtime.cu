@@ -631,6 +631,10 @@ struct tc_exec {
 
   void ensure_results(int64_t n) {
     if (n <= results_cap) return;
+    int64_t bytes = 0;
+    if (__builtin_mul_overflow(n, prog.R, &bytes) || __builtin_mul_overflow(bytes, (int64_t)8, &bytes) ||
+        bytes > ((int64_t)1 << 40))
+      throw Error{TC_OOM, "per-slice results of " + std::to_string(n) + " slices exceed device memory"};
     if (results) dcache().put(device, results);
     results = nullptr;
     int64_t dummy = 0;

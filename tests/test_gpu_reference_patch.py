@@ -86,3 +86,49 @@ def test_determinism_through_driver(patched):
     a = tc.count_text(EXAMPLE4, alpha=0.0, seed=3)
     b = tc.count_text(EXAMPLE4, alpha=0.0, seed=3)
     assert a.count == b.count and a.plan_text == b.plan_text  # test_acceptance.py:357-372
+
+
+def test_random_suite_sliced_vs_brute_force(patched):
+    """Real FactorTree networks (tied copy pieces) under budgets that make the
+    greedy slice 1-6 bonds, often inside tie classes (implied slices)."""
+    tc = patched
+    from tensorcount import driver
+    from tensorcount.formula import CnfFormula, WeightFunction, brute_force_count
+
+    from paper_2006_15512_b200 import _lib
+    from paper_2006_15512_b200.flatten import flatten
+
+    plans = []
+    real = driver.sliced_execute
+
+    def capture(n, t, mem_budget=None):  # the planned network of this formula
+        plans.append((n, t))
+        return real(n, t, mem_budget=mem_budget)
+
+    rng = random.Random(777)
+    sliced = 0
+    for k in range(60):
+        nv, nc = rng.randint(6, 14), rng.randint(8, 40)
+        clauses = []
+        for _ in range(nc):
+            vs = rng.sample(range(1, nv + 1), 3)
+            clauses.append(tuple(v if rng.random() < 0.5 else -v for v in vs))
+        f = CnfFormula(nv, tuple(clauses))
+        w = WeightFunction({v: (rng.uniform(0, 1), rng.uniform(0, 1)) for v in range(1, nv + 1)})
+        driver.sliced_execute = capture
+        try:
+            tc.count_formula(f, w, alpha=0.0, seed=k)
+        finally:
+            driver.sliced_execute = real
+        n, t = plans[-1]
+        h = _lib.PlanHandle(flatten(n, t))
+        picks = []
+        for _ in range(min(6, h.info().num_bonds)):
+            picks.append(h.choose_slice_index(picks))
+            budget = h.mem_cost(picks)
+            out = tc.count_formula(f, w, alpha=0.0, seed=k, mem_budget=budget)
+            sliced += out.num_slices > 1
+            assert out.count == pytest.approx(brute_force_count(f, w), rel=1e-9, abs=1e-12), (k, len(picks))
+            if len(picks) >= 1 + k % 4:
+                break
+    assert sliced > 60

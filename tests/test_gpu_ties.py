@@ -175,3 +175,13 @@ def test_c4_unsliced_fits_and_counts_zero():
     out, v = _run(n, t)
     assert float(v) == 0.0
     assert out.mem_estimate > 150 * 2 ** 30 and out.stats["device_peak_bytes"] < 40 * 2 ** 30
+
+
+def test_absurd_slice_counts_raise_instead_of_crashing():
+    """2^62 slices: the per-slice result buffer cannot exist; the call must
+    fail with MemoryError (TC_OOM), not crash or hang."""
+    flat, _ = planfile.load(os.path.join(os.path.dirname(__file__), "..", "data", "plans", "c1a.tcplan.npz"))
+    n, t = planfile.to_objects(flat)
+    bonds = sorted(n.bond_indices, key=lambda ix: repr(ix.id))[:62]
+    with pytest.raises(MemoryError):
+        sliced_execute(n, t, slice_indices=bonds)
