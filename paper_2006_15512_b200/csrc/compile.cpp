@@ -60,6 +60,7 @@ constexpr int32_t kTinySmemCap = 16 * 1024;  // doubles of intermediates per tin
 constexpr int64_t kAlign = 256;
 constexpr int64_t kSMs = 148;                // B200 SM count (split-K sizing)
 constexpr int kMaxTie = 4;                   // physical variables of one operand in one component
+constexpr int64_t kLateReleaseMax = (int64_t)1 << 30;  // late release (chain-link fusion) up to 1 GiB
 
 [[noreturn]] void fail(int st, const std::string& m) { throw Error{st, m}; }
 
@@ -1486,6 +1487,15 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   }
 
   tmark("emit nodes");
+  struct Pending {
+    int64_t off, bytes;
+    int reader;
+  };
+  std::vector<Pending> pending;
+  auto flush_pending = [&]() {
+    for (auto& q : pending) arena.release(q.off, q.bytes, q.reader);
+    pending.clear();
+  };
   auto emit_node = [&](int v) {
     const int k = v - p.NL, a = p.left[k], b = p.right[k];
     Step st;
@@ -1500,6 +1510,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     g.loc[v] = Loc{LOC_ARENA, arena.alloc(bytes[v], haz)};
     for (int h : haz) st.deps.push_back(h);
     st.lc = g.loc[v];
+    flush_pending();  // the previous node's inputs: free only now (see below)
     const auto& La = g.layout[a];
     const auto& Lb = g.layout[b];
     const auto& Lc = g.layout[v];
@@ -1604,6 +1615,9 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         st.nf = nf;
         st.la = g.loc[big];
         st.lb = g.loc[sm];
+        st.la_bytes = bytes[big];
+        st.lb_bytes = bytes[sm];
+        st.lc_bytes = bytes[v];
         st.work = sp.nx;
         g.n_stream++;
         done = true;
@@ -1776,8 +1790,24 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       producer[v] = me;
       g.steps.push_back(st);
     }
+    // Inputs are released one node late: the next node's output never reuses
+    // them, so a chain link (stream -> stream) may run fused in one kernel
+    // that reads this node's inputs while writing the next node's output.
+    // (only for a stream node whose parent is a stream node reading it as the
+    // big operand: elsewhere the late release would only raise the peak)
+    // (relabel aliases in between are the same buffer: look through them)
+    int cur = v, par = p.parent[v];
+    while (par >= 0 && g.cls[par] == NC_ALIAS) cur = par, par = p.parent[par];
+    bool link = g.cls[v] == NC_STREAM && par >= 0 && g.cls[par] == NC_STREAM;
+    if (link) {
+      const int pk = par - p.NL, pa = p.left[pk], pb = p.right[pk];
+      link = (eff[pb].size() <= eff[pa].size() ? pa : pb) == cur;
+    }
     for (int c : {a, b})
-      if (g.loc[c].kind == LOC_ARENA) arena.release(g.loc[c].off, bytes[c], me);
+      if (g.loc[c].kind == LOC_ARENA) {
+        if (link && bytes[c] <= kLateReleaseMax) pending.push_back({g.loc[c].off, bytes[c], me});
+        else arena.release(g.loc[c].off, bytes[c], me);
+      }
   };
 
   for (int k = 0; k < p.NN; ++k) {
@@ -1799,6 +1829,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     emit_node(v);
   }
 
+  flush_pending();
   tmark("root copy");
   accounting.get();  // rethrows TC_OVERFLOW from the accounting thread
   g.mem_estimate = mem_est;

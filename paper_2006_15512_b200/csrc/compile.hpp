@@ -34,6 +34,7 @@ struct Step {
   int32_t ns = 0, nf = 0;          // stream template selector
   int32_t bm = 6, bn = 6;          // GEMM tile bits (template selector)
   Loc la{}, lb{}, lc{}, lws{};     // operand/output/workspace locations
+  int64_t la_bytes = 0, lb_bytes = 0, lc_bytes = 0;  // their extents
   int64_t gdig_off = 0;            // generic digits offset (in GDigit units)
   int64_t work = 0;                // elements (for launch sizing)
   double alg_bytes = 0, alg_flops = 0;  // algorithmic traffic / flops of the node(s)

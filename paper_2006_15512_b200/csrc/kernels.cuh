@@ -375,6 +375,87 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream(const StreamParams p)
   pdl_launch();  // dependents start as this CTA retires (overlap the tail only)
 }
 
+// K2p: two chained stream steps, the intermediate in registers (see program.h).
+// NI inner bits, step-1 shape (NS1 summed, NF1 new), step-2 shape (NS2, NF2).
+template <int NI, int NS1, int NF1, int NS2, int NF2>
+__global__ void __launch_bounds__(kStreamThreads) k_stream_pair(const StreamPairParams p) {
+  constexpr int NQ = 1 << NI, SV1 = 1 << NS1, FV1 = 1 << NF1, SV2 = 1 << NS2, FV2 = 1 << NF2;
+  constexpr int NR = NQ / SV2;  // rest combos
+  constexpr int CB = kStreamChunkBits;
+  const int tid = threadIdx.x;
+  pdl_wait();
+  // per-thread low parts of the y address tables (y = chunk * 2^CB + u * 256 + tid)
+  int64_t ta = 0, tc = 0, t1 = 0, t2 = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if ((tid >> j) & 1) ta += p.bitA[j], tc += p.bitC[j], t1 += p.bitP1[j], t2 += p.bitP2[j];
+  int64_t la[kStreamUnroll], lc[kStreamUnroll], l1[kStreamUnroll], l2[kStreamUnroll];
+#pragma unroll
+  for (int u = 0; u < kStreamUnroll; ++u) {
+    la[u] = ta + ((u & 1) ? p.bitA[8] : 0) + ((u & 2) ? p.bitA[9] : 0);
+    lc[u] = tc + ((u & 1) ? p.bitC[8] : 0) + ((u & 2) ? p.bitC[9] : 0);
+    l1[u] = t1 + ((u & 1) ? p.bitP1[8] : 0) + ((u & 2) ? p.bitP1[9] : 0);
+    l2[u] = t2 + ((u & 1) ? p.bitP2[8] : 0) + ((u & 2) ? p.bitP2[9] : 0);
+  }
+  const int cl = max(0, p.ybits - CB);
+  const int logG = 31 - __clz(gridDim.x);
+  const int g = min(logG, cl);
+  const int b = blockIdx.x;
+  if (b >= (1 << g)) return;
+  const int kchunk = cl - g;
+  int64_t ha = 0, hc = 0, h1 = 0, h2 = 0;
+  {
+    uint64_t m = (uint64_t)b << (kchunk + CB);
+    while (m) {
+      const int j = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      ha += p.bitA[j], hc += p.bitC[j], h1 += p.bitP1[j], h2 += p.bitP2[j];
+    }
+  }
+  const int64_t ny = (int64_t)1 << p.ybits;
+  const int64_t nsteps = (int64_t)1 << kchunk;
+  for (int64_t i = 0; i < nsteps; ++i) {
+    if (i > 0) {
+      const int j = __ffsll((long long)i) - 1 + CB;
+      const int64_t sg = (((i ^ (i >> 1)) >> (j - CB)) & 1) ? 1 : -1;
+      ha += sg * p.bitA[j], hc += sg * p.bitC[j], h1 += sg * p.bitP1[j], h2 += sg * p.bitP2[j];
+    }
+#pragma unroll
+    for (int u = 0; u < kStreamUnroll; ++u) {
+      if (ny < (1 << CB) && u * kStreamThreads + tid >= ny) continue;
+      const double* Ab = p.A + ha + la[u];
+      const double* P1b = p.P1 + h1 + l1[u];
+      const double* P2b = p.P2 + h2 + l2[u];
+      double* Cb = p.C + hc + lc[u];
+      // step 1 for every inner combo (loads shared by combos with equal A offset)
+      double c1[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        double acc = 0.0;
+#pragma unroll
+        for (int s = 0; s < SV1; ++s)
+          acc = fma(__ldcs(Ab + p.qA[q] + p.offA1[s]), __ldg(P1b + p.qP1[q] + p.offP1[s * FV1 + p.qF1[q]]), acc);
+        c1[q] = acc;
+      }
+      // step 2: every (rest, f2) output sums its SV2 inner combos in s2 order
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const int q0 = r << NS2;  // s2 = 0 combo of this rest (P2 batch / C2 offsets)
+#pragma unroll
+        for (int f = 0; f < FV2; ++f) {
+          double acc = 0.0;
+#pragma unroll
+          for (int s = 0; s < SV2; ++s) {
+            acc = fma(c1[s | (r << NS2)], __ldg(P2b + p.qP2[q0] + p.offP2[s * FV2 + f]), acc);
+          }
+          Cb[p.qC[q0] + p.offC2[f]] = acc;
+        }
+      }
+    }
+  }
+  pdl_launch();
+}
+
 // A run of consecutive stream steps in ONE cooperative launch: all CTAs take
 // each step in turn, a grid barrier between steps (the launch gap and ramp of
 // a separate kernel cost more than the barrier for the small steps of tied

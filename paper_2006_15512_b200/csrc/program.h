@@ -79,6 +79,35 @@ struct StreamParams {
                       //    in smem once per CTA; 0: it is read through the L1 (direct)
 };
 
+// ---- K2p: a chain link of two stream steps in registers ----------------------
+// Step 1: C1[x1, f1] = sum_s1 A[x1, s1] P1[b1, s1, f1];  step 2 reads C1:
+// C2[x2, f2] = sum_s2 C1[x2, s2] P2[b2, s2, f2].  Threads enumerate y = the C1
+// address bits outside F1 (step 1's new bits) and S2 (step 2's summed bits);
+// the NI = |F1 u S2| inner bits of C1 live in registers: C1 is never written.
+// Every C1 value and every C2 sum is computed with exactly the operations and
+// order of the two separate steps (bitwise-identical results).
+constexpr int kPairMaxInner = 4;
+struct StreamPairParams {
+  const double* A;
+  const double* P1;
+  const double* P2;
+  double* C;
+  int32_t ybits;  // y counter bits
+  int64_t bitA[kStreamXBits], bitC[kStreamXBits], bitP1[kStreamXBits], bitP2[kStreamXBits];
+  // per inner combo q (bit t of q = inner bit t): A offset (the S2 bits that are
+  // step-1 x bits), step-1 f index, P1 batch offset, step-2 s index, step-2
+  // "rest" index (the F1 bits step 2 keeps), P2 batch offset, C2 offset
+  int64_t qA[1 << kPairMaxInner], qP1[1 << kPairMaxInner], qP2[1 << kPairMaxInner], qC[1 << kPairMaxInner];
+  int32_t qF1[1 << kPairMaxInner], qS2[1 << kPairMaxInner], qR[1 << kPairMaxInner];
+  int64_t offA1[16];   // s1 -> A offset
+  int32_t offP1[64];   // s1 * FV1 + f1 -> P1 offset
+  int32_t offP2[64];   // s2 * FV2 + f2 -> P2 offset
+  int64_t offC2[16];   // f2 -> C2 offset
+  int32_t nq;          // 2^NI
+  int32_t nrest;       // 2^(NI - NS2)
+  int32_t q_of[1 << kPairMaxInner];  // (s2 index, rest index) -> q : q_of[s2 * nrest + r]
+};
+
 // ---- K3: FP64 DMMA GEMM with bit-permuted operands (dim 2) -----------------
 // C[m, n] = sum_k A[m, k] B[k, n]. Tile bits (BM=2^6, BN=2^6, BK=2^4) are the
 // lowest-ordered m/n/k bits; the remaining ("hi") bits index the CTA grid and

@@ -462,11 +462,213 @@ struct tc_exec {
       }
       launches.push_back(std::move(L));
     }
-    group_stream_runs();
+    static const bool seq_on = std::getenv("TC_SEQ") && std::atoi(std::getenv("TC_SEQ")) == 1;
+    if (seq_on) group_stream_runs();
+    else fuse_stream_pairs();
     auto t_end = std::chrono::steady_clock::now();
     setup_ms = std::chrono::duration<double, std::milli>(t_end - t_prog).count();
     compile_ms = std::chrono::duration<double, std::milli>(t_end - t0).count();
     kernels_per_slice = (int64_t)launches.size();
+  }
+
+  // Chain links: a stream step whose big operand is the previous stream step's
+  // output runs with it as ONE k_stream_pair launch (the intermediate stays in
+  // registers; TC_FUSE=0 disables).  Pairs are formed greedily along the step
+  // order.  ldeps[i] = launches launch i depends on.
+  using PairFn = void (*)(StreamPairParams);
+  static PairFn pair_fn(int ni, int ns1, int nf1, int ns2, int nf2) {
+#define PF(a, b, c, d, e) \
+  if (ni == a && ns1 == b && nf1 == c && ns2 == d && nf2 == e) return k_stream_pair<a, b, c, d, e>;
+    PF(2, 1, 1, 1, 1) PF(1, 1, 1, 0, 1) PF(2, 0, 1, 1, 1) PF(2, 2, 1, 1, 1) PF(3, 1, 1, 2, 1)
+    PF(1, 0, 1, 0, 1) PF(2, 0, 2, 0, 2) PF(3, 2, 1, 2, 1) PF(1, 2, 1, 0, 1) PF(2, 1, 1, 1, 2)
+    PF(3, 1, 2, 1, 1) PF(2, 0, 2, 0, 1) PF(2, 0, 1, 2, 1) PF(1, 1, 1, 1, 1) PF(1, 0, 1, 1, 1)
+#undef PF
+    return nullptr;
+  }
+
+  // Derive the pair parameters from the two bound steps; false if the link
+  // does not fit the kernel family (then the steps launch separately).
+  static bool make_pair(const StreamParams& a, int ns1, int nf1, const StreamParams& b, int ns2, int nf2,
+                        StreamPairParams& o, int& ni) {
+    if (ns1 > 2 || nf1 > 2 || ns2 > 2 || nf2 > 2) return false;  // the instantiated family
+    if (b.A != a.C || b.xa2.n != 0) return false;
+    auto bits_of = [](const BitRuns& r) {
+      int n = 0;
+      for (int j = 0; j < r.n; ++j) n += r.len[j];
+      return n;
+    };
+    const int x1 = bits_of(a.xc), x2 = bits_of(b.xa);
+    if (((int64_t)1 << x1) != a.nx || ((int64_t)1 << x2) != b.nx || x1 > kStreamXBits || x2 > kStreamXBits) return false;
+    auto lg = [](int64_t v) { return (v > 0 && (v & (v - 1)) == 0) ? 63 - __builtin_clzll((unsigned long long)v) : -1; };
+    // owners of C1 address bits: step 1 (x1 bit j -> 0..x1-1, or F1 index -> 100+t)
+    int own1[64], own2[64];
+    for (int c = 0; c < 64; ++c) own1[c] = own2[c] = -1;
+    for (int j = 0; j < x1; ++j) {
+      const int c = lg(a.bitC[j]);
+      if (c < 0) return false;
+      own1[c] = j;
+    }
+    for (int t = 0; t < nf1; ++t) {
+      const int c = lg(a.offC[1 << t]);
+      if (c < 0 || own1[c] >= 0) return false;
+      own1[c] = 100 + t;
+    }
+    for (int j = 0; j < x2; ++j) {
+      const int c = lg(b.bitA[j]);
+      if (c < 0 || own2[c] >= 0) return false;
+      own2[c] = j;
+    }
+    int s2bit[4];
+    for (int t = 0; t < ns2; ++t) {
+      const int c = lg(b.offA[1 << t]);
+      if (c < 0 || own2[c] >= 0) return false;
+      own2[c] = 100 + t;
+      s2bit[t] = c;
+    }
+    const int c1bits = x1 + nf1;
+    for (int c = 0; c < c1bits; ++c)
+      if (own1[c] < 0 || own2[c] < 0) return false;
+    // inner bits: S2 (step-2 order), then the F1 bits step 2 keeps (rest)
+    int inner[8], nin = 0;
+    for (int t = 0; t < ns2; ++t) inner[nin++] = s2bit[t];
+    for (int c = 0; c < c1bits; ++c)
+      if (own1[c] >= 100 && own2[c] < 100) {
+        if (nin == 8) return false;
+        inner[nin++] = c;
+      }
+    ni = nin;
+    if (ni > 3) return false;
+    o = StreamPairParams{};
+    o.A = a.A;
+    o.P1 = a.P;
+    o.P2 = b.P;
+    o.C = b.C;
+    o.nq = 1 << ni;
+    o.nrest = 1 << (ni - ns2);
+    for (int q = 0; q < o.nq; ++q) {
+      int64_t qa = 0, qp1 = 0, qp2 = 0, qc = 0;
+      int f1 = 0;
+      for (int t = 0; t < ni; ++t) {
+        if (!((q >> t) & 1)) continue;
+        const int c = inner[t];
+        if (own1[c] < 100) qa += a.bitA[own1[c]], qp1 += a.bitPo[own1[c]];
+        else f1 |= 1 << (own1[c] - 100);
+        if (own2[c] < 100) qp2 += b.bitPo[own2[c]], qc += b.bitC[own2[c]];
+      }
+      o.qA[q] = qa;
+      o.qP1[q] = qp1;
+      o.qF1[q] = f1;
+      o.qP2[q] = qp2;
+      o.qC[q] = qc;
+      o.q_of[q] = q;  // q = s2 | rest << ns2  ->  q_of[s2 * nrest + rest]
+    }
+    for (int s2 = 0; s2 < (1 << ns2); ++s2)
+      for (int r = 0; r < o.nrest; ++r) o.q_of[s2 * o.nrest + r] = s2 | (r << ns2);
+    // y bits: the remaining C1 bits, ascending
+    int yb = 0;
+    for (int c = 0; c < c1bits; ++c) {
+      bool in = false;
+      for (int t = 0; t < ni; ++t) in |= inner[t] == c;
+      if (in) continue;
+      if (own1[c] >= 100 || own2[c] >= 100 || yb >= kStreamXBits) return false;
+      o.bitA[yb] = a.bitA[own1[c]];
+      o.bitP1[yb] = a.bitPo[own1[c]];
+      o.bitC[yb] = b.bitC[own2[c]];
+      o.bitP2[yb] = b.bitPo[own2[c]];
+      ++yb;
+    }
+    o.ybits = yb;
+    for (int s = 0; s < (1 << ns1); ++s) o.offA1[s] = a.offA[s];
+    for (int q = 0; q < ((1 << ns1) << nf1); ++q) o.offP1[q] = a.offP[q];
+    for (int q = 0; q < ((1 << ns2) << nf2); ++q) o.offP2[q] = b.offP[q];
+    for (int f = 0; f < (1 << nf2); ++f) o.offC2[f] = b.offC[f];
+    return true;
+  }
+
+  void fuse_stream_pairs() {
+    Program& g = prog;
+    const size_t S = g.steps.size();
+    static const bool on = !(std::getenv("TC_FUSE") && std::atoi(std::getenv("TC_FUSE")) == 0);
+    std::vector<int> lid(S, -1);
+    std::vector<Launch> out;
+    std::vector<std::vector<int>> odeps;
+    auto bound = [&](size_t k) {
+      StreamParams sp;
+      std::memcpy(&sp, launches[k].blob.data() + launches[k].off[0], sizeof(sp));
+      return sp;
+    };
+    for (size_t i = 0; i < S;) {
+      StreamPairParams pp;
+      int ni = 0;
+      PairFn fn = nullptr;
+      static const bool dbg = std::getenv("TC_FUSE_DEBUG") != nullptr;
+      if (dbg && i + 1 < S && g.steps[i].kind == ST_STREAM && g.steps[i + 1].kind == ST_STREAM) {
+        const Step &s1 = g.steps[i], &s2 = g.steps[i + 1];
+        bool dep = false;
+        for (int d : s2.deps) dep |= d == (int)i;
+        StreamPairParams tmp;
+        int tni = 0;
+        const bool mk = make_pair(bound(i), s1.ns, s1.nf, bound(i + 1), s2.ns, s2.nf, tmp, tni);
+        std::fprintf(stderr, "[fuse] %zu (%d,%d)->(%d,%d) dep=%d link=%d make=%d ni=%d fn=%d A=[%ld,+%ld) P1=[%ld,+%ld) C2=[%ld,+%ld) k%d%d%d\n", i, s1.ns, s1.nf, s2.ns,
+                     s2.nf, (int)dep, (int)(bound(i + 1).A == bound(i).C), (int)mk, tni,
+                     (int)(mk && pair_fn(tni, s1.ns, s1.nf, s2.ns, s2.nf) != nullptr), (long)s1.la.off, (long)s1.la_bytes,
+                     (long)s1.lb.off, (long)s1.lb_bytes, (long)s2.lc.off, (long)s2.lc_bytes, (int)s1.la.kind, (int)s1.lb.kind, (int)s2.lc.kind);
+      }
+      if (on && i + 1 < S && g.steps[i].kind == ST_STREAM && g.steps[i + 1].kind == ST_STREAM) {
+        const Step &s1 = g.steps[i], &s2 = g.steps[i + 1];
+        bool dep_ok = false;  // step 2 must consume step 1 (its RAW edge)
+        for (int d : s2.deps) dep_ok |= d == (int)i;
+        // C2 may reuse the memory step 1 read (A, P1: released after step 1);
+        // fused, those reads and the C2 writes overlap in time
+        auto overlaps = [](const Loc& x, int64_t xb, const Loc& y, int64_t yb) {
+          return x.kind == LOC_ARENA && y.kind == LOC_ARENA && x.off < y.off + yb && y.off < x.off + xb;
+        };
+        if (overlaps(s1.la, s1.la_bytes, s2.lc, s2.lc_bytes) || overlaps(s1.lb, s1.lb_bytes, s2.lc, s2.lc_bytes))
+          dep_ok = false;
+        if (dep_ok && make_pair(bound(i), s1.ns, s1.nf, bound(i + 1), s2.ns, s2.nf, pp, ni))
+          fn = pair_fn(ni, s1.ns, s1.nf, s2.ns, s2.nf);
+      }
+      if (fn) {
+        const Step &s1 = g.steps[i], &s2 = g.steps[i + 1];
+        Launch L;
+        L.kind = ST_STREAM;
+        L.slot = s2.slot;
+        L.func = (void*)fn;
+        L.block = dim3(kStreamThreads);
+        const int chunks_log = std::max(0, pp.ybits - kStreamChunkBits);
+        int gg = 0;
+        while (gg < chunks_log && (2 << gg) <= sm_count(device) * 4) ++gg;
+        L.grid = dim3(1u << gg);
+        // executed bytes: A, P1, P2 and C2 (C1 never touches memory)
+        const StreamParams sp1 = bound(i);
+        const double c1_bytes = 8.0 * (double)sp1.nx * (double)(1 << s1.nf);
+        L.bytes = s1.alg_bytes + s2.alg_bytes - 2 * c1_bytes;
+        L.flops = s1.alg_flops + s2.alg_flops;
+        L.arg(pp);
+        std::vector<int> dd;
+        for (size_t k : {i, i + 1})
+          for (int d : g.steps[k].deps)
+            if (d < (int)i) dd.push_back(lid[d]);
+        std::sort(dd.begin(), dd.end());
+        dd.erase(std::unique(dd.begin(), dd.end()), dd.end());
+        lid[i] = lid[i + 1] = (int)out.size();
+        out.push_back(std::move(L));
+        odeps.push_back(dd);
+        i += 2;
+        continue;
+      }
+      std::vector<int> dd;
+      for (int d : g.steps[i].deps) dd.push_back(lid[d]);
+      std::sort(dd.begin(), dd.end());
+      dd.erase(std::unique(dd.begin(), dd.end()), dd.end());
+      lid[i] = (int)out.size();
+      if ((int)i == rootcopy_launch) rootcopy_launch = (int)out.size();
+      out.push_back(std::move(launches[i]));
+      odeps.push_back(dd);
+      ++i;
+    }
+    launches = std::move(out);
+    ldeps = std::move(odeps);
   }
 
   // TC_SEQ=1: runs of >= 2 consecutive stream steps with small shapes become
