@@ -185,3 +185,30 @@ def test_absurd_slice_counts_raise_instead_of_crashing():
     bonds = sorted(n.bond_indices, key=lambda ix: repr(ix.id))[:62]
     with pytest.raises(MemoryError):
         sliced_execute(n, t, slice_indices=bonds)
+
+
+def test_chain_link_fusion_is_bitwise_identical():
+    """k_stream_pair computes each fused chain link with the operations and
+    order of the two separate steps: the counts are bit-identical to a run
+    with fusion disabled (TC_FUSE=0, read once per process -> subprocess)."""
+    import subprocess
+    import sys
+
+    root = os.path.join(os.path.dirname(__file__), "..")
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "import numpy as np\n"
+            "from paper_2006_15512_b200 import planfile, sliced_execute\n"
+            "for name in ('c1a', 'c2', 'c1b'):\n"
+            "    f, _ = planfile.load(%r + '/data/plans/' + name + '.tcplan.npz')\n"
+            "    n, t = planfile.to_objects(f)\n"
+            "    r = sliced_execute(n, t)\n"
+            "    print(name, float(np.asarray(r.result.values)).hex(), r.stats['gpu_launches'])\n") % (root, root)
+    out = {}
+    for fuse in ("1", "0"):
+        env = dict(os.environ, TC_FUSE=fuse)
+        res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        out[fuse] = {ln.split()[0]: ln.split()[1:] for ln in res.stdout.strip().splitlines()}
+    for name in ("c1a", "c2", "c1b"):
+        assert out["1"][name][0] == out["0"][name][0], name  # same bits
+    assert int(out["1"]["c2"][1]) < int(out["0"]["c2"][1])  # fewer launches when fused
