@@ -54,7 +54,9 @@ namespace tc {
 
 namespace {
 
-constexpr int64_t kTinyMax = 4096;           // entries per tiny tensor
+constexpr int64_t kTinyMax = 4096;
+constexpr int64_t kSegMaxEntries = (int64_t)1 << 22;  // chain tensors fused into segments (32 MB)
+constexpr int kSegMinOuter = 9;           // entries per tiny tensor
 constexpr int32_t kTinySmemCap = 16 * 1024;  // doubles of intermediates per tiny CTA (128 KB; the
                                              // rest of the 227 KB holds the staged batch)
 constexpr int64_t kAlign = 256;
@@ -1195,6 +1197,21 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
           glevel[gi] = std::max(glevel[gi], glevel[group_of[c]] + 1);
     nlevels = std::max(nlevels, glevel[gi] + 1);
   }
+  if (std::getenv("TC_TINY_DEBUG")) {
+    std::vector<size_t> sz;
+    for (auto& gr : groups) sz.push_back(gr.size());
+    std::sort(sz.rbegin(), sz.rend());
+    int64_t work_max = 0, work_sum = 0;
+    for (auto& gr : groups) {
+      int64_t w = 0;
+      for (int v : gr) w += size[v];
+      work_max = std::max(work_max, w), work_sum += w;
+    }
+    std::fprintf(stderr, "tiny: %zu groups, %d levels, nodes top:", groups.size(), nlevels);
+    for (size_t q = 0; q < sz.size() && q < 12; ++q) std::fprintf(stderr, " %zu", sz[q]);
+    std::fprintf(stderr, "  out-entries max %lld sum %lld smem max %d doubles\n", (long long)work_max,
+                 (long long)work_sum, groups.empty() ? 0 : *std::max_element(group_smem.begin(), group_smem.end()));
+  }
 
   tmark("steps + arena");
   // ---- steps + arena --------------------------------------------------------
@@ -1270,6 +1287,14 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   {
     std::vector<std::vector<int>> level_groups(nlevels);
     for (size_t gi = 0; gi < groups.size(); ++gi) level_groups[glevel[gi]].push_back((int)gi);
+    // heaviest groups first (the block scheduler hands out CTAs in order, so
+    // the long subtrees start at once on their own SMs); cost ~ outputs written
+    // plus a per-node overhead
+    std::vector<int64_t> gcost(groups.size(), 0);
+    for (size_t gi = 0; gi < groups.size(); ++gi)
+      for (int v : groups[gi]) gcost[gi] += size[v] + 32;
+    for (auto& lg : level_groups)
+      std::stable_sort(lg.begin(), lg.end(), [&](int x, int y) { return gcost[x] > gcost[y]; });
     for (int lv = 0; lv < nlevels; ++lv) {
       level_range[lv].first = (int32_t)gorder.size();
       for (int gi : level_groups[lv]) gorder.push_back(gi);
@@ -1382,10 +1407,11 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         tn.c_size = (int32_t)size[v];
         tn.s_size = (int32_t)ssz;
         tn.pow2 = p2 ? 1 : 0;
-        // lanes per output: fill the CTA's 256 threads, at most a warp, at
-        // most the number of summed terms
+        // lanes per output: fill the CTA's threads, at most a warp, at most
+        // the number of summed terms
         tn.lw = 0;
-        while (tn.lw < 5 && (tn.c_size << (tn.lw + 1)) <= 256 && (1 << (tn.lw + 1)) <= ssz) ++tn.lw;
+        while (tn.lw < 5 && (tn.c_size << (tn.lw + 1)) <= (1 << kTinyThreadsLog) && (1 << (tn.lw + 1)) <= ssz)
+          ++tn.lw;
         out.nodes.push_back(tn);
         slot.push_back(v);
         out.ga.push_back(la);
@@ -1393,6 +1419,37 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         out.go.push_back(lo);
       }
       tg.end = (int32_t)out.nodes.size();
+      // barriers: a node waits for the CTA only when it reads smem written,
+      // or overwrites smem read or written, since the last barrier (batch
+      // starts are barriers); nodes on the cooperative-reduce path are fenced
+      {
+        std::vector<std::pair<int32_t, int32_t>> ew, er;
+        auto hit = [](const std::vector<std::pair<int32_t, int32_t>>& rs, int32_t b, int32_t e) {
+          for (auto& x : rs)
+            if (b < x.second && x.first < e) return true;
+          return false;
+        };
+        bool prev_red = false;
+        for (int q2 = tg.beg; q2 < tg.end; ++q2) {
+          TinyNode& t = out.nodes[q2];
+          const int v = slot[q2];
+          const bool red = tiny_uses_reduce(t);
+          std::pair<int32_t, int32_t> rd[2];
+          int nr = 0;
+          if (out.ga[q2].kind == LOC_SMEM) rd[nr++] = {t.sa, t.sa + (int32_t)size[p.kid_l(v)]};
+          if (out.gb[q2].kind == LOC_SMEM) rd[nr++] = {t.sb, t.sb + (int32_t)size[p.kid_r(v)]};
+          const bool wr = v != r;
+          const int32_t wb = t.sout, we = t.sout + (int32_t)size[v];
+          bool need = red || prev_red || (q2 - tg.beg) % kTinyBatch == 0;
+          for (int k = 0; k < nr && !need; ++k) need = hit(ew, rd[k].first, rd[k].second);
+          if (wr && !need) need = hit(ew, wb, we) || hit(er, wb, we);
+          if (need) ew.clear(), er.clear();
+          t.sync = need ? 1 : 0;
+          for (int k = 0; k < nr; ++k) er.push_back(rd[k]);
+          if (wr) ew.push_back({wb, we});
+          prev_red = red;
+        }
+      }
       for (int x : nat_used) nat_of[x] = -1;
       nat_used.clear();
       // batches of kTinyBatch nodes: staging offsets of small global operands
@@ -1454,6 +1511,35 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       g.tiny_dig_max = std::max(g.tiny_dig_max, o.digmax);
     }
     g.n_tiny = (int)g.tiny_nodes.size();
+    if (std::getenv("TC_TINY_DEBUG")) {
+      // crude per-group cost: per node, serial iterations of one thread
+      double best = -1;
+      size_t bg = 0;
+      std::vector<double> cost(g.tiny_groups.size());
+      for (size_t q = 0; q < g.tiny_groups.size(); ++q) {
+        double c = 0;
+        for (int i = g.tiny_groups[q].beg; i < g.tiny_groups[q].end; ++i) {
+          const TinyNode& t = g.tiny_nodes[i];
+          const int per = (1 << kTinyThreadsLog) >> t.lw;
+          c += 20 + (double)((t.c_size + per - 1) / per) * ((t.s_size >> t.lw) + t.nc);
+        }
+        cost[q] = c;
+        if (c > best) best = c, bg = q;
+      }
+      std::sort(cost.rbegin(), cost.rend());
+      int nsync = 0;
+      for (auto& t : g.tiny_nodes) nsync += t.sync;
+      std::fprintf(stderr, "tiny barriers %d of %zu nodes; cost top:", nsync, g.tiny_nodes.size());
+      for (size_t q = 0; q < cost.size() && q < 8; ++q) std::fprintf(stderr, " %.0f", cost[q]);
+      std::fprintf(stderr, "\n");
+      for (int i = g.tiny_groups[bg].beg; i < g.tiny_groups[bg].end; ++i) {
+        const TinyNode& t = g.tiny_nodes[i];
+        const int per = (1 << kTinyThreadsLog) >> t.lw;
+        std::fprintf(stderr, "  c=%d s=%d nc=%d ns=%d lw=%d pow2=%d glob=%d%d%d cost=%d\n", t.c_size, t.s_size,
+                     t.nc, t.ns, t.lw, t.pow2, t.ga != nullptr, t.gb != nullptr, t.gout != nullptr,
+                     20 + ((t.c_size + per - 1) / per) * ((t.s_size >> t.lw) + t.nc));
+      }
+    }
     for (size_t gi = 0; gi < groups.size(); ++gi) {
       g.tiny_smem_doubles = std::max(g.tiny_smem_doubles, group_smem[gi]);
       producer[groups[gi].back()] = tiny_step[glevel[gi]];
@@ -1496,8 +1582,398 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     for (auto& q : pending) arena.release(q.off, q.bytes, q.reader);
     pending.clear();
   };
+  struct SegCand {
+    int nA = 0, nC = 0;
+    std::vector<int> src;       // C position -> big-operand position (-1: new variable)
+    std::vector<int64_t> pstC;  // C position -> small-operand stride (0: not a small-operand variable)
+    std::vector<int> kpos;      // summed variables: big-operand positions (ascending)
+    std::vector<int64_t> pstK;  // ... and their small-operand strides
+    bool diag = false;
+  };
+  struct StreamOut {
+    StreamParams sp{};
+    int ns = 0, nf = 0, big = -1, sm = -1;
+    SegCand cand;
+  };
+  // stream-kernel parameters of node v (false: the shape does not fit k_stream)
+  auto build_stream = [&](int v, StreamOut& o, bool want_cand) -> bool {
+    const int k = v - p.NL, a = p.left[k], b = p.right[k];
+    const auto& Lc = g.layout[v];
+    auto [c0, c1] = comps(v);
+    try {
+      const bool b_small = eff[b].size() <= eff[a].size();
+      const int big = b_small ? a : b, sm = b_small ? b : a;
+      const auto& Lg = g.layout[big];
+      const auto& Lq = g.layout[sm];
+      auto bigv = [&](const Comp* c) { return b_small ? c->a : c->b; };
+      auto nbig = [&](const Comp* c) { return b_small ? c->na : c->nb; };
+      auto smv = [&](const Comp* c) { return b_small ? c->b : c->a; };
+      auto nsm = [&](const Comp* c) { return b_small ? c->nb : c->na; };
+      SmallMap<int> pg, pc, pq;
+      for (size_t q = 0; q < Lg.size(); ++q) pg[Lg[q]] = (int)q;
+      for (size_t q = 0; q < Lc.size(); ++q) pc[Lc[q]] = (int)q;
+      for (size_t q = 0; q < Lq.size(); ++q) pq[Lq[q]] = (int)q;
+      K.clear();
+      N.clear();
+      for (const Comp* c = c0; c != c1; ++c) {
+        if (c->c >= 0) ccomp[c->c] = c;
+        if (c->c < 0) K.push_back(c);
+        else if (nbig(c) == 0) N.push_back(c);
+      }
+      auto small_off = [&](const Comp* c) {
+        int64_t o = 0;
+        for (int t = 0; t < nsm(c); ++t) o += (int64_t)1 << pq[smv(c)[t]];
+        return o;
+      };
+      // x bits: C variables with a big-side variable, in C address order
+      std::vector<std::pair<int, int>> xa, xa2, xc;
+      StreamParams sp{};
+      int j = 0;
+      bool bad = false;
+      for (size_t q = 0; q < Lc.size(); ++q) {
+        const Comp* c = ccomp[Lc[q]];
+        if (nbig(c) == 0) continue;
+        xc.push_back({j, (int)q});
+        xa.push_back({j, pg[bigv(c)[0]]});
+        if (nbig(c) == 2) xa2.push_back({j, pg[bigv(c)[1]]});
+        if (nsm(c) > 0) {  // batch variable: also indexes the small operand
+          if (sp.nbt == kStreamMaxBatch) bad = true;
+          else {
+            sp.bt_xbit[sp.nbt] = j;
+            sp.bt_poff[sp.nbt] = small_off(c);
+            sp.nbt++;
+            if (j < kStreamChunkBits) sp.nlb++;
+          }
+        }
+        j++;
+      }
+      std::sort(K.begin(), K.end(), [&](const Comp* x, const Comp* y) { return pg[bigv(x)[0]] < pg[bigv(y)[0]]; });
+      if (want_cand) {  // chain-segment view: C position -> big position / P stride
+        SegCand& sc = o.cand;
+        sc.nA = (int)Lg.size();
+        sc.nC = (int)Lc.size();
+        sc.src.assign(Lc.size(), -1);
+        sc.pstC.assign(Lc.size(), 0);
+        sc.kpos.clear();
+        sc.pstK.clear();
+        sc.diag = false;
+        for (size_t q = 0; q < Lc.size(); ++q) {
+          const Comp* c = ccomp[Lc[q]];
+          if (nbig(c) == 1) sc.src[q] = pg[bigv(c)[0]];
+          else if (nbig(c) > 1) sc.diag = true;
+          if (nsm(c) > 0) sc.pstC[q] = small_off(c);
+        }
+        for (const Comp* c : K) {
+          if (nbig(c) != 1) sc.diag = true;
+          else sc.kpos.push_back(pg[bigv(c)[0]]);
+          sc.pstK.push_back(small_off(c));
+        }
+      }
+      for (const Comp* c = c0; c != c1; ++c)
+        if (c->c >= 0) ccomp[c->c] = nullptr;
+      if (bad) throw Error{-1, "batch"};
+      sp.xa = make_runs(xa);
+      sp.xa2 = make_runs(xa2);
+      sp.xc = make_runs(xc);
+      sp.nx = (int64_t)1 << j;
+      const int ns = (int)K.size(), nf = (int)N.size();
+      // N by C position, K by big-operand position
+      std::sort(N.begin(), N.end(), [&](const Comp* x, const Comp* y) { return pc[x->c] < pc[y->c]; });
+      for (int s = 0; s < (1 << ns); ++s) {
+        int64_t o = 0, oq = 0;
+        for (int t = 0; t < ns; ++t)
+          if (s >> t & 1) {
+            for (int u = 0; u < nbig(K[t]); ++u) o += (int64_t)1 << pg[bigv(K[t])[u]];
+            oq += small_off(K[t]);
+          }
+        sp.offA[s] = o;
+        for (int f = 0; f < (1 << nf); ++f) {
+          int64_t of = 0;
+          for (int t = 0; t < nf; ++t)
+            if (f >> t & 1) of += small_off(N[t]);
+          sp.offP[s * (1 << nf) + f] = (int32_t)(oq + of);
+        }
+      }
+      for (int f = 0; f < (1 << nf); ++f) {
+        int64_t o = 0;
+        for (int t = 0; t < nf; ++t)
+          if (f >> t & 1) o += (int64_t)1 << pc[N[t]->c];
+        sp.offC[f] = o;
+      }
+      sp.stage_all = ((1 << sp.nbt) << (ns + nf)) <= kStreamStageMax;
+      if (j > kStreamXBits) throw Error{-1, "x bits"};
+      for (int jb = 0; jb < kStreamXBits; ++jb) {
+        sp.bitA[jb] = deposit((uint64_t)1 << jb, sp.xa) + deposit((uint64_t)1 << jb, sp.xa2);
+        sp.bitC[jb] = deposit((uint64_t)1 << jb, sp.xc);
+        sp.bitP[jb] = 0;
+        sp.bitPo[jb] = 0;
+        for (int t = 0; t < sp.nbt; ++t)
+          if (sp.bt_xbit[t] == jb) {
+            sp.bitP[jb] = 1 << t;
+            sp.bitPo[jb] = sp.bt_poff[t];
+          }
+      }
+      o.sp = sp;
+      o.ns = ns;
+      o.nf = nf;
+      o.big = big;
+      o.sm = sm;
+      return true;
+    } catch (const Error& e) {
+      if (e.status != -1) throw;
+    }
+    return false;
+  };
+  // ---- chain segments (program.h) ------------------------------------------
+  // A stream node whose big operand is the output of an open segment joins it
+  // while every stage's tile fits kSegTileMax bits; the segment is emitted
+  // (one launch, output allocated then) when its output is read by anything
+  // else.  Tokens name the chain tensor's variables across steps.
+  struct Seg {
+    Loc a_loc{};
+    int64_t a_bytes = 0;
+    int a_prod = -1;
+    std::vector<std::vector<int>> stages;  // tokens by address position
+    std::vector<std::vector<int>> sumt;    // per step: summed tokens
+    std::vector<int> T;                    // tokens summed or created by any step
+    std::vector<SegCand> cand;
+    std::vector<int> vslot;
+    std::vector<Loc> p_loc;
+    std::vector<int64_t> p_bytes;
+    std::vector<int> p_prod;
+    StreamParams sp0{};
+    int ns0 = 0, nf0 = 0;
+    int ntok = 0;
+  };
+  std::vector<Seg> segs;
+  // opt-in (TC_SEG=1): measured slower than k_stream + fused pairs on the
+  // benchmark plans so far
+  static const bool seg_on = std::getenv("TC_SEG") && std::atoi(std::getenv("TC_SEG")) == 1;
+  static const int seg_tile_max =
+      std::getenv("TC_SEG_TILE") ? std::max(6, std::min(kSegTileMax, std::atoi(std::getenv("TC_SEG_TILE")))) : kSegTileMax;
+  // stage tokens after applying step c to `prev` (fresh tokens from `fresh`)
+  auto seg_apply = [](const std::vector<int>& prev, const SegCand& c, int& fresh, std::vector<int>& nt,
+                      std::vector<int>& sumt) {
+    nt.assign(c.nC, -1);
+    for (int q = 0; q < c.nC; ++q) nt[q] = c.src[q] >= 0 ? prev[c.src[q]] : fresh++;
+    sumt.clear();
+    for (int kp : c.kpos) sumt.push_back(prev[kp]);
+  };
+  auto seg_tile = [](int ntok, const std::vector<int>& T, const std::vector<int>& first,
+                     const std::vector<int>& last) {
+    std::vector<char> in(ntok, 0);
+    for (int t : T) in[t] = 1;
+    for (int q = 0; q < kSegLowBits && q < (int)first.size(); ++q) in[first[q]] = 1;
+    for (int q = 0; q < kSegLowBits && q < (int)last.size(); ++q) in[last[q]] = 1;
+    return in;
+  };
+  auto seg_try_append = [&](Seg& S, const SegCand& c) {
+    if ((int)S.vslot.size() >= kSegMaxSteps || (int)S.stages.back().size() != c.nA) return false;
+    for (int64_t x : c.pstC)
+      if (x >= ((int64_t)1 << 30)) return false;
+    for (int64_t x : c.pstK)
+      if (x >= ((int64_t)1 << 30)) return false;
+    int fresh = S.ntok;
+    std::vector<int> nt, st;
+    seg_apply(S.stages.back(), c, fresh, nt, st);
+    std::vector<int> T = S.T;
+    for (int t : st) T.push_back(t);
+    for (int q = 0; q < c.nC; ++q)
+      if (c.src[q] < 0) T.push_back(nt[q]);
+    const auto in = seg_tile(fresh, T, S.stages[0], nt);
+    // tile bits: at most kSegTileMax, and few enough to leave >= 2^kSegMinOuter
+    // outer blocks (one per CTA at a time) when the tensor is large enough
+    auto fits = [&](const std::vector<int>& stg) {
+      int cnt = 0;
+      for (int t : stg) cnt += in[t];
+      return cnt <= std::min(seg_tile_max, std::max(6, (int)stg.size() - kSegMinOuter));
+    };
+    for (auto& stg : S.stages)
+      if (!fits(stg)) return false;
+    if (!fits(nt)) return false;
+    S.stages.push_back(std::move(nt));
+    S.sumt.push_back(std::move(st));
+    S.T = std::move(T);
+    S.ntok = fresh;
+    S.cand.push_back(c);
+    return true;
+  };
+  auto seg_close = [&](int slot) {
+    const int id = (int)g.loc[slot].off;
+    Seg& S = segs[id];
+    const int n = (int)S.vslot.size();
+    const int vlast = S.vslot.back();
+    Step st;
+    st.slot = vlast;
+    if (S.a_prod >= 0) st.deps.push_back(S.a_prod);
+    for (int q : S.p_prod)
+      if (q >= 0) st.deps.push_back(q);
+    haz.clear();
+    const Loc out{LOC_ARENA, arena.alloc(bytes[vlast], haz)};
+    for (int h : haz) st.deps.push_back(h);
+    flush_pending();
+    st.la = S.a_loc;
+    st.lc = out;
+    st.la_bytes = S.a_bytes;
+    st.lc_bytes = bytes[vlast];
+    if (n == 1) {
+      st.kind = ST_STREAM;
+      st.sp = S.sp0;
+      st.ns = S.ns0;
+      st.nf = S.nf0;
+      st.lb = S.p_loc[0];
+      st.lb_bytes = S.p_bytes[0];
+      st.alg_bytes = node_bytes[vlast];
+      st.alg_flops = node_flops[vlast];
+      st.work = S.sp0.nx;
+    } else {
+      const int ns_ = n + 1;
+      const auto in = seg_tile(S.ntok, S.T, S.stages[0], S.stages[n]);
+      std::vector<std::vector<int>> pos(ns_, std::vector<int>(S.ntok, -1)), rank(ns_, std::vector<int>(S.ntok, -1));
+      std::vector<int> tsz(ns_, 0);
+      int tmax = 0;
+      for (int s2 = 0; s2 < ns_; ++s2) {
+        const auto& L = S.stages[s2];
+        for (int q = 0; q < (int)L.size(); ++q) {
+          pos[s2][L[q]] = q;
+          if (in[L[q]]) rank[s2][L[q]] = tsz[s2]++;
+        }
+        tmax = std::max(tmax, tsz[s2]);
+      }
+      SegParams sg{};
+      sg.nsteps = n;
+      sg.nt0 = tsz[0];
+      sg.ntL = tsz[n];
+      sg.tile_doubles = 1 << tmax;
+      g.seg_tile_max = std::max(g.seg_tile_max, sg.tile_doubles);
+      // outer variables: untouched, present in every stage; by input position
+      st.seg_tab_off = (int64_t)g.seg_tab.size();
+      int nouter = 0;
+      for (int t : S.stages[0]) {
+        if (in[t]) continue;
+        ++nouter;
+        g.seg_tab.push_back((int64_t)1 << pos[0][t]);
+        g.seg_tab.push_back((int64_t)1 << pos[n][t]);
+        for (int k2 = 0; k2 < n; ++k2) g.seg_tab.push_back(S.cand[k2].pstC[pos[k2 + 1][t]]);
+      }
+      sg.nouter = nouter;
+      st.seg_gtab_off = (int64_t)g.seg_tab.size();
+      for (int s2 : {0, n})
+        for (int t : S.stages[s2])
+          if (in[t]) g.seg_tab.push_back((int64_t)1 << pos[s2][t]);
+      st.seg_off = (int64_t)g.seg_steps.size();
+      double pbytes = 0, fl = 0;
+      for (int k2 = 0; k2 < n; ++k2) {
+        const SegCand& c = S.cand[k2];
+        SegStep ss{};
+        ss.dig = (int32_t)g.seg_digits.size();
+        std::vector<SegDigit> fd;
+        for (int t : S.stages[k2 + 1]) {
+          if (!in[t]) continue;
+          const int ra = rank[k2][t];
+          const SegDigit d{ra >= 0 ? 1 << ra : 0, (int32_t)c.pstC[pos[k2 + 1][t]], 1 << rank[k2 + 1][t], 0};
+          if (ra >= 0) g.seg_digits.push_back(d), ss.nx++;
+          else fd.push_back(d), ss.nf++;
+        }
+        g.seg_digits.insert(g.seg_digits.end(), fd.begin(), fd.end());
+        for (size_t u = 0; u < S.sumt[k2].size(); ++u)
+          g.seg_digits.push_back(SegDigit{1 << rank[k2][S.sumt[k2][u]], (int32_t)c.pstK[u], 0, 0});
+        ss.ns = (int32_t)S.sumt[k2].size();
+        ss.pst = -1;
+        ss.pn = (int32_t)(S.p_bytes[k2] / 8);
+        {
+          bool outer_free = true;  // P offset does not depend on the outer block
+          for (int t : S.stages[0])
+            if (!in[t] && c.pstC[pos[k2 + 1][t]] != 0) outer_free = false;
+          if (outer_free && sg.pst_doubles + ss.pn <= kSegPStageMax) {
+            ss.pst = sg.pst_doubles;
+            sg.pst_doubles += (ss.pn + 1) & ~1;
+          }
+        }
+        g.seg_steps.push_back(ss);
+        g.seg_P.push_back(S.p_loc[k2]);
+        pbytes += (double)S.p_bytes[k2];
+        fl += node_flops[S.vslot[k2]];
+      }
+      st.kind = ST_SEG;
+      st.sg = sg;
+      st.alg_bytes = (double)S.a_bytes + (double)bytes[vlast] + pbytes;
+      st.alg_flops = fl;
+      st.work = (int64_t)1 << nouter;
+      g.n_seg++;
+      g.n_seg_steps += n;
+    }
+    const int me = (int)g.steps.size();
+    g.steps.push_back(st);
+    if (S.a_loc.kind == LOC_ARENA) arena.release(S.a_loc.off, S.a_bytes, me);
+    for (int k2 = 0; k2 < n; ++k2)
+      if (S.p_loc[k2].kind == LOC_ARENA) arena.release(S.p_loc[k2].off, S.p_bytes[k2], me);
+    producer[vlast] = me;
+    g.loc[vlast] = out;
+    producer[slot] = me;
+    g.loc[slot] = out;
+  };
+  // stream node v into a segment (false: emit it the ordinary way)
+  auto try_seg = [&](int v) {
+    // large chain tensors stream at HBM speed step by step (k_stream, fused
+    // pairs); segments pay off where each step is a small, latency-bound launch
+    {
+      const int k = v - p.NL;
+      if (std::max({size[p.left[k]], size[p.right[k]], size[v]}) > kSegMaxEntries) return false;
+    }
+    StreamOut so;
+    if (!build_stream(v, so, true) || so.cand.diag) return false;
+    const int big = so.big, sm = so.sm;
+    if (g.loc[sm].kind == LOC_SEG) seg_close(sm);
+    g.n_stream++;
+    if (g.loc[big].kind == LOC_SEG) {
+      const int id = (int)g.loc[big].off;
+      if (seg_try_append(segs[id], so.cand)) {
+        Seg& S = segs[id];
+        S.vslot.push_back(v);
+        S.p_loc.push_back(g.loc[sm]);
+        S.p_bytes.push_back(bytes[sm]);
+        S.p_prod.push_back(producer[sm]);
+        g.loc[v] = Loc{LOC_SEG, id};
+        producer[v] = -1;
+        return true;
+      }
+      seg_close(big);
+    }
+    Seg S;
+    S.a_loc = g.loc[big];
+    S.a_bytes = bytes[big];
+    S.a_prod = producer[big];
+    S.ntok = so.cand.nA;
+    S.stages.emplace_back(so.cand.nA);
+    for (int q = 0; q < so.cand.nA; ++q) S.stages[0][q] = q;
+    int fresh = S.ntok;
+    std::vector<int> nt, st;
+    seg_apply(S.stages[0], so.cand, fresh, nt, st);
+    for (int t : st) S.T.push_back(t);
+    for (int q = 0; q < so.cand.nC; ++q)
+      if (so.cand.src[q] < 0) S.T.push_back(nt[q]);
+    S.ntok = fresh;
+    S.stages.push_back(std::move(nt));
+    S.sumt.push_back(std::move(st));
+    S.cand.push_back(so.cand);
+    S.vslot.push_back(v);
+    S.p_loc.push_back(g.loc[sm]);
+    S.p_bytes.push_back(bytes[sm]);
+    S.p_prod.push_back(producer[sm]);
+    S.sp0 = so.sp;
+    S.ns0 = so.ns;
+    S.nf0 = so.nf;
+    segs.push_back(std::move(S));
+    g.loc[v] = Loc{LOC_SEG, (int64_t)segs.size() - 1};
+    producer[v] = -1;
+    return true;
+  };
   auto emit_node = [&](int v) {
     const int k = v - p.NL, a = p.left[k], b = p.right[k];
+    if (seg_on && g.cls[v] == NC_STREAM && try_seg(v)) return;
+    for (int c : {a, b})
+      if (g.loc[c].kind == LOC_SEG) seg_close(c);
     Step st;
     st.slot = v;
     st.alg_bytes = node_bytes[v];
@@ -1517,112 +1993,20 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     auto [c0, c1] = comps(v);
     bool done = false;
     if (g.cls[v] == NC_STREAM) {
-      try {
-        const bool b_small = eff[b].size() <= eff[a].size();
-        const int big = b_small ? a : b, sm = b_small ? b : a;
-        const auto& Lg = g.layout[big];
-        const auto& Lq = g.layout[sm];
-        auto bigv = [&](const Comp* c) { return b_small ? c->a : c->b; };
-        auto nbig = [&](const Comp* c) { return b_small ? c->na : c->nb; };
-        auto smv = [&](const Comp* c) { return b_small ? c->b : c->a; };
-        auto nsm = [&](const Comp* c) { return b_small ? c->nb : c->na; };
-        SmallMap<int> pg, pc, pq;
-        for (size_t q = 0; q < Lg.size(); ++q) pg[Lg[q]] = (int)q;
-        for (size_t q = 0; q < Lc.size(); ++q) pc[Lc[q]] = (int)q;
-        for (size_t q = 0; q < Lq.size(); ++q) pq[Lq[q]] = (int)q;
-        K.clear();
-        N.clear();
-        for (const Comp* c = c0; c != c1; ++c) {
-          if (c->c >= 0) ccomp[c->c] = c;
-          if (c->c < 0) K.push_back(c);
-          else if (nbig(c) == 0) N.push_back(c);
-        }
-        auto small_off = [&](const Comp* c) {
-          int64_t o = 0;
-          for (int t = 0; t < nsm(c); ++t) o += (int64_t)1 << pq[smv(c)[t]];
-          return o;
-        };
-        // x bits: C variables with a big-side variable, in C address order
-        std::vector<std::pair<int, int>> xa, xa2, xc;
-        StreamParams sp{};
-        int j = 0;
-        bool bad = false;
-        for (size_t q = 0; q < Lc.size(); ++q) {
-          const Comp* c = ccomp[Lc[q]];
-          if (nbig(c) == 0) continue;
-          xc.push_back({j, (int)q});
-          xa.push_back({j, pg[bigv(c)[0]]});
-          if (nbig(c) == 2) xa2.push_back({j, pg[bigv(c)[1]]});
-          if (nsm(c) > 0) {  // batch variable: also indexes the small operand
-            if (sp.nbt == kStreamMaxBatch) bad = true;
-            else {
-              sp.bt_xbit[sp.nbt] = j;
-              sp.bt_poff[sp.nbt] = small_off(c);
-              sp.nbt++;
-              if (j < kStreamChunkBits) sp.nlb++;
-            }
-          }
-          j++;
-        }
-        for (const Comp* c = c0; c != c1; ++c)
-          if (c->c >= 0) ccomp[c->c] = nullptr;
-        if (bad) throw Error{-1, "batch"};
-        sp.xa = make_runs(xa);
-        sp.xa2 = make_runs(xa2);
-        sp.xc = make_runs(xc);
-        sp.nx = (int64_t)1 << j;
-        const int ns = (int)K.size(), nf = (int)N.size();
-        // N by C position, K by big-operand position
-        std::sort(N.begin(), N.end(), [&](const Comp* x, const Comp* y) { return pc[x->c] < pc[y->c]; });
-        std::sort(K.begin(), K.end(), [&](const Comp* x, const Comp* y) { return pg[bigv(x)[0]] < pg[bigv(y)[0]]; });
-        for (int s = 0; s < (1 << ns); ++s) {
-          int64_t o = 0, oq = 0;
-          for (int t = 0; t < ns; ++t)
-            if (s >> t & 1) {
-              for (int u = 0; u < nbig(K[t]); ++u) o += (int64_t)1 << pg[bigv(K[t])[u]];
-              oq += small_off(K[t]);
-            }
-          sp.offA[s] = o;
-          for (int f = 0; f < (1 << nf); ++f) {
-            int64_t of = 0;
-            for (int t = 0; t < nf; ++t)
-              if (f >> t & 1) of += small_off(N[t]);
-            sp.offP[s * (1 << nf) + f] = (int32_t)(oq + of);
-          }
-        }
-        for (int f = 0; f < (1 << nf); ++f) {
-          int64_t o = 0;
-          for (int t = 0; t < nf; ++t)
-            if (f >> t & 1) o += (int64_t)1 << pc[N[t]->c];
-          sp.offC[f] = o;
-        }
-        sp.stage_all = ((1 << sp.nbt) << (ns + nf)) <= kStreamStageMax;
-        if (j > kStreamXBits) throw Error{-1, "x bits"};
-        for (int jb = 0; jb < kStreamXBits; ++jb) {
-          sp.bitA[jb] = deposit((uint64_t)1 << jb, sp.xa) + deposit((uint64_t)1 << jb, sp.xa2);
-          sp.bitC[jb] = deposit((uint64_t)1 << jb, sp.xc);
-          sp.bitP[jb] = 0;
-          sp.bitPo[jb] = 0;
-          for (int t = 0; t < sp.nbt; ++t)
-            if (sp.bt_xbit[t] == jb) {
-              sp.bitP[jb] = 1 << t;
-              sp.bitPo[jb] = sp.bt_poff[t];
-            }
-        }
+      StreamOut so;
+      if (build_stream(v, so, false)) {
         st.kind = ST_STREAM;
-        st.sp = sp;
-        st.ns = ns;
-        st.nf = nf;
-        st.la = g.loc[big];
-        st.lb = g.loc[sm];
-        st.la_bytes = bytes[big];
-        st.lb_bytes = bytes[sm];
+        st.sp = so.sp;
+        st.ns = so.ns;
+        st.nf = so.nf;
+        st.la = g.loc[so.big];
+        st.lb = g.loc[so.sm];
+        st.la_bytes = bytes[so.big];
+        st.lb_bytes = bytes[so.sm];
         st.lc_bytes = bytes[v];
-        st.work = sp.nx;
+        st.work = so.sp.nx;
         g.n_stream++;
         done = true;
-      } catch (const Error& e) {
-        if (e.status != -1) throw;
       }
     }
     bool diag = false;
@@ -1829,6 +2213,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     emit_node(v);
   }
 
+  if (g.loc[p.root].kind == LOC_SEG) seg_close(p.root);
   flush_pending();
   tmark("root copy");
   accounting.get();  // rethrows TC_OVERFLOW from the accounting thread

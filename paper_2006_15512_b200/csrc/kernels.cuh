@@ -88,8 +88,7 @@ __global__ void k_fold(const double* results, int64_t R, int64_t n, double* out)
 
 // ---------------------------------------------------------------------------
 // K4: one CTA walks one tiny subtree in postorder; intermediates live in smem.
-constexpr int kTinyThreads = 256;
-constexpr int kTinyMaxSum = 16;  // summed dim-2 digits with precomputed deltas
+constexpr int kTinyThreads = 1 << kTinyThreadsLog;
 
 // smem: [intermediates: smem_doubles][reduce: kTinyThreads][staged operands:
 // stage_doubles][kTinyBatch TinyNode][dig_max TinyDigit]
@@ -103,6 +102,7 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
   TinyNode* bn = (TinyNode*)(stg + stage_doubles);
   TinyDigit* bd = (TinyDigit*)(bn + kTinyBatch);
   __shared__ int dA[kTinyBatch][kTinyMaxSum], dB[kTinyBatch][kTinyMaxSum];
+  __shared__ int hA[kTinyBatch][kTinyMaxSum], hB[kTinyBatch][kTinyMaxSum];
   pdl_launch();
   pdl_wait();
   const TinyGroup G = groups[blockIdx.x];
@@ -129,23 +129,33 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
       for (int e = lane; e < n; e += 32) stg[st + e] = g[e];
     }
     // dim-2 nodes: 2^lw lanes split each output's sum; lane r takes the
-    // terms whose low lw summed bits equal r.  Stepping the high bits q ->
-    // q+1 flips q's low ones to 0 and bit t = ctz(~q) to 1, so the operand
-    // offsets move by stride_{lw+t} - sum_{i<t} stride_{lw+i}.
+    // terms whose low lw summed bits equal r.  Stepping a counter q -> q+1
+    // flips q's low ones to 0 and bit t = ctz(q+1) to 1, so an offset moves by
+    // stride_t - sum_{i<t} stride_i: dA/dB for the summed bits above lw, hA/hB
+    // for the output bits above the (kTinyThreadsLog - lw) a thread fixes.
     if (tid < cnt && bn[tid].pow2) {
       const TinyNode& t = bn[tid];
-      const TinyDigit* S = bd + (t.dig - dig0) + t.nc;
+      const TinyDigit* D = bd + (t.dig - dig0);
       int pa = 0, pb = 0;
       for (int j = t.lw; j < t.ns && j - t.lw < kTinyMaxSum; ++j) {
-        dA[tid][j - t.lw] = S[j].sa - pa;
-        dB[tid][j - t.lw] = S[j].sb - pb;
-        pa += S[j].sa;
-        pb += S[j].sb;
+        dA[tid][j - t.lw] = D[t.nc + j].sa - pa;
+        dB[tid][j - t.lw] = D[t.nc + j].sb - pb;
+        pa += D[t.nc + j].sa;
+        pb += D[t.nc + j].sb;
+      }
+      pa = pb = 0;
+      for (int j = kTinyThreadsLog - t.lw; j < t.nc; ++j) {
+        const int k = j - (kTinyThreadsLog - t.lw);
+        hA[tid][k] = D[j].sa - pa;
+        hB[tid][k] = D[j].sb - pb;
+        pa += D[j].sa;
+        pb += D[j].sb;
       }
     }
     __syncthreads();
     for (int i = 0; i < cnt; ++i) {
       const TinyNode& tn = bn[i];
+      if (i > 0 && tn.sync) __syncthreads();
       const TinyDigit* sd = bd + (tn.dig - dig0);
       const double* A = tn.sta >= 0 ? stg + tn.sta : (tn.ga ? tn.ga : sm + tn.sa);
       const double* B = tn.stb >= 0 ? stg + tn.stb : (tn.gb ? tn.gb : sm + tn.sb);
@@ -153,30 +163,40 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
       const int nc = tn.nc, ns = tn.ns;
       const TinyDigit* sdS = sd + nc;
       if (tn.pow2 && ns - tn.lw <= kTinyMaxSum) {
-        const int lw = tn.lw, W = 1 << lw;
-        const int r = lane & (W - 1);
+        // thread -> output c0 + k * 2^cl: the low cl output bits are fixed
+        // per thread, the high ones step through hA/hB
+        const int lw = tn.lw, W = 1 << lw, cl = kTinyThreadsLog - lw;
+        const int r = lane & (W - 1), c0 = tid >> lw;
         const unsigned mask = (W == 32 ? 0xffffffffu : ((1u << W) - 1u) << (lane & ~(W - 1)));
-        int ra = 0, rb = 0;
-        for (int j = 0; j < lw; ++j)
-          if ((r >> j) & 1) ra += sdS[j].sa, rb += sdS[j].sb;
-        const int nq = tn.s_size >> lw;
-        for (int c = tid >> lw; c < tn.c_size; c += (int)blockDim.x >> lw) {
-          int xa = ra, xb = rb;
-          for (int j = 0; j < nc; ++j)
-            if ((c >> j) & 1) xa += sd[j].sa, xb += sd[j].sb;
-          double acc0 = 0.0, acc1 = 0.0;
-          for (int q = 0; q < nq; ++q) {
-            if (q) {
-              const int t = __ffs(~(q - 1)) - 1;
-              xa += dA[i][t];
-              xb += dB[i][t];
+        if (c0 < tn.c_size) {
+          int xa = 0, xb = 0;
+          for (int j = 0; j < lw; ++j)
+            if ((r >> j) & 1) xa += sdS[j].sa, xb += sdS[j].sb;
+          for (int j = 0; j < cl && j < nc; ++j)
+            if ((c0 >> j) & 1) xa += sd[j].sa, xb += sd[j].sb;
+          const int nk = nc > cl ? 1 << (nc - cl) : 1;
+          const int nq = tn.s_size >> lw;
+          for (int k = 0; k < nk; ++k) {
+            if (k) {
+              const int t = __ffs(k) - 1;
+              xa += hA[i][t];
+              xb += hB[i][t];
             }
-            if (q & 1) acc1 = fma(A[xa], B[xb], acc1);
-            else acc0 = fma(A[xa], B[xb], acc0);
+            int ya = xa, yb = xb;
+            double acc0 = 0.0, acc1 = 0.0;
+            for (int q = 0; q < nq; ++q) {
+              if (q) {
+                const int t = __ffs(q) - 1;
+                ya += dA[i][t];
+                yb += dB[i][t];
+              }
+              if (q & 1) acc1 = fma(A[ya], B[yb], acc1);
+              else acc0 = fma(A[ya], B[yb], acc0);
+            }
+            double acc = acc0 + acc1;
+            for (int o = W >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(mask, acc, o);
+            if (r == 0) C[c0 + (k << cl)] = acc;
           }
-          double acc = acc0 + acc1;
-          for (int o = W >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(mask, acc, o);
-          if (r == 0) C[c] = acc;
         }
       } else if (tn.c_size * 4 >= (int)blockDim.x || tn.s_size < 64) {
         for (int c = tid; c < tn.c_size; c += blockDim.x) {
@@ -249,7 +269,6 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
           __syncthreads();
         }
       }
-      __syncthreads();
     }
   }
 }
@@ -764,6 +783,168 @@ __global__ void k_generic(const GenericParams p) {
     }
     p.C[c] = acc;
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// K2s: a chain segment (program.h "chain segments").  One CTA per outer
+// assignment at a time: gather the input tile, run the steps smem -> smem,
+// scatter the output tile.  A step is k_stream's contraction on the tile: a
+// thread owns one kept assignment x (and a share of the new variables f),
+// holds its 2^ns input values in registers and forms each output as
+// sum_s a[s] * P[s, f] in ascending s from 0.0 -- k_stream's exact order, so
+// a segment computes the same bits as its steps launched one by one.
+constexpr int kSegThreadsLog = 8;
+constexpr int kSegThreads = 1 << kSegThreadsLog;
+
+// one segment step for one thread (NS summed digits): k_stream's per-x work
+template <int NS>
+__device__ __forceinline__ void seg_step(const double* X, double* Y, const double* B, int la, int lb, int lc, int fg,
+                                         int gb, int FV, int nxh, const int* oxA, const int* oxB, const int* oxC,
+                                         const int* osA, const int* osB, const int* ofB, const int* ofC) {
+  constexpr int SV = 1 << NS;
+  for (int h = 0; h < nxh; ++h) {
+    const int ya = la + oxA[h], yb = lb + oxB[h], yc = lc + oxC[h];
+    double a[SV];
+#pragma unroll
+    for (int s = 0; s < SV; ++s) a[s] = X[ya + osA[s]];
+#pragma unroll 2
+    for (int i = 0; i < FV; ++i) {
+      const int f = fg + (i << gb);
+      const double* Pf = B + yb + ofB[f];
+      double acc = 0.0;
+#pragma unroll
+      for (int s = 0; s < SV; ++s) acc = fma(a[s], Pf[osB[s]], acc);
+      Y[yc + ofC[f]] = acc;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSegThreads, 4) k_seg(const SegParams p) {
+  extern __shared__ double sm[];
+  double* const buf0 = sm;
+  double* const buf1 = sm + p.tile_doubles;
+  __shared__ SegStep ss[kSegMaxSteps];
+  __shared__ SegDigit dg[kSegMaxSteps][kSegMaxDig];
+  // per step, offsets of: kept digits above the 8 a thread fixes (A, P, C),
+  // summed assignments (A, P), new assignments (P, C)
+  __shared__ int oxA[kSegMaxSteps][16], oxB[kSegMaxSteps][16], oxC[kSegMaxSteps][16];
+  __shared__ int osA[kSegMaxSteps][16], osB[kSegMaxSteps][16];
+  __shared__ int ofB[kSegMaxSteps][32], ofC[kSegMaxSteps][32];
+  __shared__ int lxA[kSegMaxSteps][32], lxB[kSegMaxSteps][32], lxC[kSegMaxSteps][32];  // kept bits 0-3, 4-7
+  __shared__ int64_t gh[16], sh[16];
+  int64_t* const otab = (int64_t*)(sm + 2 * p.tile_doubles);  // outer strides, staged  // gather / scatter offsets of tile bits >= 8
+  __shared__ int64_t obase[2 + kSegMaxSteps];
+  const int tid = threadIdx.x;
+  const int n = p.nsteps;
+  for (int k = tid; k < n; k += blockDim.x) ss[k] = p.steps[k];
+  __syncthreads();
+  for (int q = tid; q < n * kSegMaxDig; q += blockDim.x) {
+    const int k = q / kSegMaxDig, j = q % kSegMaxDig;
+    if (j < ss[k].nx + ss[k].nf + ss[k].ns) dg[k][j] = p.digs[ss[k].dig + j];
+  }
+  __syncthreads();
+  for (int q = tid; q < n * 32; q += blockDim.x) {
+    const int k = q >> 5, e = q & 31;
+    const SegStep& t = ss[k];
+    const SegDigit* D = dg[k];
+    const int xl = min(t.nx, kSegThreadsLog);
+    if (e < 16) {
+      int a = 0, b = 0, c = 0;
+      for (int j = 0; j < 4; ++j)
+        if (((e >> j) & 1) && xl + j < t.nx) a += D[xl + j].sa, b += D[xl + j].sb, c += D[xl + j].sc;
+      oxA[k][e] = a, oxB[k][e] = b, oxC[k][e] = c;
+      a = b = 0;
+      for (int j = 0; j < t.ns; ++j)
+        if ((e >> j) & 1) a += D[t.nx + t.nf + j].sa, b += D[t.nx + t.nf + j].sb;
+      osA[k][e] = a, osB[k][e] = b;
+    }
+    int b = 0, c = 0;
+    for (int j = 0; j < t.nf; ++j)
+      if ((e >> j) & 1) b += D[t.nx + j].sb, c += D[t.nx + j].sc;
+    ofB[k][e] = b, ofC[k][e] = c;
+    {
+      const int j0 = (e >> 4) * 4;  // e < 16: bits 0-3, else bits 4-7 (of the xl a thread fixes)
+      int a2 = 0, b2 = 0, c2 = 0;
+      for (int j = 0; j < 4; ++j)
+        if (((e >> j) & 1) && j0 + j < xl) a2 += D[j0 + j].sa, b2 += D[j0 + j].sb, c2 += D[j0 + j].sc;
+      lxA[k][e] = a2, lxB[k][e] = b2, lxC[k][e] = c2;
+    }
+  }
+  for (int q = tid; q < p.nouter * (2 + n); q += blockDim.x) otab[q] = p.otab[q];
+  double* const pstage = (double*)(otab + p.nouter * (2 + n));  // outer-independent small operands
+  if (tid < 32) {
+    const int e = tid & 15;
+    const int64_t* T = p.gtab + (tid < 16 ? 0 : p.nt0);
+    const int nt = tid < 16 ? p.nt0 : p.ntL;
+    int64_t o = 0;
+    for (int j = 0; j < 4; ++j)
+      if (((e >> j) & 1) && kSegThreadsLog + j < nt) o += T[kSegThreadsLog + j];
+    (tid < 16 ? gh : sh)[e] = o;
+  }
+  // this thread's tile entries e = tid + k * 2^8: low-bit offsets once
+  int64_t lo_g = 0, lo_s = 0;
+  for (int j = 0; j < kSegThreadsLog; ++j)
+    if ((tid >> j) & 1) {
+      if (j < p.nt0) lo_g += p.gtab[j];
+      if (j < p.ntL) lo_s += p.gtab[p.nt0 + j];
+    }
+  const int n0 = 1 << p.nt0, nL = 1 << p.ntL;
+  const int nk0 = p.nt0 > kSegThreadsLog ? 1 << (p.nt0 - kSegThreadsLog) : 1;
+  const int nkL = p.ntL > kSegThreadsLog ? 1 << (p.ntL - kSegThreadsLog) : 1;
+  const int ncol = 2 + n;
+  pdl_wait();  // operands are produced by earlier launches
+  for (int k = 0; k < n; ++k)  // (ordered before use by the block loop's first barrier)
+    if (ss[k].pst >= 0)
+      for (int q = tid; q < ss[k].pn; q += blockDim.x) pstage[ss[k].pst + q] = __ldg(ss[k].P + q);
+  const int64_t nblocks = (int64_t)1 << p.nouter;
+  for (int64_t o = blockIdx.x; o < nblocks; o += gridDim.x) {
+    if (tid < ncol) {
+      int64_t acc = 0;
+      for (int b = 0; b < p.nouter; ++b)
+        if ((o >> b) & 1) acc += otab[b * ncol + tid];
+      obase[tid] = acc;
+    }
+    __syncthreads();  // also: the previous block's scatter is done with the tiles
+    if (tid < n0) {
+      const double* Ab = p.A + obase[0] + lo_g;
+#pragma unroll 4
+      for (int k = 0; k < nk0; ++k) buf0[tid + (k << kSegThreadsLog)] = __ldcs(Ab + gh[k]);
+    }
+    __syncthreads();
+    double* X = buf0;
+    double* Y = buf1;
+    for (int k = 0; k < n; ++k) {
+      const SegStep& t = ss[k];
+      // thread -> (low kept bits, group of new assignments)
+      const int xl = min(t.nx, kSegThreadsLog);
+      const int gb = min(t.nf, kSegThreadsLog - xl);
+      if ((tid >> (xl + gb)) == 0) {
+        const int xlo = tid & ((1 << xl) - 1), fg = tid >> xl;
+        const int e0 = xlo & 15, e1 = 16 + (xlo >> 4);
+        const int la = lxA[k][e0] + lxA[k][e1], lb = lxB[k][e0] + lxB[k][e1], lc = lxC[k][e0] + lxC[k][e1];
+        const double* B = t.pst >= 0 ? pstage + t.pst : t.P + obase[2 + k];
+        const int FV = 1 << (t.nf - gb), nxh = 1 << (t.nx - xl);
+        switch (t.ns) {
+          case 0: seg_step<0>(X, Y, B, la, lb, lc, fg, gb, FV, nxh, oxA[k], oxB[k], oxC[k], osA[k], osB[k], ofB[k], ofC[k]); break;
+          case 1: seg_step<1>(X, Y, B, la, lb, lc, fg, gb, FV, nxh, oxA[k], oxB[k], oxC[k], osA[k], osB[k], ofB[k], ofC[k]); break;
+          case 2: seg_step<2>(X, Y, B, la, lb, lc, fg, gb, FV, nxh, oxA[k], oxB[k], oxC[k], osA[k], osB[k], ofB[k], ofC[k]); break;
+          case 3: seg_step<3>(X, Y, B, la, lb, lc, fg, gb, FV, nxh, oxA[k], oxB[k], oxC[k], osA[k], osB[k], ofB[k], ofC[k]); break;
+          default: seg_step<4>(X, Y, B, la, lb, lc, fg, gb, FV, nxh, oxA[k], oxB[k], oxC[k], osA[k], osB[k], ofB[k], ofC[k]); break;
+        }
+      }
+      __syncthreads();
+      double* tt = X;
+      X = Y;
+      Y = tt;
+    }
+    if (tid < nL) {
+      double* Cb = p.C + obase[1] + lo_s;
+#pragma unroll 4
+      for (int k = 0; k < nkL; ++k) __stcs(Cb + sh[k], X[tid + (k << kSegThreadsLog)]);
+    }
+  }
+  pdl_launch();
 }
 
 }  // namespace tc

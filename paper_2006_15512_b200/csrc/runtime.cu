@@ -215,6 +215,7 @@ struct Launch {
   int kind = 0, slot = -1;
   bool coop = false;  // cooperative launch (k_stream_seq: grid barriers)
   double bytes = 0, flops = 0;
+  int xbits = -1, ns = 0, nf = 0, ns2 = -1, nf2 = -1;  // stream shape (diagnostics)
   std::vector<char> blob;
   std::vector<size_t> off;
   std::vector<void*> ptrs;
@@ -251,6 +252,9 @@ struct tc_exec {
   TinyDigit* tdigs = nullptr;
   TinyGroup* tgroups = nullptr;
   GDigit* gdig = nullptr;
+  SegStep* dseg = nullptr;      // chain segments: step descriptors, digits, tables
+  SegDigit* dsegdig = nullptr;
+  int64_t* dsegtab = nullptr;
   int64_t* rootmap = nullptr;
   double** results_slot = nullptr;  // device copy of `results` read by k_rootcopy
   StreamParams* seq_params = nullptr;  // k_stream_seq step descriptors
@@ -274,7 +278,7 @@ struct tc_exec {
     if (graph) cudaGraphDestroy(graph);
     if (stream) cudaStreamSynchronize(stream);
     for (void* q : {(void*)arena, (void*)leafbuf, (void*)slicedbuf, (void*)tnodes, (void*)tdigs,
-                    (void*)tgroups, (void*)gdig, (void*)rootmap, (void*)results_slot, (void*)seq_params, (void*)seq_keys, (void*)sel, (void*)selt, (void*)eta, (void*)results,
+                    (void*)tgroups, (void*)gdig, (void*)dseg, (void*)dsegdig, (void*)dsegtab, (void*)rootmap, (void*)results_slot, (void*)seq_params, (void*)seq_keys, (void*)sel, (void*)selt, (void*)eta, (void*)results,
                     (void*)folded})
       dcache().put(device, q);
     if (stream) cudaStreamDestroy(stream);
@@ -336,6 +340,19 @@ struct tc_exec {
                            cudaMemcpyHostToDevice, stream));
       CU(cudaMemcpyAsync(tgroups, g.tiny_groups.data(), g.tiny_groups.size() * sizeof(TinyGroup),
                          cudaMemcpyHostToDevice, stream));
+    }
+    if (!g.seg_steps.empty()) {
+      std::vector<SegStep> ss = g.seg_steps;
+      for (size_t i = 0; i < ss.size(); ++i) ss[i].P = ptr(g.seg_P[i]);
+      dseg = dalloc<SegStep>(ss.size(), dev_bytes, device);
+      dsegdig = dalloc<SegDigit>(g.seg_digits.size(), dev_bytes, device);
+      dsegtab = dalloc<int64_t>(std::max<size_t>(1, g.seg_tab.size()), dev_bytes, device);
+      CU(cudaMemcpyAsync(dseg, ss.data(), ss.size() * sizeof(SegStep), cudaMemcpyHostToDevice, stream));
+      CU(cudaMemcpyAsync(dsegdig, g.seg_digits.data(), g.seg_digits.size() * sizeof(SegDigit),
+                         cudaMemcpyHostToDevice, stream));
+      if (!g.seg_tab.empty())
+        CU(cudaMemcpyAsync(dsegtab, g.seg_tab.data(), g.seg_tab.size() * 8, cudaMemcpyHostToDevice, stream));
+      CU(cudaFuncSetAttribute(k_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * g.seg_tile_max * 8 + 64 * (2 + kSegMaxSteps) * 8 + kSegPStageMax * 8));
     }
     if (!g.gdigits.empty()) {
       gdig = dalloc<GDigit>(g.gdigits.size(), dev_bytes, device);
@@ -401,8 +418,31 @@ struct tc_exec {
             int g = 0;
             while (g < chunks_log && (2 << g) <= sm_count(device) * 4) ++g;
             L.grid = dim3(1u << g);
+            L.xbits = xb, L.ns = st.ns, L.nf = st.nf;
           }
           L.arg(sp);
+          break;
+        }
+        case ST_SEG: {
+          SegParams sg = st.sg;
+          sg.A = ptr(st.la);
+          sg.C = (double*)ptr(st.lc);
+          sg.steps = dseg + st.seg_off;
+          sg.digs = dsegdig;
+          sg.otab = dsegtab + st.seg_tab_off;
+          sg.gtab = dsegtab + st.seg_gtab_off;
+          L.func = (void*)k_seg;
+          L.block = dim3(kSegThreads);
+          L.smem = (2 * sg.tile_doubles + sg.nouter * (2 + sg.nsteps) + sg.pst_doubles) * 8;
+          {
+            static thread_local std::map<int, int> occ;  // smem bytes -> resident CTAs per SM
+            int& o = occ[(int)L.smem];
+            if (o == 0) CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_seg, kSegThreads, L.smem));
+            const int64_t cap = (int64_t)sm_count(device) * std::max(1, o);
+            L.grid = dim3((unsigned)std::min<int64_t>(st.work, cap));
+          }
+          L.xbits = sg.nouter, L.ns = sg.nsteps, L.nf = sg.tile_doubles;
+          L.arg(sg);
           break;
         }
         case ST_GEMM: {
@@ -639,6 +679,7 @@ struct tc_exec {
         int gg = 0;
         while (gg < chunks_log && (2 << gg) <= sm_count(device) * 4) ++gg;
         L.grid = dim3(1u << gg);
+        L.xbits = pp.ybits, L.ns = s1.ns, L.nf = s1.nf, L.ns2 = s2.ns, L.nf2 = s2.nf;
         // executed bytes: A, P1, P2 and C2 (C1 never touches memory)
         const StreamParams sp1 = bound(i);
         const double c1_bytes = 8.0 * (double)sp1.nx * (double)(1 << s1.nf);
@@ -870,6 +911,12 @@ struct tc_exec {
     CU(cudaGetLastError());
     ms.resize(launches.size());
     for (size_t i = 0; i < launches.size(); ++i) CU(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
+    if (std::getenv("TC_PROFILE_DEBUG"))
+      for (size_t i = 0; i < launches.size(); ++i) {
+        const Launch& L = launches[i];
+        std::fprintf(stderr, "[launch] %zu kind=%d grid=%u block=%u ms=%.4f MB=%.2f xbits=%d ns=%d nf=%d ns2=%d nf2=%d\n", i,
+                     L.kind, L.grid.x * L.grid.y, L.block.x, ms[i], L.bytes / 1e6, L.xbits, L.ns, L.nf, L.ns2, L.nf2);
+      }
     for (auto& e : ev) cudaEventDestroy(e);
     last_n = 1;
   }

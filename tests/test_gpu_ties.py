@@ -187,10 +187,7 @@ def test_absurd_slice_counts_raise_instead_of_crashing():
         sliced_execute(n, t, slice_indices=bonds)
 
 
-def test_chain_link_fusion_is_bitwise_identical():
-    """k_stream_pair computes each fused chain link with the operations and
-    order of the two separate steps: the counts are bit-identical to a run
-    with fusion disabled (TC_FUSE=0, read once per process -> subprocess)."""
+def _run_plans_subprocess(env_over):
     import subprocess
     import sys
 
@@ -203,12 +200,87 @@ def test_chain_link_fusion_is_bitwise_identical():
             "    n, t = planfile.to_objects(f)\n"
             "    r = sliced_execute(n, t)\n"
             "    print(name, float(np.asarray(r.result.values)).hex(), r.stats['gpu_launches'])\n") % (root, root)
-    out = {}
-    for fuse in ("1", "0"):
-        env = dict(os.environ, TC_FUSE=fuse)
-        res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-        assert res.returncode == 0, res.stderr[-2000:]
-        out[fuse] = {ln.split()[0]: ln.split()[1:] for ln in res.stdout.strip().splitlines()}
+    env = dict(os.environ, **env_over)
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    return {ln.split()[0]: (float.fromhex(ln.split()[1]), int(ln.split()[2])) for ln in res.stdout.strip().splitlines()}
+
+
+def test_chain_link_fusion_is_bitwise_identical():
+    """k_stream_pair computes each fused chain link with the operations and
+    order of the two separate steps: the counts are bit-identical to a run
+    with fusion disabled (TC_FUSE=0, read once per process -> subprocess).
+    Chain segments are off here (TC_SEG=0) so that every link is a pair
+    candidate."""
+    on = _run_plans_subprocess({"TC_FUSE": "1", "TC_SEG": "0"})
+    off = _run_plans_subprocess({"TC_FUSE": "0", "TC_SEG": "0"})
     for name in ("c1a", "c2", "c1b"):
-        assert out["1"][name][0] == out["0"][name][0], name  # same bits
-    assert int(out["1"]["c2"][1]) < int(out["0"]["c2"][1])  # fewer launches when fused
+        assert on[name][0] == off[name][0], name  # same bits
+    assert on["c2"][1] < off["c2"][1]  # fewer launches when fused
+
+
+def test_chain_segments_match_step_by_step():
+    """k_seg runs a chain of stream steps smem -> smem in one launch with
+    k_stream's operation order: the counts are bit-identical to the
+    step-by-step execution (TC_SEG=0, TC_FUSE=0), and the launch count drops."""
+    seg = _run_plans_subprocess({"TC_SEG": "1"})
+    ref = _run_plans_subprocess({"TC_SEG": "0", "TC_FUSE": "0"})
+    for name in ("c1a", "c2", "c1b"):
+        assert seg[name][0] == ref[name][0], name
+    assert seg["c2"][1] < ref["c2"][1] // 2
+
+
+def _chain_network(seed):
+    """A rank-17 tensor contracted in turn with 14 small pieces (summing 1-2
+    of its indices, adding 0-2 new ones; some pieces are weighted deltas,
+    whose ties make later steps batch steps)."""
+    rng = np.random.default_rng(100 + seed)
+    pyr = random.Random(200 + seed)
+    cur = [Index(("b", i), 2) for i in range(17)]
+    big = Tensor(tuple(cur), rng.uniform(-1, 1, [2] * 17))
+    tree = leaf(big)
+    tensors = [big]
+    fresh = 0
+    for step in range(14):
+        summed = pyr.sample(cur, pyr.choice([1, 1, 2]))
+        new = [Index(("n", fresh + j), 2) for j in range(pyr.choice([0, 1, 1, 2]) if len(cur) > 15 else pyr.choice([1, 2]))]
+        fresh += len(new)
+        kept = [ix for ix in cur if ix not in summed]
+        inds = summed + new
+        if pyr.random() < 0.3 and len(inds) >= 2:
+            piece = _delta(inds, (rng.uniform(0.2, 1), rng.uniform(0.2, 1)))
+        else:
+            piece = Tensor(tuple(inds), rng.uniform(-1, 1, [2] * len(inds)))
+        tensors.append(piece)
+        tree = join(tree, leaf(piece)) if pyr.random() < 0.5 else join(leaf(piece), tree)
+        cur = kept + new
+    return TensorNetwork(tuple(tensors)), tree
+
+
+def _check_chain(seed):
+    n, tree = _chain_network(seed)
+    out, got = _run(n, tree)
+    want = _einsum(n, out.result.indices)
+    assert got.shape == want.shape
+    assert np.allclose(got, want, rtol=1e-11, atol=1e-11)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_stream_chains(seed):
+    """Stream-kernel chains (k_stream, fused pairs) against a dense einsum."""
+    _check_chain(seed)
+
+
+def test_stream_chains_through_segments():
+    """The same chains through k_seg (TC_SEG=1, read once per process)."""
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = ("import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+            "import test_gpu_ties as T\n"
+            "for seed in range(6): T._check_chain(seed)\n"
+            "print('ok')\n") % (os.path.join(here, ".."), here)
+    res = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, TC_SEG="1"), capture_output=True,
+                         text=True, timeout=600)
+    assert res.returncode == 0 and res.stdout.strip().endswith("ok"), res.stderr[-3000:]
