@@ -1197,6 +1197,36 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
           glevel[gi] = std::max(glevel[gi], glevel[group_of[c]] + 1);
     nlevels = std::max(nlevels, glevel[gi] + 1);
   }
+  // Level 0 splits into launches by when the chain first needs each group
+  // (the consumer's position in emission order): the graph starts the
+  // early-needed groups first and runs the rest beside the stream chain.
+  int nbuckets = groups.empty() ? 0 : 1;
+  if (!groups.empty() && !std::getenv("TC_TINY_ONE")) {
+    std::vector<int> ord_nt(S, -1);
+    int cnt2 = 0;
+    for (int k = 0; k < p.NN; ++k)
+      if (g.cls[p.NL + k] != NC_TINY && g.cls[p.NL + k] != NC_ALIAS) ord_nt[p.NL + k] = cnt2++;
+    int n0 = 0;
+    for (size_t gi = 0; gi < groups.size(); ++gi) n0 += glevel[gi] == 0;
+    if (n0 >= 8 && cnt2 >= 16) {
+      std::vector<int> bkt(groups.size(), 0);
+      int used[4] = {0, 0, 0, 0};
+      for (size_t gi = 0; gi < groups.size(); ++gi) {
+        if (glevel[gi] != 0) continue;
+        int par = p.parent[groups[gi].back()];
+        while (par >= 0 && g.cls[par] == NC_ALIAS) par = p.parent[par];
+        const int c = par >= 0 ? ord_nt[par] : -1;
+        const int b = c < cnt2 / 8 ? 0 : c < cnt2 / 4 ? 1 : c < cnt2 / 2 ? 2 : 3;
+        bkt[gi] = b;
+        used[b] = 1;
+      }
+      int remap[4], nb = 0;
+      for (int b = 0; b < 4; ++b) remap[b] = used[b] ? nb++ : -1;
+      for (size_t gi = 0; gi < groups.size(); ++gi) glevel[gi] = glevel[gi] == 0 ? remap[bkt[gi]] : glevel[gi] + nb - 1;
+      nlevels += nb - 1;
+      nbuckets = nb;
+    }
+  }
   if (std::getenv("TC_TINY_DEBUG")) {
     std::vector<size_t> sz;
     for (auto& gr : groups) sz.push_back(gr.size());
@@ -1206,6 +1236,26 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       int64_t w = 0;
       for (int v : gr) w += size[v];
       work_max = std::max(work_max, w), work_sum += w;
+    }
+    {
+      std::vector<int> ord_nt(S, -1);
+      int cnt2 = 0;
+      for (int k = 0; k < p.NN; ++k)
+        if (g.cls[p.NL + k] != NC_TINY && g.cls[p.NL + k] != NC_ALIAS) ord_nt[p.NL + k] = cnt2++;
+      std::vector<std::pair<int64_t, int>> gc;
+      for (size_t gi = 0; gi < groups.size(); ++gi) {
+        int64_t w = 0;
+        for (int v : groups[gi]) w += size[v] + 32;
+        gc.push_back({w, (int)gi});
+      }
+      std::sort(gc.rbegin(), gc.rend());
+      std::fprintf(stderr, "tiny heavy groups (cost, consumer ordinal of %d):", cnt2);
+      for (size_t q = 0; q < gc.size() && q < 24; ++q) {
+        int par = p.parent[groups[gc[q].second].back()];
+        while (par >= 0 && g.cls[par] == NC_ALIAS) par = p.parent[par];
+        std::fprintf(stderr, " (%lld,%d)", (long long)gc[q].first, par >= 0 ? ord_nt[par] : -1);
+      }
+      std::fprintf(stderr, "\n");
     }
     std::fprintf(stderr, "tiny: %zu groups, %d levels, nodes top:", groups.size(), nlevels);
     for (size_t q = 0; q < sz.size() && q < 12; ++q) std::fprintf(stderr, " %zu", sz[q]);
@@ -1255,7 +1305,8 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     Step st;
     st.kind = ST_TINY;
     if (sel_step >= 0) st.deps.push_back(sel_step);
-    if (lv > 0) st.deps.push_back(tiny_step[lv - 1]);
+    if (lv >= nbuckets)  // a later level reads forced roots of any level-0 launch
+      for (int b = 0; b < lv; ++b) st.deps.push_back(tiny_step[b]);
     tiny_step[lv] = (int)g.steps.size();
     g.steps.push_back(st);
   }
