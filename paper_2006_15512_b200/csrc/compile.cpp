@@ -1480,22 +1480,33 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
             if (b < x.second && x.first < e) return true;
           return false;
         };
-        bool prev_red = false;
+        bool prev_red = false, epoch_w0 = true;
         for (int q2 = tg.beg; q2 < tg.end; ++q2) {
           TinyNode& t = out.nodes[q2];
           const int v = slot[q2];
           const bool red = tiny_uses_reduce(t);
+          // executed by warp 0 alone (its threads are the node's only active ones)
+          const bool w0 = !red && ((t.pow2 && t.ns - t.lw <= kTinyMaxSum) ? (t.c_size << t.lw) <= 32 : t.c_size <= 32);
           std::pair<int32_t, int32_t> rd[2];
           int nr = 0;
           if (out.ga[q2].kind == LOC_SMEM) rd[nr++] = {t.sa, t.sa + (int32_t)size[p.kid_l(v)]};
           if (out.gb[q2].kind == LOC_SMEM) rd[nr++] = {t.sb, t.sb + (int32_t)size[p.kid_r(v)]};
           const bool wr = v != r;
           const int32_t wb = t.sout, we = t.sout + (int32_t)size[v];
-          bool need = red || prev_red || (q2 - tg.beg) % kTinyBatch == 0;
+          const bool batch0 = (q2 - tg.beg) % kTinyBatch == 0;
+          bool need = red || prev_red || batch0;
           for (int k = 0; k < nr && !need; ++k) need = hit(ew, rd[k].first, rd[k].second);
           if (wr && !need) need = hit(ew, wb, we) || hit(er, wb, we);
-          if (need) ew.clear(), er.clear();
-          t.sync = need ? 1 : 0;
+          // a hazard among warp-0-only nodes needs only warp 0 to sync
+          // (__syncwarp orders its shared-memory accesses); the CTA epoch
+          // keeps running for the other warps
+          if (need && !red && !prev_red && !batch0 && w0 && epoch_w0) {
+            t.sync = 2;
+          } else {
+            if (need) ew.clear(), er.clear(), epoch_w0 = true;
+            t.sync = need ? 1 : 0;
+          }
+          epoch_w0 = epoch_w0 && w0;
           for (int k = 0; k < nr; ++k) er.push_back(rd[k]);
           if (wr) ew.push_back({wb, we});
           prev_red = red;

@@ -155,7 +155,10 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
     __syncthreads();
     for (int i = 0; i < cnt; ++i) {
       const TinyNode& tn = bn[i];
-      if (i > 0 && tn.sync) __syncthreads();
+      if (i > 0 && tn.sync) {
+        if (tn.sync == 1) __syncthreads();
+        else if (warp == 0) __syncwarp();  // hazard among warp-0-only nodes
+      }
       const TinyDigit* sd = bd + (tn.dig - dig0);
       const double* A = tn.sta >= 0 ? stg + tn.sta : (tn.ga ? tn.ga : sm + tn.sa);
       const double* B = tn.stb >= 0 ? stg + tn.stb : (tn.gb ? tn.gb : sm + tn.sb);
@@ -318,16 +321,6 @@ __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, in
     lo_p[u] = staged ? (int64_t)(tp + ((u & 1) ? p.bitP[8] : 0) + ((u & 2) ? p.bitP[9] : 0)) * SVFV
                      : tpo + ((u & 1) ? p.bitPo[8] : 0) + ((u & 2) ? p.bitPo[9] : 0);
   }
-  if (staged) {
-    for (int q = tid; q < (SVFV << p.nbt); q += blockDim.x) {
-      const int bi = q / SVFV;
-      int64_t off = p.offP[q % SVFV];
-      for (int t = 0; t < p.nbt; ++t)
-        if ((bi >> t) & 1) off += p.bt_poff[t];
-      Ps[q] = p.P[off];
-    }
-    __syncthreads();
-  }
   // this CTA's fixed chunk bits
   int64_t ha = 0, hc = 0, hp = 0;
   {
@@ -339,6 +332,28 @@ __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, in
       hc += p.bitC[j];
       hp += staged ? (int64_t)p.bitP[j] * SVFV : p.bitPo[j];
     }
+  }
+  // the first chunk's big-operand loads are issued before the small operand
+  // is staged: the two global round trips overlap
+  // (small summed shapes only: the early live range costs registers)
+  constexpr bool kHoist = NS <= 2;
+  const bool full = p.nx >= (1 << CB);
+  double a[kStreamUnroll][SV];
+  if (kHoist && full) {
+#pragma unroll
+    for (int u = 0; u < kStreamUnroll; ++u)
+#pragma unroll
+      for (int s = 0; s < SV; ++s) a[u][s] = __ldcs(p.A + ha + lo_a[u] + p.offA[s]);
+  }
+  if (staged) {
+    for (int q = tid; q < (SVFV << p.nbt); q += blockDim.x) {
+      const int bi = q / SVFV;
+      int64_t off = p.offP[q % SVFV];
+      for (int t = 0; t < p.nbt; ++t)
+        if ((bi >> t) & 1) off += p.bt_poff[t];
+      Ps[q] = p.P[off];
+    }
+    __syncthreads();
   }
   const double* Pbase = staged ? Ps : p.P;
   auto pv = [&](const double* Pu, int q) { return staged ? Pu[q] : __ldg(Pu + p.offP[q]); };
@@ -354,12 +369,13 @@ __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, in
     const double* Ab = p.A + ha;
     double* Cb = p.C + hc;
     const double* Pc = Pbase + hp;
-    if (p.nx >= (1 << CB)) {
-      double a[kStreamUnroll][SV];
+    if (full) {
+      if (!kHoist || i > 0) {
 #pragma unroll
-      for (int u = 0; u < kStreamUnroll; ++u)
+        for (int u = 0; u < kStreamUnroll; ++u)
 #pragma unroll
-        for (int s = 0; s < SV; ++s) a[u][s] = __ldcs(Ab + lo_a[u] + p.offA[s]);
+          for (int s = 0; s < SV; ++s) a[u][s] = __ldcs(Ab + lo_a[u] + p.offA[s]);
+      }
 #pragma unroll
       for (int u = 0; u < kStreamUnroll; ++u) {
         const double* Pu = Pc + lo_p[u];

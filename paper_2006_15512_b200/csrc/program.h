@@ -153,7 +153,7 @@ struct TinyNode {
   int32_t sta, stb;  // staging offsets of small global operands within the batch (-1: read global)
   int32_t na, nb;    // entry counts of the staged operands
   int32_t lw;        // dim-2 nodes: 2^lw lanes share one output's sum (<= 32)
-  int32_t sync;      // CTA barrier before this node (it reads / overwrites smem a node since the last barrier touched)
+  int32_t sync;      // before this node: 1 CTA barrier, 2 warp-0 barrier (it reads / overwrites smem touched since)
   int32_t pad_;
 };
 // k_tiny processes a group in batches of kTinyBatch nodes: descriptors,

@@ -846,10 +846,28 @@ struct tc_exec {
     CU(cudaGraphCreate(&graph, 0));
     std::vector<cudaGraphNode_t> nodes(launches.size());
     kernels_per_slice = 0;
+    // TC_PDL_EDGES=1|2 (experimental): data edges become programmatic edges
+    // (1: dependent launches when every primary CTA triggered, 2: when every
+    // primary CTA started); every kernel waits (griddepcontrol.wait) before
+    // touching its operands
+    static const int pdl_edges = std::getenv("TC_PDL_EDGES") ? std::atoi(std::getenv("TC_PDL_EDGES")) : 0;
     for (size_t si = 0; si < launches.size(); ++si) {
       std::vector<cudaGraphNode_t> deps;
       for (int d : ldeps[si]) deps.push_back(nodes[d]);
       cudaKernelNodeParams kp = launches[si].params();
+      if (pdl_edges && !launches[si].coop && !deps.empty()) {
+        CU(cudaGraphAddKernelNode(&nodes[si], graph, nullptr, 0, &kp));
+        std::vector<cudaGraphEdgeData> ed(deps.size());
+        for (auto& e : ed) {
+          e = cudaGraphEdgeData{};
+          e.from_port = pdl_edges == 2 ? cudaGraphKernelNodePortLaunchCompletion : cudaGraphKernelNodePortProgrammatic;
+          e.type = cudaGraphDependencyTypeProgrammatic;
+        }
+        std::vector<cudaGraphNode_t> to(deps.size(), nodes[si]);
+        CU(cudaGraphAddDependencies_v2(graph, deps.data(), to.data(), ed.data(), deps.size()));
+        ++kernels_per_slice;
+        continue;
+      }
       CU(cudaGraphAddKernelNode(&nodes[si], graph, deps.data(), deps.size(), &kp));
       if (launches[si].coop) {
         cudaLaunchAttributeValue v{};
