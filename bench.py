@@ -290,9 +290,11 @@ def traffic_for(config, kernel):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
-    d = json.load(open(p))
-    e = d.get(config, {}).get(kernel)
-    return None if e is None else e.get("dram_bytes_per_slice")
+    d = json.load(open(p)).get(config, {})
+    # a launch class can span kernel families (stream: k_stream + fused k_stream_pair)
+    fams = {"k_stream": ("k_stream", "k_stream_pair", "k_stream_seq")}.get(kernel, (kernel,))
+    vals = [d[f]["dram_bytes_per_slice"] for f in fams if f in d and "dram_bytes_per_slice" in d[f]]
+    return sum(vals) if vals else None
 
 
 # ---------------------------------------------------------------- reference
