@@ -224,9 +224,19 @@ BitRuns make_runs(const std::vector<std::pair<int, int>>& bits) {  // (src bit, 
 
 // Split [0, n) into up to 8 contiguous ranges (at least `grain` items each)
 // run on worker threads; f(lo, hi) must not throw.
+// worker threads for the host compile (TC_COMPILE_THREADS, default 8)
+int compile_threads() {
+  static const int t = [] {
+    const char* e = std::getenv("TC_COMPILE_THREADS");
+    const int v = e ? std::atoi(e) : 8;
+    return std::max(1, std::min(64, v));
+  }();
+  return t;
+}
+
 template <class F>
 void parallel_for(int n, int grain, F f) {
-  const int T = std::max(1, std::min(8, n / std::max(1, grain)));
+  const int T = std::max(1, std::min(compile_threads(), n / std::max(1, grain)));
   if (T == 1) {
     f(0, n);
     return;
@@ -697,7 +707,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         for (int k = r - p.NL - cnt[r] + 1; k <= r - p.NL; ++k) in_task[k] = 1;
         task_nodes += cnt[r];
       }
-      const int T = (int)std::max<int64_t>(1, std::min<int64_t>(8, task_nodes / 1024));
+      const int T = (int)std::max<int64_t>(1, std::min<int64_t>(compile_threads(), task_nodes / 1024));
       std::vector<int> cut{0};
       {
         int64_t acc = 0;
@@ -1544,7 +1554,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     // split the group order into ranges of about equal node counts
     int64_t total = 0;
     for (int gi : gorder) total += (int64_t)groups[gi].size();
-    static const int tmax = std::getenv("TC_TINY_THREADS") ? std::atoi(std::getenv("TC_TINY_THREADS")) : 2;
+    static const int tmax = std::getenv("TC_TINY_THREADS") ? std::atoi(std::getenv("TC_TINY_THREADS")) : 4;
     const int T = (int)std::max<int64_t>(1, std::min<int64_t>(tmax, total / 2048));
     std::vector<int> cut{0};
     int64_t acc = 0;

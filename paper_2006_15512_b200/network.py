@@ -44,7 +44,7 @@ class TensorNetwork:
         return self._bond
 
 
-@dataclass(frozen=True, eq=False)
+@dataclass(frozen=True, eq=False, slots=True)
 class ContractionTree:
     tensor: object = None
     left: "ContractionTree | None" = None

@@ -55,7 +55,7 @@ class Assignment(dict):
                 raise BindingOutOfDomain(f"{v} outside domain of {ix.id!r}")
 
 
-@dataclass(frozen=True, eq=False)
+@dataclass(frozen=True, eq=False, slots=True)
 class Tensor:
     indices: tuple
     values: np.ndarray = field(repr=False)
