@@ -90,6 +90,50 @@ __global__ void k_fold(const double* results, int64_t R, int64_t n, double* out)
 // K4: one CTA walks one tiny subtree in postorder; intermediates live in smem.
 constexpr int kTinyThreads = 1 << kTinyThreadsLog;
 
+// one dim-2 tiny node (k_tiny): thread -> output c0 + k * 2^cl, the low cl
+// output bits fixed per thread, the high ones and the summed bits above lw
+// stepping through carry tables.  Operands and output never overlap (the
+// group's smem allocator frees a node's children after placing its output).
+__device__ __forceinline__ void tiny_pow2(const double* __restrict__ A, const double* __restrict__ B,
+                                          double* __restrict__ C, const TinyNode& tn, const TinyDigit* sd,
+                                          const int* dAr, const int* dBr, const int* hAr, const int* hBr, int tid,
+                                          int lane) {
+  const int nc = tn.nc;
+  const TinyDigit* sdS = sd + nc;
+  const int lw = tn.lw, W = 1 << lw, cl = kTinyThreadsLog - lw;
+  const int r = lane & (W - 1), c0 = tid >> lw;
+  const unsigned mask = (W == 32 ? 0xffffffffu : ((1u << W) - 1u) << (lane & ~(W - 1)));
+  if (c0 >= tn.c_size) return;
+  int xa = 0, xb = 0;
+  for (int j = 0; j < lw; ++j)
+    if ((r >> j) & 1) xa += sdS[j].sa, xb += sdS[j].sb;
+  for (int j = 0; j < cl && j < nc; ++j)
+    if ((c0 >> j) & 1) xa += sd[j].sa, xb += sd[j].sb;
+  const int nk = nc > cl ? 1 << (nc - cl) : 1;
+  const int nq = tn.s_size >> lw;
+  for (int k = 0; k < nk; ++k) {
+    if (k) {
+      const int t = __ffs(k) - 1;
+      xa += hAr[t];
+      xb += hBr[t];
+    }
+    int ya = xa, yb = xb;
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int q = 0; q < nq; ++q) {
+      if (q) {
+        const int t = __ffs(q) - 1;
+        ya += dAr[t];
+        yb += dBr[t];
+      }
+      if (q & 1) acc1 = fma(A[ya], B[yb], acc1);
+      else acc0 = fma(A[ya], B[yb], acc0);
+    }
+    double acc = acc0 + acc1;
+    for (int o = W >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(mask, acc, o);
+    if (r == 0) C[c0 + (k << cl)] = acc;
+  }
+}
+
 // smem: [intermediates: smem_doubles][reduce: kTinyThreads][staged operands:
 // stage_doubles][kTinyBatch TinyNode][dig_max TinyDigit]
 __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restrict__ nodes,
@@ -166,41 +210,7 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
       const int nc = tn.nc, ns = tn.ns;
       const TinyDigit* sdS = sd + nc;
       if (tn.pow2 && ns - tn.lw <= kTinyMaxSum) {
-        // thread -> output c0 + k * 2^cl: the low cl output bits are fixed
-        // per thread, the high ones step through hA/hB
-        const int lw = tn.lw, W = 1 << lw, cl = kTinyThreadsLog - lw;
-        const int r = lane & (W - 1), c0 = tid >> lw;
-        const unsigned mask = (W == 32 ? 0xffffffffu : ((1u << W) - 1u) << (lane & ~(W - 1)));
-        if (c0 < tn.c_size) {
-          int xa = 0, xb = 0;
-          for (int j = 0; j < lw; ++j)
-            if ((r >> j) & 1) xa += sdS[j].sa, xb += sdS[j].sb;
-          for (int j = 0; j < cl && j < nc; ++j)
-            if ((c0 >> j) & 1) xa += sd[j].sa, xb += sd[j].sb;
-          const int nk = nc > cl ? 1 << (nc - cl) : 1;
-          const int nq = tn.s_size >> lw;
-          for (int k = 0; k < nk; ++k) {
-            if (k) {
-              const int t = __ffs(k) - 1;
-              xa += hA[i][t];
-              xb += hB[i][t];
-            }
-            int ya = xa, yb = xb;
-            double acc0 = 0.0, acc1 = 0.0;
-            for (int q = 0; q < nq; ++q) {
-              if (q) {
-                const int t = __ffs(q) - 1;
-                ya += dA[i][t];
-                yb += dB[i][t];
-              }
-              if (q & 1) acc1 = fma(A[ya], B[yb], acc1);
-              else acc0 = fma(A[ya], B[yb], acc0);
-            }
-            double acc = acc0 + acc1;
-            for (int o = W >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(mask, acc, o);
-            if (r == 0) C[c0 + (k << cl)] = acc;
-          }
-        }
+        tiny_pow2(A, B, C, tn, sd, dA[i], dB[i], hA[i], hB[i], tid, lane);
       } else if (tn.c_size * 4 >= (int)blockDim.x || tn.s_size < 64) {
         for (int c = tid; c < tn.c_size; c += blockDim.x) {
           int oa = 0, ob = 0;
@@ -296,9 +306,17 @@ __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, in
   const int tid = threadIdx.x;
   const int xb = 63 - __clzll((long long)p.nx);  // nx is a power of two
   const int cl = max(0, xb - CB);
-  const int g = min(logG, cl);
-  if (b >= (1 << g)) return;
-  const int kchunk = cl - g;
+  int kchunk, cb = b, u0 = -1;
+  if (p.split_u) {  // one quarter of one chunk per CTA
+    cb = b >> 2;
+    u0 = b & 3;
+    if (cb >= (1 << cl)) return;
+    kchunk = 0;
+  } else {
+    const int g = min(logG, cl);
+    if (b >= (1 << g)) return;
+    kchunk = cl - g;
+  }
   const bool staged = p.stage_all;
   // x = chunk * 2^CB + u * 256 + tid.  Every address is a sum of per-bit
   // table entries: the thread's low parts once, the CTA's chunk bits once,
@@ -324,7 +342,7 @@ __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, in
   // this CTA's fixed chunk bits
   int64_t ha = 0, hc = 0, hp = 0;
   {
-    uint64_t m = (uint64_t)b << (kchunk + CB);
+    uint64_t m = (uint64_t)cb << (kchunk + CB);
     while (m) {
       const int j = __ffsll((long long)m) - 1;
       m &= m - 1;
@@ -342,8 +360,9 @@ __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, in
   if (kHoist && full) {
 #pragma unroll
     for (int u = 0; u < kStreamUnroll; ++u)
+      if (u0 < 0 || u == u0)
 #pragma unroll
-      for (int s = 0; s < SV; ++s) a[u][s] = __ldcs(p.A + ha + lo_a[u] + p.offA[s]);
+        for (int s = 0; s < SV; ++s) a[u][s] = __ldcs(p.A + ha + lo_a[u] + p.offA[s]);
   }
   if (staged) {
     for (int q = tid; q < (SVFV << p.nbt); q += blockDim.x) {
@@ -373,11 +392,13 @@ __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, in
       if (!kHoist || i > 0) {
 #pragma unroll
         for (int u = 0; u < kStreamUnroll; ++u)
+          if (u0 < 0 || u == u0)
 #pragma unroll
-          for (int s = 0; s < SV; ++s) a[u][s] = __ldcs(Ab + lo_a[u] + p.offA[s]);
+            for (int s = 0; s < SV; ++s) a[u][s] = __ldcs(Ab + lo_a[u] + p.offA[s]);
       }
 #pragma unroll
       for (int u = 0; u < kStreamUnroll; ++u) {
+        if (u0 >= 0 && u != u0) continue;
         const double* Pu = Pc + lo_p[u];
         double* Cu = Cb + lo_c[u];
 #pragma unroll
@@ -390,7 +411,7 @@ __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, in
       }
     } else {  // a single partial chunk (nx < 2^CB)
       for (int u = 0; u < kStreamUnroll; ++u) {
-        if (u * kStreamThreads + tid >= p.nx) continue;
+        if (u * kStreamThreads + tid >= p.nx || (u0 >= 0 && u != u0)) continue;
         const double* Pu = Pc + lo_p[u];
         for (int f = 0; f < FV; ++f) {
           double acc = 0.0;
@@ -434,13 +455,21 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream_pair(const StreamPair
   }
   const int cl = max(0, p.ybits - CB);
   const int logG = 31 - __clz(gridDim.x);
-  const int g = min(logG, cl);
   const int b = blockIdx.x;
-  if (b >= (1 << g)) return;
-  const int kchunk = cl - g;
+  int kchunk, cb = b, u0 = -1;
+  if (p.split_u) {  // one quarter of one chunk per CTA
+    cb = b >> 2;
+    u0 = b & 3;
+    if (cb >= (1 << cl)) return;
+    kchunk = 0;
+  } else {
+    const int g = min(logG, cl);
+    if (b >= (1 << g)) return;
+    kchunk = cl - g;
+  }
   int64_t ha = 0, hc = 0, h1 = 0, h2 = 0;
   {
-    uint64_t m = (uint64_t)b << (kchunk + CB);
+    uint64_t m = (uint64_t)cb << (kchunk + CB);
     while (m) {
       const int j = __ffsll((long long)m) - 1;
       m &= m - 1;
@@ -457,7 +486,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream_pair(const StreamPair
     }
 #pragma unroll
     for (int u = 0; u < kStreamUnroll; ++u) {
-      if (ny < (1 << CB) && u * kStreamThreads + tid >= ny) continue;
+      if ((ny < (1 << CB) && u * kStreamThreads + tid >= ny) || (u0 >= 0 && u != u0)) continue;
       const double* Ab = p.A + ha + la[u];
       const double* P1b = p.P1 + h1 + l1[u];
       const double* P2b = p.P2 + h2 + l2[u];
@@ -815,7 +844,8 @@ constexpr int kSegThreads = 1 << kSegThreadsLog;
 
 // one segment step for one thread (NS summed digits): k_stream's per-x work
 template <int NS>
-__device__ __forceinline__ void seg_step(const double* X, double* Y, const double* B, int la, int lb, int lc, int fg,
+__device__ __forceinline__ void seg_step(const double* __restrict__ X, double* __restrict__ Y,
+                                         const double* __restrict__ B, int la, int lb, int lc, int fg,
                                          int gb, int FV, int nxh, const int* oxA, const int* oxB, const int* oxC,
                                          const int* osA, const int* osB, const int* ofB, const int* ofC) {
   constexpr int SV = 1 << NS;

@@ -77,6 +77,8 @@ struct StreamParams {
   int32_t bitP[kStreamXBits];
   int32_t stage_all;  // 1: the small operand ((SV*FV) << nbt <= kStreamStageMax entries) is staged
                       //    in smem once per CTA; 0: it is read through the L1 (direct)
+  int32_t split_u;    // 1: CTA b takes chunk b >> 2 and only its quarter u = b & 3 (small tensors:
+                      //    4x the CTAs, a quarter of the serial work per thread)
 };
 
 // ---- K2p: a chain link of two stream steps in registers ----------------------
@@ -106,6 +108,7 @@ struct StreamPairParams {
   int32_t nq;          // 2^NI
   int32_t nrest;       // 2^(NI - NS2)
   int32_t q_of[1 << kPairMaxInner];  // (s2 index, rest index) -> q : q_of[s2 * nrest + r]
+  int32_t split_u;                    // as StreamParams::split_u
 };
 
 // ---- K3: FP64 DMMA GEMM with bit-permuted operands (dim 2) -----------------

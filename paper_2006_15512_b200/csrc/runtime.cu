@@ -418,6 +418,10 @@ struct tc_exec {
             int g = 0;
             while (g < chunks_log && (2 << g) <= sm_count(device) * 4) ++g;
             L.grid = dim3(1u << g);
+            if ((1 << chunks_log) < sm_count(device) && split_u_on()) {  // few chunks: a quarter chunk per CTA
+              sp.split_u = 1;
+              L.grid = dim3(xb >= kStreamChunkBits ? 4u << chunks_log : (unsigned)((sp.nx + 255) / 256));
+            }
             L.xbits = xb, L.ns = st.ns, L.nf = st.nf;
           }
           L.arg(sp);
@@ -679,6 +683,10 @@ struct tc_exec {
         int gg = 0;
         while (gg < chunks_log && (2 << gg) <= sm_count(device) * 4) ++gg;
         L.grid = dim3(1u << gg);
+        if ((1 << chunks_log) < sm_count(device) && split_u_on()) {
+          pp.split_u = 1;
+          L.grid = dim3(pp.ybits >= kStreamChunkBits ? 4u << chunks_log : (unsigned)((((int64_t)1 << pp.ybits) + 255) / 256));
+        }
         L.xbits = pp.ybits, L.ns = s1.ns, L.nf = s1.nf, L.ns2 = s2.ns, L.nf2 = s2.nf;
         // executed bytes: A, P1, P2 and C2 (C1 never touches memory)
         const StreamParams sp1 = bound(i);
@@ -767,6 +775,7 @@ struct tc_exec {
         std::vector<int> dd;
         for (size_t k = r.first; k < r.second; ++k) {
           std::memcpy(&sp[pos], launches[k].blob.data() + launches[k].off[0], sizeof(StreamParams));
+          sp[pos].split_u = 0;  // the cooperative grid walks whole chunks
           keys[pos] = g.steps[k].ns * 8 + g.steps[k].nf;
           ++pos;
           L.bytes += launches[k].bytes;
@@ -882,6 +891,10 @@ struct tc_exec {
   double program_ms = 0, setup_ms = 0, graph_ms = 0;
 
   int rootcopy_launch = -1;
+  static bool split_u_on() {
+    static const bool on = !(std::getenv("TC_SPLIT_U") && std::atoi(std::getenv("TC_SPLIT_U")) == 0);
+    return on;
+  }
   static bool use_pdl() {
     static const bool on = [] {
       const char* e = std::getenv("TC_PDL");
