@@ -89,6 +89,7 @@ __global__ void k_fold(const double* results, int64_t R, int64_t n, double* out)
 // ---------------------------------------------------------------------------
 // K4: one CTA walks one tiny subtree in postorder; intermediates live in smem.
 constexpr int kTinyThreads = 1 << kTinyThreadsLog;
+__device__ long long* g_tiny_trace = nullptr;  // diagnostics: node start clocks of block 0 (TC_TINY_TRACE)
 
 // one dim-2 tiny node (k_tiny): thread -> output c0 + k * 2^cl, the low cl
 // output bits fixed per thread, the high ones and the summed bits above lw
@@ -105,10 +106,13 @@ __device__ __forceinline__ void tiny_pow2(const double* __restrict__ A, const do
   const unsigned mask = (W == 32 ? 0xffffffffu : ((1u << W) - 1u) << (lane & ~(W - 1)));
   if (c0 >= tn.c_size) return;
   int xa = 0, xb = 0;
-  for (int j = 0; j < lw; ++j)
-    if ((r >> j) & 1) xa += sdS[j].sa, xb += sdS[j].sb;
-  for (int j = 0; j < cl && j < nc; ++j)
-    if ((c0 >> j) & 1) xa += sd[j].sa, xb += sd[j].sb;
+  // fixed trip counts: every digit load issues at once (no dependent chain)
+#pragma unroll
+  for (int j = 0; j < 5; ++j)
+    if (j < lw && ((r >> j) & 1)) xa += sdS[j].sa, xb += sdS[j].sb;
+#pragma unroll
+  for (int j = 0; j < kTinyThreadsLog; ++j)
+    if (j < cl && j < nc && ((c0 >> j) & 1)) xa += sd[j].sa, xb += sd[j].sb;
   const int nk = nc > cl ? 1 << (nc - cl) : 1;
   const int nq = tn.s_size >> lw;
   for (int k = 0; k < nk; ++k) {
@@ -151,6 +155,7 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
   pdl_wait();
   const TinyGroup G = groups[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  long long* const trace = (blockIdx.x == 0 && tid == 0) ? g_tiny_trace : nullptr;
   for (int b0 = G.beg; b0 < G.end; b0 += kTinyBatch) {
     const int cnt = min(kTinyBatch, G.end - b0);
     __syncthreads();  // the previous batch is done with the staging buffers
@@ -199,6 +204,7 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
     __syncthreads();
     for (int i = 0; i < cnt; ++i) {
       const TinyNode& tn = bn[i];
+      if (trace) trace[b0 + i] = clock64();
       if (i > 0 && tn.sync) {
         if (tn.sync == 1) __syncthreads();
         else if (warp == 0) __syncwarp();  // hazard among warp-0-only nodes
@@ -284,6 +290,7 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
       }
     }
   }
+  if (trace) trace[G.end] = clock64();
 }
 
 // ---------------------------------------------------------------------------

@@ -929,6 +929,12 @@ struct tc_exec {
   void profile(int64_t slice, std::vector<float>& ms) {
     CU(cudaSetDevice(device));
     ensure_results(1);
+    long long* trace = nullptr;
+    if (std::getenv("TC_TINY_TRACE") && prog.n_tiny > 0) {
+      CU(cudaMalloc(&trace, (prog.n_tiny + 1) * sizeof(long long)));
+      CU(cudaMemset(trace, 0, (prog.n_tiny + 1) * sizeof(long long)));
+      CU(cudaMemcpyToSymbol(g_tiny_trace, &trace, sizeof(trace)));
+    }
     int64_t h[2] = {slice, slice};
     CU(cudaMemcpyAsync(eta, h, sizeof(h), cudaMemcpyHostToDevice, stream));
     std::vector<cudaEvent_t> ev(launches.size() + 1);
@@ -942,6 +948,20 @@ struct tc_exec {
     CU(cudaGetLastError());
     ms.resize(launches.size());
     for (size_t i = 0; i < launches.size(); ++i) CU(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
+    if (trace) {
+      std::vector<long long> t(prog.n_tiny + 1);
+      CU(cudaMemcpy(t.data(), trace, t.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+      long long* null = nullptr;
+      CU(cudaMemcpyToSymbol(g_tiny_trace, &null, sizeof(null)));
+      cudaFree(trace);
+      for (int i = 0; i < prog.n_tiny; ++i) {
+        if (!t[i] || !t[i + 1]) continue;
+        const TinyNode& n = prog.tiny_nodes[i];
+        std::fprintf(stderr, "[tiny] %d cyc=%lld c=%d s=%d nc=%d ns=%d lw=%d sync=%d g=%d%d%d st=%d%d pow2=%d\n", i,
+                     t[i + 1] - t[i], n.c_size, n.s_size, n.nc, n.ns, n.lw, n.sync, prog.tiny_ga[i].kind != LOC_SMEM,
+                     prog.tiny_gb[i].kind != LOC_SMEM, prog.tiny_gout[i].kind != LOC_SMEM, n.sta >= 0, n.stb >= 0, n.pow2);
+      }
+    }
     if (std::getenv("TC_PROFILE_DEBUG"))
       for (size_t i = 0; i < launches.size(); ++i) {
         const Launch& L = launches[i];
