@@ -158,24 +158,60 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
   long long* const trace = (blockIdx.x == 0 && tid == 0) ? g_tiny_trace : nullptr;
   for (int b0 = G.beg; b0 < G.end; b0 += kTinyBatch) {
     const int cnt = min(kTinyBatch, G.end - b0);
-    __syncthreads();  // the previous batch is done with the staging buffers
-    {
-      const int words = cnt * (int)(sizeof(TinyNode) / 4);
-      const int* src = (const int*)(nodes + b0);
-      for (int w = tid; w < words; w += blockDim.x) ((int*)bn)[w] = src[w];
-    }
+    // Batch prologue: every global load of a round is issued before any of
+    // its shared stores (fixed trip counts), so a round costs one round trip.
+    constexpr int kWords = kTinyBatch * (int)(sizeof(TinyNode) / 4);
+    constexpr int kWordIt = (kWords + kTinyThreads - 1) / kTinyThreads;
+    const int words = cnt * (int)(sizeof(TinyNode) / 4);
+    const int* src = (const int*)(nodes + b0);
+    int wv[kWordIt];
+#pragma unroll
+    for (int k = 0; k < kWordIt; ++k)
+      if (tid + k * kTinyThreads < words) wv[k] = src[tid + k * kTinyThreads];
     const int dig0 = nodes[b0].dig;
     const int dig1 = nodes[b0 + cnt - 1].dig + nodes[b0 + cnt - 1].nc + nodes[b0 + cnt - 1].ns;
-    for (int j = tid; j < dig1 - dig0; j += blockDim.x) bd[j] = digs[dig0 + j];
+    TinyDigit dv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (tid + k * kTinyThreads < dig1 - dig0) dv[k] = digs[dig0 + tid + k * kTinyThreads];
+    __syncthreads();  // the previous batch is done with the staging buffers
+#pragma unroll
+    for (int k = 0; k < kWordIt; ++k)
+      if (tid + k * kTinyThreads < words) ((int*)bn)[tid + k * kTinyThreads] = wv[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (tid + k * kTinyThreads < dig1 - dig0) bd[tid + k * kTinyThreads] = dv[k];
+    for (int j = tid + 4 * kTinyThreads; j < dig1 - dig0; j += blockDim.x) bd[j] = digs[dig0 + j];
     __syncthreads();
-    // small global operands: one warp per operand, lanes over entries
-    for (int o = warp; o < 2 * cnt; o += kTinyThreads / 32) {
-      const TinyNode& t = bn[o >> 1];
-      const int st = (o & 1) ? t.stb : t.sta;
-      if (st < 0) continue;
-      const double* g = (o & 1) ? t.gb : t.ga;
-      const int n = (o & 1) ? t.nb : t.na;
-      for (int e = lane; e < n; e += 32) stg[st + e] = g[e];
+    // small global operands (<= kTinyStageMax entries): warp w takes operands
+    // w, w + 8, ...; lanes over entries
+    {
+      constexpr int kOpIt = 2 * kTinyBatch / (kTinyThreads / 32);
+      constexpr int kEntIt = kTinyStageMax / 32;
+      double v[kOpIt][kEntIt];
+#pragma unroll
+      for (int k = 0; k < kOpIt; ++k) {
+        const int o = warp + k * (kTinyThreads / 32);
+        if (o >= 2 * cnt) continue;
+        const TinyNode& t = bn[o >> 1];
+        const int st = (o & 1) ? t.stb : t.sta;
+        const double* g = (o & 1) ? t.gb : t.ga;
+        const int n = (o & 1) ? t.nb : t.na;
+#pragma unroll
+        for (int e = 0; e < kEntIt; ++e)
+          if (st >= 0 && lane + 32 * e < n) v[k][e] = g[lane + 32 * e];
+      }
+#pragma unroll
+      for (int k = 0; k < kOpIt; ++k) {
+        const int o = warp + k * (kTinyThreads / 32);
+        if (o >= 2 * cnt) continue;
+        const TinyNode& t = bn[o >> 1];
+        const int st = (o & 1) ? t.stb : t.sta;
+        const int n = (o & 1) ? t.nb : t.na;
+#pragma unroll
+        for (int e = 0; e < kEntIt; ++e)
+          if (st >= 0 && lane + 32 * e < n) stg[st + lane + 32 * e] = v[k][e];
+      }
     }
     // dim-2 nodes: 2^lw lanes split each output's sum; lane r takes the
     // terms whose low lw summed bits equal r.  Stepping a counter q -> q+1
