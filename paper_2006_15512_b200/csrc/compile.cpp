@@ -1616,6 +1616,16 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       g.tiny_smem_doubles = std::max(g.tiny_smem_doubles, group_smem[gi]);
       producer[groups[gi].back()] = tiny_step[glevel[gi]];
     }
+    // resolve operand / output places for the kernel: sa / sb / sout become
+    // offsets from the start of dynamic smem (staged operands included), -1
+    // for a global operand or output (one select per operand on the device)
+    const int32_t stage0 = g.tiny_smem_doubles + (1 << kTinyThreadsLog);
+    for (size_t i = 0; i < g.tiny_nodes.size(); ++i) {
+      TinyNode& t = g.tiny_nodes[i];
+      t.sa = t.sta >= 0 ? stage0 + t.sta : (g.tiny_ga[i].kind == LOC_SMEM ? t.sa : -1);
+      t.sb = t.stb >= 0 ? stage0 + t.stb : (g.tiny_gb[i].kind == LOC_SMEM ? t.sb : -1);
+      t.sout = g.tiny_gout[i].kind == LOC_SMEM ? t.sout : -1;
+    }
   }
   // forced roots consumed inside a tiny level: release with that level as reader
   for (size_t gi = 0; gi < groups.size(); ++gi)

@@ -246,9 +246,9 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
         else if (warp == 0) __syncwarp();  // hazard among warp-0-only nodes
       }
       const TinyDigit* sd = bd + (tn.dig - dig0);
-      const double* A = tn.sta >= 0 ? stg + tn.sta : (tn.ga ? tn.ga : sm + tn.sa);
-      const double* B = tn.stb >= 0 ? stg + tn.stb : (tn.gb ? tn.gb : sm + tn.sb);
-      double* C = tn.gout ? tn.gout : sm + tn.sout;
+      const double* A = tn.sa >= 0 ? sm + tn.sa : tn.ga;  // (compile.cpp resolves staged / smem / global)
+      const double* B = tn.sb >= 0 ? sm + tn.sb : tn.gb;
+      double* C = tn.sout >= 0 ? sm + tn.sout : tn.gout;
       const int nc = tn.nc, ns = tn.ns;
       const TinyDigit* sdS = sd + nc;
       if (tn.pow2 && ns - tn.lw <= kTinyMaxSum) {

@@ -148,7 +148,7 @@ struct TinyNode {
   const double* ga;  // global operand (leaf / forced root) or nullptr -> smem
   const double* gb;
   double* gout;      // global output (subtree root) or nullptr -> smem
-  int32_t sa, sb, sout;  // smem offsets in doubles
+  int32_t sa, sb, sout;  // smem offsets in doubles from the dynamic smem base (staged operands resolved), -1: global
   int32_t c_size, s_size;
   int32_t nc, ns;
   int32_t dig;   // first digit (nc C-digits then ns S-digits)
