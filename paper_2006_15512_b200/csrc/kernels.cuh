@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream_pair(const StreamPair
         double acc = 0.0;
 #pragma unroll
         for (int s = 0; s < SV1; ++s)
-          acc = fma(__ldcs(Ab + p.qA[q] + p.offA1[s]), __ldg(P1b + p.qP1[q] + p.offP1[s * FV1 + p.qF1[q]]), acc);
+          acc = fma(__ldg(Ab + p.qA[q] + p.offA1[s]), __ldg(P1b + p.qP1[q] + p.offP1[s * FV1 + p.qF1[q]]), acc);
         c1[q] = acc;
       }
       // step 2: every (rest, f2) output sums its SV2 inner combos in s2 order
