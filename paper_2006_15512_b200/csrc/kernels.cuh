@@ -405,7 +405,7 @@ __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, in
     for (int u = 0; u < kStreamUnroll; ++u)
       if (u0 < 0 || u == u0)
 #pragma unroll
-        for (int s = 0; s < SV; ++s) a[u][s] = __ldcs(p.A + ha + lo_a[u] + p.offA[s]);
+        for (int s = 0; s < SV; ++s) a[u][s] = __ldg(p.A + ha + lo_a[u] + p.offA[s]);
   }
   if (staged) {
     for (int q = tid; q < (SVFV << p.nbt); q += blockDim.x) {
@@ -437,7 +437,7 @@ __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, in
         for (int u = 0; u < kStreamUnroll; ++u)
           if (u0 < 0 || u == u0)
 #pragma unroll
-            for (int s = 0; s < SV; ++s) a[u][s] = __ldcs(Ab + lo_a[u] + p.offA[s]);
+            for (int s = 0; s < SV; ++s) a[u][s] = __ldg(Ab + lo_a[u] + p.offA[s]);
       }
 #pragma unroll
       for (int u = 0; u < kStreamUnroll; ++u) {
