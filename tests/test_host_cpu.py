@@ -281,3 +281,27 @@ def test_native_flatten_merges_equal_ids_in_first_appearance_order():
     _flat_equal(x, flatten_py(n, t))
     assert [q.id for q in x.indices] == [("a", 1), "j", "k", "free"]
     assert x.leaf_idx.tolist() == [0, 1, 1, 0, 2, 2, 3]
+
+
+def test_chain_segments_compile_on_cpu():
+    """The chain-segment compiler (TC_SEG=1, read once per process) folds the
+    C2 plan's stream chain into far fewer launches with the same reference
+    accounting and a smaller arena (compile only: no kernel runs)."""
+    import subprocess
+    import sys
+
+    code = ("import json, sys; sys.path.insert(0, %r)\n"
+            "from paper_2006_15512_b200 import _lib, planfile\n"
+            "f, _ = planfile.load(%r)\n"
+            "print(json.dumps(_lib.PlanHandle(f).compile_stats([])))\n") % (ROOT, os.path.join(PLANS, "c2.tcplan.npz"))
+    out = {}
+    for seg in ("0", "1"):
+        res = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, TC_SEG=seg), capture_output=True,
+                             text=True, timeout=300)
+        assert res.returncode == 0, res.stderr[-2000:]
+        out[seg] = json.loads(res.stdout.strip().splitlines()[-1])
+    assert out["1"]["gpu_launches"] * 3 < out["0"]["gpu_launches"]
+    assert out["1"]["n_stream_nodes"] == out["0"]["n_stream_nodes"]
+    assert out["1"]["mem_estimate"] == out["0"]["mem_estimate"]
+    assert out["1"]["peak_observed"] == out["0"]["peak_observed"]
+    assert out["1"]["device_peak_bytes"] <= out["0"]["device_peak_bytes"]
