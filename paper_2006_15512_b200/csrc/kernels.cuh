@@ -519,46 +519,61 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream_pair(const StreamPair
       ha += p.bitA[j], hc += p.bitC[j], h1 += p.bitP1[j], h2 += p.bitP2[j];
     }
   }
-  const int64_t ny = (int64_t)1 << p.ybits;
-  const int64_t nsteps = (int64_t)1 << kchunk;
-  for (int64_t i = 0; i < nsteps; ++i) {
-    if (i > 0) {
-      const int j = __ffsll((long long)i) - 1 + CB;
-      const int64_t sg = (((i ^ (i >> 1)) >> (j - CB)) & 1) ? 1 : -1;
-      ha += sg * p.bitA[j], hc += sg * p.bitC[j], h1 += sg * p.bitP1[j], h2 += sg * p.bitP2[j];
-    }
-#pragma unroll
-    for (int u = 0; u < kStreamUnroll; ++u) {
-      if ((ny < (1 << CB) && u * kStreamThreads + tid >= ny) || (u0 >= 0 && u != u0)) continue;
-      const double* Ab = p.A + ha + la[u];
-      const double* P1b = p.P1 + h1 + l1[u];
-      const double* P2b = p.P2 + h2 + l2[u];
-      double* Cb = p.C + hc + lc[u];
-      // step 1 for every inner combo (loads shared by combos with equal A offset)
-      double c1[NQ];
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        double acc = 0.0;
-#pragma unroll
-        for (int s = 0; s < SV1; ++s)
-          acc = fma(__ldg(Ab + p.qA[q] + p.offA1[s]), __ldg(P1b + p.qP1[q] + p.offP1[s * FV1 + p.qF1[q]]), acc);
-        c1[q] = acc;
+  // the chain walk, over global or smem-staged small operands (each call
+  // site inlines with its own address space)
+  auto walk = [&](const double* __restrict__ P1, const double* __restrict__ P2) {
+    const int64_t ny = (int64_t)1 << p.ybits;
+    const int64_t nsteps = (int64_t)1 << kchunk;
+    for (int64_t i = 0; i < nsteps; ++i) {
+      if (i > 0) {
+        const int j = __ffsll((long long)i) - 1 + CB;
+        const int64_t sg = (((i ^ (i >> 1)) >> (j - CB)) & 1) ? 1 : -1;
+        ha += sg * p.bitA[j], hc += sg * p.bitC[j], h1 += sg * p.bitP1[j], h2 += sg * p.bitP2[j];
       }
-      // step 2: every (rest, f2) output sums its SV2 inner combos in s2 order
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const int q0 = r << NS2;  // s2 = 0 combo of this rest (P2 batch / C2 offsets)
-#pragma unroll
-        for (int f = 0; f < FV2; ++f) {
+  #pragma unroll
+      for (int u = 0; u < kStreamUnroll; ++u) {
+        if ((ny < (1 << CB) && u * kStreamThreads + tid >= ny) || (u0 >= 0 && u != u0)) continue;
+        const double* Ab = p.A + ha + la[u];
+        const double* P1b = P1 + h1 + l1[u];
+        const double* P2b = P2 + h2 + l2[u];
+        double* Cb = p.C + hc + lc[u];
+        // step 1 for every inner combo (loads shared by combos with equal A offset)
+        double c1[NQ];
+  #pragma unroll
+        for (int q = 0; q < NQ; ++q) {
           double acc = 0.0;
-#pragma unroll
-          for (int s = 0; s < SV2; ++s) {
-            acc = fma(c1[s | (r << NS2)], __ldg(P2b + p.qP2[q0] + p.offP2[s * FV2 + f]), acc);
+  #pragma unroll
+          for (int s = 0; s < SV1; ++s)
+            acc = fma(__ldg(Ab + p.qA[q] + p.offA1[s]), P1b[p.qP1[q] + p.offP1[s * FV1 + p.qF1[q]]], acc);
+          c1[q] = acc;
+        }
+        // step 2: every (rest, f2) output sums its SV2 inner combos in s2 order
+  #pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          const int q0 = r << NS2;  // s2 = 0 combo of this rest (P2 batch / C2 offsets)
+  #pragma unroll
+          for (int f = 0; f < FV2; ++f) {
+            double acc = 0.0;
+  #pragma unroll
+            for (int s = 0; s < SV2; ++s) {
+              acc = fma(c1[s | (r << NS2)], P2b[p.qP2[q0] + p.offP2[s * FV2 + f]], acc);
+            }
+            Cb[p.qC[q0] + p.offC2[f]] = acc;
           }
-          Cb[p.qC[q0] + p.offC2[f]] = acc;
         }
       }
     }
+  };
+  // small operands staged in smem once per CTA (p.pstage): every FMA's
+  // operand then comes from a broadcast smem read instead of the L1
+  if (p.pstage) {
+    extern __shared__ double psm[];
+    for (int i = tid; i < p.p1n; i += blockDim.x) psm[i] = __ldg(p.P1 + i);
+    for (int i = tid; i < p.p2n; i += blockDim.x) psm[p.p1n + i] = __ldg(p.P2 + i);
+    __syncthreads();
+    walk(psm, psm + p.p1n);
+  } else {
+    walk(p.P1, p.P2);
   }
   pdl_launch();
 }

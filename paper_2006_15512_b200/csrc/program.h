@@ -109,7 +109,10 @@ struct StreamPairParams {
   int32_t nrest;       // 2^(NI - NS2)
   int32_t q_of[1 << kPairMaxInner];  // (s2 index, rest index) -> q : q_of[s2 * nrest + r]
   int32_t split_u;                    // as StreamParams::split_u
+  int32_t p1n, p2n;                   // small-operand entries
+  int32_t pstage;                     // 1: both small operands staged in smem (p1n + p2n <= kPairStageMax)
 };
+constexpr int kPairStageMax = 4096;
 
 // ---- K3: FP64 DMMA GEMM with bit-permuted operands (dim 2) -----------------
 // C[m, n] = sum_k A[m, k] B[k, n]. Tile bits (BM=2^6, BN=2^6, BK=2^4) are the

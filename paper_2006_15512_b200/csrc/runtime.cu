@@ -688,6 +688,13 @@ struct tc_exec {
           L.grid = dim3(pp.ybits >= kStreamChunkBits ? 4u << chunks_log : (unsigned)((((int64_t)1 << pp.ybits) + 255) / 256));
         }
         L.xbits = pp.ybits, L.ns = s1.ns, L.nf = s1.nf, L.ns2 = s2.ns, L.nf2 = s2.nf;
+        {
+          static const bool pst_on = !(std::getenv("TC_PAIR_STAGE") && std::atoi(std::getenv("TC_PAIR_STAGE")) == 0);
+          pp.p1n = (int32_t)(s1.lb_bytes / 8);
+          pp.p2n = (int32_t)(s2.lb_bytes / 8);
+          pp.pstage = pst_on && s1.lb_bytes > 0 && s2.lb_bytes > 0 && pp.p1n + pp.p2n <= kPairStageMax;
+          L.smem = pp.pstage ? (unsigned)(pp.p1n + pp.p2n) * 8 : 0;
+        }
         // executed bytes: A, P1, P2 and C2 (C1 never touches memory)
         const StreamParams sp1 = bound(i);
         const double c1_bytes = 8.0 * (double)sp1.nx * (double)(1 << s1.nf);
