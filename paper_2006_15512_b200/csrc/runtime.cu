@@ -418,7 +418,7 @@ struct tc_exec {
             int g = 0;
             while (g < chunks_log && (2 << g) <= sm_count(device) * 4) ++g;
             L.grid = dim3(1u << g);
-            if ((1 << chunks_log) < sm_count(device) && split_u_on()) {  // few chunks: a quarter chunk per CTA
+            if ((1 << chunks_log) < sm_count(device) * split_mult() && split_u_on()) {  // few chunks: a quarter chunk per CTA
               sp.split_u = 1;
               L.grid = dim3(xb >= kStreamChunkBits ? 4u << chunks_log : (unsigned)((sp.nx + 255) / 256));
             }
@@ -683,7 +683,7 @@ struct tc_exec {
         int gg = 0;
         while (gg < chunks_log && (2 << gg) <= sm_count(device) * 4) ++gg;
         L.grid = dim3(1u << gg);
-        if ((1 << chunks_log) < sm_count(device) && split_u_on()) {
+        if ((1 << chunks_log) < sm_count(device) * split_mult() && split_u_on()) {
           pp.split_u = 1;
           L.grid = dim3(pp.ybits >= kStreamChunkBits ? 4u << chunks_log : (unsigned)((((int64_t)1 << pp.ybits) + 255) / 256));
         }
@@ -898,6 +898,10 @@ struct tc_exec {
   double program_ms = 0, setup_ms = 0, graph_ms = 0;
 
   int rootcopy_launch = -1;
+  static int split_mult() {
+    static const int m = std::getenv("TC_SPLIT_MULT") ? std::max(1, std::atoi(std::getenv("TC_SPLIT_MULT"))) : 1;
+    return m;
+  }
   static bool split_u_on() {
     static const bool on = !(std::getenv("TC_SPLIT_U") && std::atoi(std::getenv("TC_SPLIT_U")) == 0);
     return on;
