@@ -991,7 +991,8 @@ struct tc_exec {
       return 0.0;
     }
     ensure_results(n);
-    const bool eager = !gexec && n * repeats <= 2;
+    static const bool oneshot_graph = std::getenv("TC_ONESHOT_GRAPH") && std::atoi(std::getenv("TC_ONESHOT_GRAPH")) == 1;
+    const bool eager = !gexec && n * repeats <= 2 && !oneshot_graph;
     if (!eager) ensure_graph();
     int64_t h[2] = {b, b};
     cudaEvent_t e0, e1;
