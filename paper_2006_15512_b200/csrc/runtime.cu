@@ -683,7 +683,8 @@ struct tc_exec {
         int gg = 0;
         while (gg < chunks_log && (2 << gg) <= sm_count(device) * 4) ++gg;
         L.grid = dim3(1u << gg);
-        if ((1 << chunks_log) < sm_count(device) * split_mult() && split_u_on()) {
+        static const int pair_mult = std::getenv("TC_SPLIT_MULT_PAIR") ? std::max(1, std::atoi(std::getenv("TC_SPLIT_MULT_PAIR"))) : split_mult();
+        if ((1 << chunks_log) < sm_count(device) * pair_mult && split_u_on()) {
           pp.split_u = 1;
           L.grid = dim3(pp.ybits >= kStreamChunkBits ? 4u << chunks_log : (unsigned)((((int64_t)1 << pp.ybits) + 255) / 256));
         }
