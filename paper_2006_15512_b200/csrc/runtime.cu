@@ -416,7 +416,7 @@ struct tc_exec {
             const int xb = 63 - __builtin_clzll((unsigned long long)sp.nx);  // nx is a power of two
             const int chunks_log = std::max(0, xb - kStreamChunkBits);
             int g = 0;
-            while (g < chunks_log && (2 << g) <= sm_count(device) * 4) ++g;
+            while (g < chunks_log && (2 << g) <= sm_count(device) * grid_mult(chunks_log)) ++g;
             L.grid = dim3(1u << g);
             if ((1 << chunks_log) < sm_count(device) * split_mult() && split_u_on()) {  // few chunks: a quarter chunk per CTA
               sp.split_u = 1;
@@ -681,7 +681,7 @@ struct tc_exec {
         L.block = dim3(kStreamThreads);
         const int chunks_log = std::max(0, pp.ybits - kStreamChunkBits);
         int gg = 0;
-        while (gg < chunks_log && (2 << gg) <= sm_count(device) * 4) ++gg;
+        while (gg < chunks_log && (2 << gg) <= sm_count(device) * grid_mult(chunks_log)) ++gg;
         L.grid = dim3(1u << gg);
         static const int pair_mult = std::getenv("TC_SPLIT_MULT_PAIR") ? std::max(1, std::atoi(std::getenv("TC_SPLIT_MULT_PAIR"))) : split_mult();
         if ((1 << chunks_log) < sm_count(device) * pair_mult && split_u_on()) {
@@ -899,6 +899,14 @@ struct tc_exec {
   double program_ms = 0, setup_ms = 0, graph_ms = 0;
 
   int rootcopy_launch = -1;
+  // stream grids: up to this many CTAs per SM, each walking >= 1 chunk.  Large
+  // launches (>= 2^12 chunks, 32 MB per operand) want more CTAs in flight (C4
+  // -7%, C1b -16%); the small ones of C2 lose ~2% with them (measured).
+  static int grid_mult(int chunks_log) {
+    static const int m = std::getenv("TC_STREAM_GRID_MULT") ? std::max(1, std::atoi(std::getenv("TC_STREAM_GRID_MULT"))) : 0;
+    if (m) return m;
+    return chunks_log >= 12 ? 16 : 4;
+  }
   static int split_mult() {
     static const int m = std::getenv("TC_SPLIT_MULT") ? std::max(1, std::atoi(std::getenv("TC_SPLIT_MULT"))) : 1;
     return m;
