@@ -900,12 +900,12 @@ struct tc_exec {
 
   int rootcopy_launch = -1;
   // stream grids: up to this many CTAs per SM, each walking >= 1 chunk.  Large
-  // launches (>= 2^12 chunks, 32 MB per operand) want more CTAs in flight (C4
+  // launches (>= 2^12 chunks, 32 MB per operand) want more CTAs in flight (32: C4
   // -7%, C1b -16%); the small ones of C2 lose ~2% with them (measured).
   static int grid_mult(int chunks_log) {
     static const int m = std::getenv("TC_STREAM_GRID_MULT") ? std::max(1, std::atoi(std::getenv("TC_STREAM_GRID_MULT"))) : 0;
     if (m) return m;
-    return chunks_log >= 12 ? 16 : 4;
+    return chunks_log >= 12 ? 32 : 4;
   }
   static int split_mult() {
     static const int m = std::getenv("TC_SPLIT_MULT") ? std::max(1, std::atoi(std::getenv("TC_SPLIT_MULT"))) : 1;
