@@ -905,7 +905,8 @@ struct tc_exec {
   static int grid_mult(int chunks_log) {
     static const int m = std::getenv("TC_STREAM_GRID_MULT") ? std::max(1, std::atoi(std::getenv("TC_STREAM_GRID_MULT"))) : 0;
     if (m) return m;
-    return chunks_log >= 12 ? 32 : 4;
+    static const int mid = std::getenv("TC_STREAM_GRID_MID") ? std::max(1, std::atoi(std::getenv("TC_STREAM_GRID_MID"))) : 4;
+    return chunks_log >= 12 ? 32 : chunks_log >= 10 ? mid : 4;
   }
   static int split_mult() {
     static const int m = std::getenv("TC_SPLIT_MULT") ? std::max(1, std::atoi(std::getenv("TC_SPLIT_MULT"))) : 1;
