@@ -22,6 +22,7 @@ import importlib
 from . import errors as own_errors
 from . import network as own_network
 from . import slicing as own_slicing
+from . import tensor as own_tensor
 
 _SAVED = {}
 
@@ -34,13 +35,16 @@ def _translate(ref_errors):
     return mapping
 
 
-def install(tensorcount=None, devices=None):
-    """Patch ``tensorcount.{driver,slicing,network}`` to use libtc."""
+def install(tensorcount=None, devices=None, contract_pair=False):
+    """Patch ``tensorcount.{driver,slicing,network}`` to use libtc.  With
+    ``contract_pair=True`` also ``tensorcount.tensor.contract_pair``
+    (tensor.py:96-108) — the reference's own test suite imports it directly."""
     if tensorcount is None:
         tensorcount = importlib.import_module("tensorcount")
     driver = importlib.import_module(tensorcount.__name__ + ".driver")
     slicing = importlib.import_module(tensorcount.__name__ + ".slicing")
     network = importlib.import_module(tensorcount.__name__ + ".network")
+    tensor = importlib.import_module(tensorcount.__name__ + ".tensor")
     ref_errors = importlib.import_module(tensorcount.__name__ + ".errors")
     emap = _translate(ref_errors)
     RefSE = slicing.SlicedExecution
@@ -75,6 +79,13 @@ def install(tensorcount=None, devices=None):
         (tensorcount, "sliced_execute"): wrap(sliced_execute, to_ref),
         (tensorcount, "execute"): wrap(execute),
     }
+    if contract_pair:
+        dev = (devices or [0])[0]
+
+        def contract_pair_gpu(a, b):
+            return own_tensor.contract_pair(a, b, device=dev)
+
+        patched[(tensor, "contract_pair")] = wrap(contract_pair_gpu)
     for (mod, name), fn in patched.items():
         _SAVED.setdefault((mod, name), getattr(mod, name))
         setattr(mod, name, fn)

@@ -10,6 +10,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+collect_ignore = ["reference_suite"]  # run in isolated subprocesses (test_gpu_reference_suite.py)
+
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 PLANS = os.path.join(ROOT, "data", "plans")
 
