@@ -104,6 +104,15 @@ typedef struct tc_stats {
   double graph_ms;               /*   CUDA graph build + instantiate          */
   tc_u128 phys_bytes;            /* per slice: executed bytes over physical (tied) variables */
   tc_u128 phys_flops;            /* per slice: executed flops over physical variables        */
+  /* slice-invariant hoisting (sliced runs): nodes with no sliced leaf below
+   * them run once per pass over the slices, not once per slice as in the
+   * reference's loop (slicing.py:139-145).  Per pass the device executes
+   * phys_*_hoisted + num_slices_run * (phys_* - phys_*_hoisted).            */
+  tc_u128 phys_bytes_hoisted;    /* of phys_bytes: executed once per pass     */
+  tc_u128 phys_flops_hoisted;
+  int64_t launches_prologue;     /* kernels launched once per pass            */
+  int64_t launches_per_slice;    /* kernels launched per slice                */
+  int64_t pinned_bytes;          /* arena prefix holding hoisted tensors      */
 } tc_stats;
 
 /* ---- symbolic plan (host) ---------------------------------------------- */
@@ -189,6 +198,16 @@ int tc_exec_fetch(tc_exec* ex, double* per_slice, double* folded);
 int tc_exec_profile(tc_exec* ex, int64_t slice, float* step_ms, int32_t* step_kind, int32_t* step_slot,
                     double* step_bytes, double* step_flops, int32_t cap, int32_t* n);
 
+/* Per-launch device time in graph mode (the bench's roofline): the prologue
+ * and per-slice CUDA graphs instrumented with an event-record node before and
+ * after every kernel node, one pass over slices [slice_begin, slice_end) with a
+ * synchronize after each graph launch.  launch_ms[i] = launch i's time summed
+ * over the pass (slice-invariant launches once); launch_inv[i] = 1 for those;
+ * *pass_ms = summed graph times of the pass.  Any pointer may be NULL. */
+int tc_exec_profile_graph(tc_exec* ex, int64_t slice_begin, int64_t slice_end, float* launch_ms,
+                          int32_t* launch_kind, int32_t* launch_inv, double* launch_bytes, double* launch_flops,
+                          int32_t cap, int32_t* n, float* pass_ms);
+
 /* Diagnostics: the launch DAG in CSR form (dep_off[n+1], deps[...]; launch
  * i depends on deps[dep_off[i] .. dep_off[i+1])).  *n = launches, *m = edges. */
 int tc_exec_deps(const tc_exec* ex, int32_t* dep_off, int32_t* deps, int32_t cap, int32_t* n, int32_t* m);
@@ -205,6 +224,13 @@ int tc_sliced_execute(const tc_plan* plan, int64_t mem_budget, const int32_t* sl
                       double* out_val, int64_t out_cap, int32_t* out_idx, int32_t idx_cap,
                       int32_t* out_rank, int32_t* chosen, int32_t chosen_cap,
                       int32_t* n_chosen, tc_stats* stats);
+
+/* Return the device's cached (currently unused) HBM blocks to the driver.
+ * libtc keeps freed program buffers in a per-device cache across calls (a
+ * multi-GB cudaMalloc/cudaFree pair costs 10-100 ms); a process that shares
+ * the GPU with other allocators (PyTorch, ...) calls this after a large run.
+ * device < 0: every device. */
+int tc_release_cache(int32_t device);
 
 const char* tc_last_error(void);
 int32_t tc_version(void);

@@ -82,6 +82,11 @@ class Stats(C.Structure):
         ("graph_ms", C.c_double),
         ("phys_bytes", U128),
         ("phys_flops", U128),
+        ("phys_bytes_hoisted", U128),
+        ("phys_flops_hoisted", U128),
+        ("launches_prologue", C.c_int64),
+        ("launches_per_slice", C.c_int64),
+        ("pinned_bytes", C.c_int64),
     ]
 
     def as_dict(self):
@@ -106,6 +111,11 @@ class Stats(C.Structure):
             graph_ms=float(self.graph_ms),
             phys_bytes=self.phys_bytes.value(),
             phys_flops=self.phys_flops.value(),
+            phys_bytes_hoisted=self.phys_bytes_hoisted.value(),
+            phys_flops_hoisted=self.phys_flops_hoisted.value(),
+            launches_prologue=int(self.launches_prologue),
+            launches_per_slice=int(self.launches_per_slice),
+            pinned_bytes=int(self.pinned_bytes),
         )
 
 
@@ -130,6 +140,8 @@ SIGNATURES = {
     "tc_exec_fetch": (C.c_int, [C.c_void_p, F64P, F64P]),
     "tc_exec_profile": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_float), I32P, I32P, F64P, F64P,
                                   C.c_int32, I32P]),
+    "tc_exec_profile_graph": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(C.c_float), I32P, I32P, F64P,
+                                        F64P, C.c_int32, I32P, C.POINTER(C.c_float)]),
     "tc_exec_result_size": (C.c_int64, [C.c_void_p]),
     "tc_exec_deps": (C.c_int, [C.c_void_p, I32P, I32P, C.c_int32, I32P, I32P]),
     "tc_sliced_execute": (
@@ -137,6 +149,7 @@ SIGNATURES = {
         [C.c_void_p, C.c_int64, I32P, C.c_int32, I32P, C.c_int32, F64P, C.c_int64, I32P, C.c_int32,
          I32P, I32P, C.c_int32, I32P, C.POINTER(Stats)],
     ),
+    "tc_release_cache": (C.c_int, [C.c_int32]),
     "tc_last_error": (C.c_char_p, []),
     "tc_version": (C.c_int32, []),
     "tc_device_count": (C.c_int32, []),
@@ -354,6 +367,24 @@ class Exec:
         return [dict(kind=self.KINDS[kind[i]], slot=int(slot[i]), ms=float(ms[i]), bytes=float(by[i]),
                      flops=float(fl[i])) for i in range(k)]
 
+    def profile_graph(self, begin: int, end: int):
+        """Per-launch graph-mode time over one pass of slices [begin, end):
+        (list of dict(kind, inv, ms, bytes, flops), summed pass ms)."""
+        cap = 1 << 20
+        ms = np.zeros(cap, dtype=np.float32)
+        kind = np.zeros(cap, dtype=np.int32)
+        inv = np.zeros(cap, dtype=np.int32)
+        by = np.zeros(cap, dtype=np.float64)
+        fl = np.zeros(cap, dtype=np.float64)
+        n = C.c_int32()
+        pm = C.c_float()
+        check(lib().tc_exec_profile_graph(self.h, int(begin), int(end), ms.ctypes.data_as(C.POINTER(C.c_float)),
+                                          _p(kind, I32P), _p(inv, I32P), _p(by, F64P), _p(fl, F64P), cap,
+                                          C.byref(n), C.byref(pm)))
+        k = n.value
+        return [dict(kind=self.KINDS[kind[i]], inv=bool(inv[i]), ms=float(ms[i]), bytes=float(by[i]),
+                     flops=float(fl[i])) for i in range(k)], float(pm.value)
+
     def deps(self):
         """Launch DAG: list of dependency lists (diagnostics)."""
         cap = 1 << 22
@@ -374,6 +405,11 @@ class Exec:
             per = np.zeros(per_slice_n * R, dtype=np.float64)
         check(lib().tc_exec_fetch(self.h, _p(per, F64P) if per is not None else None, _p(folded, F64P)))
         return folded, per
+
+
+def release_cache(device: int = -1):
+    """Return libtc's cached HBM blocks of ``device`` (-1: all) to the driver."""
+    check(lib().tc_release_cache(int(device)))
 
 
 def fold_device(per_slice_ptr: int, R: int, n: int, out_ptr: int, device: int):

@@ -66,37 +66,59 @@ constexpr int64_t kLateReleaseMax = (int64_t)1 << 30;  // late release (chain-li
 
 [[noreturn]] void fail(int st, const std::string& m) { throw Error{st, m}; }
 
+// First-fit arena simulation.  Memory classes (hoisting): class 1 holds the
+// slice-invariant tensors (written once per pass, in the prologue), class 0
+// the per-slice ones.  A range freed by one class is only reused by the same
+// class, so the write-after-read edges within each class are complete (an
+// invariant writer between two per-slice users of a range would otherwise
+// carry their ordering, and it is not in the per-slice graph).
 struct Alloc {
-  std::map<int64_t, int64_t> free_;                   // off -> size
-  std::map<int64_t, std::pair<int64_t, int>> seg;     // off -> (end, last reader step)
+  std::map<int64_t, int64_t> free_[2];                   // off -> size
+  std::map<int64_t, std::pair<int64_t, int>> seg[2];     // off -> (end, last reader step)
   int64_t top = 0;
 
   bool no_reuse = false;  // every buffer gets fresh memory: no WAR edges at all
+  // pinned region [0, pin_end): buffers that are never released (hoisting
+  // boundary tensors); the simulation proper starts above it
+  int64_t pin_top = 0, pin_end = 0;
 
-  int64_t alloc(int64_t size, std::vector<int>& hazards) {
+  void reserve_pinned(int64_t bytes) {
+    pin_end = bytes;
+    top = std::max(top, bytes);
+  }
+  int64_t alloc_pinned(int64_t size) {
+    size = (size + kAlign - 1) / kAlign * kAlign;
+    const int64_t o = pin_top;
+    pin_top += size;
+    if (pin_top > pin_end) fail(TC_BAD_ARG, "pinned arena region overflow");
+    return o;
+  }
+
+  int64_t alloc(int64_t size, std::vector<int>& hazards, int cl = 0) {
     size = (size + kAlign - 1) / kAlign * kAlign;
     if (no_reuse) {
       int64_t o = top;
       top += size;
       return o;
     }
+    auto& fr = free_[cl];
     int64_t off = -1;
-    for (auto it = free_.begin(); it != free_.end(); ++it) {
+    for (auto it = fr.begin(); it != fr.end(); ++it) {
       if (it->second >= size) {
         off = it->first;
         int64_t rest = it->second - size;
-        free_.erase(it);
-        if (rest > 0) free_[off + size] = rest;
+        fr.erase(it);
+        if (rest > 0) fr[off + size] = rest;
         break;
       }
     }
     if (off < 0) {
-      // extend: reuse a free block touching the top
-      if (!free_.empty()) {
-        auto last = std::prev(free_.end());
+      // extend: reuse a free block of this class touching the top
+      if (!fr.empty()) {
+        auto last = std::prev(fr.end());
         if (last->first + last->second == top) {
           off = last->first;
-          free_.erase(last);
+          fr.erase(last);
           top = off + size;
         }
       }
@@ -106,10 +128,11 @@ struct Alloc {
       }
     }
     // hazards: previous readers of any byte we are about to overwrite
+    auto& sg = seg[cl];
     int64_t end = off + size;
-    auto it = seg.upper_bound(off);
-    if (it != seg.begin()) --it;
-    while (it != seg.end() && it->first < end) {
+    auto it = sg.upper_bound(off);
+    if (it != sg.begin()) --it;
+    while (it != sg.end() && it->first < end) {
       int64_t s0 = it->first, s1 = it->second.first;
       int rd = it->second.second;
       if (s1 <= off) {
@@ -117,33 +140,34 @@ struct Alloc {
         continue;
       }
       hazards.push_back(rd);
-      it = seg.erase(it);
-      if (s0 < off) seg[s0] = {off, rd};
-      if (s1 > end) seg[end] = {s1, rd};
-      it = seg.lower_bound(std::min(s1, end));
+      it = sg.erase(it);
+      if (s0 < off) sg[s0] = {off, rd};
+      if (s1 > end) sg[end] = {s1, rd};
+      it = sg.lower_bound(std::min(s1, end));
     }
     return off;
   }
 
-  void release(int64_t off, int64_t size, int reader) {
-    if (no_reuse) return;
+  void release(int64_t off, int64_t size, int reader, int cl = 0) {
+    if (no_reuse || off < pin_end) return;
     size = (size + kAlign - 1) / kAlign * kAlign;
-    seg[off] = {off + size, reader};
-    auto nx = free_.lower_bound(off);
+    seg[cl][off] = {off + size, reader};
+    auto& fr = free_[cl];
+    auto nx = fr.lower_bound(off);
     int64_t o = off, s = size;
-    if (nx != free_.end() && nx->first == off + size) {
+    if (nx != fr.end() && nx->first == off + size) {
       s += nx->second;
-      nx = free_.erase(nx);
+      nx = fr.erase(nx);
     }
-    if (nx != free_.begin()) {
+    if (nx != fr.begin()) {
       auto pv = std::prev(nx);
       if (pv->first + pv->second == o) {
         o = pv->first;
         s += pv->second;
-        free_.erase(pv);
+        fr.erase(pv);
       }
     }
-    free_[o] = s;
+    fr[o] = s;
   }
 };
 
@@ -1125,6 +1149,46 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     g.sliced_doubles += size[l];
   }
 
+  // ---- slice-invariant hoisting ---------------------------------------------
+  // The reference re-executes the whole tree per slice (slicing.py:139-145).
+  // A node none of whose leaves holds a sliced index computes the same tensor
+  // for every slice, so it runs once per pass over the slices (the runtime's
+  // prologue graph) and only the `variant` nodes run per slice.  Variance is
+  // data flow: a sliced leaf is variant, a node is variant iff an operand is
+  // (an alias node is its source's buffer, so it inherits the source's).
+  // An invariant tensor read by a variant node ("boundary") must survive every
+  // slice: it lives in a pinned region at the start of the arena that the
+  // postorder simulation never hands out again.  Every other buffer keeps the
+  // simulation's offsets: the prologue finishes before the first slice, so an
+  // invariant tensor that only invariant nodes read may share memory with
+  // variant ones.  TC_HOIST=0 re-runs everything per slice (bit-identical).
+  const bool hoist_env = !(std::getenv("TC_HOIST") && std::atoi(std::getenv("TC_HOIST")) == 0) &&
+                                !(std::getenv("TC_SEG") && std::atoi(std::getenv("TC_SEG")) == 1);
+  const bool hoist = hoist_env && !g.chosen.empty();
+  std::vector<char> var_(S, 0), boundary(S, 0);
+  const int hoist_dbg = std::getenv("TC_HOIST_DBG") ? std::atoi(std::getenv("TC_HOIST_DBG")) : 0;
+  if (hoist) {
+    for (int l = 0; l < p.NL; ++l) var_[l] = g.loc[l].kind == LOC_SLICED;
+    for (int k = 0; k < p.NN; ++k) {
+      const int v = p.NL + k;
+      var_[v] = g.cls[v] == NC_ALIAS ? var_[alias_src[v]] : (char)(var_[p.left[k]] | var_[p.right[k]]);
+      if (hoist_dbg && ((hoist_dbg & 1) && g.cls[v] == NC_TINY)) var_[v] = 1;  // diagnostics: keep class per slice
+      if (hoist_dbg && ((hoist_dbg & 2) && g.cls[v] == NC_GEMM)) var_[v] = 1;
+      if (hoist_dbg && ((hoist_dbg & 4) && g.cls[v] == NC_STREAM)) var_[v] = 1;
+    }
+    for (int k = 0; k < p.NN; ++k) {
+      const int v = p.NL + k;
+      if (var_[v] || g.cls[v] == NC_ALIAS) continue;
+      // the node that reads v's buffer: look through aliases of it
+      int cur = v, u = p.parent[v];
+      while (u >= 0 && g.cls[u] == NC_ALIAS && alias_src[u] == cur) cur = u, u = p.parent[u];
+      if (u >= 0 && g.cls[u] == NC_ALIAS) continue;  // the tie-piece side of an alias: never read
+      boundary[v] = u < 0 || var_[u];                 // the root is read by k_rootcopy every slice
+    }
+    g.hoisted = true;
+  }
+  auto mcl = [&](int slot) { return hoist && !var_[slot] ? 1 : 0; };  // arena memory class
+
   tmark("tiny groups");
   // ---- tiny groups -------------------------------------------------------------
   std::vector<char> forced(S, 0);
@@ -1301,23 +1365,45 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     for (int l = 0; l < p.NL; ++l)
       if (g.loc[l].kind == LOC_SLICED) producer[l] = sel_step;
   }
-  // tiny roots: arena outputs allocated up front
   std::vector<int64_t> bytes(S);
   for (int s = 0; s < S; ++s) bytes[s] = size[s] * 8;
+  if (hoist) {  // the pinned region: boundary tensors that live in the arena
+    std::vector<char> groot(S, 0);
+    for (auto& gr : groups) groot[gr.back()] = 1;
+    int64_t pin = 0;
+    for (int k = 0; k < p.NN; ++k) {
+      const int v = p.NL + k;
+      if (boundary[v] && (g.cls[v] != NC_TINY || groot[v])) pin += (bytes[v] + kAlign - 1) / kAlign * kAlign;
+    }
+    arena.reserve_pinned(pin);
+    g.pinned_bytes = pin;
+  }
+  // tiny roots: arena outputs allocated up front
   std::vector<int> haz;
   for (size_t gi = 0; gi < groups.size(); ++gi) {
     int r = groups[gi].back();
     haz.clear();
-    g.loc[r] = Loc{LOC_ARENA, arena.alloc(bytes[r], haz)};
+    g.loc[r] = Loc{LOC_ARENA, boundary[r] ? arena.alloc_pinned(bytes[r]) : arena.alloc(bytes[r], haz, mcl(r))};
   }
-  std::vector<int> tiny_step(nlevels, -1);
-  for (int lv = 0; lv < nlevels; ++lv) {
+  // one tiny launch per level, split by variance when hoisting (key = 2*level + variant)
+  const int nkeys = hoist ? 2 * nlevels : nlevels;
+  auto gkey = [&](size_t gi) { return hoist ? 2 * glevel[gi] + (var_[groups[gi].back()] ? 1 : 0) : glevel[gi]; };
+  std::vector<int> key_groups(nkeys, 0);
+  for (size_t gi = 0; gi < groups.size(); ++gi) key_groups[gkey(gi)]++;
+  std::vector<int> tiny_step(nkeys, -1);
+  for (int kk = 0; kk < nkeys; ++kk) {
+    if (!key_groups[kk]) continue;
+    const int lv = hoist ? kk / 2 : kk;
     Step st;
     st.kind = ST_TINY;
-    if (sel_step >= 0) st.deps.push_back(sel_step);
+    st.inv = hoist && !(kk & 1);
+    if (sel_step >= 0 && !st.inv) st.deps.push_back(sel_step);
     if (lv >= nbuckets)  // a later level reads forced roots of any level-0 launch
-      for (int b = 0; b < lv; ++b) st.deps.push_back(tiny_step[b]);
-    tiny_step[lv] = (int)g.steps.size();
+      for (int b = 0; b < kk; ++b) {
+        if (tiny_step[b] < 0 || (hoist && (b / 2 >= lv || (st.inv && (b & 1))))) continue;
+        st.deps.push_back(tiny_step[b]);
+      }
+    tiny_step[kk] = (int)g.steps.size();
     g.steps.push_back(st);
   }
   tmark("tiny descriptors");
@@ -1344,10 +1430,10 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   // Groups are independent: descriptors are built on worker threads over
   // contiguous ranges of the level-major group order and concatenated.
   std::vector<int> gorder;
-  std::vector<std::pair<int32_t, int32_t>> level_range(nlevels);
+  std::vector<std::pair<int32_t, int32_t>> level_range(nkeys);
   {
-    std::vector<std::vector<int>> level_groups(nlevels);
-    for (size_t gi = 0; gi < groups.size(); ++gi) level_groups[glevel[gi]].push_back((int)gi);
+    std::vector<std::vector<int>> level_groups(nkeys);
+    for (size_t gi = 0; gi < groups.size(); ++gi) level_groups[gkey(gi)].push_back((int)gi);
     // heaviest groups first (the block scheduler hands out CTAs in order, so
     // the long subtrees start at once on their own SMs); cost ~ outputs written
     // plus a per-node overhead
@@ -1356,7 +1442,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       for (int v : groups[gi]) gcost[gi] += size[v] + 32;
     for (auto& lg : level_groups)
       std::stable_sort(lg.begin(), lg.end(), [&](int x, int y) { return gcost[x] > gcost[y]; });
-    for (int lv = 0; lv < nlevels; ++lv) {
+    for (int lv = 0; lv < nkeys; ++lv) {
       level_range[lv].first = (int32_t)gorder.size();
       for (int gi : level_groups[lv]) gorder.push_back(gi);
       level_range[lv].second = (int32_t)gorder.size();
@@ -1614,7 +1700,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     }
     for (size_t gi = 0; gi < groups.size(); ++gi) {
       g.tiny_smem_doubles = std::max(g.tiny_smem_doubles, group_smem[gi]);
-      producer[groups[gi].back()] = tiny_step[glevel[gi]];
+      producer[groups[gi].back()] = tiny_step[gkey(gi)];
     }
     // resolve operand / output places for the kernel: sa / sb / sout become
     // offsets from the start of dynamic smem (staged operands included), -1
@@ -1631,9 +1717,11 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   for (size_t gi = 0; gi < groups.size(); ++gi)
     for (int v : groups[gi])
       for (int c : {p.kid_l(v), p.kid_r(v)})
-        if (is_tiny(c) && group_of[c] != (int)gi) arena.release(g.loc[c].off, bytes[c], tiny_step[glevel[gi]]);
+        if (is_tiny(c) && group_of[c] != (int)gi)
+          arena.release(g.loc[c].off, bytes[c], tiny_step[gkey(gi)], mcl(c));
   // store level ranges in the TINY steps (reuse `work` / gdig_off fields)
-  for (int lv = 0; lv < nlevels; ++lv) {
+  for (int lv = 0; lv < nkeys; ++lv) {
+    if (tiny_step[lv] < 0) continue;
     g.steps[tiny_step[lv]].gdig_off = level_range[lv].first;
     g.steps[tiny_step[lv]].work = level_range[lv].second - level_range[lv].first;
   }
@@ -1651,17 +1739,21 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     if (g.cls[v] != NC_ALIAS) {
       g.phys_bytes += (u128)(8 * (size[a] + size[b] + size[v]));
       g.phys_flops += (u128)fl;
+      if (hoist && !var_[v]) {
+        g.phys_bytes_inv += (u128)(8 * (size[a] + size[b] + size[v]));
+        g.phys_flops_inv += (u128)fl;
+      }
     }
   }
 
   tmark("emit nodes");
   struct Pending {
     int64_t off, bytes;
-    int reader;
+    int reader, cl;
   };
   std::vector<Pending> pending;
   auto flush_pending = [&]() {
-    for (auto& q : pending) arena.release(q.off, q.bytes, q.reader);
+    for (auto& q : pending) arena.release(q.off, q.bytes, q.reader, q.cl);
     pending.clear();
   };
   struct SegCand {
@@ -2058,6 +2150,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       if (g.loc[c].kind == LOC_SEG) seg_close(c);
     Step st;
     st.slot = v;
+    st.inv = hoist && !var_[v];
     st.alg_bytes = node_bytes[v];
     st.alg_flops = node_flops[v];
     st.la = g.loc[a];
@@ -2065,7 +2158,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     for (int c : {a, b})
       if (producer[c] >= 0) st.deps.push_back(producer[c]);
     haz.clear();
-    g.loc[v] = Loc{LOC_ARENA, arena.alloc(bytes[v], haz)};
+    g.loc[v] = Loc{LOC_ARENA, boundary[v] ? arena.alloc_pinned(bytes[v]) : arena.alloc(bytes[v], haz, mcl(v))};
     for (int h : haz) st.deps.push_back(h);
     st.lc = g.loc[v];
     flush_pending();  // the previous node's inputs: free only now (see below)
@@ -2236,12 +2329,13 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       // split-K workspace: [splits][tiles][BM*BN] partial tiles, reduced in split order
       const int64_t ws_bytes = (int64_t)st.gp.splits * st.work * ((int64_t)1 << (st.bm + st.bn)) * 8;
       haz.clear();
-      st.lws = Loc{LOC_ARENA, arena.alloc(ws_bytes, haz)};
+      st.lws = Loc{LOC_ARENA, arena.alloc(ws_bytes, haz, mcl(v))};
       for (int h : haz) st.deps.push_back(h);
       g.steps.push_back(st);
       Step rd;
       rd.kind = ST_GEMM_REDUCE;
       rd.slot = v;
+      rd.inv = st.inv;
       rd.gp = st.gp;
       rd.bm = st.bm;
       rd.bn = st.bn;
@@ -2253,7 +2347,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       rd.deps.push_back(me);
       producer[v] = me + 1;
       g.steps.push_back(rd);
-      arena.release(st.lws.off, ws_bytes, me + 1);
+      arena.release(st.lws.off, ws_bytes, me + 1, mcl(v));
     } else {
       producer[v] = me;
       g.steps.push_back(st);
@@ -2273,8 +2367,8 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     }
     for (int c : {a, b})
       if (g.loc[c].kind == LOC_ARENA) {
-        if (link && bytes[c] <= kLateReleaseMax) pending.push_back({g.loc[c].off, bytes[c], me});
-        else arena.release(g.loc[c].off, bytes[c], me);
+        if (link && bytes[c] <= kLateReleaseMax) pending.push_back({g.loc[c].off, bytes[c], me, mcl(c)});
+        else arena.release(g.loc[c].off, bytes[c], me, mcl(c));
       }
   };
 
@@ -2282,7 +2376,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     const int v = p.NL + k;
     if (g.cls[v] == NC_TINY) {
       int gi = group_of[v];
-      int ts = tiny_step[glevel[gi]];
+      int ts = tiny_step[gkey(gi)];
       g.steps[ts].alg_bytes += node_bytes[v];
       g.steps[ts].alg_flops += node_flops[v];
       continue;

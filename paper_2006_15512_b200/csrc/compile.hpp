@@ -26,6 +26,7 @@ enum StepKind : int8_t {
 struct Step {
   StepKind kind;
   int slot = -1;  // node for STREAM/GEMM/GENERIC
+  bool inv = false;  // slice-invariant: runs once per pass (prologue), not per slice
   std::vector<int> deps;
   // kernel parameters with pointer fields holding Loc-encoded placeholders
   StreamParams sp{};
@@ -83,6 +84,9 @@ struct Program {
   int n_tiny = 0, n_stream = 0, n_gemm = 0, n_generic = 0, n_alias = 0;
   u128 alg_bytes = 0, alg_flops = 0;    // dense (reference) per-node work, summed
   u128 phys_bytes = 0, phys_flops = 0;  // executed work over physical variables
+  u128 phys_bytes_inv = 0, phys_flops_inv = 0;  // ... of it, slice-invariant (hoisted: once per pass)
+  bool hoisted = false;          // slice-invariant nodes run once per pass (compile.cpp)
+  int64_t pinned_bytes = 0;      // arena prefix holding hoisted tensors read by per-slice nodes
   u128 mem_estimate = 0, peak_observed = 0;
 };
 

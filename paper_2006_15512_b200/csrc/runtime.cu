@@ -214,6 +214,7 @@ struct Launch {
   unsigned smem = 0;
   int kind = 0, slot = -1;
   bool coop = false;  // cooperative launch (k_stream_seq: grid barriers)
+  bool inv = false;   // slice-invariant: in the prologue graph, once per pass
   double bytes = 0, flops = 0;
   int xbits = -1, ns = 0, nf = 0, ns2 = -1, nf2 = -1;  // stream shape (diagnostics)
   std::vector<char> blob;
@@ -267,8 +268,12 @@ struct tc_exec {
   int64_t results_cap = 0;  // slices
   double* folded = nullptr;
   cudaGraph_t graph = nullptr;
-  cudaGraphExec_t gexec = nullptr;
+  cudaGraphExec_t gexec = nullptr;      // per-slice graph
+  cudaGraph_t graph_pro = nullptr;      // slice-invariant prologue (hoisted nodes), once per pass
+  cudaGraphExec_t gexec_pro = nullptr;
   int64_t kernels_per_slice = 0;
+  int64_t kernels_prologue = 0;
+  int64_t launches_per_pass(int64_t n) const { return kernels_prologue + kernels_per_slice * n; }
   int64_t last_n = 0;
   double compile_ms = 0;
 
@@ -276,6 +281,8 @@ struct tc_exec {
     if (device >= 0) cudaSetDevice(device);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
+    if (gexec_pro) cudaGraphExecDestroy(gexec_pro);
+    if (graph_pro) cudaGraphDestroy(graph_pro);
     if (stream) cudaStreamSynchronize(stream);
     for (void* q : {(void*)arena, (void*)leafbuf, (void*)slicedbuf, (void*)tnodes, (void*)tdigs,
                     (void*)tgroups, (void*)gdig, (void*)dseg, (void*)dsegdig, (void*)dsegtab, (void*)rootmap, (void*)results_slot, (void*)seq_params, (void*)seq_keys, (void*)sel, (void*)selt, (void*)eta, (void*)results,
@@ -380,6 +387,7 @@ struct tc_exec {
       Step& st = g.steps[si];
       Launch L;
       L.kind = st.kind;
+      L.inv = st.inv;
       L.slot = st.slot;
       L.bytes = st.alg_bytes;
       L.flops = st.alg_flops;
@@ -512,7 +520,12 @@ struct tc_exec {
     auto t_end = std::chrono::steady_clock::now();
     setup_ms = std::chrono::duration<double, std::milli>(t_end - t_prog).count();
     compile_ms = std::chrono::duration<double, std::milli>(t_end - t0).count();
-    kernels_per_slice = (int64_t)launches.size();
+    count_launches();
+  }
+
+  void count_launches() {
+    kernels_prologue = kernels_per_slice = 0;
+    for (auto& L : launches) ++(L.inv ? kernels_prologue : kernels_per_slice);
   }
 
   // Chain links: a stream step whose big operand is the previous stream step's
@@ -658,7 +671,8 @@ struct tc_exec {
                      (int)(mk && pair_fn(tni, s1.ns, s1.nf, s2.ns, s2.nf) != nullptr), (long)s1.la.off, (long)s1.la_bytes,
                      (long)s1.lb.off, (long)s1.lb_bytes, (long)s2.lc.off, (long)s2.lc_bytes, (int)s1.la.kind, (int)s1.lb.kind, (int)s2.lc.kind);
       }
-      if (on && i + 1 < S && g.steps[i].kind == ST_STREAM && g.steps[i + 1].kind == ST_STREAM) {
+      if (on && i + 1 < S && g.steps[i].kind == ST_STREAM && g.steps[i + 1].kind == ST_STREAM &&
+          g.steps[i].inv == g.steps[i + 1].inv) {
         const Step &s1 = g.steps[i], &s2 = g.steps[i + 1];
         bool dep_ok = false;  // step 2 must consume step 1 (its RAW edge)
         for (int d : s2.deps) dep_ok |= d == (int)i;
@@ -676,6 +690,7 @@ struct tc_exec {
         const Step &s1 = g.steps[i], &s2 = g.steps[i + 1];
         Launch L;
         L.kind = ST_STREAM;
+        L.inv = s1.inv;
         L.slot = s2.slot;
         L.func = (void*)fn;
         L.block = dim3(kStreamThreads);
@@ -739,7 +754,7 @@ struct tc_exec {
     static const bool on = std::getenv("TC_SEQ") && std::atoi(std::getenv("TC_SEQ")) == 1;
     auto eligible = [&](size_t i) {
       const Step& st = g.steps[i];
-      return on && st.kind == ST_STREAM && st.ns <= kSeqMaxNS && st.nf <= kSeqMaxNF;
+      return on && !st.inv && st.kind == ST_STREAM && st.ns <= kSeqMaxNS && st.nf <= kSeqMaxNF;
     };
     std::vector<std::pair<size_t, size_t>> runs;  // [first, end)
     for (size_t i = 0; i < S;) {
@@ -841,59 +856,40 @@ struct tc_exec {
     }
   }
 
-  // The CUDA graph is built on the first run that replays the program more
+  // The CUDA graphs are built on the first run that replays the program more
   // than twice; one-shot calls launch the steps eagerly on the stream (with
   // PDL: each kernel's launch and prologue overlap its predecessor's tail).
-  // The graph is the explicit DAG (data + WAR edges).  TC_PDL_GRAPH=1 captures
-  // the eager PDL chain instead -- measured: no gain on C2, 38% slower on C4
-  // (early-launched dependents hold SM slots; the chain drops concurrency).
+  // Two graphs from the explicit launch DAG (data + WAR edges): the prologue
+  // (slice-invariant launches, once per pass over the slices) and the
+  // per-slice graph.  Edges between the two are implied by stream order.
   void ensure_graph() {
     if (gexec) return;
     auto t_graph0 = std::chrono::steady_clock::now();
-    kernels_per_slice = (int64_t)launches.size();
-    static const bool pdl_graph = std::getenv("TC_PDL_GRAPH") && std::atoi(std::getenv("TC_PDL_GRAPH")) == 1;
-    if (use_pdl() && pdl_graph) {
-      CU(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-      launch_eager();
-      CU(cudaStreamEndCapture(stream, &graph));
-      CU(cudaGraphInstantiate(&gexec, graph, 0));
-      graph_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_graph0).count();
-      return;
-    }
-    CU(cudaGraphCreate(&graph, 0));
-    std::vector<cudaGraphNode_t> nodes(launches.size());
-    kernels_per_slice = 0;
-    // TC_PDL_EDGES=1|2 (experimental): data edges become programmatic edges
-    // (1: dependent launches when every primary CTA triggered, 2: when every
-    // primary CTA started); every kernel waits (griddepcontrol.wait) before
-    // touching its operands
-    static const int pdl_edges = std::getenv("TC_PDL_EDGES") ? std::atoi(std::getenv("TC_PDL_EDGES")) : 0;
-    for (size_t si = 0; si < launches.size(); ++si) {
-      std::vector<cudaGraphNode_t> deps;
-      for (int d : ldeps[si]) deps.push_back(nodes[d]);
-      cudaKernelNodeParams kp = launches[si].params();
-      if (pdl_edges && !launches[si].coop && !deps.empty()) {
-        CU(cudaGraphAddKernelNode(&nodes[si], graph, nullptr, 0, &kp));
-        std::vector<cudaGraphEdgeData> ed(deps.size());
-        for (auto& e : ed) {
-          e = cudaGraphEdgeData{};
-          e.from_port = pdl_edges == 2 ? cudaGraphKernelNodePortLaunchCompletion : cudaGraphKernelNodePortProgrammatic;
-          e.type = cudaGraphDependencyTypeProgrammatic;
+    count_launches();
+    for (int pass = 0; pass < 2; ++pass) {
+      const bool want_inv = pass == 0;
+      cudaGraph_t gr = nullptr;
+      std::vector<cudaGraphNode_t> nodes(launches.size(), nullptr);
+      for (size_t si = 0; si < launches.size(); ++si) {
+        if (launches[si].inv != want_inv) continue;
+        if (!gr) CU(cudaGraphCreate(&gr, 0));
+        std::vector<cudaGraphNode_t> deps;
+        for (int d : ldeps[si])
+          if (launches[d].inv == want_inv) deps.push_back(nodes[d]);
+        cudaKernelNodeParams kp = launches[si].params();
+        CU(cudaGraphAddKernelNode(&nodes[si], gr, deps.data(), deps.size(), &kp));
+        if (launches[si].coop) {
+          cudaLaunchAttributeValue v{};
+          v.cooperative = 1;
+          CU(cudaGraphKernelNodeSetAttribute(nodes[si], cudaLaunchAttributeCooperative, &v));
         }
-        std::vector<cudaGraphNode_t> to(deps.size(), nodes[si]);
-        CU(cudaGraphAddDependencies_v2(graph, deps.data(), to.data(), ed.data(), deps.size()));
-        ++kernels_per_slice;
-        continue;
       }
-      CU(cudaGraphAddKernelNode(&nodes[si], graph, deps.data(), deps.size(), &kp));
-      if (launches[si].coop) {
-        cudaLaunchAttributeValue v{};
-        v.cooperative = 1;
-        CU(cudaGraphKernelNodeSetAttribute(nodes[si], cudaLaunchAttributeCooperative, &v));
-      }
-      ++kernels_per_slice;
+      if (!gr) continue;
+      cudaGraphExec_t ge = nullptr;
+      CU(cudaGraphInstantiate(&ge, gr, 0));
+      if (want_inv) graph_pro = gr, gexec_pro = ge;
+      else graph = gr, gexec = ge;
     }
-    CU(cudaGraphInstantiate(&gexec, graph, 0));
     graph_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_graph0).count();
   }
   double program_ms = 0, setup_ms = 0, graph_ms = 0;
@@ -940,9 +936,23 @@ struct tc_exec {
     CU(cudaStreamSynchronize(stream));
   }
 
-  // one slice in step order on the stream (no graph)
-  void launch_eager() {
-    for (size_t i = 0; i < launches.size(); ++i) launch_one(launches[i], use_pdl() && i > 0);
+  // the prologue (inv) or one slice (!inv) in step order on the stream (no graph)
+  void launch_eager(bool inv, bool first) {
+    for (size_t i = 0; i < launches.size(); ++i) {
+      if (launches[i].inv != inv) continue;
+      launch_one(launches[i], use_pdl() && !first);
+      first = false;
+    }
+  }
+  // one pass over n slices: prologue once, then the per-slice launches
+  void launch_pass(int64_t n, bool eager) {
+    if (eager) {
+      launch_eager(true, true);
+      for (int64_t s = 0; s < n; ++s) launch_eager(false, s == 0 && kernels_prologue == 0);
+      return;
+    }
+    if (gexec_pro) CU(cudaGraphLaunch(gexec_pro, stream));
+    for (int64_t s = 0; s < n; ++s) CU(cudaGraphLaunch(gexec, stream));
   }
 
   // Eager replay of one slice, one kernel at a time, timed per launch with
@@ -993,6 +1003,89 @@ struct tc_exec {
     last_n = 1;
   }
 
+  // Per-launch device time in graph mode: the prologue and per-slice graphs
+  // rebuilt with an event-record node before and after every kernel node
+  // (same DAG, same concurrency as the timed graphs), one pass over slices
+  // [b, e) with a synchronize after each slice to read the events.  ms[i] =
+  // launch i's time summed over the pass (prologue launches once).
+  void profile_graph(int64_t b, int64_t e, std::vector<float>& ms, float& pass_ms) {
+    CU(cudaSetDevice(device));
+    const int64_t n = e - b;
+    ensure_results(n);
+    ms.assign(launches.size(), 0.f);
+    pass_ms = 0.f;
+    struct PG {
+      cudaGraph_t g = nullptr;
+      cudaGraphExec_t ge = nullptr;
+      std::vector<int> idx;
+      std::vector<cudaEvent_t> e0, e1;
+      ~PG() {
+        if (ge) cudaGraphExecDestroy(ge);
+        if (g) cudaGraphDestroy(g);
+        for (auto x : e0) cudaEventDestroy(x);
+        for (auto x : e1) cudaEventDestroy(x);
+      }
+    } pg[2];
+    for (int pass = 0; pass < 2; ++pass) {
+      const bool want_inv = pass == 0;
+      PG& G = pg[pass];
+      std::vector<cudaGraphNode_t> nodes(launches.size(), nullptr);
+      for (size_t si = 0; si < launches.size(); ++si) {
+        if (launches[si].inv != want_inv) continue;
+        if (!G.g) CU(cudaGraphCreate(&G.g, 0));
+        std::vector<cudaGraphNode_t> deps;
+        for (int d : ldeps[si])
+          if (launches[d].inv == want_inv) deps.push_back(nodes[d]);
+        cudaEvent_t a, z;
+        CU(cudaEventCreate(&a));
+        CU(cudaEventCreate(&z));
+        G.e0.push_back(a);
+        G.e1.push_back(z);
+        G.idx.push_back((int)si);
+        cudaGraphNode_t r0, r1;
+        CU(cudaGraphAddEventRecordNode(&r0, G.g, deps.data(), deps.size(), a));
+        cudaKernelNodeParams kp = launches[si].params();
+        CU(cudaGraphAddKernelNode(&nodes[si], G.g, &r0, 1, &kp));
+        if (launches[si].coop) {
+          cudaLaunchAttributeValue v{};
+          v.cooperative = 1;
+          CU(cudaGraphKernelNodeSetAttribute(nodes[si], cudaLaunchAttributeCooperative, &v));
+        }
+        CU(cudaGraphAddEventRecordNode(&r1, G.g, &nodes[si], 1, z));
+      }
+      if (G.g) CU(cudaGraphInstantiate(&G.ge, G.g, 0));
+    }
+    int64_t h[2] = {b, b};
+    CU(cudaMemcpyAsync(eta, h, sizeof(h), cudaMemcpyHostToDevice, stream));
+    CU(cudaStreamSynchronize(stream));
+    cudaEvent_t p0, p1;
+    CU(cudaEventCreate(&p0));
+    CU(cudaEventCreate(&p1));
+    auto collect = [&](PG& G) {
+      for (size_t q = 0; q < G.idx.size(); ++q) {
+        float t = 0;
+        CU(cudaEventElapsedTime(&t, G.e0[q], G.e1[q]));
+        ms[G.idx[q]] += t;
+      }
+    };
+    for (int64_t s = -1; s < n; ++s) {
+      PG& G = pg[s < 0 ? 0 : 1];
+      if (!G.ge) continue;
+      CU(cudaEventRecord(p0, stream));
+      CU(cudaGraphLaunch(G.ge, stream));
+      CU(cudaEventRecord(p1, stream));
+      CU(cudaStreamSynchronize(stream));
+      CU(cudaGetLastError());
+      float t = 0;
+      CU(cudaEventElapsedTime(&t, p0, p1));
+      pass_ms += t;
+      collect(G);
+    }
+    cudaEventDestroy(p0);
+    cudaEventDestroy(p1);
+    last_n = n;
+  }
+
   double run(int64_t b, int64_t e, int64_t repeats = 1) {
     CU(cudaSetDevice(device));
     int64_t n = e - b;
@@ -1013,10 +1106,7 @@ struct tc_exec {
     CU(cudaEventRecord(e0, stream));
     for (int64_t r = 0; r < repeats; ++r) {
       if (r > 0) k_eta_reset<<<1, 1, 0, stream>>>(eta);
-      for (int64_t s = 0; s < n; ++s) {
-        if (eager) launch_eager();
-        else CU(cudaGraphLaunch(gexec, stream));
-      }
+      launch_pass(n, eager);
     }
     CU(cudaEventRecord(e1, stream));
     CU(cudaEventSynchronize(e1));
@@ -1050,7 +1140,7 @@ struct tc_exec {
       if (r > 0) k_eta_reset<<<1, 1, 0, stream>>>(eta);
       k_flush<<<grid_for(n4, 256, device), 256, 0, stream>>>(fbuf, n4, (double)r);
       CU(cudaEventRecord(ev[2 * r], stream));
-      for (int64_t s = 0; s < n; ++s) CU(cudaGraphLaunch(gexec, stream));
+      launch_pass(n, false);
       CU(cudaEventRecord(ev[2 * r + 1], stream));
     }
     CU(cudaStreamSynchronize(stream));
@@ -1117,10 +1207,36 @@ Nccl& nccl() {
 constexpr int kNcclFloat64 = 8, kNcclSum = 0;
 }  // namespace
 
+// One communicator set per device list, created on first use and kept for the
+// process (ncclCommInitAll costs ~100 ms-1 s; a counter calls sliced_execute
+// once per formula).
+const std::vector<ncclComm_t>& nccl_comms(const std::vector<int>& devs) {
+  static std::mutex mu;
+  static std::map<std::vector<int>, std::vector<ncclComm_t>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(devs);
+  if (it != cache.end()) return it->second;
+  std::vector<ncclComm_t> comms(devs.size());
+  NC(nccl().CommInitAll(comms.data(), (int)devs.size(), devs.data()));
+  return cache.emplace(devs, std::move(comms)).first->second;
+}
+
 // ---------------------------------------------------------------------------
 extern "C" {
 
 const char* tc_last_error(void) { return g_err.c_str(); }
+
+int tc_release_cache(int32_t device) {
+  return guard([&] {
+    int n = 0;
+    CU(cudaGetDeviceCount(&n));
+    for (int d = 0; d < n; ++d)
+      if (device < 0 || d == device) {
+        CU(cudaSetDevice(d));
+        dcache().release(d);
+      }
+  });
+}
 int32_t tc_version(void) { return 1; }
 int32_t tc_device_count(void) {
   int n = 0;
@@ -1228,6 +1344,10 @@ int tc_compile_stats(const tc_plan* plan, const int32_t* sliced, int32_t n_slice
     s->n_tied_leaves = g.n_tied_leaves;
     s->phys_bytes = to_abi(g.phys_bytes);
     s->phys_flops = to_abi(g.phys_flops);
+    s->phys_bytes_hoisted = to_abi(g.phys_bytes_inv);
+    s->phys_flops_hoisted = to_abi(g.phys_flops_inv);
+    for (auto& st : g.steps) ++(st.inv ? s->launches_prologue : s->launches_per_slice);
+    s->pinned_bytes = g.pinned_bytes;
     s->program_ms = ms;
   });
 }
@@ -1270,7 +1390,7 @@ static void fill_stats(const tc_exec& ex, double ms, tc_stats* s) {
   s->device_peak_bytes = ex.dev_bytes;
   s->device_ms = ms;
   s->compile_ms = ex.compile_ms;
-  s->gpu_launches = ex.kernels_per_slice * ex.last_n;
+  s->gpu_launches = ex.launches_per_pass(ex.last_n);
   s->n_tiny_nodes = g.n_tiny;
   s->n_stream_nodes = g.n_stream;
   s->n_gemm_nodes = g.n_gemm;
@@ -1281,6 +1401,11 @@ static void fill_stats(const tc_exec& ex, double ms, tc_stats* s) {
   s->n_tied_leaves = g.n_tied_leaves;
   s->phys_bytes = to_abi(g.phys_bytes);
   s->phys_flops = to_abi(g.phys_flops);
+  s->phys_bytes_hoisted = to_abi(g.phys_bytes_inv);
+  s->phys_flops_hoisted = to_abi(g.phys_flops_inv);
+  s->launches_prologue = ex.kernels_prologue;
+  s->launches_per_slice = ex.kernels_per_slice;
+  s->pinned_bytes = g.pinned_bytes;
   s->program_ms = ex.program_ms;
   s->setup_ms = ex.setup_ms;
   s->graph_ms = ex.graph_ms;
@@ -1296,7 +1421,7 @@ int tc_exec_run_repeat(tc_exec* ex, int64_t slice_begin, int64_t slice_end, int6
       throw Error{TC_BAD_ARG, "slice range out of bounds"};
     double ms = ex->run(slice_begin, slice_end, repeats);
     fill_stats(*ex, ms, stats);
-    if (stats) stats->gpu_launches = (ex->kernels_per_slice * ex->last_n + 1) * repeats - 1;
+    if (stats) stats->gpu_launches = (ex->launches_per_pass(ex->last_n) + 1) * repeats - 1;
   });
 }
 
@@ -1307,7 +1432,7 @@ int tc_exec_run_flushed(tc_exec* ex, int64_t slice_begin, int64_t slice_end, int
       throw Error{TC_BAD_ARG, "slice range out of bounds"};
     double ms = ex->run_flushed(slice_begin, slice_end, repeats, flush_bytes);
     fill_stats(*ex, ms, stats);
-    if (stats) stats->gpu_launches = ex->kernels_per_slice * ex->last_n * repeats;
+    if (stats) stats->gpu_launches = ex->launches_per_pass(ex->last_n) * repeats;
   });
 }
 
@@ -1346,6 +1471,29 @@ int tc_exec_profile(tc_exec* ex, int64_t slice, float* step_ms, int32_t* step_ki
       if (step_flops) step_flops[i] = ex->launches[i].flops;
     }
     *n = (int32_t)ms.size();
+  });
+}
+
+int tc_exec_profile_graph(tc_exec* ex, int64_t slice_begin, int64_t slice_end, float* launch_ms,
+                          int32_t* launch_kind, int32_t* launch_inv, double* launch_bytes, double* launch_flops,
+                          int32_t cap, int32_t* n, float* pass_ms) {
+  return guard([&] {
+    if (slice_begin < 0 || slice_end > ex->prog.num_slices || slice_begin >= slice_end)
+      throw Error{TC_BAD_ARG, "slice range out of bounds"};
+    std::vector<float> ms;
+    float pm = 0;
+    ex->profile_graph(slice_begin, slice_end, ms, pm);
+    int k = (int)std::min<size_t>(ms.size(), (size_t)std::max(0, cap));
+    for (int i = 0; i < k; ++i) {
+      const Launch& L = ex->launches[i];
+      if (launch_ms) launch_ms[i] = ms[i];
+      if (launch_kind) launch_kind[i] = L.kind;
+      if (launch_inv) launch_inv[i] = L.inv ? 1 : 0;
+      if (launch_bytes) launch_bytes[i] = L.bytes;
+      if (launch_flops) launch_flops[i] = L.flops;
+    }
+    *n = (int32_t)ms.size();
+    if (pass_ms) *pass_ms = pm;
   });
 }
 
@@ -1452,44 +1600,73 @@ int tc_sliced_execute(const tc_plan* plan, int64_t mem_budget, const int32_t* sl
       ex[0]->fold(out_val);
     } else {
       // zero-padded [NS][R] vector on every device, one all-reduce (exact: a
-      // single non-zero contributor per position), fold on device 0
-      auto& nc = nccl();
-      std::vector<ncclComm_t> comms(G);
-      NC(nc.CommInitAll(comms.data(), G, devs.data()));
-      std::vector<double*> full(G, nullptr);
+      // single non-zero contributor per position), fold on device 0.  The
+      // same device listed twice (tests on one GPU) gathers by peer copies
+      // instead: NCCL rejects duplicate devices in one communicator.
+      int64_t nbytes = 0;
+      if (__builtin_mul_overflow(NS, R, &nbytes) || __builtin_mul_overflow(nbytes, (int64_t)8, &nbytes) ||
+          nbytes > ((int64_t)1 << 36))
+        throw Error{TC_OOM, "per-slice result vector of " + std::to_string(NS) + " x " + std::to_string(R) +
+                                " entries exceeds the all-reduce cap (64 GiB)"};
+      struct Full {  // returned to the cache on every exit path
+        std::vector<double*> p;
+        std::vector<int> dev;
+        ~Full() {
+          for (size_t i = 0; i < p.size(); ++i)
+            if (p[i]) dcache().put(dev[i], p[i]);
+        }
+      } full;
+      full.p.assign(G, nullptr);
+      full.dev = devs;
+      std::vector<int> sorted = devs;
+      std::sort(sorted.begin(), sorted.end());
+      const bool distinct = std::unique(sorted.begin(), sorted.end()) == sorted.end();
       for (int gi = 0; gi < G; ++gi) {
+        if (!distinct && gi > 0) break;
         CU(cudaSetDevice(devs[gi]));
         int64_t dummy = 0;
-        full[gi] = dalloc<double>((size_t)(NS * R), dummy, devs[gi]);
-        CU(cudaMemsetAsync(full[gi], 0, NS * R * 8, ex[gi]->stream));
-        int64_t b = std::min<int64_t>(NS, gi * per);
-        if (ex[gi]->last_n > 0)
-          CU(cudaMemcpyAsync(full[gi] + b * R, ex[gi]->results, ex[gi]->last_n * R * 8, cudaMemcpyDeviceToDevice,
-                             ex[gi]->stream));
-      }
-      NC(nc.GroupStart());
-      for (int gi = 0; gi < G; ++gi) NC(nc.AllReduce(full[gi], full[gi], NS * R, kNcclFloat64, kNcclSum, comms[gi], ex[gi]->stream));
-      NC(nc.GroupEnd());
-      for (int gi = 0; gi < G; ++gi) {
-        CU(cudaSetDevice(devs[gi]));
-        CU(cudaStreamSynchronize(ex[gi]->stream));
+        full.p[gi] = dalloc<double>((size_t)(NS * R), dummy, devs[gi]);
+        CU(cudaMemsetAsync(full.p[gi], 0, NS * R * 8, ex[gi]->stream));
       }
       tc_exec& e0 = *ex[0];
+      if (distinct) {
+        for (int gi = 0; gi < G; ++gi) {
+          CU(cudaSetDevice(devs[gi]));
+          int64_t b = std::min<int64_t>(NS, gi * per);
+          if (ex[gi]->last_n > 0)
+            CU(cudaMemcpyAsync(full.p[gi] + b * R, ex[gi]->results, ex[gi]->last_n * R * 8,
+                               cudaMemcpyDeviceToDevice, ex[gi]->stream));
+        }
+        auto& nc = nccl();
+        const std::vector<ncclComm_t>& comms = nccl_comms(devs);
+        NC(nc.GroupStart());
+        for (int gi = 0; gi < G; ++gi)
+          NC(nc.AllReduce(full.p[gi], full.p[gi], NS * R, kNcclFloat64, kNcclSum, comms[gi], ex[gi]->stream));
+        NC(nc.GroupEnd());
+        for (int gi = 0; gi < G; ++gi) {
+          CU(cudaSetDevice(devs[gi]));
+          CU(cudaStreamSynchronize(ex[gi]->stream));
+        }
+      } else {
+        CU(cudaSetDevice(e0.device));
+        CU(cudaStreamSynchronize(e0.stream));
+        for (int gi = 0; gi < G; ++gi) {
+          int64_t b = std::min<int64_t>(NS, gi * per);
+          if (ex[gi]->last_n > 0)
+            CU(cudaMemcpyPeerAsync(full.p[0] + b * R, devs[0], ex[gi]->results, devs[gi], ex[gi]->last_n * R * 8,
+                                   e0.stream));
+        }
+      }
       CU(cudaSetDevice(e0.device));
-      k_fold<<<grid_for(R, 256, e0.device), 256, 0, e0.stream>>>(full[0], R, NS, e0.folded);
+      k_fold<<<grid_for(R, 256, e0.device), 256, 0, e0.stream>>>(full.p[0], R, NS, e0.folded);
       CU(cudaGetLastError());
       CU(cudaMemcpyAsync(out_val, e0.folded, R * 8, cudaMemcpyDeviceToHost, e0.stream));
       CU(cudaStreamSynchronize(e0.stream));
-      for (int gi = 0; gi < G; ++gi) {
-        cudaSetDevice(devs[gi]);
-        dcache().put(devs[gi], full[gi]);
-        if (nc.CommDestroy) nc.CommDestroy(comms[gi]);
-      }
     }
     if (stats) {
       fill_stats(*ex[0], *std::max_element(ms.begin(), ms.end()), stats);
       int64_t launches = 0;
-      for (auto& e : ex) launches += e->kernels_per_slice * e->last_n;
+      for (auto& e : ex) launches += e->launches_per_pass(e->last_n);
       stats->gpu_launches = launches;
       stats->num_slices = NS;
     }
