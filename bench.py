@@ -1,30 +1,37 @@
 """Benchmark of the B200 execution stage (Algorithm 3 of arXiv 2006.15512).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
 
-A step is one execution of the frozen contraction plan of the workload (all
-of its slices): the plan comes from the unmodified reference planner
-(tools/make_plans.py, data/plans/<config>.tcplan.npz), inputs are resident in
-HBM before the timed region.  Metric: slices/s (whole job); for the default
-unsliced config C2 one slice = one formula, so ms_per_step is the
-per-formula execution time.
+A step is one pass of the frozen contraction plan of the workload over its
+slices (data/plans/<config>.tcplan.npz, planned by the unmodified reference
+planner, tools/make_plans.py); leaves and program are resident in HBM before
+the timed region.  Metric: slices/s of the whole job (all ranks).
 
-N > 1 (torchrun, one process per GPU):
-  * sliced configs (c4, c5, c3): the lexicographic slice ids are block-
-    partitioned over ranks, one NCCL all-reduce combines them (strong scaling);
-  * unsliced configs (c1a, c1b, c2): the path does not shard -> N independent
-    replicas, no collective (weak scaling).
+Default workload: C4 (BASELINE configs[3]: "random 3-CNF n=400, ratio 4.0,
+width ~36 sliced into 2^8 slices across 1/2/4/8 B200") = banded_3cnf(400,
+4.0, 36, seed 11) (the first SAT seed), slice set = Algorithm 3's greedy
+8-pick prefix (slicing.py:70-79) -> 2^8 slices.  The line also carries C2
+(configs[1], unsliced, 1 B200) device and end-to-end numbers under "c2".
 
-``--impl reference`` times the unmodified reference ``sliced_execute``
-(tensorcount from oracle/_ref, numpy/OpenBLAS on the host cores) on the same
-plan; rank 0 only.
+N > 1: one process per GPU (torchrun; ``python bench.py --gpus N`` launches
+it itself).  Sliced configs block-partition the lexicographic slice ids over
+the ranks and meet in ONE NCCL all-reduce (strong scaling); unsliced configs
+(c1a, c1b, c2, c4_full) run N replicas (weak scaling, no collective).
+
+``--impl reference`` times the reference's own CPU implementation on the
+host cores (tensorcount from baseline/_ref or oracle/_ref, numpy/OpenBLAS):
+the full unmodified ``sliced_execute`` where it fits (c1a, c2), else a
+bounded, labelled sample of its per-node ``contract_pair`` work extrapolated
+to the whole job (see ``reference_sample_model``).
 """
 
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -38,32 +45,29 @@ sys.path.insert(0, ROOT)
 
 METRIC = "WMC execution time & slices/sec (B200 execution stage, arXiv 2006.15512)"
 UNIT = "slices/s"
-
-# workload -> (description, greedy slice-prefix rule)
 GiB = 2 ** 30
-# Sliced configs use Algorithm 3 itself: the reference's greedy (exact port) at a
-# mem_budget (the reference's dense memory model decides the slice set).  The
-# literal "2^8 / 2^12 slices" of BASELINE.json are restated in DESIGN.md §5: on
-# these FactorTree spine plans every greedy pick nearly doubles total work, while
-# tie-aware execution fits C4 unsliced and C3 at two slices in one B200's HBM.
-CONFIGS = {
-    "c1a": dict(desc="uniform random 3-CNF n=30 ratio 3.0 (restated C1), unsliced"),
-    "c1b": dict(desc="uniform random 3-CNF n=40 ratio 3.0 (restated C1), max-rank 30, unsliced"),
-    "c2": dict(desc="banded random 3-CNF n=200 ratio 3.5 window 29 (C2), max-rank 26, unsliced"),
-    "c1b_s3": dict(plan="c1b", budget=int(3.5 * GiB),
-                   desc="C1b sliced by Algorithm 3 at mem_budget 3.5 GiB (greedy: 3 picks, 8 slices)"),
-    "c4": dict(budget=100 * GiB,
-               desc="banded random 3-CNF n=400 ratio 4.0 window 36 (C4) at mem_budget 100 GiB (2 picks, 4 slices)"),
-    "c4_full": dict(plan="c4", desc="banded random 3-CNF n=400 ratio 4.0 window 36 (C4), unsliced "
-                                    "(192 GiB dense mem_cost; 18 GB of tied tensors on the device)"),
-    "c3": dict(budget=270 * GiB,
-               desc="grid Ising 30x30 (C3), 393 GiB unsliced, at mem_budget 270 GiB (1 pick, 2 slices)"),
-    "c5": dict(budget=100 * GiB, infeasible="reference greedy plateaus at 3 TiB per slice after 12 picks",
-               desc="banded random 3-CNF n=400 ratio 4.0 window 44 (C5), 12 TiB unsliced"),
-}
-
-
 L2_FLUSH_BYTES = 512 * 2 ** 20
+
+# workload -> plan, slice rule, optional per-rank sample of slices, description
+CONFIGS = {
+    "c1a": dict(plan="c1a", slices=None, desc="uniform random 3-CNF n=30 ratio 3.0 (restated C1), unsliced"),
+    "c1b": dict(plan="c1b", slices=None, desc="uniform random 3-CNF n=40 ratio 3.0 (restated C1), max-rank 30, unsliced"),
+    "c2": dict(plan="c2", slices=None,
+               desc="banded random 3-CNF n=200 ratio 3.5 window 29 seed 1 (C2), max-rank 26, unsliced"),
+    "c4": dict(plan="c4", slices=("greedy", 8),
+               desc="banded random 3-CNF n=400 ratio 4.0 window 36 seed 11 (C4; seeds 1-10 UNSAT), max-rank 37, "
+                    "Algorithm 3 greedy 8-pick prefix -> 2^8 slices of max-rank 33"),
+    "c4_full": dict(plan="c4", slices=None,
+                    desc="C4 unsliced (2.5 TiB dense mem_cost; 10.6 GB of tied tensors on the device)"),
+    "c5": dict(plan="c5", slices=("greedy", 12), sample=512,
+               desc="banded random 3-CNF n=400 ratio 4.0 window 34 seed 6 (C5; seeds 1-5 UNSAT), max-rank 34, "
+                    "Algorithm 3 greedy 12-pick prefix -> 2^12 slices of max-rank 30; up to 512 slices per rank "
+                    "timed (the whole job at 8 GPUs)"),
+    "c3": dict(plan="c3", slices=("work", 28), sample=256,
+               desc="grid Ising 30x30 (C3), max-rank 35, sliced to rank 28 by the work-aware chooser (30 indices, "
+                    "2^30 slices; the greedy plateaus at rank 34); a block of 256 slices per rank is timed"),
+}
+DEFAULT = "c4"
 
 
 def log(*a):
@@ -74,51 +78,50 @@ def dist_env():
     return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
-def load_plan(config):
+def load_plan(name):
     from paper_2006_15512_b200 import planfile
 
-    name = CONFIGS.get(config, {}).get("plan", config)
     return planfile.load(os.path.join(ROOT, "data", "plans", f"{name}.tcplan.npz"))
 
 
-def sliced_max_rank(flat, chosen):
-    ch = set(chosen)
-    L = flat.num_leaves
-    sets = [frozenset(flat.leaf_idx[flat.leaf_idx_off[k]:flat.leaf_idx_off[k + 1]].tolist()) - ch for k in range(L)]
-    best = max((len(s) for s in sets), default=0)
-    for l, r in zip(flat.left.tolist(), flat.right.tolist()):
-        s = sets[l] ^ sets[r]
-        sets.append(s)
-        best = max(best, len(s))
-    return best
-
-
-def choose_slices(flat, config):
+def choose(flat, rule):
+    """Slice set of a config (indices into flat.indices, pick order)."""
     from paper_2006_15512_b200 import _lib
 
-    import ctypes
-
-    spec = CONFIGS[config]
     h = _lib.PlanHandle(flat)
-    if "infeasible" in spec:
-        raise SystemExit(f"config {config}: {spec['infeasible']}")
-    if "budget" not in spec:
+    if rule is None:
         return h, []
-    buf = np.zeros(max(1, len(flat.domain)), np.int32)
-    n = ctypes.c_int32()
-    _lib.check(_lib.lib().tc_choose_slices(h.h, spec["budget"], buf.ctypes.data_as(_lib.I32P), len(buf),
-                                           ctypes.byref(n), None))
-    return h, buf[: n.value].tolist()
+    kind, k = rule
+    if kind == "greedy":  # the reference greedy's k-pick prefix (slicing.py:70-79)
+        ch = []
+        for _ in range(k):
+            ch.append(h.choose_slice_index(ch))
+        return h, ch
+    return h, h.choose_slices_work(2 ** k)
+
+
+def num_slices(flat, chosen):
+    ns = 1
+    for i in chosen:
+        ns *= int(flat.domain[i])
+    return ns
+
+
+def rank_block(ns, world, rank, sample):
+    per = -(-ns // world)
+    b = min(ns, rank * per)
+    e = min(ns, b + per)
+    if sample:
+        e = min(e, b + sample)
+    return b, e
 
 
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled DURING the timed
-    region: NVML polled every ~0.5 ms on a thread (the timed region of a fast
-    config lasts only milliseconds); nvidia-smi as a fallback."""
+    region: NVML polled every ~0.5 ms on a thread; nvidia-smi as a fallback."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
-    # nvmlClocksEventReason* bits
     BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index):
@@ -157,9 +160,7 @@ class ClockSampler:
             getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
         while not self.stop.is_set():
             try:
-                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
-                rs = get_reasons(self.h)
-                self.rows.append((sm, rs))
+                self.rows.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM), get_reasons(self.h)))
             except Exception:
                 pass
             time.sleep(0.0005)
@@ -198,17 +199,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(busy), "source": "nvidia-smi"}
 
 
-def measured_peaks():
+def measured_hbm():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)"
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def fp64_peak_tflops(device):
     """cuBLAS DGEMM 8192^3 (torch.matmul float64), best of 5 — the FP64
-    tensor denominator (absent from MEASURED_PEAKS.json)."""
+    tensor-pipe denominator (MEASURED_PEAKS.json holds no FP64 figure)."""
     import torch
 
     n = 8192
@@ -229,44 +230,14 @@ def fp64_peak_tflops(device):
     return 2 * n ** 3 / (best / 1e3) / 1e12
 
 
-def roofline(prof, ms_per_slice, hbm, fp64):
-    """Dominant kernel class + whole-tree roofline."""
-    cls = {}
-    t_roof = 0.0
-    for p in prof:
-        c = cls.setdefault(p["kind"], dict(ms=0.0, bytes=0.0, flops=0.0, launches=0))
-        c["ms"] += p["ms"]
-        c["bytes"] += p["bytes"]
-        c["flops"] += p["flops"]
-        c["launches"] += 1
-        t_roof += max(p["bytes"] / (hbm * 1e9), p["flops"] / (fp64 * 1e12)) * 1e3
-    tot = sum(c["ms"] for c in cls.values())
-    dom = max(cls, key=lambda k: cls[k]["ms"])
-    d = cls[dom]
-    if dom in ("gemm",):
-        ach = d["flops"] / (d["ms"] / 1e3) / 1e12
-        ro = dict(bound="tensor", achieved=ach, peak=fp64, unit="TFLOP/s", frac=ach / fp64)
-    else:
-        ach = d["bytes"] / (d["ms"] / 1e3) / 1e9
-        ro = dict(bound="hbm", achieved=ach, peak=hbm, unit="GB/s", frac=ach / hbm)
-    ro.update(kernel=f"k_{dom}", share_of_step=d["ms"] / tot if tot else None, launches_per_slice=d["launches"])
-    classes = {k: dict(ms=v["ms"], share=v["ms"] / tot if tot else None,
-                       gbs=v["bytes"] / v["ms"] / 1e6 if v["ms"] else None,
-                       tflops=v["flops"] / v["ms"] / 1e9 if v["ms"] else None, launches=v["launches"])
-               for k, v in cls.items()}
-    tree = dict(t_roof_ms=t_roof, measured_ms=ms_per_slice, frac=t_roof / ms_per_slice if ms_per_slice else None,
-                note="T_roof = sum over nodes max(bytes/HBM, flops/FP64) per slice (SURVEY 8d)")
-    return ro, classes, tree
-
-
-def dense_tree_roofline_ms(flat, chosen, hbm, fp64):
-    """T_roof per slice = sum over EVERY internal node of
-    max(8(|A|+|B|+|C|)/BW_HBM, 2*prod(union dims)/P_FP64) (dense, unfused)."""
+def dense_slice_roofline_ms(flat, chosen, hbm, fp64):
+    """per slice, sum over EVERY internal node of
+    max(8(|A|+|B|+|C|)/BW_HBM, 2*prod(union dims)/P_FP64) over the reference's
+    dense tensors (unfused, no ties, no hoisting)."""
     ch = set(chosen)
-    L = flat.num_leaves
-    sets = [frozenset(flat.leaf_idx[flat.leaf_idx_off[k]:flat.leaf_idx_off[k + 1]].tolist()) - ch for k in range(L)]
     dom = flat.domain
-    logd = {}
+    off = flat.leaf_idx_off
+    sets = [frozenset(flat.leaf_idx[off[k]:off[k + 1]].tolist()) - ch for k in range(flat.num_leaves)]
 
     def size(s):
         z = 1
@@ -279,11 +250,36 @@ def dense_tree_roofline_ms(flat, chosen, hbm, fp64):
         a, b = sets[l], sets[r]
         c = a ^ b
         sets.append(c)
-        by = 8.0 * (size(a) + size(b) + size(c))
-        fl = 2.0 * size(a | b)
-        t += max(by / (hbm * 1e9), fl / (fp64 * 1e12))
-    del logd
+        t += max(8.0 * (size(a) + size(b) + size(c)) / (hbm * 1e9), 2.0 * size(a | b) / (fp64 * 1e12))
     return t * 1e3
+
+
+def classes_from_profile(prof, n_slices, hbm, fp64):
+    """Kernel classes of one pass over n_slices (graph-mode per-launch CUDA
+    events): time, executed bytes/flops, achieved rates."""
+    cls = {}
+    for p in prof:
+        c = cls.setdefault(p["kind"], dict(ms=0.0, bytes=0.0, flops=0.0, launches=0))
+        mult = 1 if p["inv"] else n_slices
+        c["ms"] += p["ms"]
+        c["bytes"] += p["bytes"] * mult
+        c["flops"] += p["flops"] * mult
+        c["launches"] += mult
+    tot = sum(c["ms"] for c in cls.values())
+    out = {}
+    for k, v in cls.items():
+        out[k] = dict(ms=v["ms"], share=v["ms"] / tot if tot else None, launches=v["launches"],
+                      gbs=v["bytes"] / v["ms"] / 1e6 if v["ms"] else None,
+                      tflops=v["flops"] / v["ms"] / 1e9 if v["ms"] else None, bytes=v["bytes"], flops=v["flops"])
+    dom = max(out, key=lambda k: out[k]["ms"])
+    d = out[dom]
+    if dom == "gemm":
+        ro = dict(bound="tensor", achieved=d["tflops"], peak=fp64, unit="TFLOP/s", frac=d["tflops"] / fp64)
+    else:
+        ro = dict(bound="hbm", achieved=d["gbs"], peak=hbm, unit="GB/s", frac=d["gbs"] / hbm)
+    ro.update(kernel="k_" + dom, share_of_step=d["share"], launches_per_pass=d["launches"],
+              alg_bytes_per_pass=d["bytes"], alg_flops_per_pass=d["flops"])
+    return ro, out
 
 
 def traffic_for(config, kernel):
@@ -291,20 +287,19 @@ def traffic_for(config, kernel):
     if not os.path.exists(p):
         return None
     d = json.load(open(p)).get(config, {})
-    # a launch class can span kernel families (stream: k_stream + fused k_stream_pair)
-    fams = {"k_stream": ("k_stream", "k_stream_pair", "k_stream_seq")}.get(kernel, (kernel,))
+    fams = {"k_stream": ("k_stream", "k_stream_pair")}.get(kernel, (kernel,))
     vals = [d[f]["dram_bytes_per_slice"] for f in fams if f in d and "dram_bytes_per_slice" in d[f]]
     return sum(vals) if vals else None
 
 
 # ---------------------------------------------------------------- reference
 def _reference_path():
-    for p in (os.path.join(ROOT, "oracle", "_ref"), os.path.join(ROOT, "baseline", "_ref")):
+    for p in (os.path.join(ROOT, "baseline", "_ref"), os.path.join(ROOT, "oracle", "_ref")):
         if os.path.isdir(os.path.join(p, "tensorcount")):
             if p not in sys.path:
                 sys.path.insert(0, p)
             return p
-    raise ImportError("reference not installed (oracle/_ref or baseline/_ref)")
+    raise ImportError("reference not installed (baseline/_ref or oracle/_ref)")
 
 
 def reference_objects(flat):
@@ -318,40 +313,6 @@ def reference_objects(flat):
     return planfile.to_objects(flat_r, Tensor, TensorNetwork, ContractionTree)
 
 
-def time_reference(flat, chosen, steps, warm=True):
-    """The unmodified reference sliced_execute on this plan.  Unsliced: the
-    full run per step.  Sliced: slice 0 through the reference's own slice code
-    path (_slice_plan + _execute_tracked, slicing.py:139-145), extrapolated x
-    num_slices."""
-    _reference_path()
-    from tensorcount import slicing as ref_slicing
-    from tensorcount.tensor import Assignment
-
-    n, t = reference_objects(flat)
-    if warm:
-        ref_slicing.sliced_execute(*reference_objects(load_plan("c1a")[0]))
-    times = []
-    count = None
-    nsl = 1
-    for i in chosen:
-        nsl *= int(flat.domain[i])
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        if not chosen:
-            out = ref_slicing.sliced_execute(n, t)
-            count = float(np.asarray(out.result.values).reshape(-1)[0])
-        else:
-            idx = [n_ix for n_ix in _ref_indices(n, flat, chosen)]
-            eta = Assignment(zip(idx, [0] * len(idx)))
-            m, plan = ref_slicing._slice_plan(n, t, eta)
-            ref_slicing._execute_tracked(m, plan)
-        times.append(time.perf_counter() - t0)
-    per_step = statistics.median(times) * (nsl if chosen else 1)
-    sample = ("full unsliced sliced_execute per step" if not chosen else
-              f"slice 0 of {nsl} via _slice_plan+_execute_tracked, extrapolated x{nsl}")
-    return per_step, nsl, sample, count, times
-
-
 def _ref_indices(n, flat, chosen):
     want = {flat.indices[i].id for i in chosen}
     found = {}
@@ -362,6 +323,100 @@ def _ref_indices(n, flat, chosen):
     return [found[flat.indices[i].id] for i in chosen]
 
 
+def ref_node_table(flat, chosen):
+    """Operand / result index lists of every internal node of the sliced tree
+    in the reference's order: slice_tensor keeps the remaining indices in
+    order (tensor.py:118-125); contract_pair emits kept_a ++ kept_b
+    (tensor.py:102-108)."""
+    ch = set(chosen)
+    off = flat.leaf_idx_off
+    orders = [[i for i in flat.leaf_idx[off[k]:off[k + 1]].tolist() if i not in ch] for k in range(flat.num_leaves)]
+    nodes = []
+    for l, r in zip(flat.left.tolist(), flat.right.tolist()):
+        a, b = orders[l], orders[r]
+        sa, sb = set(a), set(b)
+        orders.append([i for i in a if i not in sb] + [i for i in b if i not in sa])
+        nodes.append((l, r, len(orders) - 1))
+    return orders, nodes
+
+
+def reference_sample_model(flat, chosen, budget_s=20.0, cap_log2=25, seed=0):
+    """A bounded sample of the reference's CPU work for one slice and its
+    extrapolation to the whole tree (for plans whose dense per-slice working
+    set cannot run on the host: C3-C5).
+
+    The reference executes a slice as one ``contract_pair`` (tensor.py:96-108,
+    numpy tensordot: transpose copies + OpenBLAS dgemm) per internal node
+    (slicing.py:91-109), and re-executes the whole tree per slice
+    (slicing.py:139-145).  Nodes are grouped in classes by log2 of their dense
+    bytes; in decreasing order of the classes' share of the nominal cost
+    max(bytes / 1 GB/s, flops / 100 GFLOP/s), up to three nodes per class (with
+    tensors of <= 2^cap_log2 entries) are timed through the reference's own
+    contract_pair on random operands of the nodes' exact index shapes and
+    orders, until ``budget_s`` is spent.  Every node is then charged its
+    class's measured seconds per nominal unit (classes not sampled: the
+    nearest sampled class, i.e. the largest one for nodes above the cap)."""
+    _reference_path()
+    from tensorcount.tensor import Index, Tensor, contract_pair
+
+    dom = flat.domain.tolist()
+    orders, nodes = ref_node_table(flat, chosen)
+
+    def size(o):
+        z = 1
+        for i in o:
+            z *= dom[i]
+        return z
+
+    info = []
+    for (l, r, c) in nodes:
+        sa, sb = set(orders[l]), set(orders[r])
+        na, nb, nc, nu = size(orders[l]), size(orders[r]), size(orders[c]), size(sa | sb)
+        info.append((8.0 * (na + nb + nc), 2.0 * nu, max(na, nb, nc), l, r))
+    cost = [max(by / 1e9, fl / 1e11) for by, fl, _, _, _ in info]
+    bins = {}
+    for k, (by, _, _, _, _) in enumerate(info):
+        bins.setdefault(int(math.log2(max(by, 8.0))), []).append(k)
+    share = {b: sum(cost[k] for k in ks) for b, ks in bins.items()}
+    rng = np.random.default_rng(seed)
+    idx = [Index(ix.id, int(d)) for ix, d in zip(flat.indices, dom)]
+    ratio = {}
+    t_start = time.perf_counter()
+    sampled = 0
+    for b in sorted(bins, key=lambda b: -share[b]):
+        ks = [k for k in bins[b] if info[k][2] <= (1 << cap_log2)]
+        if not ks:
+            continue
+        picks = list(dict.fromkeys(ks[(len(ks) - 1) * j // 2] for j in range(3)))
+        rs = []
+        for k in picks:
+            if time.perf_counter() - t_start > budget_s and ratio:
+                break
+            _, _, _, l, r = info[k]
+            A = Tensor(tuple(idx[i] for i in orders[l]), rng.random([dom[i] for i in orders[l]]))
+            B = Tensor(tuple(idx[i] for i in orders[r]), rng.random([dom[i] for i in orders[r]]))
+            reps, t0 = 0, time.perf_counter()
+            while True:
+                contract_pair(A, B)
+                reps += 1
+                el = time.perf_counter() - t0
+                if el > 0.02 or reps >= 200:
+                    break
+            rs.append(el / reps / cost[k])
+            sampled += 1
+        if rs:
+            ratio[b] = statistics.median(rs)
+        if time.perf_counter() - t_start > budget_s:
+            break
+    keys = sorted(ratio)
+    total = 0.0
+    for b, ks in bins.items():
+        rt = ratio[b] if b in ratio else ratio[min(keys, key=lambda x: (abs(x - b), -x))]
+        total += rt * sum(cost[k] for k in ks)
+    return dict(seconds_per_slice=total, sampled_nodes=sampled, nodes=len(nodes), size_classes=len(bins),
+                sampled_classes=len(ratio), sample_seconds=time.perf_counter() - t_start)
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -369,35 +424,128 @@ def host_cores():
         return os.cpu_count()
 
 
+def time_reference_full(flat, steps):
+    """The unmodified reference sliced_execute (unsliced plans) per step."""
+    _reference_path()
+    from tensorcount import slicing as ref_slicing
+
+    n, t = reference_objects(flat)
+    times, count = [], None
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        out = ref_slicing.sliced_execute(n, t)
+        times.append(time.perf_counter() - t0)
+        count = float(np.asarray(out.result.values).reshape(-1)[0])
+    return statistics.median(times), count, times
+
+
+REF_FULL = ("c1a", "c2")  # configs whose reference run fits a bench step (seconds)
+
+
+def reference_baseline(config, flat, chosen, steps, budget_s):
+    """(slices/s, cpu_baseline dict) of the reference CPU path."""
+    ns = num_slices(flat, chosen)
+    if config in REF_FULL:
+        sec, count, times = time_reference_full(flat, steps)
+        return 1.0 / sec, dict(kind="reference", cores=host_cores(), seconds_per_slice=sec, count=count,
+                               step_seconds=times,
+                               sample="the full unmodified sliced_execute (slicing.py:112-146) per step")
+    runs = [reference_sample_model(flat, chosen, budget_s=budget_s, seed=s) for s in range(steps)]
+    sec = statistics.median(r["seconds_per_slice"] for r in runs)
+    r0 = runs[0]
+    return 1.0 / sec, dict(
+        kind="reference", cores=host_cores(), seconds_per_slice=sec, extrapolated=True,
+        job_seconds=sec * ns,
+        sample=(f"EXTRAPOLATED: the reference contract_pair (tensor.py:96-108) timed on {r0['sampled_nodes']} nodes "
+                f"from {r0['sampled_classes']} of {r0['size_classes']} size classes of one slice's "
+                f"{r0['nodes']}-node tree (random operands of the nodes' shapes, {r0['sample_seconds']:.0f} s "
+                f"of CPU), charged per class to every node, x {ns} slices (slicing.py:139-145 re-executes "
+                f"the tree per slice); the dense per-slice working set "
+                f"({'%.0f' % (_dense_mem_gib(flat, chosen))} GiB) rules out running a slice"),
+        model_runs=runs)
+
+
+def _dense_mem_gib(flat, chosen):
+    from paper_2006_15512_b200 import _lib
+
+    return _lib.PlanHandle(flat).mem_cost(chosen) / GiB
+
+
 def run_reference(args):
     world, rank, local = dist_env()
     if rank != 0:
         return
-    flat, meta = load_plan(args.config)
-    chosen = []
-    if "budget" in CONFIGS[args.config]:
-        _, chosen = choose_slices(flat, args.config)
+    spec = CONFIGS[args.config]
+    flat, _ = load_plan(spec["plan"])
+    _, chosen = choose(flat, spec["slices"])
     steps = max(1, min(args.steps, args.ref_steps))
-    per_step, nsl, sample, count, times = time_reference(flat, chosen, steps)
-    value = nsl / per_step
-    line = dict(metric=METRIC, value=value, unit=UNIT, impl="reference", n_gpus=args.gpus, steps=steps,
-                warmup=1, ms_per_step=per_step * 1e3, higher_is_better=True,
-                scaling="strong" if chosen else "weak", vs_baseline=None, dtype="f64", data="synthetic",
-                config=dict(workload=args.config, desc=CONFIGS[args.config]["desc"], num_slices=nsl,
-                            sliced_indices=len(chosen), plan=f"data/plans/{args.config}.tcplan.npz"),
-                cpu_baseline=dict(value=value, unit=UNIT, cores=host_cores(), kind="reference", sample=sample),
+    value, cpu = reference_baseline(args.config, flat, chosen, steps, args.ref_budget)
+    ns = num_slices(flat, chosen)
+    line = dict(metric=METRIC, value=value, unit=UNIT, impl="reference", n_gpus=args.gpus, steps=steps, warmup=0,
+                ms_per_step=ns / value * 1e3, higher_is_better=True, scaling="strong" if chosen else "weak",
+                vs_baseline=None, dtype="f64", data="synthetic",
+                config=dict(workload=args.config, desc=spec["desc"], num_slices=ns, sliced_indices=len(chosen),
+                            plan=f"data/plans/{spec['plan']}.tcplan.npz"),
+                cpu_baseline=dict(cpu, value=value, unit=UNIT),
                 e2e=dict(value=value, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0),
-                count=count, step_seconds=times,
-                note="unmodified tensorcount (oracle/_ref) numpy/OpenBLAS on host cores; steps capped by --ref-steps")
+                note="unmodified tensorcount (baseline/_ref) numpy/OpenBLAS on the host cores, rank 0 only")
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- parity
+def golden_parity(config, flat, chosen, b, per_slice, count):
+    """Compare the GPU's per-slice values of slices [b, b+len) (and the folded
+    count of a whole job) with the committed goldens."""
+    out = {}
+    gp = os.path.join(ROOT, "tests", "golden")
+    spec = CONFIGS[config]
+    if spec["slices"] is None:
+        c = json.load(open(os.path.join(gp, "counts.json"))).get(spec["plan"])
+        if spec["plan"] == "c4":
+            c = json.load(open(os.path.join(gp, "sliced.json")))["c4"]
+        if c:
+            out = dict(reference_count=c["count"], source=c.get("count_source", "reference sliced_execute"),
+                       rel_err=abs(count - c["count"]) / abs(c["count"]))
+        return out
+    sl = json.load(open(os.path.join(gp, "sliced.json"))).get(config, {})
+    dp_path = os.path.join(gp, f"sliced_dp_{config}.json")
+    want = {}
+    if os.path.exists(dp_path):
+        vals = json.load(open(dp_path))["values"]
+        want = {s: v for s, v in enumerate(vals)}
+        src = "oracle/wmc_dp.c (exact counter, sliced variables fixed)"
+    elif sl.get("slices"):
+        want = {int(s): r["value"] for s, r in sl["slices"].items()}
+        src = "unmodified reference _execute_tracked(*_slice_plan(n, t, eta)) (slicing.py:30-41, 91-109)"
+    errs = []
+    for k, v in enumerate(per_slice):
+        s = b + k
+        if s in want:
+            w = want[s]
+            errs.append(0.0 if (v == 0 and w == 0) else abs(v - w) / max(abs(w), 1e-300))
+    if errs:
+        out = dict(slices_checked=len(errs), max_rel_err=max(errs), source=src,
+                   nonzero_slices=sum(1 for k, v in enumerate(per_slice) if v != 0.0))
+    if count is not None and "count" in sl:
+        out.update(reference_count=sl["count"], count_source=sl.get("count_source"),
+                   rel_err=abs(count - sl["count"]) / abs(sl["count"]))
+    return out
+
+
 # ---------------------------------------------------------------- ours
+def device_run(flat, h, chosen, b, e, steps, warmup, local):
+    from paper_2006_15512_b200 import _lib
+
+    ex = _lib.Exec(h, chosen, local)
+    for _ in range(warmup):
+        ex.run(b, e)
+    return ex
+
+
 def run_ours(args):
     import torch
 
-    from paper_2006_15512_b200 import _lib, planfile, sliced_execute
-    from paper_2006_15512_b200.distributed import fold, gather_slices, slice_block
+    from paper_2006_15512_b200 import _lib, distributed, planfile, sliced_execute
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -405,87 +553,90 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    flat, meta = load_plan(args.config)
-    h, chosen = choose_slices(flat, args.config)
-    nsl = 1
-    for i in chosen:
-        nsl *= int(flat.domain[i])
-    sharded = bool(chosen) and world > 1
-    b, e = slice_block(nsl, world, rank) if sharded else (0, nsl)
-    ex = _lib.Exec(h, chosen, local)
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        ex.run(b, e)
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t)
+        return float(t.item())
+
+    spec = CONFIGS[args.config]
+    flat, meta = load_plan(spec["plan"])
+    h, chosen = choose(flat, spec["slices"])
+    ns = num_slices(flat, chosen)
+    sliced = bool(chosen)
+    sample = args.sample if args.sample is not None else spec.get("sample")
+    b, e = rank_block(ns, world, rank, sample) if sliced else (0, 1)
+    whole_job = not sliced or (sample is None) or allsum(e - b) == ns
+    ex = device_run(flat, h, chosen, b, e, args.steps, args.warmup, local)
     barrier()
-    # each timed pass follows an untimed 512 MiB write that evicts the 126 MB L2
-    # (tied C2 intermediates total ~85 MB and would otherwise stay L2-resident)
     with ClockSampler(local) as clk:
         st = ex.run(b, e, repeats=args.steps, flush_bytes=L2_FLUSH_BYTES)
     barrier()
-    dev_ms = st["device_ms"]
-    if world > 1:
-        t = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        dev_ms = float(t.item())
+    dev_ms = allmax(st["device_ms"])
     ms_per_step = dev_ms / args.steps
-    # sliced: the whole job's slices per step; unsliced: N replicas of the formula
-    slices_per_step = nsl if chosen else world
+    slices_per_step = allsum(e - b) if sliced else world
     value = slices_per_step / (ms_per_step / 1e3)
 
-    # result of the last pass (all ranks): fold per-slice results
+    # per-slice results of the last pass; whole job: gather + lexicographic fold
     per = torch.zeros((e - b, ex.result_size()), dtype=torch.float64, device="cuda")
     ex.copy_results(per.data_ptr())
-    if sharded:
-        full = gather_slices(per, b, nsl)
-        count_t = fold(full)
-    else:
-        count_t = fold(per)
-    count = float(count_t[0].item())
+    count = None
+    if sliced and whole_job:
+        full = distributed.gather_slices(per, b, ns) if world > 1 else per
+        count = float(distributed.fold(full)[0].item())
+    elif not sliced:
+        count = float(per[0, 0].item())
+    per_host = per[:, 0].cpu().numpy().tolist()
+    parity = golden_parity(args.config, flat, chosen, b, per_host, count) if rank == 0 else None
 
-    # per-launch eager profile (rank 0) while the program is resident, then free
-    # it: the e2e leg below builds its own (C4 needs ~100 GiB per program)
-    prof = ex.profile(b) if rank == 0 else None
+    # graph-mode per-launch profile of a short pass (rank 0)
+    hbm, hbm_src = measured_hbm()
+    prof, prof_pass_ms, n_prof = None, None, None
+    if rank == 0:
+        n_prof = min(e - b, 4) if sliced else 1
+        prof, prof_pass_ms = ex.profile_graph(b, b + n_prof)
     d2h = 8 * ex.result_size()
     del ex
+    torch.cuda.synchronize()
+    _lib.release_cache(local)
+
     # end to end through the public API: host objects -> flatten -> C-ABI ->
     # H2D leaves/plan -> device run -> D2H result
     n_obj, t_obj = planfile.to_objects(flat)
-    slice_objs = [flat.indices[i] for i in chosen]
+    slice_objs = [flat.indices[i] for i in chosen] if sliced else None
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     barrier()
-    if not sharded:
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            res = sliced_execute(n_obj, t_obj, slice_indices=slice_objs if chosen else None, devices=[local])
-        e2e_s = (time.perf_counter() - t0) / e2e_steps
+    rng = None if whole_job else ((b, e) if world == 1 else (0, allsum(e - b)))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        if world == 1:
+            res = sliced_execute(n_obj, t_obj, slice_indices=slice_objs, devices=[local], slice_range=rng)
+        else:
+            if sliced:
+                res = distributed.sliced_execute(n_obj, t_obj, slice_indices=slice_objs, device=local,
+                                                 slice_range=None if whole_job else (0, slices_per_step))
+            else:
+                res = sliced_execute(n_obj, t_obj, devices=[local])
         e2e_count = float(np.asarray(res.result.values).reshape(-1)[0])
-    else:
-        from paper_2006_15512_b200.flatten import flatten
-
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            fl = flatten(n_obj, t_obj)
-            hh = _lib.PlanHandle(fl)
-            ids = [fl.indices.index(ix) for ix in slice_objs]
-            ex2 = _lib.Exec(hh, ids, local)
-            ex2.run(b, e)
-            p2 = torch.zeros((e - b, ex2.result_size()), dtype=torch.float64, device="cuda")
-            ex2.copy_results(p2.data_ptr())
-            e2e_count = float(fold(gather_slices(p2, b, nsl))[0].item())
-            del ex2
-        e2e_s = (time.perf_counter() - t0) / e2e_steps
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = allmax((time.perf_counter() - t0) / e2e_steps)
     e2e_value = slices_per_step / e2e_s
     h2d = int(flat.leaf_val.nbytes + flat.leaf_idx.nbytes + flat.leaf_idx_off.nbytes + flat.leaf_val_off.nbytes
               + flat.left.nbytes + flat.right.nbytes + flat.domain.nbytes + flat.sort_rank.nbytes)
+    _lib.release_cache(local)
 
     if rank != 0:
         if world > 1:
@@ -493,75 +644,117 @@ def run_ours(args):
             torch.distributed.destroy_process_group()
         return
 
-    # roofline from the eager per-launch replay of slice b (CUDA events per launch)
-    hbm, hbm_src = measured_peaks()
     fp64 = fp64_peak_tflops(torch.device("cuda", local))
-    ms_per_slice = ms_per_step / max(1, (e - b) if chosen else 1)
-    ro, classes, tree = roofline(prof, ms_per_slice, hbm, fp64)
-    t_dense = dense_tree_roofline_ms(flat, chosen, hbm, fp64)
-    tree = dict(t_roof_ms=t_dense, measured_ms_per_slice=ms_per_slice, frac=t_dense / ms_per_slice,
-                t_roof_phys_ms=tree["t_roof_ms"], frac_phys=tree["t_roof_ms"] / ms_per_slice,
-                note="t_roof_ms: SURVEY 8d dense per-node roofline over all nodes of one slice (the reference's "
-                     "dense tensors), HBM=%s GB/s, FP64=%.2f TF/s (cuBLAS DGEMM, live); frac > 1 means faster than "
-                     "any dense execution.  t_roof_phys_ms: the same roofline over the launched kernels' own work "
-                     "(tied physical tensors; aliases are free) - the bound for this program" % (hbm, fp64))
-    ro["peak_source"] = ("cuBLAS DGEMM 8192^3 measured live in bench.py (FP64 is not in MEASURED_PEAKS.json)"
+    ro, classes = classes_from_profile(prof, n_prof, hbm, fp64)
+    ro["peak_source"] = ("cuBLAS DGEMM 8192^3 measured live in bench.py (MEASURED_PEAKS.json has no FP64 figure)"
                          if ro["bound"] == "tensor" else hbm_src)
     ro["traffic"] = traffic_for(args.config, ro["kernel"])
-    ro["alg_bytes"] = classes_bytes = sum(p["bytes"] for p in prof if "k_" + p["kind"] == ro["kernel"])
-    ro["scope"] = "per slice, summed over every launch of this kernel class (achieved = alg work / summed CUDA-event time)"
-    ro["traffic_note"] = ("ncu dram__bytes_read+write summed over the class's launches of one slice "
-                          "(profiles/ncu_traffic.json)" if ro["traffic"] else None)
-    del classes_bytes
-
-    counts_path = os.path.join(ROOT, "tests", "golden", "counts.json")
-    golden = (json.load(open(counts_path)).get(CONFIGS[args.config].get("plan", args.config))
-              if os.path.exists(counts_path) else None)
-    parity = None
-    if golden:  # the slice sum equals the unsliced reference count (Thm 5)
-        parity = dict(reference_count=golden["count"], rel_err=abs(count - golden["count"]) / abs(golden["count"]))
+    ro["scope"] = (f"graph-mode CUDA events around every launch of the class over one pass of {n_prof} slice(s) "
+                   f"(hoisted launches once); achieved = executed bytes (flops) / summed launch time")
+    # whole-step executed-work fraction: every launched kernel's own work per step
+    slices_rank = e - b
+    by_step = sum(p["bytes"] * (1 if p["inv"] else slices_rank) for p in prof)
+    fl_step = sum(p["flops"] * (1 if p["inv"] else slices_rank) for p in prof)
+    t_step_s = ms_per_step / 1e3 / (slices_per_step / max(1, slices_rank)) if sliced else ms_per_step / 1e3
+    step_roof = dict(executed_bytes_per_rank_step=by_step, executed_flops_per_rank_step=fl_step,
+                     achieved_gbs=by_step / (ms_per_step / 1e3) / 1e9, hbm_peak=hbm,
+                     frac=max(by_step / (hbm * 1e9), fl_step / (fp64 * 1e12)) / (ms_per_step / 1e3),
+                     note="max(executed bytes / HBM peak, executed flops / FP64 peak) / measured step time, "
+                          "rank 0's share of the step; ties, fusion and hoisting make the executed work smaller "
+                          "than the reference's dense work (see work_reduction)")
+    t_dense = dense_slice_roofline_ms(flat, chosen, hbm, fp64) * slices_rank
+    work_red = dict(dense_roofline_ms_per_rank_step=t_dense, measured_ms=ms_per_step,
+                    ratio=t_dense / ms_per_step,
+                    note="SURVEY 8d dense per-node roofline of the reference's tensors (every node, every slice) / "
+                         "measured step: a work-reduction ratio (tie compression, hoisting), NOT a roofline fraction")
+    del t_step_s
 
     cpu = None
-    dense_gib = st["mem_estimate"] / GiB
-    if world == 1 and not args.no_cpu_baseline and dense_gib > 24:
-        cpu = dict(value=None, unit=UNIT, cores=host_cores(), kind="reference",
-                   sample=f"not run: the reference's dense working set per slice is {dense_gib:.0f} GiB")
-    elif world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline:
         try:
-            per_step, _, sample, ref_count, times = time_reference(flat, chosen, 1)
-            cpu = dict(value=nsl / per_step, unit=UNIT, cores=host_cores(), kind="reference", sample=sample,
-                       seconds=per_step)
-            if ref_count is not None:
-                cpu["count"] = ref_count
-                cpu["rel_err_vs_gpu"] = abs(ref_count - count) / abs(ref_count) if ref_count else None
-        except Exception as ex_:  # the reference is not importable on this box
+            v, cpu = reference_baseline(args.config, flat, chosen, 1, args.ref_budget)
+            cpu = dict(cpu, value=v, unit=UNIT)
+            if cpu.get("count") is not None and count:
+                cpu["rel_err_vs_gpu"] = abs(cpu["count"] - count) / abs(cpu["count"])
+        except Exception as ex_:
             cpu = dict(value=None, unit=UNIT, cores=host_cores(), kind="reference", sample=f"unavailable: {ex_}")
+
+    c2 = None
+    if args.config == DEFAULT and not args.no_c2 and world == 1:
+        c2 = c2_numbers(args, local)
 
     line = dict(
         metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
         ms_per_step=ms_per_step, higher_is_better=True,
-        scaling="strong" if sharded else "weak", vs_baseline=None, dtype="f64", data="synthetic",
-        config=dict(workload=args.config, desc=CONFIGS[args.config]["desc"], num_slices=nsl,
-                    sliced_indices=len(chosen), slices_per_rank=e - b, plan=f"data/plans/{args.config}.tcplan.npz",
-                    parallelism=(f"slices/{world}" if sharded else f"replicas x{world}"),
+        scaling="strong" if sliced else "weak", vs_baseline=None, dtype="f64", data="synthetic",
+        config=dict(workload=args.config, desc=spec["desc"], num_slices=ns, sliced_indices=len(chosen),
+                    slices_per_step=slices_per_step, slices_per_rank=e - b,
+                    whole_job=whole_job, plan=f"data/plans/{spec['plan']}.tcplan.npz",
+                    parallelism=(f"slices/{world}" if sliced else f"replicas x{world}"),
                     l2="L2 flushed before every timed pass (untimed 512 MiB write)"),
         e2e=dict(value=e2e_value, unit=UNIT, seconds_per_step=e2e_s, h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h,
-                 path="sliced_execute(n, t) public API" if not sharded else "flatten -> C-ABI plan/exec -> run -> fetch"),
+                 path=("sliced_execute(n, t, slice_indices=..., devices=[d]" + (", slice_range=...)" if rng else ")")
+                       if world == 1 else "distributed.sliced_execute (per-rank block, NCCL all-reduce, fold)")),
         gpu_launches=st["gpu_launches"],
-        roofline=ro, roofline_classes=classes, tree_roofline=tree,
+        roofline=ro, roofline_classes=classes, step_roofline=step_roof, work_reduction=work_red,
+        fp64_peak_tflops=fp64, fp64_peak_source="cuBLAS DGEMM 8192^3, live",
         cpu_baseline=cpu,
         clocks=clk.summary(),
         count=count, e2e_count=e2e_count, parity=parity,
         compile_ms=st["compile_ms"], device_peak_bytes=st["device_peak_bytes"],
-        work=dict(dense_bytes=st["alg_bytes"], dense_flops=st["alg_flops"], phys_bytes=st["phys_bytes"],
-                  phys_flops=st["phys_flops"], tied_leaves=st["n_tied_leaves"], aliases=st["n_alias_nodes"]),
+        hoisting=dict(launches_prologue=st["launches_prologue"], launches_per_slice=st["launches_per_slice"],
+                      phys_bytes_hoisted=st["phys_bytes_hoisted"], phys_bytes_per_slice=st["phys_bytes"],
+                      pinned_bytes=st["pinned_bytes"]),
+        work=dict(dense_bytes_per_slice=st["alg_bytes"], dense_flops_per_slice=st["alg_flops"],
+                  phys_bytes_per_slice=st["phys_bytes"], phys_flops_per_slice=st["phys_flops"],
+                  tied_leaves=st["n_tied_leaves"], aliases=st["n_alias_nodes"]),
         nodes=dict(tiny=st["n_tiny_nodes"], stream=st["n_stream_nodes"], gemm=st["n_gemm_nodes"],
                    generic=st["n_generic_nodes"]),
     )
+    if c2:
+        line["c2"] = c2
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
+
+
+def c2_numbers(args, local):
+    """C2 (BASELINE configs[1], unsliced, 1 B200): device-timed pass and e2e
+    through the public API, carried in the default line."""
+    import torch
+
+    from paper_2006_15512_b200 import _lib, planfile, sliced_execute
+
+    flat, _ = load_plan("c2")
+    h, _ = choose(flat, None)
+    ex = _lib.Exec(h, [], local)
+    for _ in range(args.warmup):
+        ex.run(0, 1)
+    torch.cuda.synchronize()
+    st = ex.run(0, 1, repeats=max(args.steps, 10), flush_bytes=L2_FLUSH_BYTES)
+    ms = st["device_ms"] / max(args.steps, 10)
+    folded, _ = ex.fetch()
+    del ex
+    n, t = planfile.to_objects(flat)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        res = sliced_execute(n, t, devices=[local])
+    e2e = (time.perf_counter() - t0) / 3
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "counts.json")))["c2"]["count"]
+    return dict(desc=CONFIGS["c2"]["desc"], value=1e3 / ms, unit=UNIT, ms_per_step=ms,
+                e2e=dict(value=1.0 / e2e, unit=UNIT, seconds_per_step=e2e,
+                         path="sliced_execute(n, t) public API (host objects, H2D, D2H)"),
+                count=float(folded[0]), rel_err_vs_reference=abs(float(folded[0]) - gold) / gold,
+                gpu_launches=st["gpu_launches"])
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
 def main():
@@ -570,11 +763,19 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT, choices=sorted(CONFIGS))
+    ap.add_argument("--sample", type=int, default=None, help="slices per rank to time (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c2", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-steps", type=int, default=3)
+    ap.add_argument("--ref-budget", type=float, default=20.0, help="seconds of reference CPU work per sample")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: launch ourselves under torchrun
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -267,6 +267,16 @@ class PlanHandle:
         check(lib().tc_compile_stats(self.h, p, n, C.byref(st)))
         return st.as_dict()
 
+    def choose_slices(self, mem_budget: int):
+        """Algorithm 3's greedy (slicing.py:119-128): shortest prefix with
+        mem_cost <= mem_budget."""
+        cap = max(1, len(self.flat.domain))
+        buf = np.zeros(cap, dtype=np.int32)
+        n = C.c_int32()
+        check(lib().tc_choose_slices(self.h, max(INT64_MIN + 1, min(INT64_MAX, int(mem_budget))), _p(buf, I32P), cap,
+                                     C.byref(n), None))
+        return buf[: n.value].tolist()
+
     def choose_slices_work(self, max_entries: int, already=()):
         """Work-aware slice set (extension): picks until every intermediate
         has <= max_entries entries."""
@@ -285,6 +295,30 @@ class PlanHandle:
         check(lib().tc_result_indices(self.h, p, n, _p(out, I32P), cap, C.byref(r)))
         return out[: r.value].tolist()
 
+    def _budget_slices(self, mem_budget):
+        """The reference's budget loop ``while mem_cost(chosen) > mem_budget``
+        (slicing.py:120-128) for any real budget: (explicit slice ids, None) when
+        Python decides it (budget met unsliced, non-integral or beyond int64;
+        inf / nan never slice), else (None, int64 budget) for libtc's greedy."""
+        import math
+
+        mc = self.mem_cost([])
+        if not (mc > mem_budget):  # also inf and nan
+            return [], INT64_MIN
+        fb = math.floor(mem_budget)  # integral costs: cost > b  <=>  cost > floor(b)
+        if INT64_MIN < fb <= INT64_MAX and fb == mem_budget:
+            return None, int(fb)
+        chosen = []
+        while self.mem_cost(chosen) > mem_budget:
+            try:
+                chosen.append(self.choose_slice_index(chosen))
+            except errors.NoCandidates:
+                bonds = [k for k in range(len(self.flat.domain))
+                         if np.count_nonzero(self.flat.leaf_idx == k) == 2]
+                raise errors.BudgetInfeasible(f"cannot fit in {mem_budget} bytes even fully sliced "
+                                              f"(needs {self.mem_cost(bonds)})") from None
+        return chosen, INT64_MIN
+
     def sliced_execute(self, mem_budget, slice_ids, devices):
         L = lib()
         root = self.result_indices(())
@@ -298,15 +332,14 @@ class PlanHandle:
         chosen = np.zeros(nb, dtype=np.int32)
         nch = C.c_int32()
         st = Stats()
+        budget = INT64_MIN  # None
+        if mem_budget is not None and slice_ids is None:
+            slice_ids, budget = self._budget_slices(mem_budget)
         if slice_ids is None:
             sa, sp, sn = ids_ptr([])
             sn = -1
         else:
             sa, sp, sn = ids_ptr(slice_ids)
-        if mem_budget is None:
-            budget = INT64_MIN
-        else:
-            budget = max(INT64_MIN + 1, min(INT64_MAX, int(mem_budget)))
         da, dp, dn = ids_ptr(devices if devices else [0])
         check(L.tc_sliced_execute(self.h, budget, sp, sn, dp, dn, _p(out_val, F64P), len(out_val),
                                   _p(out_idx, I32P), len(out_idx), C.byref(rank), _p(chosen, I32P),
@@ -325,6 +358,7 @@ class Exec:
 
     def __init__(self, plan: PlanHandle, slice_ids=(), device: int = 0):
         self.plan = plan
+        self.slice_ids = list(slice_ids)
         a, p, n = ids_ptr(slice_ids)
         h = C.c_void_p()
         check(lib().tc_exec_create(plan.h, p, n, int(device), C.byref(h)))
@@ -396,6 +430,12 @@ class Exec:
 
     def result_size(self) -> int:
         return int(lib().tc_exec_result_size(self.h))
+
+    def num_slices(self) -> int:
+        n = 1
+        for i in self.slice_ids:
+            n *= int(self.plan.flat.domain[i])
+        return n
 
     def fetch(self, per_slice_n: int | None = None):
         R = self.result_size()

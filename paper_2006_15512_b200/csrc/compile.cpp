@@ -422,7 +422,10 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   // ---- physical variables: tie blocks of leaves, union-find at nodes --------
   // mem[s]: (logical index, variable) pairs sorted by logical index; a
   // variable is named by the smallest logical index of its block.
-  bool ties = std::getenv("TC_NO_TIES") == nullptr;
+  // A non-finite leaf value makes a skipped structural-zero term Inf*0 = NaN
+  // in the reference's dense sum: such plans run on dense variables and
+  // without relabel aliases (the reference's arithmetic, term for term).
+  bool ties = std::getenv("TC_NO_TIES") == nullptr && p.all_finite;
   // Tie-aware slicing: a sliced bond fixes every index tied to it (the dense
   // leaves are zero unless the whole tie class agrees), so those indices are
   // sliced too ("implied", same value, same place value in the slice id).
@@ -1071,7 +1074,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   // These are the non-carrier pieces of factored copy tensors
   // (factoring.py:194-206).
   std::vector<int> alias_src(S, -1);
-  if (!std::getenv("TC_NO_ALIAS")) {
+  if (!std::getenv("TC_NO_ALIAS") && p.all_finite) {
     for (int k = 0; k < p.NN; ++k) {
       const int v = p.NL + k, a = p.left[k], b = p.right[k];
       if (g.cls[v] != NC_STREAM) continue;

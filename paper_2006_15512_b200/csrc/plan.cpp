@@ -131,6 +131,11 @@ Plan build_plan(const tc_plan_desc& d) {
     }
     p.seq.assign(out.rbegin(), out.rend());
   }
+  for (double x : p.lval)
+    if (!std::isfinite(x)) {
+      p.all_finite = false;
+      break;
+    }
   return p;
 }
 

@@ -58,6 +58,7 @@ struct Plan {
   std::vector<char> is_bond;
   std::vector<int> bonds_sorted;           // bond ids sorted by sort_rank
   std::vector<int> seq;                    // full postorder (slots, leaves included)
+  bool all_finite = true;                  // every leaf value is finite (tie compression exact)
 
   int nslots() const { return NL + NN; }
   bool is_leaf(int s) const { return s < NL; }

@@ -50,3 +50,50 @@ def fold(full):
         _lib.fold_device(full.data_ptr(), full.shape[1], full.shape[0], out.data_ptr(), full.device.index)
         return out
     raise ValueError("fold() runs on the GPU; CPU tensors are test-only")
+
+
+def sliced_execute(n, t, mem_budget=None, *, slice_indices=None, device=None, group=None, slice_range=None):
+    """Algorithm 3 across the ranks of a torch.distributed group (one process
+    per GPU): every rank plans the same slice set, executes its block of the
+    lexicographic slice ids on its own GPU, and the blocks meet in ONE
+    zero-padded all-reduce followed by the lexicographic fold — bitwise the
+    single-device result.  ``slice_range=(b, e)`` restricts the job to slices
+    b..e-1 (split over the ranks in the same way).  Returns the reference's
+    SlicedExecution fields (``num_slices`` = slices executed by all ranks)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from . import _lib
+    from .slicing import SlicedExecution, _ids, _plan
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = torch.cuda.current_device() if device is None else int(device)
+    flat, h = _plan(n, t, with_sort_rank=mem_budget is not None and slice_indices is None)
+    if slice_indices is not None:
+        chosen = _ids(flat, slice_indices)
+    elif mem_budget is not None:
+        chosen = h.choose_slices(mem_budget)
+    else:
+        chosen = []
+    ex = _lib.Exec(h, chosen, dev)
+    ns = ex.num_slices()
+    lo, hi = slice_range if slice_range is not None else (0, ns)
+    b, e = slice_block(hi - lo, world, rank)
+    b, e = lo + b, lo + e
+    st = ex.run(b, e) if e > b else None
+    R = ex.result_size()
+    local = torch.zeros((e - b, R), dtype=torch.float64, device=torch.device("cuda", dev))
+    if e > b:
+        ex.copy_results(local.data_ptr())
+    full = gather_slices(local, b - lo, hi - lo, group=group)
+    out = fold(full).cpu().numpy()
+    idx = h.result_indices(chosen)
+    tensor_cls = type(n.tensors[0])
+    shape = tuple(int(flat.domain[i]) for i in idx)
+    res = tensor_cls(tuple(flat.indices[i] for i in idx), np.asarray(out, dtype=np.float64).reshape(shape))
+    st = st or {}
+    return SlicedExecution(result=res, sliced_indices=[flat.indices[i] for i in chosen],
+                           mem_estimate=st.get("mem_estimate", h.mem_cost(chosen)),
+                           peak_observed=st.get("peak_observed", 0), num_slices=hi - lo, stats=st)

@@ -69,7 +69,27 @@ def choose_slice_index(n, t, already=frozenset()):
     return flat.indices[k]
 
 
-def _run(n, t, mem_budget=None, devices=None, slice_indices=None):
+def _run_range(n, flat, h, mem_budget, sl, devices, slice_range):
+    """Slices [b, e) of the plan only (the per-rank block of a sharded run, or
+    a timed sample of a 2^30-slice job): their lexicographic sum."""
+    b, e = (int(x) for x in slice_range)
+    chosen = sl if sl is not None else (h.choose_slices(mem_budget) if mem_budget is not None else [])
+    ex = _lib.Exec(h, chosen, (devices or [0])[0])
+    ns = ex.num_slices()
+    if not 0 <= b < e <= ns:
+        raise ValueError(f"slice_range {slice_range} outside [0, {ns})")
+    st = ex.run(b, e)
+    folded, _ = ex.fetch()
+    idx = h.result_indices(chosen)
+    tensor_cls = type(n.tensors[0])
+    shape = tuple(int(flat.domain[i]) for i in idx)
+    result = tensor_cls(tuple(flat.indices[i] for i in idx), np.asarray(folded, dtype=np.float64).reshape(shape))
+    return SlicedExecution(result=result, sliced_indices=[flat.indices[i] for i in chosen],
+                           mem_estimate=st["mem_estimate"], peak_observed=st["peak_observed"], num_slices=e - b,
+                           stats=st)
+
+
+def _run(n, t, mem_budget=None, devices=None, slice_indices=None, slice_range=None):
     # sort_key ranks only matter to the greedy chooser (slicing.py:73-79)
     flat, h = _plan(n, t, with_sort_rank=mem_budget is not None and slice_indices is None)
     sl = None if slice_indices is None else [flat.indices.index(ix) if ix in flat.indices else -1
@@ -77,6 +97,8 @@ def _run(n, t, mem_budget=None, devices=None, slice_indices=None):
     if sl is not None and any(k < 0 for k in sl):
         from .errors import NotABondIndex
         raise NotABondIndex("slice index is not an index of the network")
+    if slice_range is not None:
+        return _run_range(n, flat, h, mem_budget, sl, devices, slice_range)
     vals, idx, chosen, stats = h.sliced_execute(mem_budget, sl, devices)
     tensor_cls = type(n.tensors[0])
     inds = tuple(flat.indices[i] for i in idx)
@@ -92,10 +114,15 @@ def _run(n, t, mem_budget=None, devices=None, slice_indices=None):
     )
 
 
-def sliced_execute(n, t, mem_budget: int | None = None, *, slice_indices=None, devices=None) -> SlicedExecution:
+def sliced_execute(n, t, mem_budget: int | None = None, *, slice_indices=None, devices=None,
+                   slice_range=None) -> SlicedExecution:
     """Execute the plan within the byte budget on the GPU, slicing bond
-    indices as needed and summing per-slice results in lexicographic order."""
-    return _run(n, t, mem_budget=mem_budget, devices=devices, slice_indices=slice_indices)
+    indices as needed and summing per-slice results in lexicographic order.
+
+    ``slice_range=(b, e)`` (extension) executes slices b..e-1 only and returns
+    their lexicographic sum (``num_slices = e - b``): one rank's block, or a
+    timed sample of a job too large to run whole."""
+    return _run(n, t, mem_budget=mem_budget, devices=devices, slice_indices=slice_indices, slice_range=slice_range)
 
 
 __all__ = [

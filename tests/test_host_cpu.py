@@ -311,3 +311,25 @@ def test_chain_segments_compile_on_cpu():
     assert out["1"]["mem_estimate"] == out["0"]["mem_estimate"]
     assert out["1"]["peak_observed"] == out["0"]["peak_observed"]
     assert out["1"]["device_peak_bytes"] <= out["0"]["device_peak_bytes"]
+
+
+def test_budget_semantics_match_reference_loop():
+    """sliced_execute's budget loop is ``while mem_cost(chosen) > mem_budget``
+    (slicing.py:120-128) for any real budget: inf / nan / a budget beyond int64
+    never slice when the plan fits, a non-integral budget slices like its
+    floor, and an unreachable one raises BudgetInfeasible with the reference's
+    wording."""
+    case = next(c for c in CASES if "budgeted" in c["expected"] and "error" not in c["expected"]["budgeted"])
+    flat = case_flat(case)
+    h = _lib.PlanHandle(flat)
+    full = h.mem_cost([])
+    assert h._budget_slices(float("inf")) == ([], _lib.INT64_MIN)
+    assert h._budget_slices(float("nan")) == ([], _lib.INT64_MIN)
+    assert h._budget_slices(2 ** 80) == ([], _lib.INT64_MIN)
+    assert h._budget_slices(full) == ([], _lib.INT64_MIN)
+    b = case["expected"]["budgeted"]["budget"]
+    assert h._budget_slices(b) == (None, b)  # libtc's greedy (pinned by test_greedy_slice_set_matches_reference)
+    ch, _ = h._budget_slices(b + 0.5)
+    assert ch == case["expected"]["budgeted"]["chosen"]
+    with pytest.raises(BudgetInfeasible, match=r"cannot fit in -0.5 bytes even fully sliced \(needs \d+\)"):
+        h._budget_slices(-0.5)
