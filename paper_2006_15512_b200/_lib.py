@@ -384,7 +384,7 @@ class Exec:
         """Per-slice results of the last run -> caller's device buffer."""
         check(lib().tc_exec_copy_results(self.h, C.c_void_p(int(dst_device_ptr))))
 
-    KINDS = ["select", "tiny", "stream", "gemm", "generic", "rootcopy", "eta", "gemm_reduce", "seg"]
+    KINDS = ["select", "tiny", "stream", "gemm", "generic", "rootcopy", "eta", "gemm_reduce"]
 
     def profile(self, slice_id: int = 0):
         """Per-launch (kind, slot, ms, alg_bytes, alg_flops) of one eager slice."""

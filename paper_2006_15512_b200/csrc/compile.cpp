@@ -54,9 +54,7 @@ namespace tc {
 
 namespace {
 
-constexpr int64_t kTinyMax = 4096;
-constexpr int64_t kSegMaxEntries = (int64_t)1 << 22;  // chain tensors fused into segments (32 MB)
-constexpr int kSegMinOuter = 9;           // entries per tiny tensor
+constexpr int64_t kTinyMax = 4096;           // entries per tiny tensor
 constexpr int32_t kTinySmemCap = 16 * 1024;  // doubles of intermediates per tiny CTA (128 KB; the
                                              // rest of the 227 KB holds the staged batch)
 constexpr int64_t kAlign = 256;
@@ -1165,8 +1163,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   // simulation's offsets: the prologue finishes before the first slice, so an
   // invariant tensor that only invariant nodes read may share memory with
   // variant ones.  TC_HOIST=0 re-runs everything per slice (bit-identical).
-  const bool hoist_env = !(std::getenv("TC_HOIST") && std::atoi(std::getenv("TC_HOIST")) == 0) &&
-                                !(std::getenv("TC_SEG") && std::atoi(std::getenv("TC_SEG")) == 1);
+  const bool hoist_env = !(std::getenv("TC_HOIST") && std::atoi(std::getenv("TC_HOIST")) == 0);
   const bool hoist = hoist_env && !g.chosen.empty();
   std::vector<char> var_(S, 0), boundary(S, 0);
   const int hoist_dbg = std::getenv("TC_HOIST_DBG") ? std::atoi(std::getenv("TC_HOIST_DBG")) : 0;
@@ -1759,21 +1756,12 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     for (auto& q : pending) arena.release(q.off, q.bytes, q.reader, q.cl);
     pending.clear();
   };
-  struct SegCand {
-    int nA = 0, nC = 0;
-    std::vector<int> src;       // C position -> big-operand position (-1: new variable)
-    std::vector<int64_t> pstC;  // C position -> small-operand stride (0: not a small-operand variable)
-    std::vector<int> kpos;      // summed variables: big-operand positions (ascending)
-    std::vector<int64_t> pstK;  // ... and their small-operand strides
-    bool diag = false;
-  };
   struct StreamOut {
     StreamParams sp{};
     int ns = 0, nf = 0, big = -1, sm = -1;
-    SegCand cand;
   };
   // stream-kernel parameters of node v (false: the shape does not fit k_stream)
-  auto build_stream = [&](int v, StreamOut& o, bool want_cand) -> bool {
+  auto build_stream = [&](int v, StreamOut& o) -> bool {
     const int k = v - p.NL, a = p.left[k], b = p.right[k];
     const auto& Lc = g.layout[v];
     auto [c0, c1] = comps(v);
@@ -1825,27 +1813,6 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         j++;
       }
       std::sort(K.begin(), K.end(), [&](const Comp* x, const Comp* y) { return pg[bigv(x)[0]] < pg[bigv(y)[0]]; });
-      if (want_cand) {  // chain-segment view: C position -> big position / P stride
-        SegCand& sc = o.cand;
-        sc.nA = (int)Lg.size();
-        sc.nC = (int)Lc.size();
-        sc.src.assign(Lc.size(), -1);
-        sc.pstC.assign(Lc.size(), 0);
-        sc.kpos.clear();
-        sc.pstK.clear();
-        sc.diag = false;
-        for (size_t q = 0; q < Lc.size(); ++q) {
-          const Comp* c = ccomp[Lc[q]];
-          if (nbig(c) == 1) sc.src[q] = pg[bigv(c)[0]];
-          else if (nbig(c) > 1) sc.diag = true;
-          if (nsm(c) > 0) sc.pstC[q] = small_off(c);
-        }
-        for (const Comp* c : K) {
-          if (nbig(c) != 1) sc.diag = true;
-          else sc.kpos.push_back(pg[bigv(c)[0]]);
-          sc.pstK.push_back(small_off(c));
-        }
-      }
       for (const Comp* c = c0; c != c1; ++c)
         if (c->c >= 0) ccomp[c->c] = nullptr;
       if (bad) throw Error{-1, "batch"};
@@ -1901,256 +1868,8 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     }
     return false;
   };
-  // ---- chain segments (program.h) ------------------------------------------
-  // A stream node whose big operand is the output of an open segment joins it
-  // while every stage's tile fits kSegTileMax bits; the segment is emitted
-  // (one launch, output allocated then) when its output is read by anything
-  // else.  Tokens name the chain tensor's variables across steps.
-  struct Seg {
-    Loc a_loc{};
-    int64_t a_bytes = 0;
-    int a_prod = -1;
-    std::vector<std::vector<int>> stages;  // tokens by address position
-    std::vector<std::vector<int>> sumt;    // per step: summed tokens
-    std::vector<int> T;                    // tokens summed or created by any step
-    std::vector<SegCand> cand;
-    std::vector<int> vslot;
-    std::vector<Loc> p_loc;
-    std::vector<int64_t> p_bytes;
-    std::vector<int> p_prod;
-    StreamParams sp0{};
-    int ns0 = 0, nf0 = 0;
-    int ntok = 0;
-  };
-  std::vector<Seg> segs;
-  // opt-in (TC_SEG=1): measured slower than k_stream + fused pairs on the
-  // benchmark plans so far
-  static const bool seg_on = std::getenv("TC_SEG") && std::atoi(std::getenv("TC_SEG")) == 1;
-  static const int seg_tile_max =
-      std::getenv("TC_SEG_TILE") ? std::max(6, std::min(kSegTileMax, std::atoi(std::getenv("TC_SEG_TILE")))) : kSegTileMax;
-  // stage tokens after applying step c to `prev` (fresh tokens from `fresh`)
-  auto seg_apply = [](const std::vector<int>& prev, const SegCand& c, int& fresh, std::vector<int>& nt,
-                      std::vector<int>& sumt) {
-    nt.assign(c.nC, -1);
-    for (int q = 0; q < c.nC; ++q) nt[q] = c.src[q] >= 0 ? prev[c.src[q]] : fresh++;
-    sumt.clear();
-    for (int kp : c.kpos) sumt.push_back(prev[kp]);
-  };
-  auto seg_tile = [](int ntok, const std::vector<int>& T, const std::vector<int>& first,
-                     const std::vector<int>& last) {
-    std::vector<char> in(ntok, 0);
-    for (int t : T) in[t] = 1;
-    for (int q = 0; q < kSegLowBits && q < (int)first.size(); ++q) in[first[q]] = 1;
-    for (int q = 0; q < kSegLowBits && q < (int)last.size(); ++q) in[last[q]] = 1;
-    return in;
-  };
-  auto seg_try_append = [&](Seg& S, const SegCand& c) {
-    if ((int)S.vslot.size() >= kSegMaxSteps || (int)S.stages.back().size() != c.nA) return false;
-    for (int64_t x : c.pstC)
-      if (x >= ((int64_t)1 << 30)) return false;
-    for (int64_t x : c.pstK)
-      if (x >= ((int64_t)1 << 30)) return false;
-    int fresh = S.ntok;
-    std::vector<int> nt, st;
-    seg_apply(S.stages.back(), c, fresh, nt, st);
-    std::vector<int> T = S.T;
-    for (int t : st) T.push_back(t);
-    for (int q = 0; q < c.nC; ++q)
-      if (c.src[q] < 0) T.push_back(nt[q]);
-    const auto in = seg_tile(fresh, T, S.stages[0], nt);
-    // tile bits: at most kSegTileMax, and few enough to leave >= 2^kSegMinOuter
-    // outer blocks (one per CTA at a time) when the tensor is large enough
-    auto fits = [&](const std::vector<int>& stg) {
-      int cnt = 0;
-      for (int t : stg) cnt += in[t];
-      return cnt <= std::min(seg_tile_max, std::max(6, (int)stg.size() - kSegMinOuter));
-    };
-    for (auto& stg : S.stages)
-      if (!fits(stg)) return false;
-    if (!fits(nt)) return false;
-    S.stages.push_back(std::move(nt));
-    S.sumt.push_back(std::move(st));
-    S.T = std::move(T);
-    S.ntok = fresh;
-    S.cand.push_back(c);
-    return true;
-  };
-  auto seg_close = [&](int slot) {
-    const int id = (int)g.loc[slot].off;
-    Seg& S = segs[id];
-    const int n = (int)S.vslot.size();
-    const int vlast = S.vslot.back();
-    Step st;
-    st.slot = vlast;
-    if (S.a_prod >= 0) st.deps.push_back(S.a_prod);
-    for (int q : S.p_prod)
-      if (q >= 0) st.deps.push_back(q);
-    haz.clear();
-    const Loc out{LOC_ARENA, arena.alloc(bytes[vlast], haz)};
-    for (int h : haz) st.deps.push_back(h);
-    flush_pending();
-    st.la = S.a_loc;
-    st.lc = out;
-    st.la_bytes = S.a_bytes;
-    st.lc_bytes = bytes[vlast];
-    if (n == 1) {
-      st.kind = ST_STREAM;
-      st.sp = S.sp0;
-      st.ns = S.ns0;
-      st.nf = S.nf0;
-      st.lb = S.p_loc[0];
-      st.lb_bytes = S.p_bytes[0];
-      st.alg_bytes = node_bytes[vlast];
-      st.alg_flops = node_flops[vlast];
-      st.work = S.sp0.nx;
-    } else {
-      const int ns_ = n + 1;
-      const auto in = seg_tile(S.ntok, S.T, S.stages[0], S.stages[n]);
-      std::vector<std::vector<int>> pos(ns_, std::vector<int>(S.ntok, -1)), rank(ns_, std::vector<int>(S.ntok, -1));
-      std::vector<int> tsz(ns_, 0);
-      int tmax = 0;
-      for (int s2 = 0; s2 < ns_; ++s2) {
-        const auto& L = S.stages[s2];
-        for (int q = 0; q < (int)L.size(); ++q) {
-          pos[s2][L[q]] = q;
-          if (in[L[q]]) rank[s2][L[q]] = tsz[s2]++;
-        }
-        tmax = std::max(tmax, tsz[s2]);
-      }
-      SegParams sg{};
-      sg.nsteps = n;
-      sg.nt0 = tsz[0];
-      sg.ntL = tsz[n];
-      sg.tile_doubles = 1 << tmax;
-      g.seg_tile_max = std::max(g.seg_tile_max, sg.tile_doubles);
-      // outer variables: untouched, present in every stage; by input position
-      st.seg_tab_off = (int64_t)g.seg_tab.size();
-      int nouter = 0;
-      for (int t : S.stages[0]) {
-        if (in[t]) continue;
-        ++nouter;
-        g.seg_tab.push_back((int64_t)1 << pos[0][t]);
-        g.seg_tab.push_back((int64_t)1 << pos[n][t]);
-        for (int k2 = 0; k2 < n; ++k2) g.seg_tab.push_back(S.cand[k2].pstC[pos[k2 + 1][t]]);
-      }
-      sg.nouter = nouter;
-      st.seg_gtab_off = (int64_t)g.seg_tab.size();
-      for (int s2 : {0, n})
-        for (int t : S.stages[s2])
-          if (in[t]) g.seg_tab.push_back((int64_t)1 << pos[s2][t]);
-      st.seg_off = (int64_t)g.seg_steps.size();
-      double pbytes = 0, fl = 0;
-      for (int k2 = 0; k2 < n; ++k2) {
-        const SegCand& c = S.cand[k2];
-        SegStep ss{};
-        ss.dig = (int32_t)g.seg_digits.size();
-        std::vector<SegDigit> fd;
-        for (int t : S.stages[k2 + 1]) {
-          if (!in[t]) continue;
-          const int ra = rank[k2][t];
-          const SegDigit d{ra >= 0 ? 1 << ra : 0, (int32_t)c.pstC[pos[k2 + 1][t]], 1 << rank[k2 + 1][t], 0};
-          if (ra >= 0) g.seg_digits.push_back(d), ss.nx++;
-          else fd.push_back(d), ss.nf++;
-        }
-        g.seg_digits.insert(g.seg_digits.end(), fd.begin(), fd.end());
-        for (size_t u = 0; u < S.sumt[k2].size(); ++u)
-          g.seg_digits.push_back(SegDigit{1 << rank[k2][S.sumt[k2][u]], (int32_t)c.pstK[u], 0, 0});
-        ss.ns = (int32_t)S.sumt[k2].size();
-        ss.pst = -1;
-        ss.pn = (int32_t)(S.p_bytes[k2] / 8);
-        {
-          bool outer_free = true;  // P offset does not depend on the outer block
-          for (int t : S.stages[0])
-            if (!in[t] && c.pstC[pos[k2 + 1][t]] != 0) outer_free = false;
-          if (outer_free && sg.pst_doubles + ss.pn <= kSegPStageMax) {
-            ss.pst = sg.pst_doubles;
-            sg.pst_doubles += (ss.pn + 1) & ~1;
-          }
-        }
-        g.seg_steps.push_back(ss);
-        g.seg_P.push_back(S.p_loc[k2]);
-        pbytes += (double)S.p_bytes[k2];
-        fl += node_flops[S.vslot[k2]];
-      }
-      st.kind = ST_SEG;
-      st.sg = sg;
-      st.alg_bytes = (double)S.a_bytes + (double)bytes[vlast] + pbytes;
-      st.alg_flops = fl;
-      st.work = (int64_t)1 << nouter;
-      g.n_seg++;
-      g.n_seg_steps += n;
-    }
-    const int me = (int)g.steps.size();
-    g.steps.push_back(st);
-    if (S.a_loc.kind == LOC_ARENA) arena.release(S.a_loc.off, S.a_bytes, me);
-    for (int k2 = 0; k2 < n; ++k2)
-      if (S.p_loc[k2].kind == LOC_ARENA) arena.release(S.p_loc[k2].off, S.p_bytes[k2], me);
-    producer[vlast] = me;
-    g.loc[vlast] = out;
-    producer[slot] = me;
-    g.loc[slot] = out;
-  };
-  // stream node v into a segment (false: emit it the ordinary way)
-  auto try_seg = [&](int v) {
-    // large chain tensors stream at HBM speed step by step (k_stream, fused
-    // pairs); segments pay off where each step is a small, latency-bound launch
-    {
-      const int k = v - p.NL;
-      if (std::max({size[p.left[k]], size[p.right[k]], size[v]}) > kSegMaxEntries) return false;
-    }
-    StreamOut so;
-    if (!build_stream(v, so, true) || so.cand.diag) return false;
-    const int big = so.big, sm = so.sm;
-    if (g.loc[sm].kind == LOC_SEG) seg_close(sm);
-    g.n_stream++;
-    if (g.loc[big].kind == LOC_SEG) {
-      const int id = (int)g.loc[big].off;
-      if (seg_try_append(segs[id], so.cand)) {
-        Seg& S = segs[id];
-        S.vslot.push_back(v);
-        S.p_loc.push_back(g.loc[sm]);
-        S.p_bytes.push_back(bytes[sm]);
-        S.p_prod.push_back(producer[sm]);
-        g.loc[v] = Loc{LOC_SEG, id};
-        producer[v] = -1;
-        return true;
-      }
-      seg_close(big);
-    }
-    Seg S;
-    S.a_loc = g.loc[big];
-    S.a_bytes = bytes[big];
-    S.a_prod = producer[big];
-    S.ntok = so.cand.nA;
-    S.stages.emplace_back(so.cand.nA);
-    for (int q = 0; q < so.cand.nA; ++q) S.stages[0][q] = q;
-    int fresh = S.ntok;
-    std::vector<int> nt, st;
-    seg_apply(S.stages[0], so.cand, fresh, nt, st);
-    for (int t : st) S.T.push_back(t);
-    for (int q = 0; q < so.cand.nC; ++q)
-      if (so.cand.src[q] < 0) S.T.push_back(nt[q]);
-    S.ntok = fresh;
-    S.stages.push_back(std::move(nt));
-    S.sumt.push_back(std::move(st));
-    S.cand.push_back(so.cand);
-    S.vslot.push_back(v);
-    S.p_loc.push_back(g.loc[sm]);
-    S.p_bytes.push_back(bytes[sm]);
-    S.p_prod.push_back(producer[sm]);
-    S.sp0 = so.sp;
-    S.ns0 = so.ns;
-    S.nf0 = so.nf;
-    segs.push_back(std::move(S));
-    g.loc[v] = Loc{LOC_SEG, (int64_t)segs.size() - 1};
-    producer[v] = -1;
-    return true;
-  };
   auto emit_node = [&](int v) {
     const int k = v - p.NL, a = p.left[k], b = p.right[k];
-    if (seg_on && g.cls[v] == NC_STREAM && try_seg(v)) return;
-    for (int c : {a, b})
-      if (g.loc[c].kind == LOC_SEG) seg_close(c);
     Step st;
     st.slot = v;
     st.inv = hoist && !var_[v];
@@ -2172,7 +1891,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     bool done = false;
     if (g.cls[v] == NC_STREAM) {
       StreamOut so;
-      if (build_stream(v, so, false)) {
+      if (build_stream(v, so)) {
         st.kind = ST_STREAM;
         st.sp = so.sp;
         st.ns = so.ns;
@@ -2394,7 +2113,6 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     emit_node(v);
   }
 
-  if (g.loc[p.root].kind == LOC_SEG) seg_close(p.root);
   flush_pending();
   tmark("root copy");
   accounting.get();  // rethrows TC_OVERFLOW from the accounting thread

@@ -13,14 +13,14 @@ namespace tc {
 enum NodeClass : int8_t { NC_LEAF = 0, NC_TINY = 1, NC_STREAM = 2, NC_GEMM = 3, NC_GENERIC = 4, NC_ALIAS = 5 };
 
 // Where an operand lives at run time.
-enum LocKind : int8_t { LOC_LEAF = 0, LOC_SLICED = 1, LOC_ARENA = 2, LOC_SMEM = 3, LOC_SEG = 4 };  // SEG: inside an open chain segment (off = segment id)
+enum LocKind : int8_t { LOC_LEAF = 0, LOC_SLICED = 1, LOC_ARENA = 2, LOC_SMEM = 3 };
 struct Loc {
   LocKind kind;
   int64_t off;  // doubles (LEAF: into leaf values, SLICED: into sliced buffer) or bytes (ARENA)
 };
 
 enum StepKind : int8_t {
-  ST_SELECT, ST_TINY, ST_STREAM, ST_GEMM, ST_GENERIC, ST_ROOTCOPY, ST_ETA, ST_GEMM_REDUCE, ST_SEG
+  ST_SELECT, ST_TINY, ST_STREAM, ST_GEMM, ST_GENERIC, ST_ROOTCOPY, ST_ETA, ST_GEMM_REDUCE
 };
 
 struct Step {
@@ -38,8 +38,6 @@ struct Step {
   int64_t la_bytes = 0, lb_bytes = 0, lc_bytes = 0;  // their extents
   int64_t gdig_off = 0;            // generic digits offset (in GDigit units)
   int64_t work = 0;                // elements (for launch sizing)
-  SegParams sg{};                  // ST_SEG (pointers filled at upload)
-  int64_t seg_off = 0, seg_tab_off = 0, seg_gtab_off = 0;  // into Program::seg_steps / seg_tab
   double alg_bytes = 0, alg_flops = 0;  // algorithmic traffic / flops of the node(s)
 };
 
@@ -65,12 +63,6 @@ struct Program {
   int32_t tiny_dig_max = 0;        // per-batch digit block (max over batches)
   // generic digits
   std::vector<GDigit> gdigits;
-  std::vector<SegStep> seg_steps;  // P holds nothing: seg_P has the locations
-  std::vector<Loc> seg_P;
-  std::vector<SegDigit> seg_digits;
-  std::vector<int64_t> seg_tab;
-  int32_t seg_tile_max = 0;        // doubles
-  int n_seg = 0, n_seg_steps = 0;
   // compressed (tied) leaf values, placed after the raw leaf values on device
   std::vector<double> cvals;
   // dense result entry -> physical root offset (-1: structural zero); empty = identity

@@ -66,9 +66,10 @@ __global__ void k_rootcopy(const RootCopyParams p) {
 __global__ void k_eta(int64_t* eta) {
   pdl_launch();
   pdl_wait();
-  eta[0] += 1;
+  eta[0] += eta[2];  // lane stride (1 without slice lanes)
 }
-__global__ void k_eta_reset(int64_t* eta) { eta[0] = eta[1]; }
+// eta = [current slice, first slice of the pass, lane stride, lane]
+__global__ void k_eta_reset(int64_t* eta) { eta[0] = eta[1] + eta[3]; }
 
 // L2 eviction between timed passes (benchmark only): stream a scratch buffer
 __global__ void k_flush(double4* buf, int64_t n, double v) {
@@ -578,37 +579,6 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream_pair(const StreamPair
   pdl_launch();
 }
 
-// A run of consecutive stream steps in ONE cooperative launch: all CTAs take
-// each step in turn, a grid barrier between steps (the launch gap and ramp of
-// a separate kernel cost more than the barrier for the small steps of tied
-// programs).  Step shapes are limited so the kernel's registers stay at two
-// CTAs per SM.
-constexpr int kSeqMaxNS = 2, kSeqMaxNF = 3;
-__global__ void __launch_bounds__(kStreamThreads, 2)
-    k_stream_seq(const StreamParams* __restrict__ steps, const int* __restrict__ keys, int n, int logG) {
-  __shared__ StreamParams sp;
-  __shared__ double Ps[kStreamStageMax];
-  cg::grid_group grid = cg::this_grid();
-  for (int i = 0; i < n; ++i) {
-    {
-      const uint32_t* src = (const uint32_t*)(steps + i);
-      uint32_t* dst = (uint32_t*)&sp;
-      for (int w = threadIdx.x; w < (int)(sizeof(StreamParams) / 4); w += blockDim.x) dst[w] = src[w];
-    }
-    __syncthreads();
-    switch (keys[i]) {
-#define SQ(a, b) \
-  case a * 8 + b: stream_run<a, b>(sp, Ps, blockIdx.x, logG); break;
-      SQ(0, 0) SQ(0, 1) SQ(0, 2) SQ(0, 3)
-      SQ(1, 0) SQ(1, 1) SQ(1, 2) SQ(1, 3)
-      SQ(2, 0) SQ(2, 1) SQ(2, 2) SQ(2, 3)
-#undef SQ
-      default: break;
-    }
-    grid.sync();
-  }
-}
-
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -888,167 +858,5 @@ __global__ void k_generic(const GenericParams p) {
   }
 }
 
-
-// ---------------------------------------------------------------------------
-// K2s: a chain segment (program.h "chain segments").  One CTA per outer
-// assignment at a time: gather the input tile, run the steps smem -> smem,
-// scatter the output tile.  A step is k_stream's contraction on the tile: a
-// thread owns one kept assignment x (and a share of the new variables f),
-// holds its 2^ns input values in registers and forms each output as
-// sum_s a[s] * P[s, f] in ascending s from 0.0 -- k_stream's exact order, so
-// a segment computes the same bits as its steps launched one by one.
-constexpr int kSegThreadsLog = 8;
-constexpr int kSegThreads = 1 << kSegThreadsLog;
-
-// one segment step for one thread (NS summed digits): k_stream's per-x work
-template <int NS>
-__device__ __forceinline__ void seg_step(const double* __restrict__ X, double* __restrict__ Y,
-                                         const double* __restrict__ B, int la, int lb, int lc, int fg,
-                                         int gb, int FV, int nxh, const int* oxA, const int* oxB, const int* oxC,
-                                         const int* osA, const int* osB, const int* ofB, const int* ofC) {
-  constexpr int SV = 1 << NS;
-  for (int h = 0; h < nxh; ++h) {
-    const int ya = la + oxA[h], yb = lb + oxB[h], yc = lc + oxC[h];
-    double a[SV];
-#pragma unroll
-    for (int s = 0; s < SV; ++s) a[s] = X[ya + osA[s]];
-#pragma unroll 2
-    for (int i = 0; i < FV; ++i) {
-      const int f = fg + (i << gb);
-      const double* Pf = B + yb + ofB[f];
-      double acc = 0.0;
-#pragma unroll
-      for (int s = 0; s < SV; ++s) acc = fma(a[s], Pf[osB[s]], acc);
-      Y[yc + ofC[f]] = acc;
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kSegThreads, 4) k_seg(const SegParams p) {
-  extern __shared__ double sm[];
-  double* const buf0 = sm;
-  double* const buf1 = sm + p.tile_doubles;
-  __shared__ SegStep ss[kSegMaxSteps];
-  __shared__ SegDigit dg[kSegMaxSteps][kSegMaxDig];
-  // per step, offsets of: kept digits above the 8 a thread fixes (A, P, C),
-  // summed assignments (A, P), new assignments (P, C)
-  __shared__ int oxA[kSegMaxSteps][16], oxB[kSegMaxSteps][16], oxC[kSegMaxSteps][16];
-  __shared__ int osA[kSegMaxSteps][16], osB[kSegMaxSteps][16];
-  __shared__ int ofB[kSegMaxSteps][32], ofC[kSegMaxSteps][32];
-  __shared__ int lxA[kSegMaxSteps][32], lxB[kSegMaxSteps][32], lxC[kSegMaxSteps][32];  // kept bits 0-3, 4-7
-  __shared__ int64_t gh[16], sh[16];
-  int64_t* const otab = (int64_t*)(sm + 2 * p.tile_doubles);  // outer strides, staged  // gather / scatter offsets of tile bits >= 8
-  __shared__ int64_t obase[2 + kSegMaxSteps];
-  const int tid = threadIdx.x;
-  const int n = p.nsteps;
-  for (int k = tid; k < n; k += blockDim.x) ss[k] = p.steps[k];
-  __syncthreads();
-  for (int q = tid; q < n * kSegMaxDig; q += blockDim.x) {
-    const int k = q / kSegMaxDig, j = q % kSegMaxDig;
-    if (j < ss[k].nx + ss[k].nf + ss[k].ns) dg[k][j] = p.digs[ss[k].dig + j];
-  }
-  __syncthreads();
-  for (int q = tid; q < n * 32; q += blockDim.x) {
-    const int k = q >> 5, e = q & 31;
-    const SegStep& t = ss[k];
-    const SegDigit* D = dg[k];
-    const int xl = min(t.nx, kSegThreadsLog);
-    if (e < 16) {
-      int a = 0, b = 0, c = 0;
-      for (int j = 0; j < 4; ++j)
-        if (((e >> j) & 1) && xl + j < t.nx) a += D[xl + j].sa, b += D[xl + j].sb, c += D[xl + j].sc;
-      oxA[k][e] = a, oxB[k][e] = b, oxC[k][e] = c;
-      a = b = 0;
-      for (int j = 0; j < t.ns; ++j)
-        if ((e >> j) & 1) a += D[t.nx + t.nf + j].sa, b += D[t.nx + t.nf + j].sb;
-      osA[k][e] = a, osB[k][e] = b;
-    }
-    int b = 0, c = 0;
-    for (int j = 0; j < t.nf; ++j)
-      if ((e >> j) & 1) b += D[t.nx + j].sb, c += D[t.nx + j].sc;
-    ofB[k][e] = b, ofC[k][e] = c;
-    {
-      const int j0 = (e >> 4) * 4;  // e < 16: bits 0-3, else bits 4-7 (of the xl a thread fixes)
-      int a2 = 0, b2 = 0, c2 = 0;
-      for (int j = 0; j < 4; ++j)
-        if (((e >> j) & 1) && j0 + j < xl) a2 += D[j0 + j].sa, b2 += D[j0 + j].sb, c2 += D[j0 + j].sc;
-      lxA[k][e] = a2, lxB[k][e] = b2, lxC[k][e] = c2;
-    }
-  }
-  for (int q = tid; q < p.nouter * (2 + n); q += blockDim.x) otab[q] = p.otab[q];
-  double* const pstage = (double*)(otab + p.nouter * (2 + n));  // outer-independent small operands
-  if (tid < 32) {
-    const int e = tid & 15;
-    const int64_t* T = p.gtab + (tid < 16 ? 0 : p.nt0);
-    const int nt = tid < 16 ? p.nt0 : p.ntL;
-    int64_t o = 0;
-    for (int j = 0; j < 4; ++j)
-      if (((e >> j) & 1) && kSegThreadsLog + j < nt) o += T[kSegThreadsLog + j];
-    (tid < 16 ? gh : sh)[e] = o;
-  }
-  // this thread's tile entries e = tid + k * 2^8: low-bit offsets once
-  int64_t lo_g = 0, lo_s = 0;
-  for (int j = 0; j < kSegThreadsLog; ++j)
-    if ((tid >> j) & 1) {
-      if (j < p.nt0) lo_g += p.gtab[j];
-      if (j < p.ntL) lo_s += p.gtab[p.nt0 + j];
-    }
-  const int n0 = 1 << p.nt0, nL = 1 << p.ntL;
-  const int nk0 = p.nt0 > kSegThreadsLog ? 1 << (p.nt0 - kSegThreadsLog) : 1;
-  const int nkL = p.ntL > kSegThreadsLog ? 1 << (p.ntL - kSegThreadsLog) : 1;
-  const int ncol = 2 + n;
-  pdl_wait();  // operands are produced by earlier launches
-  for (int k = 0; k < n; ++k)  // (ordered before use by the block loop's first barrier)
-    if (ss[k].pst >= 0)
-      for (int q = tid; q < ss[k].pn; q += blockDim.x) pstage[ss[k].pst + q] = __ldg(ss[k].P + q);
-  const int64_t nblocks = (int64_t)1 << p.nouter;
-  for (int64_t o = blockIdx.x; o < nblocks; o += gridDim.x) {
-    if (tid < ncol) {
-      int64_t acc = 0;
-      for (int b = 0; b < p.nouter; ++b)
-        if ((o >> b) & 1) acc += otab[b * ncol + tid];
-      obase[tid] = acc;
-    }
-    __syncthreads();  // also: the previous block's scatter is done with the tiles
-    if (tid < n0) {
-      const double* Ab = p.A + obase[0] + lo_g;
-#pragma unroll 4
-      for (int k = 0; k < nk0; ++k) buf0[tid + (k << kSegThreadsLog)] = __ldcs(Ab + gh[k]);
-    }
-    __syncthreads();
-    double* X = buf0;
-    double* Y = buf1;
-    for (int k = 0; k < n; ++k) {
-      const SegStep& t = ss[k];
-      // thread -> (low kept bits, group of new assignments)
-      const int xl = min(t.nx, kSegThreadsLog);
-      const int gb = min(t.nf, kSegThreadsLog - xl);
-      if ((tid >> (xl + gb)) == 0) {
-        const int xlo = tid & ((1 << xl) - 1), fg = tid >> xl;
-        const int e0 = xlo & 15, e1 = 16 + (xlo >> 4);
-        const int la = lxA[k][e0] + lxA[k][e1], lb = lxB[k][e0] + lxB[k][e1], lc = lxC[k][e0] + lxC[k][e1];
-        const double* B = t.pst >= 0 ? pstage + t.pst : t.P + obase[2 + k];
-        const int FV = 1 << (t.nf - gb), nxh = 1 << (t.nx - xl);
-        switch (t.ns) {
-          case 0: seg_step<0>(X, Y, B, la, lb, lc, fg, gb, FV, nxh, oxA[k], oxB[k], oxC[k], osA[k], osB[k], ofB[k], ofC[k]); break;
-          case 1: seg_step<1>(X, Y, B, la, lb, lc, fg, gb, FV, nxh, oxA[k], oxB[k], oxC[k], osA[k], osB[k], ofB[k], ofC[k]); break;
-          case 2: seg_step<2>(X, Y, B, la, lb, lc, fg, gb, FV, nxh, oxA[k], oxB[k], oxC[k], osA[k], osB[k], ofB[k], ofC[k]); break;
-          case 3: seg_step<3>(X, Y, B, la, lb, lc, fg, gb, FV, nxh, oxA[k], oxB[k], oxC[k], osA[k], osB[k], ofB[k], ofC[k]); break;
-          default: seg_step<4>(X, Y, B, la, lb, lc, fg, gb, FV, nxh, oxA[k], oxB[k], oxC[k], osA[k], osB[k], ofB[k], ofC[k]); break;
-        }
-      }
-      __syncthreads();
-      double* tt = X;
-      X = Y;
-      Y = tt;
-    }
-    if (tid < nL) {
-      double* Cb = p.C + obase[1] + lo_s;
-#pragma unroll 4
-      for (int k = 0; k < nkL; ++k) __stcs(Cb + sh[k], X[tid + (k << kSegThreadsLog)]);
-    }
-  }
-  pdl_launch();
-}
 
 }  // namespace tc

@@ -181,44 +181,6 @@ struct TinyGroup {
   int32_t beg, end;
 };
 
-// ---- chain segments (k_seg) ---------------------------------------------------
-// A run of linked stream steps (each step's big operand is the previous step's
-// output) executed in one launch.  The variables the run sums or creates (plus
-// the input's and output's lowest address bits) form a "tile"; every other
-// variable of the chain tensor is "outer" and untouched by the run.  One CTA
-// takes one outer assignment at a time: gathers the input tile into smem, runs
-// every step smem -> smem (each a dim-2 tiny node whose small operand is read
-// from global memory at an outer-dependent offset), scatters the output tile.
-// Intermediates never reach HBM.
-constexpr int kSegTileMax = 12;   // log2 doubles of any stage's tile
-constexpr int kSegMaxSteps = 32;
-constexpr int kSegLowBits = 2;    // input / output address bits always in the tile (32-byte sectors)
-constexpr int kSegPStageMax = 2048;  // doubles of small operands staged per CTA
-constexpr int kSegMaxDig = 16;    // digits per step (nx + nf <= 12, ns <= 4)
-struct SegStep {
-  const double* P;  // small operand (host: arena / leaf placeholder)
-  int32_t nx, nf, ns;  // kept / new / summed tile digits
-  int32_t dig;         // first digit: nx kept, nf new, ns summed (SegDigit)
-  int32_t pst;         // offset of P staged in smem (doubles; P independent of the outer block), -1: global
-  int32_t pn;          // P entries (staged copy)
-};
-// strides of one tile digit: sa in the step's input tile, sb in the small
-// operand, sc in the output tile
-struct SegDigit {
-  int32_t sa, sb, sc, pad;
-};
-struct SegParams {
-  const double* A;
-  double* C;
-  const SegStep* steps;
-  const SegDigit* digs;
-  const int64_t* otab;  // [nouter][2 + nsteps]: A stride, C stride, P stride of each step
-  const int64_t* gtab;  // [nt0] input-tile bit -> A stride, then [ntL] output-tile bit -> C stride
-  int32_t nsteps, nouter, nt0, ntL;
-  int32_t tile_doubles;
-  int32_t pst_doubles;  // staged small operands
-};
-
 // ---- generic mixed-radix contraction (any domain, any size) ---------------
 struct GDigit {
   int64_t dim, sa, sb;

@@ -213,7 +213,6 @@ struct Launch {
   dim3 grid, block;
   unsigned smem = 0;
   int kind = 0, slot = -1;
-  bool coop = false;  // cooperative launch (k_stream_seq: grid barriers)
   bool inv = false;   // slice-invariant: in the prologue graph, once per pass
   double bytes = 0, flops = 0;
   int xbits = -1, ns = 0, nf = 0, ns2 = -1, nf2 = -1;  // stream shape (diagnostics)
@@ -253,13 +252,8 @@ struct tc_exec {
   TinyDigit* tdigs = nullptr;
   TinyGroup* tgroups = nullptr;
   GDigit* gdig = nullptr;
-  SegStep* dseg = nullptr;      // chain segments: step descriptors, digits, tables
-  SegDigit* dsegdig = nullptr;
-  int64_t* dsegtab = nullptr;
   int64_t* rootmap = nullptr;
   double** results_slot = nullptr;  // device copy of `results` read by k_rootcopy
-  StreamParams* seq_params = nullptr;  // k_stream_seq step descriptors
-  int* seq_keys = nullptr;
   std::vector<std::vector<int>> ldeps;  // per launch: launches it depends on
   SelEntry* sel = nullptr;
   SelTerm* selt = nullptr;
@@ -277,27 +271,70 @@ struct tc_exec {
   int64_t last_n = 0;
   double compile_ms = 0;
 
+  // Slice lanes: slices are independent (Thm 5), so a pass
+  // runs them on K concurrent streams, each lane with its own copy of the
+  // per-slice arena, sliced-leaf buffer, tiny descriptors and slice counter
+  // (the pinned hoisted tensors, leaves and result slots are shared).  The
+  // small latency-bound launches of one slice then overlap those of others.
+  // Lane 0 is the main stream and resources above.
+  struct Lane {
+    char* arena = nullptr;
+    double* sliced = nullptr;
+    TinyNode* tnodes = nullptr;
+    int64_t* eta = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+    std::vector<Launch> launches;
+    std::vector<std::vector<int>> ldeps;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+  };
+  std::vector<Lane> xl;  // lanes 1..K-1
+  cudaEvent_t pro_done = nullptr;
+
   ~tc_exec() {
     if (device >= 0) cudaSetDevice(device);
+    for (auto& L : xl) {
+      if (L.stream) cudaStreamSynchronize(L.stream);
+      if (L.gexec) cudaGraphExecDestroy(L.gexec);
+      if (L.graph) cudaGraphDestroy(L.graph);
+      for (void* q : {(void*)L.arena, (void*)L.sliced, (void*)L.tnodes, (void*)L.eta}) dcache().put(device, q);
+      if (L.done) cudaEventDestroy(L.done);
+      if (L.stream) cudaStreamDestroy(L.stream);
+    }
+    if (pro_done) cudaEventDestroy(pro_done);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
     if (gexec_pro) cudaGraphExecDestroy(gexec_pro);
     if (graph_pro) cudaGraphDestroy(graph_pro);
     if (stream) cudaStreamSynchronize(stream);
     for (void* q : {(void*)arena, (void*)leafbuf, (void*)slicedbuf, (void*)tnodes, (void*)tdigs,
-                    (void*)tgroups, (void*)gdig, (void*)dseg, (void*)dsegdig, (void*)dsegtab, (void*)rootmap, (void*)results_slot, (void*)seq_params, (void*)seq_keys, (void*)sel, (void*)selt, (void*)eta, (void*)results,
+                    (void*)tgroups, (void*)gdig, (void*)rootmap, (void*)results_slot, (void*)sel, (void*)selt, (void*)eta, (void*)results,
                     (void*)folded})
       dcache().put(device, q);
     if (stream) cudaStreamDestroy(stream);
   }
 
-  const double* ptr(const Loc& l) const {
+  // device address of a program location for lane k (hoisted pinned tensors
+  // live in lane 0's arena prefix; per-slice buffers in the lane's copies)
+  const double* ptr(const Loc& l, int k = 0) const {
     switch (l.kind) {
       case LOC_LEAF: return leafbuf + l.off;
-      case LOC_SLICED: return slicedbuf + l.off;
-      case LOC_ARENA: return (const double*)(arena + l.off);
+      case LOC_SLICED: return (k ? xl[k - 1].sliced : slicedbuf) + l.off;
+      case LOC_ARENA: return (const double*)((k && l.off >= prog.pinned_bytes ? xl[k - 1].arena : arena) + l.off);
       default: return nullptr;
     }
+  }
+
+  std::vector<TinyNode> tiny_nodes_for(int k) const {
+    const Program& g = prog;
+    std::vector<TinyNode> tn = g.tiny_nodes;
+    for (size_t i = 0; i < tn.size(); ++i) {
+      tn[i].ga = ptr(g.tiny_ga[i], k);
+      tn[i].gb = ptr(g.tiny_gb[i], k);
+      tn[i].gout = (double*)ptr(g.tiny_gout[i], k);
+    }
+    return tn;
   }
 
   void build(const Plan& p, const std::vector<int>& chosen) {
@@ -332,12 +369,7 @@ struct tc_exec {
                            stream));
     }
     if (!g.tiny_nodes.empty()) {
-      std::vector<TinyNode> tn = g.tiny_nodes;
-      for (size_t i = 0; i < tn.size(); ++i) {
-        tn[i].ga = ptr(g.tiny_ga[i]);
-        tn[i].gb = ptr(g.tiny_gb[i]);
-        tn[i].gout = (double*)ptr(g.tiny_gout[i]);
-      }
+      std::vector<TinyNode> tn = tiny_nodes_for(0);
       tnodes = dalloc<TinyNode>(tn.size(), dev_bytes, device);
       tdigs = dalloc<TinyDigit>(std::max<size_t>(1, g.tiny_digits.size()), dev_bytes, device);
       tgroups = dalloc<TinyGroup>(g.tiny_groups.size(), dev_bytes, device);
@@ -348,24 +380,11 @@ struct tc_exec {
       CU(cudaMemcpyAsync(tgroups, g.tiny_groups.data(), g.tiny_groups.size() * sizeof(TinyGroup),
                          cudaMemcpyHostToDevice, stream));
     }
-    if (!g.seg_steps.empty()) {
-      std::vector<SegStep> ss = g.seg_steps;
-      for (size_t i = 0; i < ss.size(); ++i) ss[i].P = ptr(g.seg_P[i]);
-      dseg = dalloc<SegStep>(ss.size(), dev_bytes, device);
-      dsegdig = dalloc<SegDigit>(g.seg_digits.size(), dev_bytes, device);
-      dsegtab = dalloc<int64_t>(std::max<size_t>(1, g.seg_tab.size()), dev_bytes, device);
-      CU(cudaMemcpyAsync(dseg, ss.data(), ss.size() * sizeof(SegStep), cudaMemcpyHostToDevice, stream));
-      CU(cudaMemcpyAsync(dsegdig, g.seg_digits.data(), g.seg_digits.size() * sizeof(SegDigit),
-                         cudaMemcpyHostToDevice, stream));
-      if (!g.seg_tab.empty())
-        CU(cudaMemcpyAsync(dsegtab, g.seg_tab.data(), g.seg_tab.size() * 8, cudaMemcpyHostToDevice, stream));
-      CU(cudaFuncSetAttribute(k_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * g.seg_tile_max * 8 + 64 * (2 + kSegMaxSteps) * 8 + kSegPStageMax * 8));
-    }
     if (!g.gdigits.empty()) {
       gdig = dalloc<GDigit>(g.gdigits.size(), dev_bytes, device);
       CU(cudaMemcpyAsync(gdig, g.gdigits.data(), g.gdigits.size() * sizeof(GDigit), cudaMemcpyHostToDevice, stream));
     }
-    eta = dalloc<int64_t>(2, dev_bytes, device);
+    eta = dalloc<int64_t>(4, dev_bytes, device);
     results_slot = dalloc<double*>(1, dev_bytes, device);
     folded = dalloc<double>((size_t)g.R, dev_bytes, device);
     CU(cudaStreamSynchronize(stream));
@@ -380,7 +399,22 @@ struct tc_exec {
         CU(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
       }
 
-    // ---- launch records (one per step), then the graph from them ----
+    make_launches(0, launches, ldeps, rootcopy_launch);
+    auto t_end = std::chrono::steady_clock::now();
+    setup_ms = std::chrono::duration<double, std::milli>(t_end - t_prog).count();
+    compile_ms = std::chrono::duration<double, std::milli>(t_end - t0).count();
+    count_launches();
+  }
+
+  // launch records of lane k (one per step, then chain-link fusion)
+  void make_launches(int k, std::vector<Launch>& launches, std::vector<std::vector<int>>& ldeps, int& rootcopy_launch) {
+    Program& g = prog;
+    double* slicedbuf = k ? xl[k - 1].sliced : this->slicedbuf;
+    TinyNode* tnodes = k ? xl[k - 1].tnodes : this->tnodes;
+    int64_t* eta = k ? xl[k - 1].eta : this->eta;
+    const int tiny_smem = (int)(g.tiny_smem_doubles + kTinyThreads + g.tiny_stage_doubles) * 8 +
+                          kTinyBatch * (int)sizeof(TinyNode) + g.tiny_dig_max * (int)sizeof(TinyDigit);
+    auto ptr = [&](const Loc& l) { return this->ptr(l, k); };
     launches.clear();
     launches.reserve(g.steps.size());
     for (size_t si = 0; si < g.steps.size(); ++si) {
@@ -433,28 +467,6 @@ struct tc_exec {
             L.xbits = xb, L.ns = st.ns, L.nf = st.nf;
           }
           L.arg(sp);
-          break;
-        }
-        case ST_SEG: {
-          SegParams sg = st.sg;
-          sg.A = ptr(st.la);
-          sg.C = (double*)ptr(st.lc);
-          sg.steps = dseg + st.seg_off;
-          sg.digs = dsegdig;
-          sg.otab = dsegtab + st.seg_tab_off;
-          sg.gtab = dsegtab + st.seg_gtab_off;
-          L.func = (void*)k_seg;
-          L.block = dim3(kSegThreads);
-          L.smem = (2 * sg.tile_doubles + sg.nouter * (2 + sg.nsteps) + sg.pst_doubles) * 8;
-          {
-            static thread_local std::map<int, int> occ;  // smem bytes -> resident CTAs per SM
-            int& o = occ[(int)L.smem];
-            if (o == 0) CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_seg, kSegThreads, L.smem));
-            const int64_t cap = (int64_t)sm_count(device) * std::max(1, o);
-            L.grid = dim3((unsigned)std::min<int64_t>(st.work, cap));
-          }
-          L.xbits = sg.nouter, L.ns = sg.nsteps, L.nf = sg.tile_doubles;
-          L.arg(sg);
           break;
         }
         case ST_GEMM: {
@@ -514,13 +526,7 @@ struct tc_exec {
       }
       launches.push_back(std::move(L));
     }
-    static const bool seq_on = std::getenv("TC_SEQ") && std::atoi(std::getenv("TC_SEQ")) == 1;
-    if (seq_on) group_stream_runs();
-    else fuse_stream_pairs();
-    auto t_end = std::chrono::steady_clock::now();
-    setup_ms = std::chrono::duration<double, std::milli>(t_end - t_prog).count();
-    compile_ms = std::chrono::duration<double, std::milli>(t_end - t0).count();
-    count_launches();
+    fuse_stream_pairs(launches, ldeps, rootcopy_launch);
   }
 
   void count_launches() {
@@ -642,7 +648,7 @@ struct tc_exec {
     return true;
   }
 
-  void fuse_stream_pairs() {
+  void fuse_stream_pairs(std::vector<Launch>& launches, std::vector<std::vector<int>>& ldeps, int& rootcopy_launch) {
     Program& g = prog;
     const size_t S = g.steps.size();
     static const bool on = !(std::getenv("TC_FUSE") && std::atoi(std::getenv("TC_FUSE")) == 0);
@@ -743,103 +749,9 @@ struct tc_exec {
     ldeps = std::move(odeps);
   }
 
-  // TC_SEQ=1: runs of >= 2 consecutive stream steps with small shapes become
-  // one cooperative k_stream_seq launch.  Measured slower (C2 1.56 vs 1.28 ms,
-  // C4 87 vs 70 ms): a step's cost is its DRAM/L2 ramp, not the launch, and the
-  // barrier kernel runs at half the occupancy.  Default: one launch per step.
-  // ldeps[i] = launches launch i depends on (data + WAR edges of its steps).
-  void group_stream_runs() {
-    Program& g = prog;
-    const size_t S = g.steps.size();
-    static const bool on = std::getenv("TC_SEQ") && std::atoi(std::getenv("TC_SEQ")) == 1;
-    auto eligible = [&](size_t i) {
-      const Step& st = g.steps[i];
-      return on && !st.inv && st.kind == ST_STREAM && st.ns <= kSeqMaxNS && st.nf <= kSeqMaxNF;
-    };
-    std::vector<std::pair<size_t, size_t>> runs;  // [first, end)
-    for (size_t i = 0; i < S;) {
-      size_t j = i;
-      while (j < S && eligible(j)) ++j;
-      if (j - i >= 2) runs.push_back({i, j});
-      i = (j == i) ? i + 1 : j;
-    }
-    std::vector<int> lid(S, -1);
-    if (runs.empty()) {
-      ldeps.assign(S, {});
-      for (size_t i = 0; i < S; ++i) ldeps[i] = g.steps[i].deps;
-      return;
-    }
-    int nb = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_stream_seq, kStreamThreads, 0));
-    const int64_t co = (int64_t)std::max(1, nb) * sm_count(device);
-    int logG = 0;
-    while ((int64_t)2 << logG <= co) ++logG;
-    size_t total = 0;
-    for (auto& r : runs) total += r.second - r.first;
-    std::vector<StreamParams> sp(total);
-    std::vector<int> keys(total);
-    int64_t dummy = 0;
-    seq_params = dalloc<StreamParams>(total, dev_bytes, device);
-    seq_keys = dalloc<int>(total, dummy, device);
-    std::vector<Launch> out;
-    std::vector<std::vector<int>> odeps;
-    size_t next_run = 0, pos = 0;
-    for (size_t i = 0; i < S;) {
-      if (next_run < runs.size() && runs[next_run].first == i) {
-        const auto r = runs[next_run++];
-        Launch L;
-        L.kind = ST_STREAM;
-        L.slot = g.steps[r.second - 1].slot;
-        L.coop = true;
-        L.func = (void*)k_stream_seq;
-        L.grid = dim3(1u << logG);
-        L.block = dim3(kStreamThreads);
-        const size_t p0 = pos;
-        std::vector<int> dd;
-        for (size_t k = r.first; k < r.second; ++k) {
-          std::memcpy(&sp[pos], launches[k].blob.data() + launches[k].off[0], sizeof(StreamParams));
-          sp[pos].split_u = 0;  // the cooperative grid walks whole chunks
-          keys[pos] = g.steps[k].ns * 8 + g.steps[k].nf;
-          ++pos;
-          L.bytes += launches[k].bytes;
-          L.flops += launches[k].flops;
-          for (int d : g.steps[k].deps)
-            if ((size_t)d < r.first) dd.push_back(lid[d]);
-          lid[k] = (int)out.size();
-        }
-        L.arg((const StreamParams*)(seq_params + p0));
-        L.arg((const int*)(seq_keys + p0));
-        L.arg((int)(r.second - r.first));
-        L.arg(logG);
-        std::sort(dd.begin(), dd.end());
-        dd.erase(std::unique(dd.begin(), dd.end()), dd.end());
-        out.push_back(std::move(L));
-        odeps.push_back(dd);
-        i = r.second;
-      } else {
-        std::vector<int> dd;
-        for (int d : g.steps[i].deps) dd.push_back(lid[d]);
-        std::sort(dd.begin(), dd.end());
-        dd.erase(std::unique(dd.begin(), dd.end()), dd.end());
-        lid[i] = (int)out.size();
-        if ((int)i == rootcopy_launch) rootcopy_launch = (int)out.size();
-        out.push_back(std::move(launches[i]));
-        odeps.push_back(dd);
-        ++i;
-      }
-    }
-    CU(cudaMemcpyAsync(seq_params, sp.data(), total * sizeof(StreamParams), cudaMemcpyHostToDevice, stream));
-    CU(cudaMemcpyAsync(seq_keys, keys.data(), total * sizeof(int), cudaMemcpyHostToDevice, stream));
-    CU(cudaStreamSynchronize(stream));
-    launches = std::move(out);
-    ldeps = std::move(odeps);
-  }
-
   void launch_one(Launch& L, bool pdl) {
     auto kp = L.params();
-    if (L.coop) {
-      CU(cudaLaunchCooperativeKernel(L.func, L.grid, L.block, kp.kernelParams, L.smem, stream));
-    } else if (pdl) {
+    if (pdl) {
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -862,35 +774,84 @@ struct tc_exec {
   // Two graphs from the explicit launch DAG (data + WAR edges): the prologue
   // (slice-invariant launches, once per pass over the slices) and the
   // per-slice graph.  Edges between the two are implied by stream order.
+  static void instantiate(const std::vector<Launch>& L, const std::vector<std::vector<int>>& deps, bool want_inv,
+                          cudaGraph_t& gr, cudaGraphExec_t& ge) {
+    gr = nullptr;
+    ge = nullptr;
+    std::vector<cudaGraphNode_t> nodes(L.size(), nullptr);
+    for (size_t si = 0; si < L.size(); ++si) {
+      if (L[si].inv != want_inv) continue;
+      if (!gr) CU(cudaGraphCreate(&gr, 0));
+      std::vector<cudaGraphNode_t> dd;
+      for (int d : deps[si])
+        if (L[d].inv == want_inv) dd.push_back(nodes[d]);
+      cudaKernelNodeParams kp = const_cast<Launch&>(L[si]).params();
+      CU(cudaGraphAddKernelNode(&nodes[si], gr, dd.data(), dd.size(), &kp));
+    }
+    if (gr) CU(cudaGraphInstantiate(&ge, gr, 0));
+  }
+
   void ensure_graph() {
     if (gexec) return;
     auto t_graph0 = std::chrono::steady_clock::now();
     count_launches();
-    for (int pass = 0; pass < 2; ++pass) {
-      const bool want_inv = pass == 0;
-      cudaGraph_t gr = nullptr;
-      std::vector<cudaGraphNode_t> nodes(launches.size(), nullptr);
-      for (size_t si = 0; si < launches.size(); ++si) {
-        if (launches[si].inv != want_inv) continue;
-        if (!gr) CU(cudaGraphCreate(&gr, 0));
-        std::vector<cudaGraphNode_t> deps;
-        for (int d : ldeps[si])
-          if (launches[d].inv == want_inv) deps.push_back(nodes[d]);
-        cudaKernelNodeParams kp = launches[si].params();
-        CU(cudaGraphAddKernelNode(&nodes[si], gr, deps.data(), deps.size(), &kp));
-        if (launches[si].coop) {
-          cudaLaunchAttributeValue v{};
-          v.cooperative = 1;
-          CU(cudaGraphKernelNodeSetAttribute(nodes[si], cudaLaunchAttributeCooperative, &v));
-        }
-      }
-      if (!gr) continue;
-      cudaGraphExec_t ge = nullptr;
-      CU(cudaGraphInstantiate(&ge, gr, 0));
-      if (want_inv) graph_pro = gr, gexec_pro = ge;
-      else graph = gr, gexec = ge;
-    }
+    instantiate(launches, ldeps, true, graph_pro, gexec_pro);
+    instantiate(launches, ldeps, false, graph, gexec);
     graph_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_graph0).count();
+  }
+
+  // lanes 1..K-1 (graph mode only): per-lane buffers, launch records, graph
+  void ensure_lanes(int K) {
+    if ((int)xl.size() + 1 >= K) return;
+    const Program& g = prog;
+    if (!pro_done) CU(cudaEventCreateWithFlags(&pro_done, cudaEventDisableTiming));
+    while ((int)xl.size() + 1 < K) {
+      xl.emplace_back();
+      const int k = (int)xl.size();
+      Lane& L = xl.back();
+      int64_t dummy = 0;
+      L.arena = dalloc<char>((size_t)g.arena_bytes, dev_bytes, device);
+      if (g.sliced_doubles) L.sliced = dalloc<double>((size_t)g.sliced_doubles, dev_bytes, device);
+      L.eta = dalloc<int64_t>(4, dummy, device);
+      CU(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
+      CU(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
+      if (!g.tiny_nodes.empty()) {
+        std::vector<TinyNode> tn = tiny_nodes_for(k);
+        L.tnodes = dalloc<TinyNode>(tn.size(), dev_bytes, device);
+        CU(cudaMemcpy(L.tnodes, tn.data(), tn.size() * sizeof(TinyNode), cudaMemcpyHostToDevice));
+      }
+      int rc = -1;
+      make_launches(k, L.launches, L.ldeps, rc);
+      instantiate(L.launches, L.ldeps, false, L.graph, L.gexec);
+    }
+  }
+
+  // lanes for a pass of n slices: TC_LANES (default 4), at most n, and only
+  // while the per-lane copies fit a quarter of the free HBM
+  int lanes_for(int64_t n) {
+    static const int want = std::getenv("TC_LANES") ? std::max(1, std::atoi(std::getenv("TC_LANES"))) : 4;
+    int K = (int)std::min<int64_t>(want, n);
+    if (K <= (int)xl.size() + 1) return std::max(1, K);
+    size_t fr = 0, tot = 0;
+    CU(cudaMemGetInfo(&fr, &tot));
+    const double per = (double)prog.arena_bytes + 8.0 * prog.sliced_doubles + 1e6;
+    while (K > (int)xl.size() + 1 && per * (K - 1 - (int)xl.size()) > 0.25 * (double)fr) --K;
+    return std::max(1, K);
+  }
+
+  // slice counters: [current slice, first slice of the pass, stride, lane]
+  void set_eta(int64_t b, int K) {
+    int64_t h[4] = {b, b, K, 0};
+    CU(cudaMemcpyAsync(eta, h, sizeof(h), cudaMemcpyHostToDevice, stream));
+    for (int k = 1; k < K; ++k) {
+      int64_t hk[4] = {b + k, b, K, k};
+      CU(cudaMemcpyAsync(xl[k - 1].eta, hk, sizeof(hk), cudaMemcpyHostToDevice, stream));
+    }
+    CU(cudaStreamSynchronize(stream));
+  }
+  void reset_eta(int K) {
+    k_eta_reset<<<1, 1, 0, stream>>>(eta);
+    for (int k = 1; k < K; ++k) k_eta_reset<<<1, 1, 0, stream>>>(xl[k - 1].eta);
   }
   double program_ms = 0, setup_ms = 0, graph_ms = 0;
 
@@ -945,14 +906,27 @@ struct tc_exec {
     }
   }
   // one pass over n slices: prologue once, then the per-slice launches
-  void launch_pass(int64_t n, bool eager) {
+  // (round-robin over K lanes; lane 0 is the main stream)
+  void launch_pass(int64_t n, bool eager, int K = 1) {
     if (eager) {
       launch_eager(true, true);
       for (int64_t s = 0; s < n; ++s) launch_eager(false, s == 0 && kernels_prologue == 0);
       return;
     }
     if (gexec_pro) CU(cudaGraphLaunch(gexec_pro, stream));
-    for (int64_t s = 0; s < n; ++s) CU(cudaGraphLaunch(gexec, stream));
+    if (K > 1) {
+      CU(cudaEventRecord(pro_done, stream));
+      for (int k = 1; k < K; ++k) CU(cudaStreamWaitEvent(xl[k - 1].stream, pro_done, 0));
+    }
+    for (int64_t s = 0; s < n; ++s) {
+      const int k = (int)(s % K);
+      if (k == 0) CU(cudaGraphLaunch(gexec, stream));
+      else CU(cudaGraphLaunch(xl[k - 1].gexec, xl[k - 1].stream));
+    }
+    for (int k = 1; k < K; ++k) {
+      CU(cudaEventRecord(xl[k - 1].done, xl[k - 1].stream));
+      CU(cudaStreamWaitEvent(stream, xl[k - 1].done, 0));
+    }
   }
 
   // Eager replay of one slice, one kernel at a time, timed per launch with
@@ -966,8 +940,7 @@ struct tc_exec {
       CU(cudaMemset(trace, 0, (prog.n_tiny + 1) * sizeof(long long)));
       CU(cudaMemcpyToSymbol(g_tiny_trace, &trace, sizeof(trace)));
     }
-    int64_t h[2] = {slice, slice};
-    CU(cudaMemcpyAsync(eta, h, sizeof(h), cudaMemcpyHostToDevice, stream));
+    set_eta(slice, 1);
     std::vector<cudaEvent_t> ev(launches.size() + 1);
     for (auto& e : ev) CU(cudaEventCreate(&e));
     CU(cudaEventRecord(ev[0], stream));
@@ -1046,18 +1019,11 @@ struct tc_exec {
         CU(cudaGraphAddEventRecordNode(&r0, G.g, deps.data(), deps.size(), a));
         cudaKernelNodeParams kp = launches[si].params();
         CU(cudaGraphAddKernelNode(&nodes[si], G.g, &r0, 1, &kp));
-        if (launches[si].coop) {
-          cudaLaunchAttributeValue v{};
-          v.cooperative = 1;
-          CU(cudaGraphKernelNodeSetAttribute(nodes[si], cudaLaunchAttributeCooperative, &v));
-        }
         CU(cudaGraphAddEventRecordNode(&r1, G.g, &nodes[si], 1, z));
       }
       if (G.g) CU(cudaGraphInstantiate(&G.ge, G.g, 0));
     }
-    int64_t h[2] = {b, b};
-    CU(cudaMemcpyAsync(eta, h, sizeof(h), cudaMemcpyHostToDevice, stream));
-    CU(cudaStreamSynchronize(stream));
+    set_eta(b, 1);
     cudaEvent_t p0, p1;
     CU(cudaEventCreate(&p0));
     CU(cudaEventCreate(&p1));
@@ -1097,16 +1063,16 @@ struct tc_exec {
     static const bool oneshot_graph = std::getenv("TC_ONESHOT_GRAPH") && std::atoi(std::getenv("TC_ONESHOT_GRAPH")) == 1;
     const bool eager = !gexec && n * repeats <= 2 && !oneshot_graph;
     if (!eager) ensure_graph();
-    int64_t h[2] = {b, b};
+    const int K = eager ? 1 : lanes_for(n);
+    if (K > 1) ensure_lanes(K);
     cudaEvent_t e0, e1;
     CU(cudaEventCreate(&e0));
     CU(cudaEventCreate(&e1));
-    CU(cudaMemcpyAsync(eta, h, sizeof(h), cudaMemcpyHostToDevice, stream));
-    CU(cudaStreamSynchronize(stream));
+    set_eta(b, K);
     CU(cudaEventRecord(e0, stream));
     for (int64_t r = 0; r < repeats; ++r) {
-      if (r > 0) k_eta_reset<<<1, 1, 0, stream>>>(eta);
-      launch_pass(n, eager);
+      if (r > 0) reset_eta(K);
+      launch_pass(n, eager, K);
     }
     CU(cudaEventRecord(e1, stream));
     CU(cudaEventSynchronize(e1));
@@ -1134,13 +1100,14 @@ struct tc_exec {
     double4* fbuf = dalloc<double4>((size_t)n4, scratch, device);
     std::vector<cudaEvent_t> ev(2 * repeats);
     for (auto& x : ev) CU(cudaEventCreate(&x));
-    int64_t h[2] = {b, b};
-    CU(cudaMemcpyAsync(eta, h, sizeof(h), cudaMemcpyHostToDevice, stream));
+    const int K = lanes_for(n);
+    if (K > 1) ensure_lanes(K);
+    set_eta(b, K);
     for (int64_t r = 0; r < repeats; ++r) {
-      if (r > 0) k_eta_reset<<<1, 1, 0, stream>>>(eta);
+      if (r > 0) reset_eta(K);
       k_flush<<<grid_for(n4, 256, device), 256, 0, stream>>>(fbuf, n4, (double)r);
       CU(cudaEventRecord(ev[2 * r], stream));
-      launch_pass(n, false);
+      launch_pass(n, false, K);
       CU(cudaEventRecord(ev[2 * r + 1], stream));
     }
     CU(cudaStreamSynchronize(stream));

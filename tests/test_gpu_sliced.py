@@ -188,3 +188,96 @@ def test_multi_device_nccl_bitwise():
     one = sliced_execute(n, t, slice_indices=sl, devices=[0])
     two = sliced_execute(n, t, slice_indices=sl, devices=[0, 1])
     assert np.asarray(one.result.values).tobytes() == np.asarray(two.result.values).tobytes()
+
+
+def test_nonfinite_leaf_runs_dense_like_the_reference():
+    """A non-finite leaf next to structural zeros: the reference contracts an
+    identity piece with the Inf-holding delta densely, so 0*Inf = NaN enters
+    the sum (tensor.py:96-108).  Tie compression / relabel aliasing would skip
+    that term; libtc runs plans with non-finite leaves on dense variables, so
+    it produces the reference's NaN/Inf pattern (the oracle restates the
+    reference's pairwise order)."""
+    from oracle import oracle
+    from paper_2006_15512_b200 import Index, Tensor, TensorNetwork, join, leaf
+    from paper_2006_15512_b200.flatten import flatten
+
+    i, j, k, m = (Index(c, 2) for c in "ijkm")
+    ident = Tensor((i, j), np.eye(2))
+    delta = np.zeros((2, 2, 2))
+    delta[0, 0, 0], delta[1, 1, 1] = np.inf, 0.5
+    d = Tensor((j, k, m), delta)
+    w = Tensor((k,), np.array([1.0, 2.0]))
+    a = Tensor((i,), np.array([0.25, 3.0]))
+    n = TensorNetwork((a, ident, d, w))
+    t = join(join(leaf(ident), leaf(d)), join(leaf(a), leaf(w)))
+    got = np.asarray(sliced_execute(n, t).result.values, dtype=np.float64).reshape(-1)
+    want = np.asarray(oracle.sliced_execute(flatten(n, t))["values"], dtype=np.float64).reshape(-1)
+    assert np.isnan(want).any()  # the reference's 0 * Inf
+    assert np.array_equal(np.isnan(got), np.isnan(want)) and np.array_equal(np.isinf(got), np.isinf(want))
+    fin = np.isfinite(want)
+    assert np.allclose(got[fin], want[fin], rtol=1e-12)
+
+
+def test_distributed_sliced_execute_single_rank_nccl():
+    """distributed.sliced_execute in a 1-rank NCCL group equals sliced_execute bit for bit."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2006_15512_b200 import distributed
+
+    flat = _plan("c1b")
+    n, t = planfile.to_objects(flat)
+    h = _lib.PlanHandle(flat)
+    ch = []
+    for _ in range(3):
+        ch.append(h.choose_slice_index(ch))
+    sl = [flat.indices[i] for i in ch]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        got = distributed.sliced_execute(n, t, slice_indices=sl, device=0)
+        part = distributed.sliced_execute(n, t, slice_indices=sl, device=0, slice_range=(2, 5))
+    finally:
+        dist.destroy_process_group()
+    want = sliced_execute(n, t, slice_indices=sl, devices=[0])
+    assert np.asarray(got.result.values).tobytes() == np.asarray(want.result.values).tobytes()
+    assert got.num_slices == 8 and part.num_slices == 3
+    blk = sliced_execute(n, t, slice_indices=sl, devices=[0], slice_range=(2, 5))
+    assert np.asarray(part.result.values).tobytes() == np.asarray(blk.result.values).tobytes()
+
+
+def _per_slice_subprocess(env, name, picks):
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "import numpy as np\n"
+            "from paper_2006_15512_b200 import _lib, planfile\n"
+            "f, _ = planfile.load(%r + '/data/plans/%s.tcplan.npz')\n"
+            "h = _lib.PlanHandle(f); ch = []\n"
+            "for _ in range(%d): ch.append(h.choose_slice_index(ch))\n"
+            "ex = _lib.Exec(h, ch, 0); ns = ex.num_slices()\n"
+            "ex.run(0, ns, repeats=3)\n"
+            "fo, per = ex.fetch(ns)\n"
+            "print(per.tobytes().hex(), fo.tobytes().hex())\n") % (ROOT, ROOT, name, picks)
+    res = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                         timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    return res.stdout.split()
+
+
+@pytest.mark.parametrize("name,picks", [("c1b", 3), ("c2", 4)])
+def test_slice_lanes_are_bitwise_identical(name, picks):
+    """Concurrent slice lanes (TC_LANES, read once per process) change only
+    which stream runs a slice: every per-slice value and the fold are the
+    same bits as one lane."""
+    one = _per_slice_subprocess({"TC_LANES": "1"}, name, picks)
+    for k in ("3", "4", "8"):
+        assert _per_slice_subprocess({"TC_LANES": k}, name, picks) == one, k

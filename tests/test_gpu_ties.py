@@ -213,24 +213,12 @@ def test_chain_link_fusion_is_bitwise_identical():
     """k_stream_pair computes each fused chain link with the operations and
     order of the two separate steps: the counts are bit-identical to a run
     with fusion disabled (TC_FUSE=0, read once per process -> subprocess).
-    Chain segments are off here (TC_SEG=0) so that every link is a pair
-    candidate."""
-    on = _run_plans_subprocess({"TC_FUSE": "1", "TC_SEG": "0"})
-    off = _run_plans_subprocess({"TC_FUSE": "0", "TC_SEG": "0"})
+    """
+    on = _run_plans_subprocess({"TC_FUSE": "1"})
+    off = _run_plans_subprocess({"TC_FUSE": "0"})
     for name in ("c1a", "c2", "c1b"):
         assert on[name][0] == off[name][0], name  # same bits
     assert on["c2"][1] < off["c2"][1]  # fewer launches when fused
-
-
-def test_chain_segments_match_step_by_step():
-    """k_seg runs a chain of stream steps smem -> smem in one launch with
-    k_stream's operation order: the counts are bit-identical to the
-    step-by-step execution (TC_SEG=0, TC_FUSE=0), and the launch count drops."""
-    seg = _run_plans_subprocess({"TC_SEG": "1"})
-    ref = _run_plans_subprocess({"TC_SEG": "0", "TC_FUSE": "0"})
-    for name in ("c1a", "c2", "c1b"):
-        assert seg[name][0] == ref[name][0], name
-    assert seg["c2"][1] < ref["c2"][1] // 2
 
 
 def _chain_network(seed):
@@ -272,18 +260,3 @@ def _check_chain(seed):
 def test_stream_chains(seed):
     """Stream-kernel chains (k_stream, fused pairs) against a dense einsum."""
     _check_chain(seed)
-
-
-def test_stream_chains_through_segments():
-    """The same chains through k_seg (TC_SEG=1, read once per process)."""
-    import subprocess
-    import sys
-
-    here = os.path.dirname(os.path.abspath(__file__))
-    code = ("import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
-            "import test_gpu_ties as T\n"
-            "for seed in range(6): T._check_chain(seed)\n"
-            "print('ok')\n") % (os.path.join(here, ".."), here)
-    res = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, TC_SEG="1"), capture_output=True,
-                         text=True, timeout=600)
-    assert res.returncode == 0 and res.stdout.strip().endswith("ok"), res.stderr[-3000:]
