@@ -1,0 +1,29 @@
+"""compute-sanitizer over libtc's kernels (memcheck, racecheck incl. k_tiny's
+elided barriers, synccheck): a small sliced pass with hoisting, two slice
+lanes and graph replay, an eager pass, the fused chain links of C2 and a
+split-K GEMM (tools/sanitize.py).  Zero reports required."""
+
+import os
+import re
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_sanitizer_clean(tool):
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not found")
+    res = subprocess.run([SAN, "--tool", tool, "--print-limit", "20", sys.executable,
+                          os.path.join(ROOT, "tools", "sanitize.py")], capture_output=True, text=True, timeout=1500)
+    out = res.stdout + res.stderr
+    assert res.returncode == 0, out[-4000:]
+    m = re.search(r"(ERROR SUMMARY: (\d+) errors|RACECHECK SUMMARY: (\d+) hazards)", out)
+    assert m and (m.group(2) or m.group(3)) == "0", out[-4000:]
