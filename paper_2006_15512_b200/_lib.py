@@ -15,7 +15,7 @@ import numpy as np
 
 from . import errors
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libtc.so")
+LIB_PATH = os.environ.get("TC_LIBTC") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libtc.so")
 
 I32P = C.POINTER(C.c_int32)
 I64P = C.POINTER(C.c_int64)

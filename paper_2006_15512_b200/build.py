@@ -63,27 +63,28 @@ def build_flat_ext(force: bool = False, verbose: bool = False) -> str:
     return out
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    build_flat_ext(force=force, verbose=verbose)
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    build_flat_ext(force=force and out is None, verbose=verbose)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "tc.h"))
     deps.append(os.path.abspath(__file__))
-    if not force and not _stale(LIB, deps):
-        return LIB
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
+    lib_out = out or LIB
+    if not force and not _stale(lib_out, deps):
+        return lib_out
+    os.makedirs(os.path.dirname(lib_out), exist_ok=True)
     cmd = [
-        nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-shared",
+        nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-shared", *os.environ.get("TC_NVCC_DEFS", "").split(),
         "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-O3",
         "--expt-relaxed-constexpr",
         "-I", os.path.join(ROOT, "include"), "-I", CSRC,
         *[os.path.join(CSRC, f) for f in SOURCES],
-        "-o", LIB + ".tmp", "-lpthread", "-ldl",
+        "-o", lib_out + ".tmp", "-lpthread", "-ldl",
     ]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib_out + ".tmp", lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":

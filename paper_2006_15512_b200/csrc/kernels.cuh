@@ -467,8 +467,17 @@ __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, in
   }
 }
 
+// Resident CTAs per SM the register allocation must allow.  The streams are
+// latency-hiding bound: 6 CTAs (<= 40 registers) for the common small shapes
+// beat the compiler's 58-64 registers / 4 CTAs by 17% on C4 (1380 -> 1144 ms,
+// measured; 8 CTAs spill and gain nothing more).
+#ifndef TC_STREAM_MINB
+#define TC_STREAM_MINB 6
+#endif
 template <int NS, int NF>
-__global__ void __launch_bounds__(kStreamThreads) k_stream(const StreamParams p) {
+constexpr int stream_minb() { return NS + NF <= 3 ? TC_STREAM_MINB : 1; }  // larger shapes: no spills
+template <int NS, int NF>
+__global__ void __launch_bounds__(kStreamThreads, stream_minb<NS, NF>()) k_stream(const StreamParams p) {
   __shared__ double Ps[kStreamStageMax];  // staged small operand (stage_all)
   pdl_wait();  // operands are produced by earlier launches
   stream_run<NS, NF>(p, Ps, blockIdx.x, 31 - __clz(gridDim.x));
@@ -478,7 +487,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream(const StreamParams p)
 // K2p: two chained stream steps, the intermediate in registers (see program.h).
 // NI inner bits, step-1 shape (NS1 summed, NF1 new), step-2 shape (NS2, NF2).
 template <int NI, int NS1, int NF1, int NS2, int NF2>
-__global__ void __launch_bounds__(kStreamThreads) k_stream_pair(const StreamPairParams p) {
+__global__ void __launch_bounds__(kStreamThreads, NI <= 2 ? TC_STREAM_MINB : 1) k_stream_pair(const StreamPairParams p) {
   constexpr int NQ = 1 << NI, SV1 = 1 << NS1, FV1 = 1 << NF1, SV2 = 1 << NS2, FV2 = 1 << NF2;
   constexpr int NR = NQ / SV2;  // rest combos
   constexpr int CB = kStreamChunkBits;
