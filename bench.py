@@ -516,7 +516,9 @@ def golden_parity(config, flat, chosen, b, per_slice, count):
         src = "oracle/wmc_dp.c (exact counter, sliced variables fixed)"
     elif sl.get("slices"):
         want = {int(s): r["value"] for s, r in sl["slices"].items()}
-        src = "unmodified reference _execute_tracked(*_slice_plan(n, t, eta)) (slicing.py:30-41, 91-109)"
+        srcs = {r.get("source") for r in sl["slices"].values()}
+        src = ("unmodified reference _execute_tracked(*_slice_plan(n, t, eta)) (slicing.py:30-41, 91-109)"
+               if srcs == {"reference"} else "oracle/wmc_dp.c (exact counter, sliced variables fixed)")
     errs = []
     for k, v in enumerate(per_slice):
         s = b + k

@@ -1071,6 +1071,32 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   // dense variables, a 2x2 identity piece (x*1 + y*0 == x for finite y).
   // These are the non-carrier pieces of factored copy tensors
   // (factoring.py:194-206).
+  // A leaf every index of which is sliced (chosen or implied by its tie
+  // class) selects one scalar per slice; it is 1.0 for every slice when every
+  // entry whose tied indices agree is 1.0 (the non-carrier pieces of a sliced
+  // variable's copy tensor).
+  auto unit_when_sliced = [&](int l) {
+    const auto& ro = p.ref_order[l];
+    if (ro.empty() || ro.size() > 8) return false;
+    int cls_idx[8], classes[8], nc = 0;
+    for (size_t q = 0; q < ro.size(); ++q) {
+      const int i = ro[q];
+      if (!pdrop[i] || p.dom[i] != 2) return false;
+      const int c = drop[i] ? i : implied_src[i];
+      if (c < 0) return false;
+      int k = 0;
+      while (k < nc && classes[k] != c) ++k;
+      if (k == nc) classes[nc++] = c;
+      cls_idx[q] = k;
+    }
+    const double* v = p.lval.data() + p.lval_off[l];
+    for (int m = 0; m < (1 << nc); ++m) {
+      int64_t e = 0;
+      for (size_t q = 0; q < ro.size(); ++q) e = e * 2 + ((m >> cls_idx[q]) & 1);
+      if (v[e] != 1.0) return false;
+    }
+    return true;
+  };
   std::vector<int> alias_src(S, -1);
   if (!std::getenv("TC_NO_ALIAS") && p.all_finite) {
     for (int k = 0; k < p.NN; ++k) {
@@ -1087,6 +1113,22 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       if (leaf_tied[sm]) {
         ok = true;
         for (int64_t e = 0; ok && e < size[sm]; ++e) ok = leaf_phys(sm, e) == 1.0;
+        for (const Comp* c = c0; ok && c != c1; ++c) {
+          const int nbig = b_small ? c->na : c->nb;
+          if (c->c < 0 || nbig != 1) ok = false;
+        }
+        if (ok) {
+          for (const Comp* c = c0; c != c1; ++c) ccomp[c->c] = c;
+          for (size_t i = 0; ok && i < Lv.size(); ++i) {
+            const Comp* c = ccomp[Lv[i]];
+            ok = c && (b_small ? c->a[0] : c->b[0]) == Lg[i];
+          }
+          for (const Comp* c = c0; c != c1; ++c) ccomp[c->c] = nullptr;
+        }
+      } else if (eff[sm].size() == 0 && unit_when_sliced(sm)) {
+        // a unit piece whose indices are all (implied-)sliced: the selected
+        // scalar is 1.0 for every slice, C = A * 1.0 == A
+        ok = true;
         for (const Comp* c = c0; ok && c != c1; ++c) {
           const int nbig = b_small ? c->na : c->nb;
           if (c->c < 0 || nbig != 1) ok = false;
@@ -1904,6 +1946,13 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         st.work = so.sp.nx;
         g.n_stream++;
         done = true;
+        if (std::getenv("TC_STREAM_STATS")) {  // diagnostics: low address bits of the stream shapes
+          auto lowbit = [](int64_t v) { return v ? __builtin_ctzll((unsigned long long)v) : -1; };
+          std::fprintf(stderr, "[stream] inv=%d nx=2^%d ns=%d nf=%d sbit0=%d fbit0=%d abit0=%d cbit0=%d nbt=%d stage=%d\n",
+                       (int)st.inv, 63 - __builtin_clzll((unsigned long long)so.sp.nx), so.ns, so.nf,
+                       so.ns ? lowbit(so.sp.offA[1]) : -1, so.nf ? lowbit(so.sp.offC[1]) : -1, lowbit(so.sp.bitA[0]),
+                       lowbit(so.sp.bitC[0]), so.sp.nbt, so.sp.stage_all);
+        }
       }
     }
     bool diag = false;
