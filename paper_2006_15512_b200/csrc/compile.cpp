@@ -1241,6 +1241,30 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   auto is_troot = [&](int s) {
     return is_tiny(s) && (forced[s] || p.parent[s] < 0 || !is_tiny(p.parent[s]));
   };
+  // A group is evaluated node after node by one CTA, so its cost is its node
+  // count, while the subtree's critical path is its depth (C3's largest tiny
+  // subtree: 5043 nodes, depth 177).  Along every node's deeper tiny child
+  // the group continues; the other child becomes a group of its own (a root
+  // in global memory, evaluated by another CTA of an earlier level) when its
+  // subtree has >= TC_TINY_SPLIT nodes (0: one group per tiny subtree).
+  {
+    static const int split = std::getenv("TC_TINY_SPLIT") ? std::atoi(std::getenv("TC_TINY_SPLIT")) : 8;
+    if (split > 0) {
+      std::vector<int> cnt_t(S, 0), dep_t(S, 0);
+      for (int k = 0; k < p.NN; ++k) {
+        const int v = p.NL + k, a = p.left[k], b = p.right[k];
+        if (!is_tiny(v)) continue;
+        const int ca = is_tiny(a) ? cnt_t[a] : 0, cb = is_tiny(b) ? cnt_t[b] : 0;
+        const int da = is_tiny(a) ? dep_t[a] : 0, db = is_tiny(b) ? dep_t[b] : 0;
+        cnt_t[v] = 1 + ca + cb;
+        dep_t[v] = 1 + std::max(da, db);
+        if (is_tiny(a) && is_tiny(b)) {
+          const int light = (da > db || (da == db && ca >= cb)) ? b : a;
+          if (cnt_t[light] >= split) forced[light] = 1;
+        }
+      }
+    }
+  }
   // Each group root r collects its tiny subtree (stopping at other roots) and
   // simulates first-fit smem in postorder; a group over the smem cap forces
   // r's tiny children to be roots and is re-collected (a group's node set
@@ -1412,6 +1436,13 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   if (hoist) {  // the pinned region: boundary tensors that live in the arena
     std::vector<char> groot(S, 0);
     for (auto& gr : groups) groot[gr.back()] = 1;
+    // a forced root is read by its consumer's GROUP launch, which runs per
+    // slice whenever the group's root is variant (even if the consuming node
+    // itself is invariant)
+    for (auto& gr : groups) {
+      const int r = gr.back(), u = p.parent[r];
+      if (u >= 0 && is_tiny(u) && !var_[r]) boundary[r] = var_[groups[group_of[u]].back()];
+    }
     int64_t pin = 0;
     for (int k = 0; k < p.NN; ++k) {
       const int v = p.NL + k;

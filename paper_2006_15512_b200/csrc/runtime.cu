@@ -853,7 +853,7 @@ struct tc_exec {
     k_eta_reset<<<1, 1, 0, stream>>>(eta);
     for (int k = 1; k < K; ++k) k_eta_reset<<<1, 1, 0, stream>>>(xl[k - 1].eta);
   }
-  double program_ms = 0, setup_ms = 0, graph_ms = 0;
+  double program_ms = 0, setup_ms = 0, graph_ms = 0, lanes_ms = 0;
 
   int rootcopy_launch = -1;
   // stream grids: up to this many CTAs per SM, each walking >= 1 chunk.  Large
@@ -1062,9 +1062,15 @@ struct tc_exec {
     ensure_results(n);
     static const bool oneshot_graph = std::getenv("TC_ONESHOT_GRAPH") && std::atoi(std::getenv("TC_ONESHOT_GRAPH")) == 1;
     const bool eager = !gexec && n * repeats <= 2 && !oneshot_graph;
+    auto tg0 = std::chrono::steady_clock::now();
     if (!eager) ensure_graph();
+    auto tg1 = std::chrono::steady_clock::now();
     const int K = eager ? 1 : lanes_for(n);
     if (K > 1) ensure_lanes(K);
+    lanes_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tg1).count();
+    if (std::getenv("TC_E2E_TIMING"))
+      std::fprintf(stderr, "[run] graphs %.2f ms, lanes(%d) %.2f ms\n",
+                   std::chrono::duration<double, std::milli>(tg1 - tg0).count(), K, lanes_ms);
     cudaEvent_t e0, e1;
     CU(cudaEventCreate(&e0));
     CU(cudaEventCreate(&e1));
@@ -1547,9 +1553,16 @@ int tc_sliced_execute(const tc_plan* plan, int64_t mem_budget, const int32_t* sl
       try {
         ex[gi] = std::make_unique<tc_exec>();
         ex[gi]->device = devs[gi];
+        auto t0 = std::chrono::steady_clock::now();
         ex[gi]->build(p, ch);
+        auto t1 = std::chrono::steady_clock::now();
         int64_t b = std::min<int64_t>(NS, gi * per), e = std::min<int64_t>(NS, b + per);
         ms[gi] = ex[gi]->run(b, e);
+        auto t2 = std::chrono::steady_clock::now();
+        if (std::getenv("TC_E2E_TIMING"))
+          std::fprintf(stderr, "[sliced_execute] dev %d: build %.2f ms (program %.2f setup %.2f) run %.2f ms (device %.2f)\n",
+                       devs[gi], std::chrono::duration<double, std::milli>(t1 - t0).count(), ex[gi]->program_ms,
+                       ex[gi]->setup_ms, std::chrono::duration<double, std::milli>(t2 - t1).count(), ms[gi]);
       } catch (const Error& e) {
         errs[gi] = e;
       }

@@ -132,12 +132,17 @@ def test_c3_first_slices_match_reference():
         assert _close([folded[0]], [rec["value"]]), (s, folded[0], rec["value"])
 
 
-@pytest.mark.parametrize("name,picks", [("c1b", 3), ("c2", 4), ("c1a", 5)])
+@pytest.mark.parametrize("name,picks", [("c1b", 3), ("c2", 4), ("c1a", 5), ("c3", -28)])
 def test_hoisting_is_bitwise_identical(name, picks):
+    """(C3: the work-aware rank-28 slice set, the first 8 of its 2^30 slices;
+    thousands of split tiny groups, forced roots read across hoisting.)"""
     flat = _plan(name)
     h = _lib.PlanHandle(flat)
     ch = []
-    for _ in range(picks):
+    if picks < 0:
+        ch = h.choose_slices_work(2 ** -picks)
+        picks = 3
+    for _ in range(picks if not ch else 0):
         ch.append(h.choose_slice_index(ch))
     ns = 2 ** picks
     on, fon, exon = _per_slice(flat, ch, 0, ns)
