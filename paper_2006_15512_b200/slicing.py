@@ -46,10 +46,10 @@ def _plan(n, t, with_sort_rank=True):
 
 
 def _ids(flat, indices):
-    pos = {ix: k for k, ix in enumerate(flat.indices)}
+    pos = {ix.id: k for k, ix in enumerate(flat.indices)}
     out = []
     for ix in indices:
-        k = pos.get(ix)
+        k = pos.get(ix.id)
         if k is None:
             continue  # an index absent from the network drops nothing
         out.append(k)
@@ -92,8 +92,12 @@ def _run_range(n, flat, h, mem_budget, sl, devices, slice_range):
 def _run(n, t, mem_budget=None, devices=None, slice_indices=None, slice_range=None):
     # sort_key ranks only matter to the greedy chooser (slicing.py:73-79)
     flat, h = _plan(n, t, with_sort_rank=mem_budget is not None and slice_indices is None)
-    sl = None if slice_indices is None else [flat.indices.index(ix) if ix in flat.indices else -1
-                                             for ix in slice_indices]
+    if slice_indices is None:
+        sl = None
+    else:
+        # Index equality is by id (tensor.py:29-33): key on the raw ids (C hashing)
+        pos = {ix.id: k for k, ix in enumerate(flat.indices)}
+        sl = [pos.get(ix.id, -1) for ix in slice_indices]
     if sl is not None and any(k < 0 for k in sl):
         from .errors import NotABondIndex
         raise NotABondIndex("slice index is not an index of the network")
