@@ -1246,7 +1246,8 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   // subtree: 5043 nodes, depth 177).  Along every node's deeper tiny child
   // the group continues; the other child becomes a group of its own (a root
   // in global memory, evaluated by another CTA of an earlier level) when its
-  // subtree has >= TC_TINY_SPLIT nodes (0: one group per tiny subtree).
+  // subtree has >= TC_TINY_SPLIT nodes and the node's subtree is bushy (0: one
+  // group per tiny subtree).
   {
     static const int split = std::getenv("TC_TINY_SPLIT") ? std::atoi(std::getenv("TC_TINY_SPLIT")) : 8;
     if (split > 0) {
@@ -1258,7 +1259,9 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         const int da = is_tiny(a) ? dep_t[a] : 0, db = is_tiny(b) ? dep_t[b] : 0;
         cnt_t[v] = 1 + ca + cb;
         dep_t[v] = 1 + std::max(da, db);
-        if (is_tiny(a) && is_tiny(b)) {
+        // only inside bushy subtrees (nodes >= 8x depth): cutting a near-chain
+        // adds levels (launches) without shortening its critical path (C2)
+        if (is_tiny(a) && is_tiny(b) && cnt_t[v] >= 8 * dep_t[v]) {
           const int light = (da > db || (da == db && ca >= cb)) ? b : a;
           if (cnt_t[light] >= split) forced[light] = 1;
         }
@@ -2071,9 +2074,13 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         // split-K when the output tiles cannot fill the machine; skinny
         // memory-bound GEMMs (few 8x8 tiles, one warp per CTA) want many CTAs:
         // target 16 per SM (TC_SPLITK_MULT; C2 0.93 -> 0.89 ms, C3 unchanged)
+        // The target is one wave of resident CTAs: 2 per SM for 128x64 tiles (8
+        // warps), 4 for the 4-warp tiles, 16 for the skinny 1-2-warp ones (C3's
+        // 1024x1024x4096 GEMM: 19 splits -> 3).
         const int64_t tiles = (int64_t)1 << (gp.m_hi + gp.n_hi + nbt);
         int64_t splits = 1;
-        static const int64_t ctas = kSMs * (std::getenv("TC_SPLITK_MULT") ? std::max(1, std::atoi(std::getenv("TC_SPLITK_MULT"))) : 16);
+        static const int64_t mult = std::getenv("TC_SPLITK_MULT") ? std::max(1, std::atoi(std::getenv("TC_SPLITK_MULT"))) : 0;
+        const int64_t ctas = kSMs * (mult ? mult : (MT + NT >= 13 ? 2 : MT + NT >= 10 ? 4 : 16));
         if (tiles < ctas && gp.k_tiles >= 8) splits = std::min<int64_t>(gp.k_tiles / 4, (ctas + tiles - 1) / tiles);
         splits = std::max<int64_t>(1, splits);
         gp.k_per_split = (gp.k_tiles + splits - 1) / splits;
@@ -2085,6 +2092,20 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         st.work = tiles;
         g.n_gemm++;
         done = true;
+        if (std::getenv("TC_GEMM_STATS")) {  // diagnostics: GEMM shapes (log2), tiling, C's low address bits
+          char cl[9] = "........";
+          auto mark = [&](const std::vector<const Comp*>& V, char ch, int lim) {
+            for (int t = 0; t < (int)V.size(); ++t) {
+              const int q = pc[V[t]->c];
+              if (q < 8) cl[q] = t < lim ? (char)(ch - 32) : ch;  // upper case: inside the CTA tile
+            }
+          };
+          mark(M, 'm', MT);
+          mark(N, 'n', NT);
+          mark(Bt, 'b', 0);
+          std::fprintf(stderr, "[gemm] inv=%d m=%d n=%d k=%d bt=%d tile=%dx%d tiles=%lld splits=%d clow=%s\n",
+                       (int)st.inv, m, n, kk, nbt, MT, NT, (long long)tiles, gp.splits, cl);
+        }
       } catch (const Error& e) {
         if (e.status != -1) throw;
       }

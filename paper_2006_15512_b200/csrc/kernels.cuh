@@ -822,8 +822,20 @@ __global__ void k_splitk_reduce(const GemmParams p, int64_t tiles, int tile_elem
     int64_t off;
     int r, k;
     if (!tile_elem(p.tc, e, off, r, k)) continue;
-    double acc = p.ws[ta * tile_elems + e];
-    for (int s = 1; s < p.splits; ++s) acc = acc + p.ws[((int64_t)s * tiles + ta) * tile_elems + e];
+    // loads batched 8 at a time ahead of the (fixed-order) additions: the
+    // sum is a dependent chain, the loads need not be
+    const double* w = p.ws + ta * tile_elems + e;
+    const int64_t step = tiles * tile_elems;
+    double acc = w[0];
+    int s = 1;
+    for (; s + 8 <= p.splits; s += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(w + (s + u) * step);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = acc + v[u];
+    }
+    for (; s < p.splits; ++s) acc = acc + __ldg(w + s * step);
     const int tbits = p.m_hi + p.n_hi;
     const int64_t bt = ta >> tbits;
     const int64_t t = ta & (((int64_t)1 << tbits) - 1);
