@@ -287,14 +287,21 @@ def classes_from_profile(prof, n_slices, hbm, fp64):
     return ro, out
 
 
-def traffic_for(config, kernel):
+def traffic_for(config, kernel, n_slices):
+    """ncu DRAM bytes (read + write) of the kernel class over one pass of
+    n_slices slices: hoisted (prologue) traffic once + per-slice traffic x
+    n_slices (profiles/ncu_traffic.json, tools/ncu_r2.sh)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     d = json.load(open(p)).get(config, {})
-    fams = {"k_stream": ("k_stream", "k_stream_pair")}.get(kernel, (kernel,))
-    vals = [d[f]["dram_bytes_per_slice"] for f in fams if f in d and "dram_bytes_per_slice" in d[f]]
-    return sum(vals) if vals else None
+    fams = {"k_stream": ("k_stream", "k_stream_pair"), "k_gemm": ("k_gemm", "k_splitk_reduce")}.get(kernel, (kernel,))
+    tot, seen = 0, False
+    for f in fams:
+        if f in d and "dram_bytes_per_slice" in d[f]:
+            seen = True
+            tot += d[f].get("dram_bytes_prologue", 0) + n_slices * d[f]["dram_bytes_per_slice"]
+    return tot if seen else None
 
 
 # ---------------------------------------------------------------- reference
@@ -655,7 +662,9 @@ def run_ours(args):
     ro, classes = classes_from_profile(prof, n_prof, hbm, fp64)
     ro["peak_source"] = ("cuBLAS DGEMM 8192^3 measured live in bench.py (MEASURED_PEAKS.json has no FP64 figure)"
                          if ro["bound"] == "tensor" else hbm_src)
-    ro["traffic"] = traffic_for(args.config, ro["kernel"])
+    ro["traffic"] = traffic_for(args.config, ro["kernel"], n_prof)
+    ro["traffic_scope"] = (f"ncu dram__bytes_read+write of the class over a pass of {n_prof} slice(s) (hoisted launches "
+                           "once), cold caches, profiles/ncu_traffic.json; compare with alg_bytes_per_pass")
     ro["scope"] = (f"graph-mode CUDA events around every launch of the class over one pass of {n_prof} slice(s) "
                    f"(hoisted launches once); achieved = executed bytes (flops) / summed launch time")
     # whole-step executed-work fraction: every launched kernel's own work per step

@@ -2081,7 +2081,8 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         int64_t splits = 1;
         static const int64_t mult = std::getenv("TC_SPLITK_MULT") ? std::max(1, std::atoi(std::getenv("TC_SPLITK_MULT"))) : 0;
         const int64_t ctas = kSMs * (mult ? mult : (MT + NT >= 13 ? 2 : MT + NT >= 10 ? 4 : 16));
-        if (tiles < ctas && gp.k_tiles >= 8) splits = std::min<int64_t>(gp.k_tiles / 4, (ctas + tiles - 1) / tiles);
+        // (at most one wave: a second, mostly idle wave costs more than the splits save)
+        if (tiles < ctas && gp.k_tiles >= 8) splits = std::min<int64_t>(gp.k_tiles / 4, ctas / tiles);
         splits = std::max<int64_t>(1, splits);
         gp.k_per_split = (gp.k_tiles + splits - 1) / splits;
         gp.splits = (int32_t)((gp.k_tiles + gp.k_per_split - 1) / gp.k_per_split);
