@@ -1275,6 +1275,9 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   // fixpoint as re-grouping the whole forest).  Offsets are kept for the
   // descriptor pass below.
   std::vector<int32_t> soff(S, -1);  // smem offset of a non-root tiny node
+  // TC_TINY_WAVES=0: one node after the other in postorder (round-1 order)
+  static const bool waves_on = !(std::getenv("TC_TINY_WAVES") && std::atoi(std::getenv("TC_TINY_WAVES")) == 0);
+  std::vector<int> hgt(S, 0);  // height within the node's tiny group
   {
     std::vector<std::pair<int, int32_t>> done;  // (root, peak)
     std::vector<std::vector<int>> gnodes;
@@ -1298,13 +1301,39 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         std::sort(nodes.begin(), nodes.end());
         fit.reset();
         int32_t peak = 0;
-        for (int v : nodes) {
-          if (v != r) {
-            soff[v] = fit.alloc((int32_t)size[v]);
-            peak = std::max(peak, fit.top);
+        if (waves_on) {
+          // waves: nodes of equal height within the group are independent and
+          // run on different warps (k_tiny); smem is allocated wave by wave
+          // (a wave's outputs, then the frees of its inputs)
+          for (int v : nodes) {  // ascending slot = postorder: children first
+            int h = 0;
+            for (int c : {p.kid_l(v), p.kid_r(v)})
+              if (is_tiny(c) && !is_troot(c)) h = std::max(h, hgt[c] + 1);
+            hgt[v] = h;
           }
-          for (int c : {p.kid_l(v), p.kid_r(v)})
-            if (c != r && is_tiny(c) && !is_troot(c)) fit.free(soff[c], (int32_t)size[c]);
+          std::stable_sort(nodes.begin(), nodes.end(), [&](int x, int y) { return hgt[x] < hgt[y]; });
+          for (size_t w0 = 0; w0 < nodes.size();) {
+            size_t w1 = w0;
+            while (w1 < nodes.size() && hgt[nodes[w1]] == hgt[nodes[w0]]) ++w1;
+            for (size_t q = w0; q < w1; ++q)
+              if (nodes[q] != r) {
+                soff[nodes[q]] = fit.alloc((int32_t)size[nodes[q]]);
+                peak = std::max(peak, fit.top);
+              }
+            for (size_t q = w0; q < w1; ++q)
+              for (int c : {p.kid_l(nodes[q]), p.kid_r(nodes[q])})
+                if (c != r && is_tiny(c) && !is_troot(c)) fit.free(soff[c], (int32_t)size[c]);
+            w0 = w1;
+          }
+        } else {
+          for (int v : nodes) {
+            if (v != r) {
+              soff[v] = fit.alloc((int32_t)size[v]);
+              peak = std::max(peak, fit.top);
+            }
+            for (int c : {p.kid_l(v), p.kid_r(v)})
+              if (c != r && is_tiny(c) && !is_troot(c)) fit.free(soff[c], (int32_t)size[c]);
+          }
         }
         if (peak > kTinySmemCap) {
           if (!is_tiny(p.kid_l(r)) && !is_tiny(p.kid_r(r))) fail(TC_BAD_ARG, "tiny split failed");
@@ -1573,7 +1602,18 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       const int r = nodes.back();
       TinyGroup tg;
       tg.beg = (int32_t)out.nodes.size();
+      // wave bookkeeping: per-warp load of the current wave (least loaded
+      // warp takes the next single-warp node)
+      int cur_h = -1;
+      double wload[(1 << kTinyThreadsLog) / 32] = {};
       for (int v : nodes) {
+        int hv = 0;
+        for (int c : {p.kid_l(v), p.kid_r(v)})
+          if (c != r && group_of[c] == gi && soff[c] >= 0) hv = std::max(hv, hgt[c] + 1);
+        if (hv != cur_h) {
+          cur_h = hv;
+          for (double& x : wload) x = 0;
+        }
         const int a = p.kid_l(v), b = p.kid_r(v);
         TinyNode tn{};
         Loc la{LOC_SMEM, 0}, lb{LOC_SMEM, 0}, lo{LOC_SMEM, 0};
@@ -1630,11 +1670,29 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         tn.c_size = (int32_t)size[v];
         tn.s_size = (int32_t)ssz;
         tn.pow2 = p2 ? 1 : 0;
-        // lanes per output: fill the CTA's threads, at most a warp, at most
+        // single-warp nodes (few outputs, short sums) run beside the other
+        // nodes of their wave on their own warp; the rest use the whole CTA
+        const bool single = waves_on && tn.c_size <= 32 && (p2 || ssz < 64) && (int64_t)tn.c_size * ssz <= 2048;
+        const int tlog = single ? 5 : kTinyThreadsLog;
+        // lanes per output: fill the node's threads, at most a warp, at most
         // the number of summed terms
         tn.lw = 0;
-        while (tn.lw < 5 && (tn.c_size << (tn.lw + 1)) <= (1 << kTinyThreadsLog) && (1 << (tn.lw + 1)) <= ssz)
-          ++tn.lw;
+        while (tn.lw < 5 && (tn.c_size << (tn.lw + 1)) <= (1 << tlog) && (1 << (tn.lw + 1)) <= ssz) ++tn.lw;
+        tn.wofs = -1;
+        {
+          const double cost = 24.0 + (double)tn.c_size * (double)ssz / (single ? 32.0 : 256.0);
+          if (single) {
+            int best = 0;
+            for (int w = 1; w < (1 << kTinyThreadsLog) / 32; ++w)
+              if (wload[w] < wload[best]) best = w;
+            tn.wofs = best;
+            wload[best] += cost;
+          } else {
+            double mx = 0;
+            for (double x : wload) mx = std::max(mx, x);
+            for (double& x : wload) x = mx + cost;
+          }
+        }
         out.nodes.push_back(tn);
         slot.push_back(v);
         out.ga.push_back(la);
@@ -1658,7 +1716,8 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
           const int v = slot[q2];
           const bool red = tiny_uses_reduce(t);
           // executed by warp 0 alone (its threads are the node's only active ones)
-          const bool w0 = !red && ((t.pow2 && t.ns - t.lw <= kTinyMaxSum) ? (t.c_size << t.lw) <= 32 : t.c_size <= 32);
+          const bool w0 = !waves_on && !red &&
+                          ((t.pow2 && t.ns - t.lw <= kTinyMaxSum) ? (t.c_size << t.lw) <= 32 : t.c_size <= 32);
           std::pair<int32_t, int32_t> rd[2];
           int nr = 0;
           if (out.ga[q2].kind == LOC_SMEM) rd[nr++] = {t.sa, t.sa + (int32_t)size[p.kid_l(v)]};

@@ -99,10 +99,11 @@ __device__ long long* g_tiny_trace = nullptr;  // diagnostics: node start clocks
 __device__ __forceinline__ void tiny_pow2(const double* __restrict__ A, const double* __restrict__ B,
                                           double* __restrict__ C, const TinyNode& tn, const TinyDigit* sd,
                                           const int* dAr, const int* dBr, const int* hAr, const int* hBr, int tid,
-                                          int lane) {
+                                          int lane, int tlog) {
+  // tid: the thread's index among the node's 2^tlog threads (a warp or the CTA)
   const int nc = tn.nc;
   const TinyDigit* sdS = sd + nc;
-  const int lw = tn.lw, W = 1 << lw, cl = kTinyThreadsLog - lw;
+  const int lw = tn.lw, W = 1 << lw, cl = tlog - lw;
   const int r = lane & (W - 1), c0 = tid >> lw;
   const unsigned mask = (W == 32 ? 0xffffffffu : ((1u << W) - 1u) << (lane & ~(W - 1)));
   if (c0 >= tn.c_size) return;
@@ -230,8 +231,9 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
         pb += D[t.nc + j].sb;
       }
       pa = pb = 0;
-      for (int j = kTinyThreadsLog - t.lw; j < t.nc; ++j) {
-        const int k = j - (kTinyThreadsLog - t.lw);
+      const int tl = t.wofs >= 0 ? 5 : kTinyThreadsLog;
+      for (int j = tl - t.lw; j < t.nc; ++j) {
+        const int k = j - (tl - t.lw);
         hA[tid][k] = D[j].sa - pa;
         hB[tid][k] = D[j].sb - pb;
         pa += D[j].sa;
@@ -246,6 +248,11 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
         if (tn.sync == 1) __syncthreads();
         else if (warp == 0) __syncwarp();  // hazard among warp-0-only nodes
       }
+      // a single-warp node runs on its warp only (the other warps run the
+      // other nodes of its wave); ltid / nthr index the node's threads
+      if (tn.wofs >= 0 && warp != tn.wofs) continue;
+      const int ltid = tn.wofs >= 0 ? lane : tid, nthr = tn.wofs >= 0 ? 32 : (int)blockDim.x;
+      const int tlog = tn.wofs >= 0 ? 5 : kTinyThreadsLog;
       const TinyDigit* sd = bd + (tn.dig - dig0);
       const double* A = tn.sa >= 0 ? sm + tn.sa : tn.ga;  // (compile.cpp resolves staged / smem / global)
       const double* B = tn.sb >= 0 ? sm + tn.sb : tn.gb;
@@ -253,9 +260,9 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
       const int nc = tn.nc, ns = tn.ns;
       const TinyDigit* sdS = sd + nc;
       if (tn.pow2 && ns - tn.lw <= kTinyMaxSum) {
-        tiny_pow2(A, B, C, tn, sd, dA[i], dB[i], hA[i], hB[i], tid, lane);
+        tiny_pow2(A, B, C, tn, sd, dA[i], dB[i], hA[i], hB[i], ltid, lane, tlog);
       } else if (tn.c_size * 4 >= (int)blockDim.x || tn.s_size < 64) {
-        for (int c = tid; c < tn.c_size; c += blockDim.x) {
+        for (int c = ltid; c < tn.c_size; c += nthr) {
           int oa = 0, ob = 0;
           if (tn.pow2) {
             for (int j = 0; j < nc; ++j) {
@@ -350,8 +357,10 @@ __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, in
   const int tid = threadIdx.x;
   const int xb = 63 - __clzll((long long)p.nx);  // nx is a power of two
   const int cl = max(0, xb - CB);
-  int kchunk, cb = b, u0 = -1;
-  if (p.split_u) {  // one quarter of one chunk per CTA
+  int kchunk = 0, cb = b, u0 = -1;
+  if (p.persist) {
+    cb = 0;  // chunks are assigned in the grid-stride loop below
+  } else if (p.split_u) {  // one quarter of one chunk per CTA
     cb = b >> 2;
     u0 = b & 3;
     if (cb >= (1 << cl)) return;
@@ -401,7 +410,7 @@ __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, in
   constexpr bool kHoist = NS <= 2;
   const bool full = p.nx >= (1 << CB);
   double a[kStreamUnroll][SV];
-  if (kHoist && full) {
+  if (kHoist && full && !p.persist) {
 #pragma unroll
     for (int u = 0; u < kStreamUnroll; ++u)
       if (u0 < 0 || u == u0)
@@ -420,6 +429,42 @@ __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, in
   }
   const double* Pbase = staged ? Ps : p.P;
   auto pv = [&](const double* Pu, int q) { return staged ? Pu[q] : __ldg(Pu + p.offP[q]); };
+  if (p.persist) {
+    // grid-stride over the chunks (one wave of resident CTAs: no partial
+    // last wave); a chunk's address parts are summed from the tables
+    const int64_t nch = (int64_t)1 << cl;
+    for (int64_t c = b; c < nch; c += gridDim.x) {
+      int64_t qa = 0, qc = 0, qp = 0;
+      uint64_t m = (uint64_t)c << CB;
+      while (m) {
+        const int j = __ffsll((long long)m) - 1;
+        m &= m - 1;
+        qa += p.bitA[j];
+        qc += p.bitC[j];
+        qp += staged ? (int64_t)p.bitP[j] * SVFV : p.bitPo[j];
+      }
+      const double* Ab = p.A + qa;
+      double* Cb = p.C + qc;
+      const double* Pc = Pbase + qp;
+#pragma unroll
+      for (int u = 0; u < kStreamUnroll; ++u)
+#pragma unroll
+        for (int s = 0; s < SV; ++s) a[u][s] = __ldg(Ab + lo_a[u] + p.offA[s]);
+#pragma unroll
+      for (int u = 0; u < kStreamUnroll; ++u) {
+        const double* Pu = Pc + lo_p[u];
+        double* Cu = Cb + lo_c[u];
+#pragma unroll
+        for (int f = 0; f < FV; ++f) {
+          double acc = 0.0;
+#pragma unroll
+          for (int s = 0; s < SV; ++s) acc = fma(a[u][s], pv(Pu, s * FV + f), acc);
+          Cu[p.offC[f]] = acc;
+        }
+      }
+    }
+    return;
+  }
   const int64_t nsteps = (int64_t)1 << kchunk;
   for (int64_t i = 0; i < nsteps; ++i) {
     if (i > 0) {  // Gray code: chunk bit ctz(i) flips
@@ -509,8 +554,10 @@ __global__ void __launch_bounds__(kStreamThreads, NI <= 2 ? TC_STREAM_MINB : 1) 
   const int cl = max(0, p.ybits - CB);
   const int logG = 31 - __clz(gridDim.x);
   const int b = blockIdx.x;
-  int kchunk, cb = b, u0 = -1;
-  if (p.split_u) {  // one quarter of one chunk per CTA
+  int kchunk = 0, cb = b, u0 = -1;
+  if (p.persist) {
+    cb = 0;  // grid-stride over the chunks (walk below)
+  } else if (p.split_u) {  // one quarter of one chunk per CTA
     cb = b >> 2;
     u0 = b & 3;
     if (cb >= (1 << cl)) return;
@@ -533,9 +580,17 @@ __global__ void __launch_bounds__(kStreamThreads, NI <= 2 ? TC_STREAM_MINB : 1) 
   // site inlines with its own address space)
   auto walk = [&](const double* __restrict__ P1, const double* __restrict__ P2) {
     const int64_t ny = (int64_t)1 << p.ybits;
-    const int64_t nsteps = (int64_t)1 << kchunk;
+    const int64_t nsteps = p.persist ? ((((int64_t)1 << cl) - b + gridDim.x - 1) / gridDim.x) : (int64_t)1 << kchunk;
     for (int64_t i = 0; i < nsteps; ++i) {
-      if (i > 0) {
+      if (p.persist) {  // chunk b + i * grid: address parts summed from the tables
+        ha = hc = h1 = h2 = 0;
+        uint64_t m = (uint64_t)(b + i * (int64_t)gridDim.x) << CB;
+        while (m) {
+          const int j = __ffsll((long long)m) - 1;
+          m &= m - 1;
+          ha += p.bitA[j], hc += p.bitC[j], h1 += p.bitP1[j], h2 += p.bitP2[j];
+        }
+      } else if (i > 0) {
         const int j = __ffsll((long long)i) - 1 + CB;
         const int64_t sg = (((i ^ (i >> 1)) >> (j - CB)) & 1) ? 1 : -1;
         ha += sg * p.bitA[j], hc += sg * p.bitC[j], h1 += sg * p.bitP1[j], h2 += sg * p.bitP2[j];

@@ -79,6 +79,7 @@ struct StreamParams {
                       //    in smem once per CTA; 0: it is read through the L1 (direct)
   int32_t split_u;    // 1: CTA b takes chunk b >> 2 and only its quarter u = b & 3 (small tensors:
                       //    4x the CTAs, a quarter of the serial work per thread)
+  int32_t persist;    // 1: grid-stride over the chunks with one wave of resident CTAs (large launches)
 };
 
 // ---- K2p: a chain link of two stream steps in registers ----------------------
@@ -111,6 +112,7 @@ struct StreamPairParams {
   int32_t split_u;                    // as StreamParams::split_u
   int32_t p1n, p2n;                   // small-operand entries
   int32_t pstage;                     // 1: both small operands staged in smem (p1n + p2n <= kPairStageMax)
+  int32_t persist;                    // as StreamParams::persist
 };
 constexpr int kPairStageMax = 4096;
 
@@ -160,7 +162,7 @@ struct TinyNode {
   int32_t na, nb;    // entry counts of the staged operands
   int32_t lw;        // dim-2 nodes: 2^lw lanes share one output's sum (<= 32)
   int32_t sync;      // before this node: 1 CTA barrier, 2 warp-0 barrier (it reads / overwrites smem touched since)
-  int32_t pad_;
+  int32_t wofs;      // single-warp node: the warp that runs it (its wave's other nodes run beside it); -1: whole CTA
 };
 // k_tiny processes a group in batches of kTinyBatch nodes: descriptors,
 // digits and small global operands (leaves) of a batch are copied to smem

@@ -463,6 +463,9 @@ struct tc_exec {
             if ((1 << chunks_log) < sm_count(device) * split_mult() && split_u_on()) {  // few chunks: a quarter chunk per CTA
               sp.split_u = 1;
               L.grid = dim3(xb >= kStreamChunkBits ? 4u << chunks_log : (unsigned)((sp.nx + 255) / 256));
+            } else if (persist_from() > 0 && chunks_log >= persist_from()) {  // one wave, grid-stride chunks
+              sp.persist = 1;
+              L.grid = dim3((unsigned)std::min<int64_t>((int64_t)1 << chunks_log, wave_ctas(L.func, 0)));
             }
             L.xbits = xb, L.ns = st.ns, L.nf = st.nf;
           }
@@ -708,6 +711,8 @@ struct tc_exec {
         if ((1 << chunks_log) < sm_count(device) * pair_mult && split_u_on()) {
           pp.split_u = 1;
           L.grid = dim3(pp.ybits >= kStreamChunkBits ? 4u << chunks_log : (unsigned)((((int64_t)1 << pp.ybits) + 255) / 256));
+        } else if (persist_from() > 0 && chunks_log >= persist_from()) {
+          pp.persist = 1;
         }
         L.xbits = pp.ybits, L.ns = s1.ns, L.nf = s1.nf, L.ns2 = s2.ns, L.nf2 = s2.nf;
         {
@@ -720,6 +725,8 @@ struct tc_exec {
         // executed bytes: A, P1, P2 and C2 (C1 never touches memory)
         const StreamParams sp1 = bound(i);
         const double c1_bytes = 8.0 * (double)sp1.nx * (double)(1 << s1.nf);
+        if (pp.persist)
+          L.grid = dim3((unsigned)std::min<int64_t>((int64_t)1 << chunks_log, wave_ctas(L.func, (int)L.smem)));
         L.bytes = s1.alg_bytes + s2.alg_bytes - 2 * c1_bytes;
         L.flops = s1.alg_flops + s2.alg_flops;
         L.arg(pp);
@@ -864,6 +871,30 @@ struct tc_exec {
     if (m) return m;
     static const int mid = std::getenv("TC_STREAM_GRID_MID") ? std::max(1, std::atoi(std::getenv("TC_STREAM_GRID_MID"))) : 4;
     return chunks_log >= 12 ? 32 : chunks_log >= 10 ? mid : 4;
+  }
+  // grid-stride ("persistent") stream launches from 2^k chunks up
+  // (TC_STREAM_PERSIST=k, 0: off): one wave of resident CTAs, no partial wave
+  static int persist_from() {
+    static const int k = std::getenv("TC_STREAM_PERSIST") ? std::atoi(std::getenv("TC_STREAM_PERSIST")) : 12;
+    return k;
+  }
+  // resident CTAs of a kernel on the whole GPU (occupancy x SMs), cached per function
+  int64_t wave_ctas(void* fn, int smem) {
+    static std::mutex mu;
+    static std::map<std::pair<void*, int>, int> occ;
+    int o = 0;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = occ.find({fn, smem});
+      if (it != occ.end()) o = it->second;
+    }
+    if (!o) {
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kStreamThreads, smem));
+      o = std::max(1, o);
+      std::lock_guard<std::mutex> lk(mu);
+      occ[{fn, smem}] = o;
+    }
+    return (int64_t)o * sm_count(device);
   }
   static int split_mult() {
     static const int m = std::getenv("TC_SPLIT_MULT") ? std::max(1, std::atoi(std::getenv("TC_SPLIT_MULT"))) : 1;

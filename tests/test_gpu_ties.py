@@ -260,3 +260,45 @@ def _check_chain(seed):
 def test_stream_chains(seed):
     """Stream-kernel chains (k_stream, fused pairs) against a dense einsum."""
     _check_chain(seed)
+
+
+def _big_chain_network(seed, rank=24, steps=8):
+    """A rank-24 tensor (128 MB) through a chain of small pieces: launches of
+    >= 2^12 chunks (grid-stride 'persistent' stream kernels, fused pairs)."""
+    rng = np.random.default_rng(300 + seed)
+    pyr = random.Random(400 + seed)
+    cur = [Index(("B", i), 2) for i in range(rank)]
+    big = Tensor(tuple(cur), rng.uniform(-1, 1, [2] * rank))
+    tree = leaf(big)
+    tensors = [big]
+    for step in range(steps):
+        summed = pyr.sample(cur, pyr.choice([1, 2]))
+        new = [Index(("N", seed, step, j), 2) for j in range(len(summed))]
+        kept = [ix for ix in cur if ix not in summed]
+        piece = Tensor(tuple(summed + new), rng.uniform(-1, 1, [2] * (2 * len(summed))))
+        tensors.append(piece)
+        tree = join(tree, leaf(piece))
+        cur = kept + new
+    return TensorNetwork(tuple(tensors)), tree
+
+
+def test_large_stream_launches_modes_bitwise():
+    """Grid-stride (TC_STREAM_PERSIST, default from 2^12 chunks) vs per-CTA
+    chunk blocks (TC_STREAM_PERSIST=0), fused vs unfused (TC_FUSE): the same
+    bits for a 128 MB chain (env read once per process -> subprocesses)."""
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = ("import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+            "import numpy as np, test_gpu_ties as T\n"
+            "n, t = T._big_chain_network(0)\n"
+            "out, v = T._run(n, t)\n"
+            "print(np.asarray(v).tobytes().hex()[:4096], float(np.abs(np.asarray(v)).sum()))\n") % (os.path.join(here, ".."), here)
+    outs = []
+    for env in ({}, {"TC_STREAM_PERSIST": "0"}, {"TC_FUSE": "0"}, {"TC_STREAM_PERSIST": "0", "TC_FUSE": "0"}):
+        res = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                             timeout=900)
+        assert res.returncode == 0, res.stderr[-3000:]
+        outs.append(res.stdout.strip())
+    assert len(set(outs)) == 1, outs
