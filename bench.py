@@ -483,10 +483,27 @@ def _dense_mem_gib(flat, chosen):
     return _lib.PlanHandle(flat).mem_cost(chosen) / GiB
 
 
+def all_host_threads():
+    """BLAS thread pools at every host core (torchrun exports OMP_NUM_THREADS=1)."""
+    try:
+        from threadpoolctl import threadpool_limits
+
+        return threadpool_limits(limits=host_cores())
+    except Exception:
+        import contextlib
+
+        return contextlib.nullcontext()
+
+
 def run_reference(args):
     world, rank, local = dist_env()
     if rank != 0:
         return
+    with all_host_threads():
+        _run_reference(args)
+
+
+def _run_reference(args):
     spec = CONFIGS[args.config]
     flat, _ = load_plan(spec["plan"])
     _, chosen = choose(flat, spec["slices"])
@@ -562,11 +579,21 @@ def run_ours(args):
     from paper_2006_15512_b200 import _lib, distributed, planfile, sliced_execute
 
     world, rank, local = dist_env()
+    # TC_BENCH_SHARE_GPU=1 (test only): ranks share the visible GPUs round-robin
+    # and meet over gloo (NCCL rejects two ranks on one device) -- exercises
+    # the sharded path on a one-GPU box; its timings are not scaling numbers
+    share = os.environ.get("TC_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cdev = "cpu" if share else "cuda"
 
     def barrier():
         if world > 1:
@@ -576,14 +603,14 @@ def run_ours(args):
     def allmax(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
     def allsum(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
         torch.distributed.all_reduce(t)
         return float(t.item())
 
@@ -602,7 +629,7 @@ def run_ours(args):
     barrier()
     dev_ms = allmax(st["device_ms"])
     ms_per_step = dev_ms / args.steps
-    slices_per_step = allsum(e - b) if sliced else world
+    slices_per_step = int(allsum(e - b)) if sliced else world
     value = slices_per_step / (ms_per_step / 1e3)
 
     # per-slice results of the last pass; whole job: gather + lexicographic fold
@@ -634,7 +661,7 @@ def run_ours(args):
     slice_objs = [flat.indices[i] for i in chosen] if sliced else None
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     barrier()
-    rng = None if whole_job else ((b, e) if world == 1 else (0, allsum(e - b)))
+    rng = None if whole_job else ((b, e) if world == 1 else (0, slices_per_step))
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         if world == 1:
@@ -688,7 +715,8 @@ def run_ours(args):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            v, cpu = reference_baseline(args.config, flat, chosen, 1, args.ref_budget)
+            with all_host_threads():
+                v, cpu = reference_baseline(args.config, flat, chosen, 1, args.ref_budget)
             cpu = dict(cpu, value=v, unit=UNIT)
             if cpu.get("count") is not None and count:
                 cpu["rel_err_vs_gpu"] = abs(cpu["count"] - count) / abs(cpu["count"])

@@ -30,11 +30,13 @@ def gather_slices(local, begin: int, num_slices: int, group=None):
     import torch.distributed as dist
 
     R = local.shape[1] if local.dim() == 2 else 1
-    full = torch.zeros((num_slices, R), dtype=torch.float64, device=local.device)
+    # gloo (CPU tests, ranks sharing a GPU) reduces host tensors
+    dev = "cpu" if dist.get_backend(group) == "gloo" else local.device
+    full = torch.zeros((num_slices, R), dtype=torch.float64, device=dev)
     if local.numel():
-        full[begin:begin + local.shape[0]] = local.reshape(-1, R)
+        full[begin:begin + local.shape[0]] = local.reshape(-1, R).to(dev)
     dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
-    return full
+    return full.to(local.device)
 
 
 def fold(full):
@@ -79,7 +81,7 @@ def sliced_execute(n, t, mem_budget=None, *, slice_indices=None, device=None, gr
         chosen = []
     ex = _lib.Exec(h, chosen, dev)
     ns = ex.num_slices()
-    lo, hi = slice_range if slice_range is not None else (0, ns)
+    lo, hi = (int(x) for x in slice_range) if slice_range is not None else (0, ns)
     b, e = slice_block(hi - lo, world, rank)
     b, e = lo + b, lo + e
     st = ex.run(b, e) if e > b else None
