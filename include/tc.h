@@ -202,7 +202,8 @@ int tc_exec_profile(tc_exec* ex, int64_t slice, float* step_ms, int32_t* step_ki
  * and per-slice CUDA graphs instrumented with an event-record node before and
  * after every kernel node, one pass over slices [slice_begin, slice_end) with a
  * synchronize after each graph launch.  launch_ms[i] = launch i's time summed
- * over the pass (slice-invariant launches once); launch_inv[i] = 1 for those;
+ * over the pass (slice-invariant launches once); launch_inv[i] bit 0 = 1 for
+ * those, bits 1.. = the launch's start in us from its graph launch (last one);
  * *pass_ms = summed graph times of the pass.  Any pointer may be NULL. */
 int tc_exec_profile_graph(tc_exec* ex, int64_t slice_begin, int64_t slice_end, float* launch_ms,
                           int32_t* launch_kind, int32_t* launch_inv, double* launch_bytes, double* launch_flops,

@@ -416,8 +416,8 @@ class Exec:
                                           _p(kind, I32P), _p(inv, I32P), _p(by, F64P), _p(fl, F64P), cap,
                                           C.byref(n), C.byref(pm)))
         k = n.value
-        return [dict(kind=self.KINDS[kind[i]], inv=bool(inv[i]), ms=float(ms[i]), bytes=float(by[i]),
-                     flops=float(fl[i])) for i in range(k)], float(pm.value)
+        return [dict(kind=self.KINDS[kind[i]], inv=bool(inv[i] & 1), ms=float(ms[i]), bytes=float(by[i]),
+                     flops=float(fl[i]), start_us=int(inv[i] >> 1)) for i in range(k)], float(pm.value)
 
     def deps(self):
         """Launch DAG: list of dependency lists (diagnostics)."""

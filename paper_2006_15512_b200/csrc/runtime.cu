@@ -861,6 +861,7 @@ struct tc_exec {
     for (int k = 1; k < K; ++k) k_eta_reset<<<1, 1, 0, stream>>>(xl[k - 1].eta);
   }
   double program_ms = 0, setup_ms = 0, graph_ms = 0, lanes_ms = 0;
+  std::vector<float> start_ms;  // profile_graph: launch start offset within its graph launch
 
   int rootcopy_launch = -1;
   // stream grids: up to this many CTAs per SM, each walking >= 1 chunk.  Large
@@ -1058,11 +1059,14 @@ struct tc_exec {
     cudaEvent_t p0, p1;
     CU(cudaEventCreate(&p0));
     CU(cudaEventCreate(&p1));
+    start_ms.assign(launches.size(), 0.f);
     auto collect = [&](PG& G) {
       for (size_t q = 0; q < G.idx.size(); ++q) {
-        float t = 0;
+        float t = 0, t0 = 0;
         CU(cudaEventElapsedTime(&t, G.e0[q], G.e1[q]));
+        CU(cudaEventElapsedTime(&t0, p0, G.e0[q]));
         ms[G.idx[q]] += t;
+        start_ms[G.idx[q]] = t0;  // of the last graph launch that ran it
       }
     };
     for (int64_t s = -1; s < n; ++s) {
@@ -1492,7 +1496,7 @@ int tc_exec_profile_graph(tc_exec* ex, int64_t slice_begin, int64_t slice_end, f
       const Launch& L = ex->launches[i];
       if (launch_ms) launch_ms[i] = ms[i];
       if (launch_kind) launch_kind[i] = L.kind;
-      if (launch_inv) launch_inv[i] = L.inv ? 1 : 0;
+      if (launch_inv) launch_inv[i] = (L.inv ? 1 : 0) | ((int32_t)std::lround(ex->start_ms[i] * 1000.0) << 1);
       if (launch_bytes) launch_bytes[i] = L.bytes;
       if (launch_flops) launch_flops[i] = L.flops;
     }
