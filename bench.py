@@ -57,6 +57,8 @@ CONFIGS = {
     "c4": dict(plan="c4", slices=("greedy", 8),
                desc="banded random 3-CNF n=400 ratio 4.0 window 36 seed 11 (C4; seeds 1-10 UNSAT), max-rank 37, "
                     "Algorithm 3 greedy 8-pick prefix -> 2^8 slices of max-rank 33"),
+    "c1b_s3": dict(plan="c1b", slices=("greedy", 3),
+                   desc="C1b with Algorithm 3's greedy 3-pick prefix (8 slices): a small sliced case for tests"),
     "c4_full": dict(plan="c4", slices=None,
                     desc="C4 unsliced (2.5 TiB dense mem_cost; 10.6 GB of tied tensors on the device)"),
     "c5": dict(plan="c5", slices=("greedy", 12), sample=512, sample_at_end=True,
@@ -560,6 +562,11 @@ def golden_parity(config, flat, chosen, b, per_slice, count):
     if count is not None and "count" in sl:
         out.update(reference_count=sl["count"], count_source=sl.get("count_source"),
                    rel_err=abs(count - sl["count"]) / abs(sl["count"]))
+    elif count is not None:  # a whole sliced job of a plan with a reference count (Thm 5: the slice sum)
+        c = json.load(open(os.path.join(gp, "counts.json"))).get(spec["plan"])
+        if c:
+            out.update(reference_count=c["count"], count_source="reference sliced_execute (unsliced)",
+                       rel_err=abs(count - c["count"]) / abs(c["count"]))
     return out
 
 

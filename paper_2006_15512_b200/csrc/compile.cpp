@@ -2078,7 +2078,12 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         static const int big_tiles = std::getenv("TC_GEMM_BIG") ? std::atoi(std::getenv("TC_GEMM_BIG")) : 1;
         static const int big_k = std::getenv("TC_GEMM_BIG_K") ? std::atoi(std::getenv("TC_GEMM_BIG_K")) : 4;
         const bool big = big_tiles && m >= 7 && n >= 6 && kk >= big_k;
-        const int MT = big ? 7 : std::max(3, std::min(6, m)), NT = std::max(3, std::min(6, n)), KT = 4;
+        // small-K GEMMs (K <= 2^smallk) are latency-bound on their prologue /
+        // epilogue: tiles of at most 2^small_tile per side give more CTAs
+        static const int smallk = std::getenv("TC_GEMM_SMALLK") ? std::atoi(std::getenv("TC_GEMM_SMALLK")) : -1;
+        static const int small_tile = std::getenv("TC_GEMM_SMALLK_TILE") ? std::atoi(std::getenv("TC_GEMM_SMALLK_TILE")) : 5;
+        const int tcap = (!big && kk <= smallk) ? small_tile : 6;
+        const int MT = big ? 7 : std::max(3, std::min(tcap, m)), NT = std::max(3, std::min(tcap, n)), KT = 4;
         GemmParams gp{};
         gp.m_hi = std::max(0, m - MT);
         gp.n_hi = std::max(0, n - NT);

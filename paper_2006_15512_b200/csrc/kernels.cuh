@@ -345,9 +345,9 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
 constexpr int kStreamThreads = 256;
 constexpr int kStreamUnroll = 4;
 
-// One stream step executed by CTA `b` of 2^logG CTAs (a standalone launch or
-// one step of k_stream_seq).  The 2^cl chunks split into 2^g CTA blocks of
-// 2^kchunk chunks each; CTAs beyond the chunk count idle.
+// One stream step executed by CTA `b` of 2^logG CTAs.  The 2^cl chunks split
+// into 2^g CTA blocks of 2^kchunk chunks each (CTAs beyond the chunk count
+// idle), or, for large launches (p.persist), a grid-stride walk over them.
 template <int NS, int NF>
 __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, int b, int logG) {
   constexpr int SV = 1 << NS, FV = 1 << NF, SVFV = SV * FV;

@@ -168,7 +168,10 @@ struct TinyNode {
 // digits and small global operands (leaves) of a batch are copied to smem
 // with one round of independent loads before the batch's nodes run.
 constexpr int kTinyBatch = 32;
-constexpr int kTinyThreadsLog = 8;  // k_tiny CTA = 256 threads
+#ifndef TC_TINY_THREADS_LOG
+#define TC_TINY_THREADS_LOG 8
+#endif
+constexpr int kTinyThreadsLog = TC_TINY_THREADS_LOG;  // k_tiny CTA = 2^8 threads
 constexpr int kTinyMaxSum = 16;     // summed dim-2 digits with precomputed deltas
 // k_tiny's cooperative path (CTA-wide reduce with internal barriers): mixed
 // radix or very long sums with few outputs
