@@ -21,6 +21,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <exception>
 #include <thread>
 #include <vector>
 
@@ -548,6 +549,13 @@ struct tc_exec {
     PF(2, 1, 1, 1, 1) PF(1, 1, 1, 0, 1) PF(2, 0, 1, 1, 1) PF(2, 2, 1, 1, 1) PF(3, 1, 1, 2, 1)
     PF(1, 0, 1, 0, 1) PF(2, 0, 2, 0, 2) PF(3, 2, 1, 2, 1) PF(1, 2, 1, 0, 1) PF(2, 1, 1, 1, 2)
     PF(3, 1, 2, 1, 1) PF(2, 0, 2, 0, 1) PF(2, 0, 1, 2, 1) PF(1, 1, 1, 1, 1) PF(1, 0, 1, 1, 1)
+    // links with a batch-scaling step (weighted carrier pieces: no summed, no new variable)
+    PF(1, 1, 1, 0, 0) PF(1, 0, 1, 0, 0) PF(0, 1, 0, 0, 0) PF(1, 2, 1, 0, 0) PF(0, 2, 0, 0, 0)
+    PF(1, 0, 0, 1, 1) PF(1, 0, 0, 1, 0) PF(0, 0, 0, 0, 1) PF(2, 0, 0, 2, 1)
+    // the next most frequent links of C2 / C4 / C5 (tools/fuse_stats.py)
+    PF(1, 1, 0, 1, 1) PF(2, 1, 1, 1, 0) PF(1, 1, 0, 1, 0) PF(2, 0, 1, 1, 0) PF(3, 1, 2, 1, 2)
+    PF(3, 0, 2, 1, 0) PF(3, 1, 2, 1, 0) PF(1, 1, 1, 0, 2) PF(1, 1, 0, 1, 2) PF(1, 2, 0, 1, 1)
+    PF(3, 0, 1, 2, 1) PF(1, 0, 1, 0, 2) PF(0, 1, 0, 0, 1)
 #undef PF
     return nullptr;
   }
@@ -663,38 +671,61 @@ struct tc_exec {
       std::memcpy(&sp, launches[k].blob.data() + launches[k].off[0], sizeof(sp));
       return sp;
     };
-    for (size_t i = 0; i < S;) {
+    // candidate links (i, i+1), then the set of disjoint links that saves the
+    // most intermediate traffic (a chain: O(S) dynamic program) -- a greedy
+    // left-to-right pairing can take a small link and block a large one
+    struct Cand {
+      PairFn fn = nullptr;
       StreamPairParams pp;
       int ni = 0;
-      PairFn fn = nullptr;
-      static const bool dbg = std::getenv("TC_FUSE_DEBUG") != nullptr;
-      if (dbg && i + 1 < S && g.steps[i].kind == ST_STREAM && g.steps[i + 1].kind == ST_STREAM) {
+      double gain = 0;
+    };
+    std::vector<Cand> cand(S);
+    static const bool dbg = std::getenv("TC_FUSE_DEBUG") != nullptr;
+    for (size_t i = 0; i + 1 < S; ++i) {
+      if (dbg && g.steps[i].kind == ST_STREAM && g.steps[i + 1].kind == ST_STREAM) {
         const Step &s1 = g.steps[i], &s2 = g.steps[i + 1];
         bool dep = false;
         for (int d : s2.deps) dep |= d == (int)i;
         StreamPairParams tmp;
         int tni = 0;
         const bool mk = make_pair(bound(i), s1.ns, s1.nf, bound(i + 1), s2.ns, s2.nf, tmp, tni);
-        std::fprintf(stderr, "[fuse] %zu (%d,%d)->(%d,%d) dep=%d link=%d make=%d ni=%d fn=%d A=[%ld,+%ld) P1=[%ld,+%ld) C2=[%ld,+%ld) k%d%d%d\n", i, s1.ns, s1.nf, s2.ns,
-                     s2.nf, (int)dep, (int)(bound(i + 1).A == bound(i).C), (int)mk, tni,
-                     (int)(mk && pair_fn(tni, s1.ns, s1.nf, s2.ns, s2.nf) != nullptr), (long)s1.la.off, (long)s1.la_bytes,
-                     (long)s1.lb.off, (long)s1.lb_bytes, (long)s2.lc.off, (long)s2.lc_bytes, (int)s1.la.kind, (int)s1.lb.kind, (int)s2.lc.kind);
+        std::fprintf(stderr, "[fuse] %zu (%d,%d)->(%d,%d) dep=%d link=%d make=%d ni=%d fn=%d inv=%d\n", i, s1.ns, s1.nf,
+                     s2.ns, s2.nf, (int)dep, (int)(bound(i + 1).A == bound(i).C), (int)mk, tni,
+                     (int)(mk && pair_fn(tni, s1.ns, s1.nf, s2.ns, s2.nf) != nullptr), (int)s1.inv);
       }
-      if (on && i + 1 < S && g.steps[i].kind == ST_STREAM && g.steps[i + 1].kind == ST_STREAM &&
-          g.steps[i].inv == g.steps[i + 1].inv) {
-        const Step &s1 = g.steps[i], &s2 = g.steps[i + 1];
-        bool dep_ok = false;  // step 2 must consume step 1 (its RAW edge)
-        for (int d : s2.deps) dep_ok |= d == (int)i;
-        // C2 may reuse the memory step 1 read (A, P1: released after step 1);
-        // fused, those reads and the C2 writes overlap in time
-        auto overlaps = [](const Loc& x, int64_t xb, const Loc& y, int64_t yb) {
-          return x.kind == LOC_ARENA && y.kind == LOC_ARENA && x.off < y.off + yb && y.off < x.off + xb;
-        };
-        if (overlaps(s1.la, s1.la_bytes, s2.lc, s2.lc_bytes) || overlaps(s1.lb, s1.lb_bytes, s2.lc, s2.lc_bytes))
-          dep_ok = false;
-        if (dep_ok && make_pair(bound(i), s1.ns, s1.nf, bound(i + 1), s2.ns, s2.nf, pp, ni))
-          fn = pair_fn(ni, s1.ns, s1.nf, s2.ns, s2.nf);
+      if (!(on && g.steps[i].kind == ST_STREAM && g.steps[i + 1].kind == ST_STREAM &&
+            g.steps[i].inv == g.steps[i + 1].inv))
+        continue;
+      const Step &s1 = g.steps[i], &s2 = g.steps[i + 1];
+      bool dep_ok = false;  // step 2 must consume step 1 (its RAW edge)
+      for (int d : s2.deps) dep_ok |= d == (int)i;
+      // C2 may reuse the memory step 1 read (A, P1: released after step 1);
+      // fused, those reads and the C2 writes overlap in time
+      auto overlaps = [](const Loc& x, int64_t xb, const Loc& y, int64_t yb) {
+        return x.kind == LOC_ARENA && y.kind == LOC_ARENA && x.off < y.off + yb && y.off < x.off + xb;
+      };
+      if (overlaps(s1.la, s1.la_bytes, s2.lc, s2.lc_bytes) || overlaps(s1.lb, s1.lb_bytes, s2.lc, s2.lc_bytes))
+        dep_ok = false;
+      Cand& c = cand[i];
+      if (dep_ok && make_pair(bound(i), s1.ns, s1.nf, bound(i + 1), s2.ns, s2.nf, c.pp, c.ni))
+        c.fn = pair_fn(c.ni, s1.ns, s1.nf, s2.ns, s2.nf);
+      if (c.fn) c.gain = 2.0 * 8.0 * (double)bound(i).nx * (double)(1 << s1.nf);
+    }
+    std::vector<double> best(S + 2, 0.0);
+    std::vector<char> take(S + 1, 0);
+    for (size_t i = S; i-- > 0;) {
+      best[i] = best[i + 1];
+      if (cand[i].fn && cand[i].gain + best[i + 2] > best[i]) {
+        best[i] = cand[i].gain + best[i + 2];
+        take[i] = 1;
       }
+    }
+    for (size_t i = 0; i < S;) {
+      PairFn fn = take[i] ? cand[i].fn : nullptr;
+      StreamPairParams pp = cand[i].pp;
+      int ni = cand[i].ni;
+      (void)ni;
       if (fn) {
         const Step &s1 = g.steps[i], &s2 = g.steps[i + 1];
         Launch L;
@@ -802,8 +833,19 @@ struct tc_exec {
     if (gexec) return;
     auto t_graph0 = std::chrono::steady_clock::now();
     count_launches();
-    instantiate(launches, ldeps, true, graph_pro, gexec_pro);
+    // the two graphs are independent: build them on two host threads
+    std::exception_ptr err;
+    std::thread th([&] {
+      try {
+        CU(cudaSetDevice(device));
+        instantiate(launches, ldeps, true, graph_pro, gexec_pro);
+      } catch (...) {
+        err = std::current_exception();
+      }
+    });
     instantiate(launches, ldeps, false, graph, gexec);
+    th.join();
+    if (err) std::rethrow_exception(err);
     graph_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_graph0).count();
   }
 
@@ -827,10 +869,27 @@ struct tc_exec {
         L.tnodes = dalloc<TinyNode>(tn.size(), dev_bytes, device);
         CU(cudaMemcpy(L.tnodes, tn.data(), tn.size() * sizeof(TinyNode), cudaMemcpyHostToDevice));
       }
-      int rc = -1;
-      make_launches(k, L.launches, L.ldeps, rc);
-      instantiate(L.launches, L.ldeps, false, L.graph, L.gexec);
     }
+    // launch records + graph of every new lane on its own host thread
+    std::vector<std::thread> th;
+    std::vector<std::exception_ptr> err(xl.size());
+    for (size_t q = 0; q < xl.size(); ++q) {
+      if (xl[q].gexec) continue;
+      th.emplace_back([this, q, &err] {
+        try {
+          CU(cudaSetDevice(device));
+          Lane& L = xl[q];
+          int rc = -1;
+          make_launches((int)q + 1, L.launches, L.ldeps, rc);
+          instantiate(L.launches, L.ldeps, false, L.graph, L.gexec);
+        } catch (...) {
+          err[q] = std::current_exception();
+        }
+      });
+    }
+    for (auto& t : th) t.join();
+    for (auto& e : err)
+      if (e) std::rethrow_exception(e);
   }
 
   // lanes for a pass of n slices: TC_LANES (default 4), at most n, and only
