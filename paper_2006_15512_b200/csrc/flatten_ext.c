@@ -68,7 +68,18 @@ static void pm_free(PtrMap* m) {
   PyMem_Free(m->key);
   PyMem_Free(m->val);
 }
-static inline size_t pm_hash(uintptr_t k) { return (size_t)((k >> 4) * 0x9E3779B97F4A7C15ull); }
+// full-avalanche mix (murmur3 finalizer): the map masks the LOW bits, and object
+// addresses share their low bits (fixed allocation strides), so a plain
+// multiplicative hash clusters them into long linear-probe runs
+static inline size_t pm_hash(uintptr_t k) {
+  uint64_t x = (uint64_t)k;
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return (size_t)x;
+}
 static void pm_set(PtrMap* m, uintptr_t k, int64_t v) {
   size_t h = pm_hash(k) & m->mask;
   while (m->key[h] && m->key[h] != k) h = (h + 1) & m->mask;
