@@ -119,8 +119,49 @@ class Stats(C.Structure):
         )
 
 
-# every symbol include/tc.h declares, with its ctypes signature
+class FactorInput(C.Structure):  # include/tc_factor.h
+    _fields_ = [
+        ("num_tensors", C.c_int32),
+        ("idx_off", I64P),
+        ("idx", I32P),
+        ("val_off", I64P),
+        ("val_ptr", C.POINTER(C.c_void_p)),
+        ("num_indices", C.c_int32),
+        ("domain", I32P),
+        ("sort_rank", I32P),
+        ("num_nodes", C.c_int32),
+        ("adj_off", I64P),
+        ("adj", I32P),
+        ("str_off", I64P),
+        ("str_buf", C.c_char_p),
+        ("repr_off", I64P),
+        ("repr_buf", C.c_char_p),
+        ("num_leaf_map", C.c_int32),
+        ("leaf_node", I32P),
+        ("leaf_index", I32P),
+    ]
+
+
+class FactorInfo(C.Structure):
+    _fields_ = [
+        ("trivial", C.c_int32),
+        ("branch_width", C.c_int32),
+        ("carving_width", C.c_int32),
+        ("num_pieces", C.c_int32),
+        ("num_bonds", C.c_int32),
+        ("total_idx", C.c_int64),
+        ("total_val", C.c_int64),
+        ("num_nodes", C.c_int32),
+        ("root_slot", C.c_int32),
+    ]
+
+
+# every symbol include/*.h declares, with its ctypes signature
 SIGNATURES = {
+    "tc_factor_branch": (C.c_int, [C.POINTER(FactorInput), C.POINTER(C.c_void_p)]),
+    "tc_factor_info_get": (C.c_int, [C.c_void_p, C.POINTER(FactorInfo)]),
+    "tc_factor_fetch": (C.c_int, [C.c_void_p, I32P, I32P, I64P, I32P, I64P, F64P, I32P, I32P, I32P, I32P, I32P]),
+    "tc_factor_free": (None, [C.c_void_p]),
     "tc_plan_create": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(C.c_void_p)]),
     "tc_plan_free": (None, [C.c_void_p]),
     "tc_plan_info_get": (C.c_int, [C.c_void_p, C.POINTER(PlanInfo)]),

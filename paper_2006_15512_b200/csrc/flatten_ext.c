@@ -8,6 +8,10 @@
 //       leaf_idx_off: bytes(int64), leaf_idx: bytes(int32),
 //       leaf_val_off: bytes(int64), leaf_val: bytes(float64),
 //       left: bytes(int32), right: bytes(int32), root_slot: int)
+//   flatten(tensors, tree, True): the same, but leaf_val holds one uint64
+//       data address per tensor (no copy; the native FactorTree reads the
+//       reference's dense 2^occ copy tensors in place) and a last element
+//       keeps alive the arrays converted to float64 C order.
 //
 // Reads only n.tensors[k].indices / .values, index.id / .domain_size and
 // node.tensor / .left / .right (reference network.py:83-124, tensor.py:18-62).
@@ -141,9 +145,38 @@ static Py_ssize_t put_values(Buf* vals, PyObject* values) {
   return n;
 }
 
+// pointer mode: append the address of `values`' float64 C-contiguous data
+// (converted with numpy.ascontiguousarray when needed; the converted array is
+// kept alive in `keep`); returns the entry count or -1
+static Py_ssize_t put_pointer(Buf* ptrs, PyObject* keep, PyObject* values) {
+  PyObject* arr = values;
+  Py_INCREF(arr);
+  if (!(PyArray_Check(arr) && PyArray_TYPE((PyArrayObject*)arr) == NPY_DOUBLE &&
+        PyArray_IS_C_CONTIGUOUS((PyArrayObject*)arr) && PyArray_ISNOTSWAPPED((PyArrayObject*)arr) &&
+        PyArray_ISALIGNED((PyArrayObject*)arr))) {
+    PyObject* np = PyImport_ImportModule("numpy");
+    Py_DECREF(arr);
+    if (!np) return -1;
+    arr = PyObject_CallMethod(np, "ascontiguousarray", "Os", values, "float64");
+    Py_DECREF(np);
+    if (!arr) return -1;
+    if (PyList_Append(keep, arr) < 0) {
+      Py_DECREF(arr);
+      return -1;
+    }
+  }
+  const Py_ssize_t n = PyArray_SIZE((PyArrayObject*)arr);
+  const uint64_t ptr = (uint64_t)(uintptr_t)PyArray_DATA((PyArrayObject*)arr);
+  Py_DECREF(arr);  // owned by the tensor or by `keep`
+  return buf_put(ptrs, &ptr, 8) == 0 ? n : -1;
+}
+
 static PyObject* flatten(PyObject* self, PyObject* args) {
   PyObject *tensors_in, *tree;
-  if (!PyArg_ParseTuple(args, "OO", &tensors_in, &tree)) return NULL;
+  int ptr_mode = 0;
+  if (!PyArg_ParseTuple(args, "OO|p", &tensors_in, &tree, &ptr_mode)) return NULL;
+  PyObject* keep = ptr_mode ? PyList_New(0) : NULL;
+  if (ptr_mode && !keep) return NULL;
   PyObject* tensors = PySequence_Fast(tensors_in, "n.tensors must be a sequence");
   if (!tensors) return NULL;
   const Py_ssize_t nl = PySequence_Fast_GET_SIZE(tensors);
@@ -228,7 +261,7 @@ static PyObject* flatten(PyObject* self, PyObject* args) {
     if (buf_put(&ioff, &off, 8) < 0) goto done;
     PyObject* values = PyObject_GetAttr(ten, s_values);
     if (!values) goto done;
-    Py_ssize_t nv = put_values(&vals, values);
+    Py_ssize_t nv = ptr_mode ? put_pointer(&vals, keep, values) : put_values(&vals, values);
     Py_DECREF(values);
     if (nv < 0) goto done;
     voffv += nv;
@@ -396,9 +429,12 @@ static PyObject* flatten(PyObject* self, PyObject* args) {
         if (e->parent >= 0) ent[e->parent].kid[e->side] = s;
         else root_slot = s;
       }
-      result = Py_BuildValue("(ONNNNNNNL)", indices, buf_bytes(&dom), buf_bytes(&ioff), buf_bytes(&iarr),
-                             buf_bytes(&voff), buf_bytes(&vals), buf_bytes(&lft), buf_bytes(&rgt),
-                             (long long)root_slot);
+      result = ptr_mode ? Py_BuildValue("(ONNNNNNNLO)", indices, buf_bytes(&dom), buf_bytes(&ioff), buf_bytes(&iarr),
+                                        buf_bytes(&voff), buf_bytes(&vals), buf_bytes(&lft), buf_bytes(&rgt),
+                                        (long long)root_slot, keep)
+                        : Py_BuildValue("(ONNNNNNNL)", indices, buf_bytes(&dom), buf_bytes(&ioff), buf_bytes(&iarr),
+                                        buf_bytes(&voff), buf_bytes(&vals), buf_bytes(&lft), buf_bytes(&rgt),
+                                        (long long)root_slot);
     }
   tree_fail:
     for (size_t q = 0; q < ns; ++q) Py_DECREF(ent[q].node);
@@ -420,6 +456,7 @@ done:
   PyMem_Free(rgt.p);
   Py_XDECREF(indices);
   Py_XDECREF(pos);
+  Py_XDECREF(keep);
   Py_DECREF(tensors);
   return result;
 }

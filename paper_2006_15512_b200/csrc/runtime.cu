@@ -1288,6 +1288,11 @@ const std::vector<ncclComm_t>& nccl_comms(const std::vector<int>& devs) {
   return cache.emplace(devs, std::move(comms)).first->second;
 }
 
+namespace tc {
+// the error channel of tc_last_error for the host-only parts (factor.cpp)
+int set_last_error(int status, const std::string& msg) { return set_err(status, msg); }
+}  // namespace tc
+
 // ---------------------------------------------------------------------------
 extern "C" {
 

@@ -3,7 +3,9 @@
 Names and meaning mirror the reference hierarchy
 (``pkg/src/tensorcount/errors.py``): ``IndexMismatch`` (:32),
 ``BindingOutOfDomain`` (:36), ``IndexOveruse`` (:42), ``PlanMismatch`` (:46),
-``NotABondIndex`` (:80), ``NoCandidates`` (:84), ``BudgetInfeasible`` (:88).
+``NotABondIndex`` (:80), ``NoCandidates`` (:84), ``BudgetInfeasible`` (:88),
+and for the native FactorTree step ``InvalidDecomposition`` (:52),
+``NotFactorable`` (:70), ``TooManyFreeIndices`` (:74).
 
 ``reference_patch.install`` re-raises these as the reference's own classes
 (same name) so code catching ``tensorcount.errors.BudgetInfeasible`` keeps
@@ -42,6 +44,18 @@ class NoCandidates(CounterError):
 
 
 class BudgetInfeasible(CounterError):
+    pass
+
+
+class InvalidDecomposition(CounterError):
+    pass
+
+
+class NotFactorable(CounterError):
+    pass
+
+
+class TooManyFreeIndices(CounterError):
     pass
 
 

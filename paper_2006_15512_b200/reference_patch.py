@@ -20,6 +20,7 @@ import functools
 import importlib
 
 from . import errors as own_errors
+from . import factoring as own_factoring
 from . import network as own_network
 from . import slicing as own_slicing
 from . import tensor as own_tensor
@@ -30,18 +31,24 @@ _SAVED = {}
 def _translate(ref_errors):
     mapping = {}
     for name in ("IndexMismatch", "BindingOutOfDomain", "IndexOveruse", "PlanMismatch",
-                 "NotABondIndex", "NoCandidates", "BudgetInfeasible"):
+                 "NotABondIndex", "NoCandidates", "BudgetInfeasible", "InvalidDecomposition",
+                 "NotFactorable", "TooManyFreeIndices"):
         mapping[getattr(own_errors, name)] = getattr(ref_errors, name)
     return mapping
 
 
-def install(tensorcount=None, devices=None, contract_pair=False):
+def install(tensorcount=None, devices=None, contract_pair=False, execution=True, factoring=True):
     """Patch ``tensorcount.{driver,slicing,network}`` to use libtc.  With
     ``contract_pair=True`` also ``tensorcount.tensor.contract_pair``
-    (tensor.py:96-108) — the reference's own test suite imports it directly."""
+    (tensor.py:96-108) — the reference's own test suite imports it directly.
+    ``factoring`` swaps in the native FactorTree step (``factoring.py``:
+    ``factor_branch_audit`` / ``factor_branch``, also as bound by
+    ``driver.py:22`` and ``__init__.py:5``); ``execution=False`` leaves the
+    execution path on the reference (the CPU-only check of the factoring)."""
     if tensorcount is None:
         tensorcount = importlib.import_module("tensorcount")
     driver = importlib.import_module(tensorcount.__name__ + ".driver")
+    ref_factoring = importlib.import_module(tensorcount.__name__ + ".factoring")
     slicing = importlib.import_module(tensorcount.__name__ + ".slicing")
     network = importlib.import_module(tensorcount.__name__ + ".network")
     tensor = importlib.import_module(tensorcount.__name__ + ".tensor")
@@ -70,15 +77,39 @@ def install(tensorcount=None, devices=None, contract_pair=False):
     def execute(n, t):
         return own_network.execute(n, t, devices=devices)
 
-    patched = {
-        (driver, "sliced_execute"): wrap(sliced_execute, to_ref),
-        (slicing, "sliced_execute"): wrap(sliced_execute, to_ref),
-        (slicing, "mem_cost"): wrap(own_slicing.mem_cost),
-        (slicing, "choose_slice_index"): wrap(own_slicing.choose_slice_index),
-        (network, "execute"): wrap(execute),
-        (tensorcount, "sliced_execute"): wrap(sliced_execute, to_ref),
-        (tensorcount, "execute"): wrap(execute),
-    }
+    RefFBR = ref_factoring.FactorBranchResult
+    tree_cls = network.ContractionTree
+
+    def to_ref_fbr(r):
+        return RefFBR(r.network, r.tree, r.branch_width, r.carving_width, r.piece_map)
+
+    def factor_branch_audit(n, bd, g=None):
+        return own_factoring.factor_branch_audit(n, bd, g, tree_cls=tree_cls)
+
+    def factor_branch(n, bd, g=None):
+        r = own_factoring.factor_branch_audit(n, bd, g, tree_cls=tree_cls)
+        return r.network, r.tree
+
+    patched = {}
+    if factoring:
+        patched.update({
+            (ref_factoring, "factor_branch_audit"): wrap(factor_branch_audit, to_ref_fbr),
+            (ref_factoring, "factor_branch"): wrap(factor_branch),
+            (driver, "factor_branch_audit"): wrap(factor_branch_audit, to_ref_fbr),
+            (tensorcount, "factor_branch"): wrap(factor_branch),
+        })
+    if execution:
+        patched.update({
+            (driver, "sliced_execute"): wrap(sliced_execute, to_ref),
+            (slicing, "sliced_execute"): wrap(sliced_execute, to_ref),
+            (slicing, "mem_cost"): wrap(own_slicing.mem_cost),
+            (slicing, "choose_slice_index"): wrap(own_slicing.choose_slice_index),
+            (network, "execute"): wrap(execute),
+            (tensorcount, "sliced_execute"): wrap(sliced_execute, to_ref),
+            (tensorcount, "execute"): wrap(execute),
+        })
+    else:
+        contract_pair = False
     if contract_pair:
         dev = (devices or [0])[0]
 

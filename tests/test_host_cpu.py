@@ -22,7 +22,8 @@ CASES = load_cases()
 
 
 def test_library_exports_every_header_symbol():
-    hdr = open(os.path.join(ROOT, "include", "tc.h")).read()
+    import glob
+    hdr = "".join(open(h).read() for h in sorted(glob.glob(os.path.join(ROOT, "include", "*.h"))))
     declared = set(re.findall(r"\b(tc_[a-z0-9_]+)\s*\(", hdr))
     assert declared, "no declarations parsed"
     so = ctypes.CDLL(_lib.LIB_PATH)
