@@ -156,8 +156,26 @@ class FactorInfo(C.Structure):
     ]
 
 
+class DecompInfo(C.Structure):  # include/tc_decompose.h
+    _fields_ = [
+        ("num_nodes", C.c_int32),
+        ("num_adj", C.c_int64),
+        ("num_bag", C.c_int64),
+        ("num_order", C.c_int32),
+        ("num_leaf_map", C.c_int32),
+        ("counter_end", C.c_int64),
+    ]
+
+
 # every symbol include/*.h declares, with its ctypes signature
 SIGNATURES = {
+    "tc_elim_td": (C.c_int, [C.c_int32, I64P, I32P, C.c_int32, C.POINTER(C.c_uint32), C.c_int32, C.c_int64,
+                             C.POINTER(C.c_void_p)]),
+    "tc_tree_to_branch": (C.c_int, [C.c_int32, I64P, I32P, I32P, I64P, I32P, C.c_int32, C.c_int32, I32P, I32P,
+                                    C.c_int64, C.POINTER(C.c_void_p)]),
+    "tc_decomp_info_get": (C.c_int, [C.c_void_p, C.POINTER(DecompInfo)]),
+    "tc_decomp_fetch": (C.c_int, [C.c_void_p, I32P, I64P, I64P, I32P, I64P, I32P, I32P, I32P, I32P]),
+    "tc_decomp_free": (None, [C.c_void_p]),
     "tc_factor_branch": (C.c_int, [C.POINTER(FactorInput), C.POINTER(C.c_void_p)]),
     "tc_factor_info_get": (C.c_int, [C.c_void_p, C.POINTER(FactorInfo)]),
     "tc_factor_fetch": (C.c_int, [C.c_void_p, I32P, I32P, I64P, I32P, I64P, F64P, I32P, I32P, I32P, I32P, I32P]),

@@ -19,8 +19,8 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib", "libtc.so")
 FLAT_SRC = os.path.join(CSRC, "flatten_ext.c")
 
-SOURCES = ["plan.cpp", "compile.cpp", "factor.cpp", "runtime.cu"]
-HEADERS = ["plan.hpp", "compile.hpp", "program.h", "kernels.cuh"]
+SOURCES = ["plan.cpp", "compile.cpp", "factor.cpp", "decompose.cpp", "runtime.cu"]
+HEADERS = ["plan.hpp", "compile.hpp", "program.h", "kernels.cuh", "ograph.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -68,6 +68,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "tc.h"))
     deps.append(os.path.join(ROOT, "include", "tc_factor.h"))
+    deps.append(os.path.join(ROOT, "include", "tc_decompose.h"))
     deps.append(os.path.abspath(__file__))
     lib_out = out or LIB
     if not force and not _stale(lib_out, deps):

@@ -4,7 +4,7 @@ Names and meaning mirror the reference hierarchy
 (``pkg/src/tensorcount/errors.py``): ``IndexMismatch`` (:32),
 ``BindingOutOfDomain`` (:36), ``IndexOveruse`` (:42), ``PlanMismatch`` (:46),
 ``NotABondIndex`` (:80), ``NoCandidates`` (:84), ``BudgetInfeasible`` (:88),
-and for the native FactorTree step ``InvalidDecomposition`` (:52),
+and for the native planning steps ``InvalidDecomposition`` (:52), ``NoHostBag`` (:64),
 ``NotFactorable`` (:70), ``TooManyFreeIndices`` (:74).
 
 ``reference_patch.install`` re-raises these as the reference's own classes
@@ -48,6 +48,10 @@ class BudgetInfeasible(CounterError):
 
 
 class InvalidDecomposition(CounterError):
+    pass
+
+
+class NoHostBag(CounterError):
     pass
 
 

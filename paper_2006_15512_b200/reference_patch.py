@@ -19,6 +19,7 @@ from __future__ import annotations
 import functools
 import importlib
 
+from . import decomposition as own_decomposition
 from . import errors as own_errors
 from . import factoring as own_factoring
 from . import network as own_network
@@ -32,23 +33,29 @@ def _translate(ref_errors):
     mapping = {}
     for name in ("IndexMismatch", "BindingOutOfDomain", "IndexOveruse", "PlanMismatch",
                  "NotABondIndex", "NoCandidates", "BudgetInfeasible", "InvalidDecomposition",
-                 "NotFactorable", "TooManyFreeIndices"):
+                 "NotFactorable", "TooManyFreeIndices", "NoHostBag"):
         mapping[getattr(own_errors, name)] = getattr(ref_errors, name)
     return mapping
 
 
-def install(tensorcount=None, devices=None, contract_pair=False, execution=True, factoring=True):
+def install(tensorcount=None, devices=None, contract_pair=False, execution=True, factoring=True, planning=True):
     """Patch ``tensorcount.{driver,slicing,network}`` to use libtc.  With
     ``contract_pair=True`` also ``tensorcount.tensor.contract_pair``
     (tensor.py:96-108) — the reference's own test suite imports it directly.
     ``factoring`` swaps in the native FactorTree step (``factoring.py``:
     ``factor_branch_audit`` / ``factor_branch``, also as bound by
-    ``driver.py:22`` and ``__init__.py:5``); ``execution=False`` leaves the
-    execution path on the reference (the CPU-only check of the factoring)."""
+    ``driver.py:22`` and ``__init__.py:5``); ``planning`` the native
+    min-fill / min-degree decompositions and ``tree_to_branch``
+    (``decomposition.py``, also as bound by ``portfolio.py:18-31`` and
+    ``driver.py:20``, fresh names from the reference's own counter);
+    ``execution=False`` leaves the execution path on the reference (the
+    CPU-only check of the host-side steps)."""
     if tensorcount is None:
         tensorcount = importlib.import_module("tensorcount")
     driver = importlib.import_module(tensorcount.__name__ + ".driver")
     ref_factoring = importlib.import_module(tensorcount.__name__ + ".factoring")
+    ref_decomp = importlib.import_module(tensorcount.__name__ + ".decomposition")
+    ref_portfolio = importlib.import_module(tensorcount.__name__ + ".portfolio")
     slicing = importlib.import_module(tensorcount.__name__ + ".slicing")
     network = importlib.import_module(tensorcount.__name__ + ".network")
     tensor = importlib.import_module(tensorcount.__name__ + ".tensor")
@@ -90,7 +97,24 @@ def install(tensorcount=None, devices=None, contract_pair=False, execution=True,
         r = own_factoring.factor_branch_audit(n, bd, g, tree_cls=tree_cls)
         return r.network, r.tree
 
+    counter = own_decomposition._Counter(ref_decomp)
+
+    def min_fill(g, seed=0):
+        return own_decomposition.min_fill_tree_decomposition(g, seed, ref_decomp.TreeDecomposition, counter)
+
+    def min_degree(g, seed=0):
+        return own_decomposition.min_degree_tree_decomposition(g, seed, ref_decomp.TreeDecomposition, counter)
+
+    def tree_to_branch(td, g):
+        return own_decomposition.tree_to_branch(td, g, ref_decomp.BranchDecomposition, counter)
+
     patched = {}
+    if planning:
+        for mod in (ref_decomp, ref_portfolio):
+            patched[(mod, "min_fill_tree_decomposition")] = wrap(min_fill)
+            patched[(mod, "min_degree_tree_decomposition")] = wrap(min_degree)
+        patched[(ref_decomp, "tree_to_branch")] = wrap(tree_to_branch)
+        patched[(driver, "tree_to_branch")] = wrap(tree_to_branch)
     if factoring:
         patched.update({
             (ref_factoring, "factor_branch_audit"): wrap(factor_branch_audit, to_ref_fbr),

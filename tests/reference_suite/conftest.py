@@ -12,15 +12,17 @@ prescribe:
   modules import it, so ``driver.sliced_execute``, ``slicing.sliced_execute``,
   ``slicing.mem_cost``, ``slicing.choose_slice_index``, ``network.execute`` and
   ``tensor.contract_pair`` all run on the GPU through libtc, and
-  ``factoring.factor_branch_audit`` / ``factor_branch`` natively;
+  ``factoring.factor_branch_audit`` / ``factor_branch``, the min-fill /
+  min-degree decompositions and ``tree_to_branch`` natively;
 * registers the reference's conftest as ``tests.conftest`` (a regular package
   named ``tests`` in site-packages shadows the reference's namespace dir,
   SURVEY §8c gotcha 1).
 
 ``TC_REFSUITE_PATCH=0`` runs the same files against the unpatched reference
-(the CPU baseline of the suite); ``TC_REFSUITE_PATCH=factoring`` swaps in only
-the native FactorTree step (``paper_2006_15512_b200/factoring.py``), so the
-factoring-dependent files run on the CPU.
+(the CPU baseline of the suite); ``TC_REFSUITE_PATCH=host`` swaps in only the
+native host-side steps (planning heuristics, ``tree_to_branch`` and FactorTree:
+``paper_2006_15512_b200/decomposition.py`` / ``factoring.py``), so every file
+runs on the CPU with the reference's execution path.
 """
 
 import importlib.util
@@ -39,7 +41,7 @@ sys.path.insert(0, ROOT)
 import tensorcount  # noqa: E402
 
 _MODE = os.environ.get("TC_REFSUITE_PATCH", "1")
-if _MODE == "factoring":  # CPU-only: the native FactorTree step, reference execution
+if _MODE in ("host", "factoring"):  # CPU-only: native planning + FactorTree, reference execution
     from paper_2006_15512_b200 import reference_patch  # noqa: E402
 
     reference_patch.install(tensorcount, execution=False)

@@ -1,0 +1,143 @@
+"""Native planning heuristics (paper_2006_15512_b200/decomposition.py,
+csrc/decompose.cpp) against the reference's min-fill / min-degree tree
+decompositions and tree_to_branch (decomposition.py:244-411).
+
+* golden: 40 reference runs frozen in tests/golden/decomp.json
+  (make_decomp_golden.py): node names, node / adjacency order, bags, leaf maps;
+* live: the unmodified reference side by side (same fresh-name counter) on
+  random formulas and the C2 benchmark formula (skipped without it).
+The reference's own suite with these swapped in runs in test_factoring.py.
+"""
+
+import itertools
+import json
+import os
+import random
+import sys
+
+import pytest
+
+from conftest import GOLDEN, ROOT
+from paper_2006_15512_b200 import decomposition as ND
+from paper_2006_15512_b200.errors import InvalidDecomposition, NoHostBag
+
+
+class Graph:
+    """The parts of the reference's multigraph (graphs.py:13-73) the planners read."""
+
+    def __init__(self, vertices, edges):
+        self.vertices = set(vertices)
+        self.edges = {e: frozenset(ends) for e, ends in edges.items()}
+
+    def endpoints(self, e):
+        return self.edges[e]
+
+    def simple_adjacency(self):
+        adj = {v: set() for v in self.vertices}
+        for a, b in (tuple(x) for x in self.edges.values()):
+            adj[a].add(b)
+            adj[b].add(a)
+        return adj
+
+
+def _tree(t):
+    nodes = list(t.nodes)
+    pos = {u: k for k, u in enumerate(nodes)}
+    return [list(u) for u in nodes], [[pos[w] for w in t.adj[u]] for u in nodes]
+
+
+CASES = json.load(open(os.path.join(GOLDEN, "decomp.json")))
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c['kind']}-{c['seed']}" for c in CASES])
+def test_golden_matches_reference(case):
+    verts = [f"v{k:06d}" for k in range(case["nv"])]
+    g = Graph(verts, {f"e{k:06d}": (verts[a], verts[b]) for k, (a, b) in enumerate(case["edges"])})
+    ND._fresh = itertools.count(0)
+    build = ND.min_fill_tree_decomposition if case["kind"] == "minfill" else ND.min_degree_tree_decomposition
+    td = build(g, case["seed"])
+    nodes, adj = _tree(td.tree)
+    assert nodes == case["td_nodes"] and adj == case["td_adj"]
+    assert [sorted(int(x[1:]) for x in td.bags[tuple(u)]) for u in nodes] == case["bags"]
+    bd = ND.tree_to_branch(td, g)
+    nodes, adj = _tree(bd.tree)
+    assert nodes == case["bd_nodes"] and adj == case["bd_adj"]
+    pos = {tuple(u): k for k, u in enumerate(nodes)}
+    assert [[pos[u], int(e[1:])] for u, e in bd.leaf_map.items()] == case["leaf_map"]
+
+
+def test_errors():
+    g = Graph(["a", "b", "c"], {"x": ("a", "b"), "y": ("b", "c")})
+    td = ND.min_fill_tree_decomposition(g, 0)
+    bad = ND.TreeDecomposition(td.tree, {u: frozenset() for u in td.tree.nodes})
+    with pytest.raises(NoHostBag, match="no bag contains both endpoints of edge 'x'"):
+        ND.tree_to_branch(bad, g)
+    with pytest.raises(InvalidDecomposition, match="requires a graph with edges"):
+        ND.tree_to_branch(td, Graph(["a"], {}))
+    empty = ND.min_fill_tree_decomposition(Graph([], {}), 0)
+    assert len(empty.tree) == 1 and list(empty.bags.values()) == [frozenset()]
+
+
+def _reference():
+    for p in (os.path.join(ROOT, "oracle", "_ref"), os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "tensorcount")):
+            if p not in sys.path:
+                sys.path.insert(1, p)
+            try:
+                import tensorcount  # noqa: F401
+                return True
+            except Exception:
+                return False
+    return False
+
+
+needs_ref = pytest.mark.skipif(not _reference(), reason="reference not importable")
+
+
+def _same_run(RD, g, seed, ref_build, nat_build):
+    start = next(RD._fresh)
+    RD._fresh = itertools.count(start)
+    ND._fresh = itertools.count(start)
+    td1, td2 = ref_build(g, seed), nat_build(g, seed)
+    assert _tree(td1.tree) == _tree(td2.tree) and td1.bags == td2.bags
+    if g.edges:
+        bd1, bd2 = RD.tree_to_branch(td1, g), ND.tree_to_branch(td2, g)
+        assert _tree(bd1.tree) == _tree(bd2.tree)
+        assert list(bd1.leaf_map.items()) == list(bd2.leaf_map.items())
+    assert next(RD._fresh) == next(ND._fresh)  # the same number of fresh names
+
+
+@needs_ref
+def test_live_random_structure_graphs():
+    import tensorcount.decomposition as RD
+    from tensorcount.formula import parse_dimacs
+    from tensorcount.network import structure_graph
+    from tensorcount.reduction import reduce_formula
+
+    rng = random.Random(11)
+    for trial in range(120):
+        nv = rng.randint(1, 18)
+        lines = [f"p cnf {nv} 0"]
+        clauses = []
+        for _ in range(rng.randint(0, 3 * nv)):
+            vs = rng.sample(range(1, nv + 1), min(rng.randint(1, 4), nv))
+            clauses.append(" ".join(str(v if rng.random() < 0.5 else -v) for v in vs) + " 0")
+        lines[0] = f"p cnf {nv} {len(clauses)}"
+        f, w = parse_dimacs("\n".join(lines + clauses) + "\n")
+        g = structure_graph(reduce_formula(f, w))
+        _same_run(RD, g, trial, RD.min_fill_tree_decomposition, ND.min_fill_tree_decomposition)
+        _same_run(RD, g, trial, RD.min_degree_tree_decomposition, ND.min_degree_tree_decomposition)
+
+
+@needs_ref
+def test_live_c2_formula():
+    import tensorcount.decomposition as RD
+    from tensorcount.formula import parse_dimacs
+    from tensorcount.network import structure_graph
+    from tensorcount.reduction import reduce_formula
+
+    from paper_2006_15512_b200.generators import config_dimacs
+
+    f, w = parse_dimacs(config_dimacs("c2"))
+    g = structure_graph(reduce_formula(f, w))
+    _same_run(RD, g, 0, RD.min_fill_tree_decomposition, ND.min_fill_tree_decomposition)

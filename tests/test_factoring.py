@@ -197,11 +197,12 @@ def test_live_benchmark_formulas(config):
 
 
 @needs_ref
-def test_reference_suite_with_native_factoring():
-    """All 208 reference tests with factor_branch_audit / factor_branch swapped
-    for the native step (execution stays on the reference's CPU path)."""
+def test_reference_suite_with_native_host_steps():
+    """All 208 reference tests with the native planning heuristics,
+    tree_to_branch and FactorTree swapped in (execution stays on the
+    reference's CPU path)."""
     suite = os.path.join(ROOT, "tests", "reference_suite")
-    env = dict(os.environ, PYTHONDONTWRITEBYTECODE="1", TC_REFSUITE_PATCH="factoring")
+    env = dict(os.environ, PYTHONDONTWRITEBYTECODE="1", TC_REFSUITE_PATCH="host")
     p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "--confcutdir", suite,
                         "--rootdir", suite, suite], cwd=suite, env=env, capture_output=True, text=True, timeout=1800)
     m = re.search(r"(\d+) passed", p.stdout)
