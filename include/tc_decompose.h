@@ -8,6 +8,7 @@
  *   _elimination_tree_decomposition  decomposition.py:258-275
  *   binarize_tree_decomposition      decomposition.py:278-294
  *   tree_to_branch (+ _prune_and_smooth)  decomposition.py:346-411
+ *   validate_tree_decomposition      decomposition.py:81-108
  * with the reference's exact output: the same elimination order (ties broken
  * by the same Mersenne-Twister draws as random.Random(seed).choice, the
  * caller passes the generator state), the same bags, the same decomposition
@@ -41,6 +42,16 @@ int tc_elim_td(int32_t nv, const int64_t* adj_off, const int32_t* adj, int32_t s
 int tc_tree_to_branch(int32_t nn, const int64_t* adj_off, const int32_t* adj, const int32_t* node_rank,
                       const int64_t* bag_off, const int32_t* bag, int32_t nv, int32_t ne, const int32_t* edge_u,
                       const int32_t* edge_v, int64_t counter_start, tc_decomp_result** out);
+
+/* The structural checks of validate_tree_decomposition (decomposition.py:81-108)
+ * that cost O(|E| x |bags|) in Python: the tree shape, a host bag for every
+ * edge, and connected bags per vertex.  Vertex ids >= nv are vertices outside
+ * the graph.  Results: *shape 0 ok, 1 empty tree, 2 not a tree; *bad_edge the
+ * first edge (in the given order) without a host bag or -1; disconnected[v] = 1
+ * for every vertex whose bags are disconnected. */
+int tc_validate_td(int32_t nn, const int64_t* adj_off, const int32_t* adj, const int64_t* bag_off,
+                   const int32_t* bag, int32_t nv, int32_t ne, const int32_t* edge_u, const int32_t* edge_v,
+                   int32_t* shape, int32_t* bad_edge, int8_t* disconnected);
 
 typedef struct tc_decomp_info {
   int32_t num_nodes;       /* tree nodes (networkx order)                       */

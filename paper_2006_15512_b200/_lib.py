@@ -173,6 +173,8 @@ SIGNATURES = {
                              C.POINTER(C.c_void_p)]),
     "tc_tree_to_branch": (C.c_int, [C.c_int32, I64P, I32P, I32P, I64P, I32P, C.c_int32, C.c_int32, I32P, I32P,
                                     C.c_int64, C.POINTER(C.c_void_p)]),
+    "tc_validate_td": (C.c_int, [C.c_int32, I64P, I32P, I64P, I32P, C.c_int32, C.c_int32, I32P, I32P,
+                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int8)]),
     "tc_decomp_info_get": (C.c_int, [C.c_void_p, C.POINTER(DecompInfo)]),
     "tc_decomp_fetch": (C.c_int, [C.c_void_p, I32P, I64P, I64P, I32P, I64P, I32P, I32P, I32P, I32P]),
     "tc_decomp_free": (None, [C.c_void_p]),

@@ -383,6 +383,80 @@ int tc_tree_to_branch(int32_t nn, const int64_t* adj_off, const int32_t* adj, co
   return TC_OK;
 }
 
+int tc_validate_td(int32_t nn, const int64_t* adj_off, const int32_t* adj, const int64_t* bag_off,
+                   const int32_t* bag, int32_t nv, int32_t ne, const int32_t* edge_u, const int32_t* edge_v,
+                   int32_t* shape, int32_t* bad_edge, int8_t* disconnected) {
+  if (!shape || !bad_edge || (nv > 0 && !disconnected)) return set_last_error(TC_BAD_ARG, "null output");
+  return guarded([&] {
+    *shape = 0;
+    *bad_edge = -1;
+    for (int v = 0; v < nv; ++v) disconnected[v] = 0;
+    // _check_tree_shape (decomposition.py:81-85): non-empty, connected, |E| = |V| - 1
+    if (nn == 0) {
+      *shape = 1;
+      return;
+    }
+    int64_t ends = 0;
+    for (int k = 0; k < nn; ++k)
+      for (int64_t q = adj_off[k]; q < adj_off[k + 1]; ++q) {
+        if (adj[q] < 0 || adj[q] >= nn) throw Error{TC_BAD_ARG, "bad tree adjacency"};
+        ++ends;
+      }
+    bool ok = ends == 2 * (int64_t)(nn - 1);
+    if (ok) {
+      std::vector<char> seen(nn, 0);
+      std::vector<int> st{0};
+      seen[0] = 1;
+      int cnt = 1;
+      while (!st.empty()) {
+        const int u = st.back();
+        st.pop_back();
+        for (int64_t q = adj_off[u]; q < adj_off[u + 1]; ++q)
+          if (!seen[adj[q]]) seen[adj[q]] = 1, ++cnt, st.push_back(adj[q]);
+      }
+      ok = cnt == nn;
+    }
+    if (!ok) {
+      *shape = 2;
+      return;
+    }
+    // host bags: the first edge (in order) none of whose bags holds both ends
+    std::vector<std::vector<int>> holds(std::max(0, nv));
+    std::vector<int> bag_size(nn);
+    for (int k = 0; k < nn; ++k)
+      for (int64_t q = bag_off[k]; q < bag_off[k + 1]; ++q) {
+        const int x = bag[q];
+        if (x >= 0 && x < nv && (holds[x].empty() || holds[x].back() != k)) holds[x].push_back(k);
+      }
+    for (int e = 0; e < ne && *bad_edge < 0; ++e) {
+      const auto& a = holds[edge_u[e]];
+      const auto& b = holds[edge_v[e]];
+      bool host = false;
+      for (size_t i = 0, j = 0; i < a.size() && j < b.size() && !host;) {
+        if (a[i] < b[j]) ++i;
+        else if (b[j] < a[i]) ++j;
+        else host = true;
+      }
+      if (!host) *bad_edge = e;
+    }
+    // per vertex: its bags induce a connected subtree iff nodes - edges == 1
+    std::vector<int64_t> induced_edges(std::max(0, nv), 0);
+    std::vector<int> mark(std::max(0, nv), -1);
+    for (int u = 0; u < nn; ++u) {
+      for (int64_t q = bag_off[u]; q < bag_off[u + 1]; ++q)
+        if (bag[q] >= 0 && bag[q] < nv) mark[bag[q]] = u;
+      for (int64_t q = adj_off[u]; q < adj_off[u + 1]; ++q) {
+        const int w = adj[q];
+        if (w <= u) continue;  // each tree edge once
+        for (int64_t r = bag_off[w]; r < bag_off[w + 1]; ++r)
+          if (bag[r] >= 0 && bag[r] < nv && mark[bag[r]] == u) ++induced_edges[bag[r]];
+      }
+    }
+    for (int v = 0; v < nv; ++v)
+      if (!holds[v].empty() && (int64_t)holds[v].size() - induced_edges[v] != 1) disconnected[v] = 1;
+  });
+}
+
 int tc_decomp_info_get(const tc_decomp_result* r, tc_decomp_info* info) {
   if (!r || !info) return set_last_error(TC_BAD_ARG, "null argument");
   *info = r->info;

@@ -204,3 +204,61 @@ def tree_to_branch(td, g, bd_cls=BranchDecomposition, counter=None):
     tree = _graph(labels, t_off, t_adj)
     leaf_map = {labels[k]: edges[e] for k, e in zip(leaf_node.tolist(), leaf_edge.tolist())}
     return bd_cls(tree, leaf_map)
+
+
+def validate_tree_decomposition(td, g):
+    """InvalidDecomposition unless td is a tree decomposition of g
+    (decomposition.py:88-108, same checks, order and messages); the
+    O(|E| x |bags|) host-bag and connectivity scans run natively."""
+    what = "tree decomposition"
+    nodes = list(td.tree.nodes)
+    npos = {u: k for k, u in enumerate(nodes)}
+    lists = [[npos[w] for w in td.tree.adj[u]] for u in nodes]
+    adj_off = np.zeros(len(nodes) + 1, np.int64)
+    np.cumsum([len(a) for a in lists], out=adj_off[1:])
+    adj = np.fromiter((w for a in lists for w in a), np.int32, count=int(adj_off[-1]))
+    verts = list(g.vertices)
+    vid = {v: k for k, v in enumerate(verts)}
+    if set(td.bags) != set(nodes):
+        shape_only = True
+    else:
+        shape_only = False
+    bag_lists = [[vid.get(x, len(verts)) for x in td.bags[u]] for u in nodes] if not shape_only else [[]] * len(nodes)
+    bag_off = np.zeros(len(nodes) + 1, np.int64)
+    np.cumsum([len(b) for b in bag_lists], out=bag_off[1:])
+    bag = np.fromiter((x for b in bag_lists for x in b), np.int32, count=int(bag_off[-1]))
+    edges = list(g.edges)
+    ends = [tuple(g.edges[e]) for e in edges]
+    eu = np.asarray([vid[a] for a, _ in ends], np.int32)
+    ev = np.asarray([vid[b] for _, b in ends], np.int32)
+    shape, bad_edge = C.c_int32(), C.c_int32()
+    disc = np.zeros(max(1, len(verts)), np.int8)
+    p = _lib._p
+    _lib.check(_lib.lib().tc_validate_td(len(nodes), p(adj_off, _lib.I64P), p(adj, _lib.I32P), p(bag_off, _lib.I64P),
+                                         p(bag, _lib.I32P), len(verts), len(edges), p(eu, _lib.I32P),
+                                         p(ev, _lib.I32P), C.byref(shape), C.byref(bad_edge),
+                                         p(disc, C.POINTER(C.c_int8))))
+    if shape.value == 1:
+        raise InvalidDecomposition(f"{what}: empty tree")
+    if shape.value == 2:
+        raise InvalidDecomposition(f"{what}: decomposition graph is not a tree")
+    if shape_only:
+        raise InvalidDecomposition(f"{what}: bags do not label every node")
+    covered = set().union(*td.bags.values()) if td.bags else set()
+    if covered != set(g.vertices):
+        missing = set(g.vertices) - covered
+        if missing:
+            raise InvalidDecomposition(f"{what}: vertices {missing} in no bag")
+        raise InvalidDecomposition(f"{what}: bags contain unknown vertices")
+    if bad_edge.value >= 0:
+        raise InvalidDecomposition(f"{what}: edge {edges[bad_edge.value]!r} has no host bag")
+    for v in g.vertices:
+        if disc[vid[v]]:
+            raise InvalidDecomposition(f"{what}: bags containing {v!r} are disconnected")
+
+
+def width_tree(td, g=None) -> int:
+    """decomposition.py:144-147."""
+    if g is not None:
+        validate_tree_decomposition(td, g)
+    return td.width()

@@ -108,13 +108,20 @@ def install(tensorcount=None, devices=None, contract_pair=False, execution=True,
     def tree_to_branch(td, g):
         return own_decomposition.tree_to_branch(td, g, ref_decomp.BranchDecomposition, counter)
 
+    def time_cost(n, t, throughput=1e9):  # network.py:184-188 with the native plan (contraction_ops)
+        _, h = own_slicing._plan(n, t, with_sort_rank=False)
+        return h.info().contraction_ops.value() / throughput
+
     patched = {}
     if planning:
         for mod in (ref_decomp, ref_portfolio):
             patched[(mod, "min_fill_tree_decomposition")] = wrap(min_fill)
             patched[(mod, "min_degree_tree_decomposition")] = wrap(min_degree)
+            patched[(mod, "validate_tree_decomposition")] = wrap(own_decomposition.validate_tree_decomposition)
+            patched[(mod, "width_tree")] = wrap(own_decomposition.width_tree)
         patched[(ref_decomp, "tree_to_branch")] = wrap(tree_to_branch)
         patched[(driver, "tree_to_branch")] = wrap(tree_to_branch)
+        patched[(driver, "time_cost")] = wrap(time_cost)
     if factoring:
         patched.update({
             (ref_factoring, "factor_branch_audit"): wrap(factor_branch_audit, to_ref_fbr),

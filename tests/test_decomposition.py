@@ -141,3 +141,44 @@ def test_live_c2_formula():
     f, w = parse_dimacs(config_dimacs("c2"))
     g = structure_graph(reduce_formula(f, w))
     _same_run(RD, g, 0, RD.min_fill_tree_decomposition, ND.min_fill_tree_decomposition)
+
+
+@needs_ref
+def test_validation_matches_reference():
+    import tensorcount.decomposition as RD
+    from tensorcount.errors import InvalidDecomposition as RefInvalid
+    from tensorcount.formula import parse_dimacs
+    from tensorcount.network import structure_graph
+    from tensorcount.reduction import reduce_formula
+
+    f, w = parse_dimacs("p cnf 4 4\n1 2 -3 0\n1 3 4 0\n-2 -3 0\n-3 -4 0\n")
+    g = structure_graph(reduce_formula(f, w))
+    td = RD.min_fill_tree_decomposition(g, 0)
+    ND.validate_tree_decomposition(td, g)
+    assert ND.width_tree(td, g) == RD.width_tree(td, g)
+    nodes = list(td.tree.nodes)
+    broken = [
+        RD.TreeDecomposition(td.tree, {u: b for u, b in td.bags.items() if u != nodes[0]}),  # unlabelled node
+        RD.TreeDecomposition(td.tree, {u: frozenset() for u in nodes}),  # vertices in no bag
+    ]
+    for u in nodes:  # drop one edge's host: remove a vertex from its bags one at a time
+        for v in td.bags[u]:
+            bags = dict(td.bags)
+            bags[u] = td.bags[u] - {v}
+            broken.append(RD.TreeDecomposition(td.tree, bags))
+    rejected = 0
+    for bad in broken:
+        try:
+            RD.validate_tree_decomposition(bad, g)
+        except RefInvalid as want:
+            rejected += 1
+            with pytest.raises(InvalidDecomposition) as got:
+                ND.validate_tree_decomposition(bad, g)
+            msg = str(want)
+            if "vertices {" in msg:  # the set's repr order is the caller's, compare the prefix
+                assert str(got.value).split("{")[0] == msg.split("{")[0]
+            else:
+                assert str(got.value) == msg
+        else:
+            ND.validate_tree_decomposition(bad, g)  # accepted by both
+    assert rejected >= 3
