@@ -461,7 +461,80 @@ done:
   return result;
 }
 
+// positions(indices, queries) -> list[int]: for each query Index, the position
+// of the first entry of `indices` that is the same object, else the first with
+// an equal .id (Index equality, tensor.py:29-33), else -1.  One pointer scan
+// of the (long) index table instead of a dict over all of it.
+static PyObject* positions(PyObject* self, PyObject* args) {
+  PyObject *indices_in, *queries_in;
+  if (!PyArg_ParseTuple(args, "OO", &indices_in, &queries_in)) return NULL;
+  PyObject* ind = PySequence_Fast(indices_in, "indices must be a sequence");
+  if (!ind) return NULL;
+  PyObject* qs = PySequence_Fast(queries_in, "queries must be a sequence");
+  if (!qs) {
+    Py_DECREF(ind);
+    return NULL;
+  }
+  const Py_ssize_t n = PySequence_Fast_GET_SIZE(ind), m = PySequence_Fast_GET_SIZE(qs);
+  PyObject** iv = PySequence_Fast_ITEMS(ind);
+  PyObject** qv = PySequence_Fast_ITEMS(qs);
+  PyObject* out = PyList_New(m);
+  Py_ssize_t* pos = (Py_ssize_t*)PyMem_Malloc((size_t)(m ? m : 1) * sizeof(Py_ssize_t));
+  PtrMap qm = {0};
+  if (!out || !pos || pm_init(&qm, (size_t)m) < 0) goto fail;
+  for (Py_ssize_t q = 0; q < m; ++q) pos[q] = -1;
+  for (Py_ssize_t q = m; q-- > 0;) pm_set(&qm, (uintptr_t)qv[q], q);  // first listed query wins per object
+  {
+    Py_ssize_t left = m;
+    for (Py_ssize_t k = 0; k < n && left; ++k) {
+      const int64_t q = pm_get(&qm, (uintptr_t)iv[k], -1);
+      if (q < 0) continue;
+      for (Py_ssize_t r = 0; r < m; ++r)  // every query holding this object
+        if (qv[r] == iv[k] && pos[r] < 0) pos[r] = k, --left;
+    }
+    // queries that are not the network's own objects: match by id
+    for (Py_ssize_t r = 0; r < m; ++r) {
+      if (pos[r] >= 0) continue;
+      PyObject* want = PyObject_GetAttr(qv[r], s_id);
+      if (!want) goto fail;
+      for (Py_ssize_t k = 0; k < n; ++k) {
+        PyObject* have = PyObject_GetAttr(iv[k], s_id);
+        if (!have) {
+          Py_DECREF(want);
+          goto fail;
+        }
+        const int eq = PyObject_RichCompareBool(have, want, Py_EQ);
+        Py_DECREF(have);
+        if (eq < 0) {
+          Py_DECREF(want);
+          goto fail;
+        }
+        if (eq) {
+          pos[r] = k;
+          break;
+        }
+      }
+      Py_DECREF(want);
+    }
+  }
+  for (Py_ssize_t q = 0; q < m; ++q) PyList_SET_ITEM(out, q, PyLong_FromSsize_t(pos[q]));
+  pm_free(&qm);
+  PyMem_Free(pos);
+  Py_DECREF(ind);
+  Py_DECREF(qs);
+  return out;
+fail:
+  pm_free(&qm);
+  PyMem_Free(pos);
+  Py_XDECREF(out);
+  Py_DECREF(ind);
+  Py_DECREF(qs);
+  if (!PyErr_Occurred()) PyErr_NoMemory();
+  return NULL;
+}
+
 static PyMethodDef methods[] = {
+    {"positions", positions, METH_VARARGS, "positions(indices, queries) -> first position of each query (identity, then id)"},
     {"flatten", flatten, METH_VARARGS, "flatten(tensors, tree) -> plan arrays (see paper_2006_15512_b200/flatten.py)"},
     {NULL, NULL, 0, NULL}};
 

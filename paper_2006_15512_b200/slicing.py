@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _lib
 from .errors import BudgetInfeasible, NoCandidates, PlanMismatch
-from .flatten import flatten
+from .flatten import _native, flatten
 
 BYTES_PER_ENTRY = 8
 
@@ -95,9 +95,14 @@ def _run(n, t, mem_budget=None, devices=None, slice_indices=None, slice_range=No
     if slice_indices is None:
         sl = None
     else:
-        # Index equality is by id (tensor.py:29-33): key on the raw ids (C hashing)
-        pos = {ix.id: k for k, ix in enumerate(flat.indices)}
-        sl = [pos.get(ix.id, -1) for ix in slice_indices]
+        # Index equality is by id (tensor.py:29-33); the callers' Index objects
+        # are usually the network's own, found by one pointer scan in C
+        nat = _native()
+        if nat is not None:
+            sl = nat.positions(flat.indices, list(slice_indices))
+        else:
+            pos = {ix.id: k for k, ix in enumerate(flat.indices)}
+            sl = [pos.get(ix.id, -1) for ix in slice_indices]
     if sl is not None and any(k < 0 for k in sl):
         from .errors import NotABondIndex
         raise NotABondIndex("slice index is not an index of the network")

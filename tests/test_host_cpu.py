@@ -330,3 +330,15 @@ def test_budget_semantics_match_reference_loop():
     assert ch == case["expected"]["budgeted"]["chosen"]
     with pytest.raises(BudgetInfeasible, match=r"cannot fit in -0.5 bytes even fully sliced \(needs \d+\)"):
         h._budget_slices(-0.5)
+
+
+def test_native_index_positions_identity_then_id():
+    from paper_2006_15512_b200.flatten import _native
+    from paper_2006_15512_b200.tensor import Index
+
+    nat = _native()
+    idx = [Index(("v", k), 2) for k in range(50)]
+    twin = Index(("v", 7), 2)  # equal by id, another object
+    got = nat.positions(idx, [idx[3], twin, Index("absent", 2), idx[3], idx[49]])
+    assert got == [3, 7, -1, 3, 49]
+    assert nat.positions([], [twin]) == [-1] and nat.positions(idx, []) == []
