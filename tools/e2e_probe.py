@@ -14,6 +14,7 @@ import numpy as np  # noqa: E402
 
 import bench  # noqa: E402
 from paper_2006_15512_b200 import _lib, planfile, sliced_execute, slicing  # noqa: E402
+from paper_2006_15512_b200.flatten import _native  # noqa: E402
 
 
 def main(name):
@@ -27,8 +28,7 @@ def main(name):
         T = [time.perf_counter()]
         flat, h = slicing._plan(n, t, with_sort_rank=False)
         T.append(time.perf_counter())
-        pos = {ix: k for k, ix in enumerate(flat.indices)}
-        ids = [pos[ix] for ix in sl] if sl else None
+        ids = _native().positions(flat.indices, sl) if sl else None  # as slicing._run
         T.append(time.perf_counter())
         root = h.result_indices(())
         T.append(time.perf_counter())
