@@ -23,6 +23,7 @@ from . import decomposition as own_decomposition
 from . import errors as own_errors
 from . import factoring as own_factoring
 from . import network as own_network
+from . import reduction as own_reduction
 from . import slicing as own_slicing
 from . import tensor as own_tensor
 
@@ -44,7 +45,8 @@ def install(tensorcount=None, devices=None, contract_pair=False, execution=True,
     (tensor.py:96-108) — the reference's own test suite imports it directly.
     ``factoring`` swaps in the native FactorTree step (``factoring.py``:
     ``factor_branch_audit`` / ``factor_branch``, also as bound by
-    ``driver.py:22`` and ``__init__.py:5``); ``planning`` the native
+    ``driver.py:22`` and ``__init__.py:5``) and the linear-time
+    ``reduce_formula`` (``reduction.py``, also ``driver.py:24``, ``__init__.py:9``); ``planning`` the native
     min-fill / min-degree decompositions and ``tree_to_branch``
     (``decomposition.py``, also as bound by ``portfolio.py:18-31`` and
     ``driver.py:20``, fresh names from the reference's own counter);
@@ -56,6 +58,7 @@ def install(tensorcount=None, devices=None, contract_pair=False, execution=True,
     ref_factoring = importlib.import_module(tensorcount.__name__ + ".factoring")
     ref_decomp = importlib.import_module(tensorcount.__name__ + ".decomposition")
     ref_portfolio = importlib.import_module(tensorcount.__name__ + ".portfolio")
+    ref_reduction = importlib.import_module(tensorcount.__name__ + ".reduction")
     slicing = importlib.import_module(tensorcount.__name__ + ".slicing")
     network = importlib.import_module(tensorcount.__name__ + ".network")
     tensor = importlib.import_module(tensorcount.__name__ + ".tensor")
@@ -112,7 +115,13 @@ def install(tensorcount=None, devices=None, contract_pair=False, execution=True,
         _, h = own_slicing._plan(n, t, with_sort_rank=False)
         return h.info().contraction_ops.value() / throughput
 
+    def reduce_formula(formula, weights):
+        return own_reduction.reduce_formula(formula, weights, tensor.Index, tensor.Tensor, network.TensorNetwork)
+
     patched = {}
+    if factoring:  # the FactorTree step's input: the reduction
+        for mod in (ref_reduction, driver, tensorcount):
+            patched[(mod, "reduce_formula")] = wrap(reduce_formula)
     if planning:
         for mod in (ref_decomp, ref_portfolio):
             patched[(mod, "min_fill_tree_decomposition")] = wrap(min_fill)

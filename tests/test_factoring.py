@@ -207,3 +207,29 @@ def test_reference_suite_with_native_host_steps():
                         "--rootdir", suite, suite], cwd=suite, env=env, capture_output=True, text=True, timeout=1800)
     m = re.search(r"(\d+) passed", p.stdout)
     assert p.returncode == 0 and m and int(m.group(1)) == 208, p.stdout[-3000:] + p.stderr[-2000:]
+
+
+@needs_ref
+def test_reduction_matches_reference():
+    """reduction.py: the same network as the reference's reduce_formula
+    (reduction.py:80-101), object for object: index ids and order, values."""
+    from tensorcount import tensor as RT
+    from tensorcount.formula import CnfFormula, WeightFunction, parse_dimacs
+    from tensorcount.network import TensorNetwork as RN
+    from tensorcount.reduction import reduce_formula as ref_reduce
+
+    from paper_2006_15512_b200.generators import config_dimacs
+    from paper_2006_15512_b200.reduction import reduce_formula
+
+    rng = random.Random(3)
+    texts = [config_dimacs("c1a"), "p cnf 3 0\n", "p cnf 2 1\n0\n", "p cnf 0 0\n"]
+    texts += [rand_dimacs(rng, rng.randint(1, 12), rng.randint(0, 30), rng.randint(1, 4)) for _ in range(60)]
+    forms = [parse_dimacs(t) for t in texts]
+    forms.append((CnfFormula(3, ((1, -2), (3,), ())), WeightFunction({1: (0.25, 0.75)})))
+    for f, w in forms:
+        want = ref_reduce(f, w)
+        got = reduce_formula(f, w, RT.Index, RT.Tensor, RN)
+        assert len(got.tensors) == len(want.tensors)
+        for a, b in zip(got.tensors, want.tensors):
+            assert [ix.id for ix in a.indices] == [ix.id for ix in b.indices]
+            assert a.values.shape == b.values.shape and np.array_equal(a.values, b.values)
