@@ -11,7 +11,9 @@ Default workload: C4 (BASELINE configs[3]: "random 3-CNF n=400, ratio 4.0,
 width ~36 sliced into 2^8 slices across 1/2/4/8 B200") = banded_3cnf(400,
 4.0, 36, seed 11) (the first SAT seed), slice set = Algorithm 3's greedy
 8-pick prefix (slicing.py:70-79) -> 2^8 slices.  The line also carries C2
-(configs[1], unsliced, 1 B200) device and end-to-end numbers under "c2".
+(configs[1], unsliced, 1 B200) device and end-to-end numbers under "c2", and the whole
+count of C2 from DIMACS text (native planning + FactorTree + GPU execution) under
+"c2" -> "pipeline".
 
 N > 1: one process per GPU (torchrun; ``python bench.py --gpus N`` launches
 it itself).  Sliced configs block-partition the lexicographic slice ids over
@@ -733,6 +735,7 @@ def run_ours(args):
     c2 = None
     if args.config == DEFAULT and not args.no_c2 and world == 1:
         c2 = c2_numbers(args, local)
+        c2["pipeline"] = pipeline_numbers(local)
 
     line = dict(
         metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
@@ -798,6 +801,41 @@ def c2_numbers(args, local):
                          path="sliced_execute(n, t) public API (host objects, H2D, D2H)"),
                 count=float(folded[0]), rel_err_vs_reference=abs(float(folded[0]) - gold) / gold,
                 gpu_launches=st["gpu_launches"])
+
+
+def pipeline_numbers(local, config="c2"):
+    """The whole count of one formula from DIMACS text through the reference's
+    own driver (``tensorcount.count_text``, driver.py:254-256, alpha=0) with
+    ``reference_patch.install``: the reduction, min-fill planning,
+    tree_to_branch and FactorTree native (identical plan), execution on the GPU
+    (the unmodified pipeline: profiles/r2_pipeline.jsonl)."""
+    try:
+        _reference_path()
+        import tensorcount
+        from tensorcount.network import serialize_plan  # noqa: F401  (reference installed)
+    except Exception as ex_:
+        return dict(unavailable=str(ex_))
+    from paper_2006_15512_b200 import reference_patch
+    from paper_2006_15512_b200.generators import config_dimacs
+
+    text = config_dimacs(config)
+    reference_patch.install(tensorcount, devices=[local])
+    try:
+        times, res = [], None
+        for _ in range(3):
+            t0 = time.perf_counter()
+            res = tensorcount.count_text(text, alpha=0.0)
+            times.append(time.perf_counter() - t0)
+    finally:
+        reference_patch.uninstall()
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "counts.json")))[config]["count"]
+    return dict(config=config, seconds=min(times), count=res.count,
+                rel_err_vs_reference=abs(res.count - gold) / abs(gold) if gold else None,
+                width=res.width, max_rank=res.max_rank, num_plans=res.num_plans,
+                path="tensorcount.count_text(text, alpha=0) + reference_patch.install: reduce / plan / "
+                     "FactorTree native (C++), execution on the GPU",
+                reference_seconds_box=20.8, reference_source="profiles/r2_pipeline.jsonl (unmodified "
+                                                             "tensorcount: reduce 0.06 + plan 3.24 + execute 17.46 s)")
 
 
 def free_port():
