@@ -74,6 +74,7 @@ struct Alloc {
   std::map<int64_t, int64_t> free_[2];                   // off -> size
   std::map<int64_t, std::pair<int64_t, int>> seg[2];     // off -> (end, last reader step)
   int64_t top = 0;
+  int64_t hi[2] = {0, 0};  // highest end of any allocation per memory class
 
   bool no_reuse = false;  // every buffer gets fresh memory: no WAR edges at all
   // pinned region [0, pin_end): buffers that are never released (hoisting
@@ -97,6 +98,7 @@ struct Alloc {
     if (no_reuse) {
       int64_t o = top;
       top += size;
+      hi[cl] = std::max(hi[cl], top);
       return o;
     }
     auto& fr = free_[cl];
@@ -143,6 +145,7 @@ struct Alloc {
       if (s1 > end) sg[end] = {s1, rd};
       it = sg.lower_bound(std::min(s1, end));
     }
+    hi[cl] = std::max(hi[cl], end);
     return off;
   }
 
@@ -2336,6 +2339,13 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   g.steps.push_back(et);
   tmark("end");
   g.arena_bytes = std::max<int64_t>(arena.top, kAlign);
+  // a slice lane's arena copy: the per-slice memory class above the pinned
+  // prefix (hoisted tensors outside the pinned region are lane 0's only)
+  g.lane_arena_bytes = hoist ? std::max<int64_t>(arena.hi[0] - arena.pin_end, kAlign) : g.arena_bytes - arena.pin_end;
+  g.lane_arena_bytes = std::max<int64_t>(g.lane_arena_bytes, kAlign);
+  if (timing)
+    std::fprintf(stderr, "[compile] arena %.3f GB (pinned %.3f GB), lane copy %.3f GB\n", g.arena_bytes / 1e9,
+                 arena.pin_end / 1e9, g.lane_arena_bytes / 1e9);
   for (auto& s : g.steps) {
     std::sort(s.deps.begin(), s.deps.end());
     s.deps.erase(std::unique(s.deps.begin(), s.deps.end()), s.deps.end());

@@ -70,6 +70,7 @@ struct Program {
   int n_tied_leaves = 0;
   // arena
   int64_t arena_bytes = 0;
+  int64_t lane_arena_bytes = 0;  // per-lane copy: offsets [pinned_bytes, pinned_bytes + lane_arena_bytes)
   Loc root_loc{};
   std::vector<Step> steps;
   // stats

@@ -322,7 +322,9 @@ struct tc_exec {
     switch (l.kind) {
       case LOC_LEAF: return leafbuf + l.off;
       case LOC_SLICED: return (k ? xl[k - 1].sliced : slicedbuf) + l.off;
-      case LOC_ARENA: return (const double*)((k && l.off >= prog.pinned_bytes ? xl[k - 1].arena : arena) + l.off);
+      case LOC_ARENA:  // a lane's copy holds the per-slice class above the pinned prefix
+        return (const double*)(k && l.off >= prog.pinned_bytes ? xl[k - 1].arena + (l.off - prog.pinned_bytes)
+                                                                : arena + l.off);
       default: return nullptr;
     }
   }
@@ -868,7 +870,7 @@ struct tc_exec {
       const int k = (int)xl.size();
       Lane& L = xl.back();
       int64_t dummy = 0;
-      L.arena = dalloc<char>((size_t)g.arena_bytes, dev_bytes, device);
+      L.arena = dalloc<char>((size_t)g.lane_arena_bytes, dev_bytes, device);
       if (g.sliced_doubles) L.sliced = dalloc<double>((size_t)g.sliced_doubles, dev_bytes, device);
       L.eta = dalloc<int64_t>(4, dummy, device);
       CU(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
@@ -909,7 +911,7 @@ struct tc_exec {
     if (K <= (int)xl.size() + 1) return std::max(1, K);
     size_t fr = 0, tot = 0;
     CU(cudaMemGetInfo(&fr, &tot));
-    const double per = (double)prog.arena_bytes + 8.0 * prog.sliced_doubles + 1e6;
+    const double per = (double)prog.lane_arena_bytes + 8.0 * prog.sliced_doubles + 1e6;
     while (K > (int)xl.size() + 1 && per * (K - 1 - (int)xl.size()) > 0.25 * (double)fr) --K;
     return std::max(1, K);
   }

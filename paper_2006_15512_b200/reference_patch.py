@@ -115,6 +115,16 @@ def install(tensorcount=None, devices=None, contract_pair=False, execution=True,
         _, h = own_slicing._plan(n, t, with_sort_rank=False)
         return h.info().contraction_ops.value() / throughput
 
+    def max_rank(n, t):  # network.py:178-181
+        _, h = own_slicing._plan(n, t, with_sort_rank=False)
+        return int(h.info().max_rank)
+
+    def serialize_plan(n, t):  # network.py:235-251: flatten numbers slots exactly like it
+        flat, _ = own_slicing._plan(n, t, with_sort_rank=False)
+        nl = flat.num_leaves
+        lines = [f"contract {a} {b} -> {nl + k}" for k, (a, b) in enumerate(zip(flat.left.tolist(), flat.right.tolist()))]
+        return "\n".join(lines) + ("\n" if lines else "")
+
     def reduce_formula(formula, weights):
         return own_reduction.reduce_formula(formula, weights, tensor.Index, tensor.Tensor, network.TensorNetwork)
 
@@ -131,6 +141,9 @@ def install(tensorcount=None, devices=None, contract_pair=False, execution=True,
         patched[(ref_decomp, "tree_to_branch")] = wrap(tree_to_branch)
         patched[(driver, "tree_to_branch")] = wrap(tree_to_branch)
         patched[(driver, "time_cost")] = wrap(time_cost)
+        for mod in (network, driver):  # count_formula's CountResult fields (driver.py:238-251)
+            patched[(mod, "max_rank")] = wrap(max_rank)
+            patched[(mod, "serialize_plan")] = wrap(serialize_plan)
     if factoring:
         patched.update({
             (ref_factoring, "factor_branch_audit"): wrap(factor_branch_audit, to_ref_fbr),

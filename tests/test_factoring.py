@@ -233,3 +233,31 @@ def test_reduction_matches_reference():
         for a, b in zip(got.tensors, want.tensors):
             assert [ix.id for ix in a.indices] == [ix.id for ix in b.indices]
             assert a.values.shape == b.values.shape and np.array_equal(a.values, b.values)
+
+
+@needs_ref
+def test_patched_plan_metadata_matches_reference():
+    """max_rank / serialize_plan / time_cost of the patched driver (native plan)
+    equal the reference's on C2's plan (network.py:178-201, 235-258)."""
+    import subprocess as sp
+
+    code = (
+        "import sys; sys.path[:0] = [%r, %r]\n"
+        "import tensorcount\n"
+        "from tensorcount.driver import plan_contraction\n"
+        "from tensorcount.formula import parse_dimacs\n"
+        "from tensorcount import network as RN\n"
+        "from tensorcount import driver as RD\n"
+        "from tensorcount.reduction import reduce_formula\n"
+        "from paper_2006_15512_b200 import reference_patch\n"
+        "from paper_2006_15512_b200.generators import config_dimacs\n"
+        "f, w = parse_dimacs(config_dimacs('c2')); n = reduce_formula(f, w)\n"
+        "best, _, _ = plan_contraction(n, planner_spec='minfill', alpha=0.0, seed=0)\n"
+        "m, t = best.network, best.tree\n"
+        "a = (RN.max_rank(m, t), RN.serialize_plan(m, t), RD.time_cost(m, t))\n"
+        "reference_patch.install(tensorcount, execution=False)\n"
+        "b = (RN.max_rank(m, t), RN.serialize_plan(m, t), RD.time_cost(m, t))\n"
+        "assert a == b, (a[0], b[0], a[2], b[2])\n"
+        "print('same')\n") % (ROOT, [p for p in sys.path if p.endswith("_ref") or p.endswith("pkg/src")][0])
+    out = sp.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "same" in out.stdout, out.stdout + out.stderr
