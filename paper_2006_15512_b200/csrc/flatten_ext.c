@@ -20,6 +20,7 @@
 // leaves in network order, then internal nodes in left-first postorder.
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
+#include <structmember.h>
 #define NPY_NO_DEPRECATED_API NPY_1_7_API_VERSION
 #include <numpy/arrayobject.h>
 #include <stdint.h>
@@ -49,29 +50,30 @@ static int buf_put(Buf* b, const void* src, size_t len) {
 
 static PyObject* buf_bytes(Buf* b) { return PyBytes_FromStringAndSize(b->p ? b->p : "", (Py_ssize_t)b->n); }
 
-// pointer -> int open-addressing map (leaf tensor object -> slot, tree node -> slot)
+// pointer -> int open-addressing map (leaf tensor object -> slot, tree node ->
+// slot, Index object -> dense id); key and value share a 16-byte entry, so a
+// probe touches one cache line
 typedef struct {
-  uintptr_t* key;
-  int64_t* val;
+  uintptr_t key;
+  int64_t val;
+} PmEnt;
+typedef struct {
+  PmEnt* e;
   size_t mask;
 } PtrMap;
 
 static int pm_init(PtrMap* m, size_t n) {
   size_t c = 16;
   while (c < 2 * n + 2) c <<= 1;
-  m->key = (uintptr_t*)PyMem_Calloc(c, sizeof(uintptr_t));
-  m->val = (int64_t*)PyMem_Malloc(c * sizeof(int64_t));
+  m->e = (PmEnt*)PyMem_Calloc(c, sizeof(PmEnt));
   m->mask = c - 1;
-  if (!m->key || !m->val) {
+  if (!m->e) {
     PyErr_NoMemory();
     return -1;
   }
   return 0;
 }
-static void pm_free(PtrMap* m) {
-  PyMem_Free(m->key);
-  PyMem_Free(m->val);
-}
+static void pm_free(PtrMap* m) { PyMem_Free(m->e); }
 // full-avalanche mix (murmur3 finalizer): the map masks the LOW bits, and object
 // addresses share their low bits (fixed allocation strides), so a plain
 // multiplicative hash clusters them into long linear-probe runs
@@ -86,20 +88,55 @@ static inline size_t pm_hash(uintptr_t k) {
 }
 static void pm_set(PtrMap* m, uintptr_t k, int64_t v) {
   size_t h = pm_hash(k) & m->mask;
-  while (m->key[h] && m->key[h] != k) h = (h + 1) & m->mask;
-  m->key[h] = k;
-  m->val[h] = v;
+  while (m->e[h].key && m->e[h].key != k) h = (h + 1) & m->mask;
+  m->e[h].key = k;
+  m->e[h].val = v;
 }
 static int64_t pm_get(const PtrMap* m, uintptr_t k, int64_t dflt) {
   size_t h = pm_hash(k) & m->mask;
-  while (m->key[h]) {
-    if (m->key[h] == k) return m->val[h];
+  while (m->e[h].key) {
+    if (m->e[h].key == k) return m->e[h].val;
     h = (h + 1) & m->mask;
   }
   return dflt;
 }
 
 static PyObject *s_indices, *s_values, *s_id, *s_domain_size, *s_tensor, *s_left, *s_right;
+
+// Attribute reads of __slots__ classes (this package's Tensor / Index /
+// ContractionTree): the member descriptor's offset is looked up once per
+// (type, name) and the slot read directly, the same value PyObject_GetAttr
+// returns for a type with generic attribute access (a member descriptor is a
+// data descriptor: it wins over any instance dict).  Other classes (the
+// reference's dict-based dataclasses) take PyObject_GetAttr.
+typedef struct {
+  PyTypeObject* type;
+  Py_ssize_t off;  // -1: not a plain object slot
+} SlotCache;
+
+static Py_ssize_t slot_offset(PyTypeObject* tp, PyObject* name) {
+  if (tp->tp_getattro != PyObject_GenericGetAttr) return -1;
+  PyObject* d = _PyType_Lookup(tp, name);  // borrowed
+  if (!d || !Py_IS_TYPE(d, &PyMemberDescr_Type)) return -1;
+  PyMemberDef* m = ((PyMemberDescrObject*)d)->d_member;
+  return (m->type == Py_T_OBJECT_EX && !(m->flags & Py_AUDIT_READ)) ? m->offset : -1;
+}
+
+static inline PyObject* get_attr(PyObject* o, PyObject* name, SlotCache* c) {  // new reference
+  PyTypeObject* tp = Py_TYPE(o);
+  if (tp != c->type) {
+    c->type = tp;
+    c->off = slot_offset(tp, name);
+  }
+  if (c->off >= 0) {
+    PyObject* v = *(PyObject**)((char*)o + c->off);
+    if (v) {
+      Py_INCREF(v);
+      return v;
+    }
+  }
+  return PyObject_GetAttr(o, name);  // unset slot: the AttributeError as usual
+}
 
 // append the row-major float64 contents of `values` to vals; returns entries or -1
 static Py_ssize_t put_values(Buf* vals, PyObject* values) {
@@ -177,6 +214,7 @@ static PyObject* flatten(PyObject* self, PyObject* args) {
   if (!PyArg_ParseTuple(args, "OO|p", &tensors_in, &tree, &ptr_mode)) return NULL;
   PyObject* keep = ptr_mode ? PyList_New(0) : NULL;
   if (ptr_mode && !keep) return NULL;
+  SlotCache c_indices = {0}, c_values = {0}, c_domain = {0}, c_id = {0}, c_tensor = {0}, c_left = {0}, c_right = {0};
   PyObject* tensors = PySequence_Fast(tensors_in, "n.tensors must be a sequence");
   if (!tensors) return NULL;
   const Py_ssize_t nl = PySequence_Fast_GET_SIZE(tensors);
@@ -198,7 +236,7 @@ static PyObject* flatten(PyObject* self, PyObject* args) {
   for (Py_ssize_t k = 0; k < nl; ++k) {
     PyObject* ten = tv[k];
     pm_set(&leaf, (uintptr_t)ten, k);
-    PyObject* inds = PyObject_GetAttr(ten, s_indices);
+    PyObject* inds = get_attr(ten, s_indices, &c_indices);
     if (!inds) goto done;
     PyObject* fi = PySequence_Fast(inds, "tensor.indices must be a sequence");
     Py_DECREF(inds);
@@ -216,7 +254,7 @@ static PyObject* flatten(PyObject* self, PyObject* args) {
         occ[di]++;
       } else {
         di = (int32_t)PyList_GET_SIZE(indices);
-        PyObject* ds = PyObject_GetAttr(ix, s_domain_size);
+        PyObject* ds = get_attr(ix, s_domain_size, &c_domain);
         long dsz = ds ? PyLong_AsLong(ds) : -1;
         Py_XDECREF(ds);
         int32_t dsz32 = (int32_t)dsz;
@@ -232,7 +270,7 @@ static PyObject* flatten(PyObject* self, PyObject* args) {
             goto done;
           }
           for (size_t h = 0; h <= ixp.mask; ++h)
-            if (ixp.key[h]) pm_set(&bigger, ixp.key[h], ixp.val[h]);
+            if (ixp.e[h].key) pm_set(&bigger, ixp.e[h].key, ixp.e[h].val);
           pm_free(&ixp);
           ixp = bigger;
           pm_cap *= 2;
@@ -259,7 +297,7 @@ static PyObject* flatten(PyObject* self, PyObject* args) {
     Py_DECREF(fi);
     off += r;
     if (buf_put(&ioff, &off, 8) < 0) goto done;
-    PyObject* values = PyObject_GetAttr(ten, s_values);
+    PyObject* values = get_attr(ten, s_values, &c_values);
     if (!values) goto done;
     Py_ssize_t nv = ptr_mode ? put_pointer(&vals, keep, values) : put_values(&vals, values);
     Py_DECREF(values);
@@ -283,7 +321,7 @@ static PyObject* flatten(PyObject* self, PyObject* args) {
     for (Py_ssize_t u = 0; u < nu; ++u) {
       remap[u] = (int32_t)u;
       if (occ[u] != 1) continue;
-      PyObject* key = PyObject_GetAttr(PyList_GET_ITEM(indices, u), s_id);
+      PyObject* key = get_attr(PyList_GET_ITEM(indices, u), s_id, &c_id);
       if (!key) {
         PyMem_Free(remap);
         goto done;
@@ -389,7 +427,7 @@ static PyObject* flatten(PyObject* self, PyObject* args) {
       e->parent = pd.parent;
       e->side = pd.side;
       e->kid[0] = e->kid[1] = -1;
-      PyObject* t = PyObject_GetAttr(pd.node, s_tensor);
+      PyObject* t = get_attr(pd.node, s_tensor, &c_tensor);
       if (!t) goto tree_fail;
       if (t != Py_None) {
         e->leaf = pm_get(&leaf, (uintptr_t)t, -1);
@@ -407,10 +445,10 @@ static PyObject* flatten(PyObject* self, PyObject* args) {
         }
         stk = q;
       }
-      PyObject* l = PyObject_GetAttr(pd.node, s_left);
+      PyObject* l = get_attr(pd.node, s_left, &c_left);
       if (!l) goto tree_fail;
       stk[sp++] = (Pend){l, (int64_t)(ns - 1), 0};
-      PyObject* r = PyObject_GetAttr(pd.node, s_right);
+      PyObject* r = get_attr(pd.node, s_right, &c_right);
       if (!r) goto tree_fail;
       stk[sp++] = (Pend){r, (int64_t)(ns - 1), 1};
     }
