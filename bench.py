@@ -463,9 +463,17 @@ def reference_baseline(config, flat, chosen, steps, budget_s):
     ns = num_slices(flat, chosen)
     if config in REF_FULL:
         sec, count, times = time_reference_full(flat, steps)
-        return 1.0 / sec, dict(kind="reference", cores=host_cores(), seconds_per_slice=sec, count=count,
-                               step_seconds=times,
-                               sample="the full unmodified sliced_execute (slicing.py:112-146) per step")
+        out = dict(kind="reference", cores=host_cores(), seconds_per_slice=sec, count=count,
+                   step_seconds=times, sample="the full unmodified sliced_execute (slicing.py:112-146) per step")
+        try:  # also one BLAS thread
+            from threadpoolctl import threadpool_limits
+
+            with threadpool_limits(limits=1):
+                sec1, _, _ = time_reference_full(flat, 1)
+            out["one_thread"] = dict(cores=1, seconds_per_slice=sec1, value=1.0 / sec1)
+        except Exception as ex_:
+            out["one_thread"] = dict(unavailable=str(ex_))
+        return 1.0 / sec, out
     runs = [reference_sample_model(flat, chosen, budget_s=budget_s, seed=s) for s in range(steps)]
     sec = statistics.median(r["seconds_per_slice"] for r in runs)
     r0 = runs[0]
