@@ -73,8 +73,16 @@ constexpr int64_t kLateReleaseMax = (int64_t)1 << 30;  // late release (chain-li
 struct Alloc {
   std::map<int64_t, int64_t> free_[2];                   // off -> size
   std::map<int64_t, std::pair<int64_t, int>> seg[2];     // off -> (end, last reader step)
-  int64_t top = 0;
-  int64_t hi[2] = {0, 0};  // highest end of any allocation per memory class
+  // Each memory class has its own region: class 1 (slice-invariant, the
+  // prologue's) starts above the pinned prefix; class 0 (per slice) is
+  // allocated in a tagged address space (offsets >= kTag) and relocated above
+  // class 1's region at the end of the compile (relocate()), so a slice
+  // lane's private copy holds only the per-slice region.  Without hoisting
+  // there is one class and no tag.
+  static constexpr int64_t kTag = (int64_t)1 << 56;
+  bool split = false;
+  int64_t top_[2] = {0, 0};  // per-class high-water mark (absolute, tagged for class 0 when split)
+  int64_t hi[2] = {0, 0};    // highest end of any allocation per memory class
 
   bool no_reuse = false;  // every buffer gets fresh memory: no WAR edges at all
   // pinned region [0, pin_end): buffers that are never released (hoisting
@@ -83,7 +91,11 @@ struct Alloc {
 
   void reserve_pinned(int64_t bytes) {
     pin_end = bytes;
-    top = std::max(top, bytes);
+    for (int c = 0; c < 2; ++c) top_[c] = std::max(top_[c], bytes);
+  }
+  void split_classes() {  // after reserve_pinned, before any alloc
+    split = true;
+    top_[0] = kTag;
   }
   int64_t alloc_pinned(int64_t size) {
     size = (size + kAlign - 1) / kAlign * kAlign;
@@ -92,9 +104,21 @@ struct Alloc {
     if (pin_top > pin_end) fail(TC_BAD_ARG, "pinned arena region overflow");
     return o;
   }
+  // final layout: [pinned | class 1 | class 0]; returns the class-0 base
+  int64_t region0_base() const {
+    if (!split) return pin_end;
+    return (top_[1] + kAlign - 1) / kAlign * kAlign;
+  }
+  int64_t arena_end() const {
+    if (!split) return std::max(top_[0], top_[1]);
+    return region0_base() + (top_[0] - kTag);
+  }
+  int64_t relocate(int64_t off) const { return split && off >= kTag ? off - kTag + region0_base() : off; }
 
   int64_t alloc(int64_t size, std::vector<int>& hazards, int cl = 0) {
     size = (size + kAlign - 1) / kAlign * kAlign;
+    const int r = split ? cl : 0;  // the region (top) this class allocates from
+    int64_t& top = top_[r];
     if (no_reuse) {
       int64_t o = top;
       top += size;
@@ -150,7 +174,7 @@ struct Alloc {
   }
 
   void release(int64_t off, int64_t size, int reader, int cl = 0) {
-    if (no_reuse || off < pin_end) return;
+    if (no_reuse || off < pin_end) return;  // (class-0 offsets are tagged, never below pin_end)
     size = (size + kAlign - 1) / kAlign * kAlign;
     seg[cl][off] = {off + size, reader};
     auto& fr = free_[cl];
@@ -1484,6 +1508,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       if (boundary[v] && (g.cls[v] != NC_TINY || groot[v])) pin += (bytes[v] + kAlign - 1) / kAlign * kAlign;
     }
     arena.reserve_pinned(pin);
+    arena.split_classes();
     g.pinned_bytes = pin;
   }
   // tiny roots: arena outputs allocated up front
@@ -2338,11 +2363,20 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   if (sel_step >= 0) et.deps.push_back(sel_step);
   g.steps.push_back(et);
   tmark("end");
-  g.arena_bytes = std::max<int64_t>(arena.top, kAlign);
-  // a slice lane's arena copy: the per-slice memory class above the pinned
-  // prefix (hoisted tensors outside the pinned region are lane 0's only)
-  g.lane_arena_bytes = hoist ? std::max<int64_t>(arena.hi[0] - arena.pin_end, kAlign) : g.arena_bytes - arena.pin_end;
-  g.lane_arena_bytes = std::max<int64_t>(g.lane_arena_bytes, kAlign);
+  // final arena layout [pinned | slice-invariant | per-slice]: relocate the
+  // per-slice class's tagged offsets; a slice lane's private copy holds the
+  // per-slice region only (the prologue's tensors are lane 0's)
+  auto reloc = [&](Loc& l) {
+    if (l.kind == LOC_ARENA) l.off = arena.relocate(l.off);
+  };
+  for (auto& l : g.loc) reloc(l);
+  for (auto& st : g.steps) reloc(st.la), reloc(st.lb), reloc(st.lc), reloc(st.lws);
+  for (auto* v : {&g.tiny_ga, &g.tiny_gb, &g.tiny_gout})
+    for (auto& l : *v) reloc(l);
+  reloc(g.root_loc);
+  g.lane_base = arena.region0_base();
+  g.arena_bytes = std::max<int64_t>(arena.arena_end(), kAlign);
+  g.lane_arena_bytes = std::max<int64_t>(g.arena_bytes - g.lane_base, kAlign);
   if (timing)
     std::fprintf(stderr, "[compile] arena %.3f GB (pinned %.3f GB), lane copy %.3f GB\n", g.arena_bytes / 1e9,
                  arena.pin_end / 1e9, g.lane_arena_bytes / 1e9);

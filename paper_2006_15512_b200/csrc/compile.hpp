@@ -70,7 +70,8 @@ struct Program {
   int n_tied_leaves = 0;
   // arena
   int64_t arena_bytes = 0;
-  int64_t lane_arena_bytes = 0;  // per-lane copy: offsets [pinned_bytes, pinned_bytes + lane_arena_bytes)
+  int64_t lane_base = 0;          // start of the per-slice region ([pinned | invariant | per-slice])
+  int64_t lane_arena_bytes = 0;   // a slice lane's private copy: offsets [lane_base, lane_base + lane_arena_bytes)
   Loc root_loc{};
   std::vector<Step> steps;
   // stats

@@ -322,9 +322,9 @@ struct tc_exec {
     switch (l.kind) {
       case LOC_LEAF: return leafbuf + l.off;
       case LOC_SLICED: return (k ? xl[k - 1].sliced : slicedbuf) + l.off;
-      case LOC_ARENA:  // a lane's copy holds the per-slice class above the pinned prefix
-        return (const double*)(k && l.off >= prog.pinned_bytes ? xl[k - 1].arena + (l.off - prog.pinned_bytes)
-                                                                : arena + l.off);
+      case LOC_ARENA:  // a lane's copy holds the per-slice region (compile.cpp: [pinned | invariant | per-slice])
+        return (const double*)(k && l.off >= prog.lane_base ? xl[k - 1].arena + (l.off - prog.lane_base)
+                                                            : arena + l.off);
       default: return nullptr;
     }
   }
