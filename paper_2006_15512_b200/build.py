@@ -74,14 +74,42 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
     if not force and not _stale(lib_out, deps):
         return lib_out
     os.makedirs(os.path.dirname(lib_out), exist_ok=True)
-    cmd = [
-        nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-shared", *os.environ.get("TC_NVCC_DEFS", "").split(),
-        "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-O3",
-        "--expt-relaxed-constexpr",
-        "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-        *[os.path.join(CSRC, f) for f in SOURCES],
-        "-o", lib_out + ".tmp", "-lpthread", "-ldl",
-    ]
+    # one object per source (compiled in parallel, each rebuilt only when it or a
+    # header changed), then one link: editing a host .cpp does not recompile the
+    # kernels in runtime.cu
+    objdir = os.path.join(os.path.dirname(lib_out), "obj" + ("" if out is None else "_" + os.path.basename(out)))
+    os.makedirs(objdir, exist_ok=True)
+    defs = os.environ.get("TC_NVCC_DEFS", "").split()
+    common = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", *defs, "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-O3",
+              "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    hdr = [d for d in deps if not d.endswith(tuple(SOURCES))]
+    jobs = []
+    objs = []
+    for f in SOURCES:
+        src = os.path.join(CSRC, f)
+        obj = os.path.join(objdir, f + ".o")
+        stamp = obj + ".flags"
+        flags = " ".join(common)
+        objs.append(obj)
+        old = open(stamp).read() if os.path.exists(stamp) else None
+        if force or old != flags or _stale(obj, [src, *hdr]):
+            jobs.append(([*common, "-c", src, "-o", obj + ".tmp"], obj, stamp, flags))
+
+    def run(job):
+        cmd, obj, stamp, flags = job
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        os.replace(obj + ".tmp", obj)
+        with open(stamp, "w") as fh:
+            fh.write(flags)
+
+    if jobs:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(len(jobs)) as ex:
+            list(ex.map(run, jobs))
+    cmd = [nvcc(), *ARCH, "-shared", *objs, "-o", lib_out + ".tmp", "-lpthread", "-ldl"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

@@ -790,6 +790,8 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       for (int w = 1; w < T; ++w) th.emplace_back(work, w);
       work(0);
       for (auto& x : th) x.join();
+      if (timing) std::fprintf(stderr, "[compile]   pass: %d threads, %zu task roots, %lld task nodes of %d\n", T, task_roots.size(), (long long)task_nodes, p.NN);
+      tmark("phys: spine");
       for (int w = 0; w < T; ++w) overflow |= (bool)wover[w];
       size_t nm = 0, nc = 0;
       for (int k = 0; k < p.NN; ++k)
