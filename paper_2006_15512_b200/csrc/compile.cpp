@@ -1816,24 +1816,57 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     while ((int)cut.size() <= T) cut.push_back((int)gorder.size());
     std::vector<TinyOut> outs(T);
     std::vector<std::thread> th;
-    for (int w = 1; w < T; ++w) th.emplace_back(build_groups, cut[w], cut[w + 1], std::ref(outs[w]));
-    build_groups(cut[0], cut[1], outs[0]);
+    std::vector<double> wms(T, 0.0);
+    auto timed = [&](int w) {
+      const auto t0 = std::chrono::steady_clock::now();
+      build_groups(cut[w], cut[w + 1], outs[w]);
+      wms[w] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    };
+    for (int w = 1; w < T; ++w) th.emplace_back(timed, w);
+    timed(0);
     for (auto& x : th) x.join();
-    for (auto& o : outs) {
-      const int32_t nb = (int32_t)g.tiny_nodes.size(), db = (int32_t)g.tiny_digits.size();
-      for (auto& tn : o.nodes) {
-        tn.dig += db;
-        g.tiny_nodes.push_back(tn);
-      }
-      g.tiny_digits.insert(g.tiny_digits.end(), o.digs.begin(), o.digs.end());
-      g.tiny_ga.insert(g.tiny_ga.end(), o.ga.begin(), o.ga.end());
-      g.tiny_gb.insert(g.tiny_gb.end(), o.gb.begin(), o.gb.end());
-      g.tiny_gout.insert(g.tiny_gout.end(), o.go.begin(), o.go.end());
-      for (auto tg : o.grp) g.tiny_groups.push_back(TinyGroup{tg.beg + nb, tg.end + nb});
-      g.tiny_stage_doubles = std::max(g.tiny_stage_doubles, o.stage);
-      g.tiny_dig_max = std::max(g.tiny_dig_max, o.digmax);
+    if (timing) {
+      std::fprintf(stderr, "[compile]   tiny workers:");
+      for (int w = 0; w < T; ++w) std::fprintf(stderr, " %.2f", wms[w]);
+      std::fprintf(stderr, " ms\n");
+      tmark("tiny: merge");
     }
+    // concatenate the workers' outputs: sizes first, then each worker's part
+    // copied to its offset on its own thread (no reallocation, page faults spread)
+    std::vector<size_t> nb(T + 1, 0), db(T + 1, 0), gb(T + 1, 0);
+    for (int w = 0; w < T; ++w) {
+      nb[w + 1] = nb[w] + outs[w].nodes.size();
+      db[w + 1] = db[w] + outs[w].digs.size();
+      gb[w + 1] = gb[w] + outs[w].grp.size();
+      g.tiny_stage_doubles = std::max(g.tiny_stage_doubles, outs[w].stage);
+      g.tiny_dig_max = std::max(g.tiny_dig_max, outs[w].digmax);
+    }
+    g.tiny_nodes.resize(nb[T]);
+    g.tiny_digits.resize(db[T]);
+    g.tiny_ga.resize(nb[T]);
+    g.tiny_gb.resize(nb[T]);
+    g.tiny_gout.resize(nb[T]);
+    g.tiny_groups.resize(gb[T]);
+    auto place = [&](int w) {
+      const TinyOut& o = outs[w];
+      for (size_t i = 0; i < o.nodes.size(); ++i) {
+        TinyNode tn = o.nodes[i];
+        tn.dig += (int32_t)db[w];
+        g.tiny_nodes[nb[w] + i] = tn;
+      }
+      std::copy(o.digs.begin(), o.digs.end(), g.tiny_digits.begin() + db[w]);
+      std::copy(o.ga.begin(), o.ga.end(), g.tiny_ga.begin() + nb[w]);
+      std::copy(o.gb.begin(), o.gb.end(), g.tiny_gb.begin() + nb[w]);
+      std::copy(o.go.begin(), o.go.end(), g.tiny_gout.begin() + nb[w]);
+      for (size_t i = 0; i < o.grp.size(); ++i)
+        g.tiny_groups[gb[w] + i] = TinyGroup{o.grp[i].beg + (int32_t)nb[w], o.grp[i].end + (int32_t)nb[w]};
+    };
+    th.clear();
+    for (int w = 1; w < T; ++w) th.emplace_back(place, w);
+    place(0);
+    for (auto& x : th) x.join();
     g.n_tiny = (int)g.tiny_nodes.size();
+    tmark("tiny: resolve");
     if (std::getenv("TC_TINY_DEBUG")) {
       // crude per-group cost: per node, serial iterations of one thread
       double best = -1;
@@ -1878,6 +1911,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       t.sout = g.tiny_gout[i].kind == LOC_SMEM ? t.sout : -1;
     }
   }
+  tmark("tiny: release");
   // forced roots consumed inside a tiny level: release with that level as reader
   for (size_t gi = 0; gi < groups.size(); ++gi)
     for (int v : groups[gi])

@@ -155,6 +155,9 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny(const TinyNode* __restric
   __shared__ int hA[kTinyBatch][kTinyMaxSum], hB[kTinyBatch][kTinyMaxSum];
   pdl_launch();
   pdl_wait();
+#ifdef TC_DIAG_TINY_SKIP  // diagnostics build only: tiny launches do no work (timing bound)
+  return;
+#endif
   const TinyGroup G = groups[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   long long* const trace = (blockIdx.x == 0 && tid == 0) ? g_tiny_trace : nullptr;

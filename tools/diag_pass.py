@@ -1,0 +1,23 @@
+"""Device time of a whole pass over a config's slices (graph mode), for A/B runs of
+diagnostics builds (TC_LIBTC=...), e.g. one whose k_tiny returns at entry
+(-DTC_DIAG_TINY_SKIP): an upper bound on what the tiny stage costs in the pass.
+
+    TC_LIBTC=paper_2006_15512_b200/lib/diag/libtc_tinyskip.so python tools/diag_pass.py c4
+"""
+import os
+import sys
+
+sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import bench  # noqa: E402
+from paper_2006_15512_b200 import _lib  # noqa: E402
+
+for name in sys.argv[1:]:
+    spec = bench.CONFIGS[name]
+    flat, _ = bench.load_plan(spec["plan"])
+    h, ch = bench.choose(flat, spec["slices"])
+    ex = _lib.Exec(h, ch, 0)
+    ns = min(ex.num_slices(), int(os.environ.get("DIAG_SLICES", "256")))
+    ex.run(0, ns)
+    ex.run(0, ns, repeats=2)
+    st = ex.run(0, ns, repeats=5)
+    print(name, os.path.basename(_lib.LIB_PATH), "slices", ns, "ms/pass %.3f" % (st["device_ms"] / 5), flush=True)
