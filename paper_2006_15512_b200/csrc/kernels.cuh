@@ -407,6 +407,9 @@ __device__ __forceinline__ void stream_run(const StreamParams& p, double* Ps, in
       hp += staged ? (int64_t)p.bitP[j] * SVFV : p.bitPo[j];
     }
   }
+  // everything above reads kernel parameters only: under programmatic
+  // dependencies it overlaps the predecessor; operand data is read below
+  pdl_wait();
   // the first chunk's big-operand loads are issued before the small operand
   // is staged: the two global round trips overlap
   // (small summed shapes only: the early live range costs registers)
@@ -527,7 +530,8 @@ constexpr int stream_minb() { return NS + NF <= 3 ? TC_STREAM_MINB : 1; }  // la
 template <int NS, int NF>
 __global__ void __launch_bounds__(kStreamThreads, stream_minb<NS, NF>()) k_stream(const StreamParams p) {
   __shared__ double Ps[kStreamStageMax];  // staged small operand (stage_all)
-  pdl_wait();  // operands are produced by earlier launches
+  // operands are produced by earlier launches: stream_run waits (pdl_wait)
+  // after its parameter-only address prologue
   stream_run<NS, NF>(p, Ps, blockIdx.x, 31 - __clz(gridDim.x));
   pdl_launch();  // dependents start as this CTA retires (overlap the tail only)
 }
@@ -540,7 +544,6 @@ __global__ void __launch_bounds__(kStreamThreads, NI <= 2 ? TC_STREAM_MINB : 1) 
   constexpr int NR = NQ / SV2;  // rest combos
   constexpr int CB = kStreamChunkBits;
   const int tid = threadIdx.x;
-  pdl_wait();
   // per-thread low parts of the y address tables (y = chunk * 2^CB + u * 256 + tid)
   int64_t ta = 0, tc = 0, t1 = 0, t2 = 0;
 #pragma unroll
@@ -579,6 +582,9 @@ __global__ void __launch_bounds__(kStreamThreads, NI <= 2 ? TC_STREAM_MINB : 1) 
       ha += p.bitA[j], hc += p.bitC[j], h1 += p.bitP1[j], h2 += p.bitP2[j];
     }
   }
+  // parameters only so far (overlaps the predecessor under programmatic
+  // dependencies); operand data is read below
+  pdl_wait();
   // the chain walk, over global or smem-staged small operands (each call
   // site inlines with its own address space)
   auto walk = [&](const double* __restrict__ P1, const double* __restrict__ P2) {

@@ -86,8 +86,11 @@ def sliced_execute(n, t, mem_budget=None, *, slice_indices=None, device=None, gr
     b, e = lo + b, lo + e
     st = ex.run(b, e) if e > b else None
     R = ex.result_size()
-    local = torch.zeros((e - b, R), dtype=torch.float64, device=torch.device("cuda", dev))
+    # the copy runs on libtc's stream: the buffer must have no pending write on
+    # torch's stream (a zero fill there could land after the copy)
+    local = torch.empty((e - b, R), dtype=torch.float64, device=torch.device("cuda", dev))
     if e > b:
+        torch.cuda.current_stream(dev).synchronize()
         ex.copy_results(local.data_ptr())
     full = gather_slices(local, b - lo, hi - lo, group=group)
     out = fold(full).cpu().numpy()
