@@ -14,10 +14,15 @@ from paper_2006_15512_b200 import _lib  # noqa: E402
 for name in sys.argv[1:]:
     spec = bench.CONFIGS[name]
     flat, _ = bench.load_plan(spec["plan"])
-    h, ch = bench.choose(flat, spec["slices"])
+    rule = spec["slices"]
+    if os.environ.get("DIAG_PICKS") and rule and rule[0] == "greedy":  # k-pick greedy prefix instead
+        rule = ("greedy", int(os.environ["DIAG_PICKS"]))
+    h, ch = bench.choose(flat, rule)
     ex = _lib.Exec(h, ch, 0)
     ns = min(ex.num_slices(), int(os.environ.get("DIAG_SLICES", "256")))
     ex.run(0, ns)
     ex.run(0, ns, repeats=2)
     st = ex.run(0, ns, repeats=5)
-    print(name, os.path.basename(_lib.LIB_PATH), "slices", ns, "ms/pass %.3f" % (st["device_ms"] / 5), flush=True)
+    ex_b = (st.get("phys_bytes_hoisted", 0) + ns * (st.get("phys_bytes", 0) - st.get("phys_bytes_hoisted", 0))) / 1e9
+    print(name, os.path.basename(_lib.LIB_PATH), "picks", len(ch), "slices", ns, "ms/pass %.3f" % (st["device_ms"] / 5),
+          "executed GB/pass %.1f" % ex_b, "launches/pass", st["gpu_launches"] // 5, flush=True)
