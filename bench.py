@@ -270,7 +270,7 @@ def classes_from_profile(prof, n_slices, hbm, fp64):
     cls = {}
     for p in prof:
         c = cls.setdefault(p["kind"], dict(ms=0.0, bytes=0.0, flops=0.0, launches=0))
-        mult = 1 if p["inv"] else n_slices
+        mult = p["runs"]  # prologue once, block tier once per block, else per slice
         c["ms"] += p["ms"]
         c["bytes"] += p["bytes"] * mult
         c["flops"] += p["flops"] * mult
@@ -725,8 +725,10 @@ def run_ours(args):
                    f"(hoisted launches once); achieved = executed bytes (flops) / summed launch time")
     # whole-step executed-work fraction: every launched kernel's own work per step
     slices_rank = e - b
-    by_step = sum(p["bytes"] * (1 if p["inv"] else slices_rank) for p in prof)
-    fl_step = sum(p["flops"] * (1 if p["inv"] else slices_rank) for p in prof)
+    B = max(1, int(st.get("slices_per_block", 1)))  # the timed pass's block size
+    runs_step = lambda p: 1 if p["inv"] else (-(-slices_rank // B) if p["blk"] else slices_rank)  # noqa: E731
+    by_step = sum(p["bytes"] * runs_step(p) for p in prof)
+    fl_step = sum(p["flops"] * runs_step(p) for p in prof)
     t_step_s = ms_per_step / 1e3 / (slices_per_step / max(1, slices_rank)) if sliced else ms_per_step / 1e3
     step_roof = dict(executed_bytes_per_rank_step=by_step, executed_flops_per_rank_step=fl_step,
                      achieved_gbs=by_step / (ms_per_step / 1e3) / 1e9, hbm_peak=hbm,
@@ -779,7 +781,11 @@ def run_ours(args):
         compile_ms=st["compile_ms"], device_peak_bytes=st["device_peak_bytes"],
         hoisting=dict(launches_prologue=st["launches_prologue"], launches_per_slice=st["launches_per_slice"],
                       phys_bytes_hoisted=st["phys_bytes_hoisted"], phys_bytes_per_slice=st["phys_bytes"],
-                      pinned_bytes=st["pinned_bytes"]),
+                      pinned_bytes=st["pinned_bytes"], launches_block=st["launches_block"],
+                      phys_bytes_block=st["phys_bytes_block"], slices_per_block=st["slices_per_block"],
+                      note="prologue launches run once per pass, block-tier launches once per block of "
+                           "slices_per_block consecutive slices (nodes not depending on the last chosen index), "
+                           "the rest per slice"),
         work=dict(dense_bytes_per_slice=st["alg_bytes"], dense_flops_per_slice=st["alg_flops"],
                   phys_bytes_per_slice=st["phys_bytes"], phys_flops_per_slice=st["phys_flops"],
                   tied_leaves=st["n_tied_leaves"], aliases=st["n_alias_nodes"]),

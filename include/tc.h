@@ -113,6 +113,15 @@ typedef struct tc_stats {
   int64_t launches_prologue;     /* kernels launched once per pass            */
   int64_t launches_per_slice;    /* kernels launched per slice                */
   int64_t pinned_bytes;          /* arena prefix holding hoisted tensors      */
+  /* slice blocks: per-slice nodes that do not depend on the last chosen
+   * (fastest-varying) index run once per block of slices_per_block
+   * consecutive slices.  Per pass the device executes phys_*_hoisted +
+   * blocks * phys_*_block + num_slices_run * (phys_* - phys_*_hoisted -
+   * phys_*_block).                                                          */
+  tc_u128 phys_bytes_block;      /* of phys_bytes: executed once per block     */
+  tc_u128 phys_flops_block;
+  int64_t launches_block;        /* kernels launched once per block            */
+  int64_t slices_per_block;      /* block size of the program (1: no block tier) */
 } tc_stats;
 
 /* ---- symbolic plan (host) ---------------------------------------------- */
@@ -213,6 +222,8 @@ int tc_exec_profile_graph(tc_exec* ex, int64_t slice_begin, int64_t slice_end, f
  * i depends on deps[dep_off[i] .. dep_off[i+1])).  *n = launches, *m = edges. */
 int tc_exec_deps(const tc_exec* ex, int32_t* dep_off, int32_t* deps, int32_t cap, int32_t* n, int32_t* m);
 int64_t tc_exec_result_size(const tc_exec* ex);
+/* Slices per block of the last pass (1: the block tier ran before every slice). */
+int64_t tc_exec_slices_per_block(const tc_exec* ex);
 
 /* One-shot Algorithm 3 (slicing.py:112-146) from host buffers: pick slices
  * (explicit ids when n_slice_ids >= 0, greedy from mem_budget when

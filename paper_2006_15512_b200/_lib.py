@@ -87,6 +87,10 @@ class Stats(C.Structure):
         ("launches_prologue", C.c_int64),
         ("launches_per_slice", C.c_int64),
         ("pinned_bytes", C.c_int64),
+        ("phys_bytes_block", U128),
+        ("phys_flops_block", U128),
+        ("launches_block", C.c_int64),
+        ("slices_per_block", C.c_int64),
     ]
 
     def as_dict(self):
@@ -115,6 +119,10 @@ class Stats(C.Structure):
             phys_flops_hoisted=self.phys_flops_hoisted.value(),
             launches_prologue=int(self.launches_prologue),
             launches_per_slice=int(self.launches_per_slice),
+            phys_bytes_block=self.phys_bytes_block.value(),
+            phys_flops_block=self.phys_flops_block.value(),
+            launches_block=int(self.launches_block),
+            slices_per_block=int(self.slices_per_block),
             pinned_bytes=int(self.pinned_bytes),
         )
 
@@ -204,6 +212,7 @@ SIGNATURES = {
     "tc_exec_profile_graph": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(C.c_float), I32P, I32P, F64P,
                                         F64P, C.c_int32, I32P, C.POINTER(C.c_float)]),
     "tc_exec_result_size": (C.c_int64, [C.c_void_p]),
+    "tc_exec_slices_per_block": (C.c_int64, [C.c_void_p]),
     "tc_exec_deps": (C.c_int, [C.c_void_p, I32P, I32P, C.c_int32, I32P, I32P]),
     "tc_sliced_execute": (
         C.c_int,
@@ -477,8 +486,13 @@ class Exec:
                                           _p(kind, I32P), _p(inv, I32P), _p(by, F64P), _p(fl, F64P), cap,
                                           C.byref(n), C.byref(pm)))
         k = n.value
-        return [dict(kind=self.KINDS[kind[i]], inv=bool(inv[i] & 1), ms=float(ms[i]), bytes=float(by[i]),
-                     flops=float(fl[i]), start_us=int(inv[i] >> 1)) for i in range(k)], float(pm.value)
+        # runs of each launch in the pass: prologue once, block tier once per block, else per slice
+        B = int(lib().tc_exec_slices_per_block(self.h))
+        ns = int(end) - int(begin)
+        runs = lambda x: 1 if x & 1 else (-(-ns // B) if x & 2 else ns)  # noqa: E731
+        return [dict(kind=self.KINDS[kind[i]], inv=bool(inv[i] & 1), blk=bool(inv[i] & 2), runs=runs(int(inv[i])),
+                     ms=float(ms[i]), bytes=float(by[i]), flops=float(fl[i]), start_us=int(inv[i] >> 2))
+                for i in range(k)], float(pm.value)
 
     def deps(self):
         """Launch DAG: list of dependency lists (diagnostics)."""

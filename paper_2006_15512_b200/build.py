@@ -71,8 +71,6 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
     deps.append(os.path.join(ROOT, "include", "tc_decompose.h"))
     deps.append(os.path.abspath(__file__))
     lib_out = out or LIB
-    if not force and not _stale(lib_out, deps):
-        return lib_out
     os.makedirs(os.path.dirname(lib_out), exist_ok=True)
     # one object per source (compiled in parallel, each rebuilt only when it or a
     # header changed), then one link: editing a host .cpp does not recompile the
@@ -85,14 +83,25 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
     hdr = [d for d in deps if not d.endswith(tuple(SOURCES))]
     jobs = []
     objs = []
+    import hashlib
+
+    hh = hashlib.sha256()
+    for d in hdr:
+        with open(d, "rb") as fh:
+            hh.update(fh.read())
     for f in SOURCES:
         src = os.path.join(CSRC, f)
         obj = os.path.join(objdir, f + ".o")
         stamp = obj + ".flags"
-        flags = " ".join(common)
+        # the stamp holds the flags and a hash of the source and headers (an
+        # mtime check misses an edit made while the previous compile ran)
+        h = hh.copy()
+        with open(src, "rb") as fh:
+            h.update(fh.read())
+        flags = " ".join(common) + "\n" + h.hexdigest()
         objs.append(obj)
         old = open(stamp).read() if os.path.exists(stamp) else None
-        if force or old != flags or _stale(obj, [src, *hdr]):
+        if force or old != flags or not os.path.exists(obj):
             jobs.append(([*common, "-c", src, "-o", obj + ".tmp"], obj, stamp, flags))
 
     def run(job):
@@ -109,6 +118,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
 
         with ThreadPoolExecutor(len(jobs)) as ex:
             list(ex.map(run, jobs))
+    elif not force and os.path.exists(lib_out) and not _stale(lib_out, objs):
+        return lib_out
     cmd = [nvcc(), *ARCH, "-shared", *objs, "-o", lib_out + ".tmp", "-lpthread", "-ldl"]
     if verbose:
         print(" ".join(cmd), flush=True)

@@ -71,18 +71,21 @@ constexpr int64_t kLateReleaseMax = (int64_t)1 << 30;  // late release (chain-li
 // invariant writer between two per-slice users of a range would otherwise
 // carry their ordering, and it is not in the per-slice graph).
 struct Alloc {
-  std::map<int64_t, int64_t> free_[2];                   // off -> size
-  std::map<int64_t, std::pair<int64_t, int>> seg[2];     // off -> (end, last reader step)
+  std::map<int64_t, int64_t> free_[3];                   // off -> size
+  std::map<int64_t, std::pair<int64_t, int>> seg[3];     // off -> (end, last reader step)
   // Each memory class has its own region: class 1 (slice-invariant, the
   // prologue's) starts above the pinned prefix; class 0 (per slice) is
   // allocated in a tagged address space (offsets >= kTag) and relocated above
   // class 1's region at the end of the compile (relocate()), so a slice
   // lane's private copy holds only the per-slice region.  Without hoisting
   // there is one class and no tag.
+  // Class 2 (the block tier: per-slice nodes that run once per block of
+  // slices) lives in the lane-private part too, above class 0 (tag kTag2).
   static constexpr int64_t kTag = (int64_t)1 << 56;
+  static constexpr int64_t kTag2 = (int64_t)2 << 56;
   bool split = false;
-  int64_t top_[2] = {0, 0};  // per-class high-water mark (absolute, tagged for class 0 when split)
-  int64_t hi[2] = {0, 0};    // highest end of any allocation per memory class
+  int64_t top_[3] = {0, 0, 0};  // per-class high-water mark (absolute, tagged for classes 0 / 2 when split)
+  int64_t hi[3] = {0, 0, 0};    // highest end of any allocation per memory class
 
   bool no_reuse = false;  // every buffer gets fresh memory: no WAR edges at all
   // pinned region [0, pin_end): buffers that are never released (hoisting
@@ -91,11 +94,12 @@ struct Alloc {
 
   void reserve_pinned(int64_t bytes) {
     pin_end = bytes;
-    for (int c = 0; c < 2; ++c) top_[c] = std::max(top_[c], bytes);
+    for (int c = 0; c < 3; ++c) top_[c] = std::max(top_[c], bytes);
   }
   void split_classes() {  // after reserve_pinned, before any alloc
     split = true;
     top_[0] = kTag;
+    top_[2] = kTag2;
   }
   int64_t alloc_pinned(int64_t size) {
     size = (size + kAlign - 1) / kAlign * kAlign;
@@ -104,16 +108,20 @@ struct Alloc {
     if (pin_top > pin_end) fail(TC_BAD_ARG, "pinned arena region overflow");
     return o;
   }
-  // final layout: [pinned | class 1 | class 0]; returns the class-0 base
+  // final layout: [pinned | class 1 | class 0 | class 2]; returns the class-0 base
   int64_t region0_base() const {
     if (!split) return pin_end;
     return (top_[1] + kAlign - 1) / kAlign * kAlign;
   }
+  int64_t region2_base() const { return region0_base() + (top_[0] - kTag + kAlign - 1) / kAlign * kAlign; }
   int64_t arena_end() const {
     if (!split) return std::max(top_[0], top_[1]);
-    return region0_base() + (top_[0] - kTag);
+    return region2_base() + (top_[2] - kTag2);
   }
-  int64_t relocate(int64_t off) const { return split && off >= kTag ? off - kTag + region0_base() : off; }
+  int64_t relocate(int64_t off) const {
+    if (!split || off < kTag) return off;
+    return off >= kTag2 ? off - kTag2 + region2_base() : off - kTag + region0_base();
+  }
 
   int64_t alloc(int64_t size, std::vector<int>& hazards, int cl = 0) {
     size = (size + kAlign - 1) / kAlign * kAlign;
@@ -1258,7 +1266,50 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     }
     g.hoisted = true;
   }
-  auto mcl = [&](int slot) { return hoist && !var_[slot] ? 1 : 0; };  // arena memory class
+  // ---- slice blocks -----------------------------------------------------------
+  // Slices run in lexicographic order, the last chosen index fastest, so the
+  // block_dim consecutive slices that differ only in it form a block.  A
+  // per-slice node none of whose leaves holds that index (or an index tied to
+  // it) computes the same tensor for every slice of a block: it runs once per
+  // block (the runtime's block graph, on the block's lane before its slices).
+  // Its tensors live in their own lane-private memory class (class 2), and
+  // the ones read by per-slice nodes ("block boundary") are never released,
+  // so they survive the block.  TC_BLOCK=0 runs them per slice (bit-identical).
+  std::vector<char> blk_(S, 0), blkb(S, 0);
+  if (hoist && !(std::getenv("TC_BLOCK") && std::atoi(std::getenv("TC_BLOCK")) == 0)) {
+    const int fast = g.chosen.back();
+    std::vector<char> dep(S, 0);  // depends on the fastest chosen index
+    for (int l = 0; l < p.NL; ++l)
+      for (int i : p.ref_order[l])
+        if (pdrop[i] && (i == fast || implied_src[i] == fast)) dep[l] = 1;
+    bool any = false;
+    for (int k = 0; k < p.NN; ++k) {
+      const int v = p.NL + k;
+      dep[v] = g.cls[v] == NC_ALIAS ? dep[alias_src[v]] : (char)(dep[p.left[k]] | dep[p.right[k]]);
+      blk_[v] = var_[v] && !dep[v];
+      any = any || (blk_[v] && g.cls[v] != NC_ALIAS);
+    }
+    if (any) {
+      g.block_dim = g.chosen_dim.back();
+      for (int k = 0; k < p.NN; ++k) {
+        const int v = p.NL + k;
+        if (!blk_[v] || g.cls[v] == NC_ALIAS) continue;
+        int cur = v, u = p.parent[v];
+        while (u >= 0 && g.cls[u] == NC_ALIAS && alias_src[u] == cur) cur = u, u = p.parent[u];
+        if (u >= 0 && g.cls[u] == NC_ALIAS) continue;  // the tie-piece side of an alias: never read
+        blkb[v] = u < 0 || !blk_[u];                    // read per slice (or by k_rootcopy)
+      }
+    } else {
+      std::fill(blk_.begin(), blk_.end(), 0);
+    }
+  }
+  // arena memory class: 1 slice-invariant, 2 block tier, 0 per slice
+  auto mcl = [&](int slot) { return hoist && !var_[slot] ? 1 : blk_[slot] ? 2 : 0; };
+  // a block-boundary buffer (looked up through relabel aliases) is never released
+  auto kept = [&](int slot) {
+    while (slot >= p.NL && g.cls[slot] == NC_ALIAS) slot = alias_src[slot];
+    return (bool)blkb[slot];
+  };
 
   tmark("tiny groups");
   // ---- tiny groups -------------------------------------------------------------
@@ -1504,6 +1555,19 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       const int r = gr.back(), u = p.parent[r];
       if (u >= 0 && is_tiny(u) && !var_[r]) boundary[r] = var_[groups[group_of[u]].back()];
     }
+    // the same for every arena tensor a tiny node reads (a group root or a
+    // non-tiny node): the reading launch is the reader's group launch, whose
+    // category (prologue / block / per slice) is its root's
+    for (int k = 0; k < p.NN; ++k) {
+      const int v = p.NL + k;
+      if (g.cls[v] == NC_ALIAS || (is_tiny(v) && !groot[v])) continue;
+      int cur = v, u = p.parent[v];
+      while (u >= 0 && g.cls[u] == NC_ALIAS && alias_src[u] == cur) cur = u, u = p.parent[u];
+      if (u < 0 || g.cls[u] == NC_ALIAS || !is_tiny(u)) continue;
+      const int gr = groups[group_of[u]].back();
+      if (!var_[v] && var_[gr]) boundary[v] = 1;
+      if (blk_[v] && !blk_[gr]) blkb[v] = 1;
+    }
     int64_t pin = 0;
     for (int k = 0; k < p.NN; ++k) {
       const int v = p.NL + k;
@@ -1521,21 +1585,27 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     g.loc[r] = Loc{LOC_ARENA, boundary[r] ? arena.alloc_pinned(bytes[r]) : arena.alloc(bytes[r], haz, mcl(r))};
   }
   // one tiny launch per level, split by variance when hoisting (key = 2*level + variant)
-  const int nkeys = hoist ? 2 * nlevels : nlevels;
-  auto gkey = [&](size_t gi) { return hoist ? 2 * glevel[gi] + (var_[groups[gi].back()] ? 1 : 0) : glevel[gi]; };
+  // key = H * level + category (0 prologue, 1 block, 2 per slice) when hoisting
+  const int H = hoist ? 3 : 1;
+  const int nkeys = H * nlevels;
+  auto gkey = [&](size_t gi) {
+    const int r = groups[gi].back();
+    return hoist ? 3 * glevel[gi] + (!var_[r] ? 0 : blk_[r] ? 1 : 2) : glevel[gi];
+  };
   std::vector<int> key_groups(nkeys, 0);
   for (size_t gi = 0; gi < groups.size(); ++gi) key_groups[gkey(gi)]++;
   std::vector<int> tiny_step(nkeys, -1);
   for (int kk = 0; kk < nkeys; ++kk) {
     if (!key_groups[kk]) continue;
-    const int lv = hoist ? kk / 2 : kk;
+    const int lv = kk / H, cat = kk % H;
     Step st;
     st.kind = ST_TINY;
-    st.inv = hoist && !(kk & 1);
+    st.inv = hoist && cat == 0;
+    st.blk = hoist && cat == 1;
     if (sel_step >= 0 && !st.inv) st.deps.push_back(sel_step);
     if (lv >= nbuckets)  // a later level reads forced roots of any level-0 launch
       for (int b = 0; b < kk; ++b) {
-        if (tiny_step[b] < 0 || (hoist && (b / 2 >= lv || (st.inv && (b & 1))))) continue;
+        if (tiny_step[b] < 0 || (hoist && (b / H >= lv || b % H > cat))) continue;
         st.deps.push_back(tiny_step[b]);
       }
     tiny_step[kk] = (int)g.steps.size();
@@ -1917,7 +1987,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     for (int v : groups[gi])
       for (int c : {p.kid_l(v), p.kid_r(v)})
         if (is_tiny(c) && group_of[c] != (int)gi)
-          arena.release(g.loc[c].off, bytes[c], tiny_step[gkey(gi)], mcl(c));
+          if (!kept(c)) arena.release(g.loc[c].off, bytes[c], tiny_step[gkey(gi)], mcl(c));
   // store level ranges in the TINY steps (reuse `work` / gdig_off fields)
   for (int lv = 0; lv < nkeys; ++lv) {
     if (tiny_step[lv] < 0) continue;
@@ -1941,8 +2011,57 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       if (hoist && !var_[v]) {
         g.phys_bytes_inv += (u128)(8 * (size[a] + size[b] + size[v]));
         g.phys_flops_inv += (u128)fl;
+      } else if (blk_[v]) {
+        g.phys_bytes_blk += (u128)(8 * (size[a] + size[b] + size[v]));
+        g.phys_flops_blk += (u128)fl;
       }
     }
+  }
+
+  if (hoist && std::getenv("TC_DEP_STATS")) {
+    // diagnostics: per variant node, the fastest chosen index it depends on
+    // (kmax): in lexicographic slice order its tensor changes only every
+    // prod(dims after kmax) slices -- the work a prefix-level hoist would run
+    const int nc = (int)g.chosen.size();
+    std::vector<int> kmax(S, -1);
+    std::vector<int> chosen_pos(p.NI, -1);
+    for (int j = 0; j < nc; ++j) chosen_pos[g.chosen[j]] = j;
+    for (int l = 0; l < p.NL; ++l)
+      for (int i : p.ref_order[l])
+        if (pdrop[i]) kmax[l] = std::max(kmax[l], chosen_pos[drop[i] ? i : implied_src[i]]);
+    std::vector<double> by(nc + 1, 0.0);
+    std::vector<int> cnt_by(nc + 1, 0);
+    double now = 0, pre = 0;
+    for (int k = 0; k < p.NN; ++k) {
+      const int v = p.NL + k;
+      kmax[v] = g.cls[v] == NC_ALIAS ? kmax[alias_src[v]] : std::max(kmax[p.left[k]], kmax[p.right[k]]);
+      if (g.cls[v] == NC_ALIAS || !var_[v]) continue;
+      double reps = 1;
+      for (int j = 0; j <= kmax[v]; ++j) reps *= g.chosen_dim[j];
+      by[kmax[v] + 1] += node_bytes[v];
+      cnt_by[kmax[v] + 1]++;
+      now += node_bytes[v] * (double)g.num_slices;
+      pre += node_bytes[v] * reps;
+    }
+    if (nc <= 62) {  // per dependence mask (bit j = chosen[j]): node count, per-slice bytes
+      std::vector<uint64_t> mask(S, 0);
+      for (int l = 0; l < p.NL; ++l)
+        for (int i : p.ref_order[l])
+          if (pdrop[i]) mask[l] |= 1ull << chosen_pos[drop[i] ? i : implied_src[i]];
+      std::map<uint64_t, std::pair<int, double>> bym;
+      for (int k = 0; k < p.NN; ++k) {
+        const int v = p.NL + k;
+        mask[v] = g.cls[v] == NC_ALIAS ? mask[alias_src[v]] : (mask[p.left[k]] | mask[p.right[k]]);
+        if (g.cls[v] == NC_ALIAS || !var_[v]) continue;
+        bym[mask[v]].first++;
+        bym[mask[v]].second += node_bytes[v];
+      }
+      for (auto& [m, cb] : bym) std::fprintf(stderr, "[depmask] %llx %d %.0f\n", (unsigned long long)m, cb.first, cb.second);
+    }
+    std::fprintf(stderr, "[deps] per-slice bytes by fastest chosen index (0 = slowest):");
+    for (int j = 1; j <= nc; ++j) std::fprintf(stderr, " k%d:%d nodes %.2f GB", j - 1, cnt_by[j], by[j] / 1e9);
+    std::fprintf(stderr, "\n[deps] variant bytes per pass: per slice %.1f GB, prefix-level hoist %.1f GB\n", now / 1e9,
+                 pre / 1e9);
   }
 
   tmark("emit nodes");
@@ -2072,6 +2191,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     Step st;
     st.slot = v;
     st.inv = hoist && !var_[v];
+    st.blk = blk_[v];
     st.alg_bytes = node_bytes[v];
     st.alg_flops = node_flops[v];
     st.la = g.loc[a];
@@ -2288,6 +2408,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       rd.kind = ST_GEMM_REDUCE;
       rd.slot = v;
       rd.inv = st.inv;
+      rd.blk = st.blk;
       rd.gp = st.gp;
       rd.bm = st.bm;
       rd.bn = st.bn;
@@ -2318,7 +2439,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
       link = (eff[pb].size() <= eff[pa].size() ? pa : pb) == cur;
     }
     for (int c : {a, b})
-      if (g.loc[c].kind == LOC_ARENA) {
+      if (g.loc[c].kind == LOC_ARENA && !kept(c)) {
         if (link && bytes[c] <= kLateReleaseMax) pending.push_back({g.loc[c].off, bytes[c], me, mcl(c)});
         else arena.release(g.loc[c].off, bytes[c], me, mcl(c));
       }

@@ -27,6 +27,8 @@ struct Step {
   StepKind kind;
   int slot = -1;  // node for STREAM/GEMM/GENERIC
   bool inv = false;  // slice-invariant: runs once per pass (prologue), not per slice
+  bool blk = false;  // depends on no index but the fastest sliced one's predecessors: once per block
+  int cat() const { return inv ? 0 : blk ? 1 : 2; }  // 0 prologue, 1 block, 2 per slice
   std::vector<int> deps;
   // kernel parameters with pointer fields holding Loc-encoded placeholders
   StreamParams sp{};
@@ -80,6 +82,11 @@ struct Program {
   u128 phys_bytes = 0, phys_flops = 0;  // executed work over physical variables
   u128 phys_bytes_inv = 0, phys_flops_inv = 0;  // ... of it, slice-invariant (hoisted: once per pass)
   bool hoisted = false;          // slice-invariant nodes run once per pass (compile.cpp)
+  // slice blocks: a per-slice node that does not depend on the fastest-varying
+  // sliced index (the last chosen) computes the same tensor for the block_dim
+  // consecutive slices that differ only in it: it runs once per block
+  int32_t block_dim = 1;         // slices per block (1: no block tier)
+  u128 phys_bytes_blk = 0, phys_flops_blk = 0;  // ... of phys_bytes, block tier (once per block)
   int64_t pinned_bytes = 0;      // arena prefix holding hoisted tensors read by per-slice nodes
   u128 mem_estimate = 0, peak_observed = 0;
 };

@@ -63,12 +63,16 @@ __global__ void k_rootcopy(const RootCopyParams p) {
   }
 }
 
+// eta = [current slice, first slice of the pass, stride K*B, lane's first
+// offset k*B, slices per block B]: a lane runs B consecutive slices, then
+// jumps to its next block (B = 1: every K-th slice)
 __global__ void k_eta(int64_t* eta) {
   pdl_launch();
   pdl_wait();
-  eta[0] += eta[2];  // lane stride (1 without slice lanes)
+  int64_t t = eta[0] + 1;
+  if ((t - eta[1]) % eta[4] == 0) t += eta[2] - eta[4];
+  eta[0] = t;
 }
-// eta = [current slice, first slice of the pass, lane stride, lane]
 __global__ void k_eta_reset(int64_t* eta) { eta[0] = eta[1] + eta[3]; }
 
 // L2 eviction between timed passes (benchmark only): stream a scratch buffer

@@ -215,6 +215,8 @@ struct Launch {
   unsigned smem = 0;
   int kind = 0, slot = -1;
   bool inv = false;   // slice-invariant: in the prologue graph, once per pass
+  bool blk = false;   // block tier: in the block graph, once per block of slices (compile.cpp)
+  int cat() const { return inv ? 0 : blk ? 1 : 2; }
   double bytes = 0, flops = 0;
   int xbits = -1, ns = 0, nf = 0, ns2 = -1, nf2 = -1;  // stream shape (diagnostics)
   std::vector<char> blob;
@@ -266,9 +268,21 @@ struct tc_exec {
   cudaGraphExec_t gexec = nullptr;      // per-slice graph
   cudaGraph_t graph_pro = nullptr;      // slice-invariant prologue (hoisted nodes), once per pass
   cudaGraphExec_t gexec_pro = nullptr;
+  cudaGraph_t graph_blk = nullptr;      // block tier (+ the slice select), once per block of slices
+  cudaGraphExec_t gexec_blk = nullptr;
   int64_t kernels_per_slice = 0;
   int64_t kernels_prologue = 0;
-  int64_t launches_per_pass(int64_t n) const { return kernels_prologue + kernels_per_slice * n; }
+  int64_t kernels_block = 0;            // block-graph kernels (0: no block tier)
+  int64_t last_B = 1;                   // slices per block of the last pass
+  int64_t launches_per_pass(int64_t n) const {
+    return kernels_prologue + kernels_per_slice * n + kernels_block * ((n + last_B - 1) / last_B);
+  }
+  // slices per block for a pass over [b, b + n): the program's block size when
+  // the pass covers whole blocks, else 1 (the block graph runs before every slice)
+  int64_t block_for(int64_t b, int64_t n) const {
+    const int64_t B = prog.block_dim;
+    return (kernels_block > 0 && B > 1 && b % B == 0 && n % B == 0) ? B : 1;
+  }
   int64_t last_n = 0;
   double compile_ms = 0;
 
@@ -289,6 +303,8 @@ struct tc_exec {
     std::vector<std::vector<int>> ldeps;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t gexec = nullptr;
+    cudaGraph_t graph_blk = nullptr;
+    cudaGraphExec_t gexec_blk = nullptr;
   };
   std::vector<Lane> xl;  // lanes 1..K-1
   cudaEvent_t pro_done = nullptr;
@@ -299,6 +315,8 @@ struct tc_exec {
       if (L.stream) cudaStreamSynchronize(L.stream);
       if (L.gexec) cudaGraphExecDestroy(L.gexec);
       if (L.graph) cudaGraphDestroy(L.graph);
+      if (L.gexec_blk) cudaGraphExecDestroy(L.gexec_blk);
+      if (L.graph_blk) cudaGraphDestroy(L.graph_blk);
       for (void* q : {(void*)L.arena, (void*)L.sliced, (void*)L.tnodes, (void*)L.eta}) dcache().put(device, q);
       if (L.done) cudaEventDestroy(L.done);
       if (L.stream) cudaStreamDestroy(L.stream);
@@ -308,6 +326,8 @@ struct tc_exec {
     if (graph) cudaGraphDestroy(graph);
     if (gexec_pro) cudaGraphExecDestroy(gexec_pro);
     if (graph_pro) cudaGraphDestroy(graph_pro);
+    if (gexec_blk) cudaGraphExecDestroy(gexec_blk);
+    if (graph_blk) cudaGraphDestroy(graph_blk);
     if (stream) cudaStreamSynchronize(stream);
     for (void* q : {(void*)arena, (void*)leafbuf, (void*)slicedbuf, (void*)tnodes, (void*)tdigs,
                     (void*)tgroups, (void*)gdig, (void*)rootmap, (void*)results_slot, (void*)sel, (void*)selt, (void*)eta, (void*)results,
@@ -387,7 +407,7 @@ struct tc_exec {
       gdig = dalloc<GDigit>(g.gdigits.size(), dev_bytes, device);
       CU(cudaMemcpyAsync(gdig, g.gdigits.data(), g.gdigits.size() * sizeof(GDigit), cudaMemcpyHostToDevice, stream));
     }
-    eta = dalloc<int64_t>(4, dev_bytes, device);
+    eta = dalloc<int64_t>(5, dev_bytes, device);
     results_slot = dalloc<double*>(1, dev_bytes, device);
     folded = dalloc<double>((size_t)g.R, dev_bytes, device);
     CU(cudaStreamSynchronize(stream));
@@ -425,6 +445,7 @@ struct tc_exec {
       Launch L;
       L.kind = st.kind;
       L.inv = st.inv;
+      L.blk = st.blk;
       L.slot = st.slot;
       L.bytes = st.alg_bytes;
       L.flops = st.alg_flops;
@@ -536,8 +557,10 @@ struct tc_exec {
   }
 
   void count_launches() {
-    kernels_prologue = kernels_per_slice = 0;
-    for (auto& L : launches) ++(L.inv ? kernels_prologue : kernels_per_slice);
+    kernels_prologue = kernels_per_slice = kernels_block = 0;
+    for (auto& L : launches) ++(L.inv ? kernels_prologue : L.blk ? kernels_block : kernels_per_slice);
+    if (kernels_block)  // the block graph also runs the slice select
+      for (auto& L : launches) kernels_block += L.kind == ST_SELECT;
   }
 
   // Chain links: a stream step whose big operand is the previous stream step's
@@ -697,7 +720,7 @@ struct tc_exec {
                      (int)(mk && pair_fn(tni, s1.ns, s1.nf, s2.ns, s2.nf) != nullptr), (int)s1.inv);
       }
       if (!(on && g.steps[i].kind == ST_STREAM && g.steps[i + 1].kind == ST_STREAM &&
-            g.steps[i].inv == g.steps[i + 1].inv))
+            g.steps[i].inv == g.steps[i + 1].inv && g.steps[i].blk == g.steps[i + 1].blk))
         continue;
       const Step &s1 = g.steps[i], &s2 = g.steps[i + 1];
       bool dep_ok = false;  // step 2 must consume step 1 (its RAW edge)
@@ -733,6 +756,7 @@ struct tc_exec {
         Launch L;
         L.kind = ST_STREAM;
         L.inv = s1.inv;
+        L.blk = s1.blk;
         L.slot = s2.slot;
         L.func = (void*)fn;
         L.block = dim3(kStreamThreads);
@@ -814,17 +838,21 @@ struct tc_exec {
   // Two graphs from the explicit launch DAG (data + WAR edges): the prologue
   // (slice-invariant launches, once per pass over the slices) and the
   // per-slice graph.  Edges between the two are implied by stream order.
-  static void instantiate(const std::vector<Launch>& L, const std::vector<std::vector<int>>& deps, bool want_inv,
+  // launches of graph category `want` (0 prologue, 1 block, 2 per slice); the
+  // block graph also holds the slice select (its nodes read sliced leaves)
+  static bool in_cat(const Launch& L, int want) { return L.cat() == want || (want == 1 && L.kind == ST_SELECT); }
+  static void instantiate(const std::vector<Launch>& L, const std::vector<std::vector<int>>& deps, int want,
                           cudaGraph_t& gr, cudaGraphExec_t& ge) {
     gr = nullptr;
     ge = nullptr;
+    if (want == 1 && std::none_of(L.begin(), L.end(), [](const Launch& x) { return x.blk; })) return;
     std::vector<cudaGraphNode_t> nodes(L.size(), nullptr);
     for (size_t si = 0; si < L.size(); ++si) {
-      if (L[si].inv != want_inv) continue;
+      if (!in_cat(L[si], want)) continue;
       if (!gr) CU(cudaGraphCreate(&gr, 0));
       std::vector<cudaGraphNode_t> dd;
       for (int d : deps[si])
-        if (L[d].inv == want_inv) dd.push_back(nodes[d]);
+        if (in_cat(L[d], want)) dd.push_back(nodes[d]);
       cudaKernelNodeParams kp = const_cast<Launch&>(L[si]).params();
       CU(cudaGraphAddKernelNode(&nodes[si], gr, dd.data(), dd.size(), &kp));
     }
@@ -848,12 +876,15 @@ struct tc_exec {
       th = std::thread([&] {
         try {
           CU(cudaSetDevice(device));
-          instantiate(launches, ldeps, true, graph_pro, gexec_pro);
+          instantiate(launches, ldeps, 0, graph_pro, gexec_pro);
         } catch (...) {
           err = std::current_exception();
         }
       });
-    if (!gexec) instantiate(launches, ldeps, false, graph, gexec);
+    if (!gexec) {
+      instantiate(launches, ldeps, 2, graph, gexec);
+      instantiate(launches, ldeps, 1, graph_blk, gexec_blk);
+    }
     if (th.joinable()) th.join();
     if (err) std::rethrow_exception(err);
     pro_built = pro_built || with_prologue;
@@ -872,7 +903,7 @@ struct tc_exec {
       int64_t dummy = 0;
       L.arena = dalloc<char>((size_t)g.lane_arena_bytes, dev_bytes, device);
       if (g.sliced_doubles) L.sliced = dalloc<double>((size_t)g.sliced_doubles, dev_bytes, device);
-      L.eta = dalloc<int64_t>(4, dummy, device);
+      L.eta = dalloc<int64_t>(5, dummy, device);
       CU(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
       CU(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
       if (!g.tiny_nodes.empty()) {
@@ -892,7 +923,8 @@ struct tc_exec {
           Lane& L = xl[q];
           int rc = -1;
           make_launches((int)q + 1, L.launches, L.ldeps, rc);
-          instantiate(L.launches, L.ldeps, false, L.graph, L.gexec);
+          instantiate(L.launches, L.ldeps, 2, L.graph, L.gexec);
+          instantiate(L.launches, L.ldeps, 1, L.graph_blk, L.gexec_blk);
         } catch (...) {
           err[q] = std::current_exception();
         }
@@ -916,12 +948,15 @@ struct tc_exec {
     return std::max(1, K);
   }
 
-  // slice counters: [current slice, first slice of the pass, stride, lane]
-  void set_eta(int64_t b, int K) {
-    int64_t h[4] = {b, b, K, 0};
+  // slice counters: [current slice, first slice of the pass, stride, lane's
+  // first offset, slices per block]: lane k runs blocks k, k + K, ... of B
+  // consecutive slices (k_eta steps +1 inside a block, then to its next block)
+  void set_eta(int64_t b, int K, int64_t B = 1) {
+    last_B = B;
+    int64_t h[5] = {b, b, K * B, 0, B};
     CU(cudaMemcpyAsync(eta, h, sizeof(h), cudaMemcpyHostToDevice, stream));
     for (int k = 1; k < K; ++k) {
-      int64_t hk[4] = {b + k, b, K, k};
+      int64_t hk[5] = {b + k * B, b, K * B, k * B, B};
       CU(cudaMemcpyAsync(xl[k - 1].eta, hk, sizeof(hk), cudaMemcpyHostToDevice, stream));
     }
     CU(cudaStreamSynchronize(stream));
@@ -999,10 +1034,11 @@ struct tc_exec {
     CU(cudaStreamSynchronize(stream));
   }
 
-  // the prologue (inv) or one slice (!inv) in step order on the stream (no graph)
-  void launch_eager(bool inv, bool first) {
+  // the prologue (0), a block's tier (1) or one slice (2) in step order on the stream (no graph)
+  void launch_eager(int cat, bool first) {
+    if (cat == 1 && !kernels_block) return;
     for (size_t i = 0; i < launches.size(); ++i) {
-      if (launches[i].inv != inv) continue;
+      if (!in_cat(launches[i], cat)) continue;
       launch_one(launches[i], use_pdl() && !first);
       first = false;
     }
@@ -1010,9 +1046,14 @@ struct tc_exec {
   // one pass over n slices: prologue once, then the per-slice launches
   // (round-robin over K lanes; lane 0 is the main stream)
   void launch_pass(int64_t n, bool eager, int K = 1, bool prologue_done = false) {
+    const int64_t B = last_B;  // set_eta's block size for this pass
     if (eager) {
-      launch_eager(true, true);
-      for (int64_t s = 0; s < n; ++s) launch_eager(false, s == 0 && kernels_prologue == 0);
+      launch_eager(0, true);
+      for (int64_t s = 0; s < n; ++s) {
+        const bool first = s == 0 && kernels_prologue == 0;
+        if (s % B == 0) launch_eager(1, first);
+        launch_eager(2, first && !kernels_block);
+      }
       return;
     }
     if (gexec_pro && !prologue_done) CU(cudaGraphLaunch(gexec_pro, stream));
@@ -1021,9 +1062,14 @@ struct tc_exec {
       for (int k = 1; k < K; ++k) CU(cudaStreamWaitEvent(xl[k - 1].stream, pro_done, 0));
     }
     for (int64_t s = 0; s < n; ++s) {
-      const int k = (int)(s % K);
-      if (k == 0) CU(cudaGraphLaunch(gexec, stream));
-      else CU(cudaGraphLaunch(xl[k - 1].gexec, xl[k - 1].stream));
+      const int k = (int)((s / B) % K);
+      if (k == 0) {
+        if (gexec_blk && s % B == 0) CU(cudaGraphLaunch(gexec_blk, stream));
+        CU(cudaGraphLaunch(gexec, stream));
+      } else {
+        if (xl[k - 1].gexec_blk && s % B == 0) CU(cudaGraphLaunch(xl[k - 1].gexec_blk, xl[k - 1].stream));
+        CU(cudaGraphLaunch(xl[k - 1].gexec, xl[k - 1].stream));
+      }
     }
     for (int k = 1; k < K; ++k) {
       CU(cudaEventRecord(xl[k - 1].done, xl[k - 1].stream));
@@ -1100,17 +1146,17 @@ struct tc_exec {
         for (auto x : e0) cudaEventDestroy(x);
         for (auto x : e1) cudaEventDestroy(x);
       }
-    } pg[2];
-    for (int pass = 0; pass < 2; ++pass) {
-      const bool want_inv = pass == 0;
+    } pg[3];
+    for (int pass = 0; pass < 3; ++pass) {  // prologue, block tier, per slice
       PG& G = pg[pass];
+      if (pass == 1 && !kernels_block) continue;
       std::vector<cudaGraphNode_t> nodes(launches.size(), nullptr);
       for (size_t si = 0; si < launches.size(); ++si) {
-        if (launches[si].inv != want_inv) continue;
+        if (!in_cat(launches[si], pass)) continue;
         if (!G.g) CU(cudaGraphCreate(&G.g, 0));
         std::vector<cudaGraphNode_t> deps;
         for (int d : ldeps[si])
-          if (launches[d].inv == want_inv) deps.push_back(nodes[d]);
+          if (in_cat(launches[d], pass)) deps.push_back(nodes[d]);
         cudaEvent_t a, z;
         CU(cudaEventCreate(&a));
         CU(cudaEventCreate(&z));
@@ -1125,7 +1171,8 @@ struct tc_exec {
       }
       if (G.g) CU(cudaGraphInstantiate(&G.ge, G.g, 0));
     }
-    set_eta(b, 1);
+    const int64_t B = block_for(b, n);
+    set_eta(b, 1, B);
     cudaEvent_t p0, p1;
     CU(cudaEventCreate(&p0));
     CU(cudaEventCreate(&p1));
@@ -1139,8 +1186,14 @@ struct tc_exec {
         start_ms[G.idx[q]] = t0;  // of the last graph launch that ran it
       }
     };
-    for (int64_t s = -1; s < n; ++s) {
-      PG& G = pg[s < 0 ? 0 : 1];
+    std::vector<int> seq;  // graph launches of the pass: prologue, then per slice (block tier first)
+    seq.push_back(0);
+    for (int64_t s = 0; s < n; ++s) {
+      if (s % B == 0) seq.push_back(1);
+      seq.push_back(2);
+    }
+    for (int which : seq) {
+      PG& G = pg[which];
       if (!G.ge) continue;
       CU(cudaEventRecord(p0, stream));
       CU(cudaGraphLaunch(G.ge, stream));
@@ -1179,7 +1232,7 @@ struct tc_exec {
     auto tg0 = std::chrono::steady_clock::now();
     if (overlap) {
       CU(cudaEventRecord(e0, stream));
-      launch_eager(true, true);
+      launch_eager(0, true);
     }
     if (!eager) ensure_graph(!overlap);
     auto tg1 = std::chrono::steady_clock::now();
@@ -1190,7 +1243,7 @@ struct tc_exec {
       std::fprintf(stderr, "[run] graphs %.2f ms, lanes(%d) %.2f ms%s\n",
                    std::chrono::duration<double, std::milli>(tg1 - tg0).count(), K, lanes_ms,
                    overlap ? " (overlapping the eager prologue)" : "");
-    set_eta(b, K);
+    set_eta(b, K, block_for(b, n));
     if (!overlap) CU(cudaEventRecord(e0, stream));
     for (int64_t r = 0; r < repeats; ++r) {
       if (r > 0) reset_eta(K);
@@ -1225,7 +1278,7 @@ struct tc_exec {
     for (auto& x : ev) CU(cudaEventCreate(&x));
     const int K = lanes_for(n);
     if (K > 1) ensure_lanes(K);
-    set_eta(b, K);
+    set_eta(b, K, block_for(b, n));
     for (int64_t r = 0; r < repeats; ++r) {
       if (r > 0) reset_eta(K);
       k_flush<<<grid_for(n4, 256, device), 256, 0, stream>>>(fbuf, n4, (double)r);
@@ -1441,8 +1494,11 @@ int tc_compile_stats(const tc_plan* plan, const int32_t* sliced, int32_t n_slice
     s->phys_flops = to_abi(g.phys_flops);
     s->phys_bytes_hoisted = to_abi(g.phys_bytes_inv);
     s->phys_flops_hoisted = to_abi(g.phys_flops_inv);
-    for (auto& st : g.steps) ++(st.inv ? s->launches_prologue : s->launches_per_slice);
+    for (auto& st : g.steps) ++(st.inv ? s->launches_prologue : st.blk ? s->launches_block : s->launches_per_slice);
     s->pinned_bytes = g.pinned_bytes;
+    s->phys_bytes_block = to_abi(g.phys_bytes_blk);
+    s->phys_flops_block = to_abi(g.phys_flops_blk);
+    s->slices_per_block = g.block_dim;
     s->program_ms = ms;
   });
 }
@@ -1475,6 +1531,7 @@ int tc_exec_create(const tc_plan* plan, const int32_t* sliced, int32_t n_sliced,
 void tc_exec_free(tc_exec* ex) { delete ex; }
 
 int64_t tc_exec_result_size(const tc_exec* ex) { return ex->prog.R; }
+int64_t tc_exec_slices_per_block(const tc_exec* ex) { return ex->last_B; }
 
 static void fill_stats(const tc_exec& ex, double ms, tc_stats* s) {
   if (!s) return;
@@ -1501,6 +1558,10 @@ static void fill_stats(const tc_exec& ex, double ms, tc_stats* s) {
   s->launches_prologue = ex.kernels_prologue;
   s->launches_per_slice = ex.kernels_per_slice;
   s->pinned_bytes = g.pinned_bytes;
+  s->phys_bytes_block = to_abi(g.phys_bytes_blk);
+  s->phys_flops_block = to_abi(g.phys_flops_blk);
+  s->launches_block = ex.kernels_block;
+  s->slices_per_block = ex.last_B;
   s->program_ms = ex.program_ms;
   s->setup_ms = ex.setup_ms;
   s->graph_ms = ex.graph_ms;
@@ -1583,7 +1644,7 @@ int tc_exec_profile_graph(tc_exec* ex, int64_t slice_begin, int64_t slice_end, f
       const Launch& L = ex->launches[i];
       if (launch_ms) launch_ms[i] = ms[i];
       if (launch_kind) launch_kind[i] = L.kind;
-      if (launch_inv) launch_inv[i] = (L.inv ? 1 : 0) | ((int32_t)std::lround(ex->start_ms[i] * 1000.0) << 1);
+      if (launch_inv) launch_inv[i] = (L.inv ? 1 : 0) | (L.blk ? 2 : 0) | ((int32_t)std::lround(ex->start_ms[i] * 1000.0) << 2);
       if (launch_bytes) launch_bytes[i] = L.bytes;
       if (launch_flops) launch_flops[i] = L.flops;
     }

@@ -156,6 +156,44 @@ def test_hoisting_is_bitwise_identical(name, picks):
     assert p2.reshape(ns, -1)[:, 0].tobytes() == on.tobytes()
 
 
+@pytest.mark.parametrize("name,picks", [("c1b", 3), ("c2", 4), ("c1a", 5), ("c3", -28)])
+def test_slice_blocks_are_bitwise_identical(name, picks):
+    """Block tier (nodes not depending on the last chosen index run once per
+    block of consecutive slices) vs TC_BLOCK=0 (every variant node per slice):
+    the same bits for a whole pass, a pass starting and ending mid-block (the
+    block graph then runs before every slice), one-shot and graph replay."""
+    flat = _plan(name)
+    h = _lib.PlanHandle(flat)
+    ch = []
+    if picks < 0:
+        ch = h.choose_slices_work(2 ** -picks)
+        picks = 3
+    for _ in range(picks if not ch else 0):
+        ch.append(h.choose_slice_index(ch))
+    ns = 2 ** picks
+    st = h.compile_stats(ch)
+    for b, e in ((0, ns), (1, ns - 1)):
+        on, fon, exon = _per_slice(flat, ch, b, e)
+        off, foff, _ = _per_slice(flat, ch, b, e, env={"TC_BLOCK": "0"})
+        assert on.tobytes() == off.tobytes() and fon == foff, (b, e)
+        exon.run(b, e, repeats=3)
+        f2, p2 = exon.fetch(e - b)
+        assert p2.reshape(e - b, -1)[:, 0].tobytes() == on.tobytes() and f2[0] == fon
+    if st["launches_block"]:
+        assert st["slices_per_block"] == int(flat.domain[ch[-1]])
+
+
+def test_c4_slice_blocks_cut_work():
+    flat = _plan("c4")
+    ch = _chosen(flat, _golden("c4"))
+    st = _lib.PlanHandle(flat).compile_stats(ch)
+    B = st["slices_per_block"]
+    inv, blk = st["phys_bytes_hoisted"], st["phys_bytes_block"]
+    per_pass = inv + 256 // B * blk + 256 * (st["phys_bytes"] - inv - blk)
+    assert B == 2 and blk > 0.3 * (st["phys_bytes"] - inv)
+    assert per_pass < 0.9 * (inv + 256 * (st["phys_bytes"] - inv))
+
+
 def test_c4_hoisting_cuts_work():
     flat = _plan("c4")
     ch = _chosen(flat, _golden("c4"))

@@ -310,6 +310,28 @@ def test_hoisting_compile_on_cpu(monkeypatch):
     assert h.compile_stats([])["launches_prologue"] == 0
 
 
+def test_slice_blocks_compile_on_cpu(monkeypatch):
+    """The block tier (C4, 8 greedy picks): per-slice nodes that do not depend
+    on the last chosen index run once per block of 2 slices; the reference
+    accounting and the executed work per slice are unchanged, TC_BLOCK=0
+    (read per call) runs them per slice."""
+    flat, _ = planfile.load(os.path.join(PLANS, "c4.tcplan.npz"))
+    h = _lib.PlanHandle(flat)
+    ch = []
+    for _ in range(8):
+        ch.append(h.choose_slice_index(ch))
+    on = h.compile_stats(ch)
+    monkeypatch.setenv("TC_BLOCK", "0")
+    off = h.compile_stats(ch)
+    assert on["slices_per_block"] == 2 and off["slices_per_block"] == 1
+    assert on["launches_block"] > 0 and off["launches_block"] == 0 and off["phys_bytes_block"] == 0
+    assert 0 < on["phys_bytes_block"] < on["phys_bytes"] - on["phys_bytes_hoisted"]
+    assert on["phys_bytes"] == off["phys_bytes"] and on["phys_bytes_hoisted"] == off["phys_bytes_hoisted"]
+    assert on["mem_estimate"] == off["mem_estimate"] and on["peak_observed"] == off["peak_observed"]
+    # (a tiny level may split into a block and a per-slice launch: one step more)
+    assert 0 <= on["launches_block"] + on["launches_per_slice"] - off["launches_per_slice"] <= 4
+
+
 def test_budget_semantics_match_reference_loop():
     """sliced_execute's budget loop is ``while mem_cost(chosen) > mem_budget``
     (slicing.py:120-128) for any real budget: inf / nan / a budget beyond int64

@@ -23,6 +23,8 @@ for name in sys.argv[1:]:
     ex.run(0, ns)
     ex.run(0, ns, repeats=2)
     st = ex.run(0, ns, repeats=5)
-    ex_b = (st.get("phys_bytes_hoisted", 0) + ns * (st.get("phys_bytes", 0) - st.get("phys_bytes_hoisted", 0))) / 1e9
+    B = max(1, st.get("slices_per_block", 1))
+    ex_b = (st["phys_bytes_hoisted"] + -(-ns // B) * st["phys_bytes_block"]
+            + ns * (st["phys_bytes"] - st["phys_bytes_hoisted"] - st["phys_bytes_block"])) / 1e9
     print(name, os.path.basename(_lib.LIB_PATH), "picks", len(ch), "slices", ns, "ms/pass %.3f" % (st["device_ms"] / 5),
           "executed GB/pass %.1f" % ex_b, "launches/pass", st["gpu_launches"] // 5, flush=True)
