@@ -1197,11 +1197,85 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
     }
   }
 
+  // ---- slice order: which chosen indices vary fastest ------------------------
+  // msk[s]: the chosen indices (bit = lexicographic position) slot s depends on
+  // (a sliced leaf holds them, a tied index counts as its source).  A per-slice
+  // node whose mask misses every "fast" index runs once per block (the slices
+  // that differ only in the fast indices, consecutive in iteration order).  The
+  // fast set minimises the executed bytes of a pass; the first three chosen
+  // indices stay slow, so ranges that fix them (the rank blocks of up to 8
+  // GPUs, the timed samples) map onto themselves.  TC_SLICE_ORDER=0 keeps the
+  // reference's order (fast = the last chosen index only); TC_BLOCK=0 runs
+  // every variant node per slice.
+  const int nch = (int)g.chosen.size();
+  std::vector<uint64_t> msk(S, 0);
+  uint64_t fast_mask = 0;
+  std::vector<int> iter_order;  // chosen positions, slowest first
+  for (int j = 0; j < nch; ++j) iter_order.push_back(j);
+  {
+    std::vector<int> chosen_pos(p.NI, -1);
+    for (int j = 0; j < nch; ++j) chosen_pos[g.chosen[j]] = j;
+    const bool block_env = !(std::getenv("TC_BLOCK") && std::atoi(std::getenv("TC_BLOCK")) == 0);
+    const bool order_env = !(std::getenv("TC_SLICE_ORDER") && std::atoi(std::getenv("TC_SLICE_ORDER")) == 0);
+    const bool hoist_on = !(std::getenv("TC_HOIST") && std::atoi(std::getenv("TC_HOIST")) == 0);
+    if (nch >= 1 && nch <= 62 && block_env && hoist_on) {
+      for (int l = 0; l < p.NL; ++l)
+        for (int i : p.ref_order[l])
+          if (pdrop[i]) msk[l] |= 1ull << chosen_pos[drop[i] ? i : implied_src[i]];
+      // per-mask executed bytes of the variant nodes
+      std::map<uint64_t, double> wb;
+      for (int k = 0; k < p.NN; ++k) {
+        const int v = p.NL + k, a = p.left[k], b = p.right[k];
+        msk[v] = msk[a] | msk[b];  // (a relabel alias carries its source's mask: the union is the same)
+        if (msk[v]) wb[msk[v]] += 8.0 * (double)(size[a] + size[b] + size[v]);
+      }
+      const int keep = std::min(3, nch - 1);
+      std::vector<int> cand;
+      for (int j = keep; j < nch; ++j) cand.push_back(j);
+      double NS = (double)g.num_slices, best = -1;
+      auto cost = [&](uint64_t fm) {
+        double B = 1;
+        for (int j = 0; j < nch; ++j)
+          if (fm >> j & 1) B *= g.chosen_dim[j];
+        double c = 0;
+        for (auto& [m, b] : wb) c += b * ((m & fm) ? NS : NS / B);
+        return c;
+      };
+      if (order_env && cand.size() <= 16) {
+        for (uint64_t sub = 1; sub < (1ull << cand.size()); ++sub) {
+          uint64_t fm = 0;
+          for (size_t q = 0; q < cand.size(); ++q)
+            if (sub >> q & 1) fm |= 1ull << cand[q];
+          const double c = cost(fm);
+          if (best < 0 || c < best * (1 - 1e-12)) best = c, fast_mask = fm;
+        }
+      } else {
+        fast_mask = 1ull << (nch - 1);
+      }
+      iter_order.clear();
+      for (int j = 0; j < nch; ++j)
+        if (!(fast_mask >> j & 1)) iter_order.push_back(j);
+      for (int j = 0; j < nch; ++j)
+        if (fast_mask >> j & 1) iter_order.push_back(j);
+    }
+  }
+  g.ord_dim.assign(g.chosen_dim.begin(), g.chosen_dim.end());
+  g.ord_pv_lex.assign(nch, 1);
+  for (int j = nch - 2; j >= 0; --j) g.ord_pv_lex[j] = g.ord_pv_lex[j + 1] * g.chosen_dim[j + 1];
+  g.ord_pv_iter.assign(nch, 1);
+  for (int q = nch - 2; q >= 0; --q)
+    g.ord_pv_iter[iter_order[q]] = g.ord_pv_iter[iter_order[q + 1]] * g.chosen_dim[iter_order[q + 1]];
+  for (int q = 0; q < nch; ++q)
+    if (iter_order[q] != q) {
+      g.permuted = true;
+      g.closed_granule = g.ord_pv_lex[q] * g.chosen_dim[q];
+      break;
+    }
+
   tmark("leaves");
   // ---- leaves: plain, compressed, or per-slice selected ----------------------
   g.loc.assign(S, Loc{LOC_LEAF, 0});
-  std::vector<int64_t> pv(g.chosen.size(), 1);
-  for (int j = (int)g.chosen.size() - 2; j >= 0; --j) pv[j] = pv[j + 1] * g.chosen_dim[j + 1];
+  const std::vector<int64_t>& pv = g.ord_pv_iter;  // k_select decodes the iteration id
   std::vector<int> chosen_slot(p.NI, -1);
   for (size_t j = 0; j < g.chosen.size(); ++j) chosen_slot[g.chosen[j]] = (int)j;
   const int64_t nraw = (int64_t)p.lval.size();
@@ -1276,21 +1350,18 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
   // the ones read by per-slice nodes ("block boundary") are never released,
   // so they survive the block.  TC_BLOCK=0 runs them per slice (bit-identical).
   std::vector<char> blk_(S, 0), blkb(S, 0);
-  if (hoist && !(std::getenv("TC_BLOCK") && std::atoi(std::getenv("TC_BLOCK")) == 0)) {
-    const int fast = g.chosen.back();
-    std::vector<char> dep(S, 0);  // depends on the fastest chosen index
-    for (int l = 0; l < p.NL; ++l)
-      for (int i : p.ref_order[l])
-        if (pdrop[i] && (i == fast || implied_src[i] == fast)) dep[l] = 1;
+  if (hoist && fast_mask) {
     bool any = false;
     for (int k = 0; k < p.NN; ++k) {
       const int v = p.NL + k;
-      dep[v] = g.cls[v] == NC_ALIAS ? dep[alias_src[v]] : (char)(dep[p.left[k]] | dep[p.right[k]]);
-      blk_[v] = var_[v] && !dep[v];
+      const uint64_t m = g.cls[v] == NC_ALIAS ? msk[alias_src[v]] : msk[v];
+      blk_[v] = var_[v] && !(m & fast_mask);
       any = any || (blk_[v] && g.cls[v] != NC_ALIAS);
     }
     if (any) {
-      g.block_dim = g.chosen_dim.back();
+      g.block_dim = 1;
+      for (int j = 0; j < nch; ++j)
+        if (fast_mask >> j & 1) g.block_dim *= g.chosen_dim[j];
       for (int k = 0; k < p.NN; ++k) {
         const int v = p.NL + k;
         if (!blk_[v] || g.cls[v] == NC_ALIAS) continue;

@@ -86,6 +86,14 @@ struct Program {
   // sliced index (the last chosen) computes the same tensor for the block_dim
   // consecutive slices that differ only in it: it runs once per block
   int32_t block_dim = 1;         // slices per block (1: no block tier)
+  // Slice order.  Slices run in an iteration order that may differ from the
+  // reference's lexicographic one (the fold still takes each result from its
+  // lexicographic row): the "fast" chosen indices vary fastest, so a block is
+  // the slices that differ only in them.  Per chosen index j (lexicographic
+  // position): its place value in the iteration id and in the lexicographic id.
+  std::vector<int64_t> ord_pv_iter, ord_pv_lex, ord_dim;
+  bool permuted = false;         // iteration order != lexicographic
+  int64_t closed_granule = 1;    // a range [b, e) with b, e multiples of this maps onto itself
   u128 phys_bytes_blk = 0, phys_flops_blk = 0;  // ... of phys_bytes, block tier (once per block)
   int64_t pinned_bytes = 0;      // arena prefix holding hoisted tensors read by per-slice nodes
   u128 mem_estimate = 0, peak_observed = 0;

@@ -53,7 +53,7 @@ __global__ void k_select(const SelectParams p) {
 __global__ void k_rootcopy(const RootCopyParams p) {
   pdl_launch();
   pdl_wait();
-  const int64_t slot = p.eta[0] - p.eta[1];
+  const int64_t slot = slice_lex(p.ord, p.eta[0]) - p.eta[1];  // the slice's lexicographic row
   double* results = *p.results;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < p.R;
        r += (int64_t)gridDim.x * blockDim.x) {
@@ -63,17 +63,26 @@ __global__ void k_rootcopy(const RootCopyParams p) {
   }
 }
 
-// eta = [current slice, first slice of the pass, stride K*B, lane's first
-// offset k*B, slices per block B]: a lane runs B consecutive slices, then
-// jumps to its next block (B = 1: every K-th slice)
-__global__ void k_eta(int64_t* eta) {
+// eta = [current slice (iteration id), first slice of the pass, stride K*B,
+// lane's first offset k*B, slices per block B, mode].  Mode 0: a lane runs B
+// consecutive iteration ids, then jumps to its next block (B = 1: every K-th
+// slice).  Mode 1 (a range that the slice order does not map onto itself):
+// the lane walks lexicographic ids b + k, b + k + K, ... (B = 1), held as
+// their iteration ids.
+__global__ void k_eta(int64_t* eta, const int64_t* ord) {
   pdl_launch();
   pdl_wait();
+  if (eta[5]) {
+    eta[0] = slice_iter(ord, slice_lex(ord, eta[0]) + eta[2]);
+    return;
+  }
   int64_t t = eta[0] + 1;
   if ((t - eta[1]) % eta[4] == 0) t += eta[2] - eta[4];
   eta[0] = t;
 }
-__global__ void k_eta_reset(int64_t* eta) { eta[0] = eta[1] + eta[3]; }
+__global__ void k_eta_reset(int64_t* eta, const int64_t* ord) {
+  eta[0] = eta[5] ? slice_iter(ord, eta[1] + eta[3]) : eta[1] + eta[3];
+}
 
 // L2 eviction between timed passes (benchmark only): stream a scratch buffer
 __global__ void k_flush(double4* buf, int64_t n, double v) {

@@ -223,7 +223,28 @@ struct RootCopyParams {
   double* const* results;  // device slot holding the [n][R] results buffer (re-pointed by the runtime)
   const int64_t* map;  // dense entry -> physical offset or -1 (nullptr: identity)
   int64_t R;
-  const int64_t* eta;  // [0] = current slice, [1] = first slice of the run
+  const int64_t* eta;  // [0] = current slice (iteration id), [1] = first lexicographic slice of the run
+  const int64_t* ord;  // slice order table (nullptr: iteration id = lexicographic id), see slice_lex
 };
+
+// Slice order table: [n, then per chosen index (lexicographic position j):
+// place value in the iteration id, dimension, place value in the lexicographic id]
+#ifdef __CUDACC__
+#define TC_HD __host__ __device__
+#else
+#define TC_HD
+#endif
+TC_HD inline int64_t slice_lex(const int64_t* ord, int64_t t) {
+  if (!ord) return t;
+  int64_t s = 0;
+  for (int64_t j = 0; j < ord[0]; ++j) s += ((t / ord[1 + 3 * j]) % ord[2 + 3 * j]) * ord[3 + 3 * j];
+  return s;
+}
+TC_HD inline int64_t slice_iter(const int64_t* ord, int64_t s) {
+  if (!ord) return s;
+  int64_t t = 0;
+  for (int64_t j = 0; j < ord[0]; ++j) t += ((s / ord[3 + 3 * j]) % ord[2 + 3 * j]) * ord[1 + 3 * j];
+  return t;
+}
 
 }  // namespace tc

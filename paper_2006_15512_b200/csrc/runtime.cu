@@ -261,6 +261,7 @@ struct tc_exec {
   SelEntry* sel = nullptr;
   SelTerm* selt = nullptr;
   int64_t* eta = nullptr;
+  int64_t* ordbuf = nullptr;  // slice order table (compile.hpp, slice_lex); nullptr: lexicographic order
   double* results = nullptr;
   int64_t results_cap = 0;  // slices
   double* folded = nullptr;
@@ -330,7 +331,7 @@ struct tc_exec {
     if (graph_blk) cudaGraphDestroy(graph_blk);
     if (stream) cudaStreamSynchronize(stream);
     for (void* q : {(void*)arena, (void*)leafbuf, (void*)slicedbuf, (void*)tnodes, (void*)tdigs,
-                    (void*)tgroups, (void*)gdig, (void*)rootmap, (void*)results_slot, (void*)sel, (void*)selt, (void*)eta, (void*)results,
+                    (void*)tgroups, (void*)gdig, (void*)rootmap, (void*)results_slot, (void*)sel, (void*)selt, (void*)eta, (void*)ordbuf, (void*)results,
                     (void*)folded})
       dcache().put(device, q);
     if (stream) cudaStreamDestroy(stream);
@@ -407,7 +408,18 @@ struct tc_exec {
       gdig = dalloc<GDigit>(g.gdigits.size(), dev_bytes, device);
       CU(cudaMemcpyAsync(gdig, g.gdigits.data(), g.gdigits.size() * sizeof(GDigit), cudaMemcpyHostToDevice, stream));
     }
-    eta = dalloc<int64_t>(5, dev_bytes, device);
+    eta = dalloc<int64_t>(6, dev_bytes, device);
+    if (g.permuted) {
+      std::vector<int64_t> ord{(int64_t)g.ord_dim.size()};
+      for (size_t j = 0; j < g.ord_dim.size(); ++j) {
+        ord.push_back(g.ord_pv_iter[j]);
+        ord.push_back(g.ord_dim[j]);
+        ord.push_back(g.ord_pv_lex[j]);
+      }
+      ord_host = ord;
+      ordbuf = dalloc<int64_t>(ord.size(), dev_bytes, device);
+      CU(cudaMemcpyAsync(ordbuf, ord.data(), ord.size() * 8, cudaMemcpyHostToDevice, stream));
+    }
     results_slot = dalloc<double*>(1, dev_bytes, device);
     folded = dalloc<double>((size_t)g.R, dev_bytes, device);
     CU(cudaStreamSynchronize(stream));
@@ -536,7 +548,7 @@ struct tc_exec {
           break;
         }
         case ST_ROOTCOPY: {
-          RootCopyParams rp{ptr(g.root_loc), results_slot, rootmap, g.R, eta};
+          RootCopyParams rp{ptr(g.root_loc), results_slot, rootmap, g.R, eta, ordbuf};
           L.func = (void*)k_rootcopy;
           L.grid = dim3(grid_for(g.R, 256, device));
           L.arg(rp);
@@ -548,6 +560,7 @@ struct tc_exec {
           L.grid = dim3(1);
           L.block = dim3(1);
           L.arg(eta);
+          L.arg((const int64_t*)ordbuf);
           break;
         }
       }
@@ -903,7 +916,7 @@ struct tc_exec {
       int64_t dummy = 0;
       L.arena = dalloc<char>((size_t)g.lane_arena_bytes, dev_bytes, device);
       if (g.sliced_doubles) L.sliced = dalloc<double>((size_t)g.sliced_doubles, dev_bytes, device);
-      L.eta = dalloc<int64_t>(5, dummy, device);
+      L.eta = dalloc<int64_t>(6, dummy, device);
       CU(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
       CU(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
       if (!g.tiny_nodes.empty()) {
@@ -951,19 +964,26 @@ struct tc_exec {
   // slice counters: [current slice, first slice of the pass, stride, lane's
   // first offset, slices per block]: lane k runs blocks k, k + K, ... of B
   // consecutive slices (k_eta steps +1 inside a block, then to its next block)
-  void set_eta(int64_t b, int K, int64_t B = 1) {
+  // A pass over lexicographic slices [b, b + n): mode 0 when the slice order
+  // maps the range onto itself (iteration ids [b, b + n), blocks of B), else
+  // mode 1 (lexicographic walk, B = 1; k_eta converts through the order table).
+  void set_eta(int64_t b, int K, int64_t n) {
+    const bool closed = !prog.permuted || (b % prog.closed_granule == 0 && (b + n) % prog.closed_granule == 0);
+    const int64_t B = closed ? block_for(b, n) : 1;
+    const int64_t mode = closed ? 0 : 1;
+    const int64_t* ord = ord_host.empty() ? nullptr : ord_host.data();
     last_B = B;
-    int64_t h[5] = {b, b, K * B, 0, B};
-    CU(cudaMemcpyAsync(eta, h, sizeof(h), cudaMemcpyHostToDevice, stream));
-    for (int k = 1; k < K; ++k) {
-      int64_t hk[5] = {b + k * B, b, K * B, k * B, B};
-      CU(cudaMemcpyAsync(xl[k - 1].eta, hk, sizeof(hk), cudaMemcpyHostToDevice, stream));
+    for (int k = 0; k < K; ++k) {
+      const int64_t t0 = mode ? slice_iter(ord, b + k) : b + k * B;
+      int64_t hk[6] = {t0, b, mode ? K : K * B, mode ? k : k * B, B, mode};
+      CU(cudaMemcpyAsync(k ? xl[k - 1].eta : eta, hk, sizeof(hk), cudaMemcpyHostToDevice, stream));
     }
     CU(cudaStreamSynchronize(stream));
   }
+  std::vector<int64_t> ord_host;
   void reset_eta(int K) {
-    k_eta_reset<<<1, 1, 0, stream>>>(eta);
-    for (int k = 1; k < K; ++k) k_eta_reset<<<1, 1, 0, stream>>>(xl[k - 1].eta);
+    k_eta_reset<<<1, 1, 0, stream>>>(eta, ordbuf);
+    for (int k = 1; k < K; ++k) k_eta_reset<<<1, 1, 0, stream>>>(xl[k - 1].eta, ordbuf);
   }
   double program_ms = 0, setup_ms = 0, graph_ms = 0, lanes_ms = 0;
   std::vector<float> start_ms;  // profile_graph: launch start offset within its graph launch
@@ -1088,7 +1108,7 @@ struct tc_exec {
       CU(cudaMemset(trace, 0, (prog.n_tiny + 1) * sizeof(long long)));
       CU(cudaMemcpyToSymbol(g_tiny_trace, &trace, sizeof(trace)));
     }
-    set_eta(slice, 1);
+    set_eta(slice, 1, 1);
     std::vector<cudaEvent_t> ev(launches.size() + 1);
     for (auto& e : ev) CU(cudaEventCreate(&e));
     CU(cudaEventRecord(ev[0], stream));
@@ -1171,8 +1191,8 @@ struct tc_exec {
       }
       if (G.g) CU(cudaGraphInstantiate(&G.ge, G.g, 0));
     }
-    const int64_t B = block_for(b, n);
-    set_eta(b, 1, B);
+    set_eta(b, 1, n);
+    const int64_t B = last_B;
     cudaEvent_t p0, p1;
     CU(cudaEventCreate(&p0));
     CU(cudaEventCreate(&p1));
@@ -1243,7 +1263,7 @@ struct tc_exec {
       std::fprintf(stderr, "[run] graphs %.2f ms, lanes(%d) %.2f ms%s\n",
                    std::chrono::duration<double, std::milli>(tg1 - tg0).count(), K, lanes_ms,
                    overlap ? " (overlapping the eager prologue)" : "");
-    set_eta(b, K, block_for(b, n));
+    set_eta(b, K, n);
     if (!overlap) CU(cudaEventRecord(e0, stream));
     for (int64_t r = 0; r < repeats; ++r) {
       if (r > 0) reset_eta(K);
@@ -1278,7 +1298,7 @@ struct tc_exec {
     for (auto& x : ev) CU(cudaEventCreate(&x));
     const int K = lanes_for(n);
     if (K > 1) ensure_lanes(K);
-    set_eta(b, K, block_for(b, n));
+    set_eta(b, K, n);
     for (int64_t r = 0; r < repeats; ++r) {
       if (r > 0) reset_eta(K);
       k_flush<<<grid_for(n4, 256, device), 256, 0, stream>>>(fbuf, n4, (double)r);

@@ -183,6 +183,24 @@ def test_slice_blocks_are_bitwise_identical(name, picks):
         assert st["slices_per_block"] == int(flat.domain[ch[-1]])
 
 
+@pytest.mark.parametrize("name,ranges", [("c4", ((0, 32), (3, 21), (64, 128))), ("c5", ((3584, 4096), (3584, 3600)))])
+def test_slice_order_is_bitwise_identical(name, ranges):
+    """A permuted slice order (C4: 3 fast indices, blocks of 8; C5: 5 fast
+    indices, blocks of 32) against the lexicographic order (TC_SLICE_ORDER=0)
+    and against per-slice execution (TC_BLOCK=0): the same bits in every
+    lexicographic row, for ranges the order maps onto themselves (blocks) and
+    for ranges it does not (the lexicographic walk)."""
+    flat = _plan(name)
+    ch = _chosen(flat, _golden(name))
+    st = _lib.PlanHandle(flat).compile_stats(ch)
+    assert st["slices_per_block"] > 2
+    for b, e in ranges:
+        on, fon, _ = _per_slice(flat, ch, b, e)
+        lex, flex, _ = _per_slice(flat, ch, b, e, env={"TC_SLICE_ORDER": "0"})
+        off, foff, _ = _per_slice(flat, ch, b, e, env={"TC_BLOCK": "0"})
+        assert on.tobytes() == lex.tobytes() == off.tobytes() and fon == flex == foff, (b, e)
+
+
 def test_c4_slice_blocks_cut_work():
     flat = _plan("c4")
     ch = _chosen(flat, _golden("c4"))
@@ -190,7 +208,7 @@ def test_c4_slice_blocks_cut_work():
     B = st["slices_per_block"]
     inv, blk = st["phys_bytes_hoisted"], st["phys_bytes_block"]
     per_pass = inv + 256 // B * blk + 256 * (st["phys_bytes"] - inv - blk)
-    assert B == 2 and blk > 0.3 * (st["phys_bytes"] - inv)
+    assert B >= 2 and blk > 0.2 * (st["phys_bytes"] - inv)
     assert per_pass < 0.9 * (inv + 256 * (st["phys_bytes"] - inv))
 
 

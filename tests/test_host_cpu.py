@@ -321,9 +321,13 @@ def test_slice_blocks_compile_on_cpu(monkeypatch):
     for _ in range(8):
         ch.append(h.choose_slice_index(ch))
     on = h.compile_stats(ch)
+    monkeypatch.setenv("TC_SLICE_ORDER", "0")
+    lex = h.compile_stats(ch)
     monkeypatch.setenv("TC_BLOCK", "0")
     off = h.compile_stats(ch)
-    assert on["slices_per_block"] == 2 and off["slices_per_block"] == 1
+    # the slice order makes 3 of the 8 chosen indices fast (blocks of 8); the
+    # lexicographic order only the last (blocks of 2)
+    assert on["slices_per_block"] == 8 and lex["slices_per_block"] == 2 and off["slices_per_block"] == 1
     assert on["launches_block"] > 0 and off["launches_block"] == 0 and off["phys_bytes_block"] == 0
     assert 0 < on["phys_bytes_block"] < on["phys_bytes"] - on["phys_bytes_hoisted"]
     assert on["phys_bytes"] == off["phys_bytes"] and on["phys_bytes_hoisted"] == off["phys_bytes_hoisted"]

@@ -30,5 +30,7 @@ one = per_slice(ex)
 ex.run(b, e, repeats=3)
 rep = per_slice(ex)
 ok = np.array_equal(one, rep)
-print(name, b, e, {k: os.environ.get(k) for k in ("TC_BLOCK", "TC_LANES", "TC_OVERLAP_BUILD")}, "equal", ok,
+import hashlib  # noqa: E402
+print(name, b, e, {k: os.environ.get(k) for k in ("TC_BLOCK", "TC_SLICE_ORDER", "TC_LANES", "TC_OVERLAP_BUILD")},
+      "hash", hashlib.sha1(rep.tobytes()).hexdigest()[:12], "equal", ok,
       "bad slices", np.nonzero(one != rep)[0][:16].tolist(), "nonzero one/rep", int((one != 0).sum()), int((rep != 0).sum()))

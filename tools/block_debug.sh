@@ -1,6 +1,6 @@
+# per-slice bits under the slice order / block tier / plain per-slice execution
 cd "${GRAFT_REPO_ROOT:-.}"
-for env in "TC_BLOCK=1" "TC_BLOCK=0" "TC_LANES=1" "TC_OVERLAP_BUILD=0"; do
-  env $env python tools/block_debug.py c1b_s3 0 8
-  env $env python tools/block_debug.py c1b_s3 2 6
-  env $env python tools/block_debug.py c1b_s3 1 6
+for env in "TC_BLOCK=1" "TC_SLICE_ORDER=0" "TC_BLOCK=0" "TC_LANES=1"; do
+  for r in "0 256" "32 64" "1 20" "8 40"; do env $env python tools/block_debug.py c4 $r; done
+  for r in "3584 4096" "3584 3600" "0 512"; do env $env python tools/block_debug.py c5 $r; done
 done

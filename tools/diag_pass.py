@@ -19,7 +19,7 @@ for name in sys.argv[1:]:
         rule = ("greedy", int(os.environ["DIAG_PICKS"]))
     h, ch = bench.choose(flat, rule)
     ex = _lib.Exec(h, ch, 0)
-    ns = min(ex.num_slices(), int(os.environ.get("DIAG_SLICES", "256")))
+    ns = min(ex.num_slices(), int(os.environ.get("DIAG_SLICES", "512")))
     ex.run(0, ns)
     ex.run(0, ns, repeats=2)
     st = ex.run(0, ns, repeats=5)
