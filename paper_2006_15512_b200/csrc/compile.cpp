@@ -1229,7 +1229,11 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         msk[v] = msk[a] | msk[b];  // (a relabel alias carries its source's mask: the union is the same)
         if (msk[v]) wb[msk[v]] += 8.0 * (double)(size[a] + size[b] + size[v]);
       }
-      const int keep = std::min(3, nch - 1);
+      // candidates: the chosen indices after the first three, at most the last
+      // 8 (many-index slice sets -- C3's 30 -- are run in ranges of a few
+      // hundred slices, whose free indices are the last ones: a range of 256
+      // aligned slices stays closed)
+      const int keep = std::max(std::min(3, nch - 1), nch - 8);
       std::vector<int> cand;
       for (int j = keep; j < nch; ++j) cand.push_back(j);
       double NS = (double)g.num_slices, best = -1;
@@ -1241,7 +1245,7 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         for (auto& [m, b] : wb) c += b * ((m & fm) ? NS : NS / B);
         return c;
       };
-      if (order_env && cand.size() <= 16) {
+      if (order_env) {
         for (uint64_t sub = 1; sub < (1ull << cand.size()); ++sub) {
           uint64_t fm = 0;
           for (size_t q = 0; q < cand.size(); ++q)

@@ -180,7 +180,7 @@ def test_slice_blocks_are_bitwise_identical(name, picks):
         f2, p2 = exon.fetch(e - b)
         assert p2.reshape(e - b, -1)[:, 0].tobytes() == on.tobytes() and f2[0] == fon
     if st["launches_block"]:
-        assert st["slices_per_block"] == int(flat.domain[ch[-1]])
+        assert st["slices_per_block"] % int(flat.domain[ch[-1]]) == 0
 
 
 @pytest.mark.parametrize("name,ranges", [("c4", ((0, 32), (3, 21), (64, 128))), ("c5", ((3584, 4096), (3584, 3600)))])
