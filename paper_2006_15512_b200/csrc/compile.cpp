@@ -1229,11 +1229,11 @@ Program compile_program(const Plan& p, const std::vector<int>& chosen_in, int64_
         msk[v] = msk[a] | msk[b];  // (a relabel alias carries its source's mask: the union is the same)
         if (msk[v]) wb[msk[v]] += 8.0 * (double)(size[a] + size[b] + size[v]);
       }
-      // candidates: the chosen indices after the first three, at most the last
-      // 8 (many-index slice sets -- C3's 30 -- are run in ranges of a few
-      // hundred slices, whose free indices are the last ones: a range of 256
-      // aligned slices stays closed)
-      const int keep = std::max(std::min(3, nch - 1), nch - 8);
+      // candidates: the chosen indices after the first three; for many-index
+      // slice sets (more than 12 -- C3's 30 -- run in ranges of a few hundred
+      // slices, whose free indices are the last ones) only the last 8, so an
+      // aligned range of 256 slices stays closed
+      const int keep = nch > 12 ? nch - 8 : std::min(3, nch - 1);
       std::vector<int> cand;
       for (int j = keep; j < nch; ++j) cand.push_back(j);
       double NS = (double)g.num_slices, best = -1;
